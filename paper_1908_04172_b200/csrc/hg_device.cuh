@@ -1,0 +1,303 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Device-side modular arithmetic and the per-limb negacyclic NTT block.
+//
+// Every prime handled here is < 2^30, so residues live in u32 and Harvey's lazy
+// butterflies can keep values in [0, 4q) < 2^32.  Results written to HBM are
+// always canonical ([0, q)), which is what makes them bit-identical to the
+// reference: the reference's outputs are canonical residues of the same
+// mathematical values (henet/modmath.hpp:149-165, 338-377).
+//
+// NTT convention (henet/modmath.hpp:303-377): forward is Cooley-Tukey with
+// twiddle root_powers[m + i] = psi^bitrev(m + i) at stage m (t = N / 2m),
+// pairs (j, j + t); inverse is Gentleman-Sande with psi^-bitrev(m + i) and a
+// final multiply by N^-1, which is folded into the last inverse stage here.
+// The tables keep the reference's index order, so output index i holds the
+// evaluation at psi^(2 bitrev(i) + 1) exactly as ntt_forward_limb does.
+#pragma once
+
+#include <cstdint>
+
+namespace hg {
+
+using u32 = uint32_t;
+using u64 = uint64_t;
+using i32 = int32_t;
+
+constexpr int kMaxPrimes = 24;
+
+// Per-basis-modulus constants.  Passed by value (kernel parameter space).
+struct DevPrime {
+  u32 q;
+  u32 two_q;
+  u32 half;      // floor(q / 2)
+  u32 mu32;      // floor(2^32 / q)                -> reduce a u32 to [0, q)
+  u64 mu64;      // floor(2^64 / q)                -> Barrett of a u64 accumulator
+  u32 r32;       // 2^32 mod q                      -> accumulator folding
+  u32 ninv;      // N^-1 mod q
+  u32 ninv_sh;   // floor(ninv * 2^32 / q)
+  u32 w1n;       // inv_root_powers[1] * N^-1 mod q (last inverse stage)
+  u32 w1n_sh;
+  u32 pad_;
+  const uint2* fwd;  // N entries: (psi^bitrev(i), shoup)
+  const uint2* inv;  // N entries: (psi^-bitrev(i), shoup)
+};
+
+struct Basis {
+  DevPrime p[kMaxPrimes];  // chain moduli first, special prime at index chain_len
+};
+
+// ---------------------------------------------------------------------------
+// Scalar modular helpers
+// ---------------------------------------------------------------------------
+
+// x in [0, 2q) -> [0, q): unsigned min picks x - q only when it did not wrap.
+__device__ __forceinline__ u32 csub(u32 x, u32 q) { return min(x, x - q); }
+
+// Shoup multiplication by a constant w (< q) with companion wsh = floor(w 2^32 / q).
+// For any x < 2^32 the result is congruent to x*w and lies in [0, 2q) (q < 2^31).
+__device__ __forceinline__ u32 mul_shoup_lazy(u32 x, u32 w, u32 wsh, u32 q) {
+  const u32 qhat = __umulhi(x, wsh);
+  return x * w - qhat * q;
+}
+
+__device__ __forceinline__ u32 mul_shoup(u32 x, u32 w, u32 wsh, u32 q) {
+  return csub(mul_shoup_lazy(x, w, wsh, q), q);
+}
+
+// Reduce any u32 into [0, q).
+__device__ __forceinline__ u32 reduce32(u32 x, const DevPrime& P) {
+  const u32 qhat = __umulhi(x, P.mu32);
+  u32 r = x - qhat * P.q;  // < 2q
+  return csub(r, P.q);
+}
+
+// Reduce any u64 into [0, q) (Barrett with mu = floor(2^64/q); remainder < 2q).
+__device__ __forceinline__ u32 reduce64(u64 x, const DevPrime& P) {
+  const u64 qhat = __umul64hi(x, P.mu64);
+  u32 r = static_cast<u32>(x - qhat * static_cast<u64>(P.q));
+  return csub(r, P.q);
+}
+
+__device__ __forceinline__ u32 mulmod(u32 a, u32 b, const DevPrime& P) {
+  return reduce64(static_cast<u64>(a) * b, P);
+}
+
+__device__ __forceinline__ u32 addmod(u32 a, u32 b, u32 q) { return csub(a + b, q); }
+__device__ __forceinline__ u32 submod(u32 a, u32 b, u32 q) { return csub(a + q - b, q); }
+
+// Signed value |c| < q -> residue in [0, q).
+__device__ __forceinline__ u32 from_signed(i32 c, u32 q) {
+  return c < 0 ? static_cast<u32>(c + static_cast<i32>(q)) : static_cast<u32>(c);
+}
+
+// Centered rounding remainder used by divide_round_last (henet/ckks.hpp:132-154):
+// r = (x + floor(p/2)) mod p, returned as r - floor(p/2)  (in (-p/2, p/2]).
+__device__ __forceinline__ i32 centered_round_rem(u32 x, const DevPrime& P) {
+  const u32 r = csub(x + P.half, P.q);
+  return static_cast<i32>(r) - static_cast<i32>(P.half);
+}
+
+// ---------------------------------------------------------------------------
+// NTT block: one CTA of T = N/32 threads transforms one limb held as 32
+// registers per thread, in three register passes separated by two shared
+// memory exchanges.  Register layouts (tid in [0, T), k in [0, 32)):
+//   A : j = tid | k << LOGT                     (natural order, coalesced)
+//   B : j = (tid & CBm) | (k & MBm) << CB | (tid >> CB) << LOGT | (k >> MB) << (LOGT + MB)
+//   C : j = (k & CBm) | tid << CB | (k >> CB) << (CB + LOGT)
+// Forward:  A --(stages LOGN-1..LOGT)--> smem --> B --(LOGT-1..CB)--> smem --> C --(CB-1..0)
+// Inverse runs the same passes backwards: C -> B -> A.
+// ---------------------------------------------------------------------------
+template <int LOGN_>
+struct Ntt {
+  static constexpr int LOGN = LOGN_;
+  static constexpr int N = 1 << LOGN;
+  static constexpr int LOGT = LOGN - 5;
+  static constexpr int T = 1 << LOGT;
+  static constexpr int CB = (LOGN >= 14) ? (LOGN - 10) : 3;
+  static constexpr int MB = LOGT - CB;
+  static constexpr u32 CBm = (1u << CB) - 1;
+  static constexpr u32 MBm = (1u << MB) - 1;
+  static_assert(LOGN >= 10 && LOGN <= 15, "supported ring degrees: 2^10 .. 2^15");
+  static_assert(MB >= 1 && MB <= 5 && CB <= 5, "bad pass split");
+
+  __device__ static __forceinline__ u32 jA(u32 tid, u32 k) { return tid | (k << LOGT); }
+  __device__ static __forceinline__ u32 jB(u32 tid, u32 k) {
+    return (tid & CBm) | ((k & MBm) << CB) | ((tid >> CB) << LOGT) | ((k >> MB) << (LOGT + MB));
+  }
+  __device__ static __forceinline__ u32 jC(u32 tid, u32 k) {
+    return (k & CBm) | (tid << CB) | ((k >> CB) << (CB + LOGT));
+  }
+  template <int L>
+  __device__ static __forceinline__ u32 jmap(u32 tid, u32 k) {
+    if constexpr (L == 0) return jA(tid, k);
+    else if constexpr (L == 1) return jB(tid, k);
+    else return jC(tid, k);
+  }
+
+  // XOR swizzle of the low 5 bits (the bank) with higher bits; conflict-free
+  // for all three layouts (checked in tests/test_ntt_layout.py).
+  __device__ static __forceinline__ u32 swz(u32 j) {
+    return j ^ ((j >> 5) & CBm) ^ (((j >> LOGT) & ((1u << (5 - CB)) - 1)) << CB);
+  }
+
+  template <int L>
+  __device__ static __forceinline__ void store(const u32 (&x)[32], u32* sm, u32 tid) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) sm[swz(jmap<L>(tid, k))] = x[k];
+  }
+  template <int L>
+  __device__ static __forceinline__ void load(u32 (&x)[32], const u32* sm, u32 tid) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) x[k] = sm[swz(jmap<L>(tid, k))];
+  }
+
+  // Butterfly bits of pass L occupy register bits [0, NB); the j bit of
+  // register bit 0 is BLO.
+  template <int L>
+  struct PassShape {
+    static constexpr int NB = (L == 0) ? 5 : (L == 1 ? MB : CB);
+    static constexpr int BLO = (L == 0) ? LOGT : (L == 1 ? CB : 0);
+  };
+
+  // Forward (Cooley-Tukey, Harvey lazy) stages of pass L.  Values in [0, 4q).
+  template <int L>
+  __device__ static __forceinline__ void fwd_pass(u32 (&x)[32], u32 tid, const DevPrime& P) {
+    constexpr int NB = PassShape<L>::NB;
+    constexpr int BLO = PassShape<L>::BLO;
+    const u32 q = P.q, q2 = P.two_q;
+#pragma unroll
+    for (int s = 0; s < NB; ++s) {
+      const int rb = NB - 1 - s;  // register bit of this stage
+      const int b = BLO + rb;     // j bit of this stage (t = 2^b)
+#pragma unroll
+      for (int g = 0; g < (1 << (5 - NB)); ++g) {
+#pragma unroll
+        for (int hi = 0; hi < (1 << (NB - 1 - rb)); ++hi) {
+          const u32 kh = (static_cast<u32>(g) << NB) | (static_cast<u32>(hi) << (rb + 1));
+          const u32 j = jmap<L>(tid, kh);
+          const uint2 w = __ldg(&P.fwd[(1u << (LOGN - 1 - b)) + (j >> (b + 1))]);
+#pragma unroll
+          for (int lo = 0; lo < (1 << rb); ++lo) {
+            const int k0 = kh | lo;
+            const int k1 = k0 | (1 << rb);
+            u32 X = x[k0];
+            X = min(X, X - q2);
+            const u32 Tm = mul_shoup_lazy(x[k1], w.x, w.y, q);
+            x[k0] = X + Tm;
+            x[k1] = X - Tm + q2;
+          }
+        }
+      }
+    }
+  }
+
+  // Inverse (Gentleman-Sande, Harvey lazy) stages of pass L.  Values in [0, 2q).
+  // LAST: pass A carries the final stage (m = 1), which also applies N^-1.
+  template <int L>
+  __device__ static __forceinline__ void inv_pass(u32 (&x)[32], u32 tid, const DevPrime& P) {
+    constexpr int NB = PassShape<L>::NB;
+    constexpr int BLO = PassShape<L>::BLO;
+    const u32 q = P.q, q2 = P.two_q;
+#pragma unroll
+    for (int s = 0; s < NB; ++s) {
+      const int rb = s;
+      const int b = BLO + rb;
+#pragma unroll
+      for (int g = 0; g < (1 << (5 - NB)); ++g) {
+#pragma unroll
+        for (int hi = 0; hi < (1 << (NB - 1 - rb)); ++hi) {
+          const u32 kh = (static_cast<u32>(g) << NB) | (static_cast<u32>(hi) << (rb + 1));
+          if (b == LOGN - 1) {
+#pragma unroll
+            for (int lo = 0; lo < (1 << rb); ++lo) {
+              const int k0 = kh | lo;
+              const int k1 = k0 | (1 << rb);
+              const u32 U = x[k0], V = x[k1];
+              x[k0] = mul_shoup_lazy(U + V, P.ninv, P.ninv_sh, q);
+              x[k1] = mul_shoup_lazy(U - V + q2, P.w1n, P.w1n_sh, q);
+            }
+          } else {
+            const u32 j = jmap<L>(tid, kh);
+            const uint2 w = __ldg(&P.inv[(1u << (LOGN - 1 - b)) + (j >> (b + 1))]);
+#pragma unroll
+            for (int lo = 0; lo < (1 << rb); ++lo) {
+              const int k0 = kh | lo;
+              const int k1 = k0 | (1 << rb);
+              const u32 U = x[k0], V = x[k1];
+              u32 S = U + V;
+              x[k0] = min(S, S - q2);
+              x[k1] = mul_shoup_lazy(U - V + q2, w.x, w.y, q);
+            }
+          }
+        }
+      }
+    }
+  }
+
+  // Full forward transform.  In: layout A, values < 4q.  Out: layout C,
+  // canonical.  `sm` must hold N u32; the call begins and ends with a barrier
+  // so the buffer may be reused immediately by the caller.
+  __device__ static __forceinline__ void forward(u32 (&x)[32], u32* sm, u32 tid, const DevPrime& P) {
+    fwd_pass<0>(x, tid, P);
+    __syncthreads();
+    store<0>(x, sm, tid);
+    __syncthreads();
+    load<1>(x, sm, tid);
+    fwd_pass<1>(x, tid, P);
+    store<1>(x, sm, tid);
+    __syncthreads();
+    load<2>(x, sm, tid);
+    fwd_pass<2>(x, tid, P);
+    const u32 q = P.q, q2 = P.two_q;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      u32 v = x[k];
+      v = min(v, v - q2);
+      x[k] = min(v, v - q);
+    }
+  }
+
+  // Full inverse transform.  In: layout C, values < 2q.  Out: layout A, canonical.
+  __device__ static __forceinline__ void inverse(u32 (&x)[32], u32* sm, u32 tid, const DevPrime& P) {
+    inv_pass<2>(x, tid, P);
+    __syncthreads();
+    store<2>(x, sm, tid);
+    __syncthreads();
+    load<1>(x, sm, tid);
+    inv_pass<1>(x, tid, P);
+    store<1>(x, sm, tid);
+    __syncthreads();
+    load<0>(x, sm, tid);
+    inv_pass<0>(x, tid, P);
+    const u32 q = P.q;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) x[k] = csub(x[k], q);
+  }
+
+  // Global memory helpers for one limb row.
+  __device__ static __forceinline__ void gload_A(u32 (&x)[32], const u32* __restrict__ row, u32 tid) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) x[k] = __ldg(&row[jA(tid, k)]);
+  }
+  __device__ static __forceinline__ void gstore_A(const u32 (&x)[32], u32* __restrict__ row, u32 tid) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) row[jA(tid, k)] = x[k];
+  }
+  // Layout C groups of 2^CB consecutive words -> 128-bit accesses.
+  __device__ static __forceinline__ void gload_C(u32 (&x)[32], const u32* __restrict__ row, u32 tid) {
+#pragma unroll
+    for (int k = 0; k < 32; k += 4) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(row + jC(tid, k)));
+      x[k] = v.x; x[k + 1] = v.y; x[k + 2] = v.z; x[k + 3] = v.w;
+    }
+  }
+  __device__ static __forceinline__ void gstore_C(const u32 (&x)[32], u32* __restrict__ row, u32 tid) {
+#pragma unroll
+    for (int k = 0; k < 32; k += 4) {
+      *reinterpret_cast<uint4*>(row + jC(tid, k)) = make_uint4(x[k], x[k + 1], x[k + 2], x[k + 3]);
+    }
+  }
+};
+
+}  // namespace hg

@@ -1,0 +1,1663 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Host runtime + C ABI (include/henet_b200.h).  Everything numerical runs in
+// the sm_100a kernels of hg_kernels.cu; this file owns parameters, tables,
+// scale/level bookkeeping (bit-identical double arithmetic to the reference),
+// validation with the reference's error messages, device memory, the model
+// and plan objects, and the graph executor.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <mutex>
+
+#include "hg_modmath.hpp"
+#include "hg_runtime.hpp"
+
+namespace hg {
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return HG_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "allocation failed";
+    return HG_ERR_ALLOC;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return HG_ERR_INTERNAL;
+  }
+}
+}  // namespace
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw Error(e == cudaErrorMemoryAllocation ? HG_ERR_ALLOC : HG_ERR_CUDA,
+                std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+static void check_launch(int r, const char* what) {
+  if (r < 0) throw Error(HG_ERR_UNSUPPORTED, std::string(what) + ": unsupported configuration");
+  cuda_check(cudaGetLastError(), what);
+}
+
+DeviceCore::~DeviceCore() {
+  if (stream) {
+    cudaSetDevice(device);
+    cudaStreamSynchronize(stream);
+    cudaStreamDestroy(stream);
+  }
+}
+
+DeviceBuffer::DeviceBuffer(std::shared_ptr<DeviceCore> c, size_t b, cudaStream_t s) : core(std::move(c)), bytes(b) {
+  stream = s ? s : core->stream;
+  if (bytes == 0) return;
+  cuda_check(cudaMallocAsync(&ptr, bytes, stream), "cudaMallocAsync");
+}
+
+DeviceBuffer::~DeviceBuffer() {
+  if (ptr) cudaFreeAsync(ptr, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Context (henet/params.hpp:112-129)
+// ---------------------------------------------------------------------------
+static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_len, u64 special, double scale,
+                                             int device) {
+  require(n >= 2 && (n & (n - 1)) == 0, "poly degree must be a power of two");
+  require(chain_len >= 1, "modulus chain must be non-empty");
+  u32 logn = 0;
+  while ((1u << logn) < n) ++logn;
+  if (logn < 12 || logn > 14)
+    throw Error(HG_ERR_UNSUPPORTED, "B200 kernels implement ring degrees 2^12..2^14 (got " + std::to_string(n) + ")");
+  const u32 full = chain_len + (special ? 1 : 0);
+  if (full > static_cast<u32>(kMaxPrimes)) throw Error(HG_ERR_UNSUPPORTED, "too many basis moduli");
+
+  auto ctx = std::make_shared<Context>();
+  ctx->n = n;
+  ctx->logn = logn;
+  ctx->chain.assign(chain, chain + chain_len);
+  ctx->special = special;
+  ctx->has_special = special != 0;
+  ctx->default_scale = scale;
+  for (u32 i = 0; i < full; ++i) {
+    const u64 q = ctx->basis_mod(i);
+    require(q >= 2, "modulus must be at least 2");
+    require(nt::is_prime(q), "modulus must be prime");
+    if (q >= (1ull << 30))
+      throw Error(HG_ERR_UNSUPPORTED, "B200 kernels implement primes below 2^30 (got " + std::to_string(q) + ")");
+    for (u32 j = 0; j < i; ++j) {
+      if (ctx->basis_mod(j) == q) {
+        throw Error(HG_ERR_VALIDATION, i == chain_len ? "special prime must differ from the chain"
+                                                      : "chain moduli must be pairwise distinct");
+      }
+    }
+    if ((q - 1) % (2ull * n) != 0) throw Error(HG_ERR_VALIDATION, "modulus admits no 2N-th root of unity (q != 1 mod 2N)");
+  }
+  long double acc = 1.0L;
+  ctx->modulus_products.push_back(acc);
+  for (u64 q : ctx->chain) {
+    acc *= static_cast<long double>(q);
+    ctx->modulus_products.push_back(acc);
+  }
+
+  int ndev = 0;
+  cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  require(device >= 0 && device < ndev, "no such CUDA device");
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cudaDeviceProp prop{};
+  cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10) throw Error(HG_ERR_CUDA, "kernels are built for sm_100a; device is sm_" +
+                                                     std::to_string(prop.major) + std::to_string(prop.minor));
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  ctx->core = std::make_shared<DeviceCore>();
+  ctx->core->device = device;
+  cuda_check(cudaStreamCreateWithFlags(&ctx->core->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+
+  // NTT tables (root_powers / inv_root_powers in the reference's order) + Shoup companions.
+  std::vector<uint2> tab(static_cast<size_t>(full) * 2 * n);
+  for (u32 i = 0; i < full; ++i) {
+    const u64 q = ctx->basis_mod(i);
+    const u64 psi = nt::primitive_2n_root(q, n);
+    require(nt::powmod(psi, n, q) == q - 1 && nt::powmod(psi, 2ull * n, q) == 1, "root order check failed");
+    ctx->roots.push_back(psi);
+    const u64 psi_inv = nt::inv(psi, q);
+    uint2* f = &tab[static_cast<size_t>(i) * 2 * n];
+    uint2* g = f + n;
+    for (u32 k = 0; k < n; ++k) {
+      const u32 rev = nt::bit_reverse(k, logn);
+      const u64 w = nt::powmod(psi, rev, q), wi = nt::powmod(psi_inv, rev, q);
+      f[k] = make_uint2(static_cast<u32>(w), nt::shoup(w, q));
+      g[k] = make_uint2(static_cast<u32>(wi), nt::shoup(wi, q));
+    }
+    DevPrime& P = ctx->basis.p[i];
+    P.q = static_cast<u32>(q);
+    P.two_q = static_cast<u32>(2 * q);
+    P.half = static_cast<u32>(q >> 1);
+    P.mu32 = static_cast<u32>((1ull << 32) / q);
+    P.mu64 = static_cast<u64>((static_cast<nt::u128>(1) << 64) / q);
+    P.r32 = static_cast<u32>((1ull << 32) % q);
+    const u64 ninv = nt::inv(n % q, q);
+    P.ninv = static_cast<u32>(ninv);
+    P.ninv_sh = nt::shoup(ninv, q);
+    const u64 w1n = nt::mulmod(g[1].x, ninv, q);
+    P.w1n = static_cast<u32>(w1n);
+    P.w1n_sh = nt::shoup(w1n, q);
+  }
+  ctx->tables = ctx->alloc(tab.size() * sizeof(uint2), nullptr);
+  cuda_check(cudaMemcpyAsync(ctx->tables->ptr, tab.data(), tab.size() * sizeof(uint2), cudaMemcpyHostToDevice,
+                             ctx->core->stream),
+             "upload tables");
+  for (u32 i = 0; i < full; ++i) {
+    uint2* base = static_cast<uint2*>(ctx->tables->ptr) + static_cast<size_t>(i) * 2 * n;
+    ctx->basis.p[i].fwd = base;
+    ctx->basis.p[i].inv = base + n;
+  }
+
+  // Embedding tables, computed with the reference's expressions (henet/fft.hpp:30-43)
+  // on the host libm so the GPU FFT sees identical doubles.
+  const double pi = std::acos(-1.0);
+  ctx->host_roots.resize(n);  // n/2 complex
+  for (u32 k = 0; k < n / 2; ++k) {
+    double ang = -2.0 * pi * k / n;
+    ctx->host_roots[2 * k] = std::cos(ang);
+    ctx->host_roots[2 * k + 1] = std::sin(ang);
+  }
+  ctx->host_twist.resize(2 * static_cast<size_t>(n));
+  for (u32 k = 0; k < n; ++k) {
+    double ang = pi * k / n;
+    ctx->host_twist[2 * k] = std::cos(ang);
+    ctx->host_twist[2 * k + 1] = std::sin(ang);
+  }
+  ctx->fft_tables = ctx->alloc((ctx->host_roots.size() + ctx->host_twist.size()) * sizeof(double), nullptr);
+  cuda_check(cudaMemcpyAsync(ctx->fft_tables->ptr, ctx->host_roots.data(), ctx->host_roots.size() * sizeof(double),
+                             cudaMemcpyHostToDevice, ctx->core->stream),
+             "upload fft roots");
+  cuda_check(cudaMemcpyAsync(static_cast<double*>(ctx->fft_tables->ptr) + ctx->host_roots.size(),
+                             ctx->host_twist.data(), ctx->host_twist.size() * sizeof(double),
+                             cudaMemcpyHostToDevice, ctx->core->stream),
+             "upload fft twist");
+  cuda_check(cudaStreamSynchronize(ctx->core->stream), "context init");
+  return ctx;
+}
+
+// ---------------------------------------------------------------------------
+// Helpers
+// ---------------------------------------------------------------------------
+static u32 inv_mod_u32(u64 a, u64 q) { return static_cast<u32>(nt::inv(a % q, q)); }
+
+static void ensure(const Context& ctx, CtBatch& b, u64 count, u32 polys, u32 level, cudaStream_t s) {
+  const u64 need = count * polys * level * static_cast<u64>(ctx.n) * sizeof(u32);
+  if (!b.buf || b.buf->bytes < need || b.buf.use_count() > 1) b.buf = ctx.alloc(need, s);
+  b.count = count;
+  b.polys = polys;
+  b.level = level;
+}
+
+static bool scales_match(double a, double b) { return std::fabs(a - b) / a <= std::ldexp(1.0, -40); }
+
+// check_same_shape, henet/ckks.hpp:163-169
+static void check_same_shape(const CtBatch& a, const CtBatch& b) {
+  require(a.level == b.level, "ciphertext level mismatch");
+  require(a.packing == b.packing, "packing mode mismatch");
+  require(a.polys == b.polys, "ciphertext size mismatch");
+  require(a.count == b.count, "element count mismatch");
+  require(scales_match(a.scale, b.scale), "ciphertext scale mismatch");
+}
+
+// check_cc_mul, henet/ckks.hpp:396-401
+static void check_cc_mul(const CtBatch& a) {
+  require(a.packing == HG_PACKING_REAL, "ciphertext-ciphertext multiply is undefined under complex packing");
+  require(a.polys == 2, "operands must be size-2 ciphertexts");
+  require(a.level >= 1, "ciphertext exhausted");
+}
+
+// ---------------------------------------------------------------------------
+// Device op building blocks (all asynchronous on stream s)
+// ---------------------------------------------------------------------------
+static void run_ew(const Context& ctx, EwArgs a, cudaStream_t s) {
+  a.N = ctx.n;
+  if (a.pt_div == 0) a.pt_div = 1;
+  const int r = launch_elementwise(a, ctx.basis, s);
+  check_launch(r, "elementwise");
+  ctx.count(r);
+}
+
+// rescale_next applied (level - target) times; henet/ckks.hpp:504-519.
+static CtBatch do_rescale(const Context& ctx, const CtBatch& in, u32 target, cudaStream_t s) {
+  require(in.level >= 2, "cannot rescale below level 1");
+  require(target >= 1 && target < in.level, "bad rescale target");
+  CtBatch cur = in;
+  while (cur.level > target) {
+    const u32 L = cur.level;
+    CtBatch out;
+    out.packing = cur.packing;
+    out.shape = cur.shape;
+    ensure(ctx, out, cur.count, cur.polys, L - 1, s);
+    RescaleArgs a{};
+    a.in = cur.data();
+    a.out = out.data();
+    a.rows = cur.count * cur.polys;
+    a.level = L;
+    const u64 p = ctx.chain[L - 1];
+    for (u32 i = 0; i + 1 < L; ++i) {
+      const u64 q = ctx.chain[i];
+      a.pinv[i] = inv_mod_u32(p, q);
+      a.pinv_sh[i] = nt::shoup(a.pinv[i], q);
+    }
+    const int r = launch_rescale(static_cast<int>(ctx.logn), a, ctx.basis, s);
+    check_launch(r, "rescale");
+    ctx.count(r);
+    out.scale = cur.scale / static_cast<double>(p);
+    cur = std::move(out);
+  }
+  return cur;
+}
+
+// relinearize(square / tensor / size-3) with optional fused rescale.
+static CtBatch do_relin(const Context& ctx, const RelinKeyDev& rk, const CtBatch* a, const CtBatch* b, int mode,
+                        bool rescale, cudaStream_t s) {
+  require(ctx.has_special, "relinearization needs a special prime");
+  require(rk.chain_len == ctx.chain_len(), "relinearization key has the wrong basis");
+  const u32 L = a->level;
+  const u32 n = ctx.n;
+  if (rescale) require(L >= 2, "cannot rescale below level 1");
+  CtBatch out;
+  out.packing = a->packing;
+  out.shape = a->shape;
+  ensure(ctx, out, a->count, 2, rescale ? L - 1 : L, s);
+  BufPtr D = ctx.alloc(a->count * L * static_cast<u64>(n) * 4, s);
+  BufPtr ACC = ctx.alloc(a->count * 2 * L * static_cast<u64>(n) * 4, s);
+  BufPtr CORR = ctx.alloc(a->count * 2 * static_cast<u64>(n) * 4, s);
+  RelinArgs r{};
+  r.A = a->data();
+  r.Bm = b ? b->data() : a->data();
+  r.mode = mode;
+  r.count = a->count;
+  r.level = L;
+  r.chain_len = static_cast<u32>(ctx.chain_len());
+  r.D = static_cast<u32*>(D->ptr);
+  r.ACC = static_cast<u32*>(ACC->ptr);
+  r.CORR = static_cast<i32*>(CORR->ptr);
+  r.key = static_cast<const uint2*>(rk.key->ptr);
+  r.out = out.data();
+  r.rescale = rescale ? 1 : 0;
+  for (u32 i = 0; i < L; ++i) {
+    const u64 q = ctx.chain[i];
+    r.pinvP[i] = inv_mod_u32(ctx.special, q);
+    r.pinvP_sh[i] = nt::shoup(r.pinvP[i], q);
+    if (rescale && i + 1 < L) {
+      r.pinvL[i] = inv_mod_u32(ctx.chain[L - 1], q);
+      r.pinvL_sh[i] = nt::shoup(r.pinvL[i], q);
+    }
+  }
+  const int lr = launch_relin(static_cast<int>(ctx.logn), r, ctx.basis, s);
+  check_launch(lr, "relinearize");
+  ctx.count(lr);
+  // scale: square/mul_ct_ct multiply the scales; relinearize keeps it; rescale divides.
+  double sc = a->scale;
+  if (mode == 1) sc = a->scale * (b ? b->scale : a->scale);
+  if (rescale) sc /= static_cast<double>(ctx.chain[L - 1]);
+  out.scale = sc;
+  return out;
+}
+
+// Upload a float weight tensor once per model (device copy cached on the weight).
+static const float* weight_dev(const Context& ctx, WeightTensor& w, cudaStream_t s) {
+  if (!w.dev) {
+    w.dev = ctx.alloc(w.data.size() * sizeof(float), s);
+    cuda_check(cudaMemcpyAsync(w.dev->ptr, w.data.data(), w.data.size() * sizeof(float), cudaMemcpyHostToDevice, s),
+               "upload weights");
+  }
+  return static_cast<const float*>(w.dev->ptr);
+}
+
+// encode_scalar validation (henet/encoding.hpp:122-126, 180-188) for |value| <= max_abs.
+static void check_scalar_encodable(const Context& ctx, double max_abs, u32 level, double scale) {
+  require(level >= 1 && level <= ctx.chain_len(), "encode level out of range");
+  require(scale > 0.0, "scale must be positive");
+  const long double scaled = static_cast<long double>(max_abs) * static_cast<long double>(scale);
+  require(scaled < ctx.modulus_products.at(level), "scaled magnitude exceeds q_level");
+  require(std::fabs(static_cast<double>(scaled)) < std::ldexp(1.0, 100), "scaled magnitude too large to encode");
+}
+
+// encode_vector on the GPU: FFT encoder + NTT; returns device plaintexts [count][level][N].
+static BufPtr encode_vectors_dev(const Context& ctx, const double* d_slots, u32 n_slots, u64 count, u32 level,
+                                 double scale, cudaStream_t s, std::vector<unsigned long long>& mant,
+                                 std::vector<int>& ex) {
+  require(level >= 1 && level <= ctx.chain_len(), "encode level out of range");
+  require(scale > 0.0, "scale must be positive");
+  require(n_slots <= ctx.n / 2, "more slots than the parameters provide");
+  const u32 n = ctx.n;
+  BufPtr out = ctx.alloc(count * level * static_cast<u64>(n) * 4, s);
+  BufPtr scratch = ctx.alloc(count * static_cast<u64>(n) * sizeof(double2), s);
+  BufPtr mm = ctx.alloc(count * (sizeof(unsigned long long) + sizeof(int)), s);
+  auto* d_mant = static_cast<unsigned long long*>(mm->ptr);
+  auto* d_exp = reinterpret_cast<int*>(d_mant + count);
+  const double2* roots = static_cast<const double2*>(ctx.fft_tables->ptr);
+  const double2* twist = roots + n / 2;
+  int r = launch_fft_encode(d_slots, n_slots, count, n, level, scale, roots, twist,
+                            static_cast<double2*>(scratch->ptr), static_cast<u32*>(out->ptr), d_mant, d_exp,
+                            ctx.basis, s);
+  check_launch(r, "fft encode");
+  ctx.count(r);
+  r = launch_ntt(static_cast<int>(ctx.logn), static_cast<u32*>(out->ptr), count * level, level, false, ctx.basis, s);
+  check_launch(r, "ntt");
+  ctx.count(r);
+  mant.resize(count);
+  ex.resize(count);
+  cuda_check(cudaMemcpyAsync(mant.data(), d_mant, count * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s), "d2h");
+  cuda_check(cudaMemcpyAsync(ex.data(), d_exp, count * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  cuda_check(cudaStreamSynchronize(s), "encode_vector");
+  // magnitude checks with the reference's long double arithmetic (henet/encoding.hpp:122-138)
+  for (u64 i = 0; i < count; ++i) {
+    const long double mx = mant[i] ? std::ldexp(static_cast<long double>(mant[i]), ex[i]) : 0.0L;
+    require(std::fabs(static_cast<double>(mx)) < std::ldexp(1.0, 100), "scaled magnitude too large to encode");
+    require(mx < ctx.modulus_products.at(level) / 2.0L, "scaled magnitude exceeds q_level/2");
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// Model: load_model's structural part (henet/graph.hpp:297-436)
+// ---------------------------------------------------------------------------
+static u64 elem_count(const std::vector<u32>& d) {
+  u64 n = 1;
+  for (u32 x : d) n *= x;
+  return n;
+}
+
+static std::string shape_str(const std::vector<u32>& d) {
+  std::string s = "(";
+  for (size_t i = 0; i < d.size(); ++i) {
+    if (i) s += ",";
+    s += std::to_string(d[i]);
+  }
+  return s + ")";
+}
+
+static void finalize_model(Model& model) {
+  require(!model.nodes.empty(), "manifest has no nodes");
+  // topological sort, identical traversal order to the reference (stack of ready nodes)
+  {
+    std::map<std::string, std::vector<std::string>> fanout;
+    std::map<std::string, size_t> indegree;
+    for (const auto& n : model.nodes) indegree[n.id] = n.inputs.size();
+    for (const auto& n : model.nodes) {
+      for (const auto& in : n.inputs) {
+        require(model.index.count(in), "node " + n.id + " references unknown input " + in);
+        fanout[in].push_back(n.id);
+      }
+    }
+    std::vector<Node> ordered;
+    std::vector<std::string> ready;
+    for (const auto& n : model.nodes)
+      if (indegree[n.id] == 0) ready.push_back(n.id);
+    while (!ready.empty()) {
+      std::string id = ready.back();
+      ready.pop_back();
+      ordered.push_back(model.node(id));
+      for (const auto& next : fanout[id])
+        if (--indegree[next] == 0) ready.push_back(next);
+    }
+    require(ordered.size() == model.nodes.size(), "cycle detected in the graph");
+    model.nodes = std::move(ordered);
+    model.index.clear();
+    for (size_t i = 0; i < model.nodes.size(); ++i) model.index[model.nodes[i].id] = i;
+  }
+  size_t inputs = 0, outputs = 0;
+  model.shapes.clear();
+  for (const auto& n : model.nodes) {
+    switch (n.op) {
+      case HG_OP_INPUT:
+        ++inputs;
+        require(n.inputs.empty(), "Input takes no inputs");
+        require(!n.attrs.shape.empty(), "Input needs a shape attribute");
+        model.shapes[n.id] = n.attrs.shape;
+        break;
+      case HG_OP_CONST_WEIGHT:
+        require(!n.weight_ref.empty() && model.weights.count(n.weight_ref), "ConstWeight needs a resolvable weight_ref");
+        model.shapes[n.id] = model.weights.at(n.weight_ref).dims;
+        break;
+      case HG_OP_ADD:
+      case HG_OP_MULTIPLY: {
+        require(n.inputs.size() == 2, "Add/Multiply take two inputs");
+        auto a = model.shapes.at(n.inputs[0]);
+        auto b = model.shapes.at(n.inputs[1]);
+        require(a == b || elem_count(a) == 1 || elem_count(b) == 1,
+                "shape mismatch at node " + n.id + ": " + shape_str(a) + " vs " + shape_str(b));
+        model.shapes[n.id] = elem_count(a) == 1 ? b : a;
+        break;
+      }
+      case HG_OP_SQUARE:
+        require(n.inputs.size() == 1, "Square takes one input");
+        model.shapes[n.id] = model.shapes.at(n.inputs[0]);
+        break;
+      case HG_OP_DOT: {
+        require(n.inputs.size() == 1, "Dot takes one input");
+        require(!n.weight_ref.empty() && model.weights.count(n.weight_ref), "Dot needs a resolvable weight_ref");
+        const auto& w = model.weights.at(n.weight_ref);
+        require(w.dims.size() == 2, "Dot weight must be (K,M)");
+        auto in = model.shapes.at(n.inputs[0]);
+        require(in.size() == 1 && in[0] == w.dims[0], "Dot inner dimension mismatch at node " + n.id);
+        if (!n.bias_ref.empty()) {
+          require(model.weights.count(n.bias_ref), "unresolvable bias_ref");
+          require(elem_count(model.weights.at(n.bias_ref).dims) == w.dims[1], "bias shape mismatch at node " + n.id);
+        }
+        model.shapes[n.id] = {w.dims[1]};
+        break;
+      }
+      case HG_OP_CONVOLUTION: {
+        require(n.inputs.size() == 1, "Convolution takes one input");
+        require(!n.weight_ref.empty() && model.weights.count(n.weight_ref),
+                "Convolution needs a resolvable weight_ref");
+        auto in = model.shapes.at(n.inputs[0]);
+        const auto& w = model.weights.at(n.weight_ref);
+        require(w.dims.size() == 4, "Convolution weight must be (F,C,KH,KW)");
+        require(w.dims[0] == n.attrs.filters, "filter count mismatch");
+        require(w.dims[1] == in[0], "channel count mismatch");
+        require(w.dims[2] == n.attrs.window && w.dims[3] == n.attrs.window, "kernel window mismatch");
+        if (!n.bias_ref.empty()) {
+          require(model.weights.count(n.bias_ref), "unresolvable bias_ref");
+          require(elem_count(model.weights.at(n.bias_ref).dims) == n.attrs.filters, "bias shape mismatch at node " + n.id);
+        }
+        require(in.size() == 3, "Convolution expects a (C,H,W) input");
+        const u32 h = in[1] + n.attrs.pad[0] + n.attrs.pad[2];
+        const u32 wd = in[2] + n.attrs.pad[1] + n.attrs.pad[3];
+        require(n.attrs.window >= 1 && n.attrs.stride >= 1, "bad convolution attributes");
+        require(h >= n.attrs.window && wd >= n.attrs.window, "window exceeds padded input");
+        model.shapes[n.id] = {n.attrs.filters, (h - n.attrs.window) / n.attrs.stride + 1,
+                              (wd - n.attrs.window) / n.attrs.stride + 1};
+        break;
+      }
+      case HG_OP_RESHAPE: {
+        require(n.inputs.size() == 1, "Reshape takes one input");
+        require(elem_count(n.attrs.shape) == elem_count(model.shapes.at(n.inputs[0])),
+                "Reshape changes the element count at node " + n.id);
+        model.shapes[n.id] = n.attrs.shape;
+        break;
+      }
+      case HG_OP_RELU:
+        require(n.inputs.size() == 1, "Relu takes one input");
+        model.shapes[n.id] = model.shapes.at(n.inputs[0]);
+        break;
+      case HG_OP_MAXPOOL: {
+        require(n.inputs.size() == 1, "MaxPool takes one input");
+        auto in = model.shapes.at(n.inputs[0]);
+        require(in.size() == 3, "MaxPool expects a (C,H,W) input");
+        const u32 stride = n.attrs.pool_stride ? n.attrs.pool_stride : n.attrs.window;
+        require(n.attrs.window >= 1, "bad pooling window");
+        require(in[1] >= n.attrs.window && in[2] >= n.attrs.window, "pooling window exceeds input");
+        model.shapes[n.id] = {in[0], (in[1] - n.attrs.window) / stride + 1, (in[2] - n.attrs.window) / stride + 1};
+        break;
+      }
+      case HG_OP_OUTPUT:
+        ++outputs;
+        require(n.inputs.size() == 1, "Output takes one input");
+        model.shapes[n.id] = model.shapes.at(n.inputs[0]);
+        break;
+      default:
+        throw Error(HG_ERR_VALIDATION, "unknown op");
+    }
+  }
+  require(inputs == 1, "graph needs exactly one Input node");
+  require(outputs == 1, "graph needs exactly one Output node");
+  if (model.packing == HG_PACKING_COMPLEX) {
+    for (const auto& n : model.nodes) {
+      bool cc = n.op == HG_OP_SQUARE;
+      if (n.op == HG_OP_MULTIPLY) {
+        cc = model.node(n.inputs[0]).op != HG_OP_CONST_WEIGHT && model.node(n.inputs[1]).op != HG_OP_CONST_WEIGHT;
+      }
+      require(!cc, "complex packing cannot evaluate node " + n.id + " (cipher-cipher multiplication)");
+    }
+  }
+  model.finalized = true;
+}
+
+// ---------------------------------------------------------------------------
+// plan_rescaling (henet/graph.hpp:465-584)
+// ---------------------------------------------------------------------------
+static bool raises_scale(int op) {
+  return op == HG_OP_SQUARE || op == HG_OP_DOT || op == HG_OP_CONVOLUTION || op == HG_OP_MULTIPLY;
+}
+static bool is_refresh(int op) { return op == HG_OP_RELU || op == HG_OP_MAXPOOL; }
+static bool is_cipher_producing(const Model& m, const std::string& id) { return m.node(id).op != HG_OP_CONST_WEIGHT; }
+
+static u64 elementary_products(const Model& m, const Node& n) {
+  const auto& out = m.shapes.at(n.id);
+  switch (n.op) {
+    case HG_OP_SQUARE:
+    case HG_OP_MULTIPLY:
+      return elem_count(out);
+    case HG_OP_DOT:
+      return static_cast<u64>(m.shapes.at(n.inputs[0])[0]) * elem_count(out);
+    case HG_OP_CONVOLUTION: {
+      const auto& in = m.shapes.at(n.inputs[0]);
+      u64 taps = 0;
+      for (u32 y = 0; y < out[1]; ++y)
+        for (u32 x = 0; x < out[2]; ++x)
+          for (u32 ky = 0; ky < n.attrs.window; ++ky)
+            for (u32 kx = 0; kx < n.attrs.window; ++kx) {
+              const int64_t iy = static_cast<int64_t>(y * n.attrs.stride + ky) - n.attrs.pad[0];
+              const int64_t ix = static_cast<int64_t>(x * n.attrs.stride + kx) - n.attrs.pad[1];
+              if (iy >= 0 && iy < in[1] && ix >= 0 && ix < in[2]) ++taps;
+            }
+      return taps * in[0] * out[0];
+    }
+    default:
+      return 0;
+  }
+}
+
+static Plan plan_rescaling(const Context& ctx, const Model& model, int mode) {
+  require(model.finalized, "model is not finalized");
+  Plan plan;
+  plan.mode = mode;
+  const u32 top = static_cast<u32>(ctx.chain_len());
+  std::map<std::string, bool> mult_downstream;
+  for (auto it = model.nodes.rbegin(); it != model.nodes.rend(); ++it) mult_downstream[it->id] = false;
+  for (auto it = model.nodes.rbegin(); it != model.nodes.rend(); ++it) {
+    const Node& n = *it;
+    for (const auto& in : n.inputs) {
+      const bool contributes = raises_scale(n.op) || (!is_refresh(n.op) && mult_downstream[n.id]);
+      if (contributes) mult_downstream[in] = true;
+    }
+  }
+  const double s = ctx.default_scale;
+  for (const auto& n : model.nodes) {
+    NodePlan np;
+    double scale_in = s;
+    u32 level_in = top;
+    bool first = true;
+    for (const auto& in : n.inputs) {
+      if (!is_cipher_producing(model, in)) continue;
+      const auto& p = plan.nodes.at(in);
+      if (first) {
+        level_in = p.level_out;
+        scale_in = p.scale_out;
+        first = false;
+      } else {
+        require(p.level_out == level_in, "level mismatch between inputs of node " + n.id);
+      }
+    }
+    np.level_in = level_in;
+    np.level_out = level_in;
+    np.scale_out = scale_in;
+    if (is_refresh(n.op)) {
+      np.level_out = top;
+      np.scale_out = s;
+    } else if (raises_scale(n.op)) {
+      const bool cc = n.op == HG_OP_SQUARE || (n.op == HG_OP_MULTIPLY && is_cipher_producing(model, n.inputs[0]) &&
+                                               is_cipher_producing(model, n.inputs[1]));
+      const double raised = cc ? scale_in * scale_in : scale_in * s;
+      const bool rescale_after = (mode == HG_RESCALE_NAIVE) || mult_downstream[n.id];
+      np.decision = rescale_after ? HG_RESCALE_AFTER : HG_SKIP;
+      if (rescale_after) {
+        if (level_in < 2) throw Error(HG_ERR_VALIDATION, "infeasible depth: node " + n.id + " needs a rescale below level 1");
+        np.level_out = level_in - 1;
+        np.scale_out = raised / static_cast<double>(ctx.chain[level_in - 1]);
+        plan.planned_rescale_ops += mode == HG_RESCALE_NAIVE ? elementary_products(model, n) : elem_count(model.shapes.at(n.id));
+      } else {
+        np.scale_out = raised;
+      }
+      if (static_cast<long double>(np.scale_out) >= ctx.modulus_products.at(np.level_out))
+        throw Error(HG_ERR_VALIDATION, "infeasible depth: scale overflows q_level at node " + n.id);
+    }
+    plan.nodes[n.id] = np;
+  }
+  return plan;
+}
+
+// ---------------------------------------------------------------------------
+// Executor (henet/graph.hpp:792-1117)
+// ---------------------------------------------------------------------------
+struct Value {
+  bool is_cipher = false;
+  CtBatch cipher;
+  WeightTensor* plain = nullptr;
+};
+
+class Executor {
+ public:
+  Executor(const std::shared_ptr<Context>& ctx, Model& model, const Plan& plan, const RelinKeyDev* rk,
+           hg_nonlin_fn provider, void* user, cudaStream_t s, bool timing)
+      : ctx_(ctx), model_(model), plan_(plan), rk_(rk), provider_(provider), user_(user), s_(s), timing_(timing) {}
+
+  CtBatch run(const CtBatch& input, hg_exec_stats* stats, std::array<double, 11>* node_ms) {
+    require(model_.finalized, "model is not finalized");
+    require(input.level == ctx_->chain_len(), "input must enter at the top level");
+    require(input.packing == model_.packing, "input packing does not match the model");
+    require(input.polys == 2, "input ciphertexts must have 2 polynomials");
+    const Node* in_node = nullptr;
+    for (const auto& n : model_.nodes)
+      if (n.op == HG_OP_INPUT) in_node = &n;
+    require(in_node != nullptr, "graph has no Input node");
+    require(model_.shapes.at(in_node->id) == input.shape, "input shape does not match the model");
+    const auto t0 = std::chrono::steady_clock::now();
+    std::map<std::string, size_t> uses;
+    for (const auto& n : model_.nodes)
+      for (const auto& in : n.inputs) ++uses[in];
+
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> evs;
+    std::map<std::string, Value> values;
+    u32 layer_seq = 0;
+    const std::string out_id = [&] {
+      for (const auto& n : model_.nodes)
+        if (n.op == HG_OP_OUTPUT) return n.id;
+      throw Error(HG_ERR_VALIDATION, "graph has no Output node");
+    }();
+    for (const auto& n : model_.nodes) {
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (timing_) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, s_);
+      }
+      Value v;
+      switch (n.op) {
+        case HG_OP_INPUT:
+          v.is_cipher = true;
+          v.cipher = input;  // shares the caller's device buffer; never written
+          v.cipher.shape = model_.shapes.at(n.id);
+          break;
+        case HG_OP_CONST_WEIGHT:
+          v.plain = &model_.weights.at(n.weight_ref);
+          break;
+        case HG_OP_ADD:
+        case HG_OP_MULTIPLY:
+          v = eval_elementwise(n, values);
+          break;
+        case HG_OP_SQUARE:
+          v = eval_square(n, values);
+          break;
+        case HG_OP_DOT:
+        case HG_OP_CONVOLUTION:
+          v = eval_linear(n, values);
+          break;
+        case HG_OP_RESHAPE:
+        case HG_OP_OUTPUT:
+          v = values.at(n.inputs[0]);
+          v.cipher.shape = model_.shapes.at(n.id);
+          break;
+        case HG_OP_RELU:
+        case HG_OP_MAXPOOL:
+          v = eval_nonlinear(n, values, layer_seq++, stats);
+          break;
+        default:
+          throw Error(HG_ERR_VALIDATION, "unknown op");
+      }
+      if (v.is_cipher) {
+        require(v.cipher.level == plan_.nodes.at(n.id).level_out, "executed level diverged from the plan at node " + n.id);
+      }
+      if (timing_) {
+        cudaEventRecord(e1, s_);
+        evs.push_back({n.op, {e0, e1}});
+      }
+      for (const auto& in : n.inputs)
+        if (--uses[in] == 0) values.erase(in);
+      values[n.id] = std::move(v);
+    }
+    require(rescales_ == plan_.planned_rescale_ops, "executed rescale count diverged from the plan");
+    auto it = values.find(out_id);
+    require(it != values.end(), "output value missing");
+    CtBatch out = std::move(it->second.cipher);
+    values.clear();
+    if (stats || timing_) {
+      cuda_check(cudaStreamSynchronize(s_), "execute");
+    }
+    if (node_ms) node_ms->fill(0.0);
+    for (auto& e : evs) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e.second.first, e.second.second);
+      if (node_ms) (*node_ms)[e.first] += ms;
+      cudaEventDestroy(e.second.first);
+      cudaEventDestroy(e.second.second);
+    }
+    if (stats) {
+      stats->rescale_ops = rescales_;
+      stats->relin_ops = relins_;
+      stats->nonlin_elements += 0;
+      stats->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      stats->kernel_launches = launches_;
+    }
+    return out;
+  }
+
+ private:
+  void count(int r) {
+    if (r > 0) launches_ += static_cast<u64>(r);
+  }
+
+  // Dot / Convolution: mac_output over every output (henet/graph.hpp:905-993).
+  Value eval_linear(const Node& n, std::map<std::string, Value>& values) {
+    const Context& ctx = *ctx_;
+    const CtBatch& x = values.at(n.inputs[0]).cipher;
+    const auto& np = plan_.nodes.at(n.id);
+    const bool naive = plan_.mode == HG_RESCALE_NAIVE;
+    const bool layer_rescale = np.decision == HG_RESCALE_AFTER;
+    if (naive && layer_rescale)
+      throw Error(HG_ERR_UNSUPPORTED, "naive per-term rescaling of Dot/Convolution is not implemented on the GPU path");
+    WeightTensor& w = model_.weights.at(n.weight_ref);
+    WeightTensor* b = n.bias_ref.empty() ? nullptr : &model_.weights.at(n.bias_ref);
+    const double s = ctx.default_scale;
+    const u32 L = x.level;
+    const u32 N = ctx.n;
+    const auto& out_shape = model_.shapes.at(n.id);
+    const u64 M = elem_count(out_shape);
+
+    check_scalar_encodable(ctx, w.max_abs, L, s);
+    const double acc_scale = x.scale * s;  // term.scale = x.scale * pt.scale (henet/ckks.hpp:384)
+
+    Value v;
+    v.is_cipher = true;
+    v.cipher.packing = x.packing;
+    v.cipher.scale = acc_scale;
+    v.cipher.shape = out_shape;
+    ensure(ctx, v.cipher, M, 2, L, s_);
+
+    const float* wd = weight_dev(ctx, w, s_);
+    BufPtr bias_res;
+    BufPtr bias_pt;
+    u32 fold[kMaxPrimes] = {};
+
+    if (n.op == HG_OP_DOT) {
+      const u32 K = w.dims[0], Mo = w.dims[1];
+      const u32 warps = std::min<u32>(8, (Mo + 15) / 16);
+      const u32 BM = warps * 16;
+      const u32 Mpad = (Mo + BM - 1) / BM * BM;
+      BufPtr wres = ctx.alloc(static_cast<u64>(L) * K * Mpad * 4, s_);
+      cuda_check(cudaMemsetAsync(wres->ptr, 0, static_cast<u64>(L) * K * Mpad * 4, s_), "memset");
+      int r = launch_encode_scalars_f32(wd, w.data.size(), Mo, Mpad, static_cast<u64>(K) * Mpad, L, s,
+                                        static_cast<u32*>(wres->ptr), ctx.basis, s_);
+      check_launch(r, "encode weights");
+      count(r);
+      if (b && x.packing == HG_PACKING_REAL) {
+        check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
+        const float* bd = weight_dev(ctx, *b, s_);
+        bias_res = ctx.alloc(static_cast<u64>(L) * Mpad * 4, s_);
+        r = launch_encode_scalars_f32(bd, Mo, Mo, Mpad, Mpad, L, acc_scale, static_cast<u32*>(bias_res->ptr),
+                                      ctx.basis, s_);
+        check_launch(r, "encode bias");
+        count(r);
+      }
+      MacDenseArgs a{};
+      a.X = x.data();
+      a.Y = v.cipher.data();
+      a.W = static_cast<const u32*>(wres->ptr);
+      a.bias = bias_res ? static_cast<const u32*>(bias_res->ptr) : nullptr;
+      a.K = K;
+      a.M = Mo;
+      a.Mpad = Mpad;
+      a.N = N;
+      a.level = L;
+      a.polys = 2;
+      a.x_level = x.level;
+      for (u32 i = 0; i < L; ++i) {
+        const long double qm1 = static_cast<long double>(ctx.chain[i] - 1);
+        a.fold[i] = (qm1 * qm1 * K >= 18446744073709551616.0L) ? 1 : 0;
+      }
+      r = launch_mac_dense(a, ctx.basis, s_);
+      check_launch(r, "mac_dense");
+      count(r);
+    } else {
+      const auto& in_shape = x.shape;
+      require(in_shape.size() == 3, "Convolution expects a (C,H,W) input");
+      const u32 F = n.attrs.filters, C = in_shape[0], win = n.attrs.window;
+      BufPtr wres = ctx.alloc(static_cast<u64>(L) * w.data.size() * 4, s_);
+      int r = launch_encode_scalars_f32(wd, w.data.size(), static_cast<u32>(w.data.size()),
+                                        static_cast<u32>(w.data.size()), w.data.size(), L, s,
+                                        static_cast<u32*>(wres->ptr), ctx.basis, s_);
+      check_launch(r, "encode weights");
+      count(r);
+      if (b && x.packing == HG_PACKING_REAL) {
+        check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
+        const float* bd = weight_dev(ctx, *b, s_);
+        bias_res = ctx.alloc(static_cast<u64>(L) * F * 4, s_);
+        r = launch_encode_scalars_f32(bd, F, F, F, F, L, acc_scale, static_cast<u32*>(bias_res->ptr), ctx.basis, s_);
+        check_launch(r, "encode bias");
+        count(r);
+      }
+      MacConvArgs a{};
+      a.X = x.data();
+      a.Y = v.cipher.data();
+      a.W = static_cast<const u32*>(wres->ptr);
+      a.bias = bias_res ? static_cast<const u32*>(bias_res->ptr) : nullptr;
+      a.C = C;
+      a.IH = in_shape[1];
+      a.IW = in_shape[2];
+      a.F = F;
+      a.OH = out_shape[1];
+      a.OW = out_shape[2];
+      a.win = win;
+      a.stride = n.attrs.stride;
+      a.pad_top = n.attrs.pad[0];
+      a.pad_left = n.attrs.pad[1];
+      a.level = L;
+      a.polys = 2;
+      a.x_level = x.level;
+      a.N = N;
+      for (u32 i = 0; i < L; ++i) {
+        const long double qm1 = static_cast<long double>(ctx.chain[i] - 1);
+        a.fold[i] = (qm1 * qm1 * (C * win * win) >= 18446744073709551616.0L) ? 1 : 0;
+      }
+      r = launch_mac_conv(a, ctx.basis, s_);
+      check_launch(r, "mac_conv");
+      count(r);
+    }
+    if (b && x.packing == HG_PACKING_COMPLEX) {
+      // encode_broadcast under complex packing: encode_vector of (b + b i) in every slot
+      // (henet/encoding.hpp:275-283) at (level, acc.scale); one plaintext per bias value.
+      const u64 nb = b->data.size();
+      std::vector<double> slots(nb * ctx.n);
+      for (u64 i = 0; i < nb; ++i)
+        for (u32 j = 0; j < ctx.n / 2; ++j) {
+          slots[(i * ctx.n / 2 + j) * 2] = b->data[i];
+          slots[(i * ctx.n / 2 + j) * 2 + 1] = b->data[i];
+        }
+      BufPtr ds = ctx.alloc(slots.size() * sizeof(double), s_);
+      cuda_check(cudaMemcpyAsync(ds->ptr, slots.data(), slots.size() * sizeof(double), cudaMemcpyHostToDevice, s_),
+                 "h2d");
+      std::vector<unsigned long long> mant;
+      std::vector<int> ex;
+      const u64 before = ctx.core->launches.load();
+      bias_pt = encode_vectors_dev(ctx, static_cast<const double*>(ds->ptr), ctx.n / 2, nb, L, acc_scale, s_, mant, ex);
+      count(static_cast<int>(ctx.core->launches.load() - before));
+      EwArgs e{};
+      e.op = EwOp::AddVector;
+      e.a = v.cipher.data();
+      e.b = static_cast<const u32*>(bias_pt->ptr);
+      e.per_element = 1;
+      e.pt_div = n.op == HG_OP_DOT ? 1 : out_shape[1] * out_shape[2];
+      e.out = v.cipher.data();
+      e.count = M;
+      e.polys_a = 2;
+      e.polys_out = 2;
+      e.level = L;
+      run_ew(ctx, e, s_);
+      count(1);
+    }
+    if (layer_rescale) {
+      const u64 before = ctx.core->launches.load();
+      v.cipher = do_rescale(ctx, v.cipher, L - 1, s_);
+      count(static_cast<int>(ctx.core->launches.load() - before));
+      rescales_ += M;
+    }
+    return v;
+  }
+
+  Value eval_square(const Node& n, std::map<std::string, Value>& values) {
+    const CtBatch& x = values.at(n.inputs[0]).cipher;
+    const auto& np = plan_.nodes.at(n.id);
+    require(rk_ != nullptr, "graph contains cipher-cipher products but no relin key");
+    check_cc_mul(x);
+    Value v;
+    v.is_cipher = true;
+    const bool rs = np.decision == HG_RESCALE_AFTER;
+    const u64 before = ctx_->core->launches.load();
+    v.cipher = do_relin(*ctx_, *rk_, &x, &x, 1, rs, s_);
+    count(static_cast<int>(ctx_->core->launches.load() - before));
+    v.cipher.shape = x.shape;
+    relins_ += x.count;
+    if (rs) rescales_ += x.count;
+    return v;
+  }
+
+  Value eval_elementwise(const Node& n, std::map<std::string, Value>& values) {
+    const Context& ctx = *ctx_;
+    const Value& a = values.at(n.inputs[0]);
+    const Value& b = values.at(n.inputs[1]);
+    require(a.is_cipher || b.is_cipher, "constant-only op " + n.id);
+    const auto& np = plan_.nodes.at(n.id);
+    const bool mul = n.op == HG_OP_MULTIPLY;
+    const bool rs = np.decision == HG_RESCALE_AFTER;
+    const double s = ctx.default_scale;
+    Value v;
+    v.is_cipher = true;
+    const u64 before = ctx.core->launches.load();
+    if (a.is_cipher && b.is_cipher) {
+      const CtBatch& ca = a.cipher;
+      const CtBatch& cb = b.cipher;
+      require(ca.count == cb.count, "elementwise shape mismatch");
+      if (mul) {
+        require(rk_ != nullptr, "graph contains cipher-cipher products but no relin key");
+        check_cc_mul(ca);
+        check_cc_mul(cb);
+        check_same_shape(ca, cb);
+        v.cipher = do_relin(ctx, *rk_, &ca, &cb, 1, rs, s_);
+        relins_ += ca.count;
+        if (rs) rescales_ += ca.count;
+      } else {
+        check_same_shape(ca, cb);
+        v.cipher.packing = ca.packing;
+        v.cipher.scale = ca.scale;
+        ensure(ctx, v.cipher, ca.count, 2, ca.level, s_);
+        EwArgs e{};
+        e.op = EwOp::AddCC;
+        e.a = ca.data();
+        e.b = cb.data();
+        e.out = v.cipher.data();
+        e.count = ca.count;
+        e.polys_a = 2;
+        e.polys_out = 2;
+        e.level = ca.level;
+        run_ew(ctx, e, s_);
+      }
+    } else {
+      const CtBatch& x = a.is_cipher ? a.cipher : b.cipher;
+      WeightTensor& c = *(a.is_cipher ? b.plain : a.plain);
+      const bool broadcast = c.data.size() == 1;
+      require(broadcast || c.data.size() == x.count, "elementwise shape mismatch");
+      const float* cd = weight_dev(ctx, c, s_);
+      const u32 L = x.level;
+      v.cipher.packing = x.packing;
+      if (mul) {
+        check_scalar_encodable(ctx, c.max_abs, L, s);
+        BufPtr res = ctx.alloc(static_cast<u64>(c.data.size()) * L * 4, s_);
+        // residues laid out [value][limb]
+        int r = launch_encode_scalars_f32(cd, c.data.size(), 1, L, 1, L, s, static_cast<u32*>(res->ptr), ctx.basis, s_);
+        check_launch(r, "encode");
+        ctx.count(r);
+        v.cipher.scale = x.scale * s;
+        ensure(ctx, v.cipher, x.count, 2, L, s_);
+        EwArgs e{};
+        e.op = EwOp::MulScalar;
+        e.a = x.data();
+        e.res = static_cast<const u32*>(res->ptr);
+        e.per_element = broadcast ? 0 : 1;
+        e.out = v.cipher.data();
+        e.count = x.count;
+        e.polys_a = 2;
+        e.polys_out = 2;
+        e.level = L;
+        run_ew(ctx, e, s_);
+        if (rs) {
+          v.cipher = do_rescale(ctx, v.cipher, L - 1, s_);
+          rescales_ += x.count;
+        }
+      } else {
+        v.cipher.scale = x.scale;
+        ensure(ctx, v.cipher, x.count, 2, L, s_);
+        EwArgs e{};
+        e.a = x.data();
+        e.out = v.cipher.data();
+        e.count = x.count;
+        e.polys_a = 2;
+        e.polys_out = 2;
+        e.level = L;
+        e.per_element = broadcast ? 0 : 1;
+        BufPtr res;
+        if (model_.packing == HG_PACKING_REAL) {
+          check_scalar_encodable(ctx, c.max_abs, L, x.scale);
+          res = ctx.alloc(static_cast<u64>(c.data.size()) * L * 4, s_);
+          int r = launch_encode_scalars_f32(cd, c.data.size(), 1, L, 1, L, x.scale, static_cast<u32*>(res->ptr),
+                                            ctx.basis, s_);
+          check_launch(r, "encode");
+          ctx.count(r);
+          e.op = EwOp::AddScalar;
+          e.res = static_cast<const u32*>(res->ptr);
+        } else {
+          std::vector<double> slots(c.data.size() * ctx.n);
+          for (u64 i = 0; i < c.data.size(); ++i)
+            for (u32 j = 0; j < ctx.n / 2; ++j) {
+              slots[(i * ctx.n / 2 + j) * 2] = c.data[i];
+              slots[(i * ctx.n / 2 + j) * 2 + 1] = c.data[i];
+            }
+          BufPtr ds = ctx.alloc(slots.size() * sizeof(double), s_);
+          cuda_check(cudaMemcpyAsync(ds->ptr, slots.data(), slots.size() * sizeof(double), cudaMemcpyHostToDevice, s_),
+                     "h2d");
+          std::vector<unsigned long long> mant;
+          std::vector<int> ex;
+          res = encode_vectors_dev(ctx, static_cast<const double*>(ds->ptr), ctx.n / 2, c.data.size(), L, x.scale, s_,
+                                   mant, ex);
+          e.op = EwOp::AddVector;
+          e.b = static_cast<const u32*>(res->ptr);
+        }
+        run_ew(ctx, e, s_);
+      }
+    }
+    count(static_cast<int>(ctx.core->launches.load() - before));
+    v.cipher.shape = model_.shapes.at(n.id);
+    return v;
+  }
+
+  Value eval_nonlinear(const Node& n, std::map<std::string, Value>& values, u32 layer_seq, hg_exec_stats* stats) {
+    require(provider_ != nullptr, "graph contains " + n.id + " but no nonlinearity provider is attached");
+    const Context& ctx = *ctx_;
+    const CtBatch& x = values.at(n.inputs[0]).cipher;
+    const auto& out_shape = model_.shapes.at(n.id);
+    hg_tensor req;
+    req.ctx = ctx_;
+    u32 window = 1;
+    if (n.op == HG_OP_RELU) {
+      req.b = x;
+    } else {
+      // one window-sized group per output element (henet/graph.hpp:1072-1094): gather on device
+      const u32 stride = n.attrs.pool_stride ? n.attrs.pool_stride : n.attrs.window;
+      const u32 win = n.attrs.window;
+      window = win * win;
+      const u32 C = out_shape[0], oh = out_shape[1], ow = out_shape[2];
+      const u32 ihh = x.shape[1], iww = x.shape[2];
+      CtBatch g;
+      g.packing = x.packing;
+      g.scale = x.scale;
+      ensure(ctx, g, static_cast<u64>(C) * oh * ow * window, 2, x.level, s_);
+      const u64 ct_words = 2ull * x.level * ctx.n;
+      u64 o = 0;
+      for (u32 c = 0; c < C; ++c)
+        for (u32 y = 0; y < oh; ++y)
+          for (u32 xo = 0; xo < ow; ++xo)
+            for (u32 ky = 0; ky < win; ++ky)
+              for (u32 kx = 0; kx < win; ++kx) {
+                const u64 idx = (static_cast<u64>(c) * ihh + (y * stride + ky)) * iww + (xo * stride + kx);
+                cuda_check(cudaMemcpyAsync(g.data() + o * ct_words, x.data() + idx * ct_words, ct_words * 4,
+                                           cudaMemcpyDeviceToDevice, s_),
+                           "gather");
+                ++o;
+              }
+      req.b = g;
+    }
+    hg_tensor resp;
+    resp.ctx = ctx_;
+    resp.b.packing = x.packing;
+    resp.b.scale = ctx.default_scale;
+    ensure(ctx, resp.b, elem_count(out_shape), 2, static_cast<u32>(ctx.chain_len()), s_);
+    cuda_check(cudaStreamSynchronize(s_), "nonlinearity");
+    const int rc = provider_(user_, n.op == HG_OP_RELU ? HG_NONLIN_RELU : HG_NONLIN_MAXPOOL, window, layer_seq, &req, &resp);
+    if (rc != 0) throw Error(HG_ERR_VALIDATION, "nonlinearity provider failed: " + g_last_error);
+    require(resp.b.count == elem_count(out_shape), "provider returned the wrong element count");
+    require(resp.b.level == ctx.chain_len(), "provider must refresh to the top level");
+    if (stats) stats->nonlin_elements += req.b.count;
+    Value v;
+    v.is_cipher = true;
+    v.cipher = resp.b;
+    v.cipher.shape = out_shape;
+    return v;
+  }
+
+  std::shared_ptr<Context> ctx_;
+  Model& model_;
+  const Plan& plan_;
+  const RelinKeyDev* rk_;
+  hg_nonlin_fn provider_;
+  void* user_;
+  cudaStream_t s_;
+  bool timing_;
+  u64 rescales_ = 0, relins_ = 0, launches_ = 0;
+};
+
+}  // namespace hg
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace hg;
+
+extern "C" {
+
+const char* hg_last_error(void) { return g_last_error.c_str(); }
+int hg_abi_version(void) { return HG_ABI_VERSION; }
+
+int hg_ctx_create(uint32_t poly_degree, const uint64_t* chain, uint32_t chain_len, uint64_t special,
+                  double default_scale, int device, hg_ctx** out) {
+  return guard([&] {
+    require(out != nullptr && chain != nullptr, "null argument");
+    auto c = make_context(poly_degree, chain, chain_len, special, default_scale, device);
+    *out = new hg_ctx{c, {}};
+  });
+}
+
+void hg_ctx_destroy(hg_ctx* ctx) { delete ctx; }
+
+int hg_ctx_ntt_root(const hg_ctx* ctx, uint32_t i, uint64_t* root) {
+  return guard([&] {
+    require(ctx && root, "null argument");
+    require(i < ctx->c->roots.size(), "basis index out of range");
+    *root = ctx->c->roots[i];
+  });
+}
+
+void* hg_ctx_stream(hg_ctx* ctx) { return ctx ? ctx->c->core->stream : nullptr; }
+
+int hg_ctx_synchronize(hg_ctx* ctx) {
+  return guard([&] { cuda_check(cudaStreamSynchronize(ctx->c->core->stream), "synchronize"); });
+}
+
+uint64_t hg_ctx_launch_count(const hg_ctx* ctx) { return ctx ? ctx->c->core->launches.load() : 0; }
+
+int hg_tensor_create(hg_ctx* ctx, uint64_t count, uint32_t polys, uint32_t level, double scale, int packing,
+                     hg_tensor** out) {
+  return guard([&] {
+    require(ctx && out, "null argument");
+    require(polys == 2 || polys == 3, "ciphertext must have 2 or 3 polynomials");
+    require(level >= 1 && level <= ctx->c->chain_len(), "level outside the context chain");
+    require(packing == HG_PACKING_REAL || packing == HG_PACKING_COMPLEX, "unknown packing mode");
+    auto* t = new hg_tensor;
+    t->ctx = ctx->c;
+    t->b.scale = scale;
+    t->b.packing = packing;
+    ensure(*ctx->c, t->b, count, polys, level, nullptr);
+    t->b.shape = {static_cast<u32>(count)};
+    *out = t;
+  });
+}
+
+void hg_tensor_destroy(hg_tensor* t) { delete t; }
+
+int hg_tensor_info(const hg_tensor* t, uint64_t* count, uint32_t* polys, uint32_t* level, double* scale,
+                   int* packing) {
+  return guard([&] {
+    require(t != nullptr, "null tensor");
+    if (count) *count = t->b.count;
+    if (polys) *polys = t->b.polys;
+    if (level) *level = t->b.level;
+    if (scale) *scale = t->b.scale;
+    if (packing) *packing = t->b.packing;
+  });
+}
+
+int hg_tensor_set_scale(hg_tensor* t, double scale) {
+  return guard([&] { t->b.scale = scale; });
+}
+
+int hg_tensor_set_shape(hg_tensor* t, const uint32_t* dims, uint32_t ndims) {
+  return guard([&] {
+    std::vector<u32> d(dims, dims + ndims);
+    require(elem_count(d) == t->b.count, "shape does not match the element count");
+    t->b.shape = d;
+  });
+}
+
+int hg_tensor_get_shape(const hg_tensor* t, uint32_t* dims, uint32_t* ndims) {
+  return guard([&] {
+    require(*ndims >= t->b.shape.size(), "shape buffer too small");
+    for (size_t i = 0; i < t->b.shape.size(); ++i) dims[i] = t->b.shape[i];
+    *ndims = static_cast<uint32_t>(t->b.shape.size());
+  });
+}
+
+int hg_tensor_upload(hg_tensor* t, const uint64_t* words, void* stream) {
+  return guard([&] {
+    const Context& ctx = *t->ctx;
+    cudaStream_t s = ctx.pick(stream);
+    const u64 n = t->b.words(ctx.n);
+    BufPtr stage = ctx.alloc(n * 8 + sizeof(int), s);
+    int* bad = reinterpret_cast<int*>(static_cast<char*>(stage->ptr) + n * 8);
+    cuda_check(cudaMemsetAsync(bad, 0, sizeof(int), s), "memset");
+    cuda_check(cudaMemcpyAsync(stage->ptr, words, n * 8, cudaMemcpyHostToDevice, s), "h2d");
+    const int r = launch_narrow(static_cast<const u64*>(stage->ptr), t->b.data(), n, t->b.level, ctx.n, ctx.basis, bad, s);
+    check_launch(r, "narrow");
+    ctx.count(r);
+    int hbad = 0;
+    cuda_check(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaStreamSynchronize(s), "upload");
+    require(hbad == 0, "residue out of range");
+  });
+}
+
+int hg_tensor_download(const hg_tensor* t, uint64_t* words, void* stream) {
+  return guard([&] {
+    const Context& ctx = *t->ctx;
+    cudaStream_t s = ctx.pick(stream);
+    const u64 n = t->b.words(ctx.n);
+    BufPtr stage = ctx.alloc(n * 8, s);
+    const int r = launch_widen(t->b.data(), static_cast<u64*>(stage->ptr), n, s);
+    check_launch(r, "widen");
+    ctx.count(r);
+    cuda_check(cudaMemcpyAsync(words, stage->ptr, n * 8, cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaStreamSynchronize(s), "download");
+  });
+}
+
+int hg_tensor_upload_u32(hg_tensor* t, const uint32_t* words, void* stream) {
+  return guard([&] {
+    const Context& ctx = *t->ctx;
+    cuda_check(cudaMemcpyAsync(t->b.data(), words, t->b.words(ctx.n) * 4, cudaMemcpyHostToDevice, ctx.pick(stream)),
+               "h2d");
+  });
+}
+
+int hg_tensor_download_u32(const hg_tensor* t, uint32_t* words, void* stream) {
+  return guard([&] {
+    const Context& ctx = *t->ctx;
+    cudaStream_t s = ctx.pick(stream);
+    cuda_check(cudaMemcpyAsync(words, t->b.data(), t->b.words(ctx.n) * 4, cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaStreamSynchronize(s), "download");
+  });
+}
+
+void* hg_tensor_device_ptr(hg_tensor* t) { return t ? t->b.data() : nullptr; }
+uint64_t hg_tensor_words(const hg_tensor* t) { return t ? t->b.words(t->ctx->n) : 0; }
+
+int hg_relin_key_upload(hg_ctx* ctx, const uint64_t* words, uint64_t n_words, hg_relin_key** out) {
+  return guard([&] {
+    const Context& c = *ctx->c;
+    require(c.has_special, "relinearization keys need a special prime (not present in these parameters)");
+    const u64 L = c.chain_len(), n = c.n;
+    require(n_words == L * 2 * (L + 1) * n, "malformed relinearization key");
+    std::vector<uint2> k(n_words);
+    for (u64 j = 0; j < L; ++j)
+      for (u64 p = 0; p < 2; ++p)
+        for (u64 t = 0; t <= L; ++t) {
+          const u64 q = c.basis_mod(t);
+          const u64 base = ((j * 2 + p) * (L + 1) + t) * n;
+          for (u64 i = 0; i < n; ++i) {
+            const u64 w = words[base + i];
+            require(w < q, "residue out of range");
+            k[base + i] = make_uint2(static_cast<u32>(w), nt::shoup(w, q));
+          }
+        }
+    auto* rk = new hg_relin_key;
+    rk->ctx = ctx->c;
+    rk->k.chain_len = static_cast<u32>(L);
+    rk->k.key = c.alloc(k.size() * sizeof(uint2), nullptr);
+    cuda_check(cudaMemcpyAsync(rk->k.key->ptr, k.data(), k.size() * sizeof(uint2), cudaMemcpyHostToDevice, c.core->stream),
+               "h2d");
+    cuda_check(cudaStreamSynchronize(c.core->stream), "relin key upload");
+    *out = rk;
+  });
+}
+
+void hg_relin_key_destroy(hg_relin_key* rk) { delete rk; }
+
+int hg_add_ct_ct(hg_ctx* ctx, const hg_tensor* a, const hg_tensor* b, hg_tensor* out, void* stream) {
+  return guard([&] {
+    const Context& c = *ctx->c;
+    cudaStream_t s = c.pick(stream);
+    check_same_shape(a->b, b->b);
+    CtBatch o;
+    o.packing = a->b.packing;
+    o.scale = a->b.scale;
+    o.shape = a->b.shape;
+    ensure(c, o, a->b.count, a->b.polys, a->b.level, s);
+    EwArgs e{};
+    e.op = EwOp::AddCC;
+    e.a = a->b.data();
+    e.b = b->b.data();
+    e.out = o.data();
+    e.count = a->b.count;
+    e.polys_a = a->b.polys;
+    e.polys_out = a->b.polys;
+    e.level = a->b.level;
+    run_ew(c, e, s);
+    out->b = o;
+  });
+}
+
+static BufPtr upload_residues(const Context& c, const hg_tensor* ct, const uint64_t* residues, int per_element,
+                              cudaStream_t s) {
+  const u64 nvals = (per_element ? ct->b.count : 1) * ct->b.level;
+  std::vector<u32> r(nvals);
+  for (u64 i = 0; i < nvals; ++i) {
+    const u64 q = c.chain[i % ct->b.level];
+    require(residues[i] < q, "residue out of range");
+    r[i] = static_cast<u32>(residues[i]);
+  }
+  BufPtr d = c.alloc(nvals * 4, s);
+  cuda_check(cudaMemcpyAsync(d->ptr, r.data(), nvals * 4, cudaMemcpyHostToDevice, s), "h2d");
+  cuda_check(cudaStreamSynchronize(s), "h2d");
+  return d;
+}
+
+int hg_mul_ct_pt_scalar(hg_ctx* ctx, const hg_tensor* ct, const uint64_t* residues, int per_element, double pt_scale,
+                        hg_tensor* out, void* stream) {
+  return guard([&] {
+    const Context& c = *ctx->c;
+    cudaStream_t s = c.pick(stream);
+    BufPtr r = upload_residues(c, ct, residues, per_element, s);
+    CtBatch o;
+    o.packing = ct->b.packing;
+    o.scale = ct->b.scale * pt_scale;
+    o.shape = ct->b.shape;
+    ensure(c, o, ct->b.count, ct->b.polys, ct->b.level, s);
+    EwArgs e{};
+    e.op = EwOp::MulScalar;
+    e.a = ct->b.data();
+    e.res = static_cast<const u32*>(r->ptr);
+    e.per_element = per_element;
+    e.out = o.data();
+    e.count = ct->b.count;
+    e.polys_a = ct->b.polys;
+    e.polys_out = ct->b.polys;
+    e.level = ct->b.level;
+    run_ew(c, e, s);
+    out->b = o;
+  });
+}
+
+int hg_add_ct_pt_scalar(hg_ctx* ctx, const hg_tensor* ct, const uint64_t* residues, int per_element, double pt_scale,
+                        hg_tensor* out, void* stream) {
+  return guard([&] {
+    const Context& c = *ctx->c;
+    cudaStream_t s = c.pick(stream);
+    require(scales_match(ct->b.scale, pt_scale), "ciphertext/plaintext scale mismatch");
+    BufPtr r = upload_residues(c, ct, residues, per_element, s);
+    CtBatch o;
+    o.packing = ct->b.packing;
+    o.scale = ct->b.scale;
+    o.shape = ct->b.shape;
+    ensure(c, o, ct->b.count, ct->b.polys, ct->b.level, s);
+    EwArgs e{};
+    e.op = EwOp::AddScalar;
+    e.a = ct->b.data();
+    e.res = static_cast<const u32*>(r->ptr);
+    e.per_element = per_element;
+    e.out = o.data();
+    e.count = ct->b.count;
+    e.polys_a = ct->b.polys;
+    e.polys_out = ct->b.polys;
+    e.level = ct->b.level;
+    run_ew(c, e, s);
+    out->b = o;
+  });
+}
+
+int hg_add_ct_pt_vector(hg_ctx* ctx, const hg_tensor* ct, const uint64_t* pt_words, int per_element, double pt_scale,
+                        hg_tensor* out, void* stream) {
+  return guard([&] {
+    const Context& c = *ctx->c;
+    cudaStream_t s = c.pick(stream);
+    require(scales_match(ct->b.scale, pt_scale), "ciphertext/plaintext scale mismatch");
+    const u64 L = ct->b.level, n = c.n;
+    const u64 nw = (per_element ? ct->b.count : 1) * L * n;
+    std::vector<u32> w(nw);
+    for (u64 i = 0; i < nw; ++i) {
+      require(pt_words[i] < c.chain[(i / n) % L], "residue out of range");
+      w[i] = static_cast<u32>(pt_words[i]);
+    }
+    BufPtr d = c.alloc(nw * 4, s);
+    cuda_check(cudaMemcpyAsync(d->ptr, w.data(), nw * 4, cudaMemcpyHostToDevice, s), "h2d");
+    CtBatch o;
+    o.packing = ct->b.packing;
+    o.scale = ct->b.scale;
+    o.shape = ct->b.shape;
+    ensure(c, o, ct->b.count, ct->b.polys, ct->b.level, s);
+    EwArgs e{};
+    e.op = EwOp::AddVector;
+    e.a = ct->b.data();
+    e.b = static_cast<const u32*>(d->ptr);
+    e.per_element = per_element;
+    e.out = o.data();
+    e.count = ct->b.count;
+    e.polys_a = ct->b.polys;
+    e.polys_out = ct->b.polys;
+    e.level = ct->b.level;
+    run_ew(c, e, s);
+    cuda_check(cudaStreamSynchronize(s), "add_ct_pt_vector");
+    out->b = o;
+  });
+}
+
+static void tensor_op(hg_ctx* ctx, const hg_tensor* a, const hg_tensor* b, hg_tensor* out, void* stream) {
+  const Context& c = *ctx->c;
+  cudaStream_t s = c.pick(stream);
+  check_cc_mul(a->b);
+  check_cc_mul(b->b);
+  if (a != b) check_same_shape(a->b, b->b);
+  CtBatch o;
+  o.packing = a->b.packing;
+  o.scale = a->b.scale * b->b.scale;
+  o.shape = a->b.shape;
+  ensure(c, o, a->b.count, 3, a->b.level, s);
+  EwArgs e{};
+  e.op = EwOp::Tensor;
+  e.a = a->b.data();
+  e.b = b->b.data();
+  e.out = o.data();
+  e.count = a->b.count;
+  e.polys_a = 2;
+  e.polys_out = 3;
+  e.level = a->b.level;
+  run_ew(c, e, s);
+  out->b = o;
+}
+
+int hg_square(hg_ctx* ctx, const hg_tensor* ct, hg_tensor* out, void* stream) {
+  return guard([&] { tensor_op(ctx, ct, ct, out, stream); });
+}
+
+int hg_mul_ct_ct(hg_ctx* ctx, const hg_tensor* a, const hg_tensor* b, hg_tensor* out, void* stream) {
+  return guard([&] { tensor_op(ctx, a, b, out, stream); });
+}
+
+int hg_relinearize(hg_ctx* ctx, const hg_tensor* ct, const hg_relin_key* rk, hg_tensor* out, void* stream) {
+  return guard([&] {
+    require(ct->b.polys == 3, "relinearize expects a size-3 ciphertext");
+    CtBatch o = do_relin(*ctx->c, rk->k, &ct->b, nullptr, 0, false, ctx->c->pick(stream));
+    o.shape = ct->b.shape;
+    out->b = o;
+  });
+}
+
+int hg_square_relin(hg_ctx* ctx, const hg_tensor* ct, const hg_relin_key* rk, int rescale, hg_tensor* out,
+                    void* stream) {
+  return guard([&] {
+    check_cc_mul(ct->b);
+    CtBatch o = do_relin(*ctx->c, rk->k, &ct->b, &ct->b, 1, rescale != 0, ctx->c->pick(stream));
+    o.shape = ct->b.shape;
+    out->b = o;
+  });
+}
+
+int hg_rescale(hg_ctx* ctx, const hg_tensor* ct, uint32_t target_level, hg_tensor* out, void* stream) {
+  return guard([&] {
+    CtBatch o = do_rescale(*ctx->c, ct->b, target_level, ctx->c->pick(stream));
+    o.shape = ct->b.shape;
+    out->b = o;
+  });
+}
+
+int hg_ntt_forward(hg_ctx* ctx, hg_tensor* t, void* stream) {
+  return guard([&] {
+    const Context& c = *ctx->c;
+    const int r = launch_ntt(static_cast<int>(c.logn), t->b.data(), t->b.count * t->b.polys * t->b.level, t->b.level,
+                             false, c.basis, c.pick(stream));
+    check_launch(r, "ntt");
+    c.count(r);
+  });
+}
+
+int hg_ntt_inverse(hg_ctx* ctx, hg_tensor* t, void* stream) {
+  return guard([&] {
+    const Context& c = *ctx->c;
+    const int r = launch_ntt(static_cast<int>(c.logn), t->b.data(), t->b.count * t->b.polys * t->b.level, t->b.level,
+                             true, c.basis, c.pick(stream));
+    check_launch(r, "intt");
+    c.count(r);
+  });
+}
+
+int hg_encode_scalars(hg_ctx* ctx, const double* values, uint64_t count, uint32_t level, double scale,
+                      uint64_t* out_residues) {
+  return guard([&] {
+    const Context& c = *ctx->c;
+    cudaStream_t s = c.core->stream;
+    double mx = 0;
+    for (u64 i = 0; i < count; ++i) mx = std::max(mx, std::fabs(values[i]));
+    check_scalar_encodable(c, mx, level, scale);
+    BufPtr dv = c.alloc(count * 8, s);
+    BufPtr dr = c.alloc(count * level * 4, s);
+    cuda_check(cudaMemcpyAsync(dv->ptr, values, count * 8, cudaMemcpyHostToDevice, s), "h2d");
+    const int r = launch_encode_scalars_f64(static_cast<const double*>(dv->ptr), count, 1, level, 1, level, scale,
+                                            static_cast<u32*>(dr->ptr), c.basis, s);
+    check_launch(r, "encode_scalars");
+    c.count(r);
+    std::vector<u32> h(count * level);
+    cuda_check(cudaMemcpyAsync(h.data(), dr->ptr, h.size() * 4, cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaStreamSynchronize(s), "encode_scalars");
+    for (u64 i = 0; i < h.size(); ++i) out_residues[i] = h[i];
+  });
+}
+
+int hg_encode_vector(hg_ctx* ctx, const double* slots_re_im, uint32_t n_slots, uint64_t count, uint32_t level,
+                     double scale, uint64_t* out_words) {
+  return guard([&] {
+    const Context& c = *ctx->c;
+    cudaStream_t s = c.core->stream;
+    BufPtr ds = c.alloc(count * n_slots * 2 * sizeof(double) + 16, s);
+    cuda_check(cudaMemcpyAsync(ds->ptr, slots_re_im, count * n_slots * 2 * sizeof(double), cudaMemcpyHostToDevice, s),
+               "h2d");
+    std::vector<unsigned long long> mant;
+    std::vector<int> ex;
+    BufPtr pt = encode_vectors_dev(c, static_cast<const double*>(ds->ptr), n_slots, count, level, scale, s, mant, ex);
+    const u64 nw = count * level * static_cast<u64>(c.n);
+    std::vector<u32> h(nw);
+    cuda_check(cudaMemcpyAsync(h.data(), pt->ptr, nw * 4, cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaStreamSynchronize(s), "encode_vector");
+    for (u64 i = 0; i < nw; ++i) out_words[i] = h[i];
+  });
+}
+
+int hg_model_create(int packing, hg_model** out) {
+  return guard([&] {
+    require(packing == HG_PACKING_REAL || packing == HG_PACKING_COMPLEX, "unknown packing mode");
+    auto* m = new hg_model;
+    m->m.packing = packing;
+    *out = m;
+  });
+}
+
+void hg_model_destroy(hg_model* m) { delete m; }
+
+int hg_model_add_weight(hg_model* m, const char* name, const uint32_t* dims, uint32_t ndims, const float* data) {
+  return guard([&] {
+    WeightTensor w;
+    w.dims.assign(dims, dims + ndims);
+    const u64 n = elem_count(w.dims);
+    w.data.assign(data, data + n);
+    for (float v : w.data) w.max_abs = std::max(w.max_abs, std::fabs(v));
+    m->m.weights[name] = std::move(w);
+    m->m.finalized = false;
+  });
+}
+
+int hg_model_add_node(hg_model* m, const hg_node_desc* d) {
+  return guard([&] {
+    require(d && d->id, "null node");
+    require(d->op >= HG_OP_INPUT && d->op <= HG_OP_OUTPUT, "unknown op");
+    Node n;
+    n.id = d->id;
+    n.op = d->op;
+    for (u32 i = 0; i < d->n_inputs; ++i) n.inputs.emplace_back(d->inputs[i]);
+    if (d->shape) n.attrs.shape.assign(d->shape, d->shape + d->shape_len);
+    n.attrs.stride = d->stride ? d->stride : 1;
+    n.attrs.window = d->window;
+    n.attrs.filters = d->filters;
+    n.attrs.pool_stride = d->pool_stride;
+    for (int i = 0; i < 4; ++i) n.attrs.pad[i] = d->pad[i];
+    if (d->weight_ref) n.weight_ref = d->weight_ref;
+    if (d->bias_ref) n.bias_ref = d->bias_ref;
+    require(!m->m.index.count(n.id), "duplicate node id: " + n.id);
+    m->m.index.emplace(n.id, m->m.nodes.size());
+    m->m.nodes.push_back(std::move(n));
+    m->m.finalized = false;
+  });
+}
+
+int hg_model_finalize(hg_model* m) {
+  return guard([&] { finalize_model(m->m); });
+}
+
+int hg_model_node_count(const hg_model* m, uint32_t* n) {
+  return guard([&] { *n = static_cast<uint32_t>(m->m.nodes.size()); });
+}
+
+int hg_model_shape(const hg_model* m, const char* id, uint32_t* dims, uint32_t* ndims) {
+  return guard([&] {
+    auto it = m->m.shapes.find(id);
+    require(it != m->m.shapes.end(), "unknown node id");
+    require(*ndims >= it->second.size(), "shape buffer too small");
+    for (size_t i = 0; i < it->second.size(); ++i) dims[i] = it->second[i];
+    *ndims = static_cast<uint32_t>(it->second.size());
+  });
+}
+
+int hg_plan_rescaling(const hg_ctx* ctx, const hg_model* m, int mode, hg_plan** out) {
+  return guard([&] {
+    Plan p = plan_rescaling(*ctx->c, m->m, mode);
+    *out = new hg_plan{std::move(p)};
+  });
+}
+
+int hg_plan_create(int mode, uint64_t planned, hg_plan** out) {
+  return guard([&] {
+    auto* p = new hg_plan;
+    p->p.mode = mode;
+    p->p.planned_rescale_ops = planned;
+    *out = p;
+  });
+}
+
+int hg_plan_set_node(hg_plan* p, const char* id, int decision, uint32_t level_in, uint32_t level_out, double scale_out) {
+  return guard([&] {
+    NodePlan np;
+    np.decision = decision;
+    np.level_in = level_in;
+    np.level_out = level_out;
+    np.scale_out = scale_out;
+    p->p.nodes[id] = np;
+  });
+}
+
+int hg_plan_get_node(const hg_plan* p, const char* id, int* decision, uint32_t* level_in, uint32_t* level_out,
+                     double* scale_out) {
+  return guard([&] {
+    auto it = p->p.nodes.find(id);
+    require(it != p->p.nodes.end(), "unknown node id");
+    if (decision) *decision = it->second.decision;
+    if (level_in) *level_in = it->second.level_in;
+    if (level_out) *level_out = it->second.level_out;
+    if (scale_out) *scale_out = it->second.scale_out;
+  });
+}
+
+uint64_t hg_plan_planned_rescales(const hg_plan* p) { return p ? p->p.planned_rescale_ops : 0; }
+void hg_plan_destroy(hg_plan* p) { delete p; }
+
+int hg_execute(hg_ctx* ctx, const hg_model* m, const hg_plan* plan, const hg_tensor* input, const hg_relin_key* rk,
+               hg_nonlin_fn provider, void* provider_user, hg_tensor** output, hg_exec_stats* stats, void* stream) {
+  return guard([&] {
+    require(ctx && m && plan && input && output, "null argument");
+    if (stats) *stats = hg_exec_stats{};
+    cudaStream_t s = ctx->c->pick(stream);
+    const bool timing = getenv("HG_NODE_TIMING") != nullptr;
+    Executor ex(ctx->c, const_cast<hg_model*>(m)->m, plan->p, rk ? &rk->k : nullptr, provider, provider_user, s, timing);
+    CtBatch out = ex.run(input->b, stats, timing ? &ctx->last_node_ms : nullptr);
+    auto* t = new hg_tensor;
+    t->ctx = ctx->c;
+    t->b = std::move(out);
+    *output = t;
+  });
+}
+
+int hg_bench_imad_wide(int device, double* ops_per_s) {
+  return guard([&] {
+    *ops_per_s = bench_imad_wide(device);
+    cuda_check(cudaGetLastError(), "imad probe");
+  });
+}
+
+int hg_last_exec_node_ms(hg_ctx* ctx, double* ms_by_op) {
+  return guard([&] {
+    for (int i = 0; i < 11; ++i) ms_by_op[i] = ctx->last_node_ms[i];
+  });
+}
+
+}  // extern "C"

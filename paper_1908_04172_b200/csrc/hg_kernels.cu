@@ -1,0 +1,901 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// sm_100a kernels for the nGraph-HE2 encrypted-inference hot path.
+//
+//   k_ntt         batched per-limb negacyclic NTT / INTT       (henet/modmath.hpp:338-398)
+//   k_rescale     NTT-domain rescale: INTT only the dropped limb, NTT the
+//                 rounding correction under each kept prime   (henet/ckks.hpp:132-154, 504-519)
+//   k_mac_dense   Dot: Y = W^T X per (poly, limb), lazy u64 accumulation,
+//                 one Barrett reduction, bias in the epilogue  (henet/graph.hpp:905-954)
+//   k_mac_conv    Convolution: implicit im2col, all filters of a position
+//                 share the gathered inputs                   (henet/graph.hpp:956-993)
+//   k_relin_*     square/tensor -> digit INTT -> key-switch inner product ->
+//                 special-prime mod-down (+ fused rescale)    (henet/ckks.hpp:407-499)
+//   k_ew          element-wise ct+ct, ct*pt, ct+pt, tensor    (henet/ckks.hpp:281-437)
+//   k_encode_*    exact x87 scalar encoding and the FFT vector encoder
+//                                                             (henet/encoding.hpp:122-197, fft.hpp)
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "hg_kernels.hpp"
+
+namespace hg {
+
+// ===========================================================================
+// Batched NTT (hg_ntt_forward / hg_ntt_inverse)
+// ===========================================================================
+template <int LOGN, bool INV>
+__global__ void __launch_bounds__(1 << (LOGN - 5)) k_ntt(u32* data, u32 level, Basis B) {
+  using NT = Ntt<LOGN>;
+  extern __shared__ u32 sm[];
+  const u32 tid = threadIdx.x;
+  const u64 row = blockIdx.x;
+  const DevPrime& P = B.p[row % level];
+  u32* r = data + row * NT::N;
+  u32 x[32];
+  if (!INV) {
+    NT::gload_A(x, r, tid);
+    NT::forward(x, sm, tid, P);
+    NT::gstore_C(x, r, tid);
+  } else {
+    NT::gload_C(x, r, tid);
+    NT::inverse(x, sm, tid, P);
+    NT::gstore_A(x, r, tid);
+  }
+}
+
+// residue of a signed value with |c| < 2^31 (any relation to q)
+__device__ __forceinline__ u32 signed_residue(i32 c, const DevPrime& P) {
+  const u32 m = reduce32(static_cast<u32>(c < 0 ? -c : c), P);
+  return c < 0 ? csub(P.q - m, P.q) : m;
+}
+
+// ===========================================================================
+// Rescale (one CTA per (ciphertext, polynomial))
+// ===========================================================================
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5)) k_rescale(RescaleArgs a, Basis B) {
+  using NT = Ntt<LOGN>;
+  constexpr int N = NT::N;
+  extern __shared__ u32 sm[];
+  const u32 tid = threadIdx.x;
+  const u64 row = blockIdx.x;
+  const u32 L = a.level;
+  const u32* src = a.in + row * L * N;
+  u32* dst = a.out + row * (L - 1) * N;
+
+  u32 x[32];
+  i32 c[32];
+  {
+    const DevPrime& Pl = B.p[L - 1];
+    NT::gload_C(x, src + static_cast<u64>(L - 1) * N, tid);
+    NT::inverse(x, sm, tid, Pl);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) c[k] = centered_round_rem(x[k], Pl);
+  }
+  for (u32 i = 0; i + 1 < L; ++i) {
+    const DevPrime& Pi = B.p[i];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) x[k] = signed_residue(c[k], Pi);
+    NT::forward(x, sm, tid, Pi);
+    u32 y[32];
+    NT::gload_C(y, src + static_cast<u64>(i) * N, tid);
+    const u32 q = Pi.q, pv = a.pinv[i], ps = a.pinv_sh[i];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) x[k] = mul_shoup(y[k] + q - x[k], pv, ps, q);
+    NT::gstore_C(x, dst + static_cast<u64>(i) * N, tid);
+  }
+}
+
+// ===========================================================================
+// Dense modular contraction (Dot)
+//   grid.x = N / 128 coefficient tiles, grid.y = M tiles of 16*warps outputs,
+//   grid.z = polys * level.  Warp w owns outputs m0 + 16w .. +16, lane owns
+//   coefficients n0 + 4*lane .. +4.  X and W tiles of BK = 16 taps are staged
+//   in shared memory with cp.async (double buffered).
+// ===========================================================================
+constexpr int kBK = 16;
+constexpr int kTM = 16;
+constexpr int kBN = 128;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int bytes = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__global__ void __launch_bounds__(256) k_mac_dense(MacDenseArgs a, Basis B) {
+  __shared__ __align__(16) u32 xs[2][kBK][kBN];
+  __shared__ __align__(16) u32 ws[2][kBK][kTM * 8];
+  const u32 warps = blockDim.x >> 5;
+  const u32 BM = kTM * warps;
+  const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 n0 = blockIdx.x * kBN;
+  const u32 m0 = blockIdx.y * BM;
+  const u32 pl = blockIdx.z;           // poly * level + limb
+  const u32 poly = pl / a.level, limb = pl % a.level;
+  const DevPrime& P = B.p[limb];
+  const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;  // words per input ct
+  const u32* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n0;
+  const u32* Wb = a.W + static_cast<u64>(limb) * a.K * a.Mpad + m0;
+  const bool fold = a.fold[limb] != 0;
+  const u64 r32 = P.r32;
+
+  const u32 ktiles = (a.K + kBK - 1) / kBK;
+  auto load_tile = [&](u32 kt, int st) {
+    // X tile: kBK rows x 128 words = 512 chunks of 16 B
+    for (u32 c = tid; c < kBK * (kBN / 4); c += blockDim.x) {
+      const u32 r = c / (kBN / 4), col = (c % (kBN / 4)) * 4;
+      const u32 k = kt * kBK + r;
+      const bool v = k < a.K;
+      cp_async16(&xs[st][r][col], Xb + (v ? static_cast<u64>(k) * xstride : 0) + col, v);
+    }
+    // W tile: kBK rows x BM words
+    const u32 wchunks = kBK * (BM / 4);
+    for (u32 c = tid; c < wchunks; c += blockDim.x) {
+      const u32 r = c / (BM / 4), col = (c % (BM / 4)) * 4;
+      const u32 k = kt * kBK + r;
+      const bool v = k < a.K;
+      cp_async16(&ws[st][r][col], Wb + (v ? static_cast<u64>(k) * a.Mpad : 0) + col, v);
+    }
+    cp_async_commit();
+  };
+
+  u64 acc[kTM][4];
+#pragma unroll
+  for (int i = 0; i < kTM; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0;
+
+  load_tile(0, 0);
+  for (u32 kt = 0; kt < ktiles; ++kt) {
+    const int st = kt & 1;
+    if (kt + 1 < ktiles) {
+      load_tile(kt + 1, st ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < kBK; ++kk) {
+      const uint4 xv = *reinterpret_cast<const uint4*>(&xs[st][kk][lane * 4]);
+      u32 w[kTM];
+#pragma unroll
+      for (int i = 0; i < kTM; i += 4) {
+        const uint4 wv = *reinterpret_cast<const uint4*>(&ws[st][kk][warp * kTM + i]);
+        w[i] = wv.x; w[i + 1] = wv.y; w[i + 2] = wv.z; w[i + 3] = wv.w;
+      }
+#pragma unroll
+      for (int i = 0; i < kTM; ++i) {
+        acc[i][0] += static_cast<u64>(w[i]) * xv.x;
+        acc[i][1] += static_cast<u64>(w[i]) * xv.y;
+        acc[i][2] += static_cast<u64>(w[i]) * xv.z;
+        acc[i][3] += static_cast<u64>(w[i]) * xv.w;
+      }
+      if (fold && (kk & 7) == 7) {
+#pragma unroll
+        for (int i = 0; i < kTM; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = (acc[i][j] & 0xffffffffull) + (acc[i][j] >> 32) * r32;
+      }
+    }
+    __syncthreads();
+  }
+
+  const u32 q = P.q;
+#pragma unroll
+  for (int i = 0; i < kTM; ++i) {
+    const u32 m = m0 + warp * kTM + i;
+    if (m >= a.M) continue;
+    u32 bv = 0;
+    if (a.bias != nullptr && poly == 0) bv = __ldg(&a.bias[static_cast<u64>(limb) * a.Mpad + m]);
+    uint4 o;
+    o.x = addmod(reduce64(acc[i][0], P), bv, q);
+    o.y = addmod(reduce64(acc[i][1], P), bv, q);
+    o.z = addmod(reduce64(acc[i][2], P), bv, q);
+    o.w = addmod(reduce64(acc[i][3], P), bv, q);
+    u32* yp = a.Y + ((static_cast<u64>(m) * a.polys + poly) * a.level + limb) * a.N + n0 + lane * 4;
+    *reinterpret_cast<uint4*>(yp) = o;
+  }
+}
+
+// ===========================================================================
+// Convolution (direct, implicit im2col)
+//   grid.x = N / (4 * 128), grid.y = output positions, grid.z = polys * level.
+//   Each thread: 4 coefficients x all filters (chunks of kFT).
+// ===========================================================================
+constexpr int kFT = 8;
+constexpr int kMaxTaps = 1024;
+
+__global__ void __launch_bounds__(128) k_mac_conv(MacConvArgs a, Basis B) {
+  __shared__ u32 tap_in[kMaxTaps];
+  __shared__ u32 tap_w[kMaxTaps];
+  __shared__ u32 ntaps_s;
+  __shared__ __align__(16) u32 wsm[kMaxTaps * kFT];
+  const u32 tid = threadIdx.x;
+  const u32 pos = blockIdx.y;
+  const u32 oy = pos / a.OW, ox = pos % a.OW;
+  const u32 pl = blockIdx.z;
+  const u32 poly = pl / a.level, limb = pl % a.level;
+  const DevPrime& P = B.p[limb];
+  const u32 n = (blockIdx.x * blockDim.x + tid) * 4;
+  const u32 taps_all = a.C * a.win * a.win;
+
+  if (tid == 0) {
+    // valid taps in ascending (c, ky, kx) order, henet/graph.hpp:976-989
+    u32 cnt = 0;
+    for (u32 c = 0; c < a.C; ++c)
+      for (u32 ky = 0; ky < a.win; ++ky)
+        for (u32 kx = 0; kx < a.win; ++kx) {
+          const int iy = static_cast<int>(oy * a.stride + ky) - static_cast<int>(a.pad_top);
+          const int ix = static_cast<int>(ox * a.stride + kx) - static_cast<int>(a.pad_left);
+          if (iy < 0 || iy >= static_cast<int>(a.IH) || ix < 0 || ix >= static_cast<int>(a.IW)) continue;
+          tap_in[cnt] = (c * a.IH + iy) * a.IW + ix;
+          tap_w[cnt] = (c * a.win + ky) * a.win + kx;
+          ++cnt;
+        }
+    ntaps_s = cnt;
+  }
+  __syncthreads();
+  const u32 ntaps = ntaps_s;
+  const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
+  const u32* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n;
+  const u32* Wl = a.W + static_cast<u64>(limb) * a.F * taps_all;
+  const bool fold = a.fold[limb] != 0;
+  const u64 r32 = P.r32;
+  const u32 q = P.q;
+
+  for (u32 f0 = 0; f0 < a.F; f0 += kFT) {
+    __syncthreads();
+    for (u32 i = tid; i < ntaps * kFT; i += blockDim.x) {
+      const u32 t = i / kFT, f = f0 + i % kFT;
+      wsm[i] = f < a.F ? __ldg(&Wl[static_cast<u64>(f) * taps_all + tap_w[t]]) : 0u;
+    }
+    __syncthreads();
+    u64 acc[kFT][4];
+#pragma unroll
+    for (int f = 0; f < kFT; ++f)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[f][j] = 0;
+    for (u32 t = 0; t < ntaps; ++t) {
+      const uint4 xv = __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(tap_in[t]) * xstride));
+#pragma unroll
+      for (int f = 0; f < kFT; ++f) {
+        const u32 w = wsm[t * kFT + f];
+        acc[f][0] += static_cast<u64>(w) * xv.x;
+        acc[f][1] += static_cast<u64>(w) * xv.y;
+        acc[f][2] += static_cast<u64>(w) * xv.z;
+        acc[f][3] += static_cast<u64>(w) * xv.w;
+      }
+      if (fold && (t & 7) == 7) {
+#pragma unroll
+        for (int f = 0; f < kFT; ++f)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[f][j] = (acc[f][j] & 0xffffffffull) + (acc[f][j] >> 32) * r32;
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < kFT; ++f) {
+      const u32 ff = f0 + f;
+      if (ff >= a.F) continue;
+      u32 bv = 0;
+      if (a.bias != nullptr && poly == 0) bv = __ldg(&a.bias[static_cast<u64>(limb) * a.F + ff]);
+      uint4 o;
+      o.x = addmod(reduce64(acc[f][0], P), bv, q);
+      o.y = addmod(reduce64(acc[f][1], P), bv, q);
+      o.z = addmod(reduce64(acc[f][2], P), bv, q);
+      o.w = addmod(reduce64(acc[f][3], P), bv, q);
+      const u64 e = static_cast<u64>(ff) * a.OH * a.OW + pos;
+      u32* yp = a.Y + ((e * a.polys + poly) * a.level + limb) * a.N + n;
+      *reinterpret_cast<uint4*>(yp) = o;
+    }
+  }
+}
+
+// ===========================================================================
+// Relinearization (henet/ckks.hpp:442-499), three kernels:
+//   K1 k_relin_digits  (ct, j):       c2_j -> INTT_j -> digit j (coefficient domain)
+//   K2 k_relin_keysw   (ct, t<=level): sum_j NTT_t(digit_j mod q_t) * key[j][.][t];
+//                                      t == level is the special prime P, whose
+//                                      accumulators are INTT'd into the rounding
+//                                      corrections of the mod-down.
+//   K3 k_relin_moddown (ct, poly):    d + (acc - NTT(corr)) * P^-1 [+ rescale, with
+//                                      both corrections merged into one NTT per limb]
+// ===========================================================================
+template <int LOGN>
+__device__ __forceinline__ void load_c2(u32 (&y)[32], const RelinArgs& a, u64 ct, u32 j, const DevPrime& P,
+                                        u32 tid) {
+  using NT = Ntt<LOGN>;
+  constexpr int N = NT::N;
+  const u32 L = a.level;
+  if (a.mode == 0) {
+    NT::gload_C(y, a.A + ((ct * 3 + 2) * L + j) * N, tid);
+  } else {
+    u32 b1[32];
+    NT::gload_C(y, a.A + ((ct * 2 + 1) * L + j) * N, tid);
+    NT::gload_C(b1, a.Bm + ((ct * 2 + 1) * L + j) * N, tid);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) y[k] = mulmod(y[k], b1[k], P);
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5)) k_relin_digits(RelinArgs a, Basis B) {
+  using NT = Ntt<LOGN>;
+  constexpr int N = NT::N;
+  extern __shared__ u32 sm[];
+  const u32 tid = threadIdx.x;
+  const u64 ct = blockIdx.x / a.level;
+  const u32 j = blockIdx.x % a.level;
+  const DevPrime& P = B.p[j];
+  u32 y[32];
+  load_c2<LOGN>(y, a, ct, j, P, tid);
+  NT::inverse(y, sm, tid, P);
+  NT::gstore_A(y, a.D + (ct * a.level + j) * N, tid);
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5)) k_relin_keysw(RelinArgs a, Basis B) {
+  using NT = Ntt<LOGN>;
+  constexpr int N = NT::N;
+  extern __shared__ u32 sm[];
+  const u32 tid = threadIdx.x;
+  const u32 L = a.level;
+  const u64 ct = blockIdx.x / (L + 1);
+  const u32 t = blockIdx.x % (L + 1);
+  const bool special = (t == L);
+  const u32 bidx = special ? a.chain_len : t;  // basis index == key limb index
+  const DevPrime& P = B.p[bidx];
+  const u32 q = P.q;
+  u32 acc0[32], acc1[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) acc0[k] = acc1[k] = 0;
+
+  for (u32 j = 0; j < L; ++j) {
+    u32 y[32];
+    if (!special && j == t) {
+      // NTT_t(INTT_t(c2_t)) == c2_t: the digit's own limb needs no transform.
+      load_c2<LOGN>(y, a, ct, j, P, tid);
+    } else {
+      NT::gload_A(y, a.D + (ct * L + j) * N, tid);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) y[k] = reduce32(y[k], P);  // digit mod q_t, henet/ckks.hpp:463
+      NT::forward(y, sm, tid, P);
+    }
+    const uint2* k0 = a.key + ((static_cast<u64>(j) * 2 + 0) * (a.chain_len + 1) + bidx) * N;
+    const uint2* k1 = a.key + ((static_cast<u64>(j) * 2 + 1) * (a.chain_len + 1) + bidx) * N;
+#pragma unroll
+    for (int k = 0; k < 32; k += 2) {
+      const u32 jj = NT::jC(tid, k);
+      const uint4 kv0 = __ldg(reinterpret_cast<const uint4*>(k0 + jj));
+      const uint4 kv1 = __ldg(reinterpret_cast<const uint4*>(k1 + jj));
+      acc0[k] = addmod(acc0[k], mul_shoup(y[k], kv0.x, kv0.y, q), q);
+      acc0[k + 1] = addmod(acc0[k + 1], mul_shoup(y[k + 1], kv0.z, kv0.w, q), q);
+      acc1[k] = addmod(acc1[k], mul_shoup(y[k], kv1.x, kv1.y, q), q);
+      acc1[k + 1] = addmod(acc1[k + 1], mul_shoup(y[k + 1], kv1.z, kv1.w, q), q);
+    }
+  }
+  if (!special) {
+    NT::gstore_C(acc0, a.ACC + ((ct * 2 + 0) * L + t) * N, tid);
+    NT::gstore_C(acc1, a.ACC + ((ct * 2 + 1) * L + t) * N, tid);
+  } else {
+    NT::inverse(acc0, sm, tid, P);
+    i32* c0 = a.CORR + (ct * 2 + 0) * N;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) c0[NT::jA(tid, k)] = centered_round_rem(acc0[k], P);
+    NT::inverse(acc1, sm, tid, P);
+    i32* c1 = a.CORR + (ct * 2 + 1) * N;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) c1[NT::jA(tid, k)] = centered_round_rem(acc1[k], P);
+  }
+}
+
+// d0 = c0 (mode 0) or a0*b0; d1 = c1 (mode 0) or a0*b1 + a1*b0 (henet/ckks.hpp:407-437)
+template <int LOGN>
+__device__ __forceinline__ void load_d(u32 (&d)[32], const RelinArgs& a, u64 ct, u32 poly, u32 i,
+                                       const DevPrime& P, u32 tid) {
+  using NT = Ntt<LOGN>;
+  constexpr int N = NT::N;
+  const u32 L = a.level;
+  if (a.mode == 0) {
+    NT::gload_C(d, a.A + ((ct * 3 + poly) * L + i) * N, tid);
+    return;
+  }
+  u32 x[32], y[32];
+  NT::gload_C(x, a.A + ((ct * 2 + 0) * L + i) * N, tid);
+  NT::gload_C(y, a.Bm + ((ct * 2 + poly) * L + i) * N, tid);
+#pragma unroll
+  for (int k = 0; k < 32; ++k) d[k] = mulmod(x[k], y[k], P);
+  if (poly == 1) {
+    NT::gload_C(x, a.A + ((ct * 2 + 1) * L + i) * N, tid);
+    NT::gload_C(y, a.Bm + ((ct * 2 + 0) * L + i) * N, tid);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) d[k] = addmod(d[k], mulmod(x[k], y[k], P), P.q);
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5)) k_relin_moddown(RelinArgs a, Basis B) {
+  using NT = Ntt<LOGN>;
+  constexpr int N = NT::N;
+  extern __shared__ u32 sm[];
+  const u32 tid = threadIdx.x;
+  const u32 L = a.level;
+  const u64 ct = blockIdx.x >> 1;
+  const u32 poly = blockIdx.x & 1;
+  const u32 Lout = a.rescale ? L - 1 : L;
+  u32* dst = a.out + (ct * 2 + poly) * static_cast<u64>(Lout) * N;
+
+  i32 cp[32];
+  {
+    const i32* cs = a.CORR + (ct * 2 + poly) * N;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) cp[k] = cs[NT::jA(tid, k)];
+  }
+  i32 crs[32];
+  u32 z[32], d[32], v[32];
+  // top limb first: needed by the rescale correction
+  {
+    const u32 i = L - 1;
+    const DevPrime& Pi = B.p[i];
+    const u32 q = Pi.q;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) z[k] = signed_residue(cp[k], Pi);
+    NT::forward(z, sm, tid, Pi);
+    load_d<LOGN>(d, a, ct, poly, i, Pi, tid);
+    NT::gload_C(v, a.ACC + ((ct * 2 + poly) * L + i) * N, tid);
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      z[k] = addmod(d[k], mul_shoup(v[k] + q - z[k], a.pinvP[i], a.pinvP_sh[i], q), q);
+    if (!a.rescale) {
+      NT::gstore_C(z, dst + static_cast<u64>(i) * N, tid);
+    } else {
+      NT::inverse(z, sm, tid, Pi);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) crs[k] = centered_round_rem(z[k], Pi);
+    }
+  }
+  for (u32 i = 0; i + 1 < L; ++i) {
+    const DevPrime& Pi = B.p[i];
+    const u32 q = Pi.q;
+    if (a.rescale) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        z[k] = addmod(mul_shoup(signed_residue(cp[k], Pi), a.pinvP[i], a.pinvP_sh[i], q),
+                      signed_residue(crs[k], Pi), q);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) z[k] = signed_residue(cp[k], Pi);
+    }
+    NT::forward(z, sm, tid, Pi);
+    load_d<LOGN>(d, a, ct, poly, i, Pi, tid);
+    NT::gload_C(v, a.ACC + ((ct * 2 + poly) * L + i) * N, tid);
+    if (a.rescale) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const u32 u = addmod(d[k], mul_shoup(v[k], a.pinvP[i], a.pinvP_sh[i], q), q);
+        z[k] = mul_shoup(u + q - z[k], a.pinvL[i], a.pinvL_sh[i], q);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        z[k] = addmod(d[k], mul_shoup(v[k] + q - z[k], a.pinvP[i], a.pinvP_sh[i], q), q);
+    }
+    NT::gstore_C(z, dst + static_cast<u64>(i) * N, tid);
+  }
+}
+
+// ===========================================================================
+// Element-wise kernels.  One thread per 4 coefficients of one limb row.
+// ===========================================================================
+__global__ void k_ew(EwArgs a, Basis B) {
+  const u32 N = a.N;
+  const u64 rows = a.count * a.polys_out * a.level;
+  const u64 tiles_per_row = N / 4;
+  const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= rows * tiles_per_row) return;
+  const u64 row = idx / tiles_per_row;
+  const u32 n = static_cast<u32>(idx % tiles_per_row) * 4;
+  const u32 limb = row % a.level;
+  const u32 poly = (row / a.level) % a.polys_out;
+  const u64 e = row / (static_cast<u64>(a.level) * a.polys_out);
+  const DevPrime& P = B.p[limb];
+  const u32 q = P.q;
+  auto ld = [&](const u32* base, u32 polys, u32 p) {
+    return *reinterpret_cast<const uint4*>(base + ((e * polys + p) * a.level + limb) * N + n);
+  };
+  uint4 o;
+  switch (a.op) {
+    case EwOp::AddCC: {
+      const uint4 x = ld(a.a, a.polys_a, poly), y = ld(a.b, a.polys_a, poly);
+      o = make_uint4(addmod(x.x, y.x, q), addmod(x.y, y.y, q), addmod(x.z, y.z, q), addmod(x.w, y.w, q));
+      break;
+    }
+    case EwOp::MulScalar: {
+      const uint4 x = ld(a.a, a.polys_a, poly);
+      const u32 r = a.res[(a.per_element ? e / a.pt_div : 0) * a.level + limb];
+      o = make_uint4(mulmod(x.x, r, P), mulmod(x.y, r, P), mulmod(x.z, r, P), mulmod(x.w, r, P));
+      break;
+    }
+    case EwOp::AddScalar: {
+      o = ld(a.a, a.polys_a, poly);
+      if (poly == 0) {
+        const u32 r = a.res[(a.per_element ? e / a.pt_div : 0) * a.level + limb];
+        o = make_uint4(addmod(o.x, r, q), addmod(o.y, r, q), addmod(o.z, r, q), addmod(o.w, r, q));
+      }
+      break;
+    }
+    case EwOp::AddVector: {
+      o = ld(a.a, a.polys_a, poly);
+      if (poly == 0) {
+        const uint4 y = *reinterpret_cast<const uint4*>(
+            a.b + ((a.per_element ? e / a.pt_div : 0) * a.level + limb) * static_cast<u64>(N) + n);
+        o = make_uint4(addmod(o.x, y.x, q), addmod(o.y, y.y, q), addmod(o.z, y.z, q), addmod(o.w, y.w, q));
+      }
+      break;
+    }
+    case EwOp::Tensor: {
+      // out0 = a0 b0, out1 = a0 b1 + a1 b0, out2 = a1 b1
+      uint4 x, y;
+      if (poly == 0) { x = ld(a.a, 2, 0); y = ld(a.b, 2, 0); }
+      else if (poly == 2) { x = ld(a.a, 2, 1); y = ld(a.b, 2, 1); }
+      else { x = ld(a.a, 2, 0); y = ld(a.b, 2, 1); }
+      o = make_uint4(mulmod(x.x, y.x, P), mulmod(x.y, y.y, P), mulmod(x.z, y.z, P), mulmod(x.w, y.w, P));
+      if (poly == 1) {
+        x = ld(a.a, 2, 1); y = ld(a.b, 2, 0);
+        o.x = addmod(o.x, mulmod(x.x, y.x, P), q);
+        o.y = addmod(o.y, mulmod(x.y, y.y, P), q);
+        o.z = addmod(o.z, mulmod(x.z, y.z, P), q);
+        o.w = addmod(o.w, mulmod(x.w, y.w, P), q);
+      }
+      break;
+    }
+    case EwOp::Copy:
+    default:
+      o = ld(a.a, a.polys_a, poly);
+      break;
+  }
+  *reinterpret_cast<uint4*>(a.out + ((e * a.polys_out + poly) * a.level + limb) * N + n) = o;
+}
+
+// ===========================================================================
+// Host <-> device word conversion
+// ===========================================================================
+__global__ void k_narrow(const u64* in, u32* out, u64 words, u32 level, u32 N, Basis B, int* bad) {
+  const u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  const u32 limb = (i / N) % level;
+  const u64 w = in[i];
+  if (w >= B.p[limb].q) atomicExch(bad, 1);
+  out[i] = static_cast<u32>(w);
+}
+
+__global__ void k_widen(const u32* in, u64* out, u64 words) {
+  const u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < words) out[i] = in[i];
+}
+
+// ===========================================================================
+// Encoding.  x87 emulation: the reference computes
+//   roundl((long double)value * (long double)scale)          (henet/encoding.hpp:122-126, 184)
+// in 80-bit extended precision (64-bit mantissa, round-to-nearest-even),
+// then rounds half away from zero.  The exact 106-bit product of the two
+// double mantissas is rounded to 64 bits here the same way.
+// ===========================================================================
+struct X87 {
+  bool neg;
+  unsigned long long mant;  // 64-bit normalized mantissa (0 for zero)
+  int exp;                  // value = mant * 2^exp
+};
+
+__device__ __forceinline__ void split_double(double v, unsigned long long& m, int& e) {
+  const unsigned long long bits = __double_as_longlong(v) & 0x7fffffffffffffffull;
+  const int be = static_cast<int>(bits >> 52);
+  const unsigned long long frac = bits & ((1ull << 52) - 1);
+  if (be == 0) { m = frac; e = -1074; }
+  else { m = frac | (1ull << 52); e = be - 1075; }
+}
+
+__device__ __forceinline__ X87 x87_mul(double a, double b) {
+  X87 r;
+  r.neg = (__double_as_longlong(a) ^ __double_as_longlong(b)) < 0;
+  unsigned long long ma, mb;
+  int ea, eb;
+  split_double(a, ma, ea);
+  split_double(b, mb, eb);
+  if (ma == 0 || mb == 0) { r.mant = 0; r.exp = 0; r.neg = false; return r; }
+  unsigned __int128 p = static_cast<unsigned __int128>(ma) * mb;
+  int e = ea + eb;
+  const unsigned long long hi = static_cast<unsigned long long>(p >> 64);
+  const int nb = hi ? 128 - __clzll(hi) : 64 - __clzll(static_cast<unsigned long long>(p));
+  if (nb > 64) {
+    const int sh = nb - 64;
+    unsigned __int128 m = p >> sh;
+    const unsigned __int128 rem = p & ((static_cast<unsigned __int128>(1) << sh) - 1);
+    const unsigned __int128 halfv = static_cast<unsigned __int128>(1) << (sh - 1);
+    if (rem > halfv || (rem == halfv && (m & 1))) m += 1;
+    e += sh;
+    if (m >> 64) { m >>= 1; e += 1; }
+    r.mant = static_cast<unsigned long long>(m);
+  } else {
+    const int sh = 64 - nb;  // normalize
+    r.mant = static_cast<unsigned long long>(p) << sh;
+    e -= sh;
+  }
+  r.exp = e;
+  return r;
+}
+
+// roundl (half away from zero) of |x| as a 128-bit magnitude.
+__device__ __forceinline__ unsigned __int128 x87_roundl_mag(const X87& x) {
+  if (x.mant == 0) return 0;
+  if (x.exp >= 0) return static_cast<unsigned __int128>(x.mant) << x.exp;
+  const int s = -x.exp;
+  if (s > 65) return 0;
+  const unsigned __int128 m = x.mant;
+  return (m + (static_cast<unsigned __int128>(1) << (s - 1))) >> s;
+}
+
+__device__ __forceinline__ u32 residue_mag(unsigned __int128 mag, bool neg, const DevPrime& P) {
+  const u64 q = P.q;
+  const u64 hi = static_cast<u64>(mag >> 64), lo = static_cast<u64>(mag);
+  // 2^64 mod q
+  const u64 t64 = (0xffffffffffffffffull % q + 1) % q;
+  u64 r = ((hi % q) * t64 + lo % q) % q;
+  if (neg && r != 0) r = q - r;
+  return static_cast<u32>(r);
+}
+
+template <typename T>
+__global__ void k_encode_scalars(const T* vals, u64 count, u32 row_len, u32 row_stride, u64 limb_stride,
+                                 u32 level, double scale, u32* out, Basis B) {
+  const u64 v = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= count) return;
+  const X87 x = x87_mul(static_cast<double>(vals[v]), scale);
+  const unsigned __int128 mag = x87_roundl_mag(x);
+  const u64 dst = (v / row_len) * row_stride + v % row_len;
+  for (u32 i = 0; i < level; ++i) out[i * limb_stride + dst] = residue_mag(mag, x.neg, B.p[i]);
+}
+
+// Exact complex arithmetic in the order GCC emits for std::complex<double>
+// without FMA: (a+bi)(c+di) = (ac - bd) + (ad + bc)i, every op rounded.
+__device__ __forceinline__ double2 cmul_exact(double2 x, double2 w) {
+  return make_double2(__dsub_rn(__dmul_rn(x.x, w.x), __dmul_rn(x.y, w.y)),
+                      __dadd_rn(__dmul_rn(x.x, w.y), __dmul_rn(x.y, w.x)));
+}
+
+__device__ __forceinline__ u32 bitrev_n(u32 i, u32 logn) { return __brev(i) >> (32 - logn); }
+
+// One CTA per plaintext; the FFT works on a global scratch row (L2 resident).
+__global__ void __launch_bounds__(512) k_fft_encode(const double* slots, u32 n_slots, u32 n, u32 logn, u32 level,
+                                                    double scale, const double2* roots, const double2* twist,
+                                                    double2* scratch, u32* out, unsigned long long* max_mant,
+                                                    int* max_exp, Basis B) {
+  const u64 pt = blockIdx.x;
+  const u32 tid = threadIdx.x;
+  double2* a = scratch + pt * n;
+  const double* s = slots + pt * 2 * static_cast<u64>(n_slots);
+  // conjugate extension (henet/fft.hpp:59-63), then the bit-reversal permutation (:89-92)
+  for (u32 i = tid; i < n; i += blockDim.x) {
+    const u32 j = bitrev_n(i, logn);
+    double2 e = make_double2(0.0, 0.0);
+    if (j < n_slots) e = make_double2(s[2 * j], s[2 * j + 1]);
+    else if (n - 1 - j < n_slots) { const u32 jj = n - 1 - j; e = make_double2(s[2 * jj], -s[2 * jj + 1]); }
+    __stcg(&a[i], e);
+  }
+  __syncthreads();
+  // radix-2 DIT stages (henet/fft.hpp:93-104)
+  for (u32 len = 2; len <= n; len <<= 1) {
+    const u32 half = len >> 1, step = n / len;
+    for (u32 idx = tid; idx < n / 2; idx += blockDim.x) {
+      const u32 base = (idx / half) * len, k = idx % half;
+      const double2 w = roots[k * step];
+      const double2 u = __ldcg(&a[base + k]);
+      const double2 v = cmul_exact(__ldcg(&a[base + k + half]), w);
+      __stcg(&a[base + k], make_double2(__dadd_rn(u.x, v.x), __dadd_rn(u.y, v.y)));
+      __stcg(&a[base + k + half], make_double2(__dsub_rn(u.x, v.x), __dsub_rn(u.y, v.y)));
+    }
+    __syncthreads();
+  }
+  // untwist, real part, 1/N (henet/fft.hpp:66-72), then x87 scale+round and residues
+  // (henet/encoding.hpp:153-168)
+  const double inv_n = 1.0 / static_cast<double>(n);
+  __shared__ unsigned long long s_mant[512];
+  __shared__ int s_exp[512];
+  unsigned long long bm = 0;
+  int be = -100000;
+  for (u32 k = tid; k < n; k += blockDim.x) {
+    const double2 e = __ldcg(&a[k]);
+    const double2 tw = twist[k];
+    const double re = __dsub_rn(__dmul_rn(e.x, tw.x), __dmul_rn(e.y, -tw.y));
+    const double coeff = __dmul_rn(re, inv_n);
+    const X87 x = x87_mul(coeff, scale);
+    if (x.mant != 0 && (x.exp > be || (x.exp == be && x.mant > bm))) { bm = x.mant; be = x.exp; }
+    const unsigned __int128 mag = x87_roundl_mag(x);
+    for (u32 i = 0; i < level; ++i) out[(pt * level + i) * n + k] = residue_mag(mag, x.neg, B.p[i]);
+  }
+  s_mant[tid] = bm;
+  s_exp[tid] = be;
+  __syncthreads();
+  if (tid == 0) {
+    for (u32 t = 1; t < blockDim.x; ++t) {
+      if (s_mant[t] != 0 && (s_exp[t] > be || (s_exp[t] == be && s_mant[t] > bm))) { bm = s_mant[t]; be = s_exp[t]; }
+    }
+    max_mant[pt] = bm;
+    max_exp[pt] = be;
+  }
+}
+
+// ===========================================================================
+// IMAD.WIDE throughput probe (register only)
+// ===========================================================================
+__global__ void k_imad_probe(u64* sink, u32 iters, u32 seed) {
+  u32 a0 = threadIdx.x ^ seed, a1 = a0 * 3 + 1, a2 = a0 * 5 + 7, a3 = a0 * 11 + 3;
+  u32 a4 = a0 + 13, a5 = a0 + 17, a6 = a0 + 19, a7 = a0 + 23;
+  u64 c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0, c6 = 0, c7 = 0;
+  u32 b = seed | 1;
+#define HG_MADW(c, x) asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(c) : "r"(x), "r"(b))
+  for (u32 i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      HG_MADW(c0, a0); HG_MADW(c1, a1); HG_MADW(c2, a2); HG_MADW(c3, a3);
+      HG_MADW(c4, a4); HG_MADW(c5, a5); HG_MADW(c6, a6); HG_MADW(c7, a7);
+    }
+    b += 2;
+  }
+#undef HG_MADW
+  const u64 s = c0 ^ c1 ^ c2 ^ c3 ^ c4 ^ c5 ^ c6 ^ c7;
+  if (s == 0x12345) sink[0] = s;
+}
+
+// ===========================================================================
+// Launchers
+// ===========================================================================
+#define HG_LOGN_SWITCH(logn, ...)                   \
+  switch (logn) {                                    \
+    case 12: { constexpr int LN = 12; __VA_ARGS__; } break; \
+    case 13: { constexpr int LN = 13; __VA_ARGS__; } break; \
+    case 14: { constexpr int LN = 14; __VA_ARGS__; } break; \
+    default: return -1;                              \
+  }
+
+template <typename K>
+static void set_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+}
+
+int launch_ntt(int logn, u32* data, u64 rows, u32 level, bool inverse, const Basis& B, cudaStream_t s) {
+  if (rows == 0) return 0;
+  HG_LOGN_SWITCH(logn, {
+    const size_t sm = sizeof(u32) << LN;
+    if (inverse) {
+      set_smem(k_ntt<LN, true>, sm);
+      k_ntt<LN, true><<<rows, 1 << (LN - 5), sm, s>>>(data, level, B);
+    } else {
+      set_smem(k_ntt<LN, false>, sm);
+      k_ntt<LN, false><<<rows, 1 << (LN - 5), sm, s>>>(data, level, B);
+    }
+  });
+  return 1;
+}
+
+int launch_rescale(int logn, const RescaleArgs& a, const Basis& B, cudaStream_t s) {
+  if (a.rows == 0) return 0;
+  HG_LOGN_SWITCH(logn, {
+    const size_t sm = sizeof(u32) << LN;
+    set_smem(k_rescale<LN>, sm);
+    k_rescale<LN><<<a.rows, 1 << (LN - 5), sm, s>>>(a, B);
+  });
+  return 1;
+}
+
+int launch_mac_dense(const MacDenseArgs& a, const Basis& B, cudaStream_t s) {
+  const u32 warps = std::min<u32>(8, (a.M + kTM - 1) / kTM);
+  const u32 BM = warps * kTM;
+  dim3 grid(a.N / kBN, (a.M + BM - 1) / BM, a.polys * a.level);
+  k_mac_dense<<<grid, warps * 32, 0, s>>>(a, B);
+  return 1;
+}
+
+int launch_mac_conv(const MacConvArgs& a, const Basis& B, cudaStream_t s) {
+  if (a.C * a.win * a.win > static_cast<u32>(kMaxTaps)) return -1;
+  dim3 grid(a.N / (4 * 128), a.OH * a.OW, a.polys * a.level);
+  k_mac_conv<<<grid, 128, 0, s>>>(a, B);
+  return 1;
+}
+
+int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s) {
+  if (a.count == 0) return 0;
+  HG_LOGN_SWITCH(logn, {
+    const size_t sm = sizeof(u32) << LN;
+    const int T = 1 << (LN - 5);
+    set_smem(k_relin_digits<LN>, sm);
+    set_smem(k_relin_keysw<LN>, sm);
+    set_smem(k_relin_moddown<LN>, sm);
+    k_relin_digits<LN><<<a.count * a.level, T, sm, s>>>(a, B);
+    k_relin_keysw<LN><<<a.count * (a.level + 1), T, sm, s>>>(a, B);
+    k_relin_moddown<LN><<<a.count * 2, T, sm, s>>>(a, B);
+  });
+  return 3;
+}
+
+int launch_elementwise(const EwArgs& a, const Basis& B, cudaStream_t s) {
+  const u64 threads = a.count * a.polys_out * a.level * (a.N / 4);
+  if (threads == 0) return 0;
+  k_ew<<<(threads + 255) / 256, 256, 0, s>>>(a, B);
+  return 1;
+}
+
+int launch_narrow(const u64* in, u32* out, u64 words, u32 level, u32 N, const Basis& B, int* d_bad,
+                  cudaStream_t s) {
+  if (words == 0) return 0;
+  k_narrow<<<(words + 255) / 256, 256, 0, s>>>(in, out, words, level, N, B, d_bad);
+  return 1;
+}
+
+int launch_widen(const u32* in, u64* out, u64 words, cudaStream_t s) {
+  if (words == 0) return 0;
+  k_widen<<<(words + 255) / 256, 256, 0, s>>>(in, out, words);
+  return 1;
+}
+
+int launch_encode_scalars_f32(const float* vals, u64 count, u32 row_len, u32 row_stride, u64 limb_stride,
+                              u32 level, double scale, u32* out, const Basis& B, cudaStream_t s) {
+  if (count == 0) return 0;
+  k_encode_scalars<float><<<(count + 127) / 128, 128, 0, s>>>(vals, count, row_len, row_stride, limb_stride,
+                                                              level, scale, out, B);
+  return 1;
+}
+
+int launch_encode_scalars_f64(const double* vals, u64 count, u32 row_len, u32 row_stride, u64 limb_stride,
+                              u32 level, double scale, u32* out, const Basis& B, cudaStream_t s) {
+  if (count == 0) return 0;
+  k_encode_scalars<double><<<(count + 127) / 128, 128, 0, s>>>(vals, count, row_len, row_stride, limb_stride,
+                                                               level, scale, out, B);
+  return 1;
+}
+
+int launch_fft_encode(const double* slots, u32 n_slots, u64 count, u32 n, u32 level, double scale,
+                      const double2* roots, const double2* twist, double2* scratch, u32* out,
+                      unsigned long long* max_mant, int* max_exp, const Basis& B, cudaStream_t s) {
+  if (count == 0) return 0;
+  u32 logn = 0;
+  while ((1u << logn) < n) ++logn;
+  k_fft_encode<<<count, 512, 0, s>>>(slots, n_slots, n, logn, level, scale, roots, twist, scratch, out, max_mant,
+                                      max_exp, B);
+  return 1;
+}
+
+double bench_imad_wide(int device) {
+  cudaSetDevice(device);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  u64* sink = nullptr;
+  cudaMalloc(&sink, 8);
+  const u32 iters = 4096;
+  const int blocks = sms * 8, threads = 256;
+  k_imad_probe<<<blocks, threads>>>(sink, 16, 3);  // warm-up
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  k_imad_probe<<<blocks, threads>>>(sink, iters, 5);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  const double ops = static_cast<double>(blocks) * threads * iters * 16 * 8;
+  return ops / (ms * 1e-3);
+}
+
+}  // namespace hg

@@ -1,0 +1,108 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Host-callable launchers for the sm_100a kernels in hg_kernels.cu.  Every
+// launcher enqueues on `stream` and returns the number of kernel launches it
+// issued (for the launch accounting reported by bench.py).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hg_device.cuh"
+
+namespace hg {
+
+struct RescaleArgs {
+  const u32* in;
+  u32* out;
+  u64 rows;  // ciphertexts * polys
+  u32 level;  // input level (output level - 1 ... target)
+  u32 pinv[kMaxPrimes];     // q_{level-1}^-1 mod q_i
+  u32 pinv_sh[kMaxPrimes];
+};
+
+struct MacDenseArgs {
+  const u32* X;     // [K][x_polys][x_level][N]
+  u32* Y;           // [M][polys][level][N]
+  const u32* W;     // [level][K][Mpad] weight residues
+  const u32* bias;  // [level][Mpad] residues added to poly 0, or nullptr
+  u32 K, M, Mpad, N;
+  u32 level, polys;
+  u32 x_level;      // limbs per polynomial in X (>= level)
+  u32 fold[kMaxPrimes];  // 1 if limb i needs accumulator folding (products >= 2^48)
+};
+
+struct MacConvArgs {
+  const u32* X;     // [C*IH*IW][polys][x_level][N]
+  u32* Y;           // [F*OH*OW][polys][level][N]
+  const u32* W;     // [level][F][C*win*win]
+  const u32* bias;  // [level][F] or nullptr
+  u32 C, IH, IW, F, OH, OW, win, stride, pad_top, pad_left;
+  u32 level, polys, x_level, N;
+  u32 fold[kMaxPrimes];
+};
+
+struct RelinArgs {
+  const u32* A;   // mode 0: size-3 ciphertexts; mode 1: left operand (size 2)
+  const u32* Bm;  // mode 1: right operand (size 2); may equal A (square)
+  int mode;       // 0 = relinearize(ct3), 1 = relinearize(tensor(A, B))
+  u64 count;
+  u32 level;
+  u32 chain_len;
+  u32* D;         // digits   [count][level][N]
+  u32* ACC;       // key-switch accumulators [count][2][level][N]
+  i32* CORR;      // special-prime corrections [count][2][N]
+  const uint2* key;  // [chain][2][chain+1][N] (value, shoup)
+  u32* out;       // [count][2][level or level-1][N]
+  int rescale;
+  u32 pinvP[kMaxPrimes], pinvP_sh[kMaxPrimes];  // P^-1 mod q_i
+  u32 pinvL[kMaxPrimes], pinvL_sh[kMaxPrimes];  // q_{level-1}^-1 mod q_i
+};
+
+enum class EwOp : int { AddCC = 0, MulScalar = 1, AddScalar = 2, AddVector = 3, Tensor = 4, Copy = 5 };
+
+struct EwArgs {
+  EwOp op;
+  const u32* a;
+  const u32* b;      // AddCC / Tensor: second ciphertext; AddVector: plaintexts [.][level][N]
+  const u32* res;    // MulScalar / AddScalar: residues [.][level]
+  int per_element;   // plaintext / residue indexed by element / pt_div (else broadcast)
+  u32 pt_div;
+  u32* out;
+  u64 count;
+  u32 polys_a, polys_out, level, N;
+};
+
+int launch_ntt(int logn, u32* data, u64 rows, u32 level, bool inverse, const Basis& B,
+               cudaStream_t s);
+int launch_rescale(int logn, const RescaleArgs& a, const Basis& B, cudaStream_t s);
+int launch_mac_dense(const MacDenseArgs& a, const Basis& B, cudaStream_t s);
+int launch_mac_conv(const MacConvArgs& a, const Basis& B, cudaStream_t s);
+int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s);
+int launch_elementwise(const EwArgs& a, const Basis& B, cudaStream_t s);
+
+// u64 host words -> u32 device residues with the < q check; bad != 0 on violation.
+int launch_narrow(const u64* in, u32* out, u64 words, u32 level, u32 N, const Basis& B,
+                  int* d_bad, cudaStream_t s);
+int launch_widen(const u32* in, u64* out, u64 words, cudaStream_t s);
+
+// encode_scalar for `count` values.  out[limb * limb_stride + dst(v)] with
+// dst(v) = (v / row_len) * row_stride + v % row_len.
+int launch_encode_scalars_f32(const float* vals, u64 count, u32 row_len, u32 row_stride,
+                              u64 limb_stride, u32 level, double scale, u32* out, const Basis& B,
+                              cudaStream_t s);
+int launch_encode_scalars_f64(const double* vals, u64 count, u32 row_len, u32 row_stride,
+                              u64 limb_stride, u32 level, double scale, u32* out, const Basis& B,
+                              cudaStream_t s);
+
+// encode_vector front half: conj-extend, radix-2 DIT FFT in the reference's
+// operation order, untwist, x87 scale/round, residues (coefficient domain).
+// maxmag[pt] = (mantissa, exponent) of the largest |scaled| (long double).
+int launch_fft_encode(const double* slots, u32 n_slots, u64 count, u32 n, u32 level, double scale,
+                      const double2* roots, const double2* twist, double2* scratch, u32* out,
+                      unsigned long long* max_mant, int* max_exp, const Basis& B, cudaStream_t s);
+
+double bench_imad_wide(int device);
+
+}  // namespace hg

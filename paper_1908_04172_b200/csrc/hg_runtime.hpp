@@ -1,0 +1,156 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Host runtime objects behind the C ABI: the device context (CkksContext
+// mirror), device ciphertext batches (CipherTensor mirror), the relin key,
+// the plain model (PlainModel mirror) and the rescale plan.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/henet_b200.h"
+#include "hg_kernels.hpp"
+
+namespace hg {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+inline void require(bool cond, const std::string& what) {
+  if (!cond) throw Error(HG_ERR_VALIDATION, what);
+}
+void cuda_check(cudaError_t e, const char* what);
+
+// Shared device state: the stream and device; kept alive by every buffer.
+struct DeviceCore {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::atomic<uint64_t> launches{0};
+  ~DeviceCore();
+};
+
+struct DeviceBuffer {
+  std::shared_ptr<DeviceCore> core;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaStream_t stream = nullptr;  // allocation stream; the free is ordered on it
+  DeviceBuffer(std::shared_ptr<DeviceCore> c, size_t b, cudaStream_t s);
+  ~DeviceBuffer();
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+};
+using BufPtr = std::shared_ptr<DeviceBuffer>;
+
+struct Context {
+  std::shared_ptr<DeviceCore> core;
+  u32 n = 0, logn = 0;
+  std::vector<u64> chain;
+  u64 special = 0;
+  bool has_special = false;
+  double default_scale = 0;
+  std::vector<u64> roots;                    // psi per basis index
+  std::vector<long double> modulus_products;  // q_l, henet/params.hpp:236-242
+  Basis basis{};
+  BufPtr tables;      // twiddles for all basis moduli
+  BufPtr fft_tables;  // dft roots (N/2) + twist (N), double2
+  std::vector<double> host_roots, host_twist;  // interleaved re/im
+
+  size_t chain_len() const { return chain.size(); }
+  u64 basis_mod(size_t i) const { return i < chain.size() ? chain[i] : special; }
+  cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : core->stream; }
+  void count(int launches) const { core->launches += static_cast<uint64_t>(launches > 0 ? launches : 0); }
+  BufPtr alloc(size_t bytes, cudaStream_t s) const { return std::make_shared<DeviceBuffer>(core, bytes, s); }
+};
+
+// A batch of ciphertexts with one scale (Ciphertext::scale is identical
+// across the elements of every tensor the executor produces).
+struct CtBatch {
+  BufPtr buf;
+  u64 count = 0;
+  u32 polys = 2, level = 0;
+  double scale = 0;
+  int packing = HG_PACKING_REAL;
+  std::vector<u32> shape;
+  u64 words(u32 n) const { return count * polys * level * static_cast<u64>(n); }
+  u32* data() const { return buf ? static_cast<u32*>(buf->ptr) : nullptr; }
+};
+
+struct RelinKeyDev {
+  BufPtr key;  // uint2 [chain][2][chain+1][N]
+  u32 chain_len = 0;
+};
+
+struct WeightTensor {
+  std::vector<u32> dims;
+  std::vector<float> data;
+  float max_abs = 0;
+  // device copy (uploaded lazily, per device)
+  BufPtr dev;
+};
+
+struct NodeAttrs {
+  std::vector<u32> shape;
+  u32 stride = 1, window = 0, filters = 0, pool_stride = 0;
+  std::array<u32, 4> pad{0, 0, 0, 0};
+};
+
+struct Node {
+  std::string id;
+  int op = HG_OP_INPUT;
+  NodeAttrs attrs;
+  std::vector<std::string> inputs;
+  std::string weight_ref, bias_ref;
+};
+
+struct Model {
+  int packing = HG_PACKING_REAL;
+  std::vector<Node> nodes;
+  std::map<std::string, WeightTensor> weights;
+  std::map<std::string, std::vector<u32>> shapes;
+  std::map<std::string, size_t> index;
+  bool finalized = false;
+  const Node& node(const std::string& id) const { return nodes[index.at(id)]; }
+};
+
+struct NodePlan {
+  int decision = HG_SKIP;
+  u32 level_in = 0, level_out = 0;
+  double scale_out = 0;
+};
+
+struct Plan {
+  int mode = HG_RESCALE_LAZY;
+  std::map<std::string, NodePlan> nodes;
+  u64 planned_rescale_ops = 0;
+};
+
+}  // namespace hg
+
+// C ABI handle types
+struct hg_ctx {
+  std::shared_ptr<hg::Context> c;
+  std::array<double, 11> last_node_ms{};
+};
+struct hg_tensor {
+  std::shared_ptr<hg::Context> ctx;
+  hg::CtBatch b;
+};
+struct hg_relin_key {
+  std::shared_ptr<hg::Context> ctx;
+  hg::RelinKeyDev k;
+};
+struct hg_model {
+  hg::Model m;
+};
+struct hg_plan {
+  hg::Plan p;
+};
