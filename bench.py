@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+# SPDX-License-Identifier: Apache-2.0
+"""Benchmark of the B200 encrypted-inference hot path (BASELINE.json metric).
+
+One step = one batch of 4096 encrypted 28x28 images (batch-axis packed, one
+image per slot) through the full CryptoNets-shaped network of BASELINE config 2
+(conv 5x5/2 -> square+relin+rescale -> dense 845->100 -> square -> dense
+100->10, lazy rescaling), N=8192, 7-prime chain, scale 2^24, executed by
+libhenet_b200.so's graph executor (hg_execute).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Multi-GPU (torchrun, one process per GPU): independent 4096-image batches per
+rank (config 5a: batch sharding, no collective), weak scaling; time = max over
+ranks of the device time.
+
+`value` is whole-job images/s with inputs resident in HBM (input tensor 308 MB >
+126 MB L2, so every step streams it from HBM).  `e2e` is the same metric through
+the C ABI with host buffers: per step the reference-format u64 input words are
+uploaded from pinned host memory (hg_tensor_upload), the graph executed, and the
+logits downloaded (hg_tensor_download).  Inputs are seeded uniform residues mod
+q_i: fresh RLWE ciphertexts are uniform, so the work is identical to real
+encryptions (parity on real encryptions is covered by tests/).
+
+--impl reference times the reference's own CPU implementation (the unmodified
+henet headers compiled into oracle/_ref/libhenet_ref.so, execute() with all host
+threads) on the same network, parameters and batch.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "encrypted images/sec, CryptoNets-shaped N=8192 net; % of HBM/INT32 roofline"
+IMAGES_PER_STEP = 4096
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload_config(n_gpus):
+    return {
+        "workload": "c2 CryptoNets-shaped net: conv5x5/2(5)->sq->fc845x100->sq->fc100x10, lazy rescale",
+        "images_per_step_per_gpu": IMAGES_PER_STEP,
+        "ring": "N=8192, chain [30,24x5]+30-bit special, scale 2^24",
+        "input_ciphertexts": 784,
+        "l2": "input tensor 308 MB > 126 MB L2 (no flush needed)",
+        "parallelism": f"batch-sharded replicas x{n_gpus} (config 5a), no collective",
+    }
+
+
+# ---------------------------------------------------------------------------
+# Clock sampling during the timed region
+# ---------------------------------------------------------------------------
+class Clocks:
+    def __init__(self, device):
+        self.f = tempfile.NamedTemporaryFile(prefix="clocks", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# Algorithmic work model: IMAD-class ops (modular MAC = 1,
+# NTT butterfly = 3, modmul = 3) and compulsory HBM bytes (u32 residues).
+# ---------------------------------------------------------------------------
+def work_model(n=8192):
+    import math
+    logn = int(math.log2(n))
+    bf = n // 2 * logn  # butterflies per transform
+    W = 4               # bytes per residue
+    m = {}
+
+    def add(name, ops, byts):
+        o, b = m.get(name, (0.0, 0.0))
+        m[name] = (o + ops, b + byts)
+
+    # conv1: 784 inputs at level 6 -> 845 outputs, 20480 valid taps
+    L = 6
+    add("k_mac_conv", 20480 * 2 * L * n, (784 + 845) * 2 * L * n * W)
+    # rescale after conv1: 845 cts at level 6 -> 5; after fc1: 100 cts 4 -> 3
+    for C_, l in ((845, 6), (100, 4)):
+        add("k_rescale", C_ * (2 * l * bf * 3 + 2 * (l - 1) * n * 3), C_ * (2 * l + 2 * (l - 1)) * n * W)
+    # square+relin+rescale: act1 845 cts at level 5, act2 100 cts at level 3
+    for C_, l in ((845, 5), (100, 3)):
+        add("k_relin_digits", C_ * (l * bf * 3 + l * n * 3), C_ * 2 * l * n * W)
+        key_bytes = 2 * l * (l + 1) * n * 8
+        add("k_relin_keysw", C_ * ((l * l + 2) * bf * 3 + 2 * l * (l + 1) * n * 3),
+            C_ * (l * n * W + 2 * l * n * W + 2 * n * W) + key_bytes)
+        add("k_relin_moddown", C_ * (2 * (l + 1) * bf * 3 + (6 * l - 2) * n * 3),
+            C_ * (2 * l * n * W + 2 * l * n * W + 2 * n * W + 2 * (l - 1) * n * W))
+    # fc1 845 -> 100 at level 4, fc2 100 -> 10 at level 2
+    add("k_mac_dense", 845 * 100 * 2 * 4 * n + 100 * 10 * 2 * 2 * n,
+        (845 + 100) * 2 * 4 * n * W + (100 + 10) * 2 * 2 * n * W)
+    return m
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# Reference arm
+# ---------------------------------------------------------------------------
+def reference_run(args, ws, rank):
+    from oracle import refbind as R
+    from paper_1908_04172_b200 import workloads as Wk
+
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libhenet_ref.so not built"}))
+        return 0
+    p = Wk.N8192
+    wl = Wk.cryptonets()
+    ref = R.RefContext(p["n"], p["chain"], p["special"], p["scale"])
+    keys = ref.keygen(7, True)
+    imgs = Wk.synthetic_images(wl.input_shape, wl.batch, 1)
+    words, sc = ref.encrypt_tensor(keys, imgs, 2, threads=cores)
+    # each step is one full 4096-image batch (~5-15 s on the host cores); cap the
+    # run so --steps K --warmup W finishes within a few minutes.
+    warm = min(args.warmup, 1)
+    steps = max(1, min(args.steps, 5))
+    for _ in range(warm):
+        ref.execute(keys, wl.manifest, wl.blob, words, sc, threads=cores)
+    times = []
+    for _ in range(steps):
+        _, _, st = ref.execute(keys, wl.manifest, wl.blob, words, sc, threads=cores)
+        times.append(st["exec_ms"])
+    ms = sum(times) / len(times)
+    v = IMAGES_PER_STEP / (ms / 1e3)
+    unit = "images/s"
+    line = {
+        "metric": METRIC, "value": v, "unit": unit, "impl": "reference", "n_gpus": args.gpus,
+        "steps": steps, "warmup": warm, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64 (RNS residues)", "data": "synthetic (seeded uniform pixels, real encryptions)",
+        "config": workload_config(1) | {"parallelism": f"reference execute() on {cores} host threads"},
+        "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "reference",
+                         "sample": f"{steps} x full 4096-image batch through henet::execute (oracle/_ref)"},
+        "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_baseline_sample():
+    """The reference CPU path timed on this host (rank 0, N=1): one full batch."""
+    from oracle import refbind as R
+    from paper_1908_04172_b200 import workloads as Wk
+    if not R.available():
+        return None
+    cores = os.cpu_count() or 1
+    p = Wk.N8192
+    wl = Wk.cryptonets()
+    ref = R.RefContext(p["n"], p["chain"], p["special"], p["scale"])
+    keys = ref.keygen(7, True)
+    imgs = Wk.synthetic_images(wl.input_shape, wl.batch, 1)
+    words, sc = ref.encrypt_tensor(keys, imgs, 2, threads=cores)
+    _, _, st = ref.execute(keys, wl.manifest, wl.blob, words, sc, threads=cores)
+    ms = st["exec_ms"]
+    return {"value": IMAGES_PER_STEP / (ms / 1e3), "unit": "images/s", "cores": cores, "kind": "reference",
+            "sample": "one 4096-image batch of the same network through henet::execute (oracle/_ref), "
+                      f"{ms / 1e3:.1f} s"}
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def b200_run(args, ws, rank, local):
+    import torch
+    from paper_1908_04172_b200 import henet as H
+    from paper_1908_04172_b200 import workloads as Wk
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p = Wk.N8192
+    wl = Wk.cryptonets()
+    ctx = H.CkksContext(p["n"], p["chain"], p["special"], p["scale"], device=local)
+    L = len(p["chain"])
+    rng = np.random.default_rng(100 + rank)
+    key_words = np.empty((L, 2, L + 1, p["n"]), dtype=np.uint64)
+    for t, q in enumerate(p["chain"] + [p["special"]]):
+        key_words[:, :, t, :] = rng.integers(0, q, size=(L, 2, p["n"]), dtype=np.uint64)
+    rk = H.RelinKey(ctx, key_words)
+    model = H.PlainModel.load(wl.manifest, wl.blob)
+    plan = H.RescalePlan.plan(ctx, model)
+    words = Wk.random_ciphertexts(p, wl.input_count, seed=7 + rank)
+    inp = H.CipherTensor.from_words(ctx, words, p["scale"], shape=wl.input_shape)
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=local)
+
+    def step():
+        return H.execute(ctx, model, plan, inp, rk)
+
+    clocks = Clocks(local)  # started before warm-up so nvidia-smi start-up is not inside the timed region
+    for _ in range(max(args.warmup, 3)):
+        out = step()
+    ctx.synchronize()
+    time.sleep(0.5)
+    for _ in range(2):
+        out = step()
+    ctx.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    host_t0 = time.perf_counter()
+    l0 = ctx.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        out = step()
+    e1.record(stream)
+    e1.synchronize()
+    launches = (ctx.launch_count() - l0)
+    dev_ms = e0.elapsed_time(e1)
+    host_ms = (time.perf_counter() - host_t0) * 1e3
+    clk = clocks.stop()
+    torch.cuda.synchronize()
+    t = torch.tensor([dev_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    max_ms = float(t.item())
+    ms_per_step = max_ms / args.steps
+    value = IMAGES_PER_STEP * ws / (ms_per_step / 1e3)
+    out_words = out.to_words()
+    assert out_words.shape == (10, 2, 2, p["n"])
+
+    # ---- e2e through the C ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.empty(words.size, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        host_in[:] = words.reshape(-1)
+        host_in = host_in.reshape(words.shape)
+        out_host = torch.empty(10 * 2 * 2 * p["n"], dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        dev_in = H.CipherTensor(ctx, wl.input_count, 2, L, p["scale"], shape=wl.input_shape)
+        from paper_1908_04172_b200._lib import check, lib
+
+        def e2e_step():
+            check(lib.hg_tensor_upload(dev_in.handle, H._ptr(host_in), None))
+            o = H.execute(ctx, model, plan, dev_in, rk)
+            check(lib.hg_tensor_download(o.handle, H._ptr(out_host), None))
+
+        e2e_step()
+        if ws > 1:
+            torch.distributed.barrier()
+        n_e2e = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        f1.record(stream)
+        f1.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+        e_ms = max(f0.elapsed_time(f1), wall) / n_e2e
+        te = torch.tensor([e_ms], dtype=torch.float64, device=f"cuda:{local}")
+        if ws > 1:
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        e_ms = float(te.item())
+        e2e = {"value": IMAGES_PER_STEP * ws / (e_ms / 1e3), "unit": "images/s",
+               "h2d_bytes_per_step": int(words.nbytes), "d2h_bytes_per_step": int(out_host.nbytes),
+               "ms_per_step": e_ms, "steps": n_e2e,
+               "path": "hg_tensor_upload(u64 host words) + hg_execute + hg_tensor_download"}
+
+    # ---- per-kernel roofline pass (CUDA events around every launch) ----
+    H.prof_enable(True)
+    n_prof = 3
+    for _ in range(n_prof):
+        step()
+    ctx.synchronize()
+    H.prof_enable(False)
+    prof = H.prof_report()
+    hbm_gbs, hbm_src = load_peaks()
+    int_peak = H.bench_int_peak(local, 0)
+    int_wide = H.bench_int_peak(local, 1)
+    model_w = work_model(p["n"])
+    kernels = {}
+    total_ms = sum(v["ms"] for v in prof.values()) / n_prof
+    for name, v in prof.items():
+        ms = v["ms"] / n_prof
+        ops, byts = model_w.get(name, (0.0, 0.0))
+        t_int = ops / int_peak * 1e3
+        t_hbm = byts / (hbm_gbs * 1e9) * 1e3
+        kernels[name] = {"ms_per_step": ms, "launches_per_step": v["launches"] / n_prof,
+                         "share": ms / total_ms if total_ms else 0,
+                         "int_tops": ops / (ms * 1e-3) / 1e12 if ms else 0,
+                         "hbm_gbs": byts / (ms * 1e-3) / 1e9 if ms else 0,
+                         "roofline_frac": max(t_int, t_hbm) / ms if ms else 0,
+                         "bound": "int32" if t_int >= t_hbm else "hbm"}
+    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
+    dk = kernels[dom]
+    ops, byts = model_w.get(dom, (0.0, 0.0))
+    if dk["bound"] == "int32":
+        roof = {"bound": "int32", "kernel": dom, "achieved": dk["int_tops"], "peak": int_peak / 1e12,
+                "unit": "Tops/s (IMAD-class)", "frac": dk["int_tops"] / (int_peak / 1e12),
+                "peak_source": "measured register-only IMAD probe (hg_bench_int_peak kind 0) on this GPU",
+                "imad_wide_peak": int_wide / 1e12, "hbm_gbs_achieved": dk["hbm_gbs"], "hbm_peak": hbm_gbs,
+                "traffic": None}
+    else:
+        roof = {"bound": "hbm", "kernel": dom, "achieved": dk["hbm_gbs"], "peak": hbm_gbs, "unit": "GB/s",
+                "frac": dk["hbm_gbs"] / hbm_gbs, "peak_source": hbm_src, "traffic": None}
+    roof["algorithmic_per_step"] = {"imad_ops": ops, "hbm_bytes": byts}
+    whole_t = max(sum(v[0] for v in model_w.values()) / int_peak, 0) * 1e3
+    roof["whole_step"] = {"int32_floor_ms": whole_t, "measured_ms": ms_per_step,
+                          "frac": whole_t / ms_per_step if ms_per_step else 0}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_sample()
+        except Exception as e:  # reported, not fatal
+            cpu = {"error": str(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32 (RNS residues mod 24/30-bit primes)",
+            "data": "synthetic (seeded uniform residues = fresh-ciphertext distribution; random relin key)",
+            "config": workload_config(ws), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps, "clocks": clk,
+            "host_wall_ms_per_step": host_ms / args.steps,
+            "kernels": kernels,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        return reference_run(args, ws, rank)
+    return b200_run(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

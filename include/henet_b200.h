@@ -220,6 +220,9 @@ int hg_model_shape(const hg_model* m, const char* id, uint32_t* dims, uint32_t* 
 
 /* plan_rescaling, henet/graph.hpp:504-584 */
 int hg_plan_rescaling(const hg_ctx* ctx, const hg_model* m, int mode, hg_plan** out);
+/* Same planner from the parameter fields alone (no device needed). */
+int hg_plan_rescaling_params(const uint64_t* chain, uint32_t chain_len, double default_scale,
+                             const hg_model* m, int mode, hg_plan** out);
 /* An externally built plan (the reference's own RescalePlan, or a patched one). */
 int hg_plan_create(int mode, uint64_t planned_rescale_ops, hg_plan** out);
 int hg_plan_set_node(hg_plan* p, const char* id, int decision, uint32_t level_in,
@@ -253,8 +256,14 @@ int hg_execute(hg_ctx* ctx, const hg_model* m, const hg_plan* plan, const hg_ten
 /* ------------------------------------------------------------------ */
 /* Measurement helpers (not part of the reference surface)             */
 /* ------------------------------------------------------------------ */
-/* Register-only IMAD.WIDE.U32 throughput microbenchmark: returns lane-ops/s. */
-int hg_bench_imad_wide(int device, double* ops_per_s);
+/* Register-only integer-pipe microbenchmark (the INT32 roofline denominator):
+ * kind 0 = IMAD (mad.lo.u32), 1 = IMAD.WIDE (mad.wide.u32), 2 = IMAD.HI; lane-ops/s. */
+int hg_bench_int_peak(int device, int kind, double* ops_per_s);
+/* Per-kernel CUDA-event profiler: when enabled, every kernel launch is bracketed by
+ * events on its stream; hg_prof_report writes {"kernel": {"ms": total, "launches": n}}
+ * as JSON and clears the log. */
+int hg_prof_enable(int on);
+int hg_prof_report(char* buf, uint64_t cap);
 /* Times the most recent execute's kernels (sum of per-node CUDA-event ms) by node op kind. */
 int hg_last_exec_node_ms(hg_ctx* ctx, double* ms_by_op /* 11 entries, indexed by hg_op */);
 

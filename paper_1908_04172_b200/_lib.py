@@ -96,14 +96,17 @@ PROTOTYPES = {
     "hg_model_node_count": (C.c_int, [vp, u32p]),
     "hg_model_shape": (C.c_int, [vp, C.c_char_p, u32p, u32p]),
     "hg_plan_rescaling": (C.c_int, [vp, vp, C.c_int, C.POINTER(vp)]),
+    "hg_plan_rescaling_params": (C.c_int, [u64p, C.c_uint32, C.c_double, vp, C.c_int, C.POINTER(vp)]),
     "hg_plan_create": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(vp)]),
     "hg_plan_set_node": (C.c_int, [vp, C.c_char_p, C.c_int, C.c_uint32, C.c_uint32, C.c_double]),
     "hg_plan_get_node": (C.c_int, [vp, C.c_char_p, C.POINTER(C.c_int), u32p, u32p, dblp]),
     "hg_plan_planned_rescales": (C.c_uint64, [vp]),
     "hg_plan_destroy": (None, [vp]),
     "hg_execute": (C.c_int, [vp, vp, vp, vp, vp, NONLIN_FN, vp, C.POINTER(vp), C.POINTER(hg_exec_stats), vp]),
-    "hg_bench_imad_wide": (C.c_int, [C.c_int, dblp]),
+    "hg_bench_int_peak": (C.c_int, [C.c_int, C.c_int, dblp]),
     "hg_last_exec_node_ms": (C.c_int, [vp, dblp]),
+    "hg_prof_enable": (C.c_int, [C.c_int]),
+    "hg_prof_report": (C.c_int, [C.c_char_p, C.c_uint64]),
 }
 
 

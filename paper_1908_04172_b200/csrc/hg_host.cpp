@@ -776,7 +776,6 @@ class Executor {
     const float* wd = weight_dev(ctx, w, s_);
     BufPtr bias_res;
     BufPtr bias_pt;
-    u32 fold[kMaxPrimes] = {};
 
     if (n.op == HG_OP_DOT) {
       const u32 K = w.dims[0], Mo = w.dims[1];
@@ -1596,6 +1595,24 @@ int hg_plan_rescaling(const hg_ctx* ctx, const hg_model* m, int mode, hg_plan** 
   });
 }
 
+int hg_plan_rescaling_params(const uint64_t* chain, uint32_t chain_len, double default_scale, const hg_model* m,
+                             int mode, hg_plan** out) {
+  return guard([&] {
+    require(chain && chain_len >= 1, "modulus chain must be non-empty");
+    Context c;  // host-side fields only: the planner needs no device
+    c.chain.assign(chain, chain + chain_len);
+    c.default_scale = default_scale;
+    long double acc = 1.0L;
+    c.modulus_products.push_back(acc);
+    for (u64 q : c.chain) {
+      acc *= static_cast<long double>(q);
+      c.modulus_products.push_back(acc);
+    }
+    Plan p = plan_rescaling(c, m->m, mode);
+    *out = new hg_plan{std::move(p)};
+  });
+}
+
 int hg_plan_create(int mode, uint64_t planned, hg_plan** out) {
   return guard([&] {
     auto* p = new hg_plan;
@@ -1647,10 +1664,22 @@ int hg_execute(hg_ctx* ctx, const hg_model* m, const hg_plan* plan, const hg_ten
   });
 }
 
-int hg_bench_imad_wide(int device, double* ops_per_s) {
+int hg_bench_int_peak(int device, int kind, double* ops_per_s) {
   return guard([&] {
-    *ops_per_s = bench_imad_wide(device);
+    *ops_per_s = bench_int_peak(device, kind);
     cuda_check(cudaGetLastError(), "imad probe");
+  });
+}
+
+int hg_prof_enable(int on) {
+  return guard([&] { prof_enable(on != 0); });
+}
+
+int hg_prof_report(char* buf, uint64_t cap) {
+  return guard([&] {
+    const std::string r = prof_report();
+    require(r.size() + 1 <= cap, "report buffer too small");
+    std::memcpy(buf, r.c_str(), r.size() + 1);
   });
 }
 

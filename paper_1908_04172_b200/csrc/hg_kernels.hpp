@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 
 #include "hg_device.cuh"
 
@@ -103,6 +104,10 @@ int launch_fft_encode(const double* slots, u32 n_slots, u64 count, u32 n, u32 le
                       const double2* roots, const double2* twist, double2* scratch, u32* out,
                       unsigned long long* max_mant, int* max_exp, const Basis& B, cudaStream_t s);
 
-double bench_imad_wide(int device);
+// Register-only integer pipe probe; kind 0 IMAD, 1 IMAD.WIDE, 2 IMAD.HI.  Lane-ops per second.
+double bench_int_peak(int device, int kind);
+
+void prof_enable(bool on);
+std::string prof_report();  // JSON: kernel -> {ms, launches}; clears the log
 
 }  // namespace hg

@@ -18,7 +18,7 @@ from typing import Callable, Dict, List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import NONLIN_FN, check, hg_exec_stats, hg_node_desc, lib, ValidationError  # noqa: F401
+from ._lib import NONLIN_FN, CudaError, HeError, UnsupportedError, ValidationError, check, hg_exec_stats, hg_node_desc, lib  # noqa: F401
 
 PACKING_REAL, PACKING_COMPLEX = 0, 1
 OPS = {
@@ -50,7 +50,7 @@ class CkksContext:
         self.device = device
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.hg_ctx_destroy(self._h)
             self._h = None
 
@@ -103,7 +103,7 @@ class CipherTensor:
             self.set_shape(shape)
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.hg_tensor_destroy(self._h)
             self._h = None
 
@@ -197,7 +197,7 @@ class RelinKey:
         self.ctx = ctx
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.hg_relin_key_destroy(self._h)
             self._h = None
 
@@ -341,7 +341,7 @@ class PlainModel:
         self.node_ids: List[str] = []
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.hg_model_destroy(self._h)
             self._h = None
 
@@ -418,7 +418,7 @@ class RescalePlan:
         self._h = handle
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.hg_plan_destroy(self._h)
             self._h = None
 
@@ -431,6 +431,15 @@ class RescalePlan:
         """plan_rescaling, henet/graph.hpp:504-584"""
         h = C.c_void_p()
         check(lib.hg_plan_rescaling(ctx.handle, model.handle, mode, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def plan_params(cls, chain: Sequence[int], default_scale: float, model: PlainModel,
+                    mode: int = RESCALE_LAZY) -> "RescalePlan":
+        """plan_rescaling from the parameter fields only (host logic, no GPU)."""
+        arr = (C.c_uint64 * len(chain))(*chain)
+        h = C.c_void_p()
+        check(lib.hg_plan_rescaling_params(arr, len(chain), float(default_scale), model.handle, mode, C.byref(h)))
         return cls(h)
 
     @classmethod
@@ -505,7 +514,20 @@ def execute(ctx: CkksContext, model: PlainModel, plan: RescalePlan, inp: CipherT
     return CipherTensor(ctx, 0, _handle=out)
 
 
-def bench_imad_wide(device: int = 0) -> float:
+def bench_int_peak(device: int = 0, kind: int = 0) -> float:
+    """Measured integer-pipe peak, lane-ops/s (kind 0 IMAD, 1 IMAD.WIDE, 2 IMAD.HI)."""
     v = C.c_double()
-    check(lib.hg_bench_imad_wide(device, C.byref(v)))
+    check(lib.hg_bench_int_peak(device, kind, C.byref(v)))
     return v.value
+
+
+def prof_enable(on: bool = True) -> None:
+    """Bracket every kernel launch with CUDA events on its stream."""
+    check(lib.hg_prof_enable(int(on)))
+
+
+def prof_report() -> dict:
+    """{kernel: {"ms": total_ms, "launches": n}} since the last report."""
+    buf = C.create_string_buffer(1 << 16)
+    check(lib.hg_prof_report(buf, len(buf)))
+    return json.loads(buf.value.decode())

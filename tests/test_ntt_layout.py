@@ -1,0 +1,77 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Pure-Python proof obligations for the NTT register/shared-memory layouts of
+paper_1908_04172_b200/csrc/hg_device.cuh (Ntt<LOGN>): each layout is a
+bijection onto [0, N); every butterfly pair of every stage lives in one thread;
+and the XOR swizzle makes all three shared-memory access patterns
+bank-conflict free (32 lanes -> 32 distinct banks)."""
+import pytest
+
+
+def cfg(logn):
+    logt = logn - 5
+    cb = logn - 10 if logn >= 14 else 3
+    mb = logt - cb
+    return logt, cb, mb
+
+
+def jA(logn, tid, k):
+    logt, cb, mb = cfg(logn)
+    return tid | (k << logt)
+
+
+def jB(logn, tid, k):
+    logt, cb, mb = cfg(logn)
+    cbm, mbm = (1 << cb) - 1, (1 << mb) - 1
+    return (tid & cbm) | ((k & mbm) << cb) | ((tid >> cb) << logt) | ((k >> mb) << (logt + mb))
+
+
+def jC(logn, tid, k):
+    logt, cb, mb = cfg(logn)
+    cbm = (1 << cb) - 1
+    return (k & cbm) | (tid << cb) | ((k >> cb) << (cb + logt))
+
+
+def swz(logn, j):
+    logt, cb, mb = cfg(logn)
+    cbm = (1 << cb) - 1
+    return j ^ ((j >> 5) & cbm) ^ (((j >> logt) & ((1 << (5 - cb)) - 1)) << cb)
+
+
+LAYOUTS = {"A": (jA, lambda l: (0, 5, cfg(l)[0])), "B": (jB, lambda l: (0, cfg(l)[2], cfg(l)[1])),
+           "C": (jC, lambda l: (0, cfg(l)[1], 0))}
+
+
+@pytest.mark.parametrize("logn", [12, 13, 14])
+@pytest.mark.parametrize("name", ["A", "B", "C"])
+def test_bijection_and_conflict_free(logn, name):
+    jm, _ = LAYOUTS[name]
+    n, t = 1 << logn, 1 << (logn - 5)
+    seen = set()
+    for tid in range(t):
+        for k in range(32):
+            seen.add(jm(logn, tid, k))
+    assert seen == set(range(n))
+    assert sorted(swz(logn, j) for j in range(n)) == list(range(n))
+    for w in range(t // 32):
+        for k in range(32):
+            banks = {swz(logn, jm(logn, w * 32 + lane, k)) % 32 for lane in range(32)}
+            assert len(banks) == 32, (name, w, k)
+
+
+@pytest.mark.parametrize("logn", [12, 13, 14])
+def test_butterfly_pairs_are_thread_local(logn):
+    """Stage with t = 2^b pairs j and j + 2^b; pass A covers b in [LOGT, LOGN),
+    pass B [CB, LOGT), pass C [0, CB); the pair must be (tid, k0) / (tid, k0 | 1 << rb)."""
+    logt, cb, mb = cfg(logn)
+    passes = [(jA, logt, 5), (jB, cb, mb), (jC, 0, cb)]
+    covered = []
+    for jm, blo, nb in passes:
+        for rb in range(nb):
+            b = blo + rb
+            covered.append(b)
+            for tid in range(1 << logt):
+                for k in range(32):
+                    if k & (1 << rb):
+                        continue
+                    assert jm(logn, tid, k) + (1 << b) == jm(logn, tid, k | (1 << rb))
+    assert sorted(covered) == list(range(logn))
