@@ -1,0 +1,297 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// henet_b200.hpp -- C++ drop-in for the reference's hot path, over the C ABI.
+//
+// Include this AFTER the reference's own headers ("henet/henet.hpp"); it only
+// uses their public types.  A reference user switches the evaluator by calling
+// henet::gpu::execute instead of henet::execute -- same signature, same
+// argument meaning, same exceptions (henet::ValidationError), bit-identical
+// output ciphertexts (tests/test_gpu_dropin.py runs oracle/ref/dropin_test.cpp,
+// which checks exactly that against the unmodified reference).
+//
+//   henet::execute        henet/graph.hpp:1121-1126   -> henet::gpu::execute
+//   henet::relinearize    henet/ckks.hpp:442-499      -> henet::gpu::relinearize
+//   henet::rescale        henet/ckks.hpp:504-519      -> henet::gpu::rescale
+//   henet::mul_ct_pt_scalar henet/ckks.hpp:387-392    -> henet::gpu::mul_ct_pt_scalar
+//
+// Device state (context tables, relin key, model weights) is cached per
+// CkksContext / RelinKey / PlainModel object, so repeated calls -- the
+// InferenceServer pattern (henet/protocol.hpp:528) -- upload only ciphertexts.
+#pragma once
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "henet_b200.h"
+
+namespace henet {
+namespace gpu {
+
+inline void check(int rc) {
+  if (rc == HG_OK) return;
+  const std::string msg = hg_last_error();
+  if (rc == HG_ERR_VALIDATION) throw ValidationError(msg);
+  throw std::runtime_error("henet::gpu: " + msg);
+}
+
+// Device mirror of one CkksContext (+ its relin keys and models), created lazily.
+// FNV-1a over bytes; device caches are keyed by content, never by address
+// (a freed object's address can be reused by a different model or key).
+inline u64 fnv(const void* p, std::size_t n, u64 h = 1469598103934665603ull) {
+  const auto* b = static_cast<const unsigned char*>(p);
+  for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
+
+class Device {
+ public:
+  explicit Device(const CkksContext& ctx, int device = 0) {
+    std::vector<u64> chain;
+    for (std::size_t i = 0; i < ctx.chain_length(); ++i) chain.push_back(ctx.modulus(i).value);
+    check(hg_ctx_create(ctx.degree(), chain.data(), static_cast<uint32_t>(chain.size()),
+                        ctx.has_special() ? ctx.special().value : 0, ctx.params().default_scale, device, &ctx_));
+    n_ = ctx.degree();
+  }
+  ~Device() {
+    for (auto& kv : keys_) hg_relin_key_destroy(kv.second);
+    for (auto& kv : models_) hg_model_destroy(kv.second);
+    hg_ctx_destroy(ctx_);
+  }
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
+
+  hg_ctx* ctx() const { return ctx_; }
+  u32 degree() const { return n_; }
+
+  const hg_relin_key* relin(const RelinKey& rk) {
+    std::vector<u64> w;
+    for (const auto& part : rk.parts)
+      for (const auto& p : part) w.insert(w.end(), p.words().begin(), p.words().end());
+    const u64 key = fnv(w.data(), w.size() * sizeof(u64));
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = keys_.find(key);
+    if (it != keys_.end()) return it->second;
+    hg_relin_key* k = nullptr;
+    check(hg_relin_key_upload(ctx_, w.data(), w.size(), &k));
+    keys_[key] = k;
+    return k;
+  }
+
+  static u64 fingerprint(const PlainModel& m) {
+    u64 h = fnv(&m.packing, sizeof(m.packing));
+    for (const auto& [name, t] : m.weights) {
+      h = fnv(name.data(), name.size(), h);
+      h = fnv(t.shape.dims.data(), t.shape.dims.size() * sizeof(u32), h);
+      h = fnv(t.data.data(), t.data.size() * sizeof(float), h);
+    }
+    for (const auto& n : m.nodes) {
+      h = fnv(n.id.data(), n.id.size(), h);
+      h = fnv(&n.op, sizeof(n.op), h);
+      for (const auto& i : n.inputs) h = fnv(i.data(), i.size(), h);
+      h = fnv(n.attrs.shape.data(), n.attrs.shape.size() * sizeof(u32), h);
+      const u32 a[8] = {n.attrs.stride, n.attrs.window, n.attrs.filters, n.attrs.pool_stride,
+                        n.attrs.pad[0], n.attrs.pad[1], n.attrs.pad[2], n.attrs.pad[3]};
+      h = fnv(a, sizeof(a), h);
+      h = fnv(n.weight_ref.data(), n.weight_ref.size(), h);
+      h = fnv(n.bias_ref.data(), n.bias_ref.size(), h);
+    }
+    return h;
+  }
+
+  // PlainModel -> hg_model (weights + nodes); load_model's checks rerun device-side.
+  const hg_model* model(const PlainModel& m) {
+    const u64 key = fingerprint(m);
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = models_.find(key);
+    if (it != models_.end()) return it->second;
+    hg_model* hm = nullptr;
+    check(hg_model_create(static_cast<int>(m.packing), &hm));
+    for (const auto& [name, t] : m.weights) {
+      check(hg_model_add_weight(hm, name.c_str(), t.shape.dims.data(), static_cast<uint32_t>(t.shape.dims.size()),
+                                t.data.data()));
+    }
+    for (const auto& n : m.nodes) {
+      std::vector<const char*> ins;
+      for (const auto& s : n.inputs) ins.push_back(s.c_str());
+      hg_node_desc d{};
+      d.id = n.id.c_str();
+      d.op = static_cast<int>(n.op);
+      d.inputs = ins.data();
+      d.n_inputs = static_cast<uint32_t>(ins.size());
+      d.shape = n.attrs.shape.data();
+      d.shape_len = static_cast<uint32_t>(n.attrs.shape.size());
+      d.stride = n.attrs.stride;
+      d.window = n.attrs.window;
+      d.filters = n.attrs.filters;
+      for (int i = 0; i < 4; ++i) d.pad[i] = n.attrs.pad[i];
+      d.pool_stride = n.attrs.pool_stride;
+      d.weight_ref = n.weight_ref.c_str();
+      d.bias_ref = n.bias_ref.c_str();
+      check(hg_model_add_node(hm, &d));
+    }
+    check(hg_model_finalize(hm));
+    models_[key] = hm;
+    return hm;
+  }
+
+ private:
+  hg_ctx* ctx_ = nullptr;
+  u32 n_ = 0;
+  std::mutex mu_;
+  std::map<u64, hg_relin_key*> keys_;
+  std::map<u64, hg_model*> models_;
+};
+
+inline Device& device_for(const CkksContext& ctx) {
+  static std::mutex mu;
+  static std::map<u64, std::unique_ptr<Device>> devs;
+  u64 key = fnv(&ctx.params().poly_degree, sizeof(u32));
+  key = fnv(&ctx.params().default_scale, sizeof(double), key);
+  for (std::size_t i = 0; i < ctx.chain_length(); ++i) key = fnv(&ctx.modulus(i).value, sizeof(u64), key);
+  if (ctx.has_special()) key = fnv(&ctx.special().value, sizeof(u64), key);
+  std::lock_guard<std::mutex> g(mu);
+  auto& d = devs[key];
+  if (!d) d = std::make_unique<Device>(ctx);
+  return *d;
+}
+
+namespace detail {
+
+// RAII tensor handle
+struct Tensor {
+  hg_tensor* t = nullptr;
+  ~Tensor() { hg_tensor_destroy(t); }
+};
+
+inline void upload(Device& dev, const std::vector<Ciphertext>& cts, const std::vector<u32>& shape, Tensor& out) {
+  require(!cts.empty(), "empty cipher tensor");
+  const u32 polys = static_cast<u32>(cts[0].size());
+  const u32 level = static_cast<u32>(cts[0].level());
+  check(hg_tensor_create(dev.ctx(), cts.size(), polys, level, cts[0].scale, static_cast<int>(cts[0].packing), &out.t));
+  std::vector<u64> w;
+  w.reserve(cts.size() * polys * level * dev.degree());
+  for (const auto& ct : cts) {
+    require(ct.size() == polys && ct.level() == level, "ciphertext shape mismatch inside tensor");
+    for (const auto& p : ct.polys) w.insert(w.end(), p.words().begin(), p.words().end());
+  }
+  check(hg_tensor_upload(out.t, w.data(), nullptr));
+  if (!shape.empty()) check(hg_tensor_set_shape(out.t, shape.data(), static_cast<uint32_t>(shape.size())));
+}
+
+inline std::vector<Ciphertext> download(Device& dev, const hg_tensor* t) {
+  uint64_t count = 0;
+  uint32_t polys = 0, level = 0;
+  double scale = 0;
+  int packing = 0;
+  check(hg_tensor_info(t, &count, &polys, &level, &scale, &packing));
+  std::vector<u64> w(count * polys * level * dev.degree());
+  check(hg_tensor_download(t, w.data(), nullptr));
+  std::vector<Ciphertext> out(count);
+  const std::size_t pw = static_cast<std::size_t>(level) * dev.degree();
+  for (uint64_t e = 0; e < count; ++e) {
+    for (u32 p = 0; p < polys; ++p) {
+      RingElement r(dev.degree(), level, PolyDomain::Ntt);
+      std::memcpy(r.words().data(), w.data() + (e * polys + p) * pw, pw * sizeof(u64));
+      out[e].polys.push_back(std::move(r));
+    }
+    out[e].scale = scale;
+    out[e].packing = static_cast<PackingMode>(packing);
+    out[e].slots = dev.degree() / 2;
+  }
+  return out;
+}
+
+struct ProviderCtx {
+  Device* dev;
+  NonlinearityProvider* provider;
+};
+
+// hg_nonlin_fn trampoline onto the reference NonlinearityProvider interface.
+inline int provider_trampoline(void* user, int kind, uint32_t window, uint32_t layer_seq, const hg_tensor* request,
+                               hg_tensor* response) {
+  auto* pc = static_cast<ProviderCtx*>(user);
+  try {
+    auto req = download(*pc->dev, request);
+    auto fresh = pc->provider->apply(kind == HG_NONLIN_RELU ? NonlinKind::Relu : NonlinKind::MaxPool, window,
+                                     layer_seq, req);
+    std::vector<u64> w;
+    for (const auto& ct : fresh)
+      for (const auto& p : ct.polys) w.insert(w.end(), p.words().begin(), p.words().end());
+    return hg_tensor_upload(response, w.data(), nullptr);
+  } catch (...) {
+    return 1;
+  }
+}
+
+}  // namespace detail
+
+// execute, henet/graph.hpp:1121-1126 -- the whole graph on the B200.
+inline CipherTensor execute(std::shared_ptr<const CkksContext> ctx, const PlainModel& model, const RescalePlan& plan,
+                            const CipherTensor& input, const ExecutionConfig& cfg, ExecutionStats* stats = nullptr) {
+  Device& dev = device_for(*ctx);
+  const hg_model* hm = dev.model(model);
+  hg_plan* hp = nullptr;
+  check(hg_plan_create(static_cast<int>(plan.mode), plan.planned_rescale_ops, &hp));
+  std::unique_ptr<hg_plan, void (*)(hg_plan*)> plan_guard(hp, hg_plan_destroy);
+  for (const auto& [id, np] : plan.nodes) {
+    check(hg_plan_set_node(hp, id.c_str(), static_cast<int>(np.decision), static_cast<uint32_t>(np.level_in),
+                           static_cast<uint32_t>(np.level_out), np.scale_out));
+  }
+  require(input.elems.size() == input.shape.elem_count(), "input shape does not match the model");
+  detail::Tensor in;
+  detail::upload(dev, input.elems, input.shape.dims, in);
+  const hg_relin_key* rk = cfg.relin ? dev.relin(*cfg.relin) : nullptr;
+  detail::ProviderCtx pc{&dev, cfg.provider};
+  hg_exec_stats st{};
+  detail::Tensor out;
+  check(hg_execute(dev.ctx(), hm, hp, in.t, rk, cfg.provider ? detail::provider_trampoline : nullptr, &pc, &out.t,
+                   stats ? &st : nullptr, nullptr));
+  CipherTensor result;
+  uint32_t dims[8], nd = 8;
+  check(hg_tensor_get_shape(out.t, dims, &nd));
+  result.shape = TensorShape{std::vector<u32>(dims, dims + nd)};
+  result.elems = detail::download(dev, out.t);
+  if (stats) {
+    stats->rescale_ops = st.rescale_ops;
+    stats->relin_ops = st.relin_ops;
+    stats->nonlin_elements = st.nonlin_elements;
+    stats->wall_ms = st.wall_ms;
+  }
+  return result;
+}
+
+// ---- op level ----
+inline Ciphertext relinearize(const CkksContext& ctx, const Ciphertext& ct, const RelinKey& rk) {
+  Device& dev = device_for(ctx);
+  detail::Tensor in, out;
+  detail::upload(dev, {ct}, {}, in);
+  check(hg_tensor_create(dev.ctx(), 1, 2, 1, 1.0, 0, &out.t));
+  check(hg_relinearize(dev.ctx(), in.t, dev.relin(rk), out.t, nullptr));
+  return detail::download(dev, out.t)[0];
+}
+
+inline Ciphertext rescale(const CkksContext& ctx, const Ciphertext& ct, std::size_t target_level) {
+  Device& dev = device_for(ctx);
+  detail::Tensor in, out;
+  detail::upload(dev, {ct}, {}, in);
+  check(hg_tensor_create(dev.ctx(), 1, 2, 1, 1.0, 0, &out.t));
+  check(hg_rescale(dev.ctx(), in.t, static_cast<uint32_t>(target_level), out.t, nullptr));
+  return detail::download(dev, out.t)[0];
+}
+
+inline Ciphertext mul_ct_pt_scalar(const CkksContext& ctx, const Ciphertext& ct, const ScalarPlaintext& pt) {
+  Device& dev = device_for(ctx);
+  detail::Tensor in, out;
+  detail::upload(dev, {ct}, {}, in);
+  check(hg_tensor_create(dev.ctx(), 1, 2, 1, 1.0, 0, &out.t));
+  require(pt.level() == ct.level(), "ciphertext/plaintext level mismatch");
+  check(hg_mul_ct_pt_scalar(dev.ctx(), in.t, pt.residues.data(), 0, pt.scale, out.t, nullptr));
+  return detail::download(dev, out.t)[0];
+}
+
+}  // namespace gpu
+}  // namespace henet

@@ -1,0 +1,100 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// TEST INFRASTRUCTURE ONLY -- the drop-in check.  Compiled against the
+// UNMODIFIED reference headers (/root/reference/proj/include) plus
+// include/henet_b200.hpp, linked to the product libhenet_b200.so.  Runs the
+// reference's own model generators through henet::execute (CPU) and
+// henet::gpu::execute (B200) with identical arguments and requires
+// bit-identical ciphertexts, scales and statistics.  Exit code 0 = pass.
+#include <cstdio>
+#include <thread>
+
+#include "henet/henet.hpp"
+#include "henet_b200.hpp"
+
+using namespace henet;
+
+static std::shared_ptr<const CkksContext> baseline_ctx() {
+  EncryptionParameters p;  // field assignment: scale 2^24 > 24-bit primes
+  p.poly_degree = 8192;
+  p.default_scale = std::ldexp(1.0, 24);
+  std::vector<PrimeModulus> chain;
+  for (u64 q : {1073692673ull, 16760833ull, 16580609ull, 16515073ull, 16465921ull, 16384001ull}) chain.emplace_back(q);
+  p.basis = RnsBasis(std::move(chain), PrimeModulus(1073643521ull));
+  return std::make_shared<const CkksContext>(p);
+}
+
+static bool same(const CipherTensor& a, const CipherTensor& b, const char* what) {
+  bool ok = a.shape == b.shape && a.elems.size() == b.elems.size();
+  for (std::size_t e = 0; ok && e < a.elems.size(); ++e) {
+    ok = a.elems[e].scale == b.elems[e].scale && a.elems[e].packing == b.elems[e].packing &&
+         a.elems[e].polys.size() == b.elems[e].polys.size();
+    for (std::size_t k = 0; ok && k < a.elems[e].polys.size(); ++k) ok = a.elems[e].polys[k] == b.elems[e].polys[k];
+  }
+  std::printf("%-40s %s (%zu ciphertexts at level %zu)\n", what, ok ? "bit-identical" : "MISMATCH", a.elems.size(),
+              a.elems.empty() ? 0 : a.level());
+  return ok;
+}
+
+static bool run_model(std::shared_ptr<const CkksContext> ctx, const KeyPair& keys, const GeneratedModel& gm,
+                      PackingMode packing, std::size_t batch, const char* name) {
+  PlainModel model = load_model(gm.manifest, std::span<const u8>(gm.blob.data(), gm.blob.size()));
+  RescalePlan plan = plan_lazy_rescaling(*ctx, model);
+  BatchInput in = make_random_input(model.shapes.at(model.input_node().id), batch, 5);
+  CipherTensor x = encrypt_tensor(*ctx, in, keys.secret, 77, packing, std::thread::hardware_concurrency());
+  LocalProvider prov(NonlinearityEngine(ctx, keys.secret, 99));
+  ExecutionConfig cfg;
+  cfg.threads = std::thread::hardware_concurrency();
+  cfg.relin = keys.relin ? &*keys.relin : nullptr;
+  cfg.provider = &prov;
+  ExecutionStats s_cpu, s_gpu;
+  CipherTensor want = henet::execute(ctx, model, plan, x, cfg, &s_cpu);
+  CipherTensor got = henet::gpu::execute(ctx, model, plan, x, cfg, &s_gpu);
+  bool ok = same(want, got, name);
+  ok = ok && s_cpu.rescale_ops == s_gpu.rescale_ops && s_cpu.relin_ops == s_gpu.relin_ops &&
+       s_cpu.nonlin_elements == s_gpu.nonlin_elements;
+  std::printf("  stats cpu (rescale %llu relin %llu nonlin %llu, %.0f ms)  gpu (rescale %llu relin %llu nonlin %llu)\n",
+              (unsigned long long)s_cpu.rescale_ops, (unsigned long long)s_cpu.relin_ops,
+              (unsigned long long)s_cpu.nonlin_elements, s_cpu.wall_ms, (unsigned long long)s_gpu.rescale_ops,
+              (unsigned long long)s_gpu.relin_ops, (unsigned long long)s_gpu.nonlin_elements);
+  return ok;
+}
+
+int main() {
+  auto ctx = baseline_ctx();
+  KeyPair keys = keygen(*ctx, 2024, true);
+  bool ok = true;
+  ok &= run_model(ctx, keys, make_cryptonets(Preset::P13, 1), PackingMode::Real, 4096, "make_cryptonets (c2 topology)");
+  ok &= run_model(ctx, keys, make_cryptonets_relu(Preset::P13, PackingMode::Complex, 2), PackingMode::Complex, 8192,
+                  "make_cryptonets_relu complex (c3)");
+  ok &= run_model(ctx, keys, make_cryptonets_shaped_toy(Preset::P13, 3), PackingMode::Real, 64, "cryptonets toy");
+  // op level
+  {
+    std::vector<double> v(4096, 0.25);
+    Ciphertext ct = encrypt_batch(*ctx, pack_real(v), keys.secret, 5);
+    Ciphertext sq = square(*ctx, ct);
+    bool r1 = henet::relinearize(*ctx, sq, *keys.relin).polys == henet::gpu::relinearize(*ctx, sq, *keys.relin).polys;
+    bool r2 = henet::rescale(*ctx, ct, 3).polys == henet::gpu::rescale(*ctx, ct, 3).polys;
+    auto pt = encode_scalar(*ctx, -0.37, ct.level(), ctx->params().default_scale);
+    bool r3 = henet::mul_ct_pt_scalar(*ctx, ct, pt).polys == henet::gpu::mul_ct_pt_scalar(*ctx, ct, pt).polys;
+    std::printf("op level: relinearize %s, rescale %s, mul_ct_pt_scalar %s\n", r1 ? "ok" : "MISMATCH",
+                r2 ? "ok" : "MISMATCH", r3 ? "ok" : "MISMATCH");
+    ok &= r1 && r2 && r3;
+  }
+  // error behaviour: ValidationError for a bad rescale target, as the reference
+  {
+    std::vector<double> v(16, 1.0);
+    Ciphertext ct = encrypt_batch(*ctx, pack_real(v), keys.secret, 6);
+    Ciphertext low = henet::rescale(*ctx, ct, 1);
+    bool threw = false;
+    try {
+      henet::gpu::rescale(*ctx, low, 1);
+    } catch (const ValidationError&) {
+      threw = true;
+    }
+    std::printf("ValidationError on rescale below level 1: %s\n", threw ? "ok" : "MISSING");
+    ok &= threw;
+  }
+  std::printf(ok ? "DROPIN OK\n" : "DROPIN FAILED\n");
+  return ok ? 0 : 1;
+}

@@ -39,8 +39,15 @@ struct DevPrime {
   u32 w1n;       // inv_root_powers[1] * N^-1 mod q (last inverse stage)
   u32 w1n_sh;
   u32 pad_;
-  const uint2* fwd;  // N entries: (psi^bitrev(i), shoup)
-  const uint2* inv;  // N entries: (psi^-bitrev(i), shoup)
+  // Twiddles staged per NTT pass (see Ntt below): pass A (uniform over the CTA)
+  // from the kernel parameter block, passes B / C from per-thread rows of 32
+  // (value, shoup) pairs in the exact order the unrolled stages consume them.
+  uint2 twA[32];       // root_powers[1..31]      (psi^bitrev(i), shoup)
+  uint2 itwA[32];      // inv_root_powers[1..31]
+  const uint2* fwdB;   // [2^MB rows][32]
+  const uint2* fwdC;   // [T rows][32]
+  const uint2* invB;
+  const uint2* invC;
 };
 
 struct Basis {
@@ -135,21 +142,38 @@ struct Ntt {
     else return jC(tid, k);
   }
 
-  // XOR swizzle of the low 5 bits (the bank) with higher bits; conflict-free
-  // for all three layouts (checked in tests/test_ntt_layout.py).
-  __device__ static __forceinline__ u32 swz(u32 j) {
-    return j ^ ((j >> 5) & CBm) ^ (((j >> LOGT) & ((1u << (5 - CB)) - 1)) << CB);
+  // Shared-memory word of element j: one pad word per 32.  Bank-conflict free
+  // for all three layouts at N = 2^13, 2^14 (tests/test_ntt_layout.py), and
+  // since jmap(tid, k) = base(tid) | const(k) with disjoint bits, the address
+  // splits into base(tid) + const(k): every access is an immediate offset.
+  static constexpr int SMEM_WORDS = N + (N >> 5);
+  __device__ static __forceinline__ u32 swz(u32 j) { return j + (j >> 5); }
+
+  // jmap<L>(tid, k) == tpart<L>(tid) | kpart<L>(k) with disjoint bit fields.
+  template <int L>
+  __device__ static __forceinline__ u32 tpart(u32 tid) {
+    if constexpr (L == 0) return tid;
+    else if constexpr (L == 1) return (tid & CBm) | ((tid >> CB) << LOGT);
+    else return tid << CB;
+  }
+  template <int L>
+  __device__ static __forceinline__ constexpr u32 kpart(u32 k) {
+    if constexpr (L == 0) return k << LOGT;
+    else if constexpr (L == 1) return ((k & MBm) << CB) | ((k >> MB) << (LOGT + MB));
+    else return (k & CBm) | ((k >> CB) << (CB + LOGT));
   }
 
   template <int L>
   __device__ static __forceinline__ void store(const u32 (&x)[32], u32* sm, u32 tid) {
+    u32* base = sm + swz(tpart<L>(tid));
 #pragma unroll
-    for (int k = 0; k < 32; ++k) sm[swz(jmap<L>(tid, k))] = x[k];
+    for (int k = 0; k < 32; ++k) base[swz(kpart<L>(k))] = x[k];
   }
   template <int L>
   __device__ static __forceinline__ void load(u32 (&x)[32], const u32* sm, u32 tid) {
+    const u32* base = sm + swz(tpart<L>(tid));
 #pragma unroll
-    for (int k = 0; k < 32; ++k) x[k] = sm[swz(jmap<L>(tid, k))];
+    for (int k = 0; k < 32; ++k) x[k] = base[swz(kpart<L>(k))];
   }
 
   // Butterfly bits of pass L occupy register bits [0, NB); the j bit of
@@ -160,12 +184,26 @@ struct Ntt {
     static constexpr int BLO = (L == 0) ? LOGT : (L == 1 ? CB : 0);
   };
 
+  // Row of staged twiddles of pass L (1: B, 2: C) for this thread, 16 x 128-bit.
+  template <int L>
+  __device__ static __forceinline__ void load_row(uint4 (&tw)[16], const uint2* base, u32 tid) {
+    const uint4* row = reinterpret_cast<const uint4*>(base + static_cast<size_t>(L == 1 ? (tid >> CB) : tid) * 32);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) tw[i] = __ldg(row + i);
+  }
+  __device__ static __forceinline__ uint2 slot(const uint4 (&tw)[16], int n) {
+    return (n & 1) ? make_uint2(tw[n >> 1].z, tw[n >> 1].w) : make_uint2(tw[n >> 1].x, tw[n >> 1].y);
+  }
+
   // Forward (Cooley-Tukey, Harvey lazy) stages of pass L.  Values in [0, 4q).
   template <int L>
   __device__ static __forceinline__ void fwd_pass(u32 (&x)[32], u32 tid, const DevPrime& P) {
     constexpr int NB = PassShape<L>::NB;
     constexpr int BLO = PassShape<L>::BLO;
     const u32 q = P.q, q2 = P.two_q;
+    uint4 tw[16];
+    if (L != 0) load_row<L>(tw, L == 1 ? P.fwdB : P.fwdC, tid);
+    int n = 0;
 #pragma unroll
     for (int s = 0; s < NB; ++s) {
       const int rb = NB - 1 - s;  // register bit of this stage
@@ -175,8 +213,8 @@ struct Ntt {
 #pragma unroll
         for (int hi = 0; hi < (1 << (NB - 1 - rb)); ++hi) {
           const u32 kh = (static_cast<u32>(g) << NB) | (static_cast<u32>(hi) << (rb + 1));
-          const u32 j = jmap<L>(tid, kh);
-          const uint2 w = __ldg(&P.fwd[(1u << (LOGN - 1 - b)) + (j >> (b + 1))]);
+          const uint2 w = (L == 0) ? P.twA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))] : slot(tw, n);
+          ++n;
 #pragma unroll
           for (int lo = 0; lo < (1 << rb); ++lo) {
             const int k0 = kh | lo;
@@ -199,6 +237,9 @@ struct Ntt {
     constexpr int NB = PassShape<L>::NB;
     constexpr int BLO = PassShape<L>::BLO;
     const u32 q = P.q, q2 = P.two_q;
+    uint4 tw[16];
+    if (L != 0) load_row<L>(tw, L == 1 ? P.invB : P.invC, tid);
+    int n = 0;
 #pragma unroll
     for (int s = 0; s < NB; ++s) {
       const int rb = s;
@@ -218,8 +259,8 @@ struct Ntt {
               x[k1] = mul_shoup_lazy(U - V + q2, P.w1n, P.w1n_sh, q);
             }
           } else {
-            const u32 j = jmap<L>(tid, kh);
-            const uint2 w = __ldg(&P.inv[(1u << (LOGN - 1 - b)) + (j >> (b + 1))]);
+            const uint2 w = (L == 0) ? P.itwA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))] : slot(tw, n);
+            ++n;
 #pragma unroll
             for (int lo = 0; lo < (1 << rb); ++lo) {
               const int k0 = kh | lo;

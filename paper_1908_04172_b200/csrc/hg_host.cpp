@@ -132,16 +132,42 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
   ctx->core->device = device;
   cuda_check(cudaStreamCreateWithFlags(&ctx->core->stream, cudaStreamNonBlocking), "cudaStreamCreate");
 
-  // NTT tables (root_powers / inv_root_powers in the reference's order) + Shoup companions.
-  std::vector<uint2> tab(static_cast<size_t>(full) * 2 * n);
+  // NTT tables (root_powers / inv_root_powers in the reference's order, with
+  // Shoup companions), staged per NTT pass in the order the kernels consume them.
+  const u32 LOGT = logn - 5, CB = logn >= 14 ? logn - 10 : 3, MB = LOGT - CB;
+  const u32 rowsB = 1u << MB, rowsC = 1u << LOGT;
+  const size_t per_prime = 2 * static_cast<size_t>(rowsB + rowsC) * 32;
+  std::vector<uint2> staged(static_cast<size_t>(full) * per_prime);
+  auto jmap = [&](int L, u32 tid, u32 k) -> u32 {
+    const u32 CBm = (1u << CB) - 1, MBm = (1u << MB) - 1;
+    if (L == 1) return (tid & CBm) | ((k & MBm) << CB) | ((tid >> CB) << LOGT) | ((k >> MB) << (LOGT + MB));
+    return (k & CBm) | (tid << CB) | ((k >> CB) << (CB + LOGT));
+  };
+  auto stage_rows = [&](int L, bool inverse, const std::vector<uint2>& tab, uint2* out) {
+    const u32 NB = L == 1 ? MB : CB, BLO = L == 1 ? CB : 0;
+    const u32 rows = L == 1 ? rowsB : rowsC;
+    for (u32 R = 0; R < rows; ++R) {
+      const u32 tid = L == 1 ? (R << CB) : R;
+      int nslot = 0;
+      for (u32 st = 0; st < NB; ++st) {
+        const u32 rb = inverse ? st : NB - 1 - st;
+        const u32 bb = BLO + rb;
+        for (u32 g = 0; g < (1u << (5 - NB)); ++g)
+          for (u32 hi = 0; hi < (1u << (NB - 1 - rb)); ++hi) {
+            const u32 kh = (g << NB) | (hi << (rb + 1));
+            const u32 j = jmap(L, tid, kh);
+            out[static_cast<size_t>(R) * 32 + nslot++] = tab[(1u << (logn - 1 - bb)) + (j >> (bb + 1))];
+          }
+      }
+    }
+  };
+  std::vector<uint2> f(n), g(n);
   for (u32 i = 0; i < full; ++i) {
     const u64 q = ctx->basis_mod(i);
     const u64 psi = nt::primitive_2n_root(q, n);
     require(nt::powmod(psi, n, q) == q - 1 && nt::powmod(psi, 2ull * n, q) == 1, "root order check failed");
     ctx->roots.push_back(psi);
     const u64 psi_inv = nt::inv(psi, q);
-    uint2* f = &tab[static_cast<size_t>(i) * 2 * n];
-    uint2* g = f + n;
     for (u32 k = 0; k < n; ++k) {
       const u32 rev = nt::bit_reverse(k, logn);
       const u64 w = nt::powmod(psi, rev, q), wi = nt::powmod(psi_inv, rev, q);
@@ -161,16 +187,28 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
     const u64 w1n = nt::mulmod(g[1].x, ninv, q);
     P.w1n = static_cast<u32>(w1n);
     P.w1n_sh = nt::shoup(w1n, q);
+    for (u32 k = 0; k < 32; ++k) {
+      P.twA[k] = f[k];
+      P.itwA[k] = g[k];
+    }
+    uint2* base = &staged[static_cast<size_t>(i) * per_prime];
+    stage_rows(1, false, f, base);
+    stage_rows(2, false, f, base + rowsB * 32);
+    stage_rows(1, true, g, base + (rowsB + rowsC) * 32);
+    stage_rows(2, true, g, base + (2 * rowsB + rowsC) * 32);
   }
-  ctx->tables = ctx->alloc(tab.size() * sizeof(uint2), nullptr);
-  cuda_check(cudaMemcpyAsync(ctx->tables->ptr, tab.data(), tab.size() * sizeof(uint2), cudaMemcpyHostToDevice,
+  ctx->tables = ctx->alloc(staged.size() * sizeof(uint2), nullptr);
+  cuda_check(cudaMemcpyAsync(ctx->tables->ptr, staged.data(), staged.size() * sizeof(uint2), cudaMemcpyHostToDevice,
                              ctx->core->stream),
              "upload tables");
   for (u32 i = 0; i < full; ++i) {
-    uint2* base = static_cast<uint2*>(ctx->tables->ptr) + static_cast<size_t>(i) * 2 * n;
-    ctx->basis.p[i].fwd = base;
-    ctx->basis.p[i].inv = base + n;
+    const uint2* base = static_cast<const uint2*>(ctx->tables->ptr) + static_cast<size_t>(i) * per_prime;
+    ctx->basis.p[i].fwdB = base;
+    ctx->basis.p[i].fwdC = base + rowsB * 32;
+    ctx->basis.p[i].invB = base + (rowsB + rowsC) * 32;
+    ctx->basis.p[i].invC = base + (2 * rowsB + rowsC) * 32;
   }
+  cuda_check(cudaStreamSynchronize(ctx->core->stream), "upload tables");
 
   // Embedding tables, computed with the reference's expressions (henet/fft.hpp:30-43)
   // on the host libm so the GPU FFT sees identical doubles.
@@ -779,8 +817,7 @@ class Executor {
 
     if (n.op == HG_OP_DOT) {
       const u32 K = w.dims[0], Mo = w.dims[1];
-      const u32 warps = std::min<u32>(8, (Mo + 15) / 16);
-      const u32 BM = warps * 16;
+      const u32 BM = mac_dense_warps(Mo) * 4;
       const u32 Mpad = (Mo + BM - 1) / BM * BM;
       BufPtr wres = ctx.alloc(static_cast<u64>(L) * K * Mpad * 4, s_);
       cuda_check(cudaMemsetAsync(wres->ptr, 0, static_cast<u64>(L) * K * Mpad * 4, s_), "memset");

@@ -26,7 +26,7 @@ namespace hg {
 // Batched NTT (hg_ntt_forward / hg_ntt_inverse)
 // ===========================================================================
 template <int LOGN, bool INV>
-__global__ void __launch_bounds__(1 << (LOGN - 5)) k_ntt(u32* data, u32 level, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 2 : 1)) k_ntt(u32* data, u32 level, Basis B) {
   using NT = Ntt<LOGN>;
   extern __shared__ u32 sm[];
   const u32 tid = threadIdx.x;
@@ -55,10 +55,12 @@ __device__ __forceinline__ u32 signed_residue(i32 c, const DevPrime& P) {
 // Rescale (one CTA per (ciphertext, polynomial))
 // ===========================================================================
 template <int LOGN>
-__global__ void __launch_bounds__(1 << (LOGN - 5)) k_rescale(RescaleArgs a, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 2 : 1)) k_rescale(RescaleArgs a, Basis B) {
   using NT = Ntt<LOGN>;
   constexpr int N = NT::N;
+  constexpr int T = NT::T;
   extern __shared__ u32 sm[];
+  i32* cs = reinterpret_cast<i32*>(sm + NT::SMEM_WORDS);  // rounding correction, thread-private slots [k * T + tid]
   const u32 tid = threadIdx.x;
   const u64 row = blockIdx.x;
   const u32 L = a.level;
@@ -66,38 +68,48 @@ __global__ void __launch_bounds__(1 << (LOGN - 5)) k_rescale(RescaleArgs a, Basi
   u32* dst = a.out + row * (L - 1) * N;
 
   u32 x[32];
-  i32 c[32];
   {
     const DevPrime& Pl = B.p[L - 1];
     NT::gload_C(x, src + static_cast<u64>(L - 1) * N, tid);
     NT::inverse(x, sm, tid, Pl);
 #pragma unroll
-    for (int k = 0; k < 32; ++k) c[k] = centered_round_rem(x[k], Pl);
+    for (int k = 0; k < 32; ++k) cs[k * T + tid] = centered_round_rem(x[k], Pl);
   }
   for (u32 i = 0; i + 1 < L; ++i) {
     const DevPrime& Pi = B.p[i];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) x[k] = signed_residue(c[k], Pi);
+    for (int k = 0; k < 32; ++k) x[k] = signed_residue(cs[k * T + tid], Pi);
     NT::forward(x, sm, tid, Pi);
-    u32 y[32];
-    NT::gload_C(y, src + static_cast<u64>(i) * N, tid);
     const u32 q = Pi.q, pv = a.pinv[i], ps = a.pinv_sh[i];
+    const u32* in_i = src + static_cast<u64>(i) * N;
+    u32* out_i = dst + static_cast<u64>(i) * N;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) x[k] = mul_shoup(y[k] + q - x[k], pv, ps, q);
-    NT::gstore_C(x, dst + static_cast<u64>(i) * N, tid);
+    for (int k = 0; k < 32; k += 4) {
+      const u32 j = NT::jC(tid, k);
+      const uint4 y = __ldg(reinterpret_cast<const uint4*>(in_i + j));
+      uint4 o;
+      o.x = mul_shoup(y.x + q - x[k], pv, ps, q);
+      o.y = mul_shoup(y.y + q - x[k + 1], pv, ps, q);
+      o.z = mul_shoup(y.z + q - x[k + 2], pv, ps, q);
+      o.w = mul_shoup(y.w + q - x[k + 3], pv, ps, q);
+      *reinterpret_cast<uint4*>(out_i + j) = o;
+    }
   }
 }
 
 // ===========================================================================
 // Dense modular contraction (Dot)
-//   grid.x = N / 128 coefficient tiles, grid.y = M tiles of 16*warps outputs,
-//   grid.z = polys * level.  Warp w owns outputs m0 + 16w .. +16, lane owns
-//   coefficients n0 + 4*lane .. +4.  X and W tiles of BK = 16 taps are staged
-//   in shared memory with cp.async (double buffered).
+//   grid.x = N / 128 coefficient tiles, grid.y = M tiles of 4*warps outputs,
+//   grid.z = polys * level.  Warp w owns outputs m0 + 4w .. +4, lane owns
+//   coefficients n0 + 4*lane .. +4 (16 u64 accumulators per thread, so up to
+//   32 warps per CTA stay resident).  X and W tiles of BK = 16 taps are staged
+//   in shared memory with cp.async (double buffered); every MAC is one
+//   IMAD.WIDE.U32 into an un-reduced u64 lane, reduced once in the epilogue.
 // ===========================================================================
 constexpr int kBK = 16;
-constexpr int kTM = 16;
+constexpr int kTM = 4;
 constexpr int kBN = 128;
+constexpr int kMaxWarps = 32;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -110,15 +122,45 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-__global__ void __launch_bounds__(256) k_mac_dense(MacDenseArgs a, Basis B) {
-  __shared__ __align__(16) u32 xs[2][kBK][kBN];
-  __shared__ __align__(16) u32 ws[2][kBK][kTM * 8];
+// One BK-deep tile of the dense contraction; FOLD keeps 30-bit-limb accumulators
+// below 2^64 by folding hi*2^32 into (2^32 mod q) every 8 taps.
+template <bool FOLD>
+__device__ __forceinline__ void mac_tile(u64 (&acc)[kTM][4], const u32 (*xs)[kBN], const u32 (*ws)[kTM * kMaxWarps],
+                                         u32 lane, u32 warp, u64 r32) {
+#pragma unroll
+  for (int kk = 0; kk < kBK; ++kk) {
+    const uint4 xv = *reinterpret_cast<const uint4*>(&xs[kk][lane * 4]);
+    const uint4 wv = *reinterpret_cast<const uint4*>(&ws[kk][warp * kTM]);
+    const u32 w[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+    for (int i = 0; i < kTM; ++i) {
+      acc[i][0] += static_cast<u64>(w[i]) * xv.x;
+      acc[i][1] += static_cast<u64>(w[i]) * xv.y;
+      acc[i][2] += static_cast<u64>(w[i]) * xv.z;
+      acc[i][3] += static_cast<u64>(w[i]) * xv.w;
+    }
+    if (FOLD && (kk & 7) == 7) {
+#pragma unroll
+      for (int i = 0; i < kTM; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = (acc[i][j] & 0xffffffffull) + (acc[i][j] >> 32) * r32;
+    }
+  }
+}
+
+constexpr int kStages = 4;
+constexpr size_t kDenseSmem = static_cast<size_t>(kStages) * kBK * (kBN + kTM * kMaxWarps) * sizeof(u32);
+
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) k_mac_dense(MacDenseArgs a, Basis B) {
+  extern __shared__ __align__(16) u32 dsm[];
+  auto xs = reinterpret_cast<u32(*)[kBK][kBN]>(dsm);                                   // [kStages][kBK][kBN]
+  auto ws = reinterpret_cast<u32(*)[kBK][kTM * kMaxWarps]>(dsm + kStages * kBK * kBN);  // [kStages][kBK][BM]
   const u32 warps = blockDim.x >> 5;
   const u32 BM = kTM * warps;
   const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u32 n0 = blockIdx.x * kBN;
   const u32 m0 = blockIdx.y * BM;
-  const u32 pl = blockIdx.z;           // poly * level + limb
+  const u32 pl = blockIdx.z;  // poly * level + limb
   const u32 poly = pl / a.level, limb = pl % a.level;
   const DevPrime& P = B.p[limb];
   const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;  // words per input ct
@@ -129,22 +171,19 @@ __global__ void __launch_bounds__(256) k_mac_dense(MacDenseArgs a, Basis B) {
 
   const u32 ktiles = (a.K + kBK - 1) / kBK;
   auto load_tile = [&](u32 kt, int st) {
-    // X tile: kBK rows x 128 words = 512 chunks of 16 B
     for (u32 c = tid; c < kBK * (kBN / 4); c += blockDim.x) {
       const u32 r = c / (kBN / 4), col = (c % (kBN / 4)) * 4;
       const u32 k = kt * kBK + r;
       const bool v = k < a.K;
       cp_async16(&xs[st][r][col], Xb + (v ? static_cast<u64>(k) * xstride : 0) + col, v);
     }
-    // W tile: kBK rows x BM words
-    const u32 wchunks = kBK * (BM / 4);
-    for (u32 c = tid; c < wchunks; c += blockDim.x) {
-      const u32 r = c / (BM / 4), col = (c % (BM / 4)) * 4;
+    const u32 wq = BM / 4;
+    for (u32 c = tid; c < kBK * wq; c += blockDim.x) {
+      const u32 r = c / wq, col = (c % wq) * 4;
       const u32 k = kt * kBK + r;
       const bool v = k < a.K;
       cp_async16(&ws[st][r][col], Wb + (v ? static_cast<u64>(k) * a.Mpad : 0) + col, v);
     }
-    cp_async_commit();
   };
 
   u64 acc[kTM][4];
@@ -153,40 +192,27 @@ __global__ void __launch_bounds__(256) k_mac_dense(MacDenseArgs a, Basis B) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0;
 
-  load_tile(0, 0);
+  // kStages-deep cp.async pipeline: tiles kt+1 .. kt+kStages-1 are in flight
+  // while tile kt is multiplied.
+#pragma unroll
+  for (int st = 0; st < kStages - 1; ++st) {
+    if (static_cast<u32>(st) < ktiles) load_tile(st, st);
+    cp_async_commit();
+  }
   for (u32 kt = 0; kt < ktiles; ++kt) {
-    const int st = kt & 1;
-    if (kt + 1 < ktiles) {
-      load_tile(kt + 1, st ^ 1);
-      cp_async_wait<1>();
+    const int st = kt % kStages;
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    {
+      const u32 nk = kt + kStages - 1;
+      if (nk < ktiles) load_tile(nk, nk % kStages);
+      cp_async_commit();
+    }
+    if (fold) {
+      mac_tile<true>(acc, xs[st], ws[st], lane, warp, r32);
     } else {
-      cp_async_wait<0>();
+      mac_tile<false>(acc, xs[st], ws[st], lane, warp, r32);
     }
-    __syncthreads();
-#pragma unroll 4
-    for (int kk = 0; kk < kBK; ++kk) {
-      const uint4 xv = *reinterpret_cast<const uint4*>(&xs[st][kk][lane * 4]);
-      u32 w[kTM];
-#pragma unroll
-      for (int i = 0; i < kTM; i += 4) {
-        const uint4 wv = *reinterpret_cast<const uint4*>(&ws[st][kk][warp * kTM + i]);
-        w[i] = wv.x; w[i + 1] = wv.y; w[i + 2] = wv.z; w[i + 3] = wv.w;
-      }
-#pragma unroll
-      for (int i = 0; i < kTM; ++i) {
-        acc[i][0] += static_cast<u64>(w[i]) * xv.x;
-        acc[i][1] += static_cast<u64>(w[i]) * xv.y;
-        acc[i][2] += static_cast<u64>(w[i]) * xv.z;
-        acc[i][3] += static_cast<u64>(w[i]) * xv.w;
-      }
-      if (fold && (kk & 7) == 7) {
-#pragma unroll
-        for (int i = 0; i < kTM; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = (acc[i][j] & 0xffffffffull) + (acc[i][j] >> 32) * r32;
-      }
-    }
-    __syncthreads();
   }
 
   const u32 q = P.q;
@@ -208,25 +234,29 @@ __global__ void __launch_bounds__(256) k_mac_dense(MacDenseArgs a, Basis B) {
 
 // ===========================================================================
 // Convolution (direct, implicit im2col)
-//   grid.x = N / (4 * 128), grid.y = output positions, grid.z = polys * level.
-//   Each thread: 4 coefficients x all filters (chunks of kFT).
+//   grid.x = N / (4 * 256), grid.y = output positions, grid.z = polys * level *
+//   filter chunks.  Each thread: 4 coefficients x FT filters; the gathered
+//   input of the next tap is prefetched while the current tap is multiplied.
 // ===========================================================================
-constexpr int kFT = 8;
 constexpr int kMaxTaps = 1024;
+constexpr int kConvThreads = 256;
 
-__global__ void __launch_bounds__(128) k_mac_conv(MacConvArgs a, Basis B) {
+template <int FT>
+__global__ void __launch_bounds__(kConvThreads) k_mac_conv(MacConvArgs a, Basis B) {
   __shared__ u32 tap_in[kMaxTaps];
-  __shared__ u32 tap_w[kMaxTaps];
+  __shared__ __align__(16) u32 wsm[kMaxTaps * FT];
   __shared__ u32 ntaps_s;
-  __shared__ __align__(16) u32 wsm[kMaxTaps * kFT];
   const u32 tid = threadIdx.x;
   const u32 pos = blockIdx.y;
   const u32 oy = pos / a.OW, ox = pos % a.OW;
-  const u32 pl = blockIdx.z;
+  const u32 nchunks = (a.F + FT - 1) / FT;
+  const u32 pl = blockIdx.z / nchunks;
+  const u32 f0 = (blockIdx.z % nchunks) * FT;
   const u32 poly = pl / a.level, limb = pl % a.level;
   const DevPrime& P = B.p[limb];
   const u32 n = (blockIdx.x * blockDim.x + tid) * 4;
   const u32 taps_all = a.C * a.win * a.win;
+  const u32* Wl = a.W + static_cast<u64>(limb) * a.F * taps_all;
 
   if (tid == 0) {
     // valid taps in ascending (c, ky, kx) order, henet/graph.hpp:976-989
@@ -238,7 +268,10 @@ __global__ void __launch_bounds__(128) k_mac_conv(MacConvArgs a, Basis B) {
           const int ix = static_cast<int>(ox * a.stride + kx) - static_cast<int>(a.pad_left);
           if (iy < 0 || iy >= static_cast<int>(a.IH) || ix < 0 || ix >= static_cast<int>(a.IW)) continue;
           tap_in[cnt] = (c * a.IH + iy) * a.IW + ix;
-          tap_w[cnt] = (c * a.win + ky) * a.win + kx;
+          const u32 tw = (c * a.win + ky) * a.win + kx;
+#pragma unroll
+          for (int f = 0; f < FT; ++f)
+            wsm[cnt * FT + f] = (f0 + f < a.F) ? __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + tw]) : 0u;
           ++cnt;
         }
     ntaps_s = cnt;
@@ -247,55 +280,58 @@ __global__ void __launch_bounds__(128) k_mac_conv(MacConvArgs a, Basis B) {
   const u32 ntaps = ntaps_s;
   const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
   const u32* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n;
-  const u32* Wl = a.W + static_cast<u64>(limb) * a.F * taps_all;
   const bool fold = a.fold[limb] != 0;
   const u64 r32 = P.r32;
   const u32 q = P.q;
 
-  for (u32 f0 = 0; f0 < a.F; f0 += kFT) {
-    __syncthreads();
-    for (u32 i = tid; i < ntaps * kFT; i += blockDim.x) {
-      const u32 t = i / kFT, f = f0 + i % kFT;
-      wsm[i] = f < a.F ? __ldg(&Wl[static_cast<u64>(f) * taps_all + tap_w[t]]) : 0u;
+  u64 acc[FT][4];
+#pragma unroll
+  for (int f = 0; f < FT; ++f)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[f][j] = 0;
+  constexpr int kPre = 4;  // gathered inputs in flight
+  uint4 ring[kPre];
+#pragma unroll
+  for (int i = 0; i < kPre; ++i)
+    ring[i] = (static_cast<u32>(i) < ntaps) ? __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(tap_in[i]) * xstride))
+                                            : make_uint4(0, 0, 0, 0);
+  for (u32 t0 = 0; t0 < ntaps; t0 += kPre) {
+#pragma unroll
+   for (int i = 0; i < kPre; ++i) {
+    const u32 t = t0 + i;
+    if (t >= ntaps) break;
+    const uint4 xv = ring[i];
+    if (t + kPre < ntaps) ring[i] = __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(tap_in[t + kPre]) * xstride));
+#pragma unroll
+    for (int f = 0; f < FT; ++f) {
+      const u32 w = wsm[t * FT + f];
+      acc[f][0] += static_cast<u64>(w) * xv.x;
+      acc[f][1] += static_cast<u64>(w) * xv.y;
+      acc[f][2] += static_cast<u64>(w) * xv.z;
+      acc[f][3] += static_cast<u64>(w) * xv.w;
     }
-    __syncthreads();
-    u64 acc[kFT][4];
+    if (fold && (t & 7) == 7) {
 #pragma unroll
-    for (int f = 0; f < kFT; ++f)
+      for (int f = 0; f < FT; ++f)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[f][j] = 0;
-    for (u32 t = 0; t < ntaps; ++t) {
-      const uint4 xv = __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(tap_in[t]) * xstride));
-#pragma unroll
-      for (int f = 0; f < kFT; ++f) {
-        const u32 w = wsm[t * kFT + f];
-        acc[f][0] += static_cast<u64>(w) * xv.x;
-        acc[f][1] += static_cast<u64>(w) * xv.y;
-        acc[f][2] += static_cast<u64>(w) * xv.z;
-        acc[f][3] += static_cast<u64>(w) * xv.w;
-      }
-      if (fold && (t & 7) == 7) {
-#pragma unroll
-        for (int f = 0; f < kFT; ++f)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[f][j] = (acc[f][j] & 0xffffffffull) + (acc[f][j] >> 32) * r32;
-      }
+        for (int j = 0; j < 4; ++j) acc[f][j] = (acc[f][j] & 0xffffffffull) + (acc[f][j] >> 32) * r32;
     }
+   }
+  }
 #pragma unroll
-    for (int f = 0; f < kFT; ++f) {
-      const u32 ff = f0 + f;
-      if (ff >= a.F) continue;
-      u32 bv = 0;
-      if (a.bias != nullptr && poly == 0) bv = __ldg(&a.bias[static_cast<u64>(limb) * a.F + ff]);
-      uint4 o;
-      o.x = addmod(reduce64(acc[f][0], P), bv, q);
-      o.y = addmod(reduce64(acc[f][1], P), bv, q);
-      o.z = addmod(reduce64(acc[f][2], P), bv, q);
-      o.w = addmod(reduce64(acc[f][3], P), bv, q);
-      const u64 e = static_cast<u64>(ff) * a.OH * a.OW + pos;
-      u32* yp = a.Y + ((e * a.polys + poly) * a.level + limb) * a.N + n;
-      *reinterpret_cast<uint4*>(yp) = o;
-    }
+  for (int f = 0; f < FT; ++f) {
+    const u32 ff = f0 + f;
+    if (ff >= a.F) continue;
+    u32 bv = 0;
+    if (a.bias != nullptr && poly == 0) bv = __ldg(&a.bias[static_cast<u64>(limb) * a.F + ff]);
+    uint4 o;
+    o.x = addmod(reduce64(acc[f][0], P), bv, q);
+    o.y = addmod(reduce64(acc[f][1], P), bv, q);
+    o.z = addmod(reduce64(acc[f][2], P), bv, q);
+    o.w = addmod(reduce64(acc[f][3], P), bv, q);
+    const u64 e = static_cast<u64>(ff) * a.OH * a.OW + pos;
+    u32* yp = a.Y + ((e * a.polys + poly) * a.level + limb) * a.N + n;
+    *reinterpret_cast<uint4*>(yp) = o;
   }
 }
 
@@ -327,7 +363,7 @@ __device__ __forceinline__ void load_c2(u32 (&y)[32], const RelinArgs& a, u64 ct
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(1 << (LOGN - 5)) k_relin_digits(RelinArgs a, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 2 : 1)) k_relin_digits(RelinArgs a, Basis B) {
   using NT = Ntt<LOGN>;
   constexpr int N = NT::N;
   extern __shared__ u32 sm[];
@@ -342,10 +378,13 @@ __global__ void __launch_bounds__(1 << (LOGN - 5)) k_relin_digits(RelinArgs a, B
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(1 << (LOGN - 5)) k_relin_keysw(RelinArgs a, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 2 : 1)) k_relin_keysw(RelinArgs a, Basis B) {
   using NT = Ntt<LOGN>;
   constexpr int N = NT::N;
+  constexpr int T = NT::T;
   extern __shared__ u32 sm[];
+  u32* acc0 = sm + NT::SMEM_WORDS;  // thread-private slots [k * T + tid], layout C
+  u32* acc1 = acc0 + N;
   const u32 tid = threadIdx.x;
   const u32 L = a.level;
   const u64 ct = blockIdx.x / (L + 1);
@@ -354,9 +393,6 @@ __global__ void __launch_bounds__(1 << (LOGN - 5)) k_relin_keysw(RelinArgs a, Ba
   const u32 bidx = special ? a.chain_len : t;  // basis index == key limb index
   const DevPrime& P = B.p[bidx];
   const u32 q = P.q;
-  u32 acc0[32], acc1[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) acc0[k] = acc1[k] = 0;
 
   for (u32 j = 0; j < L; ++j) {
     u32 y[32];
@@ -376,119 +412,149 @@ __global__ void __launch_bounds__(1 << (LOGN - 5)) k_relin_keysw(RelinArgs a, Ba
       const u32 jj = NT::jC(tid, k);
       const uint4 kv0 = __ldg(reinterpret_cast<const uint4*>(k0 + jj));
       const uint4 kv1 = __ldg(reinterpret_cast<const uint4*>(k1 + jj));
-      acc0[k] = addmod(acc0[k], mul_shoup(y[k], kv0.x, kv0.y, q), q);
-      acc0[k + 1] = addmod(acc0[k + 1], mul_shoup(y[k + 1], kv0.z, kv0.w, q), q);
-      acc1[k] = addmod(acc1[k], mul_shoup(y[k], kv1.x, kv1.y, q), q);
-      acc1[k + 1] = addmod(acc1[k + 1], mul_shoup(y[k + 1], kv1.z, kv1.w, q), q);
+      const u32 p00 = mul_shoup(y[k], kv0.x, kv0.y, q), p01 = mul_shoup(y[k + 1], kv0.z, kv0.w, q);
+      const u32 p10 = mul_shoup(y[k], kv1.x, kv1.y, q), p11 = mul_shoup(y[k + 1], kv1.z, kv1.w, q);
+      if (j == 0) {
+        acc0[k * T + tid] = p00;
+        acc0[(k + 1) * T + tid] = p01;
+        acc1[k * T + tid] = p10;
+        acc1[(k + 1) * T + tid] = p11;
+      } else {
+        acc0[k * T + tid] = addmod(acc0[k * T + tid], p00, q);
+        acc0[(k + 1) * T + tid] = addmod(acc0[(k + 1) * T + tid], p01, q);
+        acc1[k * T + tid] = addmod(acc1[k * T + tid], p10, q);
+        acc1[(k + 1) * T + tid] = addmod(acc1[(k + 1) * T + tid], p11, q);
+      }
     }
   }
   if (!special) {
-    NT::gstore_C(acc0, a.ACC + ((ct * 2 + 0) * L + t) * N, tid);
-    NT::gstore_C(acc1, a.ACC + ((ct * 2 + 1) * L + t) * N, tid);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const u32* acc = c ? acc1 : acc0;
+      u32* dst = a.ACC + ((ct * 2 + c) * L + t) * N;
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) {
+        *reinterpret_cast<uint4*>(dst + NT::jC(tid, k)) =
+            make_uint4(acc[k * T + tid], acc[(k + 1) * T + tid], acc[(k + 2) * T + tid], acc[(k + 3) * T + tid]);
+      }
+    }
   } else {
-    NT::inverse(acc0, sm, tid, P);
-    i32* c0 = a.CORR + (ct * 2 + 0) * N;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      const u32* acc = c ? acc1 : acc0;
+      u32 y[32];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) c0[NT::jA(tid, k)] = centered_round_rem(acc0[k], P);
-    NT::inverse(acc1, sm, tid, P);
-    i32* c1 = a.CORR + (ct * 2 + 1) * N;
+      for (int k = 0; k < 32; ++k) y[k] = acc[k * T + tid];
+      NT::inverse(y, sm, tid, P);
+      i32* cd = a.CORR + (ct * 2 + c) * N;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) c1[NT::jA(tid, k)] = centered_round_rem(acc1[k], P);
+      for (int k = 0; k < 32; ++k) cd[NT::jA(tid, k)] = centered_round_rem(y[k], P);
+    }
   }
 }
 
-// d0 = c0 (mode 0) or a0*b0; d1 = c1 (mode 0) or a0*b1 + a1*b0 (henet/ckks.hpp:407-437)
-template <int LOGN>
-__device__ __forceinline__ void load_d(u32 (&d)[32], const RelinArgs& a, u64 ct, u32 poly, u32 i,
-                                       const DevPrime& P, u32 tid) {
-  using NT = Ntt<LOGN>;
-  constexpr int N = NT::N;
+// d0 = c0 (mode 0) or a0*b0; d1 = c1 (mode 0) or a0*b1 + a1*b0 (henet/ckks.hpp:407-437), four
+// consecutive coefficients j..j+3 of limb i.
+__device__ __forceinline__ uint4 load_d4(const RelinArgs& a, u64 ct, u32 poly, u32 i, u32 j, u32 N,
+                                         const DevPrime& P) {
   const u32 L = a.level;
-  if (a.mode == 0) {
-    NT::gload_C(d, a.A + ((ct * 3 + poly) * L + i) * N, tid);
-    return;
-  }
-  u32 x[32], y[32];
-  NT::gload_C(x, a.A + ((ct * 2 + 0) * L + i) * N, tid);
-  NT::gload_C(y, a.Bm + ((ct * 2 + poly) * L + i) * N, tid);
-#pragma unroll
-  for (int k = 0; k < 32; ++k) d[k] = mulmod(x[k], y[k], P);
+  auto ld = [&](const u32* base, u32 polys, u32 p) {
+    return __ldg(reinterpret_cast<const uint4*>(base + ((ct * polys + p) * L + i) * static_cast<u64>(N) + j));
+  };
+  if (a.mode == 0) return ld(a.A, 3, poly);
+  const uint4 x = ld(a.A, 2, 0), y = ld(a.Bm, 2, poly);
+  uint4 d = make_uint4(mulmod(x.x, y.x, P), mulmod(x.y, y.y, P), mulmod(x.z, y.z, P), mulmod(x.w, y.w, P));
   if (poly == 1) {
-    NT::gload_C(x, a.A + ((ct * 2 + 1) * L + i) * N, tid);
-    NT::gload_C(y, a.Bm + ((ct * 2 + 0) * L + i) * N, tid);
-#pragma unroll
-    for (int k = 0; k < 32; ++k) d[k] = addmod(d[k], mulmod(x[k], y[k], P), P.q);
+    const uint4 u = ld(a.A, 2, 1), v = ld(a.Bm, 2, 0);
+    d.x = addmod(d.x, mulmod(u.x, v.x, P), P.q);
+    d.y = addmod(d.y, mulmod(u.y, v.y, P), P.q);
+    d.z = addmod(d.z, mulmod(u.z, v.z, P), P.q);
+    d.w = addmod(d.w, mulmod(u.w, v.w, P), P.q);
   }
+  return d;
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(1 << (LOGN - 5)) k_relin_moddown(RelinArgs a, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 2 : 1)) k_relin_moddown(RelinArgs a, Basis B) {
   using NT = Ntt<LOGN>;
   constexpr int N = NT::N;
+  constexpr int T = NT::T;
   extern __shared__ u32 sm[];
+  i32* cps = reinterpret_cast<i32*>(sm + NT::SMEM_WORDS);  // special-prime correction, slots [k * T + tid]
+  i32* crs = cps + N;                                       // rescale correction
   const u32 tid = threadIdx.x;
   const u32 L = a.level;
   const u64 ct = blockIdx.x >> 1;
   const u32 poly = blockIdx.x & 1;
   const u32 Lout = a.rescale ? L - 1 : L;
   u32* dst = a.out + (ct * 2 + poly) * static_cast<u64>(Lout) * N;
-
-  i32 cp[32];
+  const u32* accp = a.ACC + (ct * 2 + poly) * static_cast<u64>(L) * N;
   {
     const i32* cs = a.CORR + (ct * 2 + poly) * N;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) cp[k] = cs[NT::jA(tid, k)];
+    for (int k = 0; k < 32; ++k) cps[k * T + tid] = cs[NT::jA(tid, k)];
   }
-  i32 crs[32];
-  u32 z[32], d[32], v[32];
-  // top limb first: needed by the rescale correction
+  u32 z[32];
+  // top limb first: its mod-down result feeds the rescale correction
   {
     const u32 i = L - 1;
     const DevPrime& Pi = B.p[i];
-    const u32 q = Pi.q;
+    const u32 q = Pi.q, pv = a.pinvP[i], ps = a.pinvP_sh[i];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) z[k] = signed_residue(cp[k], Pi);
+    for (int k = 0; k < 32; ++k) z[k] = signed_residue(cps[k * T + tid], Pi);
     NT::forward(z, sm, tid, Pi);
-    load_d<LOGN>(d, a, ct, poly, i, Pi, tid);
-    NT::gload_C(v, a.ACC + ((ct * 2 + poly) * L + i) * N, tid);
 #pragma unroll
-    for (int k = 0; k < 32; ++k)
-      z[k] = addmod(d[k], mul_shoup(v[k] + q - z[k], a.pinvP[i], a.pinvP_sh[i], q), q);
+    for (int k = 0; k < 32; k += 4) {
+      const u32 j = NT::jC(tid, k);
+      const uint4 d = load_d4(a, ct, poly, i, j, N, Pi);
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(accp + static_cast<u64>(i) * N + j));
+      z[k] = addmod(d.x, mul_shoup(v.x + q - z[k], pv, ps, q), q);
+      z[k + 1] = addmod(d.y, mul_shoup(v.y + q - z[k + 1], pv, ps, q), q);
+      z[k + 2] = addmod(d.z, mul_shoup(v.z + q - z[k + 2], pv, ps, q), q);
+      z[k + 3] = addmod(d.w, mul_shoup(v.w + q - z[k + 3], pv, ps, q), q);
+    }
     if (!a.rescale) {
       NT::gstore_C(z, dst + static_cast<u64>(i) * N, tid);
     } else {
       NT::inverse(z, sm, tid, Pi);
 #pragma unroll
-      for (int k = 0; k < 32; ++k) crs[k] = centered_round_rem(z[k], Pi);
+      for (int k = 0; k < 32; ++k) crs[k * T + tid] = centered_round_rem(z[k], Pi);
     }
   }
   for (u32 i = 0; i + 1 < L; ++i) {
     const DevPrime& Pi = B.p[i];
-    const u32 q = Pi.q;
+    const u32 q = Pi.q, pv = a.pinvP[i], ps = a.pinvP_sh[i];
     if (a.rescale) {
 #pragma unroll
       for (int k = 0; k < 32; ++k)
-        z[k] = addmod(mul_shoup(signed_residue(cp[k], Pi), a.pinvP[i], a.pinvP_sh[i], q),
-                      signed_residue(crs[k], Pi), q);
+        z[k] = addmod(mul_shoup(signed_residue(cps[k * T + tid], Pi), pv, ps, q),
+                      signed_residue(crs[k * T + tid], Pi), q);
     } else {
 #pragma unroll
-      for (int k = 0; k < 32; ++k) z[k] = signed_residue(cp[k], Pi);
+      for (int k = 0; k < 32; ++k) z[k] = signed_residue(cps[k * T + tid], Pi);
     }
     NT::forward(z, sm, tid, Pi);
-    load_d<LOGN>(d, a, ct, poly, i, Pi, tid);
-    NT::gload_C(v, a.ACC + ((ct * 2 + poly) * L + i) * N, tid);
-    if (a.rescale) {
+    const u32 lv = a.pinvL[i], ls = a.pinvL_sh[i];
+    u32* out_i = dst + static_cast<u64>(i) * N;
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const u32 u = addmod(d[k], mul_shoup(v[k], a.pinvP[i], a.pinvP_sh[i], q), q);
-        z[k] = mul_shoup(u + q - z[k], a.pinvL[i], a.pinvL_sh[i], q);
+    for (int k = 0; k < 32; k += 4) {
+      const u32 j = NT::jC(tid, k);
+      const uint4 d = load_d4(a, ct, poly, i, j, N, Pi);
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(accp + static_cast<u64>(i) * N + j));
+      uint4 o;
+      if (a.rescale) {
+        o.x = mul_shoup(addmod(d.x, mul_shoup(v.x, pv, ps, q), q) + q - z[k], lv, ls, q);
+        o.y = mul_shoup(addmod(d.y, mul_shoup(v.y, pv, ps, q), q) + q - z[k + 1], lv, ls, q);
+        o.z = mul_shoup(addmod(d.z, mul_shoup(v.z, pv, ps, q), q) + q - z[k + 2], lv, ls, q);
+        o.w = mul_shoup(addmod(d.w, mul_shoup(v.w, pv, ps, q), q) + q - z[k + 3], lv, ls, q);
+      } else {
+        o.x = addmod(d.x, mul_shoup(v.x + q - z[k], pv, ps, q), q);
+        o.y = addmod(d.y, mul_shoup(v.y + q - z[k + 1], pv, ps, q), q);
+        o.z = addmod(d.z, mul_shoup(v.z + q - z[k + 2], pv, ps, q), q);
+        o.w = addmod(d.w, mul_shoup(v.w + q - z[k + 3], pv, ps, q), q);
       }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 32; ++k)
-        z[k] = addmod(d[k], mul_shoup(v[k] + q - z[k], a.pinvP[i], a.pinvP_sh[i], q), q);
+      *reinterpret_cast<uint4*>(out_i + j) = o;
     }
-    NT::gstore_C(z, dst + static_cast<u64>(i) * N, tid);
   }
 }
 
@@ -855,7 +921,7 @@ static void set_smem(K kernel, size_t bytes) {
 int launch_ntt(int logn, u32* data, u64 rows, u32 level, bool inverse, const Basis& B, cudaStream_t s) {
   if (rows == 0) return 0;
   HG_LOGN_SWITCH(logn, {
-    const size_t sm = sizeof(u32) << LN;
+    const size_t sm = sizeof(u32) * Ntt<LN>::SMEM_WORDS;
     if (inverse) {
       set_smem(k_ntt<LN, true>, sm);
       ProfScope ps("k_intt", s);
@@ -872,7 +938,7 @@ int launch_ntt(int logn, u32* data, u64 rows, u32 level, bool inverse, const Bas
 int launch_rescale(int logn, const RescaleArgs& a, const Basis& B, cudaStream_t s) {
   if (a.rows == 0) return 0;
   HG_LOGN_SWITCH(logn, {
-    const size_t sm = sizeof(u32) << LN;
+    const size_t sm = sizeof(u32) * (Ntt<LN>::SMEM_WORDS + Ntt<LN>::N);
     set_smem(k_rescale<LN>, sm);
     ProfScope ps("k_rescale", s);
     k_rescale<LN><<<a.rows, 1 << (LN - 5), sm, s>>>(a, B);
@@ -880,39 +946,62 @@ int launch_rescale(int logn, const RescaleArgs& a, const Basis& B, cudaStream_t 
   return 1;
 }
 
+u32 mac_dense_warps(u32 M) { return std::min<u32>(kMaxWarps, (M + kTM - 1) / kTM); }
+
 int launch_mac_dense(const MacDenseArgs& a, const Basis& B, cudaStream_t s) {
-  const u32 warps = std::min<u32>(8, (a.M + kTM - 1) / kTM);
+  const u32 warps = mac_dense_warps(a.M);
   const u32 BM = warps * kTM;
+  if (a.Mpad % BM != 0 || a.N % kBN != 0) return -1;
   dim3 grid(a.N / kBN, (a.M + BM - 1) / BM, a.polys * a.level);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mac_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDenseSmem));
+    attr = true;
+  }
   ProfScope ps("k_mac_dense", s);
-  k_mac_dense<<<grid, warps * 32, 0, s>>>(a, B);
+  k_mac_dense<<<grid, warps * 32, kDenseSmem, s>>>(a, B);
   return 1;
 }
 
+template <int FT>
+static void conv_launch(const MacConvArgs& a, const Basis& B, cudaStream_t s) {
+  const u32 nchunks = (a.F + FT - 1) / FT;
+  dim3 grid(a.N / (4 * kConvThreads), a.OH * a.OW, a.polys * a.level * nchunks);
+  k_mac_conv<FT><<<grid, kConvThreads, 0, s>>>(a, B);
+}
+
 int launch_mac_conv(const MacConvArgs& a, const Basis& B, cudaStream_t s) {
-  if (a.C * a.win * a.win > static_cast<u32>(kMaxTaps)) return -1;
-  dim3 grid(a.N / (4 * 128), a.OH * a.OW, a.polys * a.level);
+  if (a.C * a.win * a.win > static_cast<u32>(kMaxTaps) || a.N % (4 * kConvThreads) != 0) return -1;
   ProfScope ps("k_mac_conv", s);
-  k_mac_conv<<<grid, 128, 0, s>>>(a, B);
+  switch (a.F) {
+    case 1: conv_launch<1>(a, B, s); break;
+    case 2: conv_launch<2>(a, B, s); break;
+    case 3: conv_launch<3>(a, B, s); break;
+    case 4: conv_launch<4>(a, B, s); break;
+    case 5: conv_launch<5>(a, B, s); break;
+    case 6: conv_launch<6>(a, B, s); break;
+    case 7: conv_launch<7>(a, B, s); break;
+    default: conv_launch<8>(a, B, s); break;
+  }
   return 1;
 }
 
 int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s) {
   if (a.count == 0) return 0;
   HG_LOGN_SWITCH(logn, {
-    const size_t sm = sizeof(u32) << LN;
+    const size_t sm1 = sizeof(u32) * Ntt<LN>::SMEM_WORDS, sm3 = sm1 + 2 * (sizeof(u32) << LN);
     const int T = 1 << (LN - 5);
-    set_smem(k_relin_digits<LN>, sm);
-    set_smem(k_relin_keysw<LN>, sm);
-    set_smem(k_relin_moddown<LN>, sm);
+    set_smem(k_relin_digits<LN>, sm1);
+    set_smem(k_relin_keysw<LN>, sm3);
+    set_smem(k_relin_moddown<LN>, sm3);
     { ProfScope ps("k_relin_digits", s);
-    k_relin_digits<LN><<<a.count * a.level, T, sm, s>>>(a, B);
+    k_relin_digits<LN><<<a.count * a.level, T, sm1, s>>>(a, B);
     }
     { ProfScope ps("k_relin_keysw", s);
-    k_relin_keysw<LN><<<a.count * (a.level + 1), T, sm, s>>>(a, B);
+    k_relin_keysw<LN><<<a.count * (a.level + 1), T, sm3, s>>>(a, B);
     }
     { ProfScope ps("k_relin_moddown", s);
-    k_relin_moddown<LN><<<a.count * 2, T, sm, s>>>(a, B);
+    k_relin_moddown<LN><<<a.count * 2, T, sm3, s>>>(a, B);
     }
   });
   return 3;

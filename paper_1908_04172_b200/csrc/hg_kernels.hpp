@@ -78,6 +78,8 @@ struct EwArgs {
 int launch_ntt(int logn, u32* data, u64 rows, u32 level, bool inverse, const Basis& B,
                cudaStream_t s);
 int launch_rescale(int logn, const RescaleArgs& a, const Basis& B, cudaStream_t s);
+// warps per CTA of the dense kernel for M outputs (BM = 4 * warps; Mpad must be a multiple of BM)
+u32 mac_dense_warps(u32 M);
 int launch_mac_dense(const MacDenseArgs& a, const Basis& B, cudaStream_t s);
 int launch_mac_conv(const MacConvArgs& a, const Basis& B, cudaStream_t s);
 int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s);
