@@ -12,6 +12,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhenet_b200.so")
+# Kernel-variant experiments (scripts/) may point at another build of the same library.
+LIB_PATH = os.environ.get("HENET_B200_LIB", LIB_PATH)
 
 HG_OK, HG_ERR_VALIDATION, HG_ERR_CUDA, HG_ERR_UNSUPPORTED, HG_ERR_ALLOC, HG_ERR_INTERNAL = range(6)
 

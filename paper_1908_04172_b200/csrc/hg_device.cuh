@@ -26,6 +26,13 @@ using i32 = int32_t;
 
 constexpr int kMaxPrimes = 24;
 
+#ifndef HG_TW_MODE
+#define HG_TW_MODE 0  // 0: a pass's twiddle row is preloaded (16 x 128-bit); 1: loaded per use
+#endif
+#ifndef HG_NTT_MINB
+#define HG_NTT_MINB 2  // CTAs per SM the NTT kernels are register-budgeted for (N <= 2^13)
+#endif
+
 // Per-basis-modulus constants.  Passed by value (kernel parameter space).
 struct DevPrime {
   u32 q;
@@ -197,12 +204,21 @@ struct Ntt {
 
   // Forward (Cooley-Tukey, Harvey lazy) stages of pass L.  Values in [0, 4q).
   template <int L>
+  __device__ static __forceinline__ const uint2* row_ptr(const uint2* base, u32 tid) {
+    return base + static_cast<size_t>(L == 1 ? (tid >> CB) : tid) * 32;
+  }
+
+  template <int L>
   __device__ static __forceinline__ void fwd_pass(u32 (&x)[32], u32 tid, const DevPrime& P) {
     constexpr int NB = PassShape<L>::NB;
     constexpr int BLO = PassShape<L>::BLO;
     const u32 q = P.q, q2 = P.two_q;
+#if HG_TW_MODE == 0
     uint4 tw[16];
     if (L != 0) load_row<L>(tw, L == 1 ? P.fwdB : P.fwdC, tid);
+#else
+    const uint2* trow = L != 0 ? row_ptr<L>(L == 1 ? P.fwdB : P.fwdC, tid) : nullptr;
+#endif
     int n = 0;
 #pragma unroll
     for (int s = 0; s < NB; ++s) {
@@ -213,7 +229,11 @@ struct Ntt {
 #pragma unroll
         for (int hi = 0; hi < (1 << (NB - 1 - rb)); ++hi) {
           const u32 kh = (static_cast<u32>(g) << NB) | (static_cast<u32>(hi) << (rb + 1));
+#if HG_TW_MODE == 0
           const uint2 w = (L == 0) ? P.twA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))] : slot(tw, n);
+#else
+          const uint2 w = (L == 0) ? P.twA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))] : __ldg(trow + n);
+#endif
           ++n;
 #pragma unroll
           for (int lo = 0; lo < (1 << rb); ++lo) {
@@ -237,8 +257,12 @@ struct Ntt {
     constexpr int NB = PassShape<L>::NB;
     constexpr int BLO = PassShape<L>::BLO;
     const u32 q = P.q, q2 = P.two_q;
+#if HG_TW_MODE == 0
     uint4 tw[16];
     if (L != 0) load_row<L>(tw, L == 1 ? P.invB : P.invC, tid);
+#else
+    const uint2* trow = L != 0 ? row_ptr<L>(L == 1 ? P.invB : P.invC, tid) : nullptr;
+#endif
     int n = 0;
 #pragma unroll
     for (int s = 0; s < NB; ++s) {
@@ -259,7 +283,11 @@ struct Ntt {
               x[k1] = mul_shoup_lazy(U - V + q2, P.w1n, P.w1n_sh, q);
             }
           } else {
+#if HG_TW_MODE == 0
             const uint2 w = (L == 0) ? P.itwA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))] : slot(tw, n);
+#else
+            const uint2 w = (L == 0) ? P.itwA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))] : __ldg(trow + n);
+#endif
             ++n;
 #pragma unroll
             for (int lo = 0; lo < (1 << rb); ++lo) {

@@ -96,8 +96,9 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
     const u64 q = ctx->basis_mod(i);
     require(q >= 2, "modulus must be at least 2");
     require(nt::is_prime(q), "modulus must be prime");
-    if (q >= (1ull << 30))
-      throw Error(HG_ERR_UNSUPPORTED, "B200 kernels implement primes below 2^30 (got " + std::to_string(q) + ")");
+    if (q >= (1ull << 50))
+      throw Error(HG_ERR_UNSUPPORTED, "B200 kernels implement primes below 2^50 (got " + std::to_string(q) + ")");
+    if (q >= (1ull << 30)) ctx->wide = true;
     for (u32 j = 0; j < i; ++j) {
       if (ctx->basis_mod(j) == q) {
         throw Error(HG_ERR_VALIDATION, i == chain_len ? "special prime must differ from the chain"
@@ -197,6 +198,46 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
     stage_rows(1, true, g, base + (rowsB + rowsC) * 32);
     stage_rows(2, true, g, base + (2 * rowsB + rowsC) * 32);
   }
+  if (ctx->wide) {
+    // u64 path: natural-order tables with 64-bit Shoup companions (hg_wide.cuh)
+    std::vector<ulonglong2> tw(static_cast<size_t>(full) * 2 * n);
+    for (u32 i = 0; i < full; ++i) {
+      const u64 q = ctx->basis_mod(i);
+      const u64 psi = ctx->roots[i], psi_inv = nt::inv(psi, q);
+      auto sh64 = [&](u64 w) { return static_cast<u64>((static_cast<nt::u128>(w) << 64) / q); };
+      ulonglong2* fw = &tw[static_cast<size_t>(i) * 2 * n];
+      ulonglong2* iw = fw + n;
+      for (u32 k = 0; k < n; ++k) {
+        const u32 rev = nt::bit_reverse(k, logn);
+        const u64 w = nt::powmod(psi, rev, q), wi = nt::powmod(psi_inv, rev, q);
+        fw[k] = make_ulonglong2(w, sh64(w));
+        iw[k] = make_ulonglong2(wi, sh64(wi));
+      }
+      DevPrimeW& W = ctx->basisw.p[i];
+      W.q = q;
+      W.two_q = 2 * q;
+      W.half = q >> 1;
+      const u64 d1 = static_cast<u64>((static_cast<nt::u128>(1) << 64) / q);
+      const u64 r1 = static_cast<u64>((static_cast<nt::u128>(1) << 64) % q);
+      W.r128_hi = d1;
+      W.r128_lo = static_cast<u64>((static_cast<nt::u128>(r1) << 64) / q);
+      const u64 ninv = nt::inv(n % q, q);
+      W.ninv = ninv;
+      W.ninv_sh = sh64(ninv);
+      W.w1n = nt::mulmod(iw[1].x, ninv, q);
+      W.w1n_sh = sh64(W.w1n);
+      W.t64 = r1;
+    }
+    ctx->wide_tables = ctx->alloc(tw.size() * sizeof(ulonglong2), nullptr);
+    cuda_check(cudaMemcpyAsync(ctx->wide_tables->ptr, tw.data(), tw.size() * sizeof(ulonglong2),
+                               cudaMemcpyHostToDevice, ctx->core->stream),
+               "upload wide tables");
+    for (u32 i = 0; i < full; ++i) {
+      const ulonglong2* base = static_cast<const ulonglong2*>(ctx->wide_tables->ptr) + static_cast<size_t>(i) * 2 * n;
+      ctx->basisw.p[i].fwd = base;
+      ctx->basisw.p[i].inv = base + n;
+    }
+  }
   ctx->tables = ctx->alloc(staged.size() * sizeof(uint2), nullptr);
   cuda_check(cudaMemcpyAsync(ctx->tables->ptr, staged.data(), staged.size() * sizeof(uint2), cudaMemcpyHostToDevice,
                              ctx->core->stream),
@@ -243,7 +284,7 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
 static u32 inv_mod_u32(u64 a, u64 q) { return static_cast<u32>(nt::inv(a % q, q)); }
 
 static void ensure(const Context& ctx, CtBatch& b, u64 count, u32 polys, u32 level, cudaStream_t s) {
-  const u64 need = count * polys * level * static_cast<u64>(ctx.n) * sizeof(u32);
+  const u64 need = count * polys * level * static_cast<u64>(ctx.n) * ctx.word_bytes();
   if (!b.buf || b.buf->bytes < need || b.buf.use_count() > 1) b.buf = ctx.alloc(need, s);
   b.count = count;
   b.polys = polys;
@@ -274,9 +315,37 @@ static void check_cc_mul(const CtBatch& a) {
 static void run_ew(const Context& ctx, EwArgs a, cudaStream_t s) {
   a.N = ctx.n;
   if (a.pt_div == 0) a.pt_div = 1;
-  const int r = launch_elementwise(a, ctx.basis, s);
+  int r;
+  if (ctx.wide) {
+    // same argument block, u64 residues (the pointers address u64 buffers in wide mode)
+    EwArgsW w{};
+    w.op = a.op;
+    w.a = reinterpret_cast<const u64*>(a.a);
+    w.b = reinterpret_cast<const u64*>(a.b);
+    w.res = reinterpret_cast<const u64*>(a.res);
+    w.per_element = a.per_element;
+    w.pt_div = a.pt_div;
+    w.out = reinterpret_cast<u64*>(a.out);
+    w.count = a.count;
+    w.polys_a = a.polys_a;
+    w.polys_out = a.polys_out;
+    w.level = a.level;
+    w.N = a.N;
+    r = launch_elementwise_w(w, ctx.basisw, s);
+  } else {
+    r = launch_elementwise(a, ctx.basis, s);
+  }
   check_launch(r, "elementwise");
   ctx.count(r);
+}
+
+// Encoded-residue buffers hold u32 or u64 words depending on the context mode.
+static int encode_f32(const Context& ctx, const float* vals, u64 count, u32 row_len, u32 row_stride, u64 limb_stride,
+                      u32 level, double scale, void* out, cudaStream_t s) {
+  return ctx.wide ? launch_encode_scalars_w_f32(vals, count, row_len, row_stride, limb_stride, level, scale,
+                                                static_cast<u64*>(out), ctx.basisw, s)
+                  : launch_encode_scalars_f32(vals, count, row_len, row_stride, limb_stride, level, scale,
+                                              static_cast<u32*>(out), ctx.basis, s);
 }
 
 // rescale_next applied (level - target) times; henet/ckks.hpp:504-519.
@@ -290,18 +359,35 @@ static CtBatch do_rescale(const Context& ctx, const CtBatch& in, u32 target, cud
     out.packing = cur.packing;
     out.shape = cur.shape;
     ensure(ctx, out, cur.count, cur.polys, L - 1, s);
-    RescaleArgs a{};
-    a.in = cur.data();
-    a.out = out.data();
-    a.rows = cur.count * cur.polys;
-    a.level = L;
     const u64 p = ctx.chain[L - 1];
-    for (u32 i = 0; i + 1 < L; ++i) {
-      const u64 q = ctx.chain[i];
-      a.pinv[i] = inv_mod_u32(p, q);
-      a.pinv_sh[i] = nt::shoup(a.pinv[i], q);
+    int r;
+    if (ctx.wide) {
+      if (p >= (1ull << 32))
+        throw Error(HG_ERR_UNSUPPORTED, "rescale by a prime >= 2^32 is not implemented on the B200 path");
+      RescaleArgsW a{};
+      a.in = cur.data64();
+      a.out = out.data64();
+      a.rows = cur.count * cur.polys;
+      a.level = L;
+      for (u32 i = 0; i + 1 < L; ++i) {
+        const u64 q = ctx.chain[i];
+        a.pinv[i] = nt::inv(p % q, q);
+        a.pinv_sh[i] = static_cast<u64>((static_cast<nt::u128>(a.pinv[i]) << 64) / q);
+      }
+      r = launch_rescale_w(static_cast<int>(ctx.logn), a, ctx.basisw, s);
+    } else {
+      RescaleArgs a{};
+      a.in = cur.data();
+      a.out = out.data();
+      a.rows = cur.count * cur.polys;
+      a.level = L;
+      for (u32 i = 0; i + 1 < L; ++i) {
+        const u64 q = ctx.chain[i];
+        a.pinv[i] = inv_mod_u32(p, q);
+        a.pinv_sh[i] = nt::shoup(a.pinv[i], q);
+      }
+      r = launch_rescale(static_cast<int>(ctx.logn), a, ctx.basis, s);
     }
-    const int r = launch_rescale(static_cast<int>(ctx.logn), a, ctx.basis, s);
     check_launch(r, "rescale");
     ctx.count(r);
     out.scale = cur.scale / static_cast<double>(p);
@@ -315,6 +401,8 @@ static CtBatch do_relin(const Context& ctx, const RelinKeyDev& rk, const CtBatch
                         bool rescale, cudaStream_t s) {
   require(ctx.has_special, "relinearization needs a special prime");
   require(rk.chain_len == ctx.chain_len(), "relinearization key has the wrong basis");
+  if (ctx.wide)
+    throw Error(HG_ERR_UNSUPPORTED, "relinearization with primes >= 2^30 is not implemented on the B200 path yet");
   const u32 L = a->level;
   const u32 n = ctx.n;
   if (rescale) require(L >= 2, "cannot rescale below level 1");
@@ -385,19 +473,31 @@ static BufPtr encode_vectors_dev(const Context& ctx, const double* d_slots, u32 
   require(scale > 0.0, "scale must be positive");
   require(n_slots <= ctx.n / 2, "more slots than the parameters provide");
   const u32 n = ctx.n;
-  BufPtr out = ctx.alloc(count * level * static_cast<u64>(n) * 4, s);
+  BufPtr out = ctx.alloc(count * level * static_cast<u64>(n) * ctx.word_bytes(), s);
   BufPtr scratch = ctx.alloc(count * static_cast<u64>(n) * sizeof(double2), s);
+  BufPtr mags = ctx.alloc(count * static_cast<u64>(n) * sizeof(ulonglong2), s);
   BufPtr mm = ctx.alloc(count * (sizeof(unsigned long long) + sizeof(int)), s);
   auto* d_mant = static_cast<unsigned long long*>(mm->ptr);
   auto* d_exp = reinterpret_cast<int*>(d_mant + count);
   const double2* roots = static_cast<const double2*>(ctx.fft_tables->ptr);
   const double2* twist = roots + n / 2;
-  int r = launch_fft_encode(d_slots, n_slots, count, n, level, scale, roots, twist,
-                            static_cast<double2*>(scratch->ptr), static_cast<u32*>(out->ptr), d_mant, d_exp,
-                            ctx.basis, s);
+  int r = launch_fft_encode(d_slots, n_slots, count, n, level, scale, roots, twist, static_cast<double2*>(scratch->ptr),
+                            static_cast<ulonglong2*>(mags->ptr), d_mant, d_exp, s);
   check_launch(r, "fft encode");
   ctx.count(r);
-  r = launch_ntt(static_cast<int>(ctx.logn), static_cast<u32*>(out->ptr), count * level, level, false, ctx.basis, s);
+  if (ctx.wide) {
+    r = launch_mags_to_residues_w(static_cast<const ulonglong2*>(mags->ptr), count, n, level,
+                                  static_cast<u64*>(out->ptr), ctx.basisw, s);
+    check_launch(r, "residues");
+    ctx.count(r);
+    r = launch_ntt_w(static_cast<int>(ctx.logn), static_cast<u64*>(out->ptr), count * level, level, false, ctx.basisw, s);
+  } else {
+    r = launch_mags_to_residues(static_cast<const ulonglong2*>(mags->ptr), count, n, level,
+                                static_cast<u32*>(out->ptr), ctx.basis, s);
+    check_launch(r, "residues");
+    ctx.count(r);
+    r = launch_ntt(static_cast<int>(ctx.logn), static_cast<u32*>(out->ptr), count * level, level, false, ctx.basis, s);
+  }
   check_launch(r, "ntt");
   ctx.count(r);
   mant.resize(count);
@@ -815,86 +915,123 @@ class Executor {
     BufPtr bias_res;
     BufPtr bias_pt;
 
+    const size_t wb = ctx.word_bytes();
     if (n.op == HG_OP_DOT) {
       const u32 K = w.dims[0], Mo = w.dims[1];
-      const u32 BM = mac_dense_warps(Mo) * 4;
+      const u32 BM = ctx.wide ? mac_dense_w_bm() : mac_dense_warps(Mo) * 4;
       const u32 Mpad = (Mo + BM - 1) / BM * BM;
-      BufPtr wres = ctx.alloc(static_cast<u64>(L) * K * Mpad * 4, s_);
-      cuda_check(cudaMemsetAsync(wres->ptr, 0, static_cast<u64>(L) * K * Mpad * 4, s_), "memset");
-      int r = launch_encode_scalars_f32(wd, w.data.size(), Mo, Mpad, static_cast<u64>(K) * Mpad, L, s,
-                                        static_cast<u32*>(wres->ptr), ctx.basis, s_);
+      BufPtr wres = ctx.alloc(static_cast<u64>(L) * K * Mpad * wb, s_);
+      cuda_check(cudaMemsetAsync(wres->ptr, 0, static_cast<u64>(L) * K * Mpad * wb, s_), "memset");
+      int r = encode_f32(ctx, wd, w.data.size(), Mo, Mpad, static_cast<u64>(K) * Mpad, L, s, wres->ptr, s_);
       check_launch(r, "encode weights");
       count(r);
       if (b && x.packing == HG_PACKING_REAL) {
         check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
         const float* bd = weight_dev(ctx, *b, s_);
-        bias_res = ctx.alloc(static_cast<u64>(L) * Mpad * 4, s_);
-        r = launch_encode_scalars_f32(bd, Mo, Mo, Mpad, Mpad, L, acc_scale, static_cast<u32*>(bias_res->ptr),
-                                      ctx.basis, s_);
+        bias_res = ctx.alloc(static_cast<u64>(L) * Mpad * wb, s_);
+        r = encode_f32(ctx, bd, Mo, Mo, Mpad, Mpad, L, acc_scale, bias_res->ptr, s_);
         check_launch(r, "encode bias");
         count(r);
       }
-      MacDenseArgs a{};
-      a.X = x.data();
-      a.Y = v.cipher.data();
-      a.W = static_cast<const u32*>(wres->ptr);
-      a.bias = bias_res ? static_cast<const u32*>(bias_res->ptr) : nullptr;
-      a.K = K;
-      a.M = Mo;
-      a.Mpad = Mpad;
-      a.N = N;
-      a.level = L;
-      a.polys = 2;
-      a.x_level = x.level;
-      for (u32 i = 0; i < L; ++i) {
-        const long double qm1 = static_cast<long double>(ctx.chain[i] - 1);
-        a.fold[i] = (qm1 * qm1 * K >= 18446744073709551616.0L) ? 1 : 0;
+      if (ctx.wide) {
+        MacDenseArgsW a{};
+        a.X = x.data64();
+        a.Y = v.cipher.data64();
+        a.W = static_cast<const u64*>(wres->ptr);
+        a.bias = bias_res ? static_cast<const u64*>(bias_res->ptr) : nullptr;
+        a.K = K;
+        a.M = Mo;
+        a.Mpad = Mpad;
+        a.N = N;
+        a.level = L;
+        a.polys = 2;
+        a.x_level = x.level;
+        r = launch_mac_dense_w(a, ctx.basisw, s_);
+      } else {
+        MacDenseArgs a{};
+        a.X = x.data();
+        a.Y = v.cipher.data();
+        a.W = static_cast<const u32*>(wres->ptr);
+        a.bias = bias_res ? static_cast<const u32*>(bias_res->ptr) : nullptr;
+        a.K = K;
+        a.M = Mo;
+        a.Mpad = Mpad;
+        a.N = N;
+        a.level = L;
+        a.polys = 2;
+        a.x_level = x.level;
+        for (u32 i = 0; i < L; ++i) {
+          const long double qm1 = static_cast<long double>(ctx.chain[i] - 1);
+          a.fold[i] = (qm1 * qm1 * K >= 18446744073709551616.0L) ? 1 : 0;
+        }
+        r = launch_mac_dense(a, ctx.basis, s_);
       }
-      r = launch_mac_dense(a, ctx.basis, s_);
       check_launch(r, "mac_dense");
       count(r);
     } else {
       const auto& in_shape = x.shape;
       require(in_shape.size() == 3, "Convolution expects a (C,H,W) input");
       const u32 F = n.attrs.filters, C = in_shape[0], win = n.attrs.window;
-      BufPtr wres = ctx.alloc(static_cast<u64>(L) * w.data.size() * 4, s_);
-      int r = launch_encode_scalars_f32(wd, w.data.size(), static_cast<u32>(w.data.size()),
-                                        static_cast<u32>(w.data.size()), w.data.size(), L, s,
-                                        static_cast<u32*>(wres->ptr), ctx.basis, s_);
+      BufPtr wres = ctx.alloc(static_cast<u64>(L) * w.data.size() * wb, s_);
+      int r = encode_f32(ctx, wd, w.data.size(), static_cast<u32>(w.data.size()), static_cast<u32>(w.data.size()),
+                         w.data.size(), L, s, wres->ptr, s_);
       check_launch(r, "encode weights");
       count(r);
       if (b && x.packing == HG_PACKING_REAL) {
         check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
         const float* bd = weight_dev(ctx, *b, s_);
-        bias_res = ctx.alloc(static_cast<u64>(L) * F * 4, s_);
-        r = launch_encode_scalars_f32(bd, F, F, F, F, L, acc_scale, static_cast<u32*>(bias_res->ptr), ctx.basis, s_);
+        bias_res = ctx.alloc(static_cast<u64>(L) * F * wb, s_);
+        r = encode_f32(ctx, bd, F, F, F, F, L, acc_scale, bias_res->ptr, s_);
         check_launch(r, "encode bias");
         count(r);
       }
-      MacConvArgs a{};
-      a.X = x.data();
-      a.Y = v.cipher.data();
-      a.W = static_cast<const u32*>(wres->ptr);
-      a.bias = bias_res ? static_cast<const u32*>(bias_res->ptr) : nullptr;
-      a.C = C;
-      a.IH = in_shape[1];
-      a.IW = in_shape[2];
-      a.F = F;
-      a.OH = out_shape[1];
-      a.OW = out_shape[2];
-      a.win = win;
-      a.stride = n.attrs.stride;
-      a.pad_top = n.attrs.pad[0];
-      a.pad_left = n.attrs.pad[1];
-      a.level = L;
-      a.polys = 2;
-      a.x_level = x.level;
-      a.N = N;
-      for (u32 i = 0; i < L; ++i) {
-        const long double qm1 = static_cast<long double>(ctx.chain[i] - 1);
-        a.fold[i] = (qm1 * qm1 * (C * win * win) >= 18446744073709551616.0L) ? 1 : 0;
+      if (ctx.wide) {
+        MacConvArgsW a{};
+        a.X = x.data64();
+        a.Y = v.cipher.data64();
+        a.W = static_cast<const u64*>(wres->ptr);
+        a.bias = bias_res ? static_cast<const u64*>(bias_res->ptr) : nullptr;
+        a.C = C;
+        a.IH = in_shape[1];
+        a.IW = in_shape[2];
+        a.F = F;
+        a.OH = out_shape[1];
+        a.OW = out_shape[2];
+        a.win = win;
+        a.stride = n.attrs.stride;
+        a.pad_top = n.attrs.pad[0];
+        a.pad_left = n.attrs.pad[1];
+        a.level = L;
+        a.polys = 2;
+        a.x_level = x.level;
+        a.N = N;
+        r = launch_mac_conv_w(a, ctx.basisw, s_);
+      } else {
+        MacConvArgs a{};
+        a.X = x.data();
+        a.Y = v.cipher.data();
+        a.W = static_cast<const u32*>(wres->ptr);
+        a.bias = bias_res ? static_cast<const u32*>(bias_res->ptr) : nullptr;
+        a.C = C;
+        a.IH = in_shape[1];
+        a.IW = in_shape[2];
+        a.F = F;
+        a.OH = out_shape[1];
+        a.OW = out_shape[2];
+        a.win = win;
+        a.stride = n.attrs.stride;
+        a.pad_top = n.attrs.pad[0];
+        a.pad_left = n.attrs.pad[1];
+        a.level = L;
+        a.polys = 2;
+        a.x_level = x.level;
+        a.N = N;
+        for (u32 i = 0; i < L; ++i) {
+          const long double qm1 = static_cast<long double>(ctx.chain[i] - 1);
+          a.fold[i] = (qm1 * qm1 * (C * win * win) >= 18446744073709551616.0L) ? 1 : 0;
+        }
+        r = launch_mac_conv(a, ctx.basis, s_);
       }
-      r = launch_mac_conv(a, ctx.basis, s_);
       check_launch(r, "mac_conv");
       count(r);
     }
@@ -1006,9 +1143,9 @@ class Executor {
       v.cipher.packing = x.packing;
       if (mul) {
         check_scalar_encodable(ctx, c.max_abs, L, s);
-        BufPtr res = ctx.alloc(static_cast<u64>(c.data.size()) * L * 4, s_);
+        BufPtr res = ctx.alloc(static_cast<u64>(c.data.size()) * L * ctx.word_bytes(), s_);
         // residues laid out [value][limb]
-        int r = launch_encode_scalars_f32(cd, c.data.size(), 1, L, 1, L, s, static_cast<u32*>(res->ptr), ctx.basis, s_);
+        int r = encode_f32(ctx, cd, c.data.size(), 1, L, 1, L, s, res->ptr, s_);
         check_launch(r, "encode");
         ctx.count(r);
         v.cipher.scale = x.scale * s;
@@ -1042,9 +1179,8 @@ class Executor {
         BufPtr res;
         if (model_.packing == HG_PACKING_REAL) {
           check_scalar_encodable(ctx, c.max_abs, L, x.scale);
-          res = ctx.alloc(static_cast<u64>(c.data.size()) * L * 4, s_);
-          int r = launch_encode_scalars_f32(cd, c.data.size(), 1, L, 1, L, x.scale, static_cast<u32*>(res->ptr),
-                                            ctx.basis, s_);
+          res = ctx.alloc(static_cast<u64>(c.data.size()) * L * ctx.word_bytes(), s_);
+          int r = encode_f32(ctx, cd, c.data.size(), 1, L, 1, L, x.scale, res->ptr, s_);
           check_launch(r, "encode");
           ctx.count(r);
           e.op = EwOp::AddScalar;
@@ -1095,7 +1231,7 @@ class Executor {
       g.packing = x.packing;
       g.scale = x.scale;
       ensure(ctx, g, static_cast<u64>(C) * oh * ow * window, 2, x.level, s_);
-      const u64 ct_words = 2ull * x.level * ctx.n;
+      const u64 ct_bytes = 2ull * x.level * ctx.n * ctx.word_bytes();
       u64 o = 0;
       for (u32 c = 0; c < C; ++c)
         for (u32 y = 0; y < oh; ++y)
@@ -1103,7 +1239,8 @@ class Executor {
             for (u32 ky = 0; ky < win; ++ky)
               for (u32 kx = 0; kx < win; ++kx) {
                 const u64 idx = (static_cast<u64>(c) * ihh + (y * stride + ky)) * iww + (xo * stride + kx);
-                cuda_check(cudaMemcpyAsync(g.data() + o * ct_words, x.data() + idx * ct_words, ct_words * 4,
+                cuda_check(cudaMemcpyAsync(static_cast<char*>(g.buf->ptr) + o * ct_bytes,
+                                           static_cast<const char*>(x.buf->ptr) + idx * ct_bytes, ct_bytes,
                                            cudaMemcpyDeviceToDevice, s_),
                            "gather");
                 ++o;
@@ -1234,11 +1371,17 @@ int hg_tensor_upload(hg_tensor* t, const uint64_t* words, void* stream) {
     const Context& ctx = *t->ctx;
     cudaStream_t s = ctx.pick(stream);
     const u64 n = t->b.words(ctx.n);
-    BufPtr stage = ctx.alloc(n * 8 + sizeof(int), s);
-    int* bad = reinterpret_cast<int*>(static_cast<char*>(stage->ptr) + n * 8);
+    int r;
+    BufPtr stage = ctx.alloc((ctx.wide ? 0 : n * 8) + sizeof(int), s);
+    int* bad = reinterpret_cast<int*>(static_cast<char*>(stage->ptr) + (ctx.wide ? 0 : n * 8));
     cuda_check(cudaMemsetAsync(bad, 0, sizeof(int), s), "memset");
-    cuda_check(cudaMemcpyAsync(stage->ptr, words, n * 8, cudaMemcpyHostToDevice, s), "h2d");
-    const int r = launch_narrow(static_cast<const u64*>(stage->ptr), t->b.data(), n, t->b.level, ctx.n, ctx.basis, bad, s);
+    if (ctx.wide) {
+      cuda_check(cudaMemcpyAsync(t->b.data64(), words, n * 8, cudaMemcpyHostToDevice, s), "h2d");
+      r = launch_validate_w(t->b.data64(), n, t->b.level, ctx.n, ctx.basisw, bad, s);
+    } else {
+      cuda_check(cudaMemcpyAsync(stage->ptr, words, n * 8, cudaMemcpyHostToDevice, s), "h2d");
+      r = launch_narrow(static_cast<const u64*>(stage->ptr), t->b.data(), n, t->b.level, ctx.n, ctx.basis, bad, s);
+    }
     check_launch(r, "narrow");
     ctx.count(r);
     int hbad = 0;
@@ -1253,11 +1396,15 @@ int hg_tensor_download(const hg_tensor* t, uint64_t* words, void* stream) {
     const Context& ctx = *t->ctx;
     cudaStream_t s = ctx.pick(stream);
     const u64 n = t->b.words(ctx.n);
-    BufPtr stage = ctx.alloc(n * 8, s);
-    const int r = launch_widen(t->b.data(), static_cast<u64*>(stage->ptr), n, s);
-    check_launch(r, "widen");
-    ctx.count(r);
-    cuda_check(cudaMemcpyAsync(words, stage->ptr, n * 8, cudaMemcpyDeviceToHost, s), "d2h");
+    if (ctx.wide) {
+      cuda_check(cudaMemcpyAsync(words, t->b.data64(), n * 8, cudaMemcpyDeviceToHost, s), "d2h");
+    } else {
+      BufPtr stage = ctx.alloc(n * 8, s);
+      const int r = launch_widen(t->b.data(), static_cast<u64*>(stage->ptr), n, s);
+      check_launch(r, "widen");
+      ctx.count(r);
+      cuda_check(cudaMemcpyAsync(words, stage->ptr, n * 8, cudaMemcpyDeviceToHost, s), "d2h");
+    }
     cuda_check(cudaStreamSynchronize(s), "download");
   });
 }
@@ -1265,6 +1412,7 @@ int hg_tensor_download(const hg_tensor* t, uint64_t* words, void* stream) {
 int hg_tensor_upload_u32(hg_tensor* t, const uint32_t* words, void* stream) {
   return guard([&] {
     const Context& ctx = *t->ctx;
+    if (ctx.wide) throw Error(HG_ERR_UNSUPPORTED, "u32 residues: this context stores u64 words (primes >= 2^30)");
     cuda_check(cudaMemcpyAsync(t->b.data(), words, t->b.words(ctx.n) * 4, cudaMemcpyHostToDevice, ctx.pick(stream)),
                "h2d");
   });
@@ -1273,6 +1421,7 @@ int hg_tensor_upload_u32(hg_tensor* t, const uint32_t* words, void* stream) {
 int hg_tensor_download_u32(const hg_tensor* t, uint32_t* words, void* stream) {
   return guard([&] {
     const Context& ctx = *t->ctx;
+    if (ctx.wide) throw Error(HG_ERR_UNSUPPORTED, "u32 residues: this context stores u64 words (primes >= 2^30)");
     cudaStream_t s = ctx.pick(stream);
     cuda_check(cudaMemcpyAsync(words, t->b.data(), t->b.words(ctx.n) * 4, cudaMemcpyDeviceToHost, s), "d2h");
     cuda_check(cudaStreamSynchronize(s), "download");
@@ -1286,6 +1435,7 @@ int hg_relin_key_upload(hg_ctx* ctx, const uint64_t* words, uint64_t n_words, hg
   return guard([&] {
     const Context& c = *ctx->c;
     require(c.has_special, "relinearization keys need a special prime (not present in these parameters)");
+    if (c.wide) throw Error(HG_ERR_UNSUPPORTED, "relinearization keys with primes >= 2^30 are not implemented yet");
     const u64 L = c.chain_len(), n = c.n;
     require(n_words == L * 2 * (L + 1) * n, "malformed relinearization key");
     std::vector<uint2> k(n_words);
@@ -1340,14 +1490,14 @@ int hg_add_ct_ct(hg_ctx* ctx, const hg_tensor* a, const hg_tensor* b, hg_tensor*
 static BufPtr upload_residues(const Context& c, const hg_tensor* ct, const uint64_t* residues, int per_element,
                               cudaStream_t s) {
   const u64 nvals = (per_element ? ct->b.count : 1) * ct->b.level;
-  std::vector<u32> r(nvals);
-  for (u64 i = 0; i < nvals; ++i) {
-    const u64 q = c.chain[i % ct->b.level];
-    require(residues[i] < q, "residue out of range");
-    r[i] = static_cast<u32>(residues[i]);
+  for (u64 i = 0; i < nvals; ++i) require(residues[i] < c.chain[i % ct->b.level], "residue out of range");
+  BufPtr d = c.alloc(nvals * c.word_bytes(), s);
+  if (c.wide) {
+    cuda_check(cudaMemcpyAsync(d->ptr, residues, nvals * 8, cudaMemcpyHostToDevice, s), "h2d");
+  } else {
+    std::vector<u32> r(residues, residues + nvals);
+    cuda_check(cudaMemcpyAsync(d->ptr, r.data(), nvals * 4, cudaMemcpyHostToDevice, s), "h2d");
   }
-  BufPtr d = c.alloc(nvals * 4, s);
-  cuda_check(cudaMemcpyAsync(d->ptr, r.data(), nvals * 4, cudaMemcpyHostToDevice, s), "h2d");
   cuda_check(cudaStreamSynchronize(s), "h2d");
   return d;
 }
@@ -1413,13 +1563,15 @@ int hg_add_ct_pt_vector(hg_ctx* ctx, const hg_tensor* ct, const uint64_t* pt_wor
     require(scales_match(ct->b.scale, pt_scale), "ciphertext/plaintext scale mismatch");
     const u64 L = ct->b.level, n = c.n;
     const u64 nw = (per_element ? ct->b.count : 1) * L * n;
-    std::vector<u32> w(nw);
-    for (u64 i = 0; i < nw; ++i) {
-      require(pt_words[i] < c.chain[(i / n) % L], "residue out of range");
-      w[i] = static_cast<u32>(pt_words[i]);
+    for (u64 i = 0; i < nw; ++i) require(pt_words[i] < c.chain[(i / n) % L], "residue out of range");
+    BufPtr d = c.alloc(nw * c.word_bytes(), s);
+    std::vector<u32> w;
+    if (c.wide) {
+      cuda_check(cudaMemcpyAsync(d->ptr, pt_words, nw * 8, cudaMemcpyHostToDevice, s), "h2d");
+    } else {
+      w.assign(pt_words, pt_words + nw);
+      cuda_check(cudaMemcpyAsync(d->ptr, w.data(), nw * 4, cudaMemcpyHostToDevice, s), "h2d");
     }
-    BufPtr d = c.alloc(nw * 4, s);
-    cuda_check(cudaMemcpyAsync(d->ptr, w.data(), nw * 4, cudaMemcpyHostToDevice, s), "h2d");
     CtBatch o;
     o.packing = ct->b.packing;
     o.scale = ct->b.scale;
@@ -1503,8 +1655,11 @@ int hg_rescale(hg_ctx* ctx, const hg_tensor* ct, uint32_t target_level, hg_tenso
 int hg_ntt_forward(hg_ctx* ctx, hg_tensor* t, void* stream) {
   return guard([&] {
     const Context& c = *ctx->c;
-    const int r = launch_ntt(static_cast<int>(c.logn), t->b.data(), t->b.count * t->b.polys * t->b.level, t->b.level,
-                             false, c.basis, c.pick(stream));
+    const u64 rows = t->b.count * t->b.polys * t->b.level;
+    const int r = c.wide ? launch_ntt_w(static_cast<int>(c.logn), t->b.data64(), rows, t->b.level, false, c.basisw,
+                                        c.pick(stream))
+                         : launch_ntt(static_cast<int>(c.logn), t->b.data(), rows, t->b.level, false, c.basis,
+                                      c.pick(stream));
     check_launch(r, "ntt");
     c.count(r);
   });
@@ -1513,8 +1668,11 @@ int hg_ntt_forward(hg_ctx* ctx, hg_tensor* t, void* stream) {
 int hg_ntt_inverse(hg_ctx* ctx, hg_tensor* t, void* stream) {
   return guard([&] {
     const Context& c = *ctx->c;
-    const int r = launch_ntt(static_cast<int>(c.logn), t->b.data(), t->b.count * t->b.polys * t->b.level, t->b.level,
-                             true, c.basis, c.pick(stream));
+    const u64 rows = t->b.count * t->b.polys * t->b.level;
+    const int r = c.wide ? launch_ntt_w(static_cast<int>(c.logn), t->b.data64(), rows, t->b.level, true, c.basisw,
+                                        c.pick(stream))
+                         : launch_ntt(static_cast<int>(c.logn), t->b.data(), rows, t->b.level, true, c.basis,
+                                      c.pick(stream));
     check_launch(r, "intt");
     c.count(r);
   });
@@ -1529,16 +1687,23 @@ int hg_encode_scalars(hg_ctx* ctx, const double* values, uint64_t count, uint32_
     for (u64 i = 0; i < count; ++i) mx = std::max(mx, std::fabs(values[i]));
     check_scalar_encodable(c, mx, level, scale);
     BufPtr dv = c.alloc(count * 8, s);
-    BufPtr dr = c.alloc(count * level * 4, s);
+    BufPtr dr = c.alloc(count * level * c.word_bytes(), s);
     cuda_check(cudaMemcpyAsync(dv->ptr, values, count * 8, cudaMemcpyHostToDevice, s), "h2d");
-    const int r = launch_encode_scalars_f64(static_cast<const double*>(dv->ptr), count, 1, level, 1, level, scale,
-                                            static_cast<u32*>(dr->ptr), c.basis, s);
+    const int r = c.wide ? launch_encode_scalars_w_f64(static_cast<const double*>(dv->ptr), count, 1, level, 1, level,
+                                                       scale, static_cast<u64*>(dr->ptr), c.basisw, s)
+                         : launch_encode_scalars_f64(static_cast<const double*>(dv->ptr), count, 1, level, 1, level,
+                                                     scale, static_cast<u32*>(dr->ptr), c.basis, s);
     check_launch(r, "encode_scalars");
     c.count(r);
-    std::vector<u32> h(count * level);
-    cuda_check(cudaMemcpyAsync(h.data(), dr->ptr, h.size() * 4, cudaMemcpyDeviceToHost, s), "d2h");
-    cuda_check(cudaStreamSynchronize(s), "encode_scalars");
-    for (u64 i = 0; i < h.size(); ++i) out_residues[i] = h[i];
+    if (c.wide) {
+      cuda_check(cudaMemcpyAsync(out_residues, dr->ptr, count * level * 8, cudaMemcpyDeviceToHost, s), "d2h");
+      cuda_check(cudaStreamSynchronize(s), "encode_scalars");
+    } else {
+      std::vector<u32> h(count * level);
+      cuda_check(cudaMemcpyAsync(h.data(), dr->ptr, h.size() * 4, cudaMemcpyDeviceToHost, s), "d2h");
+      cuda_check(cudaStreamSynchronize(s), "encode_scalars");
+      for (u64 i = 0; i < h.size(); ++i) out_residues[i] = h[i];
+    }
   });
 }
 
@@ -1554,10 +1719,15 @@ int hg_encode_vector(hg_ctx* ctx, const double* slots_re_im, uint32_t n_slots, u
     std::vector<int> ex;
     BufPtr pt = encode_vectors_dev(c, static_cast<const double*>(ds->ptr), n_slots, count, level, scale, s, mant, ex);
     const u64 nw = count * level * static_cast<u64>(c.n);
-    std::vector<u32> h(nw);
-    cuda_check(cudaMemcpyAsync(h.data(), pt->ptr, nw * 4, cudaMemcpyDeviceToHost, s), "d2h");
-    cuda_check(cudaStreamSynchronize(s), "encode_vector");
-    for (u64 i = 0; i < nw; ++i) out_words[i] = h[i];
+    if (c.wide) {
+      cuda_check(cudaMemcpyAsync(out_words, pt->ptr, nw * 8, cudaMemcpyDeviceToHost, s), "d2h");
+      cuda_check(cudaStreamSynchronize(s), "encode_vector");
+    } else {
+      std::vector<u32> h(nw);
+      cuda_check(cudaMemcpyAsync(h.data(), pt->ptr, nw * 4, cudaMemcpyDeviceToHost, s), "d2h");
+      cuda_check(cudaStreamSynchronize(s), "encode_vector");
+      for (u64 i = 0; i < nw; ++i) out_words[i] = h[i];
+    }
   });
 }
 

@@ -19,6 +19,7 @@
 #include <cstdio>
 
 #include "hg_kernels.hpp"
+#include "hg_x87.cuh"
 
 namespace hg {
 
@@ -26,7 +27,7 @@ namespace hg {
 // Batched NTT (hg_ntt_forward / hg_ntt_inverse)
 // ===========================================================================
 template <int LOGN, bool INV>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 2 : 1)) k_ntt(u32* data, u32 level, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_ntt(u32* data, u32 level, Basis B) {
   using NT = Ntt<LOGN>;
   extern __shared__ u32 sm[];
   const u32 tid = threadIdx.x;
@@ -55,7 +56,7 @@ __device__ __forceinline__ u32 signed_residue(i32 c, const DevPrime& P) {
 // Rescale (one CTA per (ciphertext, polynomial))
 // ===========================================================================
 template <int LOGN>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 2 : 1)) k_rescale(RescaleArgs a, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_rescale(RescaleArgs a, Basis B) {
   using NT = Ntt<LOGN>;
   constexpr int N = NT::N;
   constexpr int T = NT::T;
@@ -363,7 +364,7 @@ __device__ __forceinline__ void load_c2(u32 (&y)[32], const RelinArgs& a, u64 ct
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 2 : 1)) k_relin_digits(RelinArgs a, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_relin_digits(RelinArgs a, Basis B) {
   using NT = Ntt<LOGN>;
   constexpr int N = NT::N;
   extern __shared__ u32 sm[];
@@ -378,7 +379,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 2 : 1)) k_relin
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 2 : 1)) k_relin_keysw(RelinArgs a, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_relin_keysw(RelinArgs a, Basis B) {
   using NT = Ntt<LOGN>;
   constexpr int N = NT::N;
   constexpr int T = NT::T;
@@ -475,7 +476,7 @@ __device__ __forceinline__ uint4 load_d4(const RelinArgs& a, u64 ct, u32 poly, u
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 2 : 1)) k_relin_moddown(RelinArgs a, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_relin_moddown(RelinArgs a, Basis B) {
   using NT = Ntt<LOGN>;
   constexpr int N = NT::N;
   constexpr int T = NT::T;
@@ -655,70 +656,6 @@ __global__ void k_widen(const u32* in, u64* out, u64 words) {
 // then rounds half away from zero.  The exact 106-bit product of the two
 // double mantissas is rounded to 64 bits here the same way.
 // ===========================================================================
-struct X87 {
-  bool neg;
-  unsigned long long mant;  // 64-bit normalized mantissa (0 for zero)
-  int exp;                  // value = mant * 2^exp
-};
-
-__device__ __forceinline__ void split_double(double v, unsigned long long& m, int& e) {
-  const unsigned long long bits = __double_as_longlong(v) & 0x7fffffffffffffffull;
-  const int be = static_cast<int>(bits >> 52);
-  const unsigned long long frac = bits & ((1ull << 52) - 1);
-  if (be == 0) { m = frac; e = -1074; }
-  else { m = frac | (1ull << 52); e = be - 1075; }
-}
-
-__device__ __forceinline__ X87 x87_mul(double a, double b) {
-  X87 r;
-  r.neg = (__double_as_longlong(a) ^ __double_as_longlong(b)) < 0;
-  unsigned long long ma, mb;
-  int ea, eb;
-  split_double(a, ma, ea);
-  split_double(b, mb, eb);
-  if (ma == 0 || mb == 0) { r.mant = 0; r.exp = 0; r.neg = false; return r; }
-  unsigned __int128 p = static_cast<unsigned __int128>(ma) * mb;
-  int e = ea + eb;
-  const unsigned long long hi = static_cast<unsigned long long>(p >> 64);
-  const int nb = hi ? 128 - __clzll(hi) : 64 - __clzll(static_cast<unsigned long long>(p));
-  if (nb > 64) {
-    const int sh = nb - 64;
-    unsigned __int128 m = p >> sh;
-    const unsigned __int128 rem = p & ((static_cast<unsigned __int128>(1) << sh) - 1);
-    const unsigned __int128 halfv = static_cast<unsigned __int128>(1) << (sh - 1);
-    if (rem > halfv || (rem == halfv && (m & 1))) m += 1;
-    e += sh;
-    if (m >> 64) { m >>= 1; e += 1; }
-    r.mant = static_cast<unsigned long long>(m);
-  } else {
-    const int sh = 64 - nb;  // normalize
-    r.mant = static_cast<unsigned long long>(p) << sh;
-    e -= sh;
-  }
-  r.exp = e;
-  return r;
-}
-
-// roundl (half away from zero) of |x| as a 128-bit magnitude.
-__device__ __forceinline__ unsigned __int128 x87_roundl_mag(const X87& x) {
-  if (x.mant == 0) return 0;
-  if (x.exp >= 0) return static_cast<unsigned __int128>(x.mant) << x.exp;
-  const int s = -x.exp;
-  if (s > 65) return 0;
-  const unsigned __int128 m = x.mant;
-  return (m + (static_cast<unsigned __int128>(1) << (s - 1))) >> s;
-}
-
-__device__ __forceinline__ u32 residue_mag(unsigned __int128 mag, bool neg, const DevPrime& P) {
-  const u64 q = P.q;
-  const u64 hi = static_cast<u64>(mag >> 64), lo = static_cast<u64>(mag);
-  // 2^64 mod q
-  const u64 t64 = (0xffffffffffffffffull % q + 1) % q;
-  u64 r = ((hi % q) * t64 + lo % q) % q;
-  if (neg && r != 0) r = q - r;
-  return static_cast<u32>(r);
-}
-
 template <typename T>
 __global__ void k_encode_scalars(const T* vals, u64 count, u32 row_len, u32 row_stride, u64 limb_stride,
                                  u32 level, double scale, u32* out, Basis B) {
@@ -742,8 +679,8 @@ __device__ __forceinline__ u32 bitrev_n(u32 i, u32 logn) { return __brev(i) >> (
 // One CTA per plaintext; the FFT works on a global scratch row (L2 resident).
 __global__ void __launch_bounds__(512) k_fft_encode(const double* slots, u32 n_slots, u32 n, u32 logn, u32 level,
                                                     double scale, const double2* roots, const double2* twist,
-                                                    double2* scratch, u32* out, unsigned long long* max_mant,
-                                                    int* max_exp, Basis B) {
+                                                    double2* scratch, ulonglong2* mags, unsigned long long* max_mant,
+                                                    int* max_exp) {
   const u64 pt = blockIdx.x;
   const u32 tid = threadIdx.x;
   double2* a = scratch + pt * n;
@@ -785,7 +722,7 @@ __global__ void __launch_bounds__(512) k_fft_encode(const double* slots, u32 n_s
     const X87 x = x87_mul(coeff, scale);
     if (x.mant != 0 && (x.exp > be || (x.exp == be && x.mant > bm))) { bm = x.mant; be = x.exp; }
     const unsigned __int128 mag = x87_roundl_mag(x);
-    for (u32 i = 0; i < level; ++i) out[(pt * level + i) * n + k] = residue_mag(mag, x.neg, B.p[i]);
+    mags[pt * n + k] = make_ulonglong2(static_cast<u64>(mag), static_cast<u64>(mag >> 64) | (x.neg ? (1ull << 63) : 0));
   }
   s_mant[tid] = bm;
   s_exp[tid] = be;
@@ -797,6 +734,17 @@ __global__ void __launch_bounds__(512) k_fft_encode(const double* slots, u32 n_s
     max_mant[pt] = bm;
     max_exp[pt] = be;
   }
+}
+
+// Signed 128-bit magnitudes -> residues per limb (coefficient domain), u32 basis.
+__global__ void k_mags_to_residues(const ulonglong2* mags, u64 count_n, u32 n, u32 level, u32* out, Basis B) {
+  const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= count_n) return;
+  const ulonglong2 m = mags[idx];
+  const bool neg = (m.y >> 63) != 0;
+  const unsigned __int128 mag = (static_cast<unsigned __int128>(m.y & ~(1ull << 63)) << 64) | m.x;
+  const u64 pt = idx / n, k = idx % n;
+  for (u32 i = 0; i < level; ++i) out[(pt * level + i) * n + k] = residue_mag(mag, neg, B.p[i]);
 }
 
 // ===========================================================================
@@ -1049,14 +997,22 @@ int launch_encode_scalars_f64(const double* vals, u64 count, u32 row_len, u32 ro
 }
 
 int launch_fft_encode(const double* slots, u32 n_slots, u64 count, u32 n, u32 level, double scale,
-                      const double2* roots, const double2* twist, double2* scratch, u32* out,
-                      unsigned long long* max_mant, int* max_exp, const Basis& B, cudaStream_t s) {
+                      const double2* roots, const double2* twist, double2* scratch, ulonglong2* mags,
+                      unsigned long long* max_mant, int* max_exp, cudaStream_t s) {
   if (count == 0) return 0;
   u32 logn = 0;
   while ((1u << logn) < n) ++logn;
   ProfScope ps("k_fft_encode", s);
-  k_fft_encode<<<count, 512, 0, s>>>(slots, n_slots, n, logn, level, scale, roots, twist, scratch, out, max_mant,
-                                      max_exp, B);
+  k_fft_encode<<<count, 512, 0, s>>>(slots, n_slots, n, logn, level, scale, roots, twist, scratch, mags, max_mant,
+                                      max_exp);
+  return 1;
+}
+
+int launch_mags_to_residues(const ulonglong2* mags, u64 count, u32 n, u32 level, u32* out, const Basis& B,
+                            cudaStream_t s) {
+  const u64 total = count * n;
+  if (total == 0) return 0;
+  k_mags_to_residues<<<(total + 255) / 256, 256, 0, s>>>(mags, total, n, level, out, B);
   return 1;
 }
 

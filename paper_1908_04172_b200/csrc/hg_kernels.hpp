@@ -100,11 +100,14 @@ int launch_encode_scalars_f64(const double* vals, u64 count, u32 row_len, u32 ro
                               cudaStream_t s);
 
 // encode_vector front half: conj-extend, radix-2 DIT FFT in the reference's
-// operation order, untwist, x87 scale/round, residues (coefficient domain).
-// maxmag[pt] = (mantissa, exponent) of the largest |scaled| (long double).
+// operation order, untwist, x87 scale/round -> signed 128-bit magnitudes
+// (lo, hi | sign << 63) per coefficient.  max_mant/max_exp[pt] = the largest
+// |scaled| as an exact long double (mantissa, exponent).
 int launch_fft_encode(const double* slots, u32 n_slots, u64 count, u32 n, u32 level, double scale,
-                      const double2* roots, const double2* twist, double2* scratch, u32* out,
-                      unsigned long long* max_mant, int* max_exp, const Basis& B, cudaStream_t s);
+                      const double2* roots, const double2* twist, double2* scratch, ulonglong2* mags,
+                      unsigned long long* max_mant, int* max_exp, cudaStream_t s);
+int launch_mags_to_residues(const ulonglong2* mags, u64 count, u32 n, u32 level, u32* out, const Basis& B,
+                            cudaStream_t s);
 
 // Register-only integer pipe probe; kind 0 IMAD, 1 IMAD.WIDE, 2 IMAD.HI.  Lane-ops per second.
 double bench_int_peak(int device, int kind);

@@ -18,6 +18,7 @@
 
 #include "../../include/henet_b200.h"
 #include "hg_kernels.hpp"
+#include "hg_wide.hpp"
 
 namespace hg {
 
@@ -60,11 +61,15 @@ struct Context {
   std::vector<u64> roots;                    // psi per basis index
   std::vector<long double> modulus_products;  // q_l, henet/params.hpp:236-242
   Basis basis{};
+  bool wide = false;  // some basis prime >= 2^30: every residue is stored as u64 (hg_wide.cu)
+  BasisW basisw{};
   BufPtr tables;      // twiddles for all basis moduli
+  BufPtr wide_tables; // u64 twiddles (wide mode)
   BufPtr fft_tables;  // dft roots (N/2) + twist (N), double2
   std::vector<double> host_roots, host_twist;  // interleaved re/im
 
   size_t chain_len() const { return chain.size(); }
+  size_t word_bytes() const { return wide ? 8 : 4; }
   u64 basis_mod(size_t i) const { return i < chain.size() ? chain[i] : special; }
   cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : core->stream; }
   void count(int launches) const { core->launches += static_cast<uint64_t>(launches > 0 ? launches : 0); }
@@ -82,6 +87,7 @@ struct CtBatch {
   std::vector<u32> shape;
   u64 words(u32 n) const { return count * polys * level * static_cast<u64>(n); }
   u32* data() const { return buf ? static_cast<u32*>(buf->ptr) : nullptr; }
+  u64* data64() const { return buf ? static_cast<u64*>(buf->ptr) : nullptr; }
 };
 
 struct RelinKeyDev {

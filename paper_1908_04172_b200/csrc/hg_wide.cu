@@ -1,0 +1,440 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// u64 ("wide") kernels for contexts with primes >= 2^30 (BASELINE configs 4/5b).
+// Same algorithms as the u32 kernels of hg_kernels.cu; every result canonical.
+#include <cuda_runtime.h>
+
+#include "hg_wide.hpp"
+
+namespace hg {
+
+// ---------------------------------------------------------------------------
+// Batched NTT / INTT
+// ---------------------------------------------------------------------------
+template <int LOGN, bool INV>
+__global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_ntt_w(u64* data, u32 level, BasisW B) {
+  using NT = NttW<LOGN>;
+  extern __shared__ u64 smw[];
+  const u32 tid = threadIdx.x;
+  const u64 row = blockIdx.x;
+  const DevPrimeW& P = B.p[row % level];
+  u64* r = data + row * NT::N;
+  u64 x[32];
+  if (!INV) {
+    NT::gload_A(x, r, tid);
+    NT::forward(x, smw, tid, P);
+    NT::gstore_C(x, r, tid);
+  } else {
+    NT::gload_C(x, r, tid);
+    NT::inverse(x, smw, tid, P);
+    NT::gstore_A(x, r, tid);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Rescale (henet/ckks.hpp:504-519), NTT-domain form as in k_rescale.
+// ---------------------------------------------------------------------------
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_rescale_w(RescaleArgsW a, BasisW B) {
+  using NT = NttW<LOGN>;
+  constexpr int N = NT::N;
+  constexpr int T = NT::T;
+  extern __shared__ u64 smw[];
+  i32* cs = reinterpret_cast<i32*>(smw + NT::SMEM_WORDS);  // |correction| < p_last/2 < 2^31 (checked by the host)
+  const u32 tid = threadIdx.x;
+  const u64 row = blockIdx.x;
+  const u32 L = a.level;
+  const u64* src = a.in + row * L * N;
+  u64* dst = a.out + row * (L - 1) * N;
+  u64 x[32];
+  {
+    const DevPrimeW& Pl = B.p[L - 1];
+    NT::gload_C(x, src + static_cast<u64>(L - 1) * N, tid);
+    NT::inverse(x, smw, tid, Pl);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) cs[k * T + tid] = static_cast<i32>(centered_round_rem_w(x[k], Pl));
+  }
+  for (u32 i = 0; i + 1 < L; ++i) {
+    const DevPrimeW& Pi = B.p[i];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) x[k] = signed_residue_w(cs[k * T + tid], Pi);
+    NT::forward(x, smw, tid, Pi);
+    const u64 q = Pi.q, pv = a.pinv[i], ps = a.pinv_sh[i];
+    const u64* in_i = src + static_cast<u64>(i) * N;
+    u64* out_i = dst + static_cast<u64>(i) * N;
+#pragma unroll
+    for (int k = 0; k < 32; k += 2) {
+      const u32 j = NT::NT::jC(tid, k);
+      const ulonglong2 y = __ldg(reinterpret_cast<const ulonglong2*>(in_i + j));
+      *reinterpret_cast<ulonglong2*>(out_i + j) =
+          make_ulonglong2(mul_shoup64(y.x + q - x[k], pv, ps, q), mul_shoup64(y.y + q - x[k + 1], pv, ps, q));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Dense / conv modular contraction with 128-bit accumulation for wide limbs
+// (products up to 2^80) and the u64 lazy path (with folding) for narrow limbs.
+// ---------------------------------------------------------------------------
+struct Acc128 {
+  u64 lo, hi;
+};
+__device__ __forceinline__ void mac128(Acc128& a, u64 x, u64 w) {
+  asm("mad.lo.cc.u64 %0, %2, %3, %0;\n\tmadc.hi.u64 %1, %2, %3, %1;" : "+l"(a.lo), "+l"(a.hi) : "l"(x), "l"(w));
+}
+
+constexpr int kWBK = 16, kWTM = 4, kWBN = 128, kWWarps = 8;
+
+__global__ void __launch_bounds__(kWWarps * 32) k_mac_dense_w(MacDenseArgsW a, BasisW B) {
+  __shared__ __align__(16) u64 xs[kWBK][kWBN];
+  __shared__ __align__(16) u64 ws[kWBK][kWTM * kWWarps];
+  const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 BM = kWTM * kWWarps;
+  const u32 n0 = blockIdx.x * kWBN;
+  const u32 m0 = blockIdx.y * BM;
+  const u32 poly = blockIdx.z / a.level, limb = blockIdx.z % a.level;
+  const DevPrimeW& P = B.p[limb];
+  const bool wide = P.q >= (1ull << 32);
+  const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
+  const u64* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n0;
+  const u64* Wb = a.W + static_cast<u64>(limb) * a.K * a.Mpad + m0;
+  Acc128 acc[kWTM][4];
+#pragma unroll
+  for (int i = 0; i < kWTM; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = {0, 0};
+  for (u32 k0 = 0; k0 < a.K; k0 += kWBK) {
+    for (u32 c = tid; c < kWBK * kWBN; c += blockDim.x) {
+      const u32 r = c / kWBN, col = c % kWBN, k = k0 + r;
+      xs[r][col] = k < a.K ? __ldg(Xb + static_cast<u64>(k) * xstride + col) : 0;
+    }
+    for (u32 c = tid; c < kWBK * BM; c += blockDim.x) {
+      const u32 r = c / BM, col = c % BM, k = k0 + r;
+      ws[r][col] = k < a.K ? __ldg(Wb + static_cast<u64>(k) * a.Mpad + col) : 0;
+    }
+    __syncthreads();
+    if (wide) {
+#pragma unroll 4
+      for (int kk = 0; kk < kWBK; ++kk) {
+        const ulonglong2 x01 = *reinterpret_cast<const ulonglong2*>(&xs[kk][lane * 4]);
+        const ulonglong2 x23 = *reinterpret_cast<const ulonglong2*>(&xs[kk][lane * 4 + 2]);
+#pragma unroll
+        for (int i = 0; i < kWTM; ++i) {
+          const u64 w = ws[kk][warp * kWTM + i];
+          mac128(acc[i][0], x01.x, w);
+          mac128(acc[i][1], x01.y, w);
+          mac128(acc[i][2], x23.x, w);
+          mac128(acc[i][3], x23.y, w);
+        }
+      }
+    } else {
+      // narrow limb stored wide: 32x32 products into the low word, folded every 8 taps
+      const u64 r32 = static_cast<u64>((1ull << 32) % P.q);
+#pragma unroll 4
+      for (int kk = 0; kk < kWBK; ++kk) {
+        const ulonglong2 x01 = *reinterpret_cast<const ulonglong2*>(&xs[kk][lane * 4]);
+        const ulonglong2 x23 = *reinterpret_cast<const ulonglong2*>(&xs[kk][lane * 4 + 2]);
+#pragma unroll
+        for (int i = 0; i < kWTM; ++i) {
+          const u32 w = static_cast<u32>(ws[kk][warp * kWTM + i]);
+          acc[i][0].lo += static_cast<u64>(w) * static_cast<u32>(x01.x);
+          acc[i][1].lo += static_cast<u64>(w) * static_cast<u32>(x01.y);
+          acc[i][2].lo += static_cast<u64>(w) * static_cast<u32>(x23.x);
+          acc[i][3].lo += static_cast<u64>(w) * static_cast<u32>(x23.y);
+        }
+        if ((kk & 7) == 7) {
+#pragma unroll
+          for (int i = 0; i < kWTM; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j].lo = (acc[i][j].lo & 0xffffffffull) + (acc[i][j].lo >> 32) * r32;
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < kWTM; ++i) {
+    const u32 m = m0 + warp * kWTM + i;
+    if (m >= a.M) continue;
+    const u64 bv = (a.bias != nullptr && poly == 0) ? __ldg(&a.bias[static_cast<u64>(limb) * a.Mpad + m]) : 0;
+    u64* yp = a.Y + ((static_cast<u64>(m) * a.polys + poly) * a.level + limb) * a.N + n0 + lane * 4;
+    u64 o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = addmod_w(barrett128(acc[i][j].lo, acc[i][j].hi, P), bv, P.q);
+    *reinterpret_cast<ulonglong2*>(yp) = make_ulonglong2(o[0], o[1]);
+    *reinterpret_cast<ulonglong2*>(yp + 2) = make_ulonglong2(o[2], o[3]);
+  }
+}
+
+constexpr int kWMaxTaps = 1024;
+constexpr int kWFT = 8;
+
+__global__ void __launch_bounds__(128) k_mac_conv_w(MacConvArgsW a, BasisW B) {
+  __shared__ u32 tap_in[kWMaxTaps];
+  __shared__ u32 tap_w[kWMaxTaps];
+  __shared__ u32 ntaps_s;
+  const u32 tid = threadIdx.x;
+  const u32 pos = blockIdx.y;
+  const u32 oy = pos / a.OW, ox = pos % a.OW;
+  const u32 nchunks = (a.F + kWFT - 1) / kWFT;
+  const u32 pl = blockIdx.z / nchunks;
+  const u32 f0 = (blockIdx.z % nchunks) * kWFT;
+  const u32 poly = pl / a.level, limb = pl % a.level;
+  const DevPrimeW& P = B.p[limb];
+  const u32 n = (blockIdx.x * blockDim.x + tid) * 2;
+  const u32 taps_all = a.C * a.win * a.win;
+  if (tid == 0) {
+    u32 cnt = 0;
+    for (u32 c = 0; c < a.C; ++c)
+      for (u32 ky = 0; ky < a.win; ++ky)
+        for (u32 kx = 0; kx < a.win; ++kx) {
+          const int iy = static_cast<int>(oy * a.stride + ky) - static_cast<int>(a.pad_top);
+          const int ix = static_cast<int>(ox * a.stride + kx) - static_cast<int>(a.pad_left);
+          if (iy < 0 || iy >= static_cast<int>(a.IH) || ix < 0 || ix >= static_cast<int>(a.IW)) continue;
+          tap_in[cnt] = (c * a.IH + iy) * a.IW + ix;
+          tap_w[cnt] = (c * a.win + ky) * a.win + kx;
+          ++cnt;
+        }
+    ntaps_s = cnt;
+  }
+  __syncthreads();
+  const u32 ntaps = ntaps_s;
+  const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
+  const u64* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n;
+  const u64* Wl = a.W + static_cast<u64>(limb) * a.F * taps_all;
+  Acc128 acc[kWFT][2];
+#pragma unroll
+  for (int f = 0; f < kWFT; ++f) acc[f][0] = acc[f][1] = {0, 0};
+  for (u32 t = 0; t < ntaps; ++t) {
+    const ulonglong2 xv = __ldg(reinterpret_cast<const ulonglong2*>(Xb + static_cast<u64>(tap_in[t]) * xstride));
+#pragma unroll
+    for (int f = 0; f < kWFT; ++f) {
+      if (f0 + f >= a.F) break;
+      const u64 w = __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + tap_w[t]]);
+      mac128(acc[f][0], xv.x, w);
+      mac128(acc[f][1], xv.y, w);
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < kWFT; ++f) {
+    const u32 ff = f0 + f;
+    if (ff >= a.F) continue;
+    const u64 bv = (a.bias != nullptr && poly == 0) ? __ldg(&a.bias[static_cast<u64>(limb) * a.F + ff]) : 0;
+    const u64 e = static_cast<u64>(ff) * a.OH * a.OW + pos;
+    u64* yp = a.Y + ((e * a.polys + poly) * a.level + limb) * a.N + n;
+    *reinterpret_cast<ulonglong2*>(yp) = make_ulonglong2(addmod_w(barrett128(acc[f][0].lo, acc[f][0].hi, P), bv, P.q),
+                                                         addmod_w(barrett128(acc[f][1].lo, acc[f][1].hi, P), bv, P.q));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Element-wise
+// ---------------------------------------------------------------------------
+__global__ void k_ew_w(EwArgsW a, BasisW B) {
+  const u32 N = a.N;
+  const u64 rows = a.count * a.polys_out * a.level;
+  const u64 tiles_per_row = N / 2;
+  const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= rows * tiles_per_row) return;
+  const u64 row = idx / tiles_per_row;
+  const u32 n = static_cast<u32>(idx % tiles_per_row) * 2;
+  const u32 limb = row % a.level;
+  const u32 poly = (row / a.level) % a.polys_out;
+  const u64 e = row / (static_cast<u64>(a.level) * a.polys_out);
+  const DevPrimeW& P = B.p[limb];
+  const u64 q = P.q;
+  auto ld = [&](const u64* base, u32 polys, u32 p) {
+    return *reinterpret_cast<const ulonglong2*>(base + ((e * polys + p) * a.level + limb) * N + n);
+  };
+  ulonglong2 o;
+  switch (a.op) {
+    case EwOp::AddCC: {
+      const ulonglong2 x = ld(a.a, a.polys_a, poly), y = ld(a.b, a.polys_a, poly);
+      o = make_ulonglong2(addmod_w(x.x, y.x, q), addmod_w(x.y, y.y, q));
+      break;
+    }
+    case EwOp::MulScalar: {
+      const ulonglong2 x = ld(a.a, a.polys_a, poly);
+      const u64 r = a.res[(a.per_element ? e / a.pt_div : 0) * a.level + limb];
+      o = make_ulonglong2(mulmod_w(x.x, r, P), mulmod_w(x.y, r, P));
+      break;
+    }
+    case EwOp::AddScalar: {
+      o = ld(a.a, a.polys_a, poly);
+      if (poly == 0) {
+        const u64 r = a.res[(a.per_element ? e / a.pt_div : 0) * a.level + limb];
+        o = make_ulonglong2(addmod_w(o.x, r, q), addmod_w(o.y, r, q));
+      }
+      break;
+    }
+    case EwOp::AddVector: {
+      o = ld(a.a, a.polys_a, poly);
+      if (poly == 0) {
+        const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(
+            a.b + ((a.per_element ? e / a.pt_div : 0) * a.level + limb) * static_cast<u64>(N) + n);
+        o = make_ulonglong2(addmod_w(o.x, y.x, q), addmod_w(o.y, y.y, q));
+      }
+      break;
+    }
+    case EwOp::Tensor: {
+      ulonglong2 x, y;
+      if (poly == 0) { x = ld(a.a, 2, 0); y = ld(a.b, 2, 0); }
+      else if (poly == 2) { x = ld(a.a, 2, 1); y = ld(a.b, 2, 1); }
+      else { x = ld(a.a, 2, 0); y = ld(a.b, 2, 1); }
+      o = make_ulonglong2(mulmod_w(x.x, y.x, P), mulmod_w(x.y, y.y, P));
+      if (poly == 1) {
+        x = ld(a.a, 2, 1);
+        y = ld(a.b, 2, 0);
+        o.x = addmod_w(o.x, mulmod_w(x.x, y.x, P), q);
+        o.y = addmod_w(o.y, mulmod_w(x.y, y.y, P), q);
+      }
+      break;
+    }
+    default:
+      o = ld(a.a, a.polys_a, poly);
+      break;
+  }
+  *reinterpret_cast<ulonglong2*>(a.out + ((e * a.polys_out + poly) * a.level + limb) * N + n) = o;
+}
+
+__global__ void k_validate_w(const u64* w, u64 words, u32 level, u32 N, BasisW B, int* bad) {
+  const u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  if (w[i] >= B.p[(i / N) % level].q) atomicExch(bad, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Scalar encoding with u64 residues (x87 product rounding shared with the u32 path)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_encode_scalars_w(const T* vals, u64 count, u32 row_len, u32 row_stride, u64 limb_stride,
+                                   u32 level, double scale, u64* out, BasisW B) {
+  const u64 v = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= count) return;
+  bool neg;
+  const unsigned __int128 mag = x87_round_product(static_cast<double>(vals[v]), scale, neg);
+  const u64 dst = (v / row_len) * row_stride + v % row_len;
+  for (u32 i = 0; i < level; ++i) {
+    const DevPrimeW& P = B.p[i];
+    u64 r = barrett128(static_cast<u64>(mag), static_cast<u64>(mag >> 64), P);
+    if (neg && r != 0) r = P.q - r;
+    out[i * limb_stride + dst] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+#define HG_LOGN_SWITCH_W(logn, ...)                  \
+  switch (logn) {                                    \
+    case 12: { constexpr int LN = 12; __VA_ARGS__; } break; \
+    case 13: { constexpr int LN = 13; __VA_ARGS__; } break; \
+    case 14: { constexpr int LN = 14; __VA_ARGS__; } break; \
+    default: return -1;                              \
+  }
+
+template <typename K>
+static void set_smem_w(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+}
+
+int launch_ntt_w(int logn, u64* data, u64 rows, u32 level, bool inverse, const BasisW& B, cudaStream_t s) {
+  if (rows == 0) return 0;
+  HG_LOGN_SWITCH_W(logn, {
+    const size_t sm = sizeof(u64) * NttW<LN>::SMEM_WORDS;
+    if (inverse) {
+      set_smem_w(k_ntt_w<LN, true>, sm);
+      k_ntt_w<LN, true><<<rows, 1 << (LN - 5), sm, s>>>(data, level, B);
+    } else {
+      set_smem_w(k_ntt_w<LN, false>, sm);
+      k_ntt_w<LN, false><<<rows, 1 << (LN - 5), sm, s>>>(data, level, B);
+    }
+  });
+  return 1;
+}
+
+int launch_rescale_w(int logn, const RescaleArgsW& a, const BasisW& B, cudaStream_t s) {
+  if (a.rows == 0) return 0;
+  HG_LOGN_SWITCH_W(logn, {
+    const size_t sm = sizeof(u64) * NttW<LN>::SMEM_WORDS + sizeof(i32) * NttW<LN>::N;
+    set_smem_w(k_rescale_w<LN>, sm);
+    k_rescale_w<LN><<<a.rows, 1 << (LN - 5), sm, s>>>(a, B);
+  });
+  return 1;
+}
+
+u32 mac_dense_w_bm() { return kWTM * kWWarps; }
+
+int launch_mac_dense_w(const MacDenseArgsW& a, const BasisW& B, cudaStream_t s) {
+  const u32 BM = kWTM * kWWarps;
+  if (a.Mpad % BM != 0 || a.N % kWBN != 0) return -1;
+  dim3 grid(a.N / kWBN, (a.M + BM - 1) / BM, a.polys * a.level);
+  k_mac_dense_w<<<grid, kWWarps * 32, 0, s>>>(a, B);
+  return 1;
+}
+
+int launch_mac_conv_w(const MacConvArgsW& a, const BasisW& B, cudaStream_t s) {
+  if (a.C * a.win * a.win > static_cast<u32>(kWMaxTaps) || a.N % 256 != 0) return -1;
+  const u32 nchunks = (a.F + kWFT - 1) / kWFT;
+  dim3 grid(a.N / 256, a.OH * a.OW, a.polys * a.level * nchunks);
+  k_mac_conv_w<<<grid, 128, 0, s>>>(a, B);
+  return 1;
+}
+
+int launch_elementwise_w(const EwArgsW& a, const BasisW& B, cudaStream_t s) {
+  const u64 threads = a.count * a.polys_out * a.level * (a.N / 2);
+  if (threads == 0) return 0;
+  k_ew_w<<<(threads + 255) / 256, 256, 0, s>>>(a, B);
+  return 1;
+}
+
+int launch_validate_w(const u64* w, u64 words, u32 level, u32 N, const BasisW& B, int* d_bad, cudaStream_t s) {
+  if (words == 0) return 0;
+  k_validate_w<<<(words + 255) / 256, 256, 0, s>>>(w, words, level, N, B, d_bad);
+  return 1;
+}
+
+int launch_encode_scalars_w_f32(const float* vals, u64 count, u32 row_len, u32 row_stride, u64 limb_stride, u32 level,
+                                double scale, u64* out, const BasisW& B, cudaStream_t s) {
+  if (count == 0) return 0;
+  k_encode_scalars_w<float><<<(count + 127) / 128, 128, 0, s>>>(vals, count, row_len, row_stride, limb_stride, level,
+                                                                scale, out, B);
+  return 1;
+}
+
+int launch_encode_scalars_w_f64(const double* vals, u64 count, u32 row_len, u32 row_stride, u64 limb_stride,
+                                u32 level, double scale, u64* out, const BasisW& B, cudaStream_t s) {
+  if (count == 0) return 0;
+  k_encode_scalars_w<double><<<(count + 127) / 128, 128, 0, s>>>(vals, count, row_len, row_stride, limb_stride, level,
+                                                                 scale, out, B);
+  return 1;
+}
+
+}  // namespace hg
+
+namespace hg {
+
+__global__ void k_mags_to_residues_w(const ulonglong2* mags, u64 count_n, u32 n, u32 level, u64* out, BasisW B) {
+  const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= count_n) return;
+  const ulonglong2 m = mags[idx];
+  const bool neg = (m.y >> 63) != 0;
+  const u64 hi = m.y & ~(1ull << 63);
+  const u64 pt = idx / n, k = idx % n;
+  for (u32 i = 0; i < level; ++i) {
+    const DevPrimeW& P = B.p[i];
+    u64 r = barrett128(m.x, hi, P);
+    if (neg && r != 0) r = P.q - r;
+    out[(pt * level + i) * n + k] = r;
+  }
+}
+
+int launch_mags_to_residues_w(const ulonglong2* mags, u64 count, u32 n, u32 level, u64* out, const BasisW& B,
+                              cudaStream_t s) {
+  const u64 total = count * n;
+  if (total == 0) return 0;
+  k_mags_to_residues_w<<<(total + 255) / 256, 256, 0, s>>>(mags, total, n, level, out, B);
+  return 1;
+}
+
+}  // namespace hg

@@ -210,3 +210,58 @@ def random_ciphertexts(params: dict, count: int, seed: int, level: int = None) -
     for i, q in enumerate(params["chain"][:L]):
         out[:, :, i, :] = rng.integers(0, q, size=(count, 2, params["n"]), dtype=np.uint64)
     return out
+
+
+def wide_dense(seed: int = 5, k: int = 4096, m: int = 4096, batch: int = 8192) -> Workload:
+    """Config 5b: wide dense layer k -> m on N=16384 batch-packed ciphertexts (40-bit limb 0),
+    W ~ N(0, 0.1^2) (config 4/5 weight scale), one rescale per output (patched plan, as c1)."""
+    rng = np.random.default_rng(seed)
+    blob = Blob()
+    blob.add("fc_w", [k, m], _gauss(rng, (k, m), 0.1))
+    j = {
+        "name": f"dense-{k}-{m}",
+        "packing": "real",
+        "preset": "P14",
+        "weights": blob.table,
+        "nodes": [
+            _node("input", "Input", attrs={"shape": [k]}),
+            _node("fc", "Dot", ["input"], weight_ref="fc_w"),
+            _node("out", "Output", ["fc"]),
+        ],
+    }
+    return Workload(f"c5b_dense_{k}_{m}", json.dumps(j), blob.bytes(), [k], 0, batch, patch_terminal_rescale=True)
+
+
+def mobilenet_block(seed: int = 6, hw: int = 56, cin: int = 16, expand: int = 96, cout: int = 24,
+                    batch: int = 8192) -> Workload:
+    """Config 4: MobileNetV2 inverted-residual block on (cin, hw, hw) activations: 1x1 expand
+    cin->expand, ReLU6 (client-aided), 3x3 depthwise (as a block-diagonal full convolution:
+    zero weights give exact zero residues), ReLU6, 1x1 project expand->cout.
+    Weights ~ N(0, 0.1^2).  The reference graph has no ReLU6/depthwise op: ReLU6 runs through
+    the NonlinearityProvider hook as a Relu node whose provider clips to [0, 6]."""
+    rng = np.random.default_rng(seed)
+    blob = Blob()
+    blob.add("exp_w", [expand, cin, 1, 1], _gauss(rng, (expand, cin, 1, 1), 0.1))
+    dw = np.zeros((expand, expand, 3, 3), np.float32)
+    dwv = _gauss(rng, (expand, 3, 3), 0.1).reshape(expand, 3, 3)
+    for c in range(expand):
+        dw[c, c] = dwv[c]
+    blob.add("dw_w", [expand, expand, 3, 3], dw)
+    blob.add("proj_w", [cout, expand, 1, 1], _gauss(rng, (cout, expand, 1, 1), 0.1))
+    j = {
+        "name": "mobilenetv2-block",
+        "packing": "real",
+        "preset": "P14",
+        "weights": blob.table,
+        "nodes": [
+            _node("input", "Input", attrs={"shape": [cin, hw, hw]}),
+            _node("expand", "Convolution", ["input"], {"stride": 1, "window": 1, "filters": expand}, "exp_w"),
+            _node("relu6a", "Relu", ["expand"]),
+            _node("dw", "Convolution", ["relu6a"], {"stride": 1, "window": 3, "filters": expand, "pad": [1, 1, 1, 1]},
+                  "dw_w"),
+            _node("relu6b", "Relu", ["dw"]),
+            _node("project", "Convolution", ["relu6b"], {"stride": 1, "window": 1, "filters": cout}, "proj_w"),
+            _node("out", "Output", ["project"]),
+        ],
+    }
+    return Workload("c4_mobilenetv2_block", json.dumps(j), blob.bytes(), [cin, hw, hw], 0, batch)
