@@ -26,9 +26,6 @@ using i32 = int32_t;
 
 constexpr int kMaxPrimes = 24;
 
-#ifndef HG_TW_MODE
-#define HG_TW_MODE 0  // 0: a pass's twiddle row is preloaded (16 x 128-bit); 1: loaded per use
-#endif
 #ifndef HG_NTT_MINB
 #define HG_NTT_MINB 2  // CTAs per SM the NTT kernels are register-budgeted for (N <= 2^13)
 #endif
@@ -51,10 +48,15 @@ struct DevPrime {
   // (value, shoup) pairs in the exact order the unrolled stages consume them.
   uint2 twA[32];       // root_powers[1..31]      (psi^bitrev(i), shoup)
   uint2 itwA[32];      // inv_root_powers[1..31]
-  const uint2* fwdB;   // [2^MB rows][32]
-  const uint2* fwdC;   // [T rows][32]
+  // Pass C: twiddle psi^bitrev(idx) = V(stage, c, g) * T_stage(tid) because idx's
+  // bit fields from (c, g) and from tid are disjoint and bit reversal is additive
+  // over disjoint fields.  V is uniform (here); T is one value per thread and stage.
+  uint2 tvC[32];       // forward V, consumption order
+  uint2 itvC[32];      // inverse V
+  const uint2* fwdB;   // [2^MB rows][32] staged pass-B rows
+  const uint2* fwdT;   // [T rows][4]: T_b(tid) for b = 0..CB-1
   const uint2* invB;
-  const uint2* invC;
+  const uint2* invT;
 };
 
 struct Basis {
@@ -191,34 +193,34 @@ struct Ntt {
     static constexpr int BLO = (L == 0) ? LOGT : (L == 1 ? CB : 0);
   };
 
-  // Row of staged twiddles of pass L (1: B, 2: C) for this thread, 16 x 128-bit.
-  template <int L>
-  __device__ static __forceinline__ void load_row(uint4 (&tw)[16], const uint2* base, u32 tid) {
-    const uint4* row = reinterpret_cast<const uint4*>(base + static_cast<size_t>(L == 1 ? (tid >> CB) : tid) * 32);
+  // Row of staged pass-B twiddles for this thread's group, 16 x 128-bit.
+  __device__ static __forceinline__ void load_rowB(uint4 (&tw)[16], const uint2* base, u32 tid) {
+    const uint4* row = reinterpret_cast<const uint4*>(base + static_cast<size_t>(tid >> CB) * 32);
 #pragma unroll
     for (int i = 0; i < 16; ++i) tw[i] = __ldg(row + i);
   }
   __device__ static __forceinline__ uint2 slot(const uint4 (&tw)[16], int n) {
     return (n & 1) ? make_uint2(tw[n >> 1].z, tw[n >> 1].w) : make_uint2(tw[n >> 1].x, tw[n >> 1].y);
   }
-
-  // Forward (Cooley-Tukey, Harvey lazy) stages of pass L.  Values in [0, 4q).
-  template <int L>
-  __device__ static __forceinline__ const uint2* row_ptr(const uint2* base, u32 tid) {
-    return base + static_cast<size_t>(L == 1 ? (tid >> CB) : tid) * 32;
+  // Per-thread pass-C bases T_b(tid), b = 0..CB-1 (two 128-bit loads).
+  __device__ static __forceinline__ void load_bases(uint2 (&tb)[4], const uint2* base, u32 tid) {
+    const uint4* row = reinterpret_cast<const uint4*>(base + static_cast<size_t>(tid) * 4);
+    const uint4 v0 = __ldg(row), v1 = __ldg(row + 1);
+    tb[0] = make_uint2(v0.x, v0.y);
+    tb[1] = make_uint2(v0.z, v0.w);
+    tb[2] = make_uint2(v1.x, v1.y);
+    tb[3] = make_uint2(v1.z, v1.w);
   }
 
+  // Forward (Cooley-Tukey, Harvey lazy) stages of pass L.  Values in [0, 4q).
+  // Pass A twiddles come from the parameter block, pass B from the preloaded
+  // row, pass C as V * T_b(tid) (two Shoup multiplications, no loads).
   template <int L>
-  __device__ static __forceinline__ void fwd_pass(u32 (&x)[32], u32 tid, const DevPrime& P) {
+  __device__ static __forceinline__ void fwd_pass(u32 (&x)[32], const DevPrime& P, const uint4 (&twB)[16],
+                                                  const uint2 (&tb)[4]) {
     constexpr int NB = PassShape<L>::NB;
     constexpr int BLO = PassShape<L>::BLO;
     const u32 q = P.q, q2 = P.two_q;
-#if HG_TW_MODE == 0
-    uint4 tw[16];
-    if (L != 0) load_row<L>(tw, L == 1 ? P.fwdB : P.fwdC, tid);
-#else
-    const uint2* trow = L != 0 ? row_ptr<L>(L == 1 ? P.fwdB : P.fwdC, tid) : nullptr;
-#endif
     int n = 0;
 #pragma unroll
     for (int s = 0; s < NB; ++s) {
@@ -229,11 +231,8 @@ struct Ntt {
 #pragma unroll
         for (int hi = 0; hi < (1 << (NB - 1 - rb)); ++hi) {
           const u32 kh = (static_cast<u32>(g) << NB) | (static_cast<u32>(hi) << (rb + 1));
-#if HG_TW_MODE == 0
-          const uint2 w = (L == 0) ? P.twA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))] : slot(tw, n);
-#else
-          const uint2 w = (L == 0) ? P.twA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))] : __ldg(trow + n);
-#endif
+          const uint2 w = (L == 0) ? P.twA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))]
+                                   : (L == 1 ? slot(twB, n) : P.tvC[n]);
           ++n;
 #pragma unroll
           for (int lo = 0; lo < (1 << rb); ++lo) {
@@ -241,7 +240,9 @@ struct Ntt {
             const int k1 = k0 | (1 << rb);
             u32 X = x[k0];
             X = min(X, X - q2);
-            const u32 Tm = mul_shoup_lazy(x[k1], w.x, w.y, q);
+            u32 Y = x[k1];
+            if (L == 2) Y = mul_shoup_lazy(Y, tb[b].x, tb[b].y, q);
+            const u32 Tm = mul_shoup_lazy(Y, w.x, w.y, q);
             x[k0] = X + Tm;
             x[k1] = X - Tm + q2;
           }
@@ -251,18 +252,13 @@ struct Ntt {
   }
 
   // Inverse (Gentleman-Sande, Harvey lazy) stages of pass L.  Values in [0, 2q).
-  // LAST: pass A carries the final stage (m = 1), which also applies N^-1.
+  // Pass A carries the final stage (m = 1), which also applies N^-1.
   template <int L>
-  __device__ static __forceinline__ void inv_pass(u32 (&x)[32], u32 tid, const DevPrime& P) {
+  __device__ static __forceinline__ void inv_pass(u32 (&x)[32], const DevPrime& P, const uint4 (&twB)[16],
+                                                  const uint2 (&tb)[4]) {
     constexpr int NB = PassShape<L>::NB;
     constexpr int BLO = PassShape<L>::BLO;
     const u32 q = P.q, q2 = P.two_q;
-#if HG_TW_MODE == 0
-    uint4 tw[16];
-    if (L != 0) load_row<L>(tw, L == 1 ? P.invB : P.invC, tid);
-#else
-    const uint2* trow = L != 0 ? row_ptr<L>(L == 1 ? P.invB : P.invC, tid) : nullptr;
-#endif
     int n = 0;
 #pragma unroll
     for (int s = 0; s < NB; ++s) {
@@ -283,11 +279,8 @@ struct Ntt {
               x[k1] = mul_shoup_lazy(U - V + q2, P.w1n, P.w1n_sh, q);
             }
           } else {
-#if HG_TW_MODE == 0
-            const uint2 w = (L == 0) ? P.itwA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))] : slot(tw, n);
-#else
-            const uint2 w = (L == 0) ? P.itwA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))] : __ldg(trow + n);
-#endif
+            const uint2 w = (L == 0) ? P.itwA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))]
+                                     : (L == 1 ? slot(twB, n) : P.itvC[n]);
             ++n;
 #pragma unroll
             for (int lo = 0; lo < (1 << rb); ++lo) {
@@ -296,7 +289,9 @@ struct Ntt {
               const u32 U = x[k0], V = x[k1];
               u32 S = U + V;
               x[k0] = min(S, S - q2);
-              x[k1] = mul_shoup_lazy(U - V + q2, w.x, w.y, q);
+              u32 D = U - V + q2;
+              if (L == 2) D = mul_shoup_lazy(D, tb[b].x, tb[b].y, q);
+              x[k1] = mul_shoup_lazy(D, w.x, w.y, q);
             }
           }
         }
@@ -305,19 +300,23 @@ struct Ntt {
   }
 
   // Full forward transform.  In: layout A, values < 4q.  Out: layout C,
-  // canonical.  `sm` must hold N u32; the call begins and ends with a barrier
-  // so the buffer may be reused immediately by the caller.
+  // canonical.  `sm` must hold SMEM_WORDS u32; the call begins and ends with a
+  // barrier-protected exchange so the buffer may be reused immediately.
   __device__ static __forceinline__ void forward(u32 (&x)[32], u32* sm, u32 tid, const DevPrime& P) {
-    fwd_pass<0>(x, tid, P);
+    uint4 twB[16];
+    uint2 tb[4];
+    load_rowB(twB, P.fwdB, tid);  // in flight during pass A
+    load_bases(tb, P.fwdT, tid);
+    fwd_pass<0>(x, P, twB, tb);
     __syncthreads();
     store<0>(x, sm, tid);
     __syncthreads();
     load<1>(x, sm, tid);
-    fwd_pass<1>(x, tid, P);
+    fwd_pass<1>(x, P, twB, tb);
     store<1>(x, sm, tid);
     __syncthreads();
     load<2>(x, sm, tid);
-    fwd_pass<2>(x, tid, P);
+    fwd_pass<2>(x, P, twB, tb);
     const u32 q = P.q, q2 = P.two_q;
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
@@ -329,16 +328,20 @@ struct Ntt {
 
   // Full inverse transform.  In: layout C, values < 2q.  Out: layout A, canonical.
   __device__ static __forceinline__ void inverse(u32 (&x)[32], u32* sm, u32 tid, const DevPrime& P) {
-    inv_pass<2>(x, tid, P);
+    uint4 twB[16];
+    uint2 tb[4];
+    load_bases(tb, P.invT, tid);
+    load_rowB(twB, P.invB, tid);  // in flight during pass C
+    inv_pass<2>(x, P, twB, tb);
     __syncthreads();
     store<2>(x, sm, tid);
     __syncthreads();
     load<1>(x, sm, tid);
-    inv_pass<1>(x, tid, P);
+    inv_pass<1>(x, P, twB, tb);
     store<1>(x, sm, tid);
     __syncthreads();
     load<0>(x, sm, tid);
-    inv_pass<0>(x, tid, P);
+    inv_pass<0>(x, P, twB, tb);
     const u32 q = P.q;
 #pragma unroll
     for (int k = 0; k < 32; ++k) x[k] = csub(x[k], q);

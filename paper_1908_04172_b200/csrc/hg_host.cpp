@@ -136,31 +136,52 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
   // NTT tables (root_powers / inv_root_powers in the reference's order, with
   // Shoup companions), staged per NTT pass in the order the kernels consume them.
   const u32 LOGT = logn - 5, CB = logn >= 14 ? logn - 10 : 3, MB = LOGT - CB;
-  const u32 rowsB = 1u << MB, rowsC = 1u << LOGT;
-  const size_t per_prime = 2 * static_cast<size_t>(rowsB + rowsC) * 32;
+  const u32 rowsB = 1u << MB, rowsT = 1u << LOGT;
+  const size_t per_prime = 2 * (static_cast<size_t>(rowsB) * 32 + static_cast<size_t>(rowsT) * 4);
   std::vector<uint2> staged(static_cast<size_t>(full) * per_prime);
-  auto jmap = [&](int L, u32 tid, u32 k) -> u32 {
+  auto jmapB = [&](u32 tid, u32 k) -> u32 {
     const u32 CBm = (1u << CB) - 1, MBm = (1u << MB) - 1;
-    if (L == 1) return (tid & CBm) | ((k & MBm) << CB) | ((tid >> CB) << LOGT) | ((k >> MB) << (LOGT + MB));
-    return (k & CBm) | (tid << CB) | ((k >> CB) << (CB + LOGT));
+    return (tid & CBm) | ((k & MBm) << CB) | ((tid >> CB) << LOGT) | ((k >> MB) << (LOGT + MB));
   };
-  auto stage_rows = [&](int L, bool inverse, const std::vector<uint2>& tab, uint2* out) {
-    const u32 NB = L == 1 ? MB : CB, BLO = L == 1 ? CB : 0;
-    const u32 rows = L == 1 ? rowsB : rowsC;
-    for (u32 R = 0; R < rows; ++R) {
-      const u32 tid = L == 1 ? (R << CB) : R;
+  // pass-B rows in the order the unrolled stages consume them (Ntt::fwd_pass / inv_pass)
+  auto stage_rowsB = [&](bool inverse, const std::vector<uint2>& tab, uint2* out) {
+    const u32 NB = MB, BLO = CB;
+    for (u32 R = 0; R < rowsB; ++R) {
+      const u32 tid = R << CB;
       int nslot = 0;
       for (u32 st = 0; st < NB; ++st) {
         const u32 rb = inverse ? st : NB - 1 - st;
         const u32 bb = BLO + rb;
-        for (u32 g = 0; g < (1u << (5 - NB)); ++g)
+        for (u32 gg = 0; gg < (1u << (5 - NB)); ++gg)
           for (u32 hi = 0; hi < (1u << (NB - 1 - rb)); ++hi) {
-            const u32 kh = (g << NB) | (hi << (rb + 1));
-            const u32 j = jmap(L, tid, kh);
+            const u32 kh = (gg << NB) | (hi << (rb + 1));
+            const u32 j = jmapB(tid, kh);
             out[static_cast<size_t>(R) * 32 + nslot++] = tab[(1u << (logn - 1 - bb)) + (j >> (bb + 1))];
           }
       }
     }
+  };
+  // pass C: psi^bitrev(idx) = V(b, c, g) * T_b(tid) over disjoint bit fields of idx
+  auto stage_C = [&](bool inverse, u64 root, u64 q, uint2* vtab, uint2* tbase) {
+    const u32 NB = CB;
+    int nslot = 0;
+    for (u32 st = 0; st < NB; ++st) {
+      const u32 rb = inverse ? st : NB - 1 - st;
+      const u32 bb = rb;
+      const u32 nb = logn - 1 - bb;
+      for (u32 gg = 0; gg < (1u << (5 - NB)); ++gg)
+        for (u32 hi = 0; hi < (1u << (NB - 1 - rb)); ++hi) {
+          const u32 u = hi | (gg << (CB + LOGT - bb - 1));
+          const u64 v = nt::powmod(root, nt::bit_reverse((1u << nb) | u, logn), q);
+          vtab[nslot++] = make_uint2(static_cast<u32>(v), nt::shoup(v, q));
+        }
+    }
+    for (u32 t = 0; t < rowsT; ++t)
+      for (u32 bb = 0; bb < 4; ++bb) {
+        u64 v = 1;
+        if (bb < CB) v = nt::powmod(root, nt::bit_reverse(t << (CB - bb - 1), logn), q);
+        tbase[static_cast<size_t>(t) * 4 + bb] = make_uint2(static_cast<u32>(v), nt::shoup(v, q));
+      }
   };
   std::vector<uint2> f(n), g(n);
   for (u32 i = 0; i < full; ++i) {
@@ -193,10 +214,10 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
       P.itwA[k] = g[k];
     }
     uint2* base = &staged[static_cast<size_t>(i) * per_prime];
-    stage_rows(1, false, f, base);
-    stage_rows(2, false, f, base + rowsB * 32);
-    stage_rows(1, true, g, base + (rowsB + rowsC) * 32);
-    stage_rows(2, true, g, base + (2 * rowsB + rowsC) * 32);
+    stage_rowsB(false, f, base);
+    stage_C(false, psi, q, P.tvC, base + rowsB * 32);
+    stage_rowsB(true, g, base + rowsB * 32 + rowsT * 4);
+    stage_C(true, psi_inv, q, P.itvC, base + 2 * rowsB * 32 + rowsT * 4);
   }
   if (ctx->wide) {
     // u64 path: natural-order tables with 64-bit Shoup companions (hg_wide.cuh)
@@ -245,9 +266,9 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
   for (u32 i = 0; i < full; ++i) {
     const uint2* base = static_cast<const uint2*>(ctx->tables->ptr) + static_cast<size_t>(i) * per_prime;
     ctx->basis.p[i].fwdB = base;
-    ctx->basis.p[i].fwdC = base + rowsB * 32;
-    ctx->basis.p[i].invB = base + (rowsB + rowsC) * 32;
-    ctx->basis.p[i].invC = base + (2 * rowsB + rowsC) * 32;
+    ctx->basis.p[i].fwdT = base + rowsB * 32;
+    ctx->basis.p[i].invB = base + rowsB * 32 + rowsT * 4;
+    ctx->basis.p[i].invT = base + 2 * rowsB * 32 + rowsT * 4;
   }
   cuda_check(cudaStreamSynchronize(ctx->core->stream), "upload tables");
 

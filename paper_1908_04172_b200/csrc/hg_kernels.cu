@@ -80,14 +80,17 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
     const DevPrime& Pi = B.p[i];
 #pragma unroll
     for (int k = 0; k < 32; ++k) x[k] = signed_residue(cs[k * T + tid], Pi);
-    NT::forward(x, sm, tid, Pi);
-    const u32 q = Pi.q, pv = a.pinv[i], ps = a.pinv_sh[i];
     const u32* in_i = src + static_cast<u64>(i) * N;
     u32* out_i = dst + static_cast<u64>(i) * N;
+    uint4 yv[8];  // issued before the transform so the loads overlap it
+#pragma unroll
+    for (int g = 0; g < 8; ++g) yv[g] = __ldg(reinterpret_cast<const uint4*>(in_i + NT::jC(tid, 4 * g)));
+    NT::forward(x, sm, tid, Pi);
+    const u32 q = Pi.q, pv = a.pinv[i], ps = a.pinv_sh[i];
 #pragma unroll
     for (int k = 0; k < 32; k += 4) {
       const u32 j = NT::jC(tid, k);
-      const uint4 y = __ldg(reinterpret_cast<const uint4*>(in_i + j));
+      const uint4 y = yv[k >> 2];
       uint4 o;
       o.x = mul_shoup(y.x + q - x[k], pv, ps, q);
       o.y = mul_shoup(y.y + q - x[k + 1], pv, ps, q);
@@ -408,23 +411,32 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
     }
     const uint2* k0 = a.key + ((static_cast<u64>(j) * 2 + 0) * (a.chain_len + 1) + bidx) * N;
     const uint2* k1 = a.key + ((static_cast<u64>(j) * 2 + 1) * (a.chain_len + 1) + bidx) * N;
+    // key rows are L2-resident but far: issue a round of 8 pair-loads before using any
 #pragma unroll
-    for (int k = 0; k < 32; k += 2) {
-      const u32 jj = NT::jC(tid, k);
-      const uint4 kv0 = __ldg(reinterpret_cast<const uint4*>(k0 + jj));
-      const uint4 kv1 = __ldg(reinterpret_cast<const uint4*>(k1 + jj));
-      const u32 p00 = mul_shoup(y[k], kv0.x, kv0.y, q), p01 = mul_shoup(y[k + 1], kv0.z, kv0.w, q);
-      const u32 p10 = mul_shoup(y[k], kv1.x, kv1.y, q), p11 = mul_shoup(y[k + 1], kv1.z, kv1.w, q);
-      if (j == 0) {
-        acc0[k * T + tid] = p00;
-        acc0[(k + 1) * T + tid] = p01;
-        acc1[k * T + tid] = p10;
-        acc1[(k + 1) * T + tid] = p11;
-      } else {
-        acc0[k * T + tid] = addmod(acc0[k * T + tid], p00, q);
-        acc0[(k + 1) * T + tid] = addmod(acc0[(k + 1) * T + tid], p01, q);
-        acc1[k * T + tid] = addmod(acc1[k * T + tid], p10, q);
-        acc1[(k + 1) * T + tid] = addmod(acc1[(k + 1) * T + tid], p11, q);
+    for (int half = 0; half < 2; ++half) {
+      uint4 kv0[8], kv1[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const u32 jj = NT::jC(tid, half * 16 + 2 * i);
+        kv0[i] = __ldg(reinterpret_cast<const uint4*>(k0 + jj));
+        kv1[i] = __ldg(reinterpret_cast<const uint4*>(k1 + jj));
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int k = half * 16 + 2 * i;
+        const u32 p00 = mul_shoup(y[k], kv0[i].x, kv0[i].y, q), p01 = mul_shoup(y[k + 1], kv0[i].z, kv0[i].w, q);
+        const u32 p10 = mul_shoup(y[k], kv1[i].x, kv1[i].y, q), p11 = mul_shoup(y[k + 1], kv1[i].z, kv1[i].w, q);
+        if (j == 0) {
+          acc0[k * T + tid] = p00;
+          acc0[(k + 1) * T + tid] = p01;
+          acc1[k * T + tid] = p10;
+          acc1[(k + 1) * T + tid] = p11;
+        } else {
+          acc0[k * T + tid] = addmod(acc0[k * T + tid], p00, q);
+          acc0[(k + 1) * T + tid] = addmod(acc0[(k + 1) * T + tid], p01, q);
+          acc1[k * T + tid] = addmod(acc1[k * T + tid], p10, q);
+          acc1[(k + 1) * T + tid] = addmod(acc1[(k + 1) * T + tid], p11, q);
+        }
       }
     }
   }
@@ -463,6 +475,18 @@ __device__ __forceinline__ uint4 load_d4(const RelinArgs& a, u64 ct, u32 poly, u
     return __ldg(reinterpret_cast<const uint4*>(base + ((ct * polys + p) * L + i) * static_cast<u64>(N) + j));
   };
   if (a.mode == 0) return ld(a.A, 3, poly);
+  if (a.A == a.Bm) {
+    // square (henet/ckks.hpp:424-437): d0 = c0^2, d1 = c0 c1 + c0 c1
+    const uint4 x = ld(a.A, 2, 0), y = poly ? ld(a.A, 2, 1) : x;
+    uint4 d = make_uint4(mulmod(x.x, y.x, P), mulmod(x.y, y.y, P), mulmod(x.z, y.z, P), mulmod(x.w, y.w, P));
+    if (poly == 1) {
+      d.x = addmod(d.x, d.x, P.q);
+      d.y = addmod(d.y, d.y, P.q);
+      d.z = addmod(d.z, d.z, P.q);
+      d.w = addmod(d.w, d.w, P.q);
+    }
+    return d;
+  }
   const uint4 x = ld(a.A, 2, 0), y = ld(a.Bm, 2, poly);
   uint4 d = make_uint4(mulmod(x.x, y.x, P), mulmod(x.y, y.y, P), mulmod(x.z, y.z, P), mulmod(x.w, y.w, P));
   if (poly == 1) {
@@ -507,8 +531,8 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
 #pragma unroll
     for (int k = 0; k < 32; k += 4) {
       const u32 j = NT::jC(tid, k);
-      const uint4 d = load_d4(a, ct, poly, i, j, N, Pi);
       const uint4 v = __ldg(reinterpret_cast<const uint4*>(accp + static_cast<u64>(i) * N + j));
+      const uint4 d = load_d4(a, ct, poly, i, j, N, Pi);
       z[k] = addmod(d.x, mul_shoup(v.x + q - z[k], pv, ps, q), q);
       z[k + 1] = addmod(d.y, mul_shoup(v.y + q - z[k + 1], pv, ps, q), q);
       z[k + 2] = addmod(d.z, mul_shoup(v.z + q - z[k + 2], pv, ps, q), q);
@@ -534,14 +558,21 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
 #pragma unroll
       for (int k = 0; k < 32; ++k) z[k] = signed_residue(cps[k * T + tid], Pi);
     }
+    // accumulator loads issued ahead of the transform; d products computed after it
+    uint4 vv[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) vv[g] = __ldg(reinterpret_cast<const uint4*>(accp + static_cast<u64>(i) * N + NT::jC(tid, 4 * g)));
     NT::forward(z, sm, tid, Pi);
     const u32 lv = a.pinvL[i], ls = a.pinvL_sh[i];
     u32* out_i = dst + static_cast<u64>(i) * N;
+    uint4 dd[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) dd[g] = load_d4(a, ct, poly, i, NT::jC(tid, 4 * g), N, Pi);
 #pragma unroll
     for (int k = 0; k < 32; k += 4) {
       const u32 j = NT::jC(tid, k);
-      const uint4 d = load_d4(a, ct, poly, i, j, N, Pi);
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(accp + static_cast<u64>(i) * N + j));
+      const uint4 d = dd[k >> 2];
+      const uint4 v = vv[k >> 2];
       uint4 o;
       if (a.rescale) {
         o.x = mul_shoup(addmod(d.x, mul_shoup(v.x, pv, ps, q), q) + q - z[k], lv, ls, q);

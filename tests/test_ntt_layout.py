@@ -98,3 +98,26 @@ def test_butterfly_pairs_are_thread_local(logn):
                         continue
                     assert jm(logn, tid, k) + (1 << b) == jm(logn, tid, k | (1 << rb))
     assert sorted(covered) == list(range(logn))
+
+
+@pytest.mark.parametrize("logn", [12, 13, 14])
+def test_pass_c_twiddle_factorisation(logn):
+    """NTT v3 (hg_device.cuh): in pass C the twiddle index 2^nb + (j >> (b+1)) splits into
+    disjoint bit fields from (c, g) and from tid, so bitrev(idx) = bitrev(2^nb | u_cg) +
+    bitrev(u_tid) and psi^bitrev(idx) = V(b, c, g) * T_b(tid)."""
+    logt, cb, mb = cfg(logn)
+
+    def bitrev(v, bits):
+        return int(format(v, f"0{bits}b")[::-1], 2)
+
+    for tid in range(0, 1 << logt, 7):
+        for k in range(32):
+            j = jC(logn, tid, k)
+            c, g = k & ((1 << cb) - 1), k >> cb
+            for b in range(cb):
+                nb = logn - 1 - b
+                idx = (1 << nb) + (j >> (b + 1))
+                u_cg = (c >> (b + 1)) | (g << (cb + logt - b - 1))
+                u_t = tid << (cb - b - 1)
+                assert (1 << nb) | u_cg | u_t == idx and u_cg & u_t == 0
+                assert bitrev(idx, logn) == bitrev((1 << nb) | u_cg, logn) + bitrev(u_t, logn)
