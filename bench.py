@@ -142,9 +142,19 @@ def work_model(n=8192):
         add("k_relin_moddown", C_ * (2 * (l + 1) * bf * 3 + (6 * l - 2) * n * 3),
             C_ * (2 * l * n * W + 2 * l * n * W + 2 * n * W + 2 * (l - 1) * n * W))
     # fc1 845 -> 100 at level 4, fc2 100 -> 10 at level 2
-    add("k_mac_dense", 845 * 100 * 2 * 4 * n + 100 * 10 * 2 * 2 * n,
-        (845 + 100) * 2 * 4 * n * W + (100 + 10) * 2 * 2 * n * W)
+    dense_macs = 845 * 100 * 2 * 4 * n + 100 * 10 * 2 * 2 * n
+    dense_bytes = (845 + 100) * 2 * 4 * n * W + (100 + 10) * 2 * 2 * n * W
+    add("k_mac_dense", dense_macs, dense_bytes)
+    add("k_mac_dense_tc", dense_macs, dense_bytes)
     return m
+
+
+def tc_work():
+    """int8 tensor-core MACs the byte-plane contraction needs (fc1 + fc2 of c2):
+    planes^2 byte products per modular MAC, planes = 4 for the 30-bit limb 0, 3 else."""
+    n = 8192
+    per_limb = lambda K, M, L: sum((16 if i == 0 else 9) for i in range(L)) * K * M * 2 * n
+    return per_limb(845, 100, 4) + per_limb(100, 10, 2)
 
 
 def load_peaks():
@@ -348,6 +358,15 @@ def b200_run(args, ws, rank, local):
                          "hbm_gbs": byts / (ms * 1e-3) / 1e9 if ms else 0,
                          "roofline_frac": max(t_int, t_hbm) / ms if ms else 0,
                          "bound": "int32" if t_int >= t_hbm else "hbm"}
+    if "k_mac_dense_tc" in kernels:
+        # tensor-core roofline of the int8 contraction: int8 dense peak = 2 x the measured bf16 GEMM
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
+        i8_peak = 2 * float(peaks["bf16_tflops"]) * 1e12 / 2  # MAC/s
+        k = kernels["k_mac_dense_tc"]
+        k["tensor_int8_macs_per_s"] = tc_work() / (k["ms_per_step"] * 1e-3)
+        k["tensor_frac"] = k["tensor_int8_macs_per_s"] / i8_peak
+        k["tensor_peak_note"] = "int8 dense = 2 x measured bf16 (MEASURED_PEAKS.json)"
     dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
     dk = kernels[dom]
     ops, byts = model_w.get(dom, (0.0, 0.0))
@@ -361,7 +380,7 @@ def b200_run(args, ws, rank, local):
         roof = {"bound": "hbm", "kernel": dom, "achieved": dk["hbm_gbs"], "peak": hbm_gbs, "unit": "GB/s",
                 "frac": dk["hbm_gbs"] / hbm_gbs, "peak_source": hbm_src, "traffic": None}
     roof["algorithmic_per_step"] = {"imad_ops": ops, "hbm_bytes": byts}
-    whole_t = max(sum(v[0] for v in model_w.values()) / int_peak, 0) * 1e3
+    whole_t = sum(v[0] for k_, v in model_w.items() if k_ != "k_mac_dense_tc") / int_peak * 1e3
     roof["whole_step"] = {"int32_floor_ms": whole_t, "measured_ms": ms_per_step,
                           "frac": whole_t / ms_per_step if ms_per_step else 0}
 

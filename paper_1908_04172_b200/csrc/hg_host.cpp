@@ -129,6 +129,11 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
+  {
+    // Dot on the int8 tensor cores by default; HG_DENSE_TC=0 selects the IMAD kernel
+    const char* tc = getenv("HG_DENSE_TC");
+    ctx->dense_tc = !(tc != nullptr && tc[0] == '0');
+  }
   ctx->core = std::make_shared<DeviceCore>();
   ctx->core->device = device;
   cuda_check(cudaStreamCreateWithFlags(&ctx->core->stream, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -968,6 +973,26 @@ class Executor {
         a.polys = 2;
         a.x_level = x.level;
         r = launch_mac_dense_w(a, ctx.basisw, s_);
+      } else if (ctx.dense_tc && K <= 8192) {
+        // tensor-core path: byte-plane weights packed once per call, then tcgen05.mma.kind::i8
+        BufPtr wp = ctx.alloc(tc_packed_weight_bytes(K, Mo, L), s_);
+        r = launch_pack_weights_tc(static_cast<const u32*>(wres->ptr), static_cast<uint8_t*>(wp->ptr), K, Mo, Mpad, L, s_);
+        check_launch(r, "pack weights");
+        count(r);
+        MacDenseTcArgs a{};
+        a.X = x.data();
+        a.Y = v.cipher.data();
+        a.Wp = static_cast<const uint8_t*>(wp->ptr);
+        a.bias = bias_res ? static_cast<const u32*>(bias_res->ptr) : nullptr;
+        a.K = K;
+        a.M = Mo;
+        a.Mpad = Mpad;
+        a.N = N;
+        a.level = L;
+        a.polys = 2;
+        a.x_level = x.level;
+        for (u32 i = 0; i < L; ++i) a.planes[i] = ctx.chain[i] < (1ull << 24) ? 3 : 4;
+        r = launch_mac_dense_tc(a, ctx.basis, s_);
       } else {
         MacDenseArgs a{};
         a.X = x.data();

@@ -262,23 +262,44 @@ __global__ void __launch_bounds__(kConvThreads) k_mac_conv(MacConvArgs a, Basis 
   const u32 taps_all = a.C * a.win * a.win;
   const u32* Wl = a.W + static_cast<u64>(limb) * a.F * taps_all;
 
-  if (tid == 0) {
-    // valid taps in ascending (c, ky, kx) order, henet/graph.hpp:976-989
-    u32 cnt = 0;
-    for (u32 c = 0; c < a.C; ++c)
-      for (u32 ky = 0; ky < a.win; ++ky)
-        for (u32 kx = 0; kx < a.win; ++kx) {
-          const int iy = static_cast<int>(oy * a.stride + ky) - static_cast<int>(a.pad_top);
-          const int ix = static_cast<int>(ox * a.stride + kx) - static_cast<int>(a.pad_left);
-          if (iy < 0 || iy >= static_cast<int>(a.IH) || ix < 0 || ix >= static_cast<int>(a.IW)) continue;
-          tap_in[cnt] = (c * a.IH + iy) * a.IW + ix;
-          const u32 tw = (c * a.win + ky) * a.win + kx;
+  // valid taps in ascending (c, ky, kx) order (henet/graph.hpp:976-989), built in
+  // parallel: tap t of the full window is valid iff its input pixel is in bounds,
+  // and its slot is the number of valid taps before it (warp ballot prefix).
+  if (tid == 0) ntaps_s = 0;
+  __syncthreads();
+  for (u32 base = 0; base < taps_all; base += blockDim.x) {
+    const u32 t = base + tid;
+    bool valid = false;
+    u32 in_idx = 0;
+    if (t < taps_all) {
+      const u32 c = t / (a.win * a.win), ky = (t / a.win) % a.win, kx = t % a.win;
+      const int iy = static_cast<int>(oy * a.stride + ky) - static_cast<int>(a.pad_top);
+      const int ix = static_cast<int>(ox * a.stride + kx) - static_cast<int>(a.pad_left);
+      valid = iy >= 0 && iy < static_cast<int>(a.IH) && ix >= 0 && ix < static_cast<int>(a.IW);
+      in_idx = (c * a.IH + iy) * a.IW + ix;
+    }
+    // block-wide exclusive prefix over `valid` (blockDim.x <= 1024: one ballot per warp)
+    __shared__ u32 warp_cnt[32];
+    const u32 lane = tid & 31, wid = tid >> 5;
+    const u32 bal = __ballot_sync(0xffffffffu, valid);
+    if (lane == 0) warp_cnt[wid] = __popc(bal);
+    __syncthreads();
+    u32 before = ntaps_s;
+    for (u32 w = 0; w < wid; ++w) before += warp_cnt[w];
+    before += __popc(bal & ((1u << lane) - 1));
+    if (valid) {
+      tap_in[before] = in_idx;
 #pragma unroll
-          for (int f = 0; f < FT; ++f)
-            wsm[cnt * FT + f] = (f0 + f < a.F) ? __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + tw]) : 0u;
-          ++cnt;
-        }
-    ntaps_s = cnt;
+      for (int f = 0; f < FT; ++f)
+        wsm[before * FT + f] = (f0 + f < a.F) ? __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + t]) : 0u;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      u32 tot = 0;
+      for (u32 w = 0; w < (blockDim.x + 31) / 32; ++w) tot += warp_cnt[w];
+      ntaps_s += tot;
+    }
+    __syncthreads();
   }
   __syncthreads();
   const u32 ntaps = ntaps_s;
@@ -398,32 +419,35 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
   const DevPrime& P = B.p[bidx];
   const u32 q = P.q;
 
+  // digit j+1 is loaded while digit j's key products are accumulated
+  u32 nx[32];
+  if (special || t != 0) NT::gload_A(nx, a.D + (ct * L + 0) * N, tid);
   for (u32 j = 0; j < L; ++j) {
     u32 y[32];
     if (!special && j == t) {
       // NTT_t(INTT_t(c2_t)) == c2_t: the digit's own limb needs no transform.
       load_c2<LOGN>(y, a, ct, j, P, tid);
     } else {
-      NT::gload_A(y, a.D + (ct * L + j) * N, tid);
 #pragma unroll
-      for (int k = 0; k < 32; ++k) y[k] = reduce32(y[k], P);  // digit mod q_t, henet/ckks.hpp:463
+      for (int k = 0; k < 32; ++k) y[k] = reduce32(nx[k], P);  // digit mod q_t, henet/ckks.hpp:463
       NT::forward(y, sm, tid, P);
     }
+    if (j + 1 < L && (special || j + 1 != t)) NT::gload_A(nx, a.D + (ct * L + j + 1) * N, tid);
     const uint2* k0 = a.key + ((static_cast<u64>(j) * 2 + 0) * (a.chain_len + 1) + bidx) * N;
     const uint2* k1 = a.key + ((static_cast<u64>(j) * 2 + 1) * (a.chain_len + 1) + bidx) * N;
-    // key rows are L2-resident but far: issue a round of 8 pair-loads before using any
+    // key rows are L2-resident but far: issue a round of 4 pair-loads before using any
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      uint4 kv0[8], kv1[8];
+    for (int qr = 0; qr < 4; ++qr) {
+      uint4 kv0[4], kv1[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const u32 jj = NT::jC(tid, half * 16 + 2 * i);
+      for (int i = 0; i < 4; ++i) {
+        const u32 jj = NT::jC(tid, qr * 8 + 2 * i);
         kv0[i] = __ldg(reinterpret_cast<const uint4*>(k0 + jj));
         kv1[i] = __ldg(reinterpret_cast<const uint4*>(k1 + jj));
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int k = half * 16 + 2 * i;
+      for (int i = 0; i < 4; ++i) {
+        const int k = qr * 8 + 2 * i;
         const u32 p00 = mul_shoup(y[k], kv0[i].x, kv0[i].y, q), p01 = mul_shoup(y[k + 1], kv0[i].z, kv0[i].w, q);
         const u32 p10 = mul_shoup(y[k], kv1[i].x, kv1[i].y, q), p11 = mul_shoup(y[k + 1], kv1[i].z, kv1[i].w, q);
         if (j == 0) {
@@ -835,23 +859,19 @@ bool g_prof_on = false;
 std::vector<ProfRec> g_prof;
 }  // namespace
 
-struct ProfScope {
-  const char* name;
-  cudaStream_t s;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  ProfScope(const char* n, cudaStream_t st) : name(n), s(st) {
-    if (!g_prof_on) return;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, s);
-  }
-  ~ProfScope() {
-    if (!e0) return;
-    cudaEventRecord(e1, s);
-    std::lock_guard<std::mutex> g(g_prof_mu);
-    g_prof.push_back({name, e0, e1});
-  }
-};
+ProfScope::ProfScope(const char* n, cudaStream_t st) : name(n), s(st) {
+  if (!g_prof_on) return;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+}
+
+ProfScope::~ProfScope() {
+  if (!e0) return;
+  cudaEventRecord(e1, s);
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof.push_back({name, e0, e1});
+}
 
 void prof_enable(bool on) { g_prof_on = on; }
 

@@ -112,6 +112,15 @@ int launch_mags_to_residues(const ulonglong2* mags, u64 count, u32 n, u32 level,
 // Register-only integer pipe probe; kind 0 IMAD, 1 IMAD.WIDE, 2 IMAD.HI.  Lane-ops per second.
 double bench_int_peak(int device, int kind);
 
+// Brackets one kernel launch with CUDA events on its stream when profiling is on.
+struct ProfScope {
+  const char* name;
+  cudaStream_t s;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  ProfScope(const char* n, cudaStream_t st);
+  ~ProfScope();
+};
+
 void prof_enable(bool on);
 std::string prof_report();  // JSON: kernel -> {ms, launches}; clears the log
 

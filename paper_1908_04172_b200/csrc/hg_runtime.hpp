@@ -19,6 +19,7 @@
 #include "../../include/henet_b200.h"
 #include "hg_kernels.hpp"
 #include "hg_wide.hpp"
+#include "hg_tc.hpp"
 
 namespace hg {
 
@@ -62,6 +63,7 @@ struct Context {
   std::vector<long double> modulus_products;  // q_l, henet/params.hpp:236-242
   Basis basis{};
   bool wide = false;  // some basis prime >= 2^30: every residue is stored as u64 (hg_wide.cu)
+  bool dense_tc = false;  // Dot on tcgen05 int8 tensor cores (hg_tc.cu) instead of IMAD
   BasisW basisw{};
   BufPtr tables;      // twiddles for all basis moduli
   BufPtr wide_tables; // u64 twiddles (wide mode)

@@ -1,0 +1,290 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Dense modular contraction (Dot, henet/graph.hpp:905-954) on the 5th-generation
+// tensor cores: tcgen05.mma.kind::i8 with byte-plane limb decomposition.
+//
+// For one (poly, limb) slice, Y[m][n] = sum_k W[m][k] X[k][n] mod q with
+// 24- or 30-bit residues.  Split both operands into bytes, w = sum_a w_a 2^8a,
+// x = sum_b x_b 2^8b; then
+//     Y = sum_s D_s 2^8s (mod q),   D_s = sum_{a+b=s} W_a X_b   (u8 x u8 -> s32)
+// Each D_s accumulates in its own TMEM region; <= 4 products per s and K <= 8192
+// keep D_s < 2^31.  The epilogue folds sum_s D_s (2^8s mod q) in u64 (< 2^64)
+// and reduces once -- the same canonical residue the IMAD kernel and the
+// reference produce.
+//
+// CTA tile: M = 128 outputs (one UMMA M) x N = 32 coefficients, K in steps of 32.
+// Operands are K-major, no swizzle (canonical 8-row x 16-byte core matrices:
+// LBO = 128 B between the two K halves, SBO = 256 B between 8-row groups).
+// Weights are pre-packed into that layout once per layer (k_pack_weights_tc);
+// X tiles arrive by cp.async (4-deep ring) and are split into byte planes in
+// shared memory by all threads; one elected thread issues the MMAs.
+#include <cuda_runtime.h>
+
+#include "hg_tc.hpp"
+
+namespace hg {
+
+constexpr int kTcM = 128, kTcN = 64, kTcK = 32, kTcS = 4;
+constexpr int kTcProducers = 256;                 // 8 warps split X into byte planes
+constexpr int kTcThreads = kTcProducers + 32;     // + 1 warp: bulk copies + MMA issue
+constexpr int kTcPlaneA = kTcM * kTcK;            // 4096 B per weight byte plane per K step
+constexpr int kTcPlaneB = kTcN * kTcK;            // 2048 B per input byte plane
+constexpr int kTcCols = 512;                      // TMEM columns: up to 7 accumulators x 64
+
+struct TcSmem {
+  uint8_t a[kTcS][4][kTcPlaneA];  // weight planes (K-major core matrices), filled by cp.async.bulk
+  uint8_t b[kTcS][4][kTcPlaneB];  // input planes, written by the producer warps
+  unsigned long long full_a[kTcS], full_b[kTcS], empty[kTcS];
+  u32 tmem;
+};
+
+__device__ __forceinline__ u32 smem_addr(const void* p) { return static_cast<u32>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ u64 umma_desc(u32 saddr) {
+  // start address, LBO = 128 B, SBO = 256 B (all >> 4), version 1 (sm100), SWIZZLE_NONE
+  return static_cast<u64>((saddr >> 4) & 0x3FFF) | (static_cast<u64>(128 >> 4) << 16) |
+         (static_cast<u64>(256 >> 4) << 32) | (1ull << 46);
+}
+
+// core-matrix offset of element (row r, k in [0,32)) of a K-major tile
+__device__ __forceinline__ u32 cm_off(u32 r, u32 k) { return (r >> 3) * 256 + (k >> 4) * 128 + (r & 7) * 16 + (k & 15); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, u32 parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nLAB_WAIT%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LAB_WAIT%=;\n}\n" ::"r"(smem_addr(b)),
+      "r"(parity));
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(b)));
+}
+
+// ---------------------------------------------------------------------------
+// Pack encoded weight residues [level][K][Mpad] (u32) into byte planes laid out
+// as UMMA K-major tiles: Wp[limb][mt][ks][plane][4096 B].
+// ---------------------------------------------------------------------------
+__global__ void k_pack_weights_tc(const u32* W, uint8_t* Wp, u32 K, u32 Mpad, u32 Mtiles, u32 Ksteps, u32 level) {
+  const u64 total = static_cast<u64>(level) * Mtiles * Ksteps * kTcM * kTcK;
+  const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const u32 k = idx % kTcK;
+  const u32 r = (idx / kTcK) % kTcM;
+  const u64 t = idx / (kTcK * kTcM);
+  const u32 ks = t % Ksteps;
+  const u32 mt = (t / Ksteps) % Mtiles;
+  const u32 limb = t / (static_cast<u64>(Ksteps) * Mtiles);
+  const u32 kk = ks * kTcK + k, m = mt * kTcM + r;
+  const u32 w = (kk < K && m < Mpad) ? W[(static_cast<u64>(limb) * K + kk) * Mpad + m] : 0u;
+  uint8_t* tile = Wp + (((static_cast<u64>(limb) * Mtiles + mt) * Ksteps + ks) * 4) * kTcPlaneA;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) tile[p * kTcPlaneA + cm_off(r, k)] = static_cast<uint8_t>(w >> (8 * p));
+}
+
+// ---------------------------------------------------------------------------
+// Main kernel.  grid = (N / 64, Mtiles, polys * level), 288 threads:
+//   warps 0-7  producers: X(ks) -> byte planes B[ks % S]; then the epilogue
+//   warp 8     lane 0: weight planes by cp.async.bulk into A[], MMA issue, commits
+// Rings: full_a (tx bytes), full_b (256 producer arrivals), empty (MMA commit).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a, Basis B) {
+  extern __shared__ __align__(1024) uint8_t tc_raw[];
+  TcSmem& S = *reinterpret_cast<TcSmem*>(tc_raw);
+  const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const u32 n0 = blockIdx.x * kTcN;
+  const u32 mt = blockIdx.y;
+  const u32 poly = blockIdx.z / a.level, limb = blockIdx.z % a.level;
+  const DevPrime& P = B.p[limb];
+  const u32 planes = a.planes[limb];  // 3 for q < 2^24, 4 otherwise
+  const u32 KS = a.Ksteps;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_addr(&S.tmem)),
+                 "r"(kTcCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kTcS; ++i) {
+      mbar_init(&S.full_a[i], 1);
+      mbar_init(&S.full_b[i], kTcProducers);
+      mbar_init(&S.empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const u32 tmem = S.tmem;
+
+  if (warp == kTcProducers / 32) {
+    // ===== weight loader + MMA issuer (one lane) =====
+    if (lane == 0) {
+      const uint8_t* Wt = a.Wp + ((static_cast<u64>(limb) * a.Mtiles + mt) * KS) * 4 * kTcPlaneA;
+      const u32 bytes = planes * kTcPlaneA;
+      auto load_a = [&](u32 j) {
+        const u32 st = j % kTcS;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(&S.full_a[st])),
+                     "r"(bytes));
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                smem_addr(&S.a[st][0][0])),
+            "l"(Wt + static_cast<u64>(j) * 4 * kTcPlaneA), "r"(bytes), "r"(smem_addr(&S.full_a[st])));
+      };
+      for (u32 j = 0; j < kTcS - 1 && j < KS; ++j) load_a(j);
+      // idesc: D s32, A/B u8, K-major, N = 64, M = 128
+      const u32 idesc = (2u << 4) | ((kTcN >> 3) << 17) | ((kTcM >> 4) << 24);
+      for (u32 ks = 0; ks < KS; ++ks) {
+        const u32 st = ks % kTcS, use = ks / kTcS;
+        const u32 j = ks + kTcS - 1;
+        if (j < KS) {
+          if (j >= kTcS) mbar_wait(&S.empty[j % kTcS], ((j / kTcS) - 1) & 1);
+          load_a(j);
+        }
+        mbar_wait(&S.full_a[st], use & 1);
+        mbar_wait(&S.full_b[st], use & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        for (u32 pa = 0; pa < planes; ++pa) {
+          const u64 ad = umma_desc(smem_addr(&S.a[st][pa][0]));
+          for (u32 pb = 0; pb < planes; ++pb) {
+            const u64 bd = umma_desc(smem_addr(&S.b[st][pb][0]));
+            const u32 s = pa + pb;
+            const u32 first_pa = s >= planes ? s - planes + 1 : 0;
+            const u32 accum = (ks > 0 || pa != first_pa) ? 1u : 0u;
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + s * kTcN),
+                "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            smem_addr(&S.empty[st])));
+      }
+    }
+  } else {
+    // ===== producers: thread -> (n = tid % 64, k-group = tid / 64 of 8 consecutive k) =====
+    const u32 n = tid & (kTcN - 1), kg = tid / kTcN;
+    const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
+    const u32* Xn = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n0 + n;
+    auto fetch = [&](u32 ks, u32 (&v)[8]) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const u32 k = ks * kTcK + kg * 8 + i;
+        v[i] = k < a.K ? __ldg(Xn + static_cast<u64>(k) * xstride) : 0u;
+      }
+    };
+    // 4 steps of X in flight per thread (register ring, statically indexed by unrolling)
+    constexpr int kPre = 4;
+    u32 buf[kPre][8];
+#pragma unroll
+    for (int d = 0; d < kPre; ++d) fetch(d, buf[d]);
+    for (u32 ks0 = 0; ks0 < KS; ks0 += kPre) {
+#pragma unroll
+      for (int d = 0; d < kPre; ++d) {
+        const u32 ks = ks0 + d;
+        if (ks >= KS) break;
+        const u32 st = ks % kTcS, use = ks / kTcS;
+        u32 v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = buf[d][i];
+        if (ks + kPre < KS) fetch(ks + kPre, buf[d]);
+        if (ks >= kTcS) mbar_wait(&S.empty[st], (use - 1) & 1);
+        for (u32 p = 0; p < planes; ++p) {
+          const u32 sh = 8 * p;
+          const u32 lo = ((v[0] >> sh) & 255) | (((v[1] >> sh) & 255) << 8) | (((v[2] >> sh) & 255) << 16) |
+                         (((v[3] >> sh) & 255) << 24);
+          const u32 hi = ((v[4] >> sh) & 255) | (((v[5] >> sh) & 255) << 8) | (((v[6] >> sh) & 255) << 16) |
+                         (((v[7] >> sh) & 255) << 24);
+          *reinterpret_cast<uint2*>(&S.b[st][p][cm_off(n, kg * 8)]) = make_uint2(lo, hi);
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::);
+        mbar_arrive(&S.full_b[st]);
+      }
+    }
+
+    // ===== epilogue: warp w reads TMEM lanes 32*(w%4).., columns (w/4)*32 .. +32 =====
+    mbar_wait(&S.empty[(KS - 1) % kTcS], ((KS - 1) / kTcS) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    const u32 lg = warp & 3, ch = warp >> 2;
+    const u32 m = mt * kTcM + lg * 32 + lane;
+    const u32 q = P.q;
+    u64 cs[7];
+    {
+      u64 c = 1;
+#pragma unroll
+      for (int s = 0; s < 7; ++s) {
+        cs[s] = c;
+        c = (c << 8) % q;
+      }
+    }
+    const u32 nacc = 2 * planes - 1;
+    const u32 bv = (a.bias != nullptr && poly == 0 && m < a.M) ? __ldg(&a.bias[static_cast<u64>(limb) * a.Mpad + m]) : 0u;
+#pragma unroll
+    for (u32 cc = 0; cc < 32; cc += 8) {
+      const u32 col = ch * 32 + cc;
+      u64 acc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0;
+      for (u32 s = 0; s < nacc; ++s) {
+        u32 r[8];
+        const u32 taddr = tmem + ((lg * 32) << 16) + s * kTcN + col;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                     : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += static_cast<u64>(r[i]) * cs[s];
+      }
+      if (m < a.M) {
+        u32 o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = addmod(reduce64(acc[i], P), bv, q);
+        u32* yp = a.Y + ((static_cast<u64>(m) * a.polys + poly) * a.level + limb) * a.N + n0 + col;
+        *reinterpret_cast<uint4*>(yp) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(yp + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTcCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+u64 tc_packed_weight_bytes(u32 K, u32 M, u32 level) {
+  const u32 Mtiles = (M + kTcM - 1) / kTcM, Ksteps = (K + kTcK - 1) / kTcK;
+  return static_cast<u64>(level) * Mtiles * Ksteps * 4 * kTcPlaneA;
+}
+
+int launch_pack_weights_tc(const u32* W, uint8_t* Wp, u32 K, u32 M, u32 Mpad, u32 level, cudaStream_t s) {
+  const u32 Mtiles = (M + kTcM - 1) / kTcM, Ksteps = (K + kTcK - 1) / kTcK;
+  const u64 total = static_cast<u64>(level) * Mtiles * Ksteps * kTcM * kTcK;
+  k_pack_weights_tc<<<(total + 255) / 256, 256, 0, s>>>(W, Wp, K, Mpad, Mtiles, Ksteps, level);
+  return 1;
+}
+
+int launch_mac_dense_tc(MacDenseTcArgs a, const Basis& B, cudaStream_t s) {
+  a.Mtiles = (a.M + kTcM - 1) / kTcM;
+  a.Ksteps = (a.K + kTcK - 1) / kTcK;
+  if (a.N % kTcN != 0 || a.K > 8192 || a.K == 0) return -1;
+  // 512 TMEM columns per CTA: request enough shared memory that only one CTA is
+  // resident per SM, so no CTA spins in tcgen05.alloc.
+  constexpr size_t smem = sizeof(TcSmem) > 120 * 1024 ? sizeof(TcSmem) : 120 * 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mac_dense_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = true;
+  }
+  dim3 grid(a.N / kTcN, a.Mtiles, a.polys * a.level);
+  ProfScope ps("k_mac_dense_tc", s);
+  k_mac_dense_tc<<<grid, kTcThreads, smem, s>>>(a, B);
+  return 1;
+}
+
+}  // namespace hg

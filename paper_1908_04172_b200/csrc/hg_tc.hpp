@@ -1,0 +1,26 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Tensor-core (tcgen05.mma.kind::i8) dense modular contraction, hg_tc.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "hg_kernels.hpp"
+
+namespace hg {
+
+struct MacDenseTcArgs {
+  const u32* X;          // [K][x_polys][x_level][N]
+  u32* Y;                // [M][polys][level][N]
+  const uint8_t* Wp;     // packed weight byte planes (launch_pack_weights_tc)
+  const u32* bias;       // [level][Mpad] or nullptr
+  u32 K, M, Mpad, N, level, polys, x_level;
+  u32 Mtiles, Ksteps;    // filled by the launcher
+  u32 planes[kMaxPrimes];  // byte planes per limb: 3 if q < 2^24 else 4
+};
+
+u64 tc_packed_weight_bytes(u32 K, u32 M, u32 level);
+int launch_pack_weights_tc(const u32* W, uint8_t* Wp, u32 K, u32 M, u32 Mpad, u32 level, cudaStream_t s);
+int launch_mac_dense_tc(MacDenseTcArgs a, const Basis& B, cudaStream_t s);
+
+}  // namespace hg

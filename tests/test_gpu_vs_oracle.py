@@ -156,3 +156,35 @@ def test_toy_network_decrypts(env):
     h1 = (conv ** 2).reshape(-1, 18) @ w1
     want = (h1 ** 2) @ w2
     assert np.abs(dec - want).max() < 1e-3
+
+
+def test_dense_tensor_core_path_bit_exact(env):
+    """tcgen05.mma.kind::i8 byte-plane contraction (default) == IMAD path (HG_DENSE_TC=0) == oracle,
+    on the c1 layer (845 -> 100 + bias + rescale) and a K=100 -> M=10 layer (fc2 shape)."""
+    import json
+    import os
+    p, oc = env["p"], env["oc"]
+    os.environ["HG_DENSE_TC"] = "0"
+    try:
+        ctx = H.CkksContext(p["n"], p["chain"], p["special"], p["scale"])
+    finally:
+        del os.environ["HG_DENSE_TC"]
+    ctx_tc = env["ctx"]
+    for wl, K, M, level in ((W.dense_layer(), 845, 100, 6), (W.dense_layer(seed=9, k=100, m=10), 100, 10, 6)):
+        m = H.PlainModel.load(wl.manifest, wl.blob)
+        x = W.random_ciphertexts(p, K, seed=21 + K)
+        sc2 = p["scale"] ** 2 / p["chain"][level - 1]
+        nodes = {"input": (0, level, level, p["scale"]), "fc": (1, level, level - 1, sc2),
+                 "out": (0, level - 1, level - 1, sc2)}
+        outs = []
+        for c in (ctx, ctx_tc):
+            plan = H.RescalePlan.from_nodes(0, M, nodes)
+            outs.append(H.execute(c, m, plan, H.CipherTensor.from_words(c, x, p["scale"], shape=[K])).to_words())
+        assert np.array_equal(outs[0], outs[1]), (K, M)
+        man = json.loads(wl.manifest)
+        blob = np.frombuffer(wl.blob, dtype="<f4")
+        wm = man["weights"]
+        w = blob[wm["fc_w"]["offset"] // 4:][:K * M].reshape(K, M)
+        b = blob[wm["fc_b"]["offset"] // 4:][:M]
+        want = oc.dense(x, w, level, p["scale"], bias=b, rescale=True, outputs=[0, M - 1])
+        assert np.array_equal(outs[1][0], want[0]) and np.array_equal(outs[1][M - 1], want[1])
