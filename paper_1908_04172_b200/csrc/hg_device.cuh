@@ -356,6 +356,28 @@ struct Ntt {
 #pragma unroll
     for (int k = 0; k < 32; ++k) row[jA(tid, k)] = x[k];
   }
+  // Thread-major scratch layout "P" (for buffers only these kernels read back): thread
+  // tid's registers 4c..4c+3 form the 128-bit word c * T + tid, so each access is a
+  // fully coalesced LDG/STG.128.  Register k holds the same coefficient as in layout A.
+  template <typename W>
+  __device__ static __forceinline__ void gload_P(W (&x)[32], const W* __restrict__ row, u32 tid) {
+    static_assert(sizeof(W) == 4, "32-bit words");
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(row) + c * T + tid);
+      x[4 * c] = static_cast<W>(v.x); x[4 * c + 1] = static_cast<W>(v.y);
+      x[4 * c + 2] = static_cast<W>(v.z); x[4 * c + 3] = static_cast<W>(v.w);
+    }
+  }
+  template <typename W>
+  __device__ static __forceinline__ void gstore_P(const W (&x)[32], W* __restrict__ row, u32 tid) {
+    static_assert(sizeof(W) == 4, "32-bit words");
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      reinterpret_cast<uint4*>(row)[c * T + tid] =
+          make_uint4(static_cast<u32>(x[4 * c]), static_cast<u32>(x[4 * c + 1]), static_cast<u32>(x[4 * c + 2]),
+                     static_cast<u32>(x[4 * c + 3]));
+  }
   // Layout C groups of 2^CB consecutive words -> 128-bit accesses.
   __device__ static __forceinline__ void gload_C(u32 (&x)[32], const u32* __restrict__ row, u32 tid) {
 #pragma unroll

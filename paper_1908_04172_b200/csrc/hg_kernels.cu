@@ -370,13 +370,13 @@ __global__ void __launch_bounds__(kConvThreads) k_mac_conv(MacConvArgs a, Basis 
 //   K3 k_relin_moddown (ct, poly):    d + (acc - NTT(corr)) * P^-1 [+ rescale, with
 //                                      both corrections merged into one NTT per limb]
 // ===========================================================================
-template <int LOGN>
+template <int LOGN, int MD>
 __device__ __forceinline__ void load_c2(u32 (&y)[32], const RelinArgs& a, u64 ct, u32 j, const DevPrime& P,
                                         u32 tid) {
   using NT = Ntt<LOGN>;
   constexpr int N = NT::N;
   const u32 L = a.level;
-  if (a.mode == 0) {
+  if (MD == 0) {
     NT::gload_C(y, a.A + ((ct * 3 + 2) * L + j) * N, tid);
   } else {
     u32 b1[32];
@@ -387,7 +387,7 @@ __device__ __forceinline__ void load_c2(u32 (&y)[32], const RelinArgs& a, u64 ct
   }
 }
 
-template <int LOGN>
+template <int LOGN, int MD>
 __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_relin_digits(RelinArgs a, Basis B) {
   using NT = Ntt<LOGN>;
   constexpr int N = NT::N;
@@ -397,44 +397,39 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
   const u32 j = blockIdx.x % a.level;
   const DevPrime& P = B.p[j];
   u32 y[32];
-  load_c2<LOGN>(y, a, ct, j, P, tid);
+  load_c2<LOGN, MD>(y, a, ct, j, P, tid);
   NT::inverse(y, sm, tid, P);
-  NT::gstore_A(y, a.D + (ct * a.level + j) * N, tid);
+  NT::gstore_P(y, a.D + (ct * a.level + j) * N, tid);  // scratch: layout P
 }
 
-template <int LOGN>
+// SPECIAL: the CTAs of the special prime (grid = count), else limbs t < level
+// (grid = count * level); split so neither body carries the other's code.
+template <int LOGN, int MD, bool SPECIAL>
 __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_relin_keysw(RelinArgs a, Basis B) {
   using NT = Ntt<LOGN>;
   constexpr int N = NT::N;
   constexpr int T = NT::T;
   extern __shared__ u32 sm[];
-  u32* acc0 = sm + NT::SMEM_WORDS;  // thread-private slots [k * T + tid], layout C
-  u32* acc1 = acc0 + N;
+  // Accumulators: thread-private rows of 32 words (coefficients jC(tid, 0..31)), kept in
+  // [0, 2q) and moved as 128-bit chunks; chunk c of thread tid sits at slot c ^ (tid & 7),
+  // so the 8 threads of each quarter-warp hit distinct bank groups.
   const u32 tid = threadIdx.x;
+  uint4* acc0 = reinterpret_cast<uint4*>(sm + NT::SMEM_WORDS) + tid * 8;
+  uint4* acc1 = acc0 + N / 4;
+  const u32 sw = tid & 7;
   const u32 L = a.level;
-  const u64 ct = blockIdx.x / (L + 1);
-  const u32 t = blockIdx.x % (L + 1);
-  const bool special = (t == L);
+  const u64 ct = SPECIAL ? blockIdx.x : blockIdx.x / L;
+  const u32 t = SPECIAL ? L : blockIdx.x % L;
+  constexpr bool special = SPECIAL;
   const u32 bidx = special ? a.chain_len : t;  // basis index == key limb index
   const DevPrime& P = B.p[bidx];
-  const u32 q = P.q;
+  const u32 q = P.q, q2 = P.two_q;
 
-  // digit j+1 is loaded while digit j's key products are accumulated
-  u32 nx[32];
-  if (special || t != 0) NT::gload_A(nx, a.D + (ct * L + 0) * N, tid);
-  for (u32 j = 0; j < L; ++j) {
-    u32 y[32];
-    if (!special && j == t) {
-      // NTT_t(INTT_t(c2_t)) == c2_t: the digit's own limb needs no transform.
-      load_c2<LOGN>(y, a, ct, j, P, tid);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 32; ++k) y[k] = reduce32(nx[k], P);  // digit mod q_t, henet/ckks.hpp:463
-      NT::forward(y, sm, tid, P);
-    }
-    if (j + 1 < L && (special || j + 1 != t)) NT::gload_A(nx, a.D + (ct * L + j + 1) * N, tid);
+  // acc{0,1} += y * key[j][{0,1}][t]
+  auto mac = [&](const u32 (&y)[32], u32 j) {
     const uint2* k0 = a.key + ((static_cast<u64>(j) * 2 + 0) * (a.chain_len + 1) + bidx) * N;
     const uint2* k1 = a.key + ((static_cast<u64>(j) * 2 + 1) * (a.chain_len + 1) + bidx) * N;
+    auto madd = [&](u32 acc, u32 x, u32 w, u32 wsh) { return csub(acc + mul_shoup_lazy(x, w, wsh, q), q2); };
     // key rows are L2-resident but far: issue a round of 4 pair-loads before using any
 #pragma unroll
     for (int qr = 0; qr < 4; ++qr) {
@@ -446,60 +441,96 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
         kv1[i] = __ldg(reinterpret_cast<const uint4*>(k1 + jj));
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int k = qr * 8 + 2 * i;
-        const u32 p00 = mul_shoup(y[k], kv0[i].x, kv0[i].y, q), p01 = mul_shoup(y[k + 1], kv0[i].z, kv0[i].w, q);
-        const u32 p10 = mul_shoup(y[k], kv1[i].x, kv1[i].y, q), p11 = mul_shoup(y[k + 1], kv1[i].z, kv1[i].w, q);
-        if (j == 0) {
-          acc0[k * T + tid] = p00;
-          acc0[(k + 1) * T + tid] = p01;
-          acc1[k * T + tid] = p10;
-          acc1[(k + 1) * T + tid] = p11;
-        } else {
-          acc0[k * T + tid] = addmod(acc0[k * T + tid], p00, q);
-          acc0[(k + 1) * T + tid] = addmod(acc0[(k + 1) * T + tid], p01, q);
-          acc1[k * T + tid] = addmod(acc1[k * T + tid], p10, q);
-          acc1[(k + 1) * T + tid] = addmod(acc1[(k + 1) * T + tid], p11, q);
-        }
+      for (int h = 0; h < 2; ++h) {
+        const int k = qr * 8 + 4 * h;
+        const u32 c = (k >> 2) ^ sw;
+        uint4 A0 = acc0[c], A1 = acc1[c];
+        const uint4 u0 = kv0[2 * h], v0 = kv0[2 * h + 1], u1 = kv1[2 * h], v1 = kv1[2 * h + 1];
+        A0.x = madd(A0.x, y[k], u0.x, u0.y);
+        A0.y = madd(A0.y, y[k + 1], u0.z, u0.w);
+        A0.z = madd(A0.z, y[k + 2], v0.x, v0.y);
+        A0.w = madd(A0.w, y[k + 3], v0.z, v0.w);
+        A1.x = madd(A1.x, y[k], u1.x, u1.y);
+        A1.y = madd(A1.y, y[k + 1], u1.z, u1.w);
+        A1.z = madd(A1.z, y[k + 2], v1.x, v1.y);
+        A1.w = madd(A1.w, y[k + 3], v1.z, v1.w);
+        acc0[c] = A0;
+        acc1[c] = A1;
       }
     }
+  };
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc0[c ^ sw] = acc1[c ^ sw] = make_uint4(0, 0, 0, 0);
+  // Digits j != t (all j for the special prime): NTT_t(digit_j mod q_t), digit j+1
+  // loaded during digit j's key products.  The loop body is branch-free: a j == t
+  // test inside it makes ptxas duplicate the transform (instruction-cache misses).
+  const u32 skip = special ? L : t;
+  const u32 R = special ? L : L - 1;
+  u32 nx[32];
+  NT::gload_P(nx, a.D + (ct * L + (skip == 0 ? 1 : 0)) * N, tid);
+#pragma unroll 1
+  for (u32 r = 0; r < R; ++r) {
+    const u32 j = r + (r >= skip ? 1 : 0);
+    u32 y[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) y[k] = reduce32(nx[k], P);  // digit mod q_t, henet/ckks.hpp:463
+    NT::forward(y, sm, tid, P);
+    const u32 jn = min(r + 1 + (r + 1 >= skip ? 1 : 0), L - 1);
+    NT::gload_P(nx, a.D + (ct * L + jn) * N, tid);
+    mac(y, j);
   }
-  if (!special) {
+  if constexpr (!special) {
+    // NTT_t(INTT_t(c2_t)) == c2_t: the digit's own limb needs no transform.
+    u32 y[32];
+    load_c2<LOGN, MD>(y, a, ct, t, P, tid);
+    mac(y, t);
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      const u32* acc = c ? acc1 : acc0;
+      const uint4* acc = c ? acc1 : acc0;
       u32* dst = a.ACC + ((ct * 2 + c) * L + t) * N;
 #pragma unroll
       for (int k = 0; k < 32; k += 4) {
-        *reinterpret_cast<uint4*>(dst + NT::jC(tid, k)) =
-            make_uint4(acc[k * T + tid], acc[(k + 1) * T + tid], acc[(k + 2) * T + tid], acc[(k + 3) * T + tid]);
+        uint4 v = acc[(k >> 2) ^ sw];
+        v.x = csub(v.x, q);
+        v.y = csub(v.y, q);
+        v.z = csub(v.z, q);
+        v.w = csub(v.w, q);
+        *reinterpret_cast<uint4*>(dst + NT::jC(tid, k)) = v;
       }
     }
   } else {
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) {
-      const u32* acc = c ? acc1 : acc0;
+      const uint4* acc = c ? acc1 : acc0;
       u32 y[32];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) y[k] = acc[k * T + tid];
+      for (int k = 0; k < 32; k += 4) {
+        const uint4 v = acc[(k >> 2) ^ sw];
+        y[k] = csub(v.x, q);
+        y[k + 1] = csub(v.y, q);
+        y[k + 2] = csub(v.z, q);
+        y[k + 3] = csub(v.w, q);
+      }
       NT::inverse(y, sm, tid, P);
-      i32* cd = a.CORR + (ct * 2 + c) * N;
+      i32 cr[32];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) cd[NT::jA(tid, k)] = centered_round_rem(y[k], P);
+      for (int k = 0; k < 32; ++k) cr[k] = centered_round_rem(y[k], P);
+      NT::gstore_P(cr, a.CORR + (ct * 2 + c) * N, tid);  // scratch: layout P
     }
   }
 }
 
 // d0 = c0 (mode 0) or a0*b0; d1 = c1 (mode 0) or a0*b1 + a1*b0 (henet/ckks.hpp:407-437), four
 // consecutive coefficients j..j+3 of limb i.
+template <int MD>  // 0: three-poly input, 1: square (A == Bm), 2: product A x Bm
 __device__ __forceinline__ uint4 load_d4(const RelinArgs& a, u64 ct, u32 poly, u32 i, u32 j, u32 N,
                                          const DevPrime& P) {
   const u32 L = a.level;
   auto ld = [&](const u32* base, u32 polys, u32 p) {
     return __ldg(reinterpret_cast<const uint4*>(base + ((ct * polys + p) * L + i) * static_cast<u64>(N) + j));
   };
-  if (a.mode == 0) return ld(a.A, 3, poly);
-  if (a.A == a.Bm) {
+  if (MD == 0) return ld(a.A, 3, poly);
+  if (MD == 1) {
     // square (henet/ckks.hpp:424-437): d0 = c0^2, d1 = c0 c1 + c0 c1
     const uint4 x = ld(a.A, 2, 0), y = poly ? ld(a.A, 2, 1) : x;
     uint4 d = make_uint4(mulmod(x.x, y.x, P), mulmod(x.y, y.y, P), mulmod(x.z, y.z, P), mulmod(x.w, y.w, P));
@@ -523,93 +554,99 @@ __device__ __forceinline__ uint4 load_d4(const RelinArgs& a, u64 ct, u32 poly, u
   return d;
 }
 
-template <int LOGN>
+// MD selects the d0/d1 source (load_d4), RS whether the rescale is merged: one
+// instantiation per combination keeps each kernel body inside the instruction cache.
+template <int LOGN, int MD, bool RS>
 __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_relin_moddown(RelinArgs a, Basis B) {
   using NT = Ntt<LOGN>;
   constexpr int N = NT::N;
   constexpr int T = NT::T;
   extern __shared__ u32 sm[];
-  i32* cps = reinterpret_cast<i32*>(sm + NT::SMEM_WORDS);  // special-prime correction, slots [k * T + tid]
-  i32* crs = cps + N;                                       // rescale correction
+  // special-prime (cps) and rescale (crs) corrections: thread-private 32-word rows,
+  // 128-bit chunks at slot c ^ (tid & 7) (see k_relin_keysw)
+  int4* cps = reinterpret_cast<int4*>(sm + NT::SMEM_WORDS) + threadIdx.x * 8;
+  int4* crs = cps + N / 4;
+  const u32 sw = threadIdx.x & 7;
   const u32 tid = threadIdx.x;
   const u32 L = a.level;
   const u64 ct = blockIdx.x >> 1;
   const u32 poly = blockIdx.x & 1;
-  const u32 Lout = a.rescale ? L - 1 : L;
+  const u32 Lout = RS ? L - 1 : L;
   u32* dst = a.out + (ct * 2 + poly) * static_cast<u64>(Lout) * N;
   const u32* accp = a.ACC + (ct * 2 + poly) * static_cast<u64>(L) * N;
   {
-    const i32* cs = a.CORR + (ct * 2 + poly) * N;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) cps[k * T + tid] = cs[NT::jA(tid, k)];
+    for (int c = 0; c < 8; ++c)
+      cps[c ^ sw] = __ldg(reinterpret_cast<const int4*>(a.CORR + (ct * 2 + poly) * N) + c * T + tid);  // layout P
   }
-  u32 z[32];
-  // top limb first: its mod-down result feeds the rescale correction
-  {
-    const u32 i = L - 1;
+  // One loop, one inlined forward transform (the kernel body otherwise overflows the
+  // instruction cache): iteration 0 is the top limb L-1, whose mod-down result feeds the
+  // rescale correction; iterations 1.. are limbs 0..L-2.
+#pragma unroll 1
+  for (u32 it = 0; it < L; ++it) {
+    const bool top = (it == 0);
+    const u32 i = top ? L - 1 : it - 1;
     const DevPrime& Pi = B.p[i];
     const u32 q = Pi.q, pv = a.pinvP[i], ps = a.pinvP_sh[i];
+    u32 z[32];
+    if (RS && !top) {
 #pragma unroll
-    for (int k = 0; k < 32; ++k) z[k] = signed_residue(cps[k * T + tid], Pi);
-    NT::forward(z, sm, tid, Pi);
-#pragma unroll
-    for (int k = 0; k < 32; k += 4) {
-      const u32 j = NT::jC(tid, k);
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(accp + static_cast<u64>(i) * N + j));
-      const uint4 d = load_d4(a, ct, poly, i, j, N, Pi);
-      z[k] = addmod(d.x, mul_shoup(v.x + q - z[k], pv, ps, q), q);
-      z[k + 1] = addmod(d.y, mul_shoup(v.y + q - z[k + 1], pv, ps, q), q);
-      z[k + 2] = addmod(d.z, mul_shoup(v.z + q - z[k + 2], pv, ps, q), q);
-      z[k + 3] = addmod(d.w, mul_shoup(v.w + q - z[k + 3], pv, ps, q), q);
-    }
-    if (!a.rescale) {
-      NT::gstore_C(z, dst + static_cast<u64>(i) * N, tid);
-    } else {
-      NT::inverse(z, sm, tid, Pi);
-#pragma unroll
-      for (int k = 0; k < 32; ++k) crs[k * T + tid] = centered_round_rem(z[k], Pi);
-    }
-  }
-  for (u32 i = 0; i + 1 < L; ++i) {
-    const DevPrime& Pi = B.p[i];
-    const u32 q = Pi.q, pv = a.pinvP[i], ps = a.pinvP_sh[i];
-    if (a.rescale) {
-#pragma unroll
-      for (int k = 0; k < 32; ++k)
-        z[k] = addmod(mul_shoup(signed_residue(cps[k * T + tid], Pi), pv, ps, q),
-                      signed_residue(crs[k * T + tid], Pi), q);
+      for (int c = 0; c < 8; ++c) {
+        const int4 u = cps[c ^ sw], v = crs[c ^ sw];
+        z[4 * c] = addmod(mul_shoup(signed_residue(u.x, Pi), pv, ps, q), signed_residue(v.x, Pi), q);
+        z[4 * c + 1] = addmod(mul_shoup(signed_residue(u.y, Pi), pv, ps, q), signed_residue(v.y, Pi), q);
+        z[4 * c + 2] = addmod(mul_shoup(signed_residue(u.z, Pi), pv, ps, q), signed_residue(v.z, Pi), q);
+        z[4 * c + 3] = addmod(mul_shoup(signed_residue(u.w, Pi), pv, ps, q), signed_residue(v.w, Pi), q);
+      }
     } else {
 #pragma unroll
-      for (int k = 0; k < 32; ++k) z[k] = signed_residue(cps[k * T + tid], Pi);
+      for (int c = 0; c < 8; ++c) {
+        const int4 u = cps[c ^ sw];
+        z[4 * c] = signed_residue(u.x, Pi);
+        z[4 * c + 1] = signed_residue(u.y, Pi);
+        z[4 * c + 2] = signed_residue(u.z, Pi);
+        z[4 * c + 3] = signed_residue(u.w, Pi);
+      }
     }
     // accumulator loads issued ahead of the transform; d products computed after it
     uint4 vv[8];
 #pragma unroll
     for (int g = 0; g < 8; ++g) vv[g] = __ldg(reinterpret_cast<const uint4*>(accp + static_cast<u64>(i) * N + NT::jC(tid, 4 * g)));
     NT::forward(z, sm, tid, Pi);
-    const u32 lv = a.pinvL[i], ls = a.pinvL_sh[i];
-    u32* out_i = dst + static_cast<u64>(i) * N;
     uint4 dd[8];
 #pragma unroll
-    for (int g = 0; g < 8; ++g) dd[g] = load_d4(a, ct, poly, i, NT::jC(tid, 4 * g), N, Pi);
+    for (int g = 0; g < 8; ++g) dd[g] = load_d4<MD>(a, ct, poly, i, NT::jC(tid, 4 * g), N, Pi);
+    u32* out_i = dst + static_cast<u64>(i) * N;
+    if (RS && !top) {
+      const u32 lv = a.pinvL[i], ls = a.pinvL_sh[i];
 #pragma unroll
-    for (int k = 0; k < 32; k += 4) {
-      const u32 j = NT::jC(tid, k);
-      const uint4 d = dd[k >> 2];
-      const uint4 v = vv[k >> 2];
-      uint4 o;
-      if (a.rescale) {
+      for (int k = 0; k < 32; k += 4) {
+        const uint4 d = dd[k >> 2], v = vv[k >> 2];
+        uint4 o;
         o.x = mul_shoup(addmod(d.x, mul_shoup(v.x, pv, ps, q), q) + q - z[k], lv, ls, q);
         o.y = mul_shoup(addmod(d.y, mul_shoup(v.y, pv, ps, q), q) + q - z[k + 1], lv, ls, q);
         o.z = mul_shoup(addmod(d.z, mul_shoup(v.z, pv, ps, q), q) + q - z[k + 2], lv, ls, q);
         o.w = mul_shoup(addmod(d.w, mul_shoup(v.w, pv, ps, q), q) + q - z[k + 3], lv, ls, q);
-      } else {
-        o.x = addmod(d.x, mul_shoup(v.x + q - z[k], pv, ps, q), q);
-        o.y = addmod(d.y, mul_shoup(v.y + q - z[k + 1], pv, ps, q), q);
-        o.z = addmod(d.z, mul_shoup(v.z + q - z[k + 2], pv, ps, q), q);
-        o.w = addmod(d.w, mul_shoup(v.w + q - z[k + 3], pv, ps, q), q);
+        *reinterpret_cast<uint4*>(out_i + NT::jC(tid, k)) = o;
       }
-      *reinterpret_cast<uint4*>(out_i + j) = o;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) {
+        const uint4 d = dd[k >> 2], v = vv[k >> 2];
+        z[k] = addmod(d.x, mul_shoup(v.x + q - z[k], pv, ps, q), q);
+        z[k + 1] = addmod(d.y, mul_shoup(v.y + q - z[k + 1], pv, ps, q), q);
+        z[k + 2] = addmod(d.z, mul_shoup(v.z + q - z[k + 2], pv, ps, q), q);
+        z[k + 3] = addmod(d.w, mul_shoup(v.w + q - z[k + 3], pv, ps, q), q);
+      }
+      if (!RS) {
+        NT::gstore_C(z, out_i, tid);
+      } else {
+        NT::inverse(z, sm, tid, Pi);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          crs[c ^ sw] = make_int4(centered_round_rem(z[4 * c], Pi), centered_round_rem(z[4 * c + 1], Pi),
+                                  centered_round_rem(z[4 * c + 2], Pi), centered_round_rem(z[4 * c + 3], Pi));
+      }
     }
   }
 }
@@ -990,17 +1027,27 @@ int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s) {
   HG_LOGN_SWITCH(logn, {
     const size_t sm1 = sizeof(u32) * Ntt<LN>::SMEM_WORDS, sm3 = sm1 + 2 * (sizeof(u32) << LN);
     const int T = 1 << (LN - 5);
-    set_smem(k_relin_digits<LN>, sm1);
-    set_smem(k_relin_keysw<LN>, sm3);
-    set_smem(k_relin_moddown<LN>, sm3);
+    const bool prod = a.mode != 0;
+    auto dk = prod ? k_relin_digits<LN, 1> : k_relin_digits<LN, 0>;
+    auto kn = prod ? k_relin_keysw<LN, 1, false> : k_relin_keysw<LN, 0, false>;
+    auto ks = prod ? k_relin_keysw<LN, 1, true> : k_relin_keysw<LN, 0, true>;
+    set_smem(dk, sm1);
+    set_smem(kn, sm3);
+    set_smem(ks, sm3);
     { ProfScope ps("k_relin_digits", s);
-    k_relin_digits<LN><<<a.count * a.level, T, sm1, s>>>(a, B);
+    dk<<<a.count * a.level, T, sm1, s>>>(a, B);
     }
     { ProfScope ps("k_relin_keysw", s);
-    k_relin_keysw<LN><<<a.count * (a.level + 1), T, sm3, s>>>(a, B);
+    ks<<<a.count, T, sm3, s>>>(a, B);
+    kn<<<a.count * a.level, T, sm3, s>>>(a, B);
     }
     { ProfScope ps("k_relin_moddown", s);
-    k_relin_moddown<LN><<<a.count * 2, T, sm3, s>>>(a, B);
+    const int md = a.mode == 0 ? 0 : (a.A == a.Bm ? 1 : 2);
+    auto mdk = md == 0 ? (a.rescale ? k_relin_moddown<LN, 0, true> : k_relin_moddown<LN, 0, false>)
+             : md == 1 ? (a.rescale ? k_relin_moddown<LN, 1, true> : k_relin_moddown<LN, 1, false>)
+                       : (a.rescale ? k_relin_moddown<LN, 2, true> : k_relin_moddown<LN, 2, false>);
+    set_smem(mdk, sm3);
+    mdk<<<a.count * 2, T, sm3, s>>>(a, B);
     }
   });
   return 3;
