@@ -117,35 +117,45 @@ class Clocks:
 # NTT butterfly = 3, modmul = 3) and compulsory HBM bytes (u32 residues).
 # ---------------------------------------------------------------------------
 def work_model(n=8192):
+    """Algorithmic work of one c2 step per kernel: (modmul, mac, bytes).
+
+    modmul = Shoup modular products (one per NTT butterfly + one per point-wise
+    product), the unit the NTT-family kernels are bound by: each is IMAD.HI + 2 IMAD,
+    and IMAD.HI issues at a quarter of the FFMA rate on sm_100 (scripts/int_pipe_probe.cu).
+    mac = 32x32->64-bit multiply-accumulates (IMAD.WIDE) of the MAC kernels.
+    bytes = compulsory HBM traffic (inputs read once, outputs written once)."""
     import math
     logn = int(math.log2(n))
     bf = n // 2 * logn  # butterflies per transform
     W = 4               # bytes per residue
     m = {}
 
-    def add(name, ops, byts):
-        o, b = m.get(name, (0.0, 0.0))
-        m[name] = (o + ops, b + byts)
+    def add(name, modmul=0.0, mac=0.0, byts=0.0):
+        o = m.get(name, (0.0, 0.0, 0.0))
+        m[name] = (o[0] + modmul, o[1] + mac, o[2] + byts)
 
     # conv1: 784 inputs at level 6 -> 845 outputs, 20480 valid taps
     L = 6
-    add("k_mac_conv", 20480 * 2 * L * n, (784 + 845) * 2 * L * n * W)
+    add("k_mac_conv", mac=20480 * 2 * L * n, byts=(784 + 845) * 2 * L * n * W)
     # rescale after conv1: 845 cts at level 6 -> 5; after fc1: 100 cts 4 -> 3
+    # (per poly: INTT of the dropped limb + NTT of l-1 corrections, then l-1 scalings)
     for C_, l in ((845, 6), (100, 4)):
-        add("k_rescale", C_ * (2 * l * bf * 3 + 2 * (l - 1) * n * 3), C_ * (2 * l + 2 * (l - 1)) * n * W)
+        add("k_rescale", modmul=C_ * (2 * l * bf + 2 * (l - 1) * n), byts=C_ * (2 * l + 2 * (l - 1)) * n * W)
     # square+relin+rescale: act1 845 cts at level 5, act2 100 cts at level 3
     for C_, l in ((845, 5), (100, 3)):
-        add("k_relin_digits", C_ * (l * bf * 3 + l * n * 3), C_ * 2 * l * n * W)
+        add("k_relin_digits", modmul=C_ * (l * bf + l * n), byts=C_ * 2 * l * n * W)
         key_bytes = 2 * l * (l + 1) * n * 8
-        add("k_relin_keysw", C_ * ((l * l + 2) * bf * 3 + 2 * l * (l + 1) * n * 3),
-            C_ * (l * n * W + 2 * l * n * W + 2 * n * W) + key_bytes)
-        add("k_relin_moddown", C_ * (2 * (l + 1) * bf * 3 + (6 * l - 2) * n * 3),
-            C_ * (2 * l * n * W + 2 * l * n * W + 2 * n * W + 2 * (l - 1) * n * W))
+        # l(l-1) + l forward transforms (digit j under prime t != j, and the special prime),
+        # 2 inverse transforms of the special accumulators, 2 key products per digit/limb
+        add("k_relin_keysw", modmul=C_ * ((l * l + 2) * bf + 2 * l * (l + 1) * n),
+            byts=C_ * (l * n * W + 2 * l * n * W + 2 * n * W) + key_bytes)
+        add("k_relin_moddown", modmul=C_ * (2 * (l + 1) * bf + (6 * l - 2) * n),
+            byts=C_ * (2 * l * n * W + 2 * l * n * W + 2 * n * W + 2 * (l - 1) * n * W))
     # fc1 845 -> 100 at level 4, fc2 100 -> 10 at level 2
     dense_macs = 845 * 100 * 2 * 4 * n + 100 * 10 * 2 * 2 * n
     dense_bytes = (845 + 100) * 2 * 4 * n * W + (100 + 10) * 2 * 2 * n * W
-    add("k_mac_dense", dense_macs, dense_bytes)
-    add("k_mac_dense_tc", dense_macs, dense_bytes)
+    add("k_mac_dense", mac=dense_macs, byts=dense_bytes)
+    add("k_mac_dense_tc", mac=dense_macs, byts=dense_bytes)
     return m
 
 
@@ -342,46 +352,56 @@ def b200_run(args, ws, rank, local):
     H.prof_enable(False)
     prof = H.prof_report()
     hbm_gbs, hbm_src = load_peaks()
-    int_peak = H.bench_int_peak(local, 0)
-    int_wide = H.bench_int_peak(local, 1)
+    shoup_peak = H.bench_int_peak(local, 3)  # Shoup modular products / s
+    wide_peak = H.bench_int_peak(local, 1)   # IMAD.WIDE MACs / s
+    imad_peak = H.bench_int_peak(local, 0)
     model_w = work_model(p["n"])
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
+    i8_peak = 2 * float(peaks["bf16_tflops"]) * 1e12 / 2  # int8 dense MAC/s = 2 x bf16 FLOP/s / 2
     kernels = {}
     total_ms = sum(v["ms"] for v in prof.values()) / n_prof
     for name, v in prof.items():
         ms = v["ms"] / n_prof
-        ops, byts = model_w.get(name, (0.0, 0.0))
-        t_int = ops / int_peak * 1e3
+        mm, mac, byts = model_w.get(name, (0.0, 0.0, 0.0))
+        t_int = (mm / shoup_peak + mac / wide_peak) * 1e3
         t_hbm = byts / (hbm_gbs * 1e9) * 1e3
-        kernels[name] = {"ms_per_step": ms, "launches_per_step": v["launches"] / n_prof,
-                         "share": ms / total_ms if total_ms else 0,
-                         "int_tops": ops / (ms * 1e-3) / 1e12 if ms else 0,
-                         "hbm_gbs": byts / (ms * 1e-3) / 1e9 if ms else 0,
-                         "roofline_frac": max(t_int, t_hbm) / ms if ms else 0,
-                         "bound": "int32" if t_int >= t_hbm else "hbm"}
-    if "k_mac_dense_tc" in kernels:
-        # tensor-core roofline of the int8 contraction: int8 dense peak = 2 x the measured bf16 GEMM
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
-        i8_peak = 2 * float(peaks["bf16_tflops"]) * 1e12 / 2  # MAC/s
-        k = kernels["k_mac_dense_tc"]
-        k["tensor_int8_macs_per_s"] = tc_work() / (k["ms_per_step"] * 1e-3)
-        k["tensor_frac"] = k["tensor_int8_macs_per_s"] / i8_peak
-        k["tensor_peak_note"] = "int8 dense = 2 x measured bf16 (MEASURED_PEAKS.json)"
+        k = {"ms_per_step": ms, "launches_per_step": v["launches"] / n_prof,
+             "share": ms / total_ms if total_ms else 0,
+             "modmul_t_per_s": mm / (ms * 1e-3) / 1e12 if ms else 0,
+             "mac_t_per_s": mac / (ms * 1e-3) / 1e12 if ms else 0,
+             "hbm_gbs": byts / (ms * 1e-3) / 1e9 if ms else 0,
+             "int32_floor_ms": t_int, "hbm_floor_ms": t_hbm,
+             "roofline_frac": max(t_int, t_hbm) / ms if ms else 0,
+             "bound": "int32" if t_int >= t_hbm else "hbm"}
+        if name == "k_mac_dense_tc":
+            # the contraction runs on the tensor cores: its roofline is int8 MMA throughput
+            t_tc = tc_work() / i8_peak * 1e3
+            k.update({"bound": "tensor", "tensor_int8_macs_per_s": tc_work() / (ms * 1e-3),
+                      "tensor_floor_ms": t_tc, "roofline_frac": max(t_tc, t_hbm) / ms if ms else 0,
+                      "tensor_peak_note": "int8 dense = 2 x measured bf16 (MEASURED_PEAKS.json)"})
+        kernels[name] = k
     dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
     dk = kernels[dom]
-    ops, byts = model_w.get(dom, (0.0, 0.0))
-    if dk["bound"] == "int32":
-        roof = {"bound": "int32", "kernel": dom, "achieved": dk["int_tops"], "peak": int_peak / 1e12,
-                "unit": "Tops/s (IMAD-class)", "frac": dk["int_tops"] / (int_peak / 1e12),
-                "peak_source": "measured register-only IMAD probe (hg_bench_int_peak kind 0) on this GPU",
-                "imad_wide_peak": int_wide / 1e12, "hbm_gbs_achieved": dk["hbm_gbs"], "hbm_peak": hbm_gbs,
-                "traffic": None}
+    mm, mac, byts = model_w.get(dom, (0.0, 0.0, 0.0))
+    if dk["bound"] == "int32" and mm >= mac:
+        roof = {"bound": "int32", "kernel": dom, "achieved": dk["modmul_t_per_s"], "peak": shoup_peak / 1e12,
+                "unit": "T modmul/s (Shoup: IMAD.HI + 2 IMAD)", "frac": dk["modmul_t_per_s"] / (shoup_peak / 1e12),
+                "peak_source": "measured register-only Shoup-product probe (hg_bench_int_peak kind 3) on this GPU",
+                "imad_peak": imad_peak / 1e12, "imad_wide_peak": wide_peak / 1e12,
+                "hbm_gbs_achieved": dk["hbm_gbs"], "hbm_peak": hbm_gbs, "traffic": None}
+    elif dk["bound"] == "int32":
+        roof = {"bound": "int32", "kernel": dom, "achieved": dk["mac_t_per_s"], "peak": wide_peak / 1e12,
+                "unit": "T MAC/s (IMAD.WIDE)", "frac": dk["mac_t_per_s"] / (wide_peak / 1e12),
+                "peak_source": "measured register-only IMAD.WIDE probe (hg_bench_int_peak kind 1) on this GPU",
+                "hbm_gbs_achieved": dk["hbm_gbs"], "hbm_peak": hbm_gbs, "traffic": None}
     else:
         roof = {"bound": "hbm", "kernel": dom, "achieved": dk["hbm_gbs"], "peak": hbm_gbs, "unit": "GB/s",
                 "frac": dk["hbm_gbs"] / hbm_gbs, "peak_source": hbm_src, "traffic": None}
-    roof["algorithmic_per_step"] = {"imad_ops": ops, "hbm_bytes": byts}
-    whole_t = sum(v[0] for k_, v in model_w.items() if k_ != "k_mac_dense_tc") / int_peak * 1e3
-    roof["whole_step"] = {"int32_floor_ms": whole_t, "measured_ms": ms_per_step,
+    roof["algorithmic_per_step"] = {"modmul": mm, "mac": mac, "hbm_bytes": byts}
+    whole_t = sum(max(k["int32_floor_ms"] if k["bound"] != "tensor" else k["tensor_floor_ms"], k["hbm_floor_ms"])
+                  for k in kernels.values())
+    roof["whole_step"] = {"floor_ms": whole_t, "measured_ms": ms_per_step,
                           "frac": whole_t / ms_per_step if ms_per_step else 0}
 
     cpu = None

@@ -844,7 +844,9 @@ __global__ void k_mags_to_residues(const ulonglong2* mags, u64 count_n, u32 n, u
 // ===========================================================================
 template <int KIND>
 __global__ void k_imad_probe(u64* sink, u32 iters, u32 seed) {
-  // KIND 0: IMAD (mad.lo.u32), 1: IMAD.WIDE (mad.wide.u32), 2: IMAD.HI (mul.hi.u32)
+  // KIND 0: IMAD (mad.lo.u32), 1: IMAD.WIDE (mad.wide.u32), 2: IMAD.HI (mul.hi.u32),
+  // 3: Shoup lazy modular product (IMAD.HI + 2 IMAD; IMAD.HI/IMAD.WIDE issue at a
+  //    quarter of the FFMA rate on sm_100, IMAD at half, so this is the NTT's unit)
   u32 a[8];
   u64 c[8];
 #pragma unroll
@@ -861,10 +863,16 @@ __global__ void k_imad_probe(u64* sink, u32 iters, u32 seed) {
           u32 lo = static_cast<u32>(c[i]);
           asm volatile("mad.lo.u32 %0, %1, %2, %0;" : "+r"(lo) : "r"(a[i]), "r"(b));
           c[i] = lo;
-        } else {
+        } else if (KIND == 2) {
           u32 lo = static_cast<u32>(c[i]);
           asm volatile("mul.hi.u32 %0, %1, %2;" : "=r"(lo) : "r"(a[i] ^ lo), "r"(b));
           c[i] = lo;
+        } else {  // KIND 3: Shoup lazy product chain x <- x*w - hi(x*wsh)*q (IMAD.HI + 2 IMAD)
+          u32 x = static_cast<u32>(c[i]), h, lo;
+          asm volatile("mul.hi.u32 %0, %1, %2;" : "=r"(h) : "r"(x), "r"(a[i]));
+          asm volatile("mul.lo.u32 %0, %1, %2;" : "=r"(lo) : "r"(x), "r"(b));
+          asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(x) : "r"(h), "r"(0xc0004001u), "r"(lo));
+          c[i] = x;
         }
       }
     }
@@ -1125,7 +1133,8 @@ double bench_int_peak(int device, int kind) {
   auto launch = [&](u32 it) {
     if (kind == 0) k_imad_probe<0><<<blocks, threads>>>(sink, it, 5);
     else if (kind == 1) k_imad_probe<1><<<blocks, threads>>>(sink, it, 5);
-    else k_imad_probe<2><<<blocks, threads>>>(sink, it, 5);
+    else if (kind == 2) k_imad_probe<2><<<blocks, threads>>>(sink, it, 5);
+    else k_imad_probe<3><<<blocks, threads>>>(sink, it, 5);
   };
   launch(16);
   cudaEvent_t e0, e1;
