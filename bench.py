@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5b"],
+                    help="c2 (default, the BASELINE metric) or c5b: wide dense 4096->4096 at N=16384, "
+                         "output-sharded over the ranks with an NCCL all-gather")
     return ap.parse_args()
 
 
@@ -428,9 +431,163 @@ def b200_run(args, ws, rank, local):
     return 0
 
 
+# ---------------------------------------------------------------------------
+# Config 5b: wide dense layer, output-neuron sharded
+# ---------------------------------------------------------------------------
+C5B_K = C5B_M = 4096
+C5B_IMAGES = 8192  # images per ciphertext at N=16384 (one pass of the layer)
+C5B_METRIC = "encrypted images/sec, c5b wide dense 4096->4096 N=16384, output-sharded + all-gather"
+
+
+def c5b_config(ws):
+    return {"workload": f"c5b wide dense {C5B_K}->{C5B_M}, one rescale per output (patched plan, as c1)",
+            "ring": "N=16384, chain [40,30x7]+40-bit special, scale 2^30 (u64 residue storage)",
+            "images_per_step": C5B_IMAGES, "input_ciphertexts": C5B_K,
+            "l2": "input tensor 8.6 GB > 126 MB L2 (no flush needed)",
+            "parallelism": f"output-neuron sharded x{ws}, all inputs on every rank, NCCL all-gather of outputs"}
+
+
+def c5b_work(n=16384, L=8):
+    """(mac, bytes) of the layer: K*M*2*L*N MACs (limb 0 40-bit: 128-bit MACs); u64 words."""
+    return C5B_K * C5B_M * 2 * L * n, (C5B_K * 2 * L + C5B_M * 2 * (L - 1)) * n * 8
+
+
+def c5b_reference_sample(cores):
+    """Reference execute() on a K_s x M_s slice of the layer (same parameters, per-tap cost
+    is uniform), extrapolated to K x M (subset of outputs, labelled)."""
+    from oracle import refbind as R
+    from paper_1908_04172_b200 import workloads as Wk
+    p = Wk.N16384
+    ks, ms = 128, max(cores, 4)
+    wl = Wk.wide_dense(k=ks, m=ms)
+    ref = R.RefContext(p["n"], p["chain"], p["special"], p["scale"])
+    x = Wk.random_ciphertexts(p, ks, seed=31)
+    _, _, st = ref.execute(None, wl.manifest, wl.blob, x, p["scale"], patch=True, threads=cores)
+    ms_full = st["exec_ms"] * (C5B_K * C5B_M) / (ks * ms)
+    return C5B_IMAGES / (ms_full / 1e3), f"K={ks} x M={ms} slice of the layer through henet::execute " \
+        f"(oracle/_ref, {st['exec_ms'] / 1e3:.1f} s), extrapolated x{C5B_K * C5B_M // (ks * ms)} to 4096x4096"
+
+
+def c5b_run(args, ws, rank, local):
+    import torch
+    from paper_1908_04172_b200 import henet as H
+    from paper_1908_04172_b200 import workloads as Wk
+    from paper_1908_04172_b200.sharded import OutputShardedDense
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p = Wk.N16384
+    ctx = H.CkksContext(p["n"], p["chain"], p["special"], p["scale"], device=local)
+    L = len(p["chain"])
+    layer = OutputShardedDense(ctx, Wk.wide_dense_weights(k=C5B_K, m=C5B_M), rank, ws)
+    # inputs generated on the device (seeded uniform residues per limb; 8.6 GB)
+    x = H.CipherTensor(ctx, C5B_K, 2, L, p["scale"], shape=[C5B_K])
+    ctx.synchronize()
+    xv = x.torch_view(local).view(C5B_K, 2, L, p["n"])
+    g = torch.Generator(device=f"cuda:{local}")
+    g.manual_seed(41)  # identical inputs on every rank
+    for i, q in enumerate(p["chain"]):
+        xv[:, :, i, :] = torch.randint(0, q, (C5B_K, 2, p["n"]), device=f"cuda:{local}", dtype=torch.int64,
+                                       generator=g)
+    torch.cuda.synchronize()
+    ext = torch.cuda.ExternalStream(ctx.stream(), device=local)
+    cur = torch.cuda.current_stream(local)
+    clocks = Clocks(local)
+    for _ in range(max(args.warmup, 3)):
+        out = layer.forward(x)
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    steps = max(1, min(args.steps, 5))
+    l0 = ctx.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(ext)
+    for _ in range(steps):
+        out = layer.forward(x)
+    e1.record(cur)
+    e1.synchronize()
+    dev_ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count() - l0
+    clk = clocks.stop()
+    t = torch.tensor([dev_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item()) / steps
+    value = C5B_IMAGES / (ms / 1e3)
+    # per-kernel share (rank-local profile of one step)
+    H.prof_enable(True)
+    layer.forward(x)
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    H.prof_enable(False)
+    prof = H.prof_report()
+    mac, byts = c5b_work(p["n"], L)
+    mac_r, byts_r = mac * len(layer.rows) / C5B_M, byts  # this rank's share of the MACs
+    wide_peak = H.bench_int_peak(local, 1)
+    hbm_gbs, hbm_src = load_peaks()
+    kern = {k: {"ms_per_step": v["ms"], "launches_per_step": v["launches"]} for k, v in prof.items()}
+    dk = max(kern, key=lambda k: kern[k]["ms_per_step"])
+    kms = kern[dk]["ms_per_step"]
+    # 40-bit limb 0: 128-bit MACs cost ~4 IMAD.WIDE; limbs 1..7 one IMAD.WIDE each
+    imadw = mac_r * (4 + (L - 1)) / L
+    roof = {"bound": "int32", "kernel": dk, "achieved": imadw / (kms * 1e-3) / 1e12, "peak": wide_peak / 1e12,
+            "unit": "T IMAD.WIDE/s (limb-0 128-bit MAC = 4)", "frac": imadw / (kms * 1e-3) / wide_peak,
+            "peak_source": "measured register-only IMAD.WIDE probe (hg_bench_int_peak kind 1)",
+            "hbm_gbs_achieved": byts_r / (kms * 1e-3) / 1e9, "hbm_peak": hbm_gbs, "traffic": None,
+            "algorithmic_per_step": {"mac": mac_r, "hbm_bytes": byts_r}}
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import refbind as R
+            if R.available():
+                v, sample = c5b_reference_sample(os.cpu_count() or 1)
+                cpu = {"value": v, "unit": "images/s", "cores": os.cpu_count() or 1, "kind": "reference",
+                       "sample": sample}
+        except Exception as e:  # reported, not fatal
+            cpu = {"error": str(e)}
+    if rank == 0:
+        print(json.dumps({
+            "metric": C5B_METRIC, "value": value, "unit": "images/s", "n_gpus": ws, "steps": steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64 (RNS residues, 40/30-bit primes)",
+            "data": "synthetic (seeded uniform residues generated on device; W ~ N(0, 0.1^2) f32)",
+            "config": c5b_config(ws), "roofline": roof, "cpu_baseline": cpu,
+            "e2e": None, "e2e_note": "not measured for c5b (8.6 GB of host input per step; c2 carries the e2e line)",
+            "gpu_launches": launches, "clocks": clk, "kernels": kern,
+            "outputs": {"count": out.count, "level": out.level, "scale": out.scale}}))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def c5b_reference_run(args, ws, rank):
+    from oracle import refbind as R
+    if rank != 0:
+        return 0
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libhenet_ref.so not built"}))
+        return 0
+    cores = os.cpu_count() or 1
+    v, sample = c5b_reference_sample(cores)
+    print(json.dumps({
+        "metric": C5B_METRIC, "value": v, "unit": "images/s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": 1, "warmup": 0, "ms_per_step": C5B_IMAGES / v * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64 (RNS residues)",
+        "data": "synthetic (seeded uniform residues)", "config": c5b_config(1) | {"parallelism": f"{cores} host threads"},
+        "cpu_baseline": {"value": v, "unit": "images/s", "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+    return 0
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
+    if args.workload == "c5b":
+        return c5b_reference_run(args, ws, rank) if args.impl == "reference" else c5b_run(args, ws, rank, local)
     if args.impl == "reference":
         return reference_run(args, ws, rank)
     return b200_run(args, ws, rank, local)

@@ -122,9 +122,12 @@ int hg_tensor_download(const hg_tensor* t, uint64_t* words, void* stream);
 /* Same, in the device's compact u32 word order (no widening). */
 int hg_tensor_upload_u32(hg_tensor* t, const uint32_t* words, void* stream);
 int hg_tensor_download_u32(const hg_tensor* t, uint32_t* words, void* stream);
-/* Raw device pointer to the u32 residues (for zero-copy interop). */
+/* Raw device pointer to the residues (for zero-copy interop, e.g. NCCL): u32 words, or
+ * u64 words when the context has a prime >= 2^30 (hg_tensor_word_bytes says which);
+ * hg_tensor_words = count * polys * level * N residues in [elem][poly][limb][N] order. */
 void* hg_tensor_device_ptr(hg_tensor* t);
 uint64_t hg_tensor_words(const hg_tensor* t);
+uint32_t hg_tensor_word_bytes(const hg_tensor* t);
 
 /* ------------------------------------------------------------------ */
 /* Relinearization key, words in serialize_relin_key order             */

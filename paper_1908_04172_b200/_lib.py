@@ -75,6 +75,7 @@ PROTOTYPES = {
     "hg_tensor_download_u32": (C.c_int, [vp, vp, vp]),
     "hg_tensor_device_ptr": (vp, [vp]),
     "hg_tensor_words": (C.c_uint64, [vp]),
+    "hg_tensor_word_bytes": (C.c_uint32, [vp]),
     "hg_relin_key_upload": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(vp)]),
     "hg_relin_key_destroy": (None, [vp]),
     "hg_add_ct_ct": (C.c_int, [vp, vp, vp, vp, vp]),

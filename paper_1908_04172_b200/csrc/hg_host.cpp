@@ -1476,6 +1476,7 @@ int hg_tensor_download_u32(const hg_tensor* t, uint32_t* words, void* stream) {
 
 void* hg_tensor_device_ptr(hg_tensor* t) { return t ? t->b.data() : nullptr; }
 uint64_t hg_tensor_words(const hg_tensor* t) { return t ? t->b.words(t->ctx->n) : 0; }
+uint32_t hg_tensor_word_bytes(const hg_tensor* t) { return t ? (t->ctx->wide ? 8u : 4u) : 0u; }
 
 int hg_relin_key_upload(hg_ctx* ctx, const uint64_t* words, uint64_t n_words, hg_relin_key** out) {
   return guard([&] {

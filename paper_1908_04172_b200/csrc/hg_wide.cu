@@ -344,10 +344,14 @@ int launch_ntt_w(int logn, u64* data, u64 rows, u32 level, bool inverse, const B
     const size_t sm = sizeof(u64) * NttW<LN>::SMEM_WORDS;
     if (inverse) {
       set_smem_w(k_ntt_w<LN, true>, sm);
+      { ProfScope ps_("k_ntt_w", s);
       k_ntt_w<LN, true><<<rows, 1 << (LN - 5), sm, s>>>(data, level, B);
+      }
     } else {
       set_smem_w(k_ntt_w<LN, false>, sm);
+      { ProfScope ps_("k_ntt_w", s);
       k_ntt_w<LN, false><<<rows, 1 << (LN - 5), sm, s>>>(data, level, B);
+      }
     }
   });
   return 1;
@@ -358,7 +362,9 @@ int launch_rescale_w(int logn, const RescaleArgsW& a, const BasisW& B, cudaStrea
   HG_LOGN_SWITCH_W(logn, {
     const size_t sm = sizeof(u64) * NttW<LN>::SMEM_WORDS + sizeof(i32) * NttW<LN>::N;
     set_smem_w(k_rescale_w<LN>, sm);
+    { ProfScope ps_("k_rescale_w", s);
     k_rescale_w<LN><<<a.rows, 1 << (LN - 5), sm, s>>>(a, B);
+    }
   });
   return 1;
 }
@@ -369,7 +375,9 @@ int launch_mac_dense_w(const MacDenseArgsW& a, const BasisW& B, cudaStream_t s) 
   const u32 BM = kWTM * kWWarps;
   if (a.Mpad % BM != 0 || a.N % kWBN != 0) return -1;
   dim3 grid(a.N / kWBN, (a.M + BM - 1) / BM, a.polys * a.level);
+  { ProfScope ps_("k_mac_dense_w", s);
   k_mac_dense_w<<<grid, kWWarps * 32, 0, s>>>(a, B);
+  }
   return 1;
 }
 
@@ -377,36 +385,46 @@ int launch_mac_conv_w(const MacConvArgsW& a, const BasisW& B, cudaStream_t s) {
   if (a.C * a.win * a.win > static_cast<u32>(kWMaxTaps) || a.N % 256 != 0) return -1;
   const u32 nchunks = (a.F + kWFT - 1) / kWFT;
   dim3 grid(a.N / 256, a.OH * a.OW, a.polys * a.level * nchunks);
+  { ProfScope ps_("k_mac_conv_w", s);
   k_mac_conv_w<<<grid, 128, 0, s>>>(a, B);
+  }
   return 1;
 }
 
 int launch_elementwise_w(const EwArgsW& a, const BasisW& B, cudaStream_t s) {
   const u64 threads = a.count * a.polys_out * a.level * (a.N / 2);
   if (threads == 0) return 0;
+  { ProfScope ps_("k_ew_w", s);
   k_ew_w<<<(threads + 255) / 256, 256, 0, s>>>(a, B);
+  }
   return 1;
 }
 
 int launch_validate_w(const u64* w, u64 words, u32 level, u32 N, const BasisW& B, int* d_bad, cudaStream_t s) {
   if (words == 0) return 0;
+  { ProfScope ps_("k_validate_w", s);
   k_validate_w<<<(words + 255) / 256, 256, 0, s>>>(w, words, level, N, B, d_bad);
+  }
   return 1;
 }
 
 int launch_encode_scalars_w_f32(const float* vals, u64 count, u32 row_len, u32 row_stride, u64 limb_stride, u32 level,
                                 double scale, u64* out, const BasisW& B, cudaStream_t s) {
   if (count == 0) return 0;
+  { ProfScope ps_("k_encode_scalars_w", s);
   k_encode_scalars_w<float><<<(count + 127) / 128, 128, 0, s>>>(vals, count, row_len, row_stride, limb_stride, level,
                                                                 scale, out, B);
+  }
   return 1;
 }
 
 int launch_encode_scalars_w_f64(const double* vals, u64 count, u32 row_len, u32 row_stride, u64 limb_stride,
                                 u32 level, double scale, u64* out, const BasisW& B, cudaStream_t s) {
   if (count == 0) return 0;
+  { ProfScope ps_("k_encode_scalars_w", s);
   k_encode_scalars_w<double><<<(count + 127) / 128, 128, 0, s>>>(vals, count, row_len, row_stride, limb_stride, level,
                                                                  scale, out, B);
+  }
   return 1;
 }
 
@@ -433,7 +451,9 @@ int launch_mags_to_residues_w(const ulonglong2* mags, u64 count, u32 n, u32 leve
                               cudaStream_t s) {
   const u64 total = count * n;
   if (total == 0) return 0;
+  { ProfScope ps_("k_mags_to_residues_w", s);
   k_mags_to_residues_w<<<(total + 255) / 256, 256, 0, s>>>(mags, total, n, level, out, B);
+  }
   return 1;
 }
 

@@ -185,6 +185,31 @@ class CipherTensor:
     def device_ptr(self) -> int:
         return lib.hg_tensor_device_ptr(self._h)
 
+    @property
+    def word_bytes(self) -> int:
+        """4 (u32 residues) or 8 (u64, contexts with a prime >= 2^30)."""
+        return int(lib.hg_tensor_word_bytes(self._h))
+
+    def torch_view(self, device: Optional[int] = None):
+        """Zero-copy torch view (count, polys * level * N) of the device residues, int32 or
+        int64 by word size (bit patterns; residues are < 2^63).  The view keeps this tensor
+        alive.  Work queued on the context stream must be synchronised before the view is
+        used on another stream (CkksContext.synchronize())."""
+        import torch
+        cnt, polys, level, _, _ = self.info()
+        wb = self.word_bytes
+
+        class _Cai:
+            pass
+
+        cai = _Cai()
+        cai.owner = self
+        cai.__cuda_array_interface__ = {"shape": (cnt, polys * level * self.ctx.n),
+                                        "typestr": "<i8" if wb == 8 else "<i4",
+                                        "data": (int(self.device_ptr() or 0), False), "version": 3}
+        dev = torch.cuda.current_device() if device is None else device
+        return torch.as_tensor(cai, device=f"cuda:{dev}")
+
 
 class RelinKey:
     """RelinKey (henet/ckks.hpp:25-27) uploaded from serialize_relin_key word order."""

@@ -212,12 +212,16 @@ def random_ciphertexts(params: dict, count: int, seed: int, level: int = None) -
     return out
 
 
+def wide_dense_weights(seed: int = 5, k: int = 4096, m: int = 4096) -> np.ndarray:
+    """The c5b weight matrix, K x M row-major f32, W ~ N(0, 0.1^2)."""
+    return np.asarray(_gauss(np.random.default_rng(seed), (k, m), 0.1), dtype=np.float32).reshape(k, m)
+
+
 def wide_dense(seed: int = 5, k: int = 4096, m: int = 4096, batch: int = 8192) -> Workload:
     """Config 5b: wide dense layer k -> m on N=16384 batch-packed ciphertexts (40-bit limb 0),
     W ~ N(0, 0.1^2) (config 4/5 weight scale), one rescale per output (patched plan, as c1)."""
-    rng = np.random.default_rng(seed)
     blob = Blob()
-    blob.add("fc_w", [k, m], _gauss(rng, (k, m), 0.1))
+    blob.add("fc_w", [k, m], wide_dense_weights(seed, k, m))
     j = {
         "name": f"dense-{k}-{m}",
         "packing": "real",
