@@ -343,6 +343,50 @@ int ref_plan_json(void* c, const char* manifest, const uint8_t* blob, uint64_t b
   });
 }
 
+namespace {
+// ReLU6 for config 4: the reference graph has no ReLU6 op; its Relu nodes
+// run through a NonlinearityProvider.  With a clip bound set (ref_set_relu_clip), Relu
+// clamps each decrypted slot component to [0, hi] instead of [0, inf); everything else
+// (decode, encode at (L, default scale), per-group seeds) follows
+// NonlinearityEngine::apply (henet/graph.hpp:707-741).  MaxPool is unchanged.
+double g_relu_clip_hi = 0.0;  // 0: plain ReLU
+
+std::vector<Ciphertext> clip_apply(const std::shared_ptr<const CkksContext>& sctx, const SecretKey& sk, u64 seed,
+                                   NonlinKind kind, u32 window, u32 layer_seq, const std::vector<Ciphertext>& cts) {
+  if (kind != NonlinKind::Relu || g_relu_clip_hi <= 0.0)
+    return NonlinearityEngine(sctx, sk, seed).apply(kind, window, layer_seq, cts);
+  require(window == 1, "ReLU is element-wise");
+  const CkksContext& ctx = *sctx;
+  const double hi = g_relu_clip_hi;
+  auto clamp = [hi](double v) { return v < 0.0 ? 0.0 : (v > hi ? hi : v); };
+  std::vector<Ciphertext> out(cts.size());
+  for (std::size_t g = 0; g < cts.size(); ++g) {
+    auto slots = decode_slots(ctx, decrypt(ctx, cts[g], sk));
+    for (auto& z : slots) z = {clamp(z.real()), clamp(z.imag())};
+    auto pt = encode_vector(ctx, slots, ctx.chain_length(), ctx.params().default_scale);
+    out[g] = encrypt(ctx, pt, sk, derive_seed(derive_seed(seed, layer_seq), g), cts[g].packing);
+  }
+  return out;
+}
+
+class ClipProvider : public NonlinearityProvider {
+ public:
+  ClipProvider(std::shared_ptr<const CkksContext> ctx, SecretKey sk, u64 seed)
+      : ctx_(std::move(ctx)), sk_(std::move(sk)), seed_(seed) {}
+  std::vector<Ciphertext> apply(NonlinKind kind, u32 window, u32 layer_seq,
+                                const std::vector<Ciphertext>& cts) override {
+    return clip_apply(ctx_, sk_, seed_, kind, window, layer_seq, cts);
+  }
+
+ private:
+  std::shared_ptr<const CkksContext> ctx_;
+  SecretKey sk_;
+  u64 seed_;
+};
+}  // namespace
+
+void ref_set_relu_clip(double hi) { g_relu_clip_hi = hi; }
+
 int ref_execute(void* c, void* k, const char* manifest, const uint8_t* blob, uint64_t blob_len, int mode, int patch,
                 const uint64_t* in_words, uint64_t in_count, double in_scale, unsigned threads, uint64_t refresh_seed,
                 uint64_t* out_words, uint64_t out_capacity_words, uint64_t* out_count, uint32_t* out_level,
@@ -362,9 +406,9 @@ int ref_execute(void* c, void* k, const char* manifest, const uint8_t* blob, uin
     ExecutionConfig cfg;
     cfg.threads = threads ? threads : std::thread::hardware_concurrency();
     if (keys && keys->kp.relin) cfg.relin = &*keys->kp.relin;
-    std::unique_ptr<LocalProvider> prov;
+    std::unique_ptr<ClipProvider> prov;
     if (keys) {
-      prov = std::make_unique<LocalProvider>(NonlinearityEngine(sctx, keys->kp.secret, refresh_seed));
+      prov = std::make_unique<ClipProvider>(sctx, keys->kp.secret, refresh_seed);
       cfg.provider = prov.get();
     }
     ExecutionStats st;
@@ -384,7 +428,8 @@ int ref_execute(void* c, void* k, const char* manifest, const uint8_t* blob, uin
 }
 
 // NonlinearityEngine::apply for the GPU path's provider callback in tests:
-// decrypt -> relu/maxpool -> re-encrypt at the top level, seeded like the reference.
+// decrypt -> relu (or ReLU6 when a clip bound is set)/maxpool -> re-encrypt at the top
+// level, seeded like the reference.
 int ref_nonlin_apply(void* c, void* k, int kind, uint32_t window, uint32_t layer_seq, uint64_t refresh_seed,
                      const uint64_t* words, uint64_t count, uint32_t level, double scale, int packing,
                      uint64_t* out_words) {
@@ -392,9 +437,9 @@ int ref_nonlin_apply(void* c, void* k, int kind, uint32_t window, uint32_t layer
     auto sctx = static_cast<RefCtx*>(c)->ctx;
     auto& ctx = *sctx;
     auto* keys = static_cast<RefKeys*>(k);
-    NonlinearityEngine eng(sctx, keys->kp.secret, refresh_seed);
     auto cts = cts_from(ctx, words, count, 2, level, scale, packing);
-    auto out = eng.apply(kind == 1 ? NonlinKind::Relu : NonlinKind::MaxPool, window, layer_seq, cts);
+    auto out = clip_apply(sctx, keys->kp.secret, refresh_seed, kind == 1 ? NonlinKind::Relu : NonlinKind::MaxPool,
+                          window, layer_seq, cts);
     cts_to(out, out_words);
   });
 }

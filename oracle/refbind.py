@@ -61,6 +61,7 @@ _PROTOS = {
     "ref_execute": (C.c_int, [vp, vp, C.c_char_p, vp, C.c_uint64, C.c_int, C.c_int, vp, C.c_uint64, C.c_double,
                               C.c_uint, C.c_uint64, vp, C.c_uint64, u64p, C.POINTER(C.c_uint32),
                               C.POINTER(C.c_double), C.POINTER(C.c_double), u64p, u64p]),
+    "ref_set_relu_clip": (None, [C.c_double]),
     "ref_nonlin_apply": (C.c_int, [vp, vp, C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, vp, C.c_uint64, C.c_uint32,
                                    C.c_double, C.c_int, vp]),
 }
@@ -253,6 +254,12 @@ class RefContext:
         _chk(lib().ref_nonlin_apply(self._h, keys._h, kind, window, layer_seq, refresh_seed, _p(w), count, level,
                                     scale, packing, _p(out)))
         return out
+
+
+def set_relu_clip(hi: float) -> None:
+    """Relu nodes clamp to [0, hi] in the reference-side providers (config 4's ReLU6,
+    SURVEY H8); 0 restores plain ReLU."""
+    lib().ref_set_relu_clip(float(hi))
 
 
 class RefKeys:

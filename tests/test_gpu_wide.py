@@ -103,6 +103,35 @@ def test_conv_c4_shape_small_bit_exact(env):
     assert np.array_equal(out.to_words(), want)
 
 
+def test_c4_block_relu6_provider_bit_exact(env):
+    """Full c4 block on a 4x4 tile of real encryptions of N(0,1) activations: 1x1 expand,
+    ReLU6, 3x3 depthwise (pad 1), ReLU6, 1x1 project.  ReLU6 is client-aided: the Relu nodes
+    go through the provider, here the reference's refresh with a [0, 6] clamp,
+    called from the GPU executor's callback exactly as the reference executor calls it."""
+    ctx, ref, p, keys = env["ctx"], env["ref"], env["p"], env["keys"]
+    wl = W.mobilenet_block(hw=4, cin=4, expand=6, cout=3)
+    acts = np.random.default_rng(12).normal(0, 1, (ctx.slot_count(), wl.input_count))
+    words, sc = ref.encrypt_tensor(keys, acts, 13)
+    R.set_relu_clip(6.0)
+    try:
+        want, want_sc, st = ref.execute(keys, wl.manifest, wl.blob, words, sc, refresh_seed=77)
+        model = H.PlainModel.load(wl.manifest, wl.blob)
+        plan = H.RescalePlan.plan(ctx, model)
+        assert plan.planned_rescale_ops == st["rescale_ops"]
+
+        def provider(kind, window, layer_seq, req):
+            return ref.nonlin_apply(keys, kind, window, layer_seq, 77, req.to_words(), req.scale, req.packing)
+
+        stats = H.ExecutionStats()
+        out = H.execute(ctx, model, plan, H.CipherTensor.from_words(ctx, words, sc, shape=wl.input_shape), None,
+                        provider, stats)
+    finally:
+        R.set_relu_clip(0.0)
+    assert out.scale == want_sc
+    assert np.array_equal(out.to_words(), want)
+    assert stats.nonlin_elements == 2 * 6 * 4 * 4  # two ReLU6 layers over (6, 4, 4)
+
+
 def test_wide_relin_is_refused_not_wrong(env):
     ctx, p = env["ctx"], env["p"]
     t = H.CipherTensor.from_words(ctx, W.random_ciphertexts(p, 1, seed=11), 1.0)
