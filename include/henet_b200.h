@@ -98,7 +98,8 @@ int hg_ctx_ntt_root(const hg_ctx* ctx, uint32_t basis_index, uint64_t* root);
 /* cudaStream_t the context enqueues on when a call passes stream == NULL. */
 void* hg_ctx_stream(hg_ctx* ctx);
 int hg_ctx_synchronize(hg_ctx* ctx);
-/* Kernel launches issued through this context since creation (all ops). */
+/* Kernel launches issued by this library in this process (all contexts; differences
+ * around a region count the region's launches). */
 uint64_t hg_ctx_launch_count(const hg_ctx* ctx);
 
 /* ------------------------------------------------------------------ */

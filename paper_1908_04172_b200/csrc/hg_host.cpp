@@ -362,7 +362,6 @@ static void run_ew(const Context& ctx, EwArgs a, cudaStream_t s) {
     r = launch_elementwise(a, ctx.basis, s);
   }
   check_launch(r, "elementwise");
-  ctx.count(r);
 }
 
 // Encoded-residue buffers hold u32 or u64 words depending on the context mode.
@@ -415,7 +414,6 @@ static CtBatch do_rescale(const Context& ctx, const CtBatch& in, u32 target, cud
       r = launch_rescale(static_cast<int>(ctx.logn), a, ctx.basis, s);
     }
     check_launch(r, "rescale");
-    ctx.count(r);
     out.scale = cur.scale / static_cast<double>(p);
     cur = std::move(out);
   }
@@ -463,7 +461,6 @@ static CtBatch do_relin(const Context& ctx, const RelinKeyDev& rk, const CtBatch
   }
   const int lr = launch_relin(static_cast<int>(ctx.logn), r, ctx.basis, s);
   check_launch(lr, "relinearize");
-  ctx.count(lr);
   // scale: square/mul_ct_ct multiply the scales; relinearize keeps it; rescale divides.
   double sc = a->scale;
   if (mode == 1) sc = a->scale * (b ? b->scale : a->scale);
@@ -510,22 +507,18 @@ static BufPtr encode_vectors_dev(const Context& ctx, const double* d_slots, u32 
   int r = launch_fft_encode(d_slots, n_slots, count, n, level, scale, roots, twist, static_cast<double2*>(scratch->ptr),
                             static_cast<ulonglong2*>(mags->ptr), d_mant, d_exp, s);
   check_launch(r, "fft encode");
-  ctx.count(r);
   if (ctx.wide) {
     r = launch_mags_to_residues_w(static_cast<const ulonglong2*>(mags->ptr), count, n, level,
                                   static_cast<u64*>(out->ptr), ctx.basisw, s);
     check_launch(r, "residues");
-    ctx.count(r);
     r = launch_ntt_w(static_cast<int>(ctx.logn), static_cast<u64*>(out->ptr), count * level, level, false, ctx.basisw, s);
   } else {
     r = launch_mags_to_residues(static_cast<const ulonglong2*>(mags->ptr), count, n, level,
                                 static_cast<u32*>(out->ptr), ctx.basis, s);
     check_launch(r, "residues");
-    ctx.count(r);
     r = launch_ntt(static_cast<int>(ctx.logn), static_cast<u32*>(out->ptr), count * level, level, false, ctx.basis, s);
   }
   check_launch(r, "ntt");
-  ctx.count(r);
   mant.resize(count);
   ex.resize(count);
   cuda_check(cudaMemcpyAsync(mant.data(), d_mant, count * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s), "d2h");
@@ -900,16 +893,12 @@ class Executor {
       stats->relin_ops = relins_;
       stats->nonlin_elements += 0;
       stats->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-      stats->kernel_launches = launches_;
+      stats->kernel_launches = launches_total() - launches0_;
     }
     return out;
   }
 
  private:
-  void count(int r) {
-    if (r > 0) launches_ += static_cast<u64>(r);
-  }
-
   // Dot / Convolution: mac_output over every output (henet/graph.hpp:905-993).
   Value eval_linear(const Node& n, std::map<std::string, Value>& values) {
     const Context& ctx = *ctx_;
@@ -950,14 +939,12 @@ class Executor {
       cuda_check(cudaMemsetAsync(wres->ptr, 0, static_cast<u64>(L) * K * Mpad * wb, s_), "memset");
       int r = encode_f32(ctx, wd, w.data.size(), Mo, Mpad, static_cast<u64>(K) * Mpad, L, s, wres->ptr, s_);
       check_launch(r, "encode weights");
-      count(r);
       if (b && x.packing == HG_PACKING_REAL) {
         check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
         const float* bd = weight_dev(ctx, *b, s_);
         bias_res = ctx.alloc(static_cast<u64>(L) * Mpad * wb, s_);
         r = encode_f32(ctx, bd, Mo, Mo, Mpad, Mpad, L, acc_scale, bias_res->ptr, s_);
         check_launch(r, "encode bias");
-        count(r);
       }
       if (ctx.wide) {
         MacDenseArgsW a{};
@@ -978,7 +965,6 @@ class Executor {
         BufPtr wp = ctx.alloc(tc_packed_weight_bytes(K, Mo, L), s_);
         r = launch_pack_weights_tc(static_cast<const u32*>(wres->ptr), static_cast<uint8_t*>(wp->ptr), K, Mo, Mpad, L, s_);
         check_launch(r, "pack weights");
-        count(r);
         MacDenseTcArgs a{};
         a.X = x.data();
         a.Y = v.cipher.data();
@@ -1013,7 +999,6 @@ class Executor {
         r = launch_mac_dense(a, ctx.basis, s_);
       }
       check_launch(r, "mac_dense");
-      count(r);
     } else {
       const auto& in_shape = x.shape;
       require(in_shape.size() == 3, "Convolution expects a (C,H,W) input");
@@ -1022,14 +1007,12 @@ class Executor {
       int r = encode_f32(ctx, wd, w.data.size(), static_cast<u32>(w.data.size()), static_cast<u32>(w.data.size()),
                          w.data.size(), L, s, wres->ptr, s_);
       check_launch(r, "encode weights");
-      count(r);
       if (b && x.packing == HG_PACKING_REAL) {
         check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
         const float* bd = weight_dev(ctx, *b, s_);
         bias_res = ctx.alloc(static_cast<u64>(L) * F * wb, s_);
         r = encode_f32(ctx, bd, F, F, F, F, L, acc_scale, bias_res->ptr, s_);
         check_launch(r, "encode bias");
-        count(r);
       }
       if (ctx.wide) {
         MacConvArgsW a{};
@@ -1079,7 +1062,6 @@ class Executor {
         r = launch_mac_conv(a, ctx.basis, s_);
       }
       check_launch(r, "mac_conv");
-      count(r);
     }
     if (b && x.packing == HG_PACKING_COMPLEX) {
       // encode_broadcast under complex packing: encode_vector of (b + b i) in every slot
@@ -1096,9 +1078,7 @@ class Executor {
                  "h2d");
       std::vector<unsigned long long> mant;
       std::vector<int> ex;
-      const u64 before = ctx.core->launches.load();
       bias_pt = encode_vectors_dev(ctx, static_cast<const double*>(ds->ptr), ctx.n / 2, nb, L, acc_scale, s_, mant, ex);
-      count(static_cast<int>(ctx.core->launches.load() - before));
       EwArgs e{};
       e.op = EwOp::AddVector;
       e.a = v.cipher.data();
@@ -1111,12 +1091,9 @@ class Executor {
       e.polys_out = 2;
       e.level = L;
       run_ew(ctx, e, s_);
-      count(1);
     }
     if (layer_rescale) {
-      const u64 before = ctx.core->launches.load();
       v.cipher = do_rescale(ctx, v.cipher, L - 1, s_);
-      count(static_cast<int>(ctx.core->launches.load() - before));
       rescales_ += M;
     }
     return v;
@@ -1130,9 +1107,7 @@ class Executor {
     Value v;
     v.is_cipher = true;
     const bool rs = np.decision == HG_RESCALE_AFTER;
-    const u64 before = ctx_->core->launches.load();
     v.cipher = do_relin(*ctx_, *rk_, &x, &x, 1, rs, s_);
-    count(static_cast<int>(ctx_->core->launches.load() - before));
     v.cipher.shape = x.shape;
     relins_ += x.count;
     if (rs) rescales_ += x.count;
@@ -1150,7 +1125,6 @@ class Executor {
     const double s = ctx.default_scale;
     Value v;
     v.is_cipher = true;
-    const u64 before = ctx.core->launches.load();
     if (a.is_cipher && b.is_cipher) {
       const CtBatch& ca = a.cipher;
       const CtBatch& cb = b.cipher;
@@ -1193,7 +1167,6 @@ class Executor {
         // residues laid out [value][limb]
         int r = encode_f32(ctx, cd, c.data.size(), 1, L, 1, L, s, res->ptr, s_);
         check_launch(r, "encode");
-        ctx.count(r);
         v.cipher.scale = x.scale * s;
         ensure(ctx, v.cipher, x.count, 2, L, s_);
         EwArgs e{};
@@ -1228,7 +1201,6 @@ class Executor {
           res = ctx.alloc(static_cast<u64>(c.data.size()) * L * ctx.word_bytes(), s_);
           int r = encode_f32(ctx, cd, c.data.size(), 1, L, 1, L, x.scale, res->ptr, s_);
           check_launch(r, "encode");
-          ctx.count(r);
           e.op = EwOp::AddScalar;
           e.res = static_cast<const u32*>(res->ptr);
         } else {
@@ -1251,7 +1223,6 @@ class Executor {
         run_ew(ctx, e, s_);
       }
     }
-    count(static_cast<int>(ctx.core->launches.load() - before));
     v.cipher.shape = model_.shapes.at(n.id);
     return v;
   }
@@ -1319,7 +1290,8 @@ class Executor {
   void* user_;
   cudaStream_t s_;
   bool timing_;
-  u64 rescales_ = 0, relins_ = 0, launches_ = 0;
+  u64 rescales_ = 0, relins_ = 0;
+  u64 launches0_ = launches_total();  // kernel launches are counted process-wide
 };
 
 }  // namespace hg
@@ -1359,7 +1331,7 @@ int hg_ctx_synchronize(hg_ctx* ctx) {
   return guard([&] { cuda_check(cudaStreamSynchronize(ctx->c->core->stream), "synchronize"); });
 }
 
-uint64_t hg_ctx_launch_count(const hg_ctx* ctx) { return ctx ? ctx->c->core->launches.load() : 0; }
+uint64_t hg_ctx_launch_count(const hg_ctx* ctx) { return ctx ? hg::launches_total() : 0; }
 
 int hg_tensor_create(hg_ctx* ctx, uint64_t count, uint32_t polys, uint32_t level, double scale, int packing,
                      hg_tensor** out) {
@@ -1429,7 +1401,6 @@ int hg_tensor_upload(hg_tensor* t, const uint64_t* words, void* stream) {
       r = launch_narrow(static_cast<const u64*>(stage->ptr), t->b.data(), n, t->b.level, ctx.n, ctx.basis, bad, s);
     }
     check_launch(r, "narrow");
-    ctx.count(r);
     int hbad = 0;
     cuda_check(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
     cuda_check(cudaStreamSynchronize(s), "upload");
@@ -1448,7 +1419,6 @@ int hg_tensor_download(const hg_tensor* t, uint64_t* words, void* stream) {
       BufPtr stage = ctx.alloc(n * 8, s);
       const int r = launch_widen(t->b.data(), static_cast<u64*>(stage->ptr), n, s);
       check_launch(r, "widen");
-      ctx.count(r);
       cuda_check(cudaMemcpyAsync(words, stage->ptr, n * 8, cudaMemcpyDeviceToHost, s), "d2h");
     }
     cuda_check(cudaStreamSynchronize(s), "download");
@@ -1708,7 +1678,6 @@ int hg_ntt_forward(hg_ctx* ctx, hg_tensor* t, void* stream) {
                          : launch_ntt(static_cast<int>(c.logn), t->b.data(), rows, t->b.level, false, c.basis,
                                       c.pick(stream));
     check_launch(r, "ntt");
-    c.count(r);
   });
 }
 
@@ -1721,7 +1690,6 @@ int hg_ntt_inverse(hg_ctx* ctx, hg_tensor* t, void* stream) {
                          : launch_ntt(static_cast<int>(c.logn), t->b.data(), rows, t->b.level, true, c.basis,
                                       c.pick(stream));
     check_launch(r, "intt");
-    c.count(r);
   });
 }
 
@@ -1741,7 +1709,6 @@ int hg_encode_scalars(hg_ctx* ctx, const double* values, uint64_t count, uint32_
                          : launch_encode_scalars_f64(static_cast<const double*>(dv->ptr), count, 1, level, 1, level,
                                                      scale, static_cast<u32*>(dr->ptr), c.basis, s);
     check_launch(r, "encode_scalars");
-    c.count(r);
     if (c.wide) {
       cuda_check(cudaMemcpyAsync(out_residues, dr->ptr, count * level * 8, cudaMemcpyDeviceToHost, s), "d2h");
       cuda_check(cudaStreamSynchronize(s), "encode_scalars");

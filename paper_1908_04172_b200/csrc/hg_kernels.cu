@@ -889,6 +889,7 @@ __global__ void k_imad_probe(u64* sink, u32 iters, u32 seed) {
 // roofline pass).  Events are recorded on the launch stream around each kernel.
 // ===========================================================================
 }  // namespace hg
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <string>
@@ -904,7 +905,11 @@ bool g_prof_on = false;
 std::vector<ProfRec> g_prof;
 }  // namespace
 
+static std::atomic<u64> g_launches{0};
+u64 launches_total() { return g_launches.load(std::memory_order_relaxed); }
+
 ProfScope::ProfScope(const char* n, cudaStream_t st) : name(n), s(st) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   if (!g_prof_on) return;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -1011,12 +1016,12 @@ template <int FT>
 static void conv_launch(const MacConvArgs& a, const Basis& B, cudaStream_t s) {
   const u32 nchunks = (a.F + FT - 1) / FT;
   dim3 grid(a.N / (4 * kConvThreads), a.OH * a.OW, a.polys * a.level * nchunks);
+  ProfScope ps("k_mac_conv", s);
   k_mac_conv<FT><<<grid, kConvThreads, 0, s>>>(a, B);
 }
 
 int launch_mac_conv(const MacConvArgs& a, const Basis& B, cudaStream_t s) {
   if (a.C * a.win * a.win > static_cast<u32>(kMaxTaps) || a.N % (4 * kConvThreads) != 0) return -1;
-  ProfScope ps("k_mac_conv", s);
   switch (a.F) {
     case 1: conv_launch<1>(a, B, s); break;
     case 2: conv_launch<2>(a, B, s); break;
@@ -1047,6 +1052,8 @@ int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s) {
     }
     { ProfScope ps("k_relin_keysw", s);
     ks<<<a.count, T, sm3, s>>>(a, B);
+    }
+    { ProfScope ps("k_relin_keysw", s);
     kn<<<a.count * a.level, T, sm3, s>>>(a, B);
     }
     { ProfScope ps("k_relin_moddown", s);
@@ -1118,6 +1125,7 @@ int launch_mags_to_residues(const ulonglong2* mags, u64 count, u32 n, u32 level,
                             cudaStream_t s) {
   const u64 total = count * n;
   if (total == 0) return 0;
+  ProfScope ps("k_mags_to_residues", s);
   k_mags_to_residues<<<(total + 255) / 256, 256, 0, s>>>(mags, total, n, level, out, B);
   return 1;
 }

@@ -113,6 +113,9 @@ int launch_mags_to_residues(const ulonglong2* mags, u64 count, u32 n, u32 level,
 double bench_int_peak(int device, int kind);
 
 // Brackets one kernel launch with CUDA events on its stream when profiling is on.
+// Wraps exactly one kernel launch: counts it (launches_total) and, while the profiler is
+// on, brackets it with CUDA events on its stream.
+u64 launches_total();
 struct ProfScope {
   const char* name;
   cudaStream_t s;

@@ -36,7 +36,6 @@ void cuda_check(cudaError_t e, const char* what);
 struct DeviceCore {
   int device = 0;
   cudaStream_t stream = nullptr;
-  std::atomic<uint64_t> launches{0};
   ~DeviceCore();
 };
 
@@ -74,7 +73,6 @@ struct Context {
   size_t word_bytes() const { return wide ? 8 : 4; }
   u64 basis_mod(size_t i) const { return i < chain.size() ? chain[i] : special; }
   cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : core->stream; }
-  void count(int launches) const { core->launches += static_cast<uint64_t>(launches > 0 ? launches : 0); }
   BufPtr alloc(size_t bytes, cudaStream_t s) const { return std::make_shared<DeviceBuffer>(core, bytes, s); }
 };
 

@@ -265,6 +265,7 @@ u64 tc_packed_weight_bytes(u32 K, u32 M, u32 level) {
 int launch_pack_weights_tc(const u32* W, uint8_t* Wp, u32 K, u32 M, u32 Mpad, u32 level, cudaStream_t s) {
   const u32 Mtiles = (M + kTcM - 1) / kTcM, Ksteps = (K + kTcK - 1) / kTcK;
   const u64 total = static_cast<u64>(level) * Mtiles * Ksteps * kTcM * kTcK;
+  ProfScope ps("k_pack_weights_tc", s);
   k_pack_weights_tc<<<(total + 255) / 256, 256, 0, s>>>(W, Wp, K, Mpad, Mtiles, Ksteps, level);
   return 1;
 }
