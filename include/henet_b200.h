@@ -261,7 +261,8 @@ int hg_execute(hg_ctx* ctx, const hg_model* m, const hg_plan* plan, const hg_ten
 /* Measurement helpers (not part of the reference surface)             */
 /* ------------------------------------------------------------------ */
 /* Register-only integer-pipe microbenchmark (the INT32 roofline denominator):
- * kind 0 = IMAD (mad.lo.u32), 1 = IMAD.WIDE (mad.wide.u32), 2 = IMAD.HI, 3 = Shoup lazy
+ * kind 0 = IMAD (mad.lo.u32), 1 = IMAD.WIDE (mul.wide.u32, high word consumed: the cost of
+ * one 32x32->64 MAC), 2 = IMAD.HI, 3 = Shoup lazy
  * modular product (IMAD.HI + 2 IMAD, the NTT butterfly's multiply); lane-ops/s. */
 int hg_bench_int_peak(int device, int kind, double* ops_per_s);
 /* Per-kernel CUDA-event profiler: when enabled, every kernel launch is bracketed by

@@ -42,6 +42,8 @@ struct DevPrime {
   u32 ninv_sh;   // floor(ninv * 2^32 / q)
   u32 w1n;       // inv_root_powers[1] * N^-1 mod q (last inverse stage)
   u32 w1n_sh;
+  u32 bsh;       // k - 1, k = bit length of q       -> product Barrett (mulmod)
+  u32 bmu;       // floor(2^(k+31) / q) (< 2^32)
   u32 pad_;
   // Twiddles staged per NTT pass (see Ntt below): pass A (uniform over the CTA)
   // from the kernel parameter block, passes B / C from per-thread rows of 32
@@ -95,8 +97,17 @@ __device__ __forceinline__ u32 reduce64(u64 x, const DevPrime& P) {
   return csub(r, P.q);
 }
 
+// a * b mod q for a, b < 2^k (k = bit length of q, so any canonical residues): Barrett on
+// the top k+1 bits of the product, x' = floor(ab / 2^(k-1)) < 2^(k+1),
+// qhat = floor(x' * floor(2^(k+31)/q) / 2^32) in [floor(ab/q) - 2, floor(ab/q)], so the low
+// word of ab - qhat*q is the remainder plus at most 2q (< 2^32 for q < 2^30).  One IMAD.HI
+// instead of the 64x64 high product of reduce64.
 __device__ __forceinline__ u32 mulmod(u32 a, u32 b, const DevPrime& P) {
-  return reduce64(static_cast<u64>(a) * b, P);
+  const u64 x = static_cast<u64>(a) * b;
+  const u32 xs = static_cast<u32>(x >> P.bsh);
+  u32 r = static_cast<u32>(x) - __umulhi(xs, P.bmu) * P.q;
+  r = min(r, r - P.two_q);  // [0, 3q) -> [0, 2q)
+  return csub(r, P.q);
 }
 
 __device__ __forceinline__ u32 addmod(u32 a, u32 b, u32 q) { return csub(a + b, q); }
@@ -124,6 +135,10 @@ __device__ __forceinline__ i32 centered_round_rem(u32 x, const DevPrime& P) {
 // Forward:  A --(stages LOGN-1..LOGT)--> smem --> B --(LOGT-1..CB)--> smem --> C --(CB-1..0)
 // Inverse runs the same passes backwards: C -> B -> A.
 // ---------------------------------------------------------------------------
+#ifndef HG_NTT_SPLIT
+#define HG_NTT_SPLIT 1
+#endif
+
 template <int LOGN_>
 struct Ntt {
   static constexpr int LOGN = LOGN_;
@@ -226,6 +241,45 @@ struct Ntt {
     for (int s = 0; s < NB; ++s) {
       const int rb = NB - 1 - s;  // register bit of this stage
       const int b = BLO + rb;     // j bit of this stage (t = 2^b)
+#if HG_NTT_SPLIT
+      // all 16 products of the stage first (independent IMAD.HI chains), then the adds
+      u32 Tm[16];
+      int m = 0;
+#pragma unroll
+      for (int g = 0; g < (1 << (5 - NB)); ++g) {
+#pragma unroll
+        for (int hi = 0; hi < (1 << (NB - 1 - rb)); ++hi) {
+          const u32 kh = (static_cast<u32>(g) << NB) | (static_cast<u32>(hi) << (rb + 1));
+          const uint2 w = (L == 0) ? P.twA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))]
+                                   : (L == 1 ? slot(twB, n) : P.tvC[n]);
+          ++n;
+#pragma unroll
+          for (int lo = 0; lo < (1 << rb); ++lo) {
+            u32 Y = x[(kh | lo) | (1 << rb)];
+            if (L == 2) Y = mul_shoup_lazy(Y, tb[b].x, tb[b].y, q);
+            Tm[m++] = mul_shoup_lazy(Y, w.x, w.y, q);
+          }
+        }
+      }
+      m = 0;
+#pragma unroll
+      for (int g = 0; g < (1 << (5 - NB)); ++g) {
+#pragma unroll
+        for (int hi = 0; hi < (1 << (NB - 1 - rb)); ++hi) {
+          const u32 kh = (static_cast<u32>(g) << NB) | (static_cast<u32>(hi) << (rb + 1));
+#pragma unroll
+          for (int lo = 0; lo < (1 << rb); ++lo) {
+            const int k0 = kh | lo;
+            const int k1 = k0 | (1 << rb);
+            u32 X = x[k0];
+            X = min(X, X - q2);
+            x[k0] = X + Tm[m];
+            x[k1] = X - Tm[m] + q2;
+            ++m;
+          }
+        }
+      }
+#else
 #pragma unroll
       for (int g = 0; g < (1 << (5 - NB)); ++g) {
 #pragma unroll
@@ -248,6 +302,7 @@ struct Ntt {
           }
         }
       }
+#endif
     }
   }
 

@@ -208,6 +208,12 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
     P.mu32 = static_cast<u32>((1ull << 32) / q);
     P.mu64 = static_cast<u64>((static_cast<nt::u128>(1) << 64) / q);
     P.r32 = static_cast<u32>((1ull << 32) % q);
+    {
+      u32 k = 0;
+      while ((1ull << k) <= q) ++k;  // bit length
+      P.bsh = k - 1;
+      P.bmu = static_cast<u32>((static_cast<nt::u128>(1) << (k + 31)) / q);
+    }
     const u64 ninv = nt::inv(n % q, q);
     P.ninv = static_cast<u32>(ninv);
     P.ninv_sh = nt::shoup(ninv, q);
@@ -430,6 +436,16 @@ static CtBatch do_relin(const Context& ctx, const RelinKeyDev& rk, const CtBatch
   const u32 L = a->level;
   const u32 n = ctx.n;
   if (rescale) require(L >= 2, "cannot rescale below level 1");
+  // The merged mod-down + rescale feeds the rescale correction (|c| <= q_{L-1}/2) into the
+  // lazy transform as c + q_i, which needs q_{L-1}/2 <= q_i for every kept limb; otherwise
+  // (never for the BASELINE chains) relinearise, then rescale separately.
+  bool fuse_rescale = rescale;
+  for (u32 i = 0; rescale && i + 1 < L; ++i)
+    if (ctx.chain[L - 1] / 2 > ctx.chain[i]) fuse_rescale = false;
+  if (rescale && !fuse_rescale) {
+    CtBatch r = do_relin(ctx, rk, a, b, mode, false, s);
+    return do_rescale(ctx, r, L - 1, s);
+  }
   CtBatch out;
   out.packing = a->packing;
   out.shape = a->shape;
@@ -454,6 +470,7 @@ static CtBatch do_relin(const Context& ctx, const RelinKeyDev& rk, const CtBatch
     const u64 q = ctx.chain[i];
     r.pinvP[i] = inv_mod_u32(ctx.special, q);
     r.pinvP_sh[i] = nt::shoup(r.pinvP[i], q);
+    r.pmP[i] = static_cast<u32>((ctx.special / 2 + q - 1) / q * q);
     if (rescale && i + 1 < L) {
       r.pinvL[i] = inv_mod_u32(ctx.chain[L - 1], q);
       r.pinvL_sh[i] = nt::shoup(r.pinvL[i], q);

@@ -471,9 +471,18 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
 #pragma unroll 1
   for (u32 r = 0; r < R; ++r) {
     const u32 j = r + (r >= skip ? 1 : 0);
+    // digit mod q_t (henet/ckks.hpp:463): the lazy forward transform accepts inputs < 4 q_t
+    // and returns canonical values, so only a digit of a prime >= 4 q_t needs reducing
+    // (the 30-bit limb 0 under a 24-bit target).
     u32 y[32];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) y[k] = reduce32(nx[k], P);  // digit mod q_t, henet/ckks.hpp:463
+    for (int k = 0; k < 32; ++k) y[k] = nx[k];
+    // (always reduced in the special-prime kernel: a branch there makes ptxas duplicate the
+    // transform, and that kernel runs 1/(l+1) of the transforms)
+    if (special || (B.p[j].q >> 2) >= q) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) y[k] = reduce32(y[k], P);
+    }
     NT::forward(y, sm, tid, P);
     const u32 jn = min(r + 1 + (r + 1 >= skip ? 1 : 0), L - 1);
     NT::gload_P(nx, a.D + (ct * L + jn) * N, tid);
@@ -588,24 +597,29 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
     const u32 i = top ? L - 1 : it - 1;
     const DevPrime& Pi = B.p[i];
     const u32 q = Pi.q, pv = a.pinvP[i], ps = a.pinvP_sh[i];
+    // Transform inputs, lazily reduced (the forward transform takes values < 4q):
+    //   rescale limbs: cps * P^-1 + crs = Shoup(cps + pm, P^-1) in [0, 2q) + (crs + q) in
+    //   [0, 2q) (|crs| <= q_{L-1}/2 <= q, checked by the host);
+    //   otherwise:     cps + pm reduced once (|cps| <= P/2 may exceed q).
+    const u32 pm = a.pmP[i];
     u32 z[32];
     if (RS && !top) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int4 u = cps[c ^ sw], v = crs[c ^ sw];
-        z[4 * c] = addmod(mul_shoup(signed_residue(u.x, Pi), pv, ps, q), signed_residue(v.x, Pi), q);
-        z[4 * c + 1] = addmod(mul_shoup(signed_residue(u.y, Pi), pv, ps, q), signed_residue(v.y, Pi), q);
-        z[4 * c + 2] = addmod(mul_shoup(signed_residue(u.z, Pi), pv, ps, q), signed_residue(v.z, Pi), q);
-        z[4 * c + 3] = addmod(mul_shoup(signed_residue(u.w, Pi), pv, ps, q), signed_residue(v.w, Pi), q);
+        z[4 * c] = mul_shoup_lazy(static_cast<u32>(u.x) + pm, pv, ps, q) + (static_cast<u32>(v.x) + q);
+        z[4 * c + 1] = mul_shoup_lazy(static_cast<u32>(u.y) + pm, pv, ps, q) + (static_cast<u32>(v.y) + q);
+        z[4 * c + 2] = mul_shoup_lazy(static_cast<u32>(u.z) + pm, pv, ps, q) + (static_cast<u32>(v.z) + q);
+        z[4 * c + 3] = mul_shoup_lazy(static_cast<u32>(u.w) + pm, pv, ps, q) + (static_cast<u32>(v.w) + q);
       }
     } else {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int4 u = cps[c ^ sw];
-        z[4 * c] = signed_residue(u.x, Pi);
-        z[4 * c + 1] = signed_residue(u.y, Pi);
-        z[4 * c + 2] = signed_residue(u.z, Pi);
-        z[4 * c + 3] = signed_residue(u.w, Pi);
+        z[4 * c] = reduce32(static_cast<u32>(u.x) + pm, Pi);
+        z[4 * c + 1] = reduce32(static_cast<u32>(u.y) + pm, Pi);
+        z[4 * c + 2] = reduce32(static_cast<u32>(u.z) + pm, Pi);
+        z[4 * c + 3] = reduce32(static_cast<u32>(u.w) + pm, Pi);
       }
     }
     // accumulator loads issued ahead of the transform; d products computed after it
@@ -623,10 +637,12 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
       for (int k = 0; k < 32; k += 4) {
         const uint4 d = dd[k >> 2], v = vv[k >> 2];
         uint4 o;
-        o.x = mul_shoup(addmod(d.x, mul_shoup(v.x, pv, ps, q), q) + q - z[k], lv, ls, q);
-        o.y = mul_shoup(addmod(d.y, mul_shoup(v.y, pv, ps, q), q) + q - z[k + 1], lv, ls, q);
-        o.z = mul_shoup(addmod(d.z, mul_shoup(v.z, pv, ps, q), q) + q - z[k + 2], lv, ls, q);
-        o.w = mul_shoup(addmod(d.w, mul_shoup(v.w, pv, ps, q), q) + q - z[k + 3], lv, ls, q);
+        // (d + acc * P^-1 - z) * q_{L-1}^-1 with a lazy inner product: < 4q + q, any u32
+        // input is fine for the outer Shoup multiplication, which returns canonical
+        o.x = mul_shoup(d.x + mul_shoup_lazy(v.x, pv, ps, q) + q - z[k], lv, ls, q);
+        o.y = mul_shoup(d.y + mul_shoup_lazy(v.y, pv, ps, q) + q - z[k + 1], lv, ls, q);
+        o.z = mul_shoup(d.z + mul_shoup_lazy(v.z, pv, ps, q) + q - z[k + 2], lv, ls, q);
+        o.w = mul_shoup(d.w + mul_shoup_lazy(v.w, pv, ps, q) + q - z[k + 3], lv, ls, q);
         *reinterpret_cast<uint4*>(out_i + NT::jC(tid, k)) = o;
       }
     } else {
@@ -844,7 +860,7 @@ __global__ void k_mags_to_residues(const ulonglong2* mags, u64 count_n, u32 n, u
 // ===========================================================================
 template <int KIND>
 __global__ void k_imad_probe(u64* sink, u32 iters, u32 seed) {
-  // KIND 0: IMAD (mad.lo.u32), 1: IMAD.WIDE (mad.wide.u32), 2: IMAD.HI (mul.hi.u32),
+  // KIND 0: IMAD (mad.lo.u32), 1: IMAD.WIDE (mul.wide.u32, high word consumed), 2: IMAD.HI (mul.hi.u32),
   // 3: Shoup lazy modular product (IMAD.HI + 2 IMAD; IMAD.HI/IMAD.WIDE issue at a
   //    quarter of the FFMA rate on sm_100, IMAD at half, so this is the NTT's unit)
   u32 a[8];
@@ -858,7 +874,11 @@ __global__ void k_imad_probe(u64* sink, u32 iters, u32 seed) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         if (KIND == 1) {
-          asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(c[i]) : "r"(a[i]), "r"(b));
+          // dependent chain x <- hi(x * b): a loop-invariant `c += a*b` would be strength-
+          // reduced by ptxas into 64-bit adds and measure IADD3, not IMAD.WIDE
+          u64 p;
+          asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(static_cast<u32>(c[i]) ^ a[i]), "r"(b));
+          c[i] = p >> 32;
         } else if (KIND == 0) {
           u32 lo = static_cast<u32>(c[i]);
           asm volatile("mad.lo.u32 %0, %1, %2, %0;" : "+r"(lo) : "r"(a[i]), "r"(b));
@@ -1035,6 +1055,22 @@ int launch_mac_conv(const MacConvArgs& a, const Basis& B, cudaStream_t s) {
   return 1;
 }
 
+// One non-blocking auxiliary stream per device for intra-op fork/join (HG_AUX_STREAM=0 off).
+static cudaStream_t aux_stream() {
+  static const bool on = [] {
+    const char* e = getenv("HG_AUX_STREAM");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  if (!on) return nullptr;
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+  return streams[dev];
+}
+
 int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s) {
   if (a.count == 0) return 0;
   HG_LOGN_SWITCH(logn, {
@@ -1050,11 +1086,29 @@ int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s) {
     { ProfScope ps("k_relin_digits", s);
     dk<<<a.count * a.level, T, sm1, s>>>(a, B);
     }
-    { ProfScope ps("k_relin_keysw", s);
-    ks<<<a.count, T, sm3, s>>>(a, B);
+    // the special-prime and the limb key switches are independent: the special one runs on
+    // an auxiliary stream so each fills the other's tail wave (act2 has only `count` special
+    // CTAs for 148 SMs)
+    cudaStream_t aux = aux_stream();
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (aux) {
+      cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+      cudaEventRecord(fork, s);
+      cudaStreamWaitEvent(aux, fork, 0);
+    }
+    const cudaStream_t ss = aux ? aux : s;
+    { ProfScope ps("k_relin_keysw", ss);
+    ks<<<a.count, T, sm3, ss>>>(a, B);
     }
     { ProfScope ps("k_relin_keysw", s);
     kn<<<a.count * a.level, T, sm3, s>>>(a, B);
+    }
+    if (aux) {
+      cudaEventRecord(join, aux);
+      cudaStreamWaitEvent(s, join, 0);
+      cudaEventDestroy(fork);
+      cudaEventDestroy(join);
     }
     { ProfScope ps("k_relin_moddown", s);
     const int md = a.mode == 0 ? 0 : (a.A == a.Bm ? 1 : 2);

@@ -59,6 +59,7 @@ struct RelinArgs {
   int rescale;
   u32 pinvP[kMaxPrimes], pinvP_sh[kMaxPrimes];  // P^-1 mod q_i
   u32 pinvL[kMaxPrimes], pinvL_sh[kMaxPrimes];  // q_{level-1}^-1 mod q_i
+  u32 pmP[kMaxPrimes];  // multiple of q_i >= floor(P/2): special-prime correction + pmP >= 0
 };
 
 enum class EwOp : int { AddCC = 0, MulScalar = 1, AddScalar = 2, AddVector = 3, Tensor = 4, Copy = 5 };

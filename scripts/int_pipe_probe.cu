@@ -17,6 +17,9 @@ __global__ void probe(u32* sink, u32 iters, u32 seed) {
   for (int i = 0; i < 8; ++i) x[i] = (threadIdx.x ^ seed) * (2 * i + 3) + i;
   const u32 w = seed * 0x9e3779b1u, ws = seed * 0x85ebca6bu, q = 0x3fffc001u | seed;
   const double wq = 0.4375 + seed * 1e-9, cq = 4503599627370496.0 * (1.0 - wq);
+  u64 a64[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a64[i] = x[i] * 3ull + i;
   for (u32 it = 0; it < iters; ++it) {
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
@@ -55,6 +58,26 @@ __global__ void probe(u32* sink, u32 iters, u32 seed) {
           u32 lo;
           asm volatile("mul.lo.u32 %0, %1, %2;" : "=r"(lo) : "r"(v), "r"(w));
           asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(v) : "r"(h), "r"(0u - q), "r"(lo));
+        } else if (KIND == 9) {  // IMAD.WIDE accumulate chain (64-bit accumulator carried)
+          u64 acc = (static_cast<u64>(x[(i + 1) & 7]) << 32) | v;
+          asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(v), "r"(ws));
+          v = static_cast<u32>(acc >> 32) ^ static_cast<u32>(acc);
+        } else if (KIND == 10) {  // IMAD.WIDE with a register (opaque zero) addend, high word used
+          u64 p;
+          const u64 z = static_cast<u64>(seed >> 31);  // 0 at run time, opaque to the compiler
+          asm volatile("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(v), "r"(ws), "l"(z));
+          v = static_cast<u32>(p >> 32);
+        } else if (KIND == 11) {  // IMAD.HI with a register addend
+          asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(v) : "r"(ws), "r"(seed >> 31));
+        } else if (KIND == 12) {  // Shoup with the quotient from mad.wide + register zero
+          u64 p;
+          u32 lo;
+          const u64 z = static_cast<u64>(seed >> 31);
+          asm volatile("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(v), "r"(ws), "l"(z));
+          asm volatile("mul.lo.u32 %0, %1, %2;" : "=r"(lo) : "r"(v), "r"(w));
+          asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(v) : "r"(static_cast<u32>(p >> 32)), "r"(0u - q), "r"(lo));
+        } else if (KIND == 13) {  // IMAD.WIDE accumulate, multiplicand = another chain's low word
+          asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a64[i]) : "r"(static_cast<u32>(a64[(i + 3) & 7])), "r"(ws));
         } else if (KIND == 8) {  // pure DFMA chain on doubles
           double d = __hiloint2double(v, v);
           asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(d) : "d"(wq), "d"(cq));
@@ -66,7 +89,7 @@ __global__ void probe(u32* sink, u32 iters, u32 seed) {
   }
   u32 s = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) s ^= x[i];
+  for (int i = 0; i < 8; ++i) s ^= x[i] ^ static_cast<u32>(a64[i] >> 17);
   if (s == 0x12345u) sink[0] = s;
 }
 
@@ -102,10 +125,12 @@ int main() {
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   const double per_clk = sms * (clk * 1e3);
   const char* names[] = {"IMAD.HI (mul.hi)", "IMAD (mul.lo)", "IMAD.WIDE hi (mul.wide)", "Shoup mul.hi form",
-                         "Shoup mul.wide form", "IADD3", "pair+DFMA.RM", "Shoup DFMA quotient", "DFMA chain"};
-  double r[9] = {run<0>(sms), run<1>(sms), run<2>(sms), run<3>(sms), run<4>(sms),
-                 run<5>(sms), run<6>(sms), run<7>(sms), run<8>(sms)};
-  for (int k = 0; k < 9; ++k)
+                         "Shoup mul.wide form", "IADD3", "pair+DFMA.RM", "Shoup DFMA quotient", "DFMA chain",
+                         "IMAD.WIDE acc chain", "IMAD.WIDE reg-addend hi", "IMAD.HI reg-addend",
+                         "Shoup mad.wide+reg0 form", "IMAD.WIDE accumulate (MAC)"};
+  double r[14] = {run<0>(sms), run<1>(sms), run<2>(sms),  run<3>(sms),  run<4>(sms),  run<5>(sms),  run<6>(sms),
+                  run<7>(sms), run<8>(sms), run<9>(sms), run<10>(sms), run<11>(sms), run<12>(sms), run<13>(sms)};
+  for (int k = 0; k < 14; ++k)
     printf("%-26s %8.2f T steps/s  %6.1f lanes/clk/SM\n", names[k], r[k] / 1e12, r[k] / per_clk);
   return 0;
 }

@@ -5,5 +5,5 @@ for so in build_variants/*.so; do
   echo "== $tag"
   HENET_B200_LIB=$PWD/$so python scripts/ntt_micro.py 2>&1 | grep -E "fwd|inv"
   HENET_B200_LIB=$PWD/$so python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_$tag.json 2>/dev/null
-  python scripts/show_bench.py gpurun_out/bench_$tag.json | grep -E "^value|k_relin|k_rescale|k_ntt"
+  python scripts/show_bench.py gpurun_out/bench_$tag.json 2>/dev/null | grep -E "^value|k_relin|k_rescale|k_ntt"
 done
