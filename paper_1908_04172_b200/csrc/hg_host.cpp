@@ -412,10 +412,13 @@ static CtBatch do_rescale(const Context& ctx, const CtBatch& in, u32 target, cud
       a.out = out.data();
       a.rows = cur.count * cur.polys;
       a.level = L;
+      a.lazy = 1;
       for (u32 i = 0; i + 1 < L; ++i) {
         const u64 q = ctx.chain[i];
         a.pinv[i] = inv_mod_u32(p, q);
         a.pinv_sh[i] = nt::shoup(a.pinv[i], q);
+        a.pm[i] = static_cast<u32>((p / 2 + q - 1) / q * q);
+        if (a.pm[i] + p / 2 >= 4 * q) a.lazy = 0;
       }
       r = launch_rescale(static_cast<int>(ctx.logn), a, ctx.basis, s);
     }

@@ -46,22 +46,19 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
   }
 }
 
-// residue of a signed value with |c| < 2^31 (any relation to q)
-__device__ __forceinline__ u32 signed_residue(i32 c, const DevPrime& P) {
-  const u32 m = reduce32(static_cast<u32>(c < 0 ? -c : c), P);
-  return c < 0 ? csub(P.q - m, P.q) : m;
-}
-
 // ===========================================================================
 // Rescale (one CTA per (ciphertext, polynomial))
 // ===========================================================================
-template <int LOGN>
+// LAZY: the centred correction c (|c| <= q_{L-1}/2) enters each forward transform as
+// c + pm_i < 4 q_i (the lazy transform's input range) instead of being reduced mod q_i.
+template <int LOGN, bool LAZY>
 __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_rescale(RescaleArgs a, Basis B) {
   using NT = Ntt<LOGN>;
   constexpr int N = NT::N;
-  constexpr int T = NT::T;
   extern __shared__ u32 sm[];
-  i32* cs = reinterpret_cast<i32*>(sm + NT::SMEM_WORDS);  // rounding correction, thread-private slots [k * T + tid]
+  // rounding correction: thread-private 32-word row, 128-bit chunks at slot c ^ (tid & 7)
+  int4* cs = reinterpret_cast<int4*>(sm + NT::SMEM_WORDS) + threadIdx.x * 8;
+  const u32 sw = threadIdx.x & 7;
   const u32 tid = threadIdx.x;
   const u64 row = blockIdx.x;
   const u32 L = a.level;
@@ -74,12 +71,26 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
     NT::gload_C(x, src + static_cast<u64>(L - 1) * N, tid);
     NT::inverse(x, sm, tid, Pl);
 #pragma unroll
-    for (int k = 0; k < 32; ++k) cs[k * T + tid] = centered_round_rem(x[k], Pl);
+    for (int c = 0; c < 8; ++c)
+      cs[c ^ sw] = make_int4(centered_round_rem(x[4 * c], Pl), centered_round_rem(x[4 * c + 1], Pl),
+                             centered_round_rem(x[4 * c + 2], Pl), centered_round_rem(x[4 * c + 3], Pl));
   }
+#pragma unroll 1
   for (u32 i = 0; i + 1 < L; ++i) {
     const DevPrime& Pi = B.p[i];
+    const u32 pm = a.pm[i];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) x[k] = signed_residue(cs[k * T + tid], Pi);
+    for (int c = 0; c < 8; ++c) {
+      const int4 v = cs[c ^ sw];
+      x[4 * c] = static_cast<u32>(v.x) + pm;
+      x[4 * c + 1] = static_cast<u32>(v.y) + pm;
+      x[4 * c + 2] = static_cast<u32>(v.z) + pm;
+      x[4 * c + 3] = static_cast<u32>(v.w) + pm;
+    }
+    if (!LAZY) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) x[k] = reduce32(x[k], Pi);
+    }
     const u32* in_i = src + static_cast<u64>(i) * N;
     u32* out_i = dst + static_cast<u64>(i) * N;
     uint4 yv[8];  // issued before the transform so the loads overlap it
@@ -1008,9 +1019,10 @@ int launch_rescale(int logn, const RescaleArgs& a, const Basis& B, cudaStream_t 
   if (a.rows == 0) return 0;
   HG_LOGN_SWITCH(logn, {
     const size_t sm = sizeof(u32) * (Ntt<LN>::SMEM_WORDS + Ntt<LN>::N);
-    set_smem(k_rescale<LN>, sm);
+    auto rk = a.lazy ? k_rescale<LN, true> : k_rescale<LN, false>;
+    set_smem(rk, sm);
     ProfScope ps("k_rescale", s);
-    k_rescale<LN><<<a.rows, 1 << (LN - 5), sm, s>>>(a, B);
+    rk<<<a.rows, 1 << (LN - 5), sm, s>>>(a, B);
   });
   return 1;
 }

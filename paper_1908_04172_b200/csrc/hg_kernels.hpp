@@ -21,6 +21,8 @@ struct RescaleArgs {
   u32 level;  // input level (output level - 1 ... target)
   u32 pinv[kMaxPrimes];     // q_{level-1}^-1 mod q_i
   u32 pinv_sh[kMaxPrimes];
+  u32 pm[kMaxPrimes];       // multiple of q_i >= floor(q_{level-1}/2): correction + pm >= 0
+  int lazy;                 // every pm_i + floor(q_{level-1}/2) < 4 q_i: feed c + pm_i unreduced
 };
 
 struct MacDenseArgs {
