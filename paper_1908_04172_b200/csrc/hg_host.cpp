@@ -1075,9 +1075,16 @@ class Executor {
         a.polys = 2;
         a.x_level = x.level;
         a.N = N;
+        static const bool fp64_on = [] {
+          const char* e = getenv("HG_CONV_FP64");
+          return !(e != nullptr && e[0] == '0');
+        }();
         for (u32 i = 0; i < L; ++i) {
           const long double qm1 = static_cast<long double>(ctx.chain[i] - 1);
-          a.fold[i] = (qm1 * qm1 * (C * win * win) >= 18446744073709551616.0L) ? 1 : 0;
+          const u32 taps = C * win * win;
+          a.fold[i] = (qm1 * qm1 * taps >= 18446744073709551616.0L) ? 1 : 0;
+          // a sum of `taps` products of residues is an integer < 2^53: exact in double
+          a.fp64[i] = (fp64_on && taps <= 32 && qm1 * qm1 * taps < 9007199254740992.0L) ? 1 : 0;
         }
         r = launch_mac_conv(a, ctx.basis, s_);
       }

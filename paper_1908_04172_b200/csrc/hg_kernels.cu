@@ -256,8 +256,85 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_mac_dense(MacDenseArgs a,
 constexpr int kMaxTaps = 1024;
 constexpr int kConvThreads = 256;
 
+// Tap loop of the convolution with its MACs split over two pipes: filters [0, KI) on
+// IMAD.WIDE (fma pipe, u64 accumulators), filters [KI, FT) as DFMAs on the FP64 pipe.
+// Exact: residues < 2^24-ish and at most 32 taps keep every partial sum an integer
+// < 2^53 (host flag fp64[limb]); both accumulators are reduced the same way at the end.
+// A u32 becomes a double with the 2^52 pair trick (MOV + DADD), not the slow I2F.F64.
+__device__ __forceinline__ double u32_to_f64(u32 x) {
+  return __hiloint2double(0x43300000, static_cast<int>(x)) - 4503599627370496.0;
+}
+
+template <int FT, int kPre>
+__device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevPrime& P, const u32* tap_in,
+                                                const u32* wsm, u32 ntaps, const u32* Xb, u64 xstride, u32 poly,
+                                                u32 limb, u32 f0, u32 pos, u32 n) {
+  constexpr int KI = (2 * FT + 2) / 5;  // IMAD.WIDE : DFMA issue-cycle balance (4 vs 2 + conversions)
+  constexpr int KF = FT - KI;
+  u64 acc[KI > 0 ? KI : 1][4];
+  double dacc[KF][4];
+#pragma unroll
+  for (int f = 0; f < KI; ++f)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[f][j] = 0;
+#pragma unroll
+  for (int f = 0; f < KF; ++f)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dacc[f][j] = 0.0;
+  uint4 ring[kPre];
+#pragma unroll
+  for (int i = 0; i < kPre; ++i)
+    ring[i] = (static_cast<u32>(i) < ntaps) ? __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(tap_in[i]) * xstride))
+                                            : make_uint4(0, 0, 0, 0);
+  for (u32 t0 = 0; t0 < ntaps; t0 += kPre) {
+#pragma unroll
+    for (int i = 0; i < kPre; ++i) {
+      const u32 t = t0 + i;
+      if (t >= ntaps) break;
+      const uint4 xv = ring[i];
+      if (t + kPre < ntaps) ring[i] = __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(tap_in[t + kPre]) * xstride));
+#pragma unroll
+      for (int f = 0; f < KI; ++f) {
+        const u64 w = wsm[t * FT + f];
+        acc[f][0] += w * xv.x;
+        acc[f][1] += w * xv.y;
+        acc[f][2] += w * xv.z;
+        acc[f][3] += w * xv.w;
+      }
+      const double x0 = u32_to_f64(xv.x), x1 = u32_to_f64(xv.y), x2 = u32_to_f64(xv.z), x3 = u32_to_f64(xv.w);
+#pragma unroll
+      for (int f = 0; f < KF; ++f) {
+        const double w = u32_to_f64(wsm[t * FT + KI + f]);
+        dacc[f][0] = fma(w, x0, dacc[f][0]);
+        dacc[f][1] = fma(w, x1, dacc[f][1]);
+        dacc[f][2] = fma(w, x2, dacc[f][2]);
+        dacc[f][3] = fma(w, x3, dacc[f][3]);
+      }
+    }
+  }
+  const u32 q = P.q;
+#pragma unroll
+  for (int f = 0; f < FT; ++f) {
+    const u32 ff = f0 + f;
+    if (ff >= a.F) continue;
+    u32 bv = 0;
+    if (a.bias != nullptr && poly == 0) bv = __ldg(&a.bias[static_cast<u64>(limb) * a.F + ff]);
+    u64 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      v[j] = f < KI ? acc[f < KI ? f : 0][j] : static_cast<u64>(dacc[f < KI ? 0 : f - KI][j]);
+    uint4 o;
+    o.x = addmod(reduce64(v[0], P), bv, q);
+    o.y = addmod(reduce64(v[1], P), bv, q);
+    o.z = addmod(reduce64(v[2], P), bv, q);
+    o.w = addmod(reduce64(v[3], P), bv, q);
+    const u64 e = static_cast<u64>(ff) * a.OH * a.OW + pos;
+    *reinterpret_cast<uint4*>(a.Y + ((e * a.polys + poly) * a.level + limb) * a.N + n) = o;
+  }
+}
+
 template <int FT>
-__global__ void __launch_bounds__(kConvThreads) k_mac_conv(MacConvArgs a, Basis B) {
+__global__ void __launch_bounds__(kConvThreads, 3) k_mac_conv(MacConvArgs a, Basis B) {
   __shared__ u32 tap_in[kMaxTaps];
   __shared__ __align__(16) u32 wsm[kMaxTaps * FT];
   __shared__ u32 ntaps_s;
@@ -320,12 +397,16 @@ __global__ void __launch_bounds__(kConvThreads) k_mac_conv(MacConvArgs a, Basis 
   const u64 r32 = P.r32;
   const u32 q = P.q;
 
+  constexpr int kPre = 4;  // gathered inputs in flight
+  if (a.fp64[limb] && ntaps <= 32) {
+    conv_taps_mixed<FT, kPre>(a, P, tap_in, wsm, ntaps, Xb, xstride, poly, limb, f0, pos, n);
+    return;
+  }
   u64 acc[FT][4];
 #pragma unroll
   for (int f = 0; f < FT; ++f)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[f][j] = 0;
-  constexpr int kPre = 4;  // gathered inputs in flight
   uint4 ring[kPre];
 #pragma unroll
   for (int i = 0; i < kPre; ++i)

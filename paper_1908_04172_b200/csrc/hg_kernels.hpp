@@ -44,6 +44,7 @@ struct MacConvArgs {
   u32 C, IH, IW, F, OH, OW, win, stride, pad_top, pad_left;
   u32 level, polys, x_level, N;
   u32 fold[kMaxPrimes];
+  u32 fp64[kMaxPrimes];  // taps * (q-1)^2 < 2^53 and taps <= 32: part of the MACs as exact DFMAs
 };
 
 struct RelinArgs {

@@ -17,6 +17,9 @@ __global__ void probe(u32* sink, u32 iters, u32 seed) {
   for (int i = 0; i < 8; ++i) x[i] = (threadIdx.x ^ seed) * (2 * i + 3) + i;
   const u32 w = seed * 0x9e3779b1u, ws = seed * 0x85ebca6bu, q = 0x3fffc001u | seed;
   const double wq = 0.4375 + seed * 1e-9, cq = 4503599627370496.0 * (1.0 - wq);
+  double dacc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dacc[i] = 1.0 + i * seed;
   u64 a64[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) a64[i] = x[i] * 3ull + i;
@@ -78,6 +81,14 @@ __global__ void probe(u32* sink, u32 iters, u32 seed) {
           asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(v) : "r"(static_cast<u32>(p >> 32)), "r"(0u - q), "r"(lo));
         } else if (KIND == 13) {  // IMAD.WIDE accumulate, multiplicand = another chain's low word
           asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a64[i]) : "r"(static_cast<u32>(a64[(i + 3) & 7])), "r"(ws));
+        } else if (KIND == 14) {  // pure DFMA chains (no integer work)
+          asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(dacc[i]) : "d"(wq), "d"(cq));
+        } else if (KIND == 15) {  // u32 -> f64 by I2F.F64.U32 + DADD into an accumulator
+          dacc[i] += static_cast<double>(v);
+          v += w;
+        } else if (KIND == 16) {  // u32 -> f64 by the 2^52 pair trick (MOV + DADD)
+          dacc[i] += __hiloint2double(0x43300000, v) - 4503599627370496.0;
+          v += w;
         } else if (KIND == 8) {  // pure DFMA chain on doubles
           double d = __hiloint2double(v, v);
           asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(d) : "d"(wq), "d"(cq));
@@ -89,7 +100,7 @@ __global__ void probe(u32* sink, u32 iters, u32 seed) {
   }
   u32 s = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) s ^= x[i] ^ static_cast<u32>(a64[i] >> 17);
+  for (int i = 0; i < 8; ++i) s ^= x[i] ^ static_cast<u32>(a64[i] >> 17) ^ static_cast<u32>(dacc[i]);
   if (s == 0x12345u) sink[0] = s;
 }
 
@@ -127,10 +138,12 @@ int main() {
   const char* names[] = {"IMAD.HI (mul.hi)", "IMAD (mul.lo)", "IMAD.WIDE hi (mul.wide)", "Shoup mul.hi form",
                          "Shoup mul.wide form", "IADD3", "pair+DFMA.RM", "Shoup DFMA quotient", "DFMA chain",
                          "IMAD.WIDE acc chain", "IMAD.WIDE reg-addend hi", "IMAD.HI reg-addend",
-                         "Shoup mad.wide+reg0 form", "IMAD.WIDE accumulate (MAC)"};
-  double r[14] = {run<0>(sms), run<1>(sms), run<2>(sms),  run<3>(sms),  run<4>(sms),  run<5>(sms),  run<6>(sms),
-                  run<7>(sms), run<8>(sms), run<9>(sms), run<10>(sms), run<11>(sms), run<12>(sms), run<13>(sms)};
-  for (int k = 0; k < 14; ++k)
+                         "Shoup mad.wide+reg0 form", "IMAD.WIDE accumulate (MAC)", "DFMA (pure)",
+                         "I2F.F64 + DADD", "pair-MOV + 2 DADD"};
+  double r[17] = {run<0>(sms),  run<1>(sms),  run<2>(sms),  run<3>(sms),  run<4>(sms),  run<5>(sms),
+                  run<6>(sms),  run<7>(sms),  run<8>(sms),  run<9>(sms),  run<10>(sms), run<11>(sms),
+                  run<12>(sms), run<13>(sms), run<14>(sms), run<15>(sms), run<16>(sms)};
+  for (int k = 0; k < 17; ++k)
     printf("%-26s %8.2f T steps/s  %6.1f lanes/clk/SM\n", names[k], r[k] / 1e12, r[k] / per_clk);
   return 0;
 }
