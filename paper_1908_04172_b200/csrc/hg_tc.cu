@@ -24,7 +24,10 @@
 
 namespace hg {
 
-constexpr int kTcM = 128, kTcN = 64, kTcK = 32, kTcS = 4;
+#ifndef HG_TC_STAGES
+#define HG_TC_STAGES 4
+#endif
+constexpr int kTcM = 128, kTcN = 64, kTcK = 32, kTcS = HG_TC_STAGES;
 constexpr int kTcProducers = 256;                 // 8 warps split X into byte planes
 constexpr int kTcThreads = kTcProducers + 32;     // + 1 warp: bulk copies + MMA issue
 constexpr int kTcPlaneA = kTcM * kTcK;            // 4096 B per weight byte plane per K step
@@ -33,7 +36,9 @@ constexpr int kTcCols = 512;                      // TMEM columns: up to 7 accum
 
 struct TcSmem {
   uint8_t a[kTcS][4][kTcPlaneA];  // weight planes (K-major core matrices), filled by cp.async.bulk
-  uint8_t b[kTcS][4][kTcPlaneB];  // input planes, written by the producer warps
+  uint8_t b[kTcS][4][kTcPlaneB];  // input planes, written by the producer warps; the planes of a
+                                  // stage are consecutive, i.e. one K-major (planes*64) x 32 matrix
+  uint8_t zero_a[kTcPlaneA];      // zero weight plane: initialises the upper accumulators
   unsigned long long full_a[kTcS], full_b[kTcS], empty[kTcS];
   u32 tmem;
 };
@@ -114,6 +119,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
   }
+  for (u32 i = tid; i < kTcPlaneA / 16; i += kTcThreads)
+    reinterpret_cast<uint4*>(S.zero_a)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::);  // generic-proxy zeros -> MMA reads
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
@@ -134,8 +142,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
             "l"(Wt + static_cast<u64>(j) * 4 * kTcPlaneA), "r"(bytes), "r"(smem_addr(&S.full_a[st])));
       };
       for (u32 j = 0; j < kTcS - 1 && j < KS; ++j) load_a(j);
-      // idesc: D s32, A/B u8, K-major, N = 64, M = 128
-      const u32 idesc = (2u << 4) | ((kTcN >> 3) << 17) | ((kTcM >> 4) << 24);
+      // One MMA per weight plane pa against all input planes at once: B = the stage's planes
+      // stacked along N (planes * 64 rows), D at TMEM column pa * 64, so input plane pb lands
+      // in columns (pa + pb) * 64: the diagonal accumulator D_s, s = pa + pb, with no
+      // per-(pa, pb) MMA.  idesc: D s32, A/B u8, K-major, N = planes * 64, M = 128.
+      const u32 idesc = (2u << 4) | (((planes * kTcN) >> 3) << 17) | ((kTcM >> 4) << 24);
+      const u64 zd = umma_desc(smem_addr(&S.zero_a[0]));
       for (u32 ks = 0; ks < KS; ++ks) {
         const u32 st = ks % kTcS, use = ks / kTcS;
         const u32 j = ks + kTcS - 1;
@@ -146,18 +158,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
         mbar_wait(&S.full_a[st], use & 1);
         mbar_wait(&S.full_b[st], use & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        const u64 bd = umma_desc(smem_addr(&S.b[st][0][0]));
+        if (ks == 0) {
+          // columns [planes * 64, 2 * planes * 64) (diagonals s >= planes) start at zero
+          asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 0;\n" ::"r"(tmem + planes * kTcN),
+                       "l"(zd), "l"(bd), "r"(idesc));
+        }
         for (u32 pa = 0; pa < planes; ++pa) {
           const u64 ad = umma_desc(smem_addr(&S.a[st][pa][0]));
-          for (u32 pb = 0; pb < planes; ++pb) {
-            const u64 bd = umma_desc(smem_addr(&S.b[st][pb][0]));
-            const u32 s = pa + pb;
-            const u32 first_pa = s >= planes ? s - planes + 1 : 0;
-            const u32 accum = (ks > 0 || pa != first_pa) ? 1u : 0u;
-            asm volatile(
-                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + s * kTcN),
-                "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
-          }
+          const u32 accum = (ks > 0 || pa > 0) ? 1u : 0u;  // pa = 0 of step 0 initialises s < planes
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + pa * kTcN),
+              "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
             smem_addr(&S.empty[st])));
