@@ -32,6 +32,7 @@ constexpr int kTcProducers = 256;                 // 8 warps split X into byte p
 constexpr int kTcThreads = kTcProducers + 32;     // + 1 warp: bulk copies + MMA issue
 constexpr int kTcPlaneA = kTcM * kTcK;            // 4096 B per weight byte plane per K step
 constexpr int kTcPlaneB = kTcN * kTcK;            // 2048 B per input byte plane
+constexpr int kTcXS = 6;                          // cp.async stages of input residues (8 KB each)
 constexpr int kTcCols = 512;                      // TMEM columns: up to 7 accumulators x 64
 
 struct TcSmem {
@@ -39,6 +40,7 @@ struct TcSmem {
   uint8_t b[kTcS][4][kTcPlaneB];  // input planes, written by the producer warps; the planes of a
                                   // stage are consecutive, i.e. one K-major (planes*64) x 32 matrix
   uint8_t zero_a[kTcPlaneA];      // zero weight plane: initialises the upper accumulators
+  u32 xs[kTcXS][kTcK][kTcN];      // input residues staged by cp.async (producer ring)
   unsigned long long full_a[kTcS], full_b[kTcS], empty[kTcS];
   u32 tmem;
 };
@@ -177,45 +179,51 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
       }
     }
   } else {
-    // ===== producers: thread -> (n = tid % 64, k-group = tid / 64 of 8 consecutive k) =====
+    // ===== producers: residues -> shared memory by cp.async (kTcXS steps in flight, no
+    // register cost), then thread -> (n = tid % 64, k-group = tid / 64 of 8 consecutive k)
+    // splits its 8 residues into byte planes of the B stage =====
     const u32 n = tid & (kTcN - 1), kg = tid / kTcN;
     const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
-    const u32* Xn = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n0 + n;
-    auto fetch = [&](u32 ks, u32 (&v)[8]) {
+    const u32* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n0;
+    auto issue = [&](u32 ks) {
+      // 32 rows x 64 residues = 512 chunks of 16 B, two per producer thread; rows >= K zero-fill
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const u32 k = ks * kTcK + kg * 8 + i;
-        v[i] = k < a.K ? __ldg(Xn + static_cast<u64>(k) * xstride) : 0u;
+      for (int i = 0; i < 2; ++i) {
+        const u32 c = tid + i * kTcProducers, row = c >> 4, c4 = (c & 15) * 4;
+        const u32 k = ks * kTcK + row;
+        const u32* src = Xb + static_cast<u64>(k < a.K ? k : 0) * xstride + c4;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(&S.xs[ks % kTcXS][row][c4])),
+                     "l"(src), "r"(k < a.K ? 16 : 0));
       }
     };
-    // 4 steps of X in flight per thread (register ring, statically indexed by unrolling)
-    constexpr int kPre = 4;
-    u32 buf[kPre][8];
-#pragma unroll
-    for (int d = 0; d < kPre; ++d) fetch(d, buf[d]);
-    for (u32 ks0 = 0; ks0 < KS; ks0 += kPre) {
-#pragma unroll
-      for (int d = 0; d < kPre; ++d) {
-        const u32 ks = ks0 + d;
-        if (ks >= KS) break;
-        const u32 st = ks % kTcS, use = ks / kTcS;
-        u32 v[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = buf[d][i];
-        if (ks + kPre < KS) fetch(ks + kPre, buf[d]);
-        if (ks >= kTcS) mbar_wait(&S.empty[st], (use - 1) & 1);
-        for (u32 p = 0; p < planes; ++p) {
-          const u32 sh = 8 * p;
-          const u32 lo = ((v[0] >> sh) & 255) | (((v[1] >> sh) & 255) << 8) | (((v[2] >> sh) & 255) << 16) |
-                         (((v[3] >> sh) & 255) << 24);
-          const u32 hi = ((v[4] >> sh) & 255) | (((v[5] >> sh) & 255) << 8) | (((v[6] >> sh) & 255) << 16) |
-                         (((v[7] >> sh) & 255) << 24);
-          *reinterpret_cast<uint2*>(&S.b[st][p][cm_off(n, kg * 8)]) = make_uint2(lo, hi);
-        }
-        asm volatile("fence.proxy.async.shared::cta;\n" ::);
-        mbar_arrive(&S.full_b[st]);
-      }
+#pragma unroll 1
+    for (u32 j = 0; j < kTcXS - 1; ++j) {
+      if (j < KS) issue(j);
+      asm volatile("cp.async.commit_group;\n" ::);
     }
+    for (u32 ks = 0; ks < KS; ++ks) {
+      const u32 st = ks % kTcS, use = ks / kTcS;
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kTcXS - 2));
+      // every producer's copies of step ks have landed; every producer is done with step ks-1
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kTcProducers));
+      if (ks + kTcXS - 1 < KS) issue(ks + kTcXS - 1);
+      asm volatile("cp.async.commit_group;\n" ::);
+      u32 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = S.xs[ks % kTcXS][kg * 8 + i][n];
+      if (ks >= kTcS) mbar_wait(&S.empty[st], (use - 1) & 1);
+      for (u32 p = 0; p < planes; ++p) {
+        const u32 sh = 8 * p;
+        const u32 lo = ((v[0] >> sh) & 255) | (((v[1] >> sh) & 255) << 8) | (((v[2] >> sh) & 255) << 16) |
+                       (((v[3] >> sh) & 255) << 24);
+        const u32 hi = ((v[4] >> sh) & 255) | (((v[5] >> sh) & 255) << 8) | (((v[6] >> sh) & 255) << 16) |
+                       (((v[7] >> sh) & 255) << 24);
+        *reinterpret_cast<uint2*>(&S.b[st][p][cm_off(n, kg * 8)]) = make_uint2(lo, hi);
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::);
+      mbar_arrive(&S.full_b[st]);
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
 
     // ===== epilogue: warp w reads TMEM lanes 32*(w%4).., columns (w/4)*32 .. +32 =====
     mbar_wait(&S.empty[(KS - 1) % kTcS], ((KS - 1) / kTcS) & 1);
