@@ -32,7 +32,10 @@ constexpr int kTcProducers = 256;                 // 8 warps split X into byte p
 constexpr int kTcThreads = kTcProducers + 32;     // + 1 warp: bulk copies + MMA issue
 constexpr int kTcPlaneA = kTcM * kTcK;            // 4096 B per weight byte plane per K step
 constexpr int kTcPlaneB = kTcN * kTcK;            // 2048 B per input byte plane
-constexpr int kTcXS = 6;                          // cp.async stages of input residues (8 KB each)
+#ifndef HG_TC_XS
+#define HG_TC_XS 6
+#endif
+constexpr int kTcXS = HG_TC_XS;                          // cp.async stages of input residues (8 KB each)
 constexpr int kTcCols = 512;                      // TMEM columns: up to 7 accumulators x 64
 
 struct TcSmem {
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
   if (tid == 0) {
     for (int i = 0; i < kTcS; ++i) {
       mbar_init(&S.full_a[i], 1);
-      mbar_init(&S.full_b[i], kTcProducers);
+      mbar_init(&S.full_b[i], kTcProducers / 32);  // one arrive per producer warp
       mbar_init(&S.empty[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
@@ -180,16 +183,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
     }
   } else {
     // ===== producers: residues -> shared memory by cp.async (kTcXS steps in flight, no
-    // register cost), then thread -> (n = tid % 64, k-group = tid / 64 of 8 consecutive k)
-    // splits its 8 residues into byte planes of the B stage =====
-    const u32 n = tid & (kTcN - 1), kg = tid / kTcN;
+    // register cost).  Warp w owns k rows [4w, 4w+4) of every step: it copies them, reads
+    // them back (so a __syncwarp, not a CTA barrier, orders the two) and writes their byte
+    // planes, lane l for columns l and l + 32; one elected lane arrives per warp. =====
     const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
     const u32* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n0;
+    const u32 r0 = warp * 4;
     auto issue = [&](u32 ks) {
-      // 32 rows x 64 residues = 512 chunks of 16 B, two per producer thread; rows >= K zero-fill
+      // 4 rows x 64 residues = 64 chunks of 16 B, two per lane; rows >= K zero-fill
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const u32 c = tid + i * kTcProducers, row = c >> 4, c4 = (c & 15) * 4;
+        const u32 c = lane + i * 32, row = r0 + (c >> 4), c4 = (c & 15) * 4;
         const u32 k = ks * kTcK + row;
         const u32* src = Xb + static_cast<u64>(k < a.K ? k : 0) * xstride + c4;
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(&S.xs[ks % kTcXS][row][c4])),
@@ -204,24 +208,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
     for (u32 ks = 0; ks < KS; ++ks) {
       const u32 st = ks % kTcS, use = ks / kTcS;
       asm volatile("cp.async.wait_group %0;\n" ::"n"(kTcXS - 2));
-      // every producer's copies of step ks have landed; every producer is done with step ks-1
-      asm volatile("bar.sync 1, %0;\n" ::"n"(kTcProducers));
+      __syncwarp();
+      u32 v0[4], v1[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        v0[i] = S.xs[ks % kTcXS][r0 + i][lane];
+        v1[i] = S.xs[ks % kTcXS][r0 + i][lane + 32];
+      }
+      __syncwarp();  // step ks's rows are consumed before the ring slot is refilled
       if (ks + kTcXS - 1 < KS) issue(ks + kTcXS - 1);
       asm volatile("cp.async.commit_group;\n" ::);
-      u32 v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = S.xs[ks % kTcXS][kg * 8 + i][n];
       if (ks >= kTcS) mbar_wait(&S.empty[st], (use - 1) & 1);
       for (u32 p = 0; p < planes; ++p) {
         const u32 sh = 8 * p;
-        const u32 lo = ((v[0] >> sh) & 255) | (((v[1] >> sh) & 255) << 8) | (((v[2] >> sh) & 255) << 16) |
-                       (((v[3] >> sh) & 255) << 24);
-        const u32 hi = ((v[4] >> sh) & 255) | (((v[5] >> sh) & 255) << 8) | (((v[6] >> sh) & 255) << 16) |
-                       (((v[7] >> sh) & 255) << 24);
-        *reinterpret_cast<uint2*>(&S.b[st][p][cm_off(n, kg * 8)]) = make_uint2(lo, hi);
+        const u32 b0 = ((v0[0] >> sh) & 255) | (((v0[1] >> sh) & 255) << 8) | (((v0[2] >> sh) & 255) << 16) |
+                       (((v0[3] >> sh) & 255) << 24);
+        const u32 b1 = ((v1[0] >> sh) & 255) | (((v1[1] >> sh) & 255) << 8) | (((v1[2] >> sh) & 255) << 16) |
+                       (((v1[3] >> sh) & 255) << 24);
+        *reinterpret_cast<u32*>(&S.b[st][p][cm_off(lane, r0)]) = b0;
+        *reinterpret_cast<u32*>(&S.b[st][p][cm_off(lane + 32, r0)]) = b1;
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::);
-      mbar_arrive(&S.full_b[st]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.full_b[st]);
     }
     asm volatile("cp.async.wait_group 0;\n" ::);
 
