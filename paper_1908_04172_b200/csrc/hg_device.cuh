@@ -26,6 +26,9 @@ using i32 = int32_t;
 
 constexpr int kMaxPrimes = 24;
 
+#ifndef HG_NTT_TWS_MINB
+#define HG_NTT_TWS_MINB 3  // ... and the kernels with staged pass-B twiddles (Ntt<LOGN, true>)
+#endif
 #ifndef HG_NTT_MINB
 #define HG_NTT_MINB 2  // CTAs per SM the NTT kernels are register-budgeted for (N <= 2^13)
 #endif
@@ -138,8 +141,26 @@ __device__ __forceinline__ i32 centered_round_rem(u32 x, const DevPrime& P) {
 #ifndef HG_NTT_SPLIT
 #define HG_NTT_SPLIT 1
 #endif
+// Pass-B twiddle holder: a row of 32 (w, shoup) pairs in 16 x 128-bit registers, or a
+// pointer to the row staged in shared memory (TWS).
+template <bool TWS>
+struct NttTwB;
+template <>
+struct NttTwB<false> {
+  uint4 r[16];
+  __device__ __forceinline__ uint2 at(int n) const {
+    return (n & 1) ? make_uint2(r[n >> 1].z, r[n >> 1].w) : make_uint2(r[n >> 1].x, r[n >> 1].y);
+  }
+};
+template <>
+struct NttTwB<true> {
+  const uint2* row;
+  __device__ __forceinline__ uint2 at(int n) const { return row[n]; }
+};
 
-template <int LOGN_>
+// TWS: pass-B twiddles staged in shared memory (64 fewer registers per thread, 31 LDS.64
+// per transform): the choice of kernels that gain a CTA per SM from it.
+template <int LOGN_, bool TWS = false>
 struct Ntt {
   static constexpr int LOGN = LOGN_;
   static constexpr int N = 1 << LOGN;
@@ -170,8 +191,14 @@ struct Ntt {
   // for all three layouts at N = 2^13, 2^14 (tests/test_ntt_layout.py), and
   // since jmap(tid, k) = base(tid) | const(k) with disjoint bits, the address
   // splits into base(tid) + const(k): every access is an immediate offset.
-  static constexpr int SMEM_WORDS = N + (N >> 5);
+  static constexpr int XCHG_WORDS = N + (N >> 5);  // exchange buffer
   __device__ static __forceinline__ u32 swz(u32 j) { return j + (j >> 5); }
+  // Pass-B twiddles staged (TWS) after the exchange buffer, T >> CB rows padded to 33
+  // pairs so the 4 rows a warp touches fall in different banks.
+  static constexpr int TWB_ROWS = T >> CB;
+  static constexpr int TWB_STRIDE = 33;
+  static constexpr int TWB_WORDS = TWS ? TWB_ROWS * TWB_STRIDE * 2 : 0;
+  static constexpr int SMEM_WORDS = XCHG_WORDS + TWB_WORDS;
 
   // jmap<L>(tid, k) == tpart<L>(tid) | kpart<L>(k) with disjoint bit fields.
   template <int L>
@@ -208,14 +235,25 @@ struct Ntt {
     static constexpr int BLO = (L == 0) ? LOGT : (L == 1 ? CB : 0);
   };
 
-  // Row of staged pass-B twiddles for this thread's group, 16 x 128-bit.
-  __device__ static __forceinline__ void load_rowB(uint4 (&tw)[16], const uint2* base, u32 tid) {
-    const uint4* row = reinterpret_cast<const uint4*>(base + static_cast<size_t>(tid >> CB) * 32);
+  using TwB = NttTwB<TWS>;
+  // Row of staged pass-B twiddles for this thread's group (rows of 32 pairs in global).
+  // The shared-memory variant is ordered before pass B by the transform's first barrier,
+  // and the previous transform finished reading it before its last barrier.
+  __device__ static __forceinline__ void load_rowB(TwB& tw, const uint2* base, u32* sm, u32 tid) {
+    if constexpr (TWS) {
+      uint2* st = reinterpret_cast<uint2*>(sm + XCHG_WORDS);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) tw[i] = __ldg(row + i);
-  }
-  __device__ static __forceinline__ uint2 slot(const uint4 (&tw)[16], int n) {
-    return (n & 1) ? make_uint2(tw[n >> 1].z, tw[n >> 1].w) : make_uint2(tw[n >> 1].x, tw[n >> 1].y);
+      for (int i = 0; i < TWB_ROWS * 32 / T; ++i) {
+        const u32 e = tid + i * T;
+        st[(e >> 5) * TWB_STRIDE + (e & 31)] = __ldg(base + e);
+      }
+      tw.row = st + (tid >> CB) * TWB_STRIDE;
+    } else {
+      (void)sm;
+      const uint4* row = reinterpret_cast<const uint4*>(base + static_cast<size_t>(tid >> CB) * 32);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) tw.r[i] = __ldg(row + i);
+    }
   }
   // Per-thread pass-C bases T_b(tid), b = 0..CB-1 (two 128-bit loads).
   __device__ static __forceinline__ void load_bases(uint2 (&tb)[4], const uint2* base, u32 tid) {
@@ -231,7 +269,7 @@ struct Ntt {
   // Pass A twiddles come from the parameter block, pass B from the preloaded
   // row, pass C as V * T_b(tid) (two Shoup multiplications, no loads).
   template <int L>
-  __device__ static __forceinline__ void fwd_pass(u32 (&x)[32], const DevPrime& P, const uint4 (&twB)[16],
+  __device__ static __forceinline__ void fwd_pass(u32 (&x)[32], const DevPrime& P, const TwB& twB,
                                                   const uint2 (&tb)[4]) {
     constexpr int NB = PassShape<L>::NB;
     constexpr int BLO = PassShape<L>::BLO;
@@ -251,7 +289,7 @@ struct Ntt {
         for (int hi = 0; hi < (1 << (NB - 1 - rb)); ++hi) {
           const u32 kh = (static_cast<u32>(g) << NB) | (static_cast<u32>(hi) << (rb + 1));
           const uint2 w = (L == 0) ? P.twA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))]
-                                   : (L == 1 ? slot(twB, n) : P.tvC[n]);
+                                   : (L == 1 ? twB.at(n) : P.tvC[n]);
           ++n;
 #pragma unroll
           for (int lo = 0; lo < (1 << rb); ++lo) {
@@ -286,7 +324,7 @@ struct Ntt {
         for (int hi = 0; hi < (1 << (NB - 1 - rb)); ++hi) {
           const u32 kh = (static_cast<u32>(g) << NB) | (static_cast<u32>(hi) << (rb + 1));
           const uint2 w = (L == 0) ? P.twA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))]
-                                   : (L == 1 ? slot(twB, n) : P.tvC[n]);
+                                   : (L == 1 ? twB.at(n) : P.tvC[n]);
           ++n;
 #pragma unroll
           for (int lo = 0; lo < (1 << rb); ++lo) {
@@ -309,7 +347,7 @@ struct Ntt {
   // Inverse (Gentleman-Sande, Harvey lazy) stages of pass L.  Values in [0, 2q).
   // Pass A carries the final stage (m = 1), which also applies N^-1.
   template <int L>
-  __device__ static __forceinline__ void inv_pass(u32 (&x)[32], const DevPrime& P, const uint4 (&twB)[16],
+  __device__ static __forceinline__ void inv_pass(u32 (&x)[32], const DevPrime& P, const TwB& twB,
                                                   const uint2 (&tb)[4]) {
     constexpr int NB = PassShape<L>::NB;
     constexpr int BLO = PassShape<L>::BLO;
@@ -335,7 +373,7 @@ struct Ntt {
             }
           } else {
             const uint2 w = (L == 0) ? P.itwA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))]
-                                     : (L == 1 ? slot(twB, n) : P.itvC[n]);
+                                     : (L == 1 ? twB.at(n) : P.itvC[n]);
             ++n;
 #pragma unroll
             for (int lo = 0; lo < (1 << rb); ++lo) {
@@ -358,9 +396,9 @@ struct Ntt {
   // canonical.  `sm` must hold SMEM_WORDS u32; the call begins and ends with a
   // barrier-protected exchange so the buffer may be reused immediately.
   __device__ static __forceinline__ void forward(u32 (&x)[32], u32* sm, u32 tid, const DevPrime& P) {
-    uint4 twB[16];
+    TwB twB;
     uint2 tb[4];
-    load_rowB(twB, P.fwdB, tid);  // in flight during pass A
+    load_rowB(twB, P.fwdB, sm, tid);  // in flight during pass A
     load_bases(tb, P.fwdT, tid);
     fwd_pass<0>(x, P, twB, tb);
     __syncthreads();
@@ -383,10 +421,10 @@ struct Ntt {
 
   // Full inverse transform.  In: layout C, values < 2q.  Out: layout A, canonical.
   __device__ static __forceinline__ void inverse(u32 (&x)[32], u32* sm, u32 tid, const DevPrime& P) {
-    uint4 twB[16];
+    TwB twB;
     uint2 tb[4];
     load_bases(tb, P.invT, tid);
-    load_rowB(twB, P.invB, tid);  // in flight during pass C
+    load_rowB(twB, P.invB, sm, tid);  // in flight during pass C
     inv_pass<2>(x, P, twB, tb);
     __syncthreads();
     store<2>(x, sm, tid);

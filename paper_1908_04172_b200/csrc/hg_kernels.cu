@@ -27,8 +27,8 @@ namespace hg {
 // Batched NTT (hg_ntt_forward / hg_ntt_inverse)
 // ===========================================================================
 template <int LOGN, bool INV>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_ntt(u32* data, u32 level, Basis B) {
-  using NT = Ntt<LOGN>;
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_TWS_MINB : 1)) k_ntt(u32* data, u32 level, Basis B) {
+  using NT = Ntt<LOGN, true>;  // staged pass-B twiddles: 3 CTAs per SM
   extern __shared__ u32 sm[];
   const u32 tid = threadIdx.x;
   const u64 row = blockIdx.x;
@@ -52,8 +52,8 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
 // LAZY: the centred correction c (|c| <= q_{L-1}/2) enters each forward transform as
 // c + pm_i < 4 q_i (the lazy transform's input range) instead of being reduced mod q_i.
 template <int LOGN, bool LAZY>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_rescale(RescaleArgs a, Basis B) {
-  using NT = Ntt<LOGN>;
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_TWS_MINB : 1)) k_rescale(RescaleArgs a, Basis B) {
+  using NT = Ntt<LOGN, true>;  // staged pass-B twiddles: 3 CTAs per SM
   constexpr int N = NT::N;
   extern __shared__ u32 sm[];
   // rounding correction: thread-private 32-word row, 128-bit chunks at slot c ^ (tid & 7)
@@ -480,8 +480,8 @@ __device__ __forceinline__ void load_c2(u32 (&y)[32], const RelinArgs& a, u64 ct
 }
 
 template <int LOGN, int MD>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_relin_digits(RelinArgs a, Basis B) {
-  using NT = Ntt<LOGN>;
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_TWS_MINB : 1)) k_relin_digits(RelinArgs a, Basis B) {
+  using NT = Ntt<LOGN, true>;  // staged pass-B twiddles: 3 CTAs per SM
   constexpr int N = NT::N;
   extern __shared__ u32 sm[];
   const u32 tid = threadIdx.x;
@@ -1082,7 +1082,7 @@ static void set_smem(K kernel, size_t bytes) {
 int launch_ntt(int logn, u32* data, u64 rows, u32 level, bool inverse, const Basis& B, cudaStream_t s) {
   if (rows == 0) return 0;
   HG_LOGN_SWITCH(logn, {
-    const size_t sm = sizeof(u32) * Ntt<LN>::SMEM_WORDS;
+    const size_t sm = sizeof(u32) * Ntt<LN, true>::SMEM_WORDS;
     if (inverse) {
       set_smem(k_ntt<LN, true>, sm);
       ProfScope ps("k_intt", s);
@@ -1099,7 +1099,7 @@ int launch_ntt(int logn, u32* data, u64 rows, u32 level, bool inverse, const Bas
 int launch_rescale(int logn, const RescaleArgs& a, const Basis& B, cudaStream_t s) {
   if (a.rows == 0) return 0;
   HG_LOGN_SWITCH(logn, {
-    const size_t sm = sizeof(u32) * (Ntt<LN>::SMEM_WORDS + Ntt<LN>::N);
+    const size_t sm = sizeof(u32) * (Ntt<LN, true>::SMEM_WORDS + Ntt<LN>::N);
     auto rk = a.lazy ? k_rescale<LN, true> : k_rescale<LN, false>;
     set_smem(rk, sm);
     ProfScope ps("k_rescale", s);
@@ -1167,7 +1167,8 @@ static cudaStream_t aux_stream() {
 int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s) {
   if (a.count == 0) return 0;
   HG_LOGN_SWITCH(logn, {
-    const size_t sm1 = sizeof(u32) * Ntt<LN>::SMEM_WORDS, sm3 = sm1 + 2 * (sizeof(u32) << LN);
+    const size_t sm1 = sizeof(u32) * Ntt<LN, true>::SMEM_WORDS;  // digits (staged twiddles)
+    const size_t sm3 = sizeof(u32) * Ntt<LN>::SMEM_WORDS + 2 * (sizeof(u32) << LN);
     const int T = 1 << (LN - 5);
     const bool prod = a.mode != 0;
     auto dk = prod ? k_relin_digits<LN, 1> : k_relin_digits<LN, 0>;

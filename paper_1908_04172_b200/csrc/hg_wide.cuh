@@ -76,7 +76,7 @@ template <int LOGN_>
 struct NttW {
   using NT = Ntt<LOGN_>;
   static constexpr int LOGN = LOGN_, N = NT::N, LOGT = NT::LOGT, T = NT::T, CB = NT::CB, MB = NT::MB;
-  static constexpr int SMEM_WORDS = NT::SMEM_WORDS;  // u64 words
+  static constexpr int SMEM_WORDS = NT::XCHG_WORDS;  // u64 words
 
   template <int L>
   __device__ static __forceinline__ void store(const u64 (&x)[32], u64* sm, u32 tid) {
