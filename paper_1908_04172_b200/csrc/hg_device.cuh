@@ -129,6 +129,51 @@ __device__ __forceinline__ i32 centered_round_rem(u32 x, const DevPrime& P) {
 }
 
 // ---------------------------------------------------------------------------
+// Tensor memory as per-thread scratch.  A CTA of T threads takes 64 * T / 128 TMEM
+// columns; warp w owns lanes 32 (w % 4) .. + 32 and columns 64 (w / 4) .. + 64, so every
+// thread has 64 private 32-bit cells (its lane) that tcgen05.ld / st move 8 at a time.
+// Keeping a kernel's per-thread rows there instead of in shared memory frees the shared
+// memory that otherwise limits it to 2 CTAs per SM.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u32 tm_smem_addr(const void* p) { return static_cast<u32>(__cvta_generic_to_shared(p)); }
+
+template <int T>
+struct TmemScratch {
+  static constexpr u32 kCols = 64 * (T / 128) < 32 ? 32 : 64 * (T / 128);
+  u32 base;  // this thread's cell 0: lane | column
+  // warp 0 allocates; every thread learns the base after the barrier (slot: one smem word)
+  __device__ __forceinline__ void alloc(u32* slot, u32 tid) {
+    if (tid < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tm_smem_addr(slot)),
+                   "r"(kCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    const u32 w = tid >> 5;
+    base = *slot + (((w & 3) * 32) << 16) + (w >> 2) * 64;
+  }
+  __device__ __forceinline__ void free(u32 tid) {
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+    __syncthreads();
+    if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(base & 0xFFFFu), "r"(kCols));
+  }
+  __device__ __forceinline__ void ld8(u32 col, u32 (&r)[8]) const {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(base + col));
+  }
+  __device__ __forceinline__ void st8(u32 col, const u32 (&r)[8]) const {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(base + col),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+  }
+  __device__ __forceinline__ static void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+  __device__ __forceinline__ static void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+};
+
+// ---------------------------------------------------------------------------
 // NTT block: one CTA of T = N/32 threads transforms one limb held as 32
 // registers per thread, in three register passes separated by two shared
 // memory exchanges.  Register layouts (tid in [0, T), k in [0, 32)):

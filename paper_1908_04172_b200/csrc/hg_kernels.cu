@@ -496,19 +496,20 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_TWS_MINB
 
 // SPECIAL: the CTAs of the special prime (grid = count), else limbs t < level
 // (grid = count * level); split so neither body carries the other's code.
+// The two accumulator rows live in tensor memory (TmemScratch: 64 cells per thread), so
+// shared memory holds only the transform's exchange buffer and staged twiddles and
+// 3 CTAs fit per SM.
 template <int LOGN, int MD, bool SPECIAL>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_relin_keysw(RelinArgs a, Basis B) {
-  using NT = Ntt<LOGN>;
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_TWS_MINB : 1)) k_relin_keysw(RelinArgs a, Basis B) {
+  using NT = Ntt<LOGN, true>;
   constexpr int N = NT::N;
   constexpr int T = NT::T;
   extern __shared__ u32 sm[];
-  // Accumulators: thread-private rows of 32 words (coefficients jC(tid, 0..31)), kept in
-  // [0, 2q) and moved as 128-bit chunks; chunk c of thread tid sits at slot c ^ (tid & 7),
-  // so the 8 threads of each quarter-warp hit distinct bank groups.
   const u32 tid = threadIdx.x;
-  uint4* acc0 = reinterpret_cast<uint4*>(sm + NT::SMEM_WORDS) + tid * 8;
-  uint4* acc1 = acc0 + N / 4;
-  const u32 sw = tid & 7;
+  TmemScratch<T> tm;
+  tm.alloc(sm + NT::SMEM_WORDS, tid);
+  // cells [0, 32): acc0 (c0 part), [32, 64): acc1, coefficient jC(tid, k) at cell k; values
+  // kept in [0, 2q)
   const u32 L = a.level;
   const u64 ct = SPECIAL ? blockIdx.x : blockIdx.x / L;
   const u32 t = SPECIAL ? L : blockIdx.x % L;
@@ -522,6 +523,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
     const uint2* k0 = a.key + ((static_cast<u64>(j) * 2 + 0) * (a.chain_len + 1) + bidx) * N;
     const uint2* k1 = a.key + ((static_cast<u64>(j) * 2 + 1) * (a.chain_len + 1) + bidx) * N;
     auto madd = [&](u32 acc, u32 x, u32 w, u32 wsh) { return csub(acc + mul_shoup_lazy(x, w, wsh, q), q2); };
+    TmemScratch<T>::wait_st();  // the previous digit's stores of these cells
     // key rows are L2-resident but far: issue a round of 4 pair-loads before using any
 #pragma unroll
     for (int qr = 0; qr < 4; ++qr) {
@@ -532,27 +534,27 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
         kv0[i] = __ldg(reinterpret_cast<const uint4*>(k0 + jj));
         kv1[i] = __ldg(reinterpret_cast<const uint4*>(k1 + jj));
       }
+      u32 A0[8], A1[8];
+      tm.ld8(qr * 8, A0);
+      tm.ld8(32 + qr * 8, A1);
+      TmemScratch<T>::wait_ld();
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int k = qr * 8 + 4 * h;
-        const u32 c = (k >> 2) ^ sw;
-        uint4 A0 = acc0[c], A1 = acc1[c];
-        const uint4 u0 = kv0[2 * h], v0 = kv0[2 * h + 1], u1 = kv1[2 * h], v1 = kv1[2 * h + 1];
-        A0.x = madd(A0.x, y[k], u0.x, u0.y);
-        A0.y = madd(A0.y, y[k + 1], u0.z, u0.w);
-        A0.z = madd(A0.z, y[k + 2], v0.x, v0.y);
-        A0.w = madd(A0.w, y[k + 3], v0.z, v0.w);
-        A1.x = madd(A1.x, y[k], u1.x, u1.y);
-        A1.y = madd(A1.y, y[k + 1], u1.z, u1.w);
-        A1.z = madd(A1.z, y[k + 2], v1.x, v1.y);
-        A1.w = madd(A1.w, y[k + 3], v1.z, v1.w);
-        acc0[c] = A0;
-        acc1[c] = A1;
+      for (int i = 0; i < 4; ++i) {
+        const int k = qr * 8 + 2 * i;
+        A0[2 * i] = madd(A0[2 * i], y[k], kv0[i].x, kv0[i].y);
+        A0[2 * i + 1] = madd(A0[2 * i + 1], y[k + 1], kv0[i].z, kv0[i].w);
+        A1[2 * i] = madd(A1[2 * i], y[k], kv1[i].x, kv1[i].y);
+        A1[2 * i + 1] = madd(A1[2 * i + 1], y[k + 1], kv1[i].z, kv1[i].w);
       }
+      tm.st8(qr * 8, A0);
+      tm.st8(32 + qr * 8, A1);
     }
   };
+  {
+    const u32 z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-  for (int c = 0; c < 8; ++c) acc0[c ^ sw] = acc1[c ^ sw] = make_uint4(0, 0, 0, 0);
+    for (int c = 0; c < 64; c += 8) tm.st8(c, z);
+  }
   // Digits j != t (all j for the special prime): NTT_t(digit_j mod q_t), digit j+1
   // loaded during digit j's key products.  The loop body is branch-free: a j == t
   // test inside it makes ptxas duplicate the transform (instruction-cache misses).
@@ -580,37 +582,38 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
     NT::gload_P(nx, a.D + (ct * L + jn) * N, tid);
     mac(y, j);
   }
+  TmemScratch<T>::wait_st();
   if constexpr (!special) {
     // NTT_t(INTT_t(c2_t)) == c2_t: the digit's own limb needs no transform.
     u32 y[32];
     load_c2<LOGN, MD>(y, a, ct, t, P, tid);
     mac(y, t);
+    TmemScratch<T>::wait_st();
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      const uint4* acc = c ? acc1 : acc0;
       u32* dst = a.ACC + ((ct * 2 + c) * L + t) * N;
 #pragma unroll
-      for (int k = 0; k < 32; k += 4) {
-        uint4 v = acc[(k >> 2) ^ sw];
-        v.x = csub(v.x, q);
-        v.y = csub(v.y, q);
-        v.z = csub(v.z, q);
-        v.w = csub(v.w, q);
-        *reinterpret_cast<uint4*>(dst + NT::jC(tid, k)) = v;
+      for (int k = 0; k < 32; k += 8) {
+        u32 v[8];
+        tm.ld8(c * 32 + k, v);
+        TmemScratch<T>::wait_ld();
+        *reinterpret_cast<uint4*>(dst + NT::jC(tid, k)) =
+            make_uint4(csub(v[0], q), csub(v[1], q), csub(v[2], q), csub(v[3], q));
+        *reinterpret_cast<uint4*>(dst + NT::jC(tid, k + 4)) =
+            make_uint4(csub(v[4], q), csub(v[5], q), csub(v[6], q), csub(v[7], q));
       }
     }
   } else {
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) {
-      const uint4* acc = c ? acc1 : acc0;
       u32 y[32];
 #pragma unroll
-      for (int k = 0; k < 32; k += 4) {
-        const uint4 v = acc[(k >> 2) ^ sw];
-        y[k] = csub(v.x, q);
-        y[k + 1] = csub(v.y, q);
-        y[k + 2] = csub(v.z, q);
-        y[k + 3] = csub(v.w, q);
+      for (int k = 0; k < 32; k += 8) {
+        u32 v[8];
+        tm.ld8(c * 32 + k, v);
+        TmemScratch<T>::wait_ld();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[k + i] = csub(v[i], q);
       }
       NT::inverse(y, sm, tid, P);
       i32 cr[32];
@@ -619,6 +622,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
       NT::gstore_P(cr, a.CORR + (ct * 2 + c) * N, tid);  // scratch: layout P
     }
   }
+  tm.free(tid);
 }
 
 // d0 = c0 (mode 0) or a0*b0; d1 = c1 (mode 0) or a0*b1 + a1*b0 (henet/ckks.hpp:407-437), four
@@ -1168,15 +1172,16 @@ int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s) {
   if (a.count == 0) return 0;
   HG_LOGN_SWITCH(logn, {
     const size_t sm1 = sizeof(u32) * Ntt<LN, true>::SMEM_WORDS;  // digits (staged twiddles)
-    const size_t sm3 = sizeof(u32) * Ntt<LN>::SMEM_WORDS + 2 * (sizeof(u32) << LN);
+    const size_t sm3 = sizeof(u32) * Ntt<LN>::SMEM_WORDS + 2 * (sizeof(u32) << LN);  // mod-down
+    const size_t smk = sizeof(u32) * (Ntt<LN, true>::SMEM_WORDS + 4);               // key switch
     const int T = 1 << (LN - 5);
     const bool prod = a.mode != 0;
     auto dk = prod ? k_relin_digits<LN, 1> : k_relin_digits<LN, 0>;
     auto kn = prod ? k_relin_keysw<LN, 1, false> : k_relin_keysw<LN, 0, false>;
     auto ks = prod ? k_relin_keysw<LN, 1, true> : k_relin_keysw<LN, 0, true>;
     set_smem(dk, sm1);
-    set_smem(kn, sm3);
-    set_smem(ks, sm3);
+    set_smem(kn, smk);
+    set_smem(ks, smk);
     { ProfScope ps("k_relin_digits", s);
     dk<<<a.count * a.level, T, sm1, s>>>(a, B);
     }
@@ -1193,10 +1198,10 @@ int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s) {
     }
     const cudaStream_t ss = aux ? aux : s;
     { ProfScope ps("k_relin_keysw", ss);
-    ks<<<a.count, T, sm3, ss>>>(a, B);
+    ks<<<a.count, T, smk, ss>>>(a, B);
     }
     { ProfScope ps("k_relin_keysw", s);
-    kn<<<a.count * a.level, T, sm3, s>>>(a, B);
+    kn<<<a.count * a.level, T, smk, s>>>(a, B);
     }
     if (aux) {
       cudaEventRecord(join, aux);
