@@ -29,6 +29,9 @@ constexpr int kMaxPrimes = 24;
 #ifndef HG_NTT_TWS_MINB
 #define HG_NTT_TWS_MINB 3  // ... and the kernels with staged pass-B twiddles (Ntt<LOGN, true>)
 #endif
+#ifndef HG_MODDOWN_MINB
+#define HG_MODDOWN_MINB 2  // mod-down: its accumulator prefetch needs > 80 registers
+#endif
 #ifndef HG_NTT_MINB
 #define HG_NTT_MINB 2  // CTAs per SM the NTT kernels are register-budgeted for (N <= 2^13)
 #endif

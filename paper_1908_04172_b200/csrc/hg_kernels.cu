@@ -662,27 +662,29 @@ __device__ __forceinline__ uint4 load_d4(const RelinArgs& a, u64 ct, u32 poly, u
 // MD selects the d0/d1 source (load_d4), RS whether the rescale is merged: one
 // instantiation per combination keeps each kernel body inside the instruction cache.
 template <int LOGN, int MD, bool RS>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1)) k_relin_moddown(RelinArgs a, Basis B) {
-  using NT = Ntt<LOGN>;
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_MODDOWN_MINB : 1)) k_relin_moddown(RelinArgs a, Basis B) {
+  using NT = Ntt<LOGN, true>;
   constexpr int N = NT::N;
   constexpr int T = NT::T;
   extern __shared__ u32 sm[];
-  // special-prime (cps) and rescale (crs) corrections: thread-private 32-word rows,
-  // 128-bit chunks at slot c ^ (tid & 7) (see k_relin_keysw)
-  int4* cps = reinterpret_cast<int4*>(sm + NT::SMEM_WORDS) + threadIdx.x * 8;
-  int4* crs = cps + N / 4;
-  const u32 sw = threadIdx.x & 7;
   const u32 tid = threadIdx.x;
+  // special-prime (cps, cells [0, 32)) and rescale (crs, cells [32, 64)) corrections:
+  // thread-private rows in tensor memory (see k_relin_keysw), i32 bit patterns
+  TmemScratch<T> tm;
+  tm.alloc(sm + NT::SMEM_WORDS, tid);
   const u32 L = a.level;
   const u64 ct = blockIdx.x >> 1;
   const u32 poly = blockIdx.x & 1;
   const u32 Lout = RS ? L - 1 : L;
   u32* dst = a.out + (ct * 2 + poly) * static_cast<u64>(Lout) * N;
   const u32* accp = a.ACC + (ct * 2 + poly) * static_cast<u64>(L) * N;
-  {
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
-      cps[c ^ sw] = __ldg(reinterpret_cast<const int4*>(a.CORR + (ct * 2 + poly) * N) + c * T + tid);  // layout P
+  for (int c = 0; c < 8; c += 2) {
+    const int4* src = reinterpret_cast<const int4*>(a.CORR + (ct * 2 + poly) * N);  // layout P
+    const int4 u = __ldg(src + c * T + tid), v = __ldg(src + (c + 1) * T + tid);
+    const u32 w[8] = {static_cast<u32>(u.x), static_cast<u32>(u.y), static_cast<u32>(u.z), static_cast<u32>(u.w),
+                      static_cast<u32>(v.x), static_cast<u32>(v.y), static_cast<u32>(v.z), static_cast<u32>(v.w)};
+    tm.st8(4 * c, w);
   }
   // One loop, one inlined forward transform (the kernel body otherwise overflows the
   // instruction cache): iteration 0 is the top limb L-1, whose mod-down result feeds the
@@ -699,23 +701,25 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
     //   otherwise:     cps + pm reduced once (|cps| <= P/2 may exceed q).
     const u32 pm = a.pmP[i];
     u32 z[32];
+    TmemScratch<T>::wait_st();  // the correction rows written before this limb
     if (RS && !top) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int4 u = cps[c ^ sw], v = crs[c ^ sw];
-        z[4 * c] = mul_shoup_lazy(static_cast<u32>(u.x) + pm, pv, ps, q) + (static_cast<u32>(v.x) + q);
-        z[4 * c + 1] = mul_shoup_lazy(static_cast<u32>(u.y) + pm, pv, ps, q) + (static_cast<u32>(v.y) + q);
-        z[4 * c + 2] = mul_shoup_lazy(static_cast<u32>(u.z) + pm, pv, ps, q) + (static_cast<u32>(v.z) + q);
-        z[4 * c + 3] = mul_shoup_lazy(static_cast<u32>(u.w) + pm, pv, ps, q) + (static_cast<u32>(v.w) + q);
+      for (int c = 0; c < 32; c += 8) {
+        u32 u[8], v[8];
+        tm.ld8(c, u);
+        tm.ld8(32 + c, v);
+        TmemScratch<T>::wait_ld();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) z[c + e] = mul_shoup_lazy(u[e] + pm, pv, ps, q) + (v[e] + q);
       }
     } else {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int4 u = cps[c ^ sw];
-        z[4 * c] = reduce32(static_cast<u32>(u.x) + pm, Pi);
-        z[4 * c + 1] = reduce32(static_cast<u32>(u.y) + pm, Pi);
-        z[4 * c + 2] = reduce32(static_cast<u32>(u.z) + pm, Pi);
-        z[4 * c + 3] = reduce32(static_cast<u32>(u.w) + pm, Pi);
+      for (int c = 0; c < 32; c += 8) {
+        u32 u[8];
+        tm.ld8(c, u);
+        TmemScratch<T>::wait_ld();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) z[c + e] = reduce32(u[e] + pm, Pi);
       }
     }
     // accumulator loads issued ahead of the transform; d products computed after it
@@ -755,12 +759,16 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_MINB : 1
       } else {
         NT::inverse(z, sm, tid, Pi);
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          crs[c ^ sw] = make_int4(centered_round_rem(z[4 * c], Pi), centered_round_rem(z[4 * c + 1], Pi),
-                                  centered_round_rem(z[4 * c + 2], Pi), centered_round_rem(z[4 * c + 3], Pi));
+        for (int c = 0; c < 32; c += 8) {
+          u32 w[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) w[e] = static_cast<u32>(centered_round_rem(z[c + e], Pi));
+          tm.st8(32 + c, w);
+        }
       }
     }
   }
+  tm.free(tid);
 }
 
 // ===========================================================================
@@ -1172,8 +1180,7 @@ int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s) {
   if (a.count == 0) return 0;
   HG_LOGN_SWITCH(logn, {
     const size_t sm1 = sizeof(u32) * Ntt<LN, true>::SMEM_WORDS;  // digits (staged twiddles)
-    const size_t sm3 = sizeof(u32) * Ntt<LN>::SMEM_WORDS + 2 * (sizeof(u32) << LN);  // mod-down
-    const size_t smk = sizeof(u32) * (Ntt<LN, true>::SMEM_WORDS + 4);               // key switch
+    const size_t smk = sizeof(u32) * (Ntt<LN, true>::SMEM_WORDS + 4);  // key switch, mod-down
     const int T = 1 << (LN - 5);
     const bool prod = a.mode != 0;
     auto dk = prod ? k_relin_digits<LN, 1> : k_relin_digits<LN, 0>;
@@ -1214,8 +1221,8 @@ int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s) {
     auto mdk = md == 0 ? (a.rescale ? k_relin_moddown<LN, 0, true> : k_relin_moddown<LN, 0, false>)
              : md == 1 ? (a.rescale ? k_relin_moddown<LN, 1, true> : k_relin_moddown<LN, 1, false>)
                        : (a.rescale ? k_relin_moddown<LN, 2, true> : k_relin_moddown<LN, 2, false>);
-    set_smem(mdk, sm3);
-    mdk<<<a.count * 2, T, sm3, s>>>(a, B);
+    set_smem(mdk, smk);
+    mdk<<<a.count * 2, T, smk, s>>>(a, B);
     }
   });
   return 3;
