@@ -29,6 +29,9 @@ constexpr int kMaxPrimes = 24;
 #ifndef HG_NTT_TWS_MINB
 #define HG_NTT_TWS_MINB 3  // ... and the kernels with staged pass-B twiddles (Ntt<LOGN, true>)
 #endif
+#ifndef HG_KEYSW_MINB
+#define HG_KEYSW_MINB 4  // key switch: accumulators in TMEM (4 x 128 columns), 41 KB smem
+#endif
 #ifndef HG_MODDOWN_MINB
 #define HG_MODDOWN_MINB 2  // mod-down: its accumulator prefetch needs > 80 registers
 #endif

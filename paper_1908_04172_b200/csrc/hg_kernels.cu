@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_TWS_MINB
 // shared memory holds only the transform's exchange buffer and staged twiddles and
 // 3 CTAs fit per SM.
 template <int LOGN, int MD, bool SPECIAL>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_TWS_MINB : 1)) k_relin_keysw(RelinArgs a, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_KEYSW_MINB : 1)) k_relin_keysw(RelinArgs a, Basis B) {
   using NT = Ntt<LOGN, true>;
   constexpr int N = NT::N;
   constexpr int T = NT::T;
@@ -1166,7 +1166,7 @@ static cudaStream_t aux_stream() {
     const char* e = getenv("HG_AUX_STREAM");
     return !(e != nullptr && e[0] == '0');
   }();
-  if (!on) return nullptr;
+  if (!on || g_prof_on) return nullptr;  // the per-kernel profiler serialises launches for attribution
   static std::mutex mu;
   static cudaStream_t streams[64] = {};
   int dev = 0;
