@@ -28,10 +28,12 @@ def launches(path):
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += v
-    tot = sum(v[1] for v in agg.values())
-    out = ["| kernel | launches | total (ncu units) | share |", "|---|---:|---:|---:|"]
+    # bench.py's roofline-denominator probes are not part of the step: listed, not shared
+    tot = sum(v[1] for k, v in agg.items() if "probe" not in k)
+    out = ["| kernel | launches | total (ncu units) | share of the step's kernels |", "|---|---:|---:|---:|"]
     for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
-        out.append(f"| {k} | {v[0]} | {v[1]:.1f} | {v[1] / tot:.3f} |")
+        share = "(peak probe)" if "probe" in k else f"{v[1] / tot:.3f}"
+        out.append(f"| {k} | {v[0]} | {v[1]:.1f} | {share} |")
     return "\n".join(out)
 
 
