@@ -1075,6 +1075,41 @@ class Executor {
         a.polys = 2;
         a.x_level = x.level;
         a.N = N;
+        // valid-tap table per output position (geometry only; henet/graph.hpp:976-989),
+        // cached on the context: (input element, window tap), ascending per position
+        {
+          const u32 npos = a.OH * a.OW;
+          const std::vector<u32> key = {C, a.IH, a.IW, a.OH, a.OW, win, a.stride, a.pad_top, a.pad_left};
+          std::lock_guard<std::mutex> g(ctx.geo_mu);
+          BufPtr& tb = ctx.geo_cache[key];
+          const size_t toff = ((npos + 1) * 4 + 15) / 16 * 16;
+          if (!tb) {
+            std::vector<u32> tab(npos + 1);
+            std::vector<uint2> taps;
+            for (u32 oy = 0; oy < a.OH; ++oy)
+              for (u32 ox = 0; ox < a.OW; ++ox) {
+                for (u32 c = 0; c < C; ++c)
+                  for (u32 ky = 0; ky < win; ++ky)
+                    for (u32 kx = 0; kx < win; ++kx) {
+                      const int iy = static_cast<int>(oy * a.stride + ky) - static_cast<int>(a.pad_top);
+                      const int ix = static_cast<int>(ox * a.stride + kx) - static_cast<int>(a.pad_left);
+                      if (iy < 0 || iy >= static_cast<int>(a.IH) || ix < 0 || ix >= static_cast<int>(a.IW)) continue;
+                      taps.push_back(make_uint2((c * a.IH + static_cast<u32>(iy)) * a.IW + static_cast<u32>(ix),
+                                                (c * win + ky) * win + kx));
+                    }
+                tab[oy * a.OW + ox + 1] = static_cast<u32>(taps.size());
+              }
+            tb = ctx.alloc(toff + taps.size() * 8 + 16, s_);
+            cuda_check(cudaMemcpyAsync(tb->ptr, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, s_), "taps");
+            if (!taps.empty())
+              cuda_check(cudaMemcpyAsync(static_cast<char*>(tb->ptr) + toff, taps.data(), taps.size() * 8,
+                                         cudaMemcpyHostToDevice, s_),
+                         "taps");
+            cuda_check(cudaStreamSynchronize(s_), "taps");  // host vectors leave scope
+          }
+          a.tap_off = static_cast<const u32*>(tb->ptr);
+          a.taps = reinterpret_cast<const uint2*>(static_cast<const char*>(tb->ptr) + toff);
+        }
         static const bool fp64_on = [] {
           const char* e = getenv("HG_CONV_FP64");
           return !(e != nullptr && e[0] == '0');

@@ -337,10 +337,8 @@ template <int FT>
 __global__ void __launch_bounds__(kConvThreads, 3) k_mac_conv(MacConvArgs a, Basis B) {
   __shared__ u32 tap_in[kMaxTaps];
   __shared__ __align__(16) u32 wsm[kMaxTaps * FT];
-  __shared__ u32 ntaps_s;
   const u32 tid = threadIdx.x;
   const u32 pos = blockIdx.y;
-  const u32 oy = pos / a.OW, ox = pos % a.OW;
   const u32 nchunks = (a.F + FT - 1) / FT;
   const u32 pl = blockIdx.z / nchunks;
   const u32 f0 = (blockIdx.z % nchunks) * FT;
@@ -350,47 +348,19 @@ __global__ void __launch_bounds__(kConvThreads, 3) k_mac_conv(MacConvArgs a, Bas
   const u32 taps_all = a.C * a.win * a.win;
   const u32* Wl = a.W + static_cast<u64>(limb) * a.F * taps_all;
 
-  // valid taps in ascending (c, ky, kx) order (henet/graph.hpp:976-989), built in
-  // parallel: tap t of the full window is valid iff its input pixel is in bounds,
-  // and its slot is the number of valid taps before it (warp ballot prefix).
-  if (tid == 0) ntaps_s = 0;
-  __syncthreads();
-  for (u32 base = 0; base < taps_all; base += blockDim.x) {
-    const u32 t = base + tid;
-    bool valid = false;
-    u32 in_idx = 0;
-    if (t < taps_all) {
-      const u32 c = t / (a.win * a.win), ky = (t / a.win) % a.win, kx = t % a.win;
-      const int iy = static_cast<int>(oy * a.stride + ky) - static_cast<int>(a.pad_top);
-      const int ix = static_cast<int>(ox * a.stride + kx) - static_cast<int>(a.pad_left);
-      valid = iy >= 0 && iy < static_cast<int>(a.IH) && ix >= 0 && ix < static_cast<int>(a.IW);
-      in_idx = (c * a.IH + iy) * a.IW + ix;
-    }
-    // block-wide exclusive prefix over `valid` (blockDim.x <= 1024: one ballot per warp)
-    __shared__ u32 warp_cnt[32];
-    const u32 lane = tid & 31, wid = tid >> 5;
-    const u32 bal = __ballot_sync(0xffffffffu, valid);
-    if (lane == 0) warp_cnt[wid] = __popc(bal);
-    __syncthreads();
-    u32 before = ntaps_s;
-    for (u32 w = 0; w < wid; ++w) before += warp_cnt[w];
-    before += __popc(bal & ((1u << lane) - 1));
-    if (valid) {
-      tap_in[before] = in_idx;
-#pragma unroll
-      for (int f = 0; f < FT; ++f)
-        wsm[before * FT + f] = (f0 + f < a.F) ? __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + t]) : 0u;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      u32 tot = 0;
-      for (u32 w = 0; w < (blockDim.x + 31) / 32; ++w) tot += warp_cnt[w];
-      ntaps_s += tot;
-    }
-    __syncthreads();
+  // valid taps of this position in ascending (c, ky, kx) order (henet/graph.hpp:976-989),
+  // from the host-built table (input index, window tap); compact input indices and the
+  // FT weights of each valid tap are staged in shared memory (one barrier)
+  const u32 off0 = __ldg(&a.tap_off[pos]);
+  const u32 ntaps_v = __ldg(&a.tap_off[pos + 1]) - off0;
+  for (u32 i = tid; i < ntaps_v * FT; i += blockDim.x) {
+    const u32 tt = i / FT, f = i % FT;
+    const uint2 e = __ldg(&a.taps[off0 + tt]);
+    if (f == 0) tap_in[tt] = e.x;
+    wsm[i] = (f0 + f < a.F) ? __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + e.y]) : 0u;
   }
   __syncthreads();
-  const u32 ntaps = ntaps_s;
+  const u32 ntaps = ntaps_v;
   const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
   const u32* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n;
   const bool fold = a.fold[limb] != 0;

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cstdint>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -74,6 +75,10 @@ struct Context {
   u64 basis_mod(size_t i) const { return i < chain.size() ? chain[i] : special; }
   cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : core->stream; }
   BufPtr alloc(size_t bytes, cudaStream_t s) const { return std::make_shared<DeviceBuffer>(core, bytes, s); }
+  // Device tables that depend only on a layer's geometry (convolution valid-tap lists),
+  // built and uploaded once per distinct key.
+  mutable std::mutex geo_mu;
+  mutable std::map<std::vector<u32>, BufPtr> geo_cache;
 };
 
 // A batch of ciphertexts with one scale (Ciphertext::scale is identical
