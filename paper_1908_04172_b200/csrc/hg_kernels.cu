@@ -255,6 +255,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_mac_dense(MacDenseArgs a,
 // ===========================================================================
 constexpr int kMaxTaps = 1024;
 constexpr int kConvThreads = 256;
+#ifndef HG_CONV_PP
+#define HG_CONV_PP 2
+#endif
+constexpr u32 kConvPos = HG_CONV_PP;  // output positions per CTA
 
 // Tap loop of the convolution with its MACs split over two pipes: filters [0, KI) on
 // IMAD.WIDE (fma pipe, u64 accumulators), filters [KI, FT) as DFMAs on the FP64 pipe.
@@ -266,7 +270,7 @@ __device__ __forceinline__ double u32_to_f64(u32 x) {
 }
 
 template <int FT, int kPre>
-__device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevPrime& P, const u32* tap_in,
+__device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevPrime& P, const uint2* tp,
                                                 const u32* wsm, u32 ntaps, const u32* Xb, u64 xstride, u32 poly,
                                                 u32 limb, u32 f0, u32 pos, u32 n) {
   constexpr int KI = (2 * FT + 2) / 5;  // IMAD.WIDE : DFMA issue-cycle balance (4 vs 2 + conversions)
@@ -282,20 +286,29 @@ __device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevP
 #pragma unroll
     for (int j = 0; j < 4; ++j) dacc[f][j] = 0.0;
   uint4 ring[kPre];
+  u32 wring[kPre];
 #pragma unroll
-  for (int i = 0; i < kPre; ++i)
-    ring[i] = (static_cast<u32>(i) < ntaps) ? __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(tap_in[i]) * xstride))
+  for (int i = 0; i < kPre; ++i) {
+    const uint2 e = static_cast<u32>(i) < ntaps ? __ldg(tp + i) : make_uint2(0, 0);
+    wring[i] = e.y;
+    ring[i] = (static_cast<u32>(i) < ntaps) ? __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(e.x) * xstride))
                                             : make_uint4(0, 0, 0, 0);
+  }
   for (u32 t0 = 0; t0 < ntaps; t0 += kPre) {
 #pragma unroll
     for (int i = 0; i < kPre; ++i) {
       const u32 t = t0 + i;
       if (t >= ntaps) break;
       const uint4 xv = ring[i];
-      if (t + kPre < ntaps) ring[i] = __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(tap_in[t + kPre]) * xstride));
+      const u32* wt = wsm + wring[i] * FT;
+      if (t + kPre < ntaps) {
+        const uint2 e = __ldg(tp + t + kPre);
+        wring[i] = e.y;
+        ring[i] = __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(e.x) * xstride));
+      }
 #pragma unroll
       for (int f = 0; f < KI; ++f) {
-        const u64 w = wsm[t * FT + f];
+        const u64 w = wt[f];
         acc[f][0] += w * xv.x;
         acc[f][1] += w * xv.y;
         acc[f][2] += w * xv.z;
@@ -304,7 +317,7 @@ __device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevP
       const double x0 = u32_to_f64(xv.x), x1 = u32_to_f64(xv.y), x2 = u32_to_f64(xv.z), x3 = u32_to_f64(xv.w);
 #pragma unroll
       for (int f = 0; f < KF; ++f) {
-        const double w = u32_to_f64(wsm[t * FT + KI + f]);
+        const double w = u32_to_f64(wt[KI + f]);
         dacc[f][0] = fma(w, x0, dacc[f][0]);
         dacc[f][1] = fma(w, x1, dacc[f][1]);
         dacc[f][2] = fma(w, x2, dacc[f][2]);
@@ -333,77 +346,54 @@ __device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevP
   }
 }
 
-template <int FT>
-__global__ void __launch_bounds__(kConvThreads, 3) k_mac_conv(MacConvArgs a, Basis B) {
-  __shared__ u32 tap_in[kMaxTaps];
-  __shared__ __align__(16) u32 wsm[kMaxTaps * FT];
-  const u32 tid = threadIdx.x;
-  const u32 pos = blockIdx.y;
-  const u32 nchunks = (a.F + FT - 1) / FT;
-  const u32 pl = blockIdx.z / nchunks;
-  const u32 f0 = (blockIdx.z % nchunks) * FT;
-  const u32 poly = pl / a.level, limb = pl % a.level;
-  const DevPrime& P = B.p[limb];
-  const u32 n = (blockIdx.x * blockDim.x + tid) * 4;
-  const u32 taps_all = a.C * a.win * a.win;
-  const u32* Wl = a.W + static_cast<u64>(limb) * a.F * taps_all;
-
-  // valid taps of this position in ascending (c, ky, kx) order (henet/graph.hpp:976-989),
-  // from the host-built table (input index, window tap); compact input indices and the
-  // FT weights of each valid tap are staged in shared memory (one barrier)
-  const u32 off0 = __ldg(&a.tap_off[pos]);
-  const u32 ntaps_v = __ldg(&a.tap_off[pos + 1]) - off0;
-  for (u32 i = tid; i < ntaps_v * FT; i += blockDim.x) {
-    const u32 tt = i / FT, f = i % FT;
-    const uint2 e = __ldg(&a.taps[off0 + tt]);
-    if (f == 0) tap_in[tt] = e.x;
-    wsm[i] = (f0 + f < a.F) ? __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + e.y]) : 0u;
-  }
-  __syncthreads();
-  const u32 ntaps = ntaps_v;
-  const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
-  const u32* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n;
+template <int FT, int kPre>
+__device__ __forceinline__ void conv_taps_int(const MacConvArgs& a, const DevPrime& P, const uint2* tp,
+                                              const u32* wsm, u32 ntaps, const u32* Xb, u64 xstride, u32 poly,
+                                              u32 limb, u32 f0, u32 pos, u32 n) {
   const bool fold = a.fold[limb] != 0;
   const u64 r32 = P.r32;
   const u32 q = P.q;
-
-  constexpr int kPre = 4;  // gathered inputs in flight
-  if (a.fp64[limb] && ntaps <= 32) {
-    conv_taps_mixed<FT, kPre>(a, P, tap_in, wsm, ntaps, Xb, xstride, poly, limb, f0, pos, n);
-    return;
-  }
   u64 acc[FT][4];
 #pragma unroll
   for (int f = 0; f < FT; ++f)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[f][j] = 0;
   uint4 ring[kPre];
+  u32 wring[kPre];
 #pragma unroll
-  for (int i = 0; i < kPre; ++i)
-    ring[i] = (static_cast<u32>(i) < ntaps) ? __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(tap_in[i]) * xstride))
+  for (int i = 0; i < kPre; ++i) {
+    const uint2 e = static_cast<u32>(i) < ntaps ? __ldg(tp + i) : make_uint2(0, 0);
+    wring[i] = e.y;
+    ring[i] = (static_cast<u32>(i) < ntaps) ? __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(e.x) * xstride))
                                             : make_uint4(0, 0, 0, 0);
+  }
   for (u32 t0 = 0; t0 < ntaps; t0 += kPre) {
 #pragma unroll
-   for (int i = 0; i < kPre; ++i) {
-    const u32 t = t0 + i;
-    if (t >= ntaps) break;
-    const uint4 xv = ring[i];
-    if (t + kPre < ntaps) ring[i] = __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(tap_in[t + kPre]) * xstride));
+    for (int i = 0; i < kPre; ++i) {
+      const u32 t = t0 + i;
+      if (t >= ntaps) break;
+      const uint4 xv = ring[i];
+      const u32* wt = wsm + wring[i] * FT;
+      if (t + kPre < ntaps) {
+        const uint2 e = __ldg(tp + t + kPre);
+        wring[i] = e.y;
+        ring[i] = __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(e.x) * xstride));
+      }
 #pragma unroll
-    for (int f = 0; f < FT; ++f) {
-      const u32 w = wsm[t * FT + f];
-      acc[f][0] += static_cast<u64>(w) * xv.x;
-      acc[f][1] += static_cast<u64>(w) * xv.y;
-      acc[f][2] += static_cast<u64>(w) * xv.z;
-      acc[f][3] += static_cast<u64>(w) * xv.w;
+      for (int f = 0; f < FT; ++f) {
+        const u32 w = wt[f];
+        acc[f][0] += static_cast<u64>(w) * xv.x;
+        acc[f][1] += static_cast<u64>(w) * xv.y;
+        acc[f][2] += static_cast<u64>(w) * xv.z;
+        acc[f][3] += static_cast<u64>(w) * xv.w;
+      }
+      if (fold && (t & 7) == 7) {
+#pragma unroll
+        for (int f = 0; f < FT; ++f)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[f][j] = (acc[f][j] & 0xffffffffull) + (acc[f][j] >> 32) * r32;
+      }
     }
-    if (fold && (t & 7) == 7) {
-#pragma unroll
-      for (int f = 0; f < FT; ++f)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[f][j] = (acc[f][j] & 0xffffffffull) + (acc[f][j] >> 32) * r32;
-    }
-   }
   }
 #pragma unroll
   for (int f = 0; f < FT; ++f) {
@@ -417,8 +407,45 @@ __global__ void __launch_bounds__(kConvThreads, 3) k_mac_conv(MacConvArgs a, Bas
     o.z = addmod(reduce64(acc[f][2], P), bv, q);
     o.w = addmod(reduce64(acc[f][3], P), bv, q);
     const u64 e = static_cast<u64>(ff) * a.OH * a.OW + pos;
-    u32* yp = a.Y + ((e * a.polys + poly) * a.level + limb) * a.N + n;
-    *reinterpret_cast<uint4*>(yp) = o;
+    *reinterpret_cast<uint4*>(a.Y + ((e * a.polys + poly) * a.level + limb) * a.N + n) = o;
+  }
+}
+
+// CTA: kConvPos consecutive output positions x (4 * kConvThreads coefficients of one
+// (poly, limb)) x FT filters.  The FT weights of every window tap are staged once
+// ([window tap][FT]); each position's valid taps come from the host-built table.
+template <int FT>
+__global__ void __launch_bounds__(kConvThreads, 3) k_mac_conv(MacConvArgs a, Basis B) {
+  __shared__ __align__(16) u32 wsm[kMaxTaps * FT];
+  const u32 tid = threadIdx.x;
+  const u32 npos = a.OH * a.OW;
+  const u32 nchunks = (a.F + FT - 1) / FT;
+  const u32 pl = blockIdx.z / nchunks;
+  const u32 f0 = (blockIdx.z % nchunks) * FT;
+  const u32 poly = pl / a.level, limb = pl % a.level;
+  const DevPrime& P = B.p[limb];
+  const u32 n = (blockIdx.x * blockDim.x + tid) * 4;
+  const u32 taps_all = a.C * a.win * a.win;
+  const u32* Wl = a.W + static_cast<u64>(limb) * a.F * taps_all;
+  for (u32 i = tid; i < taps_all * FT; i += blockDim.x) {
+    const u32 t = i / FT, f = i % FT;
+    wsm[i] = (f0 + f < a.F) ? __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + t]) : 0u;
+  }
+  __syncthreads();
+  const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
+  const u32* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n;
+  const bool fp = a.fp64[limb] != 0;
+  constexpr int kPre = 4;  // gathered inputs in flight
+  const u32 p1 = min(npos, (blockIdx.y + 1) * kConvPos);
+#pragma unroll 1
+  for (u32 pos = blockIdx.y * kConvPos; pos < p1; ++pos) {
+    // valid taps in ascending (c, ky, kx) order (henet/graph.hpp:976-989)
+    const u32 off0 = __ldg(&a.tap_off[pos]);
+    const u32 ntaps = __ldg(&a.tap_off[pos + 1]) - off0;
+    if (fp && ntaps <= 32)
+      conv_taps_mixed<FT, kPre>(a, P, a.taps + off0, wsm, ntaps, Xb, xstride, poly, limb, f0, pos, n);
+    else
+      conv_taps_int<FT, kPre>(a, P, a.taps + off0, wsm, ntaps, Xb, xstride, poly, limb, f0, pos, n);
   }
 }
 
@@ -1110,7 +1137,7 @@ int launch_mac_dense(const MacDenseArgs& a, const Basis& B, cudaStream_t s) {
 template <int FT>
 static void conv_launch(const MacConvArgs& a, const Basis& B, cudaStream_t s) {
   const u32 nchunks = (a.F + FT - 1) / FT;
-  dim3 grid(a.N / (4 * kConvThreads), a.OH * a.OW, a.polys * a.level * nchunks);
+  dim3 grid(a.N / (4 * kConvThreads), (a.OH * a.OW + kConvPos - 1) / kConvPos, a.polys * a.level * nchunks);
   ProfScope ps("k_mac_conv", s);
   k_mac_conv<FT><<<grid, kConvThreads, 0, s>>>(a, B);
 }
