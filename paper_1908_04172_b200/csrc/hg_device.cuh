@@ -27,7 +27,13 @@ using i32 = int32_t;
 constexpr int kMaxPrimes = 24;
 
 #ifndef HG_NTT_TWS_MINB
-#define HG_NTT_TWS_MINB 3  // ... and the kernels with staged pass-B twiddles (Ntt<LOGN, true>)
+#define HG_NTT_TWS_MINB 4  // ... and the kernels with staged pass-B twiddles (Ntt<LOGN, true>)
+#endif
+#ifndef HG_RESCALE_MINB
+#define HG_RESCALE_MINB 4  // rescale: correction row in TMEM, 41 KB smem, 64 registers
+#endif
+#ifndef HG_DIGITS_MINB
+#define HG_DIGITS_MINB 4
 #endif
 #ifndef HG_KEYSW_MINB
 #define HG_KEYSW_MINB 4  // key switch: accumulators in TMEM (4 x 128 columns), 41 KB smem

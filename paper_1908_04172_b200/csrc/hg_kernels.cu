@@ -52,14 +52,14 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_TWS_MINB
 // LAZY: the centred correction c (|c| <= q_{L-1}/2) enters each forward transform as
 // c + pm_i < 4 q_i (the lazy transform's input range) instead of being reduced mod q_i.
 template <int LOGN, bool LAZY>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_TWS_MINB : 1)) k_rescale(RescaleArgs a, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_RESCALE_MINB : 1)) k_rescale(RescaleArgs a, Basis B) {
   using NT = Ntt<LOGN, true>;  // staged pass-B twiddles: 3 CTAs per SM
   constexpr int N = NT::N;
   extern __shared__ u32 sm[];
-  // rounding correction: thread-private 32-word row, 128-bit chunks at slot c ^ (tid & 7)
-  int4* cs = reinterpret_cast<int4*>(sm + NT::SMEM_WORDS) + threadIdx.x * 8;
-  const u32 sw = threadIdx.x & 7;
   const u32 tid = threadIdx.x;
+  // rounding correction: thread-private row in tensor memory (cells [0, 32), i32 bits)
+  TmemScratch<NT::T> tm;
+  tm.alloc(sm + NT::SMEM_WORDS, tid);
   const u64 row = blockIdx.x;
   const u32 L = a.level;
   const u32* src = a.in + row * L * N;
@@ -71,21 +71,25 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_TWS_MINB
     NT::gload_C(x, src + static_cast<u64>(L - 1) * N, tid);
     NT::inverse(x, sm, tid, Pl);
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
-      cs[c ^ sw] = make_int4(centered_round_rem(x[4 * c], Pl), centered_round_rem(x[4 * c + 1], Pl),
-                             centered_round_rem(x[4 * c + 2], Pl), centered_round_rem(x[4 * c + 3], Pl));
+    for (int c = 0; c < 32; c += 8) {
+      u32 w[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) w[e] = static_cast<u32>(centered_round_rem(x[c + e], Pl));
+      tm.st8(c, w);
+    }
+    TmemScratch<NT::T>::wait_st();
   }
 #pragma unroll 1
   for (u32 i = 0; i + 1 < L; ++i) {
     const DevPrime& Pi = B.p[i];
     const u32 pm = a.pm[i];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int4 v = cs[c ^ sw];
-      x[4 * c] = static_cast<u32>(v.x) + pm;
-      x[4 * c + 1] = static_cast<u32>(v.y) + pm;
-      x[4 * c + 2] = static_cast<u32>(v.z) + pm;
-      x[4 * c + 3] = static_cast<u32>(v.w) + pm;
+    for (int c = 0; c < 32; c += 8) {
+      u32 v[8];
+      tm.ld8(c, v);
+      TmemScratch<NT::T>::wait_ld();
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[c + e] = v[e] + pm;
     }
     if (!LAZY) {
 #pragma unroll
@@ -110,6 +114,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_TWS_MINB
       *reinterpret_cast<uint4*>(out_i + j) = o;
     }
   }
+  tm.free(tid);
 }
 
 // ===========================================================================
@@ -477,7 +482,7 @@ __device__ __forceinline__ void load_c2(u32 (&y)[32], const RelinArgs& a, u64 ct
 }
 
 template <int LOGN, int MD>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_TWS_MINB : 1)) k_relin_digits(RelinArgs a, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_DIGITS_MINB : 1)) k_relin_digits(RelinArgs a, Basis B) {
   using NT = Ntt<LOGN, true>;  // staged pass-B twiddles: 3 CTAs per SM
   constexpr int N = NT::N;
   extern __shared__ u32 sm[];
@@ -1108,7 +1113,7 @@ int launch_ntt(int logn, u32* data, u64 rows, u32 level, bool inverse, const Bas
 int launch_rescale(int logn, const RescaleArgs& a, const Basis& B, cudaStream_t s) {
   if (a.rows == 0) return 0;
   HG_LOGN_SWITCH(logn, {
-    const size_t sm = sizeof(u32) * (Ntt<LN, true>::SMEM_WORDS + Ntt<LN>::N);
+    const size_t sm = sizeof(u32) * (Ntt<LN, true>::SMEM_WORDS + 4);
     auto rk = a.lazy ? k_rescale<LN, true> : k_rescale<LN, false>;
     set_smem(rk, sm);
     ProfScope ps("k_rescale", s);
