@@ -38,6 +38,9 @@ constexpr int kMaxPrimes = 24;
 #ifndef HG_KEYSW_MINB
 #define HG_KEYSW_MINB 4  // key switch: accumulators in TMEM (4 x 128 columns), 41 KB smem
 #endif
+#ifndef HG_MODDOWN_PREFETCH
+#define HG_MODDOWN_PREFETCH 1  // accumulator row loaded before the transform (registers)
+#endif
 #ifndef HG_MODDOWN_MINB
 #define HG_MODDOWN_MINB 2  // mod-down: its accumulator prefetch needs > 80 registers
 #endif

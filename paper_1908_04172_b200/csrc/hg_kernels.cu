@@ -725,9 +725,14 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_MODDOWN_MINB
       }
     }
     // accumulator loads issued ahead of the transform; d products computed after it
+#if HG_MODDOWN_PREFETCH
     uint4 vv[8];
 #pragma unroll
     for (int g = 0; g < 8; ++g) vv[g] = __ldg(reinterpret_cast<const uint4*>(accp + static_cast<u64>(i) * N + NT::jC(tid, 4 * g)));
+#define HG_MD_V(g) vv[g]
+#else
+#define HG_MD_V(g) __ldg(reinterpret_cast<const uint4*>(accp + static_cast<u64>(i) * N + NT::jC(tid, 4 * (g))))
+#endif
     NT::forward(z, sm, tid, Pi);
     uint4 dd[8];
 #pragma unroll
@@ -737,7 +742,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_MODDOWN_MINB
       const u32 lv = a.pinvL[i], ls = a.pinvL_sh[i];
 #pragma unroll
       for (int k = 0; k < 32; k += 4) {
-        const uint4 d = dd[k >> 2], v = vv[k >> 2];
+        const uint4 d = dd[k >> 2], v = HG_MD_V(k >> 2);
         uint4 o;
         // (d + acc * P^-1 - z) * q_{L-1}^-1 with a lazy inner product: < 4q + q, any u32
         // input is fine for the outer Shoup multiplication, which returns canonical
@@ -750,7 +755,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_MODDOWN_MINB
     } else {
 #pragma unroll
       for (int k = 0; k < 32; k += 4) {
-        const uint4 d = dd[k >> 2], v = vv[k >> 2];
+        const uint4 d = dd[k >> 2], v = HG_MD_V(k >> 2);
         z[k] = addmod(d.x, mul_shoup(v.x + q - z[k], pv, ps, q), q);
         z[k + 1] = addmod(d.y, mul_shoup(v.y + q - z[k + 1], pv, ps, q), q);
         z[k + 2] = addmod(d.z, mul_shoup(v.z + q - z[k + 2], pv, ps, q), q);
