@@ -1452,7 +1452,13 @@ int hg_tensor_upload(hg_tensor* t, const uint64_t* words, void* stream) {
     cudaStream_t s = ctx.pick(stream);
     const u64 n = t->b.words(ctx.n);
     int r;
-    BufPtr stage = ctx.alloc((ctx.wide ? 0 : n * 8) + sizeof(int), s);
+    const size_t need = (ctx.wide ? 0 : n * 8) + sizeof(int);
+    if (!t->stage || t->stage->bytes < need) {
+      // allocated on the context's own stream (it outlives any caller stream), then ready
+      t->stage = ctx.alloc(need, ctx.core->stream);
+      cuda_check(cudaStreamSynchronize(ctx.core->stream), "upload staging");
+    }
+    BufPtr stage = t->stage;
     int* bad = reinterpret_cast<int*>(static_cast<char*>(stage->ptr) + (ctx.wide ? 0 : n * 8));
     cuda_check(cudaMemsetAsync(bad, 0, sizeof(int), s), "memset");
     if (ctx.wide) {

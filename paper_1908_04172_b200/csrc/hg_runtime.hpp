@@ -154,6 +154,9 @@ struct hg_ctx {
 struct hg_tensor {
   std::shared_ptr<hg::Context> ctx;
   hg::CtBatch b;
+  // upload staging (u64 words + validation flag), kept across uploads: a fresh 617 MB
+  // stream-ordered allocation per call cannot always reuse a block freed on another stream
+  hg::BufPtr stage;
 };
 struct hg_relin_key {
   std::shared_ptr<hg::Context> ctx;
