@@ -967,6 +967,16 @@ class Executor {
         check_launch(r, "encode bias");
       }
       if (ctx.wide) {
+        // Limbs whose prime is < 2^30 (BASELINE c4/c5b: limbs 1..7) go through the int8 tensor
+        // cores on a u32 copy of their residues; the rest (the 40-bit limb 0) on the wide
+        // CUDA-core kernel.
+        u32 tc_lo = L;
+        if (ctx.dense_tc && K <= 8192 && L >= 2) {
+          tc_lo = 1;
+          for (u32 i = 1; i < L; ++i)
+            if (ctx.chain[i] >= (1ull << 30)) tc_lo = L;
+          if (ctx.chain[0] < (1ull << 30)) tc_lo = L;  // all narrow: no wide context would exist
+        }
         MacDenseArgsW a{};
         a.X = x.data64();
         a.Y = v.cipher.data64();
@@ -979,7 +989,52 @@ class Executor {
         a.level = L;
         a.polys = 2;
         a.x_level = x.level;
+        a.limb_lo = 0;
+        a.limb_cnt = tc_lo;
         r = launch_mac_dense_w(a, ctx.basisw, s_);
+        if (r >= 0 && tc_lo < L) {
+          check_launch(r, "mac_dense_w");
+          const u32 cnt = L - tc_lo;
+          // u32 copies: inputs [K][2][cnt][N], weights [cnt][K][Mpad], bias [cnt][Mpad]
+          BufPtr xn = ctx.alloc(static_cast<u64>(K) * 2 * cnt * N * 4, s_);
+          BufPtr yn = ctx.alloc(static_cast<u64>(Mo) * 2 * cnt * N * 4, s_);
+          BufPtr wn = ctx.alloc(static_cast<u64>(cnt) * K * Mpad * 4, s_);
+          check_launch(launch_limbs_to_u32(x.data64(), static_cast<u32*>(xn->ptr), static_cast<u64>(K) * 2, x.level,
+                                           tc_lo, cnt, N, s_),
+                       "narrow inputs");
+          check_launch(launch_limbs_to_u32(static_cast<const u64*>(wres->ptr), static_cast<u32*>(wn->ptr), 1, L, tc_lo,
+                                           cnt, static_cast<u32>(static_cast<u64>(K) * Mpad), s_),
+                       "narrow weights");
+          BufPtr bn;
+          if (bias_res) {
+            bn = ctx.alloc(static_cast<u64>(cnt) * Mpad * 4, s_);
+            check_launch(launch_limbs_to_u32(static_cast<const u64*>(bias_res->ptr), static_cast<u32*>(bn->ptr), 1, L,
+                                             tc_lo, cnt, Mpad, s_),
+                         "narrow bias");
+          }
+          BufPtr wp = ctx.alloc(tc_packed_weight_bytes(K, Mo, cnt), s_);
+          check_launch(launch_pack_weights_tc(static_cast<const u32*>(wn->ptr), static_cast<uint8_t*>(wp->ptr), K, Mo,
+                                              Mpad, cnt, s_),
+                       "pack weights");
+          Basis sub{};  // the narrow constants of limbs tc_lo.. (every basis entry < 2^32 is valid)
+          for (u32 i = 0; i < cnt; ++i) sub.p[i] = ctx.basis.p[tc_lo + i];
+          MacDenseTcArgs t{};
+          t.X = static_cast<const u32*>(xn->ptr);
+          t.Y = static_cast<u32*>(yn->ptr);
+          t.Wp = static_cast<const uint8_t*>(wp->ptr);
+          t.bias = bn ? static_cast<const u32*>(bn->ptr) : nullptr;
+          t.K = K;
+          t.M = Mo;
+          t.Mpad = Mpad;
+          t.N = N;
+          t.level = cnt;
+          t.polys = 2;
+          t.x_level = cnt;
+          for (u32 i = 0; i < cnt; ++i) t.planes[i] = ctx.chain[tc_lo + i] < (1ull << 24) ? 3 : 4;
+          check_launch(launch_mac_dense_tc(t, sub, s_), "mac_dense_tc");
+          r = launch_limbs_to_u64(static_cast<const u32*>(yn->ptr), v.cipher.data64(), static_cast<u64>(Mo) * 2, L, tc_lo,
+                                  cnt, N, s_);
+        }
       } else if (ctx.dense_tc && K <= 8192) {
         // tensor-core path: byte-plane weights packed once per call, then tcgen05.mma.kind::i8
         BufPtr wp = ctx.alloc(tc_packed_weight_bytes(K, Mo, L), s_);

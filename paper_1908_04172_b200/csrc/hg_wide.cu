@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(kWWarps * 32) k_mac_dense_w(MacDenseArgsW a, B
   const u32 BM = kWTM * kWWarps;
   const u32 n0 = blockIdx.x * kWBN;
   const u32 m0 = blockIdx.y * BM;
-  const u32 poly = blockIdx.z / a.level, limb = blockIdx.z % a.level;
+  const u32 nl = a.limb_cnt ? a.limb_cnt : a.level;
+  const u32 poly = blockIdx.z / nl, limb = a.limb_lo + blockIdx.z % nl;
   const DevPrimeW& P = B.p[limb];
   const bool wide = P.q >= (1ull << 32);
   const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
@@ -374,10 +375,46 @@ u32 mac_dense_w_bm() { return kWTM * kWWarps; }
 int launch_mac_dense_w(const MacDenseArgsW& a, const BasisW& B, cudaStream_t s) {
   const u32 BM = kWTM * kWWarps;
   if (a.Mpad % BM != 0 || a.N % kWBN != 0) return -1;
-  dim3 grid(a.N / kWBN, (a.M + BM - 1) / BM, a.polys * a.level);
+  dim3 grid(a.N / kWBN, (a.M + BM - 1) / BM, a.polys * (a.limb_cnt ? a.limb_cnt : a.level));
   { ProfScope ps_("k_mac_dense_w", s);
   k_mac_dense_w<<<grid, kWWarps * 32, 0, s>>>(a, B);
   }
+  return 1;
+}
+
+__global__ void k_limbs_to_u32(const u64* __restrict__ in, u32* __restrict__ out, u64 rows, u32 Lw, u32 lo, u32 cnt,
+                               u32 N) {
+  const u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;  // one u64x2 -> u32x2
+  const u64 per_row = static_cast<u64>(cnt) * N / 2;
+  if (i >= rows * per_row) return;
+  const u64 r = i / per_row, j = (i % per_row) * 2;
+  const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(in + (r * Lw + lo) * N + j);
+  *reinterpret_cast<uint2*>(out + r * cnt * N + j) = make_uint2(static_cast<u32>(v.x), static_cast<u32>(v.y));
+}
+
+__global__ void k_limbs_to_u64(const u32* __restrict__ in, u64* __restrict__ out, u64 rows, u32 Lw, u32 lo, u32 cnt,
+                               u32 N) {
+  const u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const u64 per_row = static_cast<u64>(cnt) * N / 2;
+  if (i >= rows * per_row) return;
+  const u64 r = i / per_row, j = (i % per_row) * 2;
+  const uint2 v = *reinterpret_cast<const uint2*>(in + r * cnt * N + j);
+  *reinterpret_cast<ulonglong2*>(out + (r * Lw + lo) * N + j) = make_ulonglong2(v.x, v.y);
+}
+
+int launch_limbs_to_u32(const u64* in, u32* out, u64 rows, u32 Lw, u32 lo, u32 cnt, u32 N, cudaStream_t s) {
+  const u64 threads = rows * cnt * N / 2;
+  if (threads == 0) return 0;
+  ProfScope ps_("k_limbs_to_u32", s);
+  k_limbs_to_u32<<<(threads + 255) / 256, 256, 0, s>>>(in, out, rows, Lw, lo, cnt, N);
+  return 1;
+}
+
+int launch_limbs_to_u64(const u32* in, u64* out, u64 rows, u32 Lw, u32 lo, u32 cnt, u32 N, cudaStream_t s) {
+  const u64 threads = rows * cnt * N / 2;
+  if (threads == 0) return 0;
+  ProfScope ps_("k_limbs_to_u64", s);
+  k_limbs_to_u64<<<(threads + 255) / 256, 256, 0, s>>>(in, out, rows, Lw, lo, cnt, N);
   return 1;
 }
 

@@ -26,6 +26,7 @@ struct MacDenseArgsW {
   const u64* W;     // [level][K][Mpad]
   const u64* bias;  // [level][Mpad] or nullptr
   u32 K, M, Mpad, N, level, polys, x_level;
+  u32 limb_lo, limb_cnt;  // limbs computed: [limb_lo, limb_lo + limb_cnt); limb_cnt 0 = all
 };
 
 struct MacConvArgsW {
@@ -53,6 +54,10 @@ int launch_ntt_w(int logn, u64* data, u64 rows, u32 level, bool inverse, const B
 int launch_rescale_w(int logn, const RescaleArgsW& a, const BasisW& B, cudaStream_t s);
 u32 mac_dense_w_bm();  // Mpad must be a multiple of this
 int launch_mac_dense_w(const MacDenseArgsW& a, const BasisW& B, cudaStream_t s);
+// Limb range copies between u64 tensors [E][P][Lw][N] and u32 tensors [E][P][cnt][N]
+// (limbs [lo, lo + cnt) of the wide layout; residues < 2^32, so the low word is exact).
+int launch_limbs_to_u32(const u64* in, u32* out, u64 elems_polys, u32 Lw, u32 lo, u32 cnt, u32 N, cudaStream_t s);
+int launch_limbs_to_u64(const u32* in, u64* out, u64 elems_polys, u32 Lw, u32 lo, u32 cnt, u32 N, cudaStream_t s);
 int launch_mac_conv_w(const MacConvArgsW& a, const BasisW& B, cudaStream_t s);
 int launch_elementwise_w(const EwArgsW& a, const BasisW& B, cudaStream_t s);
 int launch_validate_w(const u64* w, u64 words, u32 level, u32 N, const BasisW& B, int* d_bad, cudaStream_t s);
