@@ -594,19 +594,23 @@ def c5b_run(args, ws, rank, local):
     H.prof_enable(False)
     prof = H.prof_report()
     mac, byts = c5b_work(p["n"], L)
-    mac_r, byts_r = mac * len(layer.rows) / C5B_M, byts  # this rank's share of the MACs
-    wide_peak = H.bench_int_peak(local, 1)
+    mac_r = mac * len(layer.rows) / C5B_M  # this rank's share of the modular MACs
     hbm_gbs, hbm_src = load_peaks()
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
+    i8_peak = 2 * float(peaks["bf16_tflops"]) * 1e12 / 2  # int8 dense MAC/s
     kern = {k: {"ms_per_step": v["ms"], "launches_per_step": v["launches"]} for k, v in prof.items()}
-    dk = max(kern, key=lambda k: kern[k]["ms_per_step"])
-    kms = kern[dk]["ms_per_step"]
-    # 40-bit limb 0: 128-bit MACs cost ~4 IMAD.WIDE; limbs 1..7 one IMAD.WIDE each
-    imadw = mac_r * (4 + (L - 1)) / L
-    roof = {"bound": "int32", "kernel": dk, "achieved": imadw / (kms * 1e-3) / 1e12, "peak": wide_peak / 1e12,
-            "unit": "T IMAD.WIDE/s (limb-0 128-bit MAC = 4)", "frac": imadw / (kms * 1e-3) / wide_peak,
-            "peak_source": "measured register-only IMAD.WIDE probe (hg_bench_int_peak kind 1)",
-            "hbm_gbs_achieved": byts_r / (kms * 1e-3) / 1e9, "hbm_peak": hbm_gbs, "traffic": None,
-            "algorithmic_per_step": {"mac": mac_r, "hbm_bytes": byts_r}}
+    # the contraction runs on the tensor cores: limbs 1..7 (30-bit) as 4 x 4 byte-plane
+    # products, the 40-bit limb 0 as 5 x 5 (k_mac_dense_tc + k_mac_dense_tc_w)
+    tc_names = [k for k in kern if k.startswith("k_mac_dense_tc")]
+    tc_ms = sum(kern[k]["ms_per_step"] for k in tc_names)
+    i8_macs = mac_r / L * ((L - 1) * 16 + 25)
+    roof = {"bound": "tensor", "kernel": "+".join(tc_names), "achieved": i8_macs / (tc_ms * 1e-3) / 1e12,
+            "peak": i8_peak / 1e12, "unit": "T int8 MAC/s", "frac": i8_macs / (tc_ms * 1e-3) / i8_peak,
+            "peak_source": "int8 dense = 2 x measured bf16 (MEASURED_PEAKS.json)",
+            "modular_mac_t_per_s": mac_r / (tc_ms * 1e-3) / 1e12,
+            "hbm_gbs_achieved": byts / (tc_ms * 1e-3) / 1e9, "hbm_peak": hbm_gbs, "traffic": None,
+            "algorithmic_per_step": {"modular_mac": mac_r, "int8_mac": i8_macs, "hbm_bytes": byts}}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:

@@ -991,7 +991,41 @@ class Executor {
         a.x_level = x.level;
         a.limb_lo = 0;
         a.limb_cnt = tc_lo;
-        r = launch_mac_dense_w(a, ctx.basisw, s_);
+        // the 40-bit limb itself on the tensor cores (5 byte planes, k_mac_dense_tc_w) when
+        // the rest of the layer is there too and K keeps its diagonal sums < 2^31
+        static const bool wide_tc = [] {
+          const char* e = getenv("HG_WIDE_TC");
+          return !(e != nullptr && e[0] == '0');
+        }();
+        const bool limb0_tc = wide_tc && tc_lo == 1 && ctx.chain[0] < (1ull << 40) && K <= 6605;
+        if (limb0_tc) {
+          BufPtr wp0 = ctx.alloc(tc_packed_weight_bytes_w(K, Mo), s_);
+          check_launch(launch_pack_weights_tc_w(static_cast<const u64*>(wres->ptr), static_cast<uint8_t*>(wp0->ptr), K,
+                                                Mo, Mpad, s_),
+                       "pack weights (wide)");
+          MacDenseTcWArgs t{};
+          t.X = x.data64();
+          t.Y = v.cipher.data64();
+          t.Wp = static_cast<const uint8_t*>(wp0->ptr);
+          t.bias = bias_res ? static_cast<const u64*>(bias_res->ptr) : nullptr;  // limb 0 row
+          t.K = K;
+          t.M = Mo;
+          t.Mpad = Mpad;
+          t.N = N;
+          t.level = L;
+          t.polys = 2;
+          t.x_level = x.level;
+          t.limb = 0;
+          const u64 q0 = ctx.chain[0];
+          u64 c = 1;
+          for (int i = 0; i < 9; ++i) {
+            t.cs[i] = c;
+            c = static_cast<u64>((static_cast<nt::u128>(c) << 8) % q0);
+          }
+          r = launch_mac_dense_tc_w(t, &ctx.basisw.p[0], s_);
+        } else {
+          r = launch_mac_dense_w(a, ctx.basisw, s_);
+        }
         if (r >= 0 && tc_lo < L) {
           check_launch(r, "mac_dense_w");
           const u32 cnt = L - tc_lo;

@@ -12,15 +12,17 @@
 // and reduces once -- the same canonical residue the IMAD kernel and the
 // reference produce.
 //
-// CTA tile: M = 128 outputs (one UMMA M) x N = 32 coefficients, K in steps of 32.
+// CTA tile: M = 128 outputs (one UMMA M) x N = 64 coefficients, K in steps of 32.
 // Operands are K-major, no swizzle (canonical 8-row x 16-byte core matrices:
 // LBO = 128 B between the two K halves, SBO = 256 B between 8-row groups).
 // Weights are pre-packed into that layout once per layer (k_pack_weights_tc);
-// X tiles arrive by cp.async (4-deep ring) and are split into byte planes in
-// shared memory by all threads; one elected thread issues the MMAs.
+// X tiles arrive by cp.async (6-deep ring) and are split into byte planes in
+// shared memory by 8 producer warps; one elected thread issues one MMA per weight
+// plane against all input planes stacked along N.
 #include <cuda_runtime.h>
 
 #include "hg_tc.hpp"
+#include "hg_wide.cuh"
 
 namespace hg {
 
@@ -285,6 +287,203 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
 }
 
 // ---------------------------------------------------------------------------
+// Wide limb: q in [2^30, 2^40), u64 residues, 5 byte planes.  Same pipeline with an
+// N = 32 tile: one MMA per weight plane against the 5 input planes stacked along N
+// (N = 160), D at TMEM column 32 pa, diagonals s = 0..8 in columns 32 s (288 of 512).
+// D_s sums at most 5 plane pairs: 5 K 255^2 < 2^31 for K <= 6605.  The epilogue folds
+// sum_s D_s (2^8s mod q) in 128 bits and reduces with the reference's Barrett128.
+// ---------------------------------------------------------------------------
+constexpr int kTwN = 32, kTwP = 5;
+constexpr int kTwPlaneB = kTwN * kTcK;  // 1024 B
+
+struct TcSmemW {
+  uint8_t a[kTcS][kTwP][kTcPlaneA];
+  uint8_t b[kTcS][kTwP][kTwPlaneB];
+  uint8_t zero_a[kTcPlaneA];
+  u64 xs[kTcXS][kTcK][kTwN];
+  unsigned long long full_a[kTcS], full_b[kTcS], empty[kTcS];
+  u32 tmem;
+};
+
+__global__ void k_pack_weights_tc_w(const u64* W, uint8_t* Wp, u32 K, u32 Mpad, u32 Mtiles, u32 Ksteps) {
+  const u64 total = static_cast<u64>(Mtiles) * Ksteps * kTcM * kTcK;
+  const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const u32 k = idx % kTcK;
+  const u32 r = (idx / kTcK) % kTcM;
+  const u64 t = idx / (kTcK * kTcM);
+  const u32 ks = t % Ksteps;
+  const u32 mt = t / Ksteps;
+  const u32 kk = ks * kTcK + k, m = mt * kTcM + r;
+  const u64 w = (kk < K && m < Mpad) ? W[static_cast<u64>(kk) * Mpad + m] : 0ull;
+  uint8_t* tile = Wp + ((static_cast<u64>(mt) * Ksteps + ks) * kTwP) * kTcPlaneA;
+#pragma unroll
+  for (int p = 0; p < kTwP; ++p) tile[p * kTcPlaneA + cm_off(r, k)] = static_cast<uint8_t>(w >> (8 * p));
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc_w(MacDenseTcWArgs a, DevPrimeW P) {
+  extern __shared__ __align__(1024) uint8_t tcw_raw[];
+  TcSmemW& S = *reinterpret_cast<TcSmemW*>(tcw_raw);
+  const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const u32 n0 = blockIdx.x * kTwN;
+  const u32 mt = blockIdx.y;
+  const u32 poly = blockIdx.z;
+  const u32 KS = a.Ksteps;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_addr(&S.tmem)),
+                 "r"(kTcCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kTcS; ++i) {
+      mbar_init(&S.full_a[i], 1);
+      mbar_init(&S.full_b[i], kTcProducers / 32);
+      mbar_init(&S.empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  for (u32 i = tid; i < kTcPlaneA / 16; i += kTcThreads) reinterpret_cast<uint4*>(S.zero_a)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::);
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const u32 tmem = S.tmem;
+
+  if (warp == kTcProducers / 32) {
+    if (lane == 0) {
+      const uint8_t* Wt = a.Wp + (static_cast<u64>(mt) * KS) * kTwP * kTcPlaneA;
+      constexpr u32 bytes = kTwP * kTcPlaneA;
+      auto load_a = [&](u32 j) {
+        const u32 st = j % kTcS;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(&S.full_a[st])),
+                     "r"(bytes));
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                smem_addr(&S.a[st][0][0])),
+            "l"(Wt + static_cast<u64>(j) * kTwP * kTcPlaneA), "r"(bytes), "r"(smem_addr(&S.full_a[st])));
+      };
+      for (u32 j = 0; j < kTcS - 1 && j < KS; ++j) load_a(j);
+      constexpr u32 idesc = (2u << 4) | (((kTwP * kTwN) >> 3) << 17) | ((kTcM >> 4) << 24);
+      const u64 zd = umma_desc(smem_addr(&S.zero_a[0]));
+      for (u32 ks = 0; ks < KS; ++ks) {
+        const u32 st = ks % kTcS, use = ks / kTcS;
+        const u32 j = ks + kTcS - 1;
+        if (j < KS) {
+          if (j >= kTcS) mbar_wait(&S.empty[j % kTcS], ((j / kTcS) - 1) & 1);
+          load_a(j);
+        }
+        mbar_wait(&S.full_a[st], use & 1);
+        mbar_wait(&S.full_b[st], use & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        const u64 bd = umma_desc(smem_addr(&S.b[st][0][0]));
+        if (ks == 0)
+          asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 0;\n" ::"r"(tmem + kTwP * kTwN), "l"(zd),
+                       "l"(bd), "r"(idesc));
+#pragma unroll
+        for (u32 pa = 0; pa < kTwP; ++pa) {
+          const u64 ad = umma_desc(smem_addr(&S.a[st][pa][0]));
+          const u32 accum = (ks > 0 || pa > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + pa * kTwN),
+              "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            smem_addr(&S.empty[st])));
+      }
+    }
+  } else {
+    // producers: warp w owns k rows [4w, 4w+4) of every step; lane = column
+    const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
+    const u64* Xb = a.X + (static_cast<u64>(poly) * a.x_level + a.limb) * a.N + n0;
+    const u32 r0 = warp * 4;
+    auto issue = [&](u32 ks) {
+      // 4 rows x 32 residues (u64) = 64 chunks of 16 B, two per lane; rows >= K zero-fill
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const u32 c = lane + i * 32, row = r0 + (c >> 4), c2 = (c & 15) * 2;
+        const u32 k = ks * kTcK + row;
+        const u64* src = Xb + static_cast<u64>(k < a.K ? k : 0) * xstride + c2;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(&S.xs[ks % kTcXS][row][c2])),
+                     "l"(src), "r"(k < a.K ? 16 : 0));
+      }
+    };
+#pragma unroll 1
+    for (u32 j = 0; j < kTcXS - 1; ++j) {
+      if (j < KS) issue(j);
+      asm volatile("cp.async.commit_group;\n" ::);
+    }
+    for (u32 ks = 0; ks < KS; ++ks) {
+      const u32 st = ks % kTcS, use = ks / kTcS;
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kTcXS - 2));
+      __syncwarp();
+      u64 v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = S.xs[ks % kTcXS][r0 + i][lane];
+      __syncwarp();
+      if (ks + kTcXS - 1 < KS) issue(ks + kTcXS - 1);
+      asm volatile("cp.async.commit_group;\n" ::);
+      if (ks >= kTcS) mbar_wait(&S.empty[st], (use - 1) & 1);
+#pragma unroll
+      for (u32 p = 0; p < kTwP; ++p) {
+        const u32 sh = 8 * p;
+        const u32 b4 = static_cast<u32>((v[0] >> sh) & 255) | (static_cast<u32>((v[1] >> sh) & 255) << 8) |
+                       (static_cast<u32>((v[2] >> sh) & 255) << 16) | (static_cast<u32>((v[3] >> sh) & 255) << 24);
+        *reinterpret_cast<u32*>(&S.b[st][p][cm_off(lane, r0)]) = b4;
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.full_b[st]);
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+
+    // epilogue: warp w reads TMEM lanes 32 (w % 4) .., columns 16 (w / 4) .. + 16
+    mbar_wait(&S.empty[(KS - 1) % kTcS], ((KS - 1) / kTcS) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    const u32 lg = warp & 3, ch = warp >> 2;
+    const u32 m = mt * kTcM + lg * 32 + lane;
+    const u64 bv = (a.bias != nullptr && poly == 0 && m < a.M) ? __ldg(&a.bias[m]) : 0ull;
+#pragma unroll
+    for (u32 cc = 0; cc < 16; cc += 8) {
+      const u32 col = ch * 16 + cc;
+      u64 lo[8], hi[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) lo[i] = hi[i] = 0;
+#pragma unroll 1
+      for (u32 s = 0; s < 2 * kTwP - 1; ++s) {
+        u32 r[8];
+        const u32 taddr = tmem + ((lg * 32) << 16) + s * kTwN + col;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                     : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+        const u64 c = a.cs[s];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const u64 pl = static_cast<u64>(r[i]) * c, ph = __umul64hi(static_cast<u64>(r[i]), c);
+          lo[i] += pl;
+          hi[i] += ph + (lo[i] < pl ? 1 : 0);
+        }
+      }
+      if (m < a.M) {
+        u64 o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = addmod_w(barrett128(lo[i], hi[i], P), bv, P.q);
+        u64* yp = a.Y + ((static_cast<u64>(m) * a.polys + poly) * a.level + a.limb) * a.N + n0 + col;
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) *reinterpret_cast<ulonglong2*>(yp + i) = make_ulonglong2(o[i], o[i + 1]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTcCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------
 u64 tc_packed_weight_bytes(u32 K, u32 M, u32 level) {
@@ -297,6 +496,35 @@ int launch_pack_weights_tc(const u32* W, uint8_t* Wp, u32 K, u32 M, u32 Mpad, u3
   const u64 total = static_cast<u64>(level) * Mtiles * Ksteps * kTcM * kTcK;
   ProfScope ps("k_pack_weights_tc", s);
   k_pack_weights_tc<<<(total + 255) / 256, 256, 0, s>>>(W, Wp, K, Mpad, Mtiles, Ksteps, level);
+  return 1;
+}
+
+u64 tc_packed_weight_bytes_w(u32 K, u32 M) {
+  const u32 Mtiles = (M + kTcM - 1) / kTcM, Ksteps = (K + kTcK - 1) / kTcK;
+  return static_cast<u64>(Mtiles) * Ksteps * kTwP * kTcPlaneA;
+}
+
+int launch_pack_weights_tc_w(const u64* W, uint8_t* Wp, u32 K, u32 M, u32 Mpad, cudaStream_t s) {
+  const u32 Mtiles = (M + kTcM - 1) / kTcM, Ksteps = (K + kTcK - 1) / kTcK;
+  const u64 total = static_cast<u64>(Mtiles) * Ksteps * kTcM * kTcK;
+  ProfScope ps("k_pack_weights_tc_w", s);
+  k_pack_weights_tc_w<<<(total + 255) / 256, 256, 0, s>>>(W, Wp, K, Mpad, Mtiles, Ksteps);
+  return 1;
+}
+
+int launch_mac_dense_tc_w(MacDenseTcWArgs a, const void* P, cudaStream_t s) {
+  a.Mtiles = (a.M + kTcM - 1) / kTcM;
+  a.Ksteps = (a.K + kTcK - 1) / kTcK;
+  if (a.N % kTwN != 0 || a.K > 6605 || a.K == 0) return -1;  // 5 K 255^2 < 2^31
+  constexpr size_t smem = sizeof(TcSmemW) > 120 * 1024 ? sizeof(TcSmemW) : 120 * 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mac_dense_tc_w, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = true;
+  }
+  dim3 grid(a.N / kTwN, a.Mtiles, a.polys);
+  ProfScope ps("k_mac_dense_tc_w", s);
+  k_mac_dense_tc_w<<<grid, kTcThreads, smem, s>>>(a, *static_cast<const DevPrimeW*>(P));
   return 1;
 }
 

@@ -19,7 +19,23 @@ struct MacDenseTcArgs {
   u32 planes[kMaxPrimes];  // byte planes per limb: 3 if q < 2^24 else 4
 };
 
+// One limb with a prime in [2^30, 2^40) (BASELINE c4/c5b limb 0), u64 residues: 5 byte
+// planes, N tile 32 so the 9 diagonal accumulators fit in tensor memory.
+struct MacDenseTcWArgs {
+  const u64* X;          // [K][x_polys][x_level][N]
+  u64* Y;                // [M][polys][level][N]
+  const uint8_t* Wp;     // launch_pack_weights_tc_w
+  const u64* bias;       // [Mpad] of this limb or nullptr
+  u32 K, M, Mpad, N, level, polys, x_level, limb;
+  u32 Mtiles, Ksteps;    // filled by the launcher
+  u64 cs[9];             // 2^(8s) mod q
+};
+
 u64 tc_packed_weight_bytes(u32 K, u32 M, u32 level);
+u64 tc_packed_weight_bytes_w(u32 K, u32 M);
+int launch_pack_weights_tc_w(const u64* W, uint8_t* Wp, u32 K, u32 M, u32 Mpad, cudaStream_t s);
+// P: the limb's wide constants (hg_wide.cuh DevPrimeW, passed opaquely)
+int launch_mac_dense_tc_w(MacDenseTcWArgs a, const void* P, cudaStream_t s);
 int launch_pack_weights_tc(const u32* W, uint8_t* Wp, u32 K, u32 M, u32 Mpad, u32 level, cudaStream_t s);
 int launch_mac_dense_tc(MacDenseTcArgs a, const Basis& B, cudaStream_t s);
 
