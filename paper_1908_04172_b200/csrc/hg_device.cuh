@@ -120,6 +120,14 @@ __device__ __forceinline__ u32 reduce64(u64 x, const DevPrime& P) {
 // qhat = floor(x' * floor(2^(k+31)/q) / 2^32) in [floor(ab/q) - 2, floor(ab/q)], so the low
 // word of ab - qhat*q is the remainder plus at most 2q (< 2^32 for q < 2^30).  One IMAD.HI
 // instead of the 64x64 high product of reduce64.
+// Lazy variant: congruent to a * b, in [0, 2q).
+__device__ __forceinline__ u32 mulmod_lazy2(u32 a, u32 b, const DevPrime& P) {
+  const u64 x = static_cast<u64>(a) * b;
+  const u32 xs = static_cast<u32>(x >> P.bsh);
+  const u32 r = static_cast<u32>(x) - __umulhi(xs, P.bmu) * P.q;
+  return min(r, r - P.two_q);
+}
+
 __device__ __forceinline__ u32 mulmod(u32 a, u32 b, const DevPrime& P) {
   const u64 x = static_cast<u64>(a) * b;
   const u32 xs = static_cast<u32>(x >> P.bsh);

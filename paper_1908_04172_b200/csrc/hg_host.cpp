@@ -466,7 +466,7 @@ static CtBatch do_relin(const Context& ctx, const RelinKeyDev& rk, const CtBatch
   r.D = static_cast<u32*>(D->ptr);
   r.ACC = static_cast<u32*>(ACC->ptr);
   r.CORR = static_cast<i32*>(CORR->ptr);
-  r.key = static_cast<const uint2*>(rk.key->ptr);
+  r.key = rk.key->ptr;
   r.out = out.data();
   r.rescale = rescale ? 1 : 0;
   for (u32 i = 0; i < L; ++i) {
@@ -1612,7 +1612,9 @@ int hg_relin_key_upload(hg_ctx* ctx, const uint64_t* words, uint64_t n_words, hg
     if (c.wide) throw Error(HG_ERR_UNSUPPORTED, "relinearization keys with primes >= 2^30 are not implemented yet");
     const u64 L = c.chain_len(), n = c.n;
     require(n_words == L * 2 * (L + 1) * n, "malformed relinearization key");
-    std::vector<uint2> k(n_words);
+    // device layout (hg::kKeyShoup): (value, shoup) pairs, or values only
+    const size_t esz = kKeyShoup ? sizeof(uint2) : sizeof(u32);
+    std::vector<unsigned char> k(n_words * esz);
     for (u64 j = 0; j < L; ++j)
       for (u64 p = 0; p < 2; ++p)
         for (u64 t = 0; t <= L; ++t) {
@@ -1621,15 +1623,17 @@ int hg_relin_key_upload(hg_ctx* ctx, const uint64_t* words, uint64_t n_words, hg
           for (u64 i = 0; i < n; ++i) {
             const u64 w = words[base + i];
             require(w < q, "residue out of range");
-            k[base + i] = make_uint2(static_cast<u32>(w), nt::shoup(w, q));
+            if (kKeyShoup)
+              reinterpret_cast<uint2*>(k.data())[base + i] = make_uint2(static_cast<u32>(w), nt::shoup(w, q));
+            else
+              reinterpret_cast<u32*>(k.data())[base + i] = static_cast<u32>(w);
           }
         }
     auto* rk = new hg_relin_key;
     rk->ctx = ctx->c;
     rk->k.chain_len = static_cast<u32>(L);
-    rk->k.key = c.alloc(k.size() * sizeof(uint2), nullptr);
-    cuda_check(cudaMemcpyAsync(rk->k.key->ptr, k.data(), k.size() * sizeof(uint2), cudaMemcpyHostToDevice, c.core->stream),
-               "h2d");
+    rk->k.key = c.alloc(k.size(), nullptr);
+    cuda_check(cudaMemcpyAsync(rk->k.key->ptr, k.data(), k.size(), cudaMemcpyHostToDevice, c.core->stream), "h2d");
     cuda_check(cudaStreamSynchronize(c.core->stream), "relin key upload");
     *out = rk;
   });

@@ -522,34 +522,70 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_KEYSW_MINB :
 
   // acc{0,1} += y * key[j][{0,1}][t]
   auto mac = [&](const u32 (&y)[32], u32 j) {
-    const uint2* k0 = a.key + ((static_cast<u64>(j) * 2 + 0) * (a.chain_len + 1) + bidx) * N;
-    const uint2* k1 = a.key + ((static_cast<u64>(j) * 2 + 1) * (a.chain_len + 1) + bidx) * N;
-    auto madd = [&](u32 acc, u32 x, u32 w, u32 wsh) { return csub(acc + mul_shoup_lazy(x, w, wsh, q), q2); };
+    const u64 r0 = ((static_cast<u64>(j) * 2 + 0) * (a.chain_len + 1) + bidx) * N;
+    const u64 r1 = ((static_cast<u64>(j) * 2 + 1) * (a.chain_len + 1) + bidx) * N;
     TmemScratch<T>::wait_st();  // the previous digit's stores of these cells
-    // key rows are L2-resident but far: issue a round of 4 pair-loads before using any
+    if constexpr (kKeyShoup) {
+      const uint2* k0 = static_cast<const uint2*>(a.key) + r0;
+      const uint2* k1 = static_cast<const uint2*>(a.key) + r1;
+      auto madd = [&](u32 acc, u32 x, u32 w, u32 wsh) { return csub(acc + mul_shoup_lazy(x, w, wsh, q), q2); };
+      // key rows are L2-resident but far: issue a round of 4 pair-loads before using any
 #pragma unroll
-    for (int qr = 0; qr < 4; ++qr) {
-      uint4 kv0[4], kv1[4];
+      for (int qr = 0; qr < 4; ++qr) {
+        uint4 kv0[4], kv1[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const u32 jj = NT::jC(tid, qr * 8 + 2 * i);
-        kv0[i] = __ldg(reinterpret_cast<const uint4*>(k0 + jj));
-        kv1[i] = __ldg(reinterpret_cast<const uint4*>(k1 + jj));
+        for (int i = 0; i < 4; ++i) {
+          const u32 jj = NT::jC(tid, qr * 8 + 2 * i);
+          kv0[i] = __ldg(reinterpret_cast<const uint4*>(k0 + jj));
+          kv1[i] = __ldg(reinterpret_cast<const uint4*>(k1 + jj));
+        }
+        u32 A0[8], A1[8];
+        tm.ld8(qr * 8, A0);
+        tm.ld8(32 + qr * 8, A1);
+        TmemScratch<T>::wait_ld();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int k = qr * 8 + 2 * i;
+          A0[2 * i] = madd(A0[2 * i], y[k], kv0[i].x, kv0[i].y);
+          A0[2 * i + 1] = madd(A0[2 * i + 1], y[k + 1], kv0[i].z, kv0[i].w);
+          A1[2 * i] = madd(A1[2 * i], y[k], kv1[i].x, kv1[i].y);
+          A1[2 * i + 1] = madd(A1[2 * i + 1], y[k + 1], kv1[i].z, kv1[i].w);
+        }
+        tm.st8(qr * 8, A0);
+        tm.st8(32 + qr * 8, A1);
       }
-      u32 A0[8], A1[8];
-      tm.ld8(qr * 8, A0);
-      tm.ld8(32 + qr * 8, A1);
-      TmemScratch<T>::wait_ld();
+    } else {
+      const u32* k0 = static_cast<const u32*>(a.key) + r0;
+      const u32* k1 = static_cast<const u32*>(a.key) + r1;
+      auto madd = [&](u32 acc, u32 x, u32 w) { return csub(acc + mulmod_lazy2(x, w, P), q2); };
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int k = qr * 8 + 2 * i;
-        A0[2 * i] = madd(A0[2 * i], y[k], kv0[i].x, kv0[i].y);
-        A0[2 * i + 1] = madd(A0[2 * i + 1], y[k + 1], kv0[i].z, kv0[i].w);
-        A1[2 * i] = madd(A1[2 * i], y[k], kv1[i].x, kv1[i].y);
-        A1[2 * i + 1] = madd(A1[2 * i + 1], y[k + 1], kv1[i].z, kv1[i].w);
+      for (int qr = 0; qr < 4; ++qr) {
+        uint4 kv0[2], kv1[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const u32 jj = NT::jC(tid, qr * 8 + 4 * h);
+          kv0[h] = __ldg(reinterpret_cast<const uint4*>(k0 + jj));
+          kv1[h] = __ldg(reinterpret_cast<const uint4*>(k1 + jj));
+        }
+        u32 A0[8], A1[8];
+        tm.ld8(qr * 8, A0);
+        tm.ld8(32 + qr * 8, A1);
+        TmemScratch<T>::wait_ld();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = qr * 8 + 4 * h;
+          A0[4 * h] = madd(A0[4 * h], y[k], kv0[h].x);
+          A0[4 * h + 1] = madd(A0[4 * h + 1], y[k + 1], kv0[h].y);
+          A0[4 * h + 2] = madd(A0[4 * h + 2], y[k + 2], kv0[h].z);
+          A0[4 * h + 3] = madd(A0[4 * h + 3], y[k + 3], kv0[h].w);
+          A1[4 * h] = madd(A1[4 * h], y[k], kv1[h].x);
+          A1[4 * h + 1] = madd(A1[4 * h + 1], y[k + 1], kv1[h].y);
+          A1[4 * h + 2] = madd(A1[4 * h + 2], y[k + 2], kv1[h].z);
+          A1[4 * h + 3] = madd(A1[4 * h + 3], y[k + 3], kv1[h].w);
+        }
+        tm.st8(qr * 8, A0);
+        tm.st8(32 + qr * 8, A1);
       }
-      tm.st8(qr * 8, A0);
-      tm.st8(32 + qr * 8, A1);
     }
   };
   {

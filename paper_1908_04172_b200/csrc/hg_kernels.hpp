@@ -49,6 +49,13 @@ struct MacConvArgs {
   const uint2* taps;     // (input element, window tap (c*win + ky)*win + kx), ascending per position
 };
 
+#ifndef HG_KEY_SHOUP
+#define HG_KEY_SHOUP 0
+#endif
+// Relinearisation key layout: (value, Shoup companion) pairs, or values only (half the
+// key-switch L1 traffic; the products then use the one-IMAD.HI product Barrett).
+constexpr bool kKeyShoup = HG_KEY_SHOUP != 0;
+
 struct RelinArgs {
   const u32* A;   // mode 0: size-3 ciphertexts; mode 1: left operand (size 2)
   const u32* Bm;  // mode 1: right operand (size 2); may equal A (square)
@@ -59,7 +66,7 @@ struct RelinArgs {
   u32* D;         // digits   [count][level][N]
   u32* ACC;       // key-switch accumulators [count][2][level][N]
   i32* CORR;      // special-prime corrections [count][2][N]
-  const uint2* key;  // [chain][2][chain+1][N] (value, shoup)
+  const void* key;   // [chain][2][chain+1][N]: uint2 (value, shoup) if kKeyShoup, else u32 value
   u32* out;       // [count][2][level or level-1][N]
   int rescale;
   u32 pinvP[kMaxPrimes], pinvP_sh[kMaxPrimes];  // P^-1 mod q_i

@@ -96,7 +96,7 @@ struct CtBatch {
 };
 
 struct RelinKeyDev {
-  BufPtr key;  // uint2 [chain][2][chain+1][N]
+  BufPtr key;  // [chain][2][chain+1][N]: u32 values, or (value, shoup) pairs (kKeyShoup)
   u32 chain_len = 0;
 };
 
