@@ -222,8 +222,12 @@ struct NttTwB<false> {
 };
 template <>
 struct NttTwB<true> {
-  const uint2* row;
-  __device__ __forceinline__ uint2 at(int n) const { return row[n]; }
+  const uint4* row4;  // 16-byte-aligned row in shared memory
+  mutable uint4 cur;  // the pair holding slots (2i, 2i+1); stages start at even slots
+  __device__ __forceinline__ uint2 at(int slot) const {
+    if ((slot & 1) == 0) cur = row4[slot >> 1];
+    return (slot & 1) ? make_uint2(cur.z, cur.w) : make_uint2(cur.x, cur.y);
+  }
 };
 
 // TWS: pass-B twiddles staged in shared memory (64 fewer registers per thread, 31 LDS.64
@@ -261,10 +265,11 @@ struct Ntt {
   // splits into base(tid) + const(k): every access is an immediate offset.
   static constexpr int XCHG_WORDS = N + (N >> 5);  // exchange buffer
   __device__ static __forceinline__ u32 swz(u32 j) { return j + (j >> 5); }
-  // Pass-B twiddles staged (TWS) after the exchange buffer, T >> CB rows padded to 33
-  // pairs so the 4 rows a warp touches fall in different banks.
+  // Pass-B twiddles staged (TWS) after the exchange buffer, T >> CB rows padded to 34
+  // pairs: 16-byte aligned for 128-bit pair loads, and the 4 rows a warp touches start
+  // 4 banks apart.
   static constexpr int TWB_ROWS = T >> CB;
-  static constexpr int TWB_STRIDE = 33;
+  static constexpr int TWB_STRIDE = 34;
   static constexpr int TWB_WORDS = TWS ? TWB_ROWS * TWB_STRIDE * 2 : 0;
   static constexpr int SMEM_WORDS = XCHG_WORDS + TWB_WORDS;
 
@@ -315,7 +320,7 @@ struct Ntt {
         const u32 e = tid + i * T;
         st[(e >> 5) * TWB_STRIDE + (e & 31)] = __ldg(base + e);
       }
-      tw.row = st + (tid >> CB) * TWB_STRIDE;
+      tw.row4 = reinterpret_cast<const uint4*>(st + (tid >> CB) * TWB_STRIDE);
     } else {
       (void)sm;
       const uint4* row = reinterpret_cast<const uint4*>(base + static_cast<size_t>(tid >> CB) * 32);
@@ -343,10 +348,12 @@ struct Ntt {
     constexpr int BLO = PassShape<L>::BLO;
     const u32 q = P.q, q2 = P.two_q;
     int n = 0;
+    int slot = 0;  // pass-B row slot: every stage starts at an even slot (128-bit pair loads)
 #pragma unroll
     for (int s = 0; s < NB; ++s) {
       const int rb = NB - 1 - s;  // register bit of this stage
       const int b = BLO + rb;     // j bit of this stage (t = 2^b)
+      slot = (slot + 1) & ~1;
 #if HG_NTT_SPLIT
       // all 16 products of the stage first (independent IMAD.HI chains), then the adds
       u32 Tm[16];
@@ -357,8 +364,9 @@ struct Ntt {
         for (int hi = 0; hi < (1 << (NB - 1 - rb)); ++hi) {
           const u32 kh = (static_cast<u32>(g) << NB) | (static_cast<u32>(hi) << (rb + 1));
           const uint2 w = (L == 0) ? P.twA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))]
-                                   : (L == 1 ? twB.at(n) : P.tvC[n]);
+                                   : (L == 1 ? twB.at(slot) : P.tvC[n]);
           ++n;
+          ++slot;
 #pragma unroll
           for (int lo = 0; lo < (1 << rb); ++lo) {
             u32 Y = x[(kh | lo) | (1 << rb)];
@@ -392,8 +400,9 @@ struct Ntt {
         for (int hi = 0; hi < (1 << (NB - 1 - rb)); ++hi) {
           const u32 kh = (static_cast<u32>(g) << NB) | (static_cast<u32>(hi) << (rb + 1));
           const uint2 w = (L == 0) ? P.twA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))]
-                                   : (L == 1 ? twB.at(n) : P.tvC[n]);
+                                   : (L == 1 ? twB.at(slot) : P.tvC[n]);
           ++n;
+          ++slot;
 #pragma unroll
           for (int lo = 0; lo < (1 << rb); ++lo) {
             const int k0 = kh | lo;
@@ -421,10 +430,12 @@ struct Ntt {
     constexpr int BLO = PassShape<L>::BLO;
     const u32 q = P.q, q2 = P.two_q;
     int n = 0;
+    int slot = 0;
 #pragma unroll
     for (int s = 0; s < NB; ++s) {
       const int rb = s;
       const int b = BLO + rb;
+      slot = (slot + 1) & ~1;
 #pragma unroll
       for (int g = 0; g < (1 << (5 - NB)); ++g) {
 #pragma unroll
@@ -441,8 +452,9 @@ struct Ntt {
             }
           } else {
             const uint2 w = (L == 0) ? P.itwA[(1u << (LOGN - 1 - b)) + (kh >> (rb + 1))]
-                                     : (L == 1 ? twB.at(n) : P.itvC[n]);
+                                     : (L == 1 ? twB.at(slot) : P.itvC[n]);
             ++n;
+            ++slot;
 #pragma unroll
             for (int lo = 0; lo < (1 << rb); ++lo) {
               const int k0 = kh | lo;

@@ -157,6 +157,7 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
       for (u32 st = 0; st < NB; ++st) {
         const u32 rb = inverse ? st : NB - 1 - st;
         const u32 bb = BLO + rb;
+        nslot = (nslot + 1) & ~1;  // stages start at even slots (Ntt::fwd_pass / inv_pass)
         for (u32 gg = 0; gg < (1u << (5 - NB)); ++gg)
           for (u32 hi = 0; hi < (1u << (NB - 1 - rb)); ++hi) {
             const u32 kh = (gg << NB) | (hi << (rb + 1));
