@@ -1,0 +1,70 @@
+# SPDX-License-Identifier: Apache-2.0
+"""The alternate kernel paths stay bit-exact: each environment switch (read once per
+process by the library) selects a different kernel for the same operation, so every case
+runs in its own subprocess and compares with the reference (oracle/_ref).
+
+  HG_DENSE_TC=0   Dot on the CUDA-core IMAD kernel instead of the int8 tensor cores
+  HG_WIDE_TC=0    the 40-bit limb of a wide Dot on the CUDA-core 128-bit MAC kernel
+  HG_CONV_FP64=0  convolution MACs all on IMAD.WIDE (no DFMA split)
+  HG_AUX_STREAM=0 special-prime key switch on the main stream
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle import refbind as R
+from paper_1908_04172_b200 import henet as H, workloads as W
+
+def run(p, wl, seed, keys_relin):
+    ctx = H.CkksContext(p["n"], p["chain"], p["special"], p["scale"])
+    ref = R.RefContext(p["n"], p["chain"], p["special"], p["scale"])
+    keys = ref.keygen(5, keys_relin)
+    if wl.name.startswith("c5b"):
+        x = W.random_ciphertexts(p, wl.input_count, seed=seed)
+        sc = p["scale"]
+    else:
+        imgs = W.synthetic_images(wl.input_shape, wl.batch, seed)
+        x, sc = ref.encrypt_tensor(keys, imgs, seed + 1, packing=wl.packing)
+    want, want_sc, st = ref.execute(keys if keys_relin else None, wl.manifest, wl.blob, x, sc,
+                                    patch=wl.patch_terminal_rescale)
+    rp = ref.plan(wl.manifest, wl.blob, patch=wl.patch_terminal_rescale)
+    nodes = {n["id"]: (n["decision"], n["level_in"], n["level_out"],
+                       np.array([n["scale_out_bits"]], dtype=np.uint64).view(np.float64)[0]) for n in rp["nodes"]}
+    plan = H.RescalePlan.from_nodes(0, rp["planned_rescale_ops"], nodes)
+    model = H.PlainModel.load(wl.manifest, wl.blob)
+    rk = None
+    if keys_relin:
+        rk = H.RelinKey(ctx, keys.rk_words())
+    out = H.execute(ctx, model, plan, H.CipherTensor.from_words(ctx, x, sc, shape=wl.input_shape), rk)
+    assert out.scale == want_sc, (out.scale, want_sc)
+    assert np.array_equal(out.to_words(), want)
+
+which = sys.argv[2]
+if which == "toy":
+    run(W.N8192, W.toy_cryptonets(), 3, True)
+else:
+    run(W.N16384, W.wide_dense(k=96, m=40), 4, False)
+print("OK")
+'''
+
+
+@pytest.mark.parametrize("env,which", [
+    ({"HG_DENSE_TC": "0"}, "toy"),
+    ({"HG_CONV_FP64": "0"}, "toy"),
+    ({"HG_AUX_STREAM": "0"}, "toy"),
+    ({"HG_WIDE_TC": "0"}, "wide"),
+    ({"HG_DENSE_TC": "0"}, "wide"),
+])
+def test_alternate_paths_bit_exact(env, which):
+    r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, which], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
