@@ -396,17 +396,53 @@ static CtBatch do_rescale(const Context& ctx, const CtBatch& in, u32 target, cud
     if (ctx.wide) {
       if (p >= (1ull << 32))
         throw Error(HG_ERR_UNSUPPORTED, "rescale by a prime >= 2^32 is not implemented on the B200 path");
+      // Limbs with primes < 2^30 (all but the 40-bit limb 0 of the BASELINE wide chain) are
+      // rescaled by the u32 kernel on a copy of their residues; the wide kernel then only
+      // handles limb 0 (it repeats the dropped limb's inverse transform for its correction).
+      bool hybrid = L >= 3 && p < (1ull << 30) && ctx.chain[0] >= (1ull << 30);
+      for (u32 i = 1; hybrid && i + 1 < L; ++i) hybrid = ctx.chain[i] < (1ull << 30);
+      static const bool wide_narrow = [] {
+        const char* e = getenv("HG_WIDE_NARROW_RESCALE");
+        return !(e != nullptr && e[0] == '0');
+      }();
+      hybrid = hybrid && wide_narrow;
       RescaleArgsW a{};
       a.in = cur.data64();
       a.out = out.data64();
       a.rows = cur.count * cur.polys;
       a.level = L;
+      a.limb_cnt = hybrid ? 1 : 0;
       for (u32 i = 0; i + 1 < L; ++i) {
         const u64 q = ctx.chain[i];
         a.pinv[i] = nt::inv(p % q, q);
         a.pinv_sh[i] = static_cast<u64>((static_cast<nt::u128>(a.pinv[i]) << 64) / q);
       }
       r = launch_rescale_w(static_cast<int>(ctx.logn), a, ctx.basisw, s);
+      if (hybrid && r >= 0) {
+        check_launch(r, "rescale (wide limb)");
+        const u32 cnt = L - 1;  // limbs 1 .. L-1 (the dropped one last)
+        const u64 rows = cur.count * cur.polys;
+        BufPtr xn = ctx.alloc(rows * cnt * ctx.n * 4, s), yn = ctx.alloc(rows * (cnt - 1) * ctx.n * 4, s);
+        check_launch(launch_limbs_to_u32(cur.data64(), static_cast<u32*>(xn->ptr), rows, L, 1, cnt, ctx.n, s),
+                     "narrow limbs");
+        RescaleArgs na{};
+        na.in = static_cast<const u32*>(xn->ptr);
+        na.out = static_cast<u32*>(yn->ptr);
+        na.rows = rows;
+        na.level = cnt;
+        na.lazy = 1;
+        Basis sub{};
+        for (u32 i = 0; i < cnt; ++i) sub.p[i] = ctx.basis.p[1 + i];
+        for (u32 i = 0; i + 1 < cnt; ++i) {
+          const u64 q = ctx.chain[1 + i];
+          na.pinv[i] = inv_mod_u32(p, q);
+          na.pinv_sh[i] = nt::shoup(na.pinv[i], q);
+          na.pm[i] = static_cast<u32>((p / 2 + q - 1) / q * q);
+          if (na.pm[i] + p / 2 >= 4 * q) na.lazy = 0;
+        }
+        check_launch(launch_rescale(static_cast<int>(ctx.logn), na, sub, s), "rescale (narrow limbs)");
+        r = launch_limbs_to_u64(static_cast<const u32*>(yn->ptr), out.data64(), rows, L - 1, 1, cnt - 1, ctx.n, s);
+      }
     } else {
       RescaleArgs a{};
       a.in = cur.data();

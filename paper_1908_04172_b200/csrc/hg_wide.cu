@@ -54,7 +54,8 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_rescale_w(RescaleArgsW a
 #pragma unroll
     for (int k = 0; k < 32; ++k) cs[k * T + tid] = static_cast<i32>(centered_round_rem_w(x[k], Pl));
   }
-  for (u32 i = 0; i + 1 < L; ++i) {
+  const u32 kept = a.limb_cnt ? a.limb_cnt : L - 1;
+  for (u32 i = 0; i < kept; ++i) {
     const DevPrimeW& Pi = B.p[i];
 #pragma unroll
     for (int k = 0; k < 32; ++k) x[k] = signed_residue_w(cs[k * T + tid], Pi);

@@ -17,6 +17,7 @@ struct RescaleArgsW {
   u64* out;
   u64 rows;
   u32 level;
+  u32 limb_cnt;  // kept limbs computed: [0, limb_cnt); 0 = all (level - 1)
   u64 pinv[kMaxPrimes], pinv_sh[kMaxPrimes];
 };
 
