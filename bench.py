@@ -470,6 +470,17 @@ def b200_run(args, ws, rank, local):
         roof = {"bound": "hbm", "kernel": dom, "achieved": dk["hbm_gbs"], "peak": hbm_gbs, "unit": "GB/s",
                 "frac": dk["hbm_gbs"] / hbm_gbs, "peak_source": hbm_src, "traffic": None}
     roof["algorithmic_per_step"] = {"modmul": mm, "mac": mac, "hbm_bytes": byts}
+    # measured DRAM traffic of the dominant kernel's first launch (act1 for the key switch),
+    # from the committed `ncu --set full` capture summarised in profiles/ncu_traffic.json
+    try:
+        nt = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        hits = {k: v for k, v in nt["kernels"].items() if k.split("<")[0].split("(")[0] == dom}
+        if hits:
+            roof["traffic"] = sum(v["dram_bytes_read"] + v["dram_bytes_write"] for v in hits.values())
+            roof["traffic_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum of one launch of " +
+                                    ", ".join(sorted(hits)) + "; " + nt["source"])
+    except (OSError, ValueError, KeyError):
+        pass
     whole_t = sum(max(k["int32_floor_ms"] if k["bound"] != "tensor" else k["tensor_floor_ms"], k["hbm_floor_ms"])
                   for k in kernels.values())
     roof["whole_step"] = {"floor_ms": whole_t, "measured_ms": ms_per_step,
