@@ -38,17 +38,26 @@ constexpr int kTcPlaneB = kTcN * kTcK;            // 2048 B per input byte plane
 #define HG_TC_XS 6
 #endif
 constexpr int kTcXS = HG_TC_XS;                          // cp.async stages of input residues (8 KB each)
-constexpr int kTcCols = 512;                      // TMEM columns: up to 7 accumulators x 64
+constexpr int kTcCols = 512;                      // TMEM columns of the wide kernel (9 x 32 used)
+#ifndef HG_TC_SMALLK
+#define HG_TC_SMALLK 2048
+#endif
+constexpr u32 kTcSmallK = HG_TC_SMALLK;           // K at or below which the N = 32 tile is used
 
+template <int TN>
 struct TcSmem {
   uint8_t a[kTcS][4][kTcPlaneA];  // weight planes (K-major core matrices), filled by cp.async.bulk
-  uint8_t b[kTcS][4][kTcPlaneB];  // input planes, written by the producer warps; the planes of a
-                                  // stage are consecutive, i.e. one K-major (planes*64) x 32 matrix
+  uint8_t b[kTcS][4][TN * kTcK];  // input planes, written by the producer warps; the planes of a
+                                  // stage are consecutive, i.e. one K-major (planes*TN) x 32 matrix
   uint8_t zero_a[kTcPlaneA];      // zero weight plane: initialises the upper accumulators
-  u32 xs[kTcXS][kTcK][kTcN];      // input residues staged by cp.async (producer ring)
+  u32 xs[kTcXS][kTcK][TN];        // input residues staged by cp.async (producer ring)
   unsigned long long full_a[kTcS], full_b[kTcS], empty[kTcS];
   u32 tmem;
 };
+// TMEM columns: 7 diagonal accumulators of TN columns (512 for TN = 64: one CTA per SM;
+// 256 for TN = 32: two CTAs per SM, one's epilogue overlapping the other's MMAs)
+template <int TN>
+constexpr u32 tc_cols() { return TN == 64 ? 512u : 256u; }
 
 __device__ __forceinline__ u32 smem_addr(const void* p) { return static_cast<u32>(__cvta_generic_to_shared(p)); }
 
@@ -102,11 +111,13 @@ __global__ void k_pack_weights_tc(const u32* W, uint8_t* Wp, u32 K, u32 Mpad, u3
 //   warp 8     lane 0: weight planes by cp.async.bulk into A[], MMA issue, commits
 // Rings: full_a (tx bytes), full_b (256 producer arrivals), empty (MMA commit).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a, Basis B) {
+template <int TN>
+__global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(MacDenseTcArgs a, Basis B) {
   extern __shared__ __align__(1024) uint8_t tc_raw[];
-  TcSmem& S = *reinterpret_cast<TcSmem*>(tc_raw);
+  TcSmem<TN>& S = *reinterpret_cast<TcSmem<TN>*>(tc_raw);
+  constexpr u32 kCols = tc_cols<TN>();
   const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const u32 n0 = blockIdx.x * kTcN;
+  const u32 n0 = blockIdx.x * TN;
   const u32 mt = blockIdx.y;
   const u32 poly = blockIdx.z / a.level, limb = blockIdx.z % a.level;
   const DevPrime& P = B.p[limb];
@@ -115,7 +126,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_addr(&S.tmem)),
-                 "r"(kTcCols));
+                 "r"(kCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
   }
   if (tid == 0) {
@@ -153,7 +164,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
       // stacked along N (planes * 64 rows), D at TMEM column pa * 64, so input plane pb lands
       // in columns (pa + pb) * 64: the diagonal accumulator D_s, s = pa + pb, with no
       // per-(pa, pb) MMA.  idesc: D s32, A/B u8, K-major, N = planes * 64, M = 128.
-      const u32 idesc = (2u << 4) | (((planes * kTcN) >> 3) << 17) | ((kTcM >> 4) << 24);
+      const u32 idesc = (2u << 4) | (((planes * TN) >> 3) << 17) | ((kTcM >> 4) << 24);
       const u64 zd = umma_desc(smem_addr(&S.zero_a[0]));
       for (u32 ks = 0; ks < KS; ++ks) {
         const u32 st = ks % kTcS, use = ks / kTcS;
@@ -168,7 +179,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
         const u64 bd = umma_desc(smem_addr(&S.b[st][0][0]));
         if (ks == 0) {
           // columns [planes * 64, 2 * planes * 64) (diagonals s >= planes) start at zero
-          asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 0;\n" ::"r"(tmem + planes * kTcN),
+          asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 0;\n" ::"r"(tmem + planes * TN),
                        "l"(zd), "l"(bd), "r"(idesc));
         }
         for (u32 pa = 0; pa < planes; ++pa) {
@@ -176,7 +187,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
           const u32 accum = (ks > 0 || pa > 0) ? 1u : 0u;  // pa = 0 of step 0 initialises s < planes
           asm volatile(
               "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + pa * kTcN),
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + pa * TN),
               "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -192,10 +203,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
     const u32* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n0;
     const u32 r0 = warp * 4;
     auto issue = [&](u32 ks) {
-      // 4 rows x 64 residues = 64 chunks of 16 B, two per lane; rows >= K zero-fill
+      // 4 rows x TN residues = TN chunks of 16 B, TN / 32 per lane; rows >= K zero-fill
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const u32 c = lane + i * 32, row = r0 + (c >> 4), c4 = (c & 15) * 4;
+      for (int i = 0; i < TN / 32; ++i) {
+        const u32 c = lane + i * 32, row = r0 + c / (TN / 4), c4 = (c % (TN / 4)) * 4;
         const u32 k = ks * kTcK + row;
         const u32* src = Xb + static_cast<u64>(k < a.K ? k : 0) * xstride + c4;
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(&S.xs[ks % kTcXS][row][c4])),
@@ -211,24 +222,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
       const u32 st = ks % kTcS, use = ks / kTcS;
       asm volatile("cp.async.wait_group %0;\n" ::"n"(kTcXS - 2));
       __syncwarp();
-      u32 v0[4], v1[4];
+      u32 v[TN / 32][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        v0[i] = S.xs[ks % kTcXS][r0 + i][lane];
-        v1[i] = S.xs[ks % kTcXS][r0 + i][lane + 32];
-      }
+      for (int h = 0; h < TN / 32; ++h)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[h][i] = S.xs[ks % kTcXS][r0 + i][lane + 32 * h];
       __syncwarp();  // step ks's rows are consumed before the ring slot is refilled
       if (ks + kTcXS - 1 < KS) issue(ks + kTcXS - 1);
       asm volatile("cp.async.commit_group;\n" ::);
       if (ks >= kTcS) mbar_wait(&S.empty[st], (use - 1) & 1);
       for (u32 p = 0; p < planes; ++p) {
         const u32 sh = 8 * p;
-        const u32 b0 = ((v0[0] >> sh) & 255) | (((v0[1] >> sh) & 255) << 8) | (((v0[2] >> sh) & 255) << 16) |
-                       (((v0[3] >> sh) & 255) << 24);
-        const u32 b1 = ((v1[0] >> sh) & 255) | (((v1[1] >> sh) & 255) << 8) | (((v1[2] >> sh) & 255) << 16) |
-                       (((v1[3] >> sh) & 255) << 24);
-        *reinterpret_cast<u32*>(&S.b[st][p][cm_off(lane, r0)]) = b0;
-        *reinterpret_cast<u32*>(&S.b[st][p][cm_off(lane + 32, r0)]) = b1;
+#pragma unroll
+        for (int h = 0; h < TN / 32; ++h) {
+          const u32 b4 = ((v[h][0] >> sh) & 255) | (((v[h][1] >> sh) & 255) << 8) | (((v[h][2] >> sh) & 255) << 16) |
+                         (((v[h][3] >> sh) & 255) << 24);
+          *reinterpret_cast<u32*>(&S.b[st][p][cm_off(lane + 32 * h, r0)]) = b4;
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::);
       __syncwarp();
@@ -242,26 +252,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
     const u32 lg = warp & 3, ch = warp >> 2;
     const u32 m = mt * kTcM + lg * 32 + lane;
     const u32 q = P.q;
-    u64 cs[7];
-    {
-      u64 c = 1;
-#pragma unroll
-      for (int s = 0; s < 7; ++s) {
-        cs[s] = c;
-        c = (c << 8) % q;
-      }
-    }
+    const u64* cs = a.cs[limb];  // 2^(8s) mod q (host)
     const u32 nacc = 2 * planes - 1;
     const u32 bv = (a.bias != nullptr && poly == 0 && m < a.M) ? __ldg(&a.bias[static_cast<u64>(limb) * a.Mpad + m]) : 0u;
 #pragma unroll
-    for (u32 cc = 0; cc < 32; cc += 8) {
-      const u32 col = ch * 32 + cc;
+    for (u32 cc = 0; cc < TN / 2; cc += 8) {
+      const u32 col = ch * (TN / 2) + cc;
       u64 acc[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] = 0;
       for (u32 s = 0; s < nacc; ++s) {
         u32 r[8];
-        const u32 taddr = tmem + ((lg * 32) << 16) + s * kTcN + col;
+        const u32 taddr = tmem + ((lg * 32) << 16) + s * TN + col;
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                      : "r"(taddr));
@@ -282,7 +284,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc(MacDenseTcArgs a
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
   __syncthreads();
   if (warp == 0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTcCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kCols));
   }
 }
 
@@ -528,21 +530,44 @@ int launch_mac_dense_tc_w(MacDenseTcWArgs a, const void* P, cudaStream_t s) {
   return 1;
 }
 
+template <int TN>
+static void tc_launch(const MacDenseTcArgs& a, const Basis& B, cudaStream_t s) {
+  // TN = 64: request enough shared memory that only one CTA is resident per SM (512 TMEM
+  // columns), so no CTA spins in tcgen05.alloc; TN = 32: two CTAs of 256 columns.
+  constexpr size_t smem = TN == 64 ? (sizeof(TcSmem<TN>) > 120 * 1024 ? sizeof(TcSmem<TN>) : 120 * 1024)
+                                   : sizeof(TcSmem<TN>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mac_dense_tc<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = true;
+  }
+  dim3 grid(a.N / TN, a.Mtiles, a.polys * a.level);
+  ProfScope ps("k_mac_dense_tc", s);
+  k_mac_dense_tc<TN><<<grid, kTcThreads, smem, s>>>(a, B);
+}
+
 int launch_mac_dense_tc(MacDenseTcArgs a, const Basis& B, cudaStream_t s) {
   a.Mtiles = (a.M + kTcM - 1) / kTcM;
   a.Ksteps = (a.K + kTcK - 1) / kTcK;
-  if (a.N % kTcN != 0 || a.K > 8192 || a.K == 0) return -1;
-  // 512 TMEM columns per CTA: request enough shared memory that only one CTA is
-  // resident per SM, so no CTA spins in tcgen05.alloc.
-  constexpr size_t smem = sizeof(TcSmem) > 120 * 1024 ? sizeof(TcSmem) : 120 * 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_mac_dense_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr = true;
+  if (a.N % 64 != 0 || a.K > 8192 || a.K == 0) return -1;
+  for (u32 l = 0; l < a.level; ++l) {
+    const u64 q = B.p[l].q;
+    u64 c = 1;
+    for (int i = 0; i < 7; ++i) {
+      a.cs[l][i] = c;
+      c = (c << 8) % q;
+    }
   }
-  dim3 grid(a.N / kTcN, a.Mtiles, a.polys * a.level);
-  ProfScope ps("k_mac_dense_tc", s);
-  k_mac_dense_tc<<<grid, kTcThreads, smem, s>>>(a, B);
+  // short contractions are dominated by per-CTA prologue/epilogue: two CTAs per SM overlap them
+  static const int tn_env = [] {
+    const char* e = getenv("HG_TC_N");
+    return e ? atoi(e) : 0;
+  }();
+  const int tn = tn_env ? tn_env : (a.K <= kTcSmallK ? 32 : 64);
+  if (tn == 32)
+    tc_launch<32>(a, B, s);
+  else
+    tc_launch<64>(a, B, s);
   return 1;
 }
 

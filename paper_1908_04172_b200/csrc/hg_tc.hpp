@@ -17,6 +17,7 @@ struct MacDenseTcArgs {
   u32 K, M, Mpad, N, level, polys, x_level;
   u32 Mtiles, Ksteps;    // filled by the launcher
   u32 planes[kMaxPrimes];  // byte planes per limb: 3 if q < 2^24 else 4
+  u64 cs[kMaxPrimes][7];   // 2^(8s) mod q per limb (filled by the launcher)
 };
 
 // One limb with a prime in [2^30, 2^40) (BASELINE c4/c5b limb 0), u64 residues: 5 byte
