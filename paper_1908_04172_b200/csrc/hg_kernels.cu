@@ -276,8 +276,8 @@ __device__ __forceinline__ double u32_to_f64(u32 x) {
 
 template <int FT, int kPre>
 __device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevPrime& P, const uint2* tp,
-                                                const u32* wsm, u32 ntaps, const u32* Xb, u64 xstride, u32 poly,
-                                                u32 limb, u32 f0, u32 pos, u32 n) {
+                                                const u32* wsm, const double* wsd, u32 ntaps, const u32* Xb,
+                                                u64 xstride, u32 poly, u32 limb, u32 f0, u32 pos, u32 n) {
   constexpr int KI = (2 * FT + 2) / 5;  // IMAD.WIDE : DFMA issue-cycle balance (4 vs 2 + conversions)
   constexpr int KF = FT - KI;
   u64 acc[KI > 0 ? KI : 1][4];
@@ -306,6 +306,7 @@ __device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevP
       if (t >= ntaps) break;
       const uint4 xv = ring[i];
       const u32* wt = wsm + wring[i] * FT;
+      const double* wd = wsd + wring[i] * FT;
       if (t + kPre < ntaps) {
         const uint2 e = __ldg(tp + t + kPre);
         wring[i] = e.y;
@@ -322,7 +323,7 @@ __device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevP
       const double x0 = u32_to_f64(xv.x), x1 = u32_to_f64(xv.y), x2 = u32_to_f64(xv.z), x3 = u32_to_f64(xv.w);
 #pragma unroll
       for (int f = 0; f < KF; ++f) {
-        const double w = u32_to_f64(wt[KI + f]);
+        const double w = wd[KI + f];
         dacc[f][0] = fma(w, x0, dacc[f][0]);
         dacc[f][1] = fma(w, x1, dacc[f][1]);
         dacc[f][2] = fma(w, x2, dacc[f][2]);
@@ -422,6 +423,7 @@ __device__ __forceinline__ void conv_taps_int(const MacConvArgs& a, const DevPri
 template <int FT>
 __global__ void __launch_bounds__(kConvThreads, 3) k_mac_conv(MacConvArgs a, Basis B) {
   __shared__ __align__(16) u32 wsm[kMaxTaps * FT];
+  __shared__ double wsd[32 * FT];  // the same weights as doubles for the DFMA filters (<= 32 taps)
   const u32 tid = threadIdx.x;
   const u32 npos = a.OH * a.OW;
   const u32 nchunks = (a.F + FT - 1) / FT;
@@ -434,7 +436,9 @@ __global__ void __launch_bounds__(kConvThreads, 3) k_mac_conv(MacConvArgs a, Bas
   const u32* Wl = a.W + static_cast<u64>(limb) * a.F * taps_all;
   for (u32 i = tid; i < taps_all * FT; i += blockDim.x) {
     const u32 t = i / FT, f = i % FT;
-    wsm[i] = (f0 + f < a.F) ? __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + t]) : 0u;
+    const u32 w = (f0 + f < a.F) ? __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + t]) : 0u;
+    wsm[i] = w;
+    if (i < 32 * FT) wsd[i] = static_cast<double>(w);
   }
   __syncthreads();
   const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(kConvThreads, 3) k_mac_conv(MacConvArgs a, Bas
     const u32 off0 = __ldg(&a.tap_off[pos]);
     const u32 ntaps = __ldg(&a.tap_off[pos + 1]) - off0;
     if (fp && ntaps <= 32)
-      conv_taps_mixed<FT, kPre>(a, P, a.taps + off0, wsm, ntaps, Xb, xstride, poly, limb, f0, pos, n);
+      conv_taps_mixed<FT, kPre>(a, P, a.taps + off0, wsm, wsd, ntaps, Xb, xstride, poly, limb, f0, pos, n);
     else
       conv_taps_int<FT, kPre>(a, P, a.taps + off0, wsm, ntaps, Xb, xstride, poly, limb, f0, pos, n);
   }
