@@ -312,13 +312,26 @@ struct Ntt {
   // Row of staged pass-B twiddles for this thread's group (rows of 32 pairs in global).
   // The shared-memory variant is ordered before pass B by the transform's first barrier,
   // and the previous transform finished reading it before its last barrier.
-  __device__ static __forceinline__ void load_rowB(TwB& tw, const uint2* base, u32* sm, u32 tid) {
+  // stage = false reuses the rows staged earlier for the same prime and direction (the key
+  // switch stages once with stage_rowsB and runs all its forward transforms under one prime).
+  __device__ static __forceinline__ void stage_rowsB(const uint2* base, u32* sm, u32 tid) {
+    static_assert(TWS, "staging needs the shared-memory twiddle variant");
+    uint2* st = reinterpret_cast<uint2*>(sm + XCHG_WORDS);
+#pragma unroll
+    for (int i = 0; i < TWB_ROWS * 32 / T; ++i) {
+      const u32 e = tid + i * T;
+      st[(e >> 5) * TWB_STRIDE + (e & 31)] = __ldg(base + e);
+    }
+  }
+  __device__ static __forceinline__ void load_rowB(TwB& tw, const uint2* base, u32* sm, u32 tid, bool stage = true) {
     if constexpr (TWS) {
       uint2* st = reinterpret_cast<uint2*>(sm + XCHG_WORDS);
+      if (stage) {
 #pragma unroll
-      for (int i = 0; i < TWB_ROWS * 32 / T; ++i) {
-        const u32 e = tid + i * T;
-        st[(e >> 5) * TWB_STRIDE + (e & 31)] = __ldg(base + e);
+        for (int i = 0; i < TWB_ROWS * 32 / T; ++i) {
+          const u32 e = tid + i * T;
+          st[(e >> 5) * TWB_STRIDE + (e & 31)] = __ldg(base + e);
+        }
       }
       tw.row4 = reinterpret_cast<const uint4*>(st + (tid >> CB) * TWB_STRIDE);
     } else {
@@ -475,10 +488,11 @@ struct Ntt {
   // Full forward transform.  In: layout A, values < 4q.  Out: layout C,
   // canonical.  `sm` must hold SMEM_WORDS u32; the call begins and ends with a
   // barrier-protected exchange so the buffer may be reused immediately.
-  __device__ static __forceinline__ void forward(u32 (&x)[32], u32* sm, u32 tid, const DevPrime& P) {
+  __device__ static __forceinline__ void forward(u32 (&x)[32], u32* sm, u32 tid, const DevPrime& P,
+                                                 bool stage_twiddles = true) {
     TwB twB;
     uint2 tb[4];
-    load_rowB(twB, P.fwdB, sm, tid);  // in flight during pass A
+    load_rowB(twB, P.fwdB, sm, tid, stage_twiddles);  // in flight during pass A
     load_bases(tb, P.fwdT, tid);
     fwd_pass<0>(x, P, twB, tb);
     __syncthreads();

@@ -604,6 +604,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_KEYSW_MINB :
   const u32 R = special ? L : L - 1;
   u32 nx[32];
   NT::gload_P(nx, a.D + (ct * L + (skip == 0 ? 1 : 0)) * N, tid);
+  NT::stage_rowsB(P.fwdB, sm, tid);  // ordered before pass B by the transform's first barrier
 #pragma unroll 1
   for (u32 r = 0; r < R; ++r) {
     const u32 j = r + (r >= skip ? 1 : 0);
@@ -619,7 +620,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_KEYSW_MINB :
 #pragma unroll
       for (int k = 0; k < 32; ++k) y[k] = reduce32(y[k], P);
     }
-    NT::forward(y, sm, tid, P);
+    NT::forward(y, sm, tid, P, false);  // one prime per CTA: pass-B twiddles staged once, above
     const u32 jn = min(r + 1 + (r + 1 >= skip ? 1 : 0), L - 1);
     NT::gload_P(nx, a.D + (ct * L + jn) * N, tid);
     mac(y, j);
