@@ -1205,7 +1205,13 @@ class Executor {
         // cached on the context: (input element, window tap), ascending per position
         {
           const u32 npos = a.OH * a.OW;
-          const std::vector<u32> key = {C, a.IH, a.IW, a.OH, a.OW, win, a.stride, a.pad_top, a.pad_left};
+          // entries carry the input's word offset (element * polys * x_level * N): no address
+          // multiply per tap in the kernel
+          const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
+          require(static_cast<u64>(C) * a.IH * a.IW * xstride < (1ull << 32),
+                  "convolution input too large for 32-bit tap offsets");
+          const std::vector<u32> key = {C, a.IH, a.IW, a.OH, a.OW, win, a.stride, a.pad_top, a.pad_left,
+                                        static_cast<u32>(xstride)};
           std::lock_guard<std::mutex> g(ctx.geo_mu);
           BufPtr& tb = ctx.geo_cache[key];
           const size_t toff = ((npos + 1) * 4 + 15) / 16 * 16;
@@ -1220,8 +1226,9 @@ class Executor {
                       const int iy = static_cast<int>(oy * a.stride + ky) - static_cast<int>(a.pad_top);
                       const int ix = static_cast<int>(ox * a.stride + kx) - static_cast<int>(a.pad_left);
                       if (iy < 0 || iy >= static_cast<int>(a.IH) || ix < 0 || ix >= static_cast<int>(a.IW)) continue;
-                      taps.push_back(make_uint2((c * a.IH + static_cast<u32>(iy)) * a.IW + static_cast<u32>(ix),
-                                                (c * win + ky) * win + kx));
+                      taps.push_back(make_uint2(
+                          static_cast<u32>(((c * a.IH + static_cast<u32>(iy)) * a.IW + static_cast<u32>(ix)) * xstride),
+                          (c * win + ky) * win + kx));
                     }
                 tab[oy * a.OW + ox + 1] = static_cast<u32>(taps.size());
               }

@@ -274,12 +274,20 @@ __device__ __forceinline__ double u32_to_f64(u32 x) {
   return __hiloint2double(0x43300000, static_cast<int>(x)) - 4503599627370496.0;
 }
 
+template <int FT>
+struct ConvSplit {
+  static constexpr int KI = (2 * FT + 2) / 5;  // IMAD.WIDE : DFMA issue-cycle balance (4 vs 2 + conversions)
+  static constexpr int KF = FT - KI;
+  static constexpr int KIP = (KI + 1) & ~1;    // per-tap weight rows padded for 64 / 128-bit loads
+  static constexpr int KFP = (KF + 1) & ~1;
+};
+
 template <int FT, int kPre>
 __device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevPrime& P, const uint2* tp,
-                                                const u32* wsm, const double* wsd, u32 ntaps, const u32* Xb,
-                                                u64 xstride, u32 poly, u32 limb, u32 f0, u32 pos, u32 n) {
-  constexpr int KI = (2 * FT + 2) / 5;  // IMAD.WIDE : DFMA issue-cycle balance (4 vs 2 + conversions)
-  constexpr int KF = FT - KI;
+                                                const u32* wmi, const double* wmd, u32 ntaps, const u32* Xb,
+                                                u32 poly, u32 limb, u32 f0, u32 pos, u32 n) {
+  constexpr int KI = ConvSplit<FT>::KI, KF = ConvSplit<FT>::KF;
+  constexpr int KIP = ConvSplit<FT>::KIP, KFP = ConvSplit<FT>::KFP;
   u64 acc[KI > 0 ? KI : 1][4];
   double dacc[KF][4];
 #pragma unroll
@@ -296,7 +304,7 @@ __device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevP
   for (int i = 0; i < kPre; ++i) {
     const uint2 e = static_cast<u32>(i) < ntaps ? __ldg(tp + i) : make_uint2(0, 0);
     wring[i] = e.y;
-    ring[i] = (static_cast<u32>(i) < ntaps) ? __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(e.x) * xstride))
+    ring[i] = (static_cast<u32>(i) < ntaps) ? __ldg(reinterpret_cast<const uint4*>(Xb + e.x))
                                             : make_uint4(0, 0, 0, 0);
   }
   for (u32 t0 = 0; t0 < ntaps; t0 += kPre) {
@@ -305,16 +313,28 @@ __device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevP
       const u32 t = t0 + i;
       if (t >= ntaps) break;
       const uint4 xv = ring[i];
-      const u32* wt = wsm + wring[i] * FT;
-      const double* wd = wsd + wring[i] * FT;
+      u32 wi[KIP > 0 ? KIP : 2];
+      double wf[KFP];
+#pragma unroll
+      for (int c = 0; c < KIP; c += 2) {
+        const uint2 v = *reinterpret_cast<const uint2*>(wmi + wring[i] * KIP + c);
+        wi[c] = v.x;
+        wi[c + 1] = v.y;
+      }
+#pragma unroll
+      for (int c = 0; c < KFP; c += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(wmd + wring[i] * KFP + c);
+        wf[c] = v.x;
+        wf[c + 1] = v.y;
+      }
       if (t + kPre < ntaps) {
         const uint2 e = __ldg(tp + t + kPre);
         wring[i] = e.y;
-        ring[i] = __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(e.x) * xstride));
+        ring[i] = __ldg(reinterpret_cast<const uint4*>(Xb + e.x));
       }
 #pragma unroll
       for (int f = 0; f < KI; ++f) {
-        const u64 w = wt[f];
+        const u64 w = wi[f];
         acc[f][0] += w * xv.x;
         acc[f][1] += w * xv.y;
         acc[f][2] += w * xv.z;
@@ -323,7 +343,7 @@ __device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevP
       const double x0 = u32_to_f64(xv.x), x1 = u32_to_f64(xv.y), x2 = u32_to_f64(xv.z), x3 = u32_to_f64(xv.w);
 #pragma unroll
       for (int f = 0; f < KF; ++f) {
-        const double w = wd[KI + f];
+        const double w = wf[f];
         dacc[f][0] = fma(w, x0, dacc[f][0]);
         dacc[f][1] = fma(w, x1, dacc[f][1]);
         dacc[f][2] = fma(w, x2, dacc[f][2]);
@@ -354,8 +374,8 @@ __device__ __forceinline__ void conv_taps_mixed(const MacConvArgs& a, const DevP
 
 template <int FT, int kPre>
 __device__ __forceinline__ void conv_taps_int(const MacConvArgs& a, const DevPrime& P, const uint2* tp,
-                                              const u32* wsm, u32 ntaps, const u32* Xb, u64 xstride, u32 poly,
-                                              u32 limb, u32 f0, u32 pos, u32 n) {
+                                              const u32* wsm, u32 ntaps, const u32* Xb, u32 poly, u32 limb, u32 f0,
+                                              u32 pos, u32 n) {
   const bool fold = a.fold[limb] != 0;
   const u64 r32 = P.r32;
   const u32 q = P.q;
@@ -370,7 +390,7 @@ __device__ __forceinline__ void conv_taps_int(const MacConvArgs& a, const DevPri
   for (int i = 0; i < kPre; ++i) {
     const uint2 e = static_cast<u32>(i) < ntaps ? __ldg(tp + i) : make_uint2(0, 0);
     wring[i] = e.y;
-    ring[i] = (static_cast<u32>(i) < ntaps) ? __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(e.x) * xstride))
+    ring[i] = (static_cast<u32>(i) < ntaps) ? __ldg(reinterpret_cast<const uint4*>(Xb + e.x))
                                             : make_uint4(0, 0, 0, 0);
   }
   for (u32 t0 = 0; t0 < ntaps; t0 += kPre) {
@@ -383,7 +403,7 @@ __device__ __forceinline__ void conv_taps_int(const MacConvArgs& a, const DevPri
       if (t + kPre < ntaps) {
         const uint2 e = __ldg(tp + t + kPre);
         wring[i] = e.y;
-        ring[i] = __ldg(reinterpret_cast<const uint4*>(Xb + static_cast<u64>(e.x) * xstride));
+        ring[i] = __ldg(reinterpret_cast<const uint4*>(Xb + e.x));
       }
 #pragma unroll
       for (int f = 0; f < FT; ++f) {
@@ -423,7 +443,10 @@ __device__ __forceinline__ void conv_taps_int(const MacConvArgs& a, const DevPri
 template <int FT>
 __global__ void __launch_bounds__(kConvThreads, 3) k_mac_conv(MacConvArgs a, Basis B) {
   __shared__ __align__(16) u32 wsm[kMaxTaps * FT];
-  __shared__ double wsd[32 * FT];  // the same weights as doubles for the DFMA filters (<= 32 taps)
+  // the mixed path's (<= 32 taps) weights again, per tap: IMAD.WIDE filters as u32 pairs,
+  // DFMA filters as pre-converted doubles (128-bit loads)
+  __shared__ __align__(16) u32 wmi[32 * (ConvSplit<FT>::KIP > 0 ? ConvSplit<FT>::KIP : 2)];
+  __shared__ __align__(16) double wmd[32 * ConvSplit<FT>::KFP];
   const u32 tid = threadIdx.x;
   const u32 npos = a.OH * a.OW;
   const u32 nchunks = (a.F + FT - 1) / FT;
@@ -438,7 +461,19 @@ __global__ void __launch_bounds__(kConvThreads, 3) k_mac_conv(MacConvArgs a, Bas
     const u32 t = i / FT, f = i % FT;
     const u32 w = (f0 + f < a.F) ? __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + t]) : 0u;
     wsm[i] = w;
-    if (i < 32 * FT) wsd[i] = static_cast<double>(w);
+    if (t < 32) {
+      constexpr int KI = ConvSplit<FT>::KI, KIP = ConvSplit<FT>::KIP, KFP = ConvSplit<FT>::KFP;
+      if (static_cast<int>(f) < KI)
+        wmi[t * KIP + f] = w;
+      else
+        wmd[t * KFP + (f - KI)] = static_cast<double>(w);
+    }
+  }
+  if (tid < 32) {  // zero the padding slots
+    constexpr int KI = ConvSplit<FT>::KI, KIP = ConvSplit<FT>::KIP, KF = ConvSplit<FT>::KF;
+    constexpr int KFP = ConvSplit<FT>::KFP;
+    for (int c = KI; c < KIP; ++c) wmi[tid * KIP + c] = 0u;
+    for (int c = KF; c < KFP; ++c) wmd[tid * KFP + c] = 0.0;
   }
   __syncthreads();
   const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
@@ -452,9 +487,9 @@ __global__ void __launch_bounds__(kConvThreads, 3) k_mac_conv(MacConvArgs a, Bas
     const u32 off0 = __ldg(&a.tap_off[pos]);
     const u32 ntaps = __ldg(&a.tap_off[pos + 1]) - off0;
     if (fp && ntaps <= 32)
-      conv_taps_mixed<FT, kPre>(a, P, a.taps + off0, wsm, wsd, ntaps, Xb, xstride, poly, limb, f0, pos, n);
+      conv_taps_mixed<FT, kPre>(a, P, a.taps + off0, wmi, wmd, ntaps, Xb, poly, limb, f0, pos, n);
     else
-      conv_taps_int<FT, kPre>(a, P, a.taps + off0, wsm, ntaps, Xb, xstride, poly, limb, f0, pos, n);
+      conv_taps_int<FT, kPre>(a, P, a.taps + off0, wsm, ntaps, Xb, poly, limb, f0, pos, n);
   }
 }
 

@@ -46,7 +46,7 @@ struct MacConvArgs {
   u32 fold[kMaxPrimes];
   u32 fp64[kMaxPrimes];  // taps * (q-1)^2 < 2^53 and taps <= 32: part of the MACs as exact DFMAs
   const u32* tap_off;    // [OH*OW + 1]: position p's valid taps are taps[tap_off[p] .. tap_off[p+1])
-  const uint2* taps;     // (input element, window tap (c*win + ky)*win + kx), ascending per position
+  const uint2* taps;     // (input word offset, window tap (c*win + ky)*win + kx), ascending per position
 };
 
 #ifndef HG_KEY_SHOUP
