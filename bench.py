@@ -429,7 +429,7 @@ def b200_run(args, ws, rank, local):
     model_w = work_model(p["n"])
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
-    i8_peak = 2 * float(peaks["bf16_tflops"]) * 1e12 / 2  # int8 dense MAC/s = 2 x bf16 FLOP/s / 2
+    i8_peak = H.bench_int_peak(local, 4)  # measured int8 tcgen05 MMA MAC/s (raw, static operands)
     kernels = {}
     total_ms = sum(v["ms"] for v in prof.values()) / n_prof
     for name, v in prof.items():
@@ -450,7 +450,7 @@ def b200_run(args, ws, rank, local):
             t_tc = tc_work() / i8_peak * 1e3
             k.update({"bound": "tensor", "tensor_int8_macs_per_s": tc_work() / (ms * 1e-3),
                       "tensor_floor_ms": t_tc, "roofline_frac": max(t_tc, t_hbm) / ms if ms else 0,
-                      "tensor_peak_note": "int8 dense = 2 x measured bf16 (MEASURED_PEAKS.json)"})
+                      "tensor_peak_note": "measured raw tcgen05.mma.kind::i8 rate (hg_bench_int_peak kind 4)"})
         kernels[name] = k
     dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
     dk = kernels[dom]
@@ -609,7 +609,7 @@ def c5b_run(args, ws, rank, local):
     hbm_gbs, hbm_src = load_peaks()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
-    i8_peak = 2 * float(peaks["bf16_tflops"]) * 1e12 / 2  # int8 dense MAC/s
+    i8_peak = H.bench_int_peak(local, 4)  # measured int8 tcgen05 MMA MAC/s
     kern = {k: {"ms_per_step": v["ms"], "launches_per_step": v["launches"]} for k, v in prof.items()}
     # the contraction runs on the tensor cores: limbs 1..7 (30-bit) as 4 x 4 byte-plane
     # products, the 40-bit limb 0 as 5 x 5 (k_mac_dense_tc + k_mac_dense_tc_w)
@@ -618,7 +618,7 @@ def c5b_run(args, ws, rank, local):
     i8_macs = mac_r / L * ((L - 1) * 16 + 25)
     roof = {"bound": "tensor", "kernel": "+".join(tc_names), "achieved": i8_macs / (tc_ms * 1e-3) / 1e12,
             "peak": i8_peak / 1e12, "unit": "T int8 MAC/s", "frac": i8_macs / (tc_ms * 1e-3) / i8_peak,
-            "peak_source": "int8 dense = 2 x measured bf16 (MEASURED_PEAKS.json)",
+            "peak_source": "measured raw tcgen05.mma.kind::i8 rate, M=128 x N=256 x K=32 (hg_bench_int_peak kind 4)",
             "modular_mac_t_per_s": mac_r / (tc_ms * 1e-3) / 1e12,
             "hbm_gbs_achieved": byts / (tc_ms * 1e-3) / 1e9, "hbm_peak": hbm_gbs, "traffic": None,
             "algorithmic_per_step": {"modular_mac": mac_r, "int8_mac": i8_macs, "hbm_bytes": byts}}

@@ -263,7 +263,8 @@ int hg_execute(hg_ctx* ctx, const hg_model* m, const hg_plan* plan, const hg_ten
 /* Register-only integer-pipe microbenchmark (the INT32 roofline denominator):
  * kind 0 = IMAD (mad.lo.u32), 1 = IMAD.WIDE (mul.wide.u32, high word consumed: the cost of
  * one 32x32->64 MAC), 2 = IMAD.HI, 3 = Shoup lazy
- * modular product (IMAD.HI + 2 IMAD, the NTT butterfly's multiply); lane-ops/s. */
+ * modular product (IMAD.HI + 2 IMAD, the NTT butterfly's multiply), 4 = int8 tensor-core MACs
+ * (tcgen05.mma.kind::i8, M=128 x N=256 x K=32, one CTA per SM); lane-ops/s (MAC/s for 4). */
 int hg_bench_int_peak(int device, int kind, double* ops_per_s);
 /* Per-kernel CUDA-event profiler: when enabled, every kernel launch is bracketed by
  * events on its stream; hg_prof_report writes {"kernel": {"ms": total, "launches": n}}

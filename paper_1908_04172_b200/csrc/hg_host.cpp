@@ -2092,7 +2092,7 @@ int hg_execute(hg_ctx* ctx, const hg_model* m, const hg_plan* plan, const hg_ten
 
 int hg_bench_int_peak(int device, int kind, double* ops_per_s) {
   return guard([&] {
-    *ops_per_s = bench_int_peak(device, kind);
+    *ops_per_s = kind == 4 ? bench_tc_i8_peak(device) : bench_int_peak(device, kind);
     cuda_check(cudaGetLastError(), "imad probe");
   });
 }

@@ -231,14 +231,16 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
       if (ks + kTcXS - 1 < KS) issue(ks + kTcXS - 1);
       asm volatile("cp.async.commit_group;\n" ::);
       if (ks >= kTcS) mbar_wait(&S.empty[st], (use - 1) & 1);
-      for (u32 p = 0; p < planes; ++p) {
-        const u32 sh = 8 * p;
 #pragma unroll
-        for (int h = 0; h < TN / 32; ++h) {
-          const u32 b4 = ((v[h][0] >> sh) & 255) | (((v[h][1] >> sh) & 255) << 8) | (((v[h][2] >> sh) & 255) << 16) |
-                         (((v[h][3] >> sh) & 255) << 24);
-          *reinterpret_cast<u32*>(&S.b[st][p][cm_off(lane + 32 * h, r0)]) = b4;
-        }
+      for (int h = 0; h < TN / 32; ++h) {
+        // 4 x 4 byte transpose (8 PRMT): plane p gets byte p of the 4 residues k = r0 .. r0+3
+        const u32 t0 = __byte_perm(v[h][0], v[h][1], 0x5140), t1 = __byte_perm(v[h][0], v[h][1], 0x7362);
+        const u32 t2 = __byte_perm(v[h][2], v[h][3], 0x5140), t3 = __byte_perm(v[h][2], v[h][3], 0x7362);
+        const u32 o[4] = {__byte_perm(t0, t2, 0x5410), __byte_perm(t0, t2, 0x7632), __byte_perm(t1, t3, 0x5410),
+                          __byte_perm(t1, t3, 0x7632)};
+#pragma unroll
+        for (u32 p = 0; p < 4; ++p)
+          if (p < planes) *reinterpret_cast<u32*>(&S.b[st][p][cm_off(lane + 32 * h, r0)]) = o[p];
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::);
       __syncwarp();
@@ -483,6 +485,70 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc_w(MacDenseTcWArg
   if (warp == 0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTcCols));
   }
+}
+
+// ---------------------------------------------------------------------------
+// int8 tensor-core peak probe (the tensor roofline denominator): one CTA per SM issues
+// back-to-back M=128 x N=256 x K=32 kind::i8 MMAs from static shared-memory operands in
+// this file's layout (scripts/umma_probe.cu sweeps N).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128, 1) k_umma_probe(u32 iters) {
+  extern __shared__ __align__(1024) uint8_t pr_raw[];
+  __shared__ u32 tmem;
+  __shared__ __align__(8) unsigned long long bar;
+  for (u32 i = threadIdx.x; i < (4096 + 256 * 32) / 4; i += blockDim.x)
+    reinterpret_cast<u32*>(pr_raw)[i] = i * 2654435761u;
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_addr(&tmem)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::);
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  if (threadIdx.x == 0) {
+    constexpr u32 idesc = (2u << 4) | ((256 >> 3) << 17) | ((128 >> 4) << 24);
+    const u64 ad = umma_desc(smem_addr(pr_raw)), bd = umma_desc(smem_addr(pr_raw + 4096));
+    for (u32 it = 0; it < iters; ++it)
+      asm volatile(
+          "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+          "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc),
+          "r"(it));
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_addr(&bar)));
+    mbar_wait(&bar, 0);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+}
+
+double bench_tc_i8_peak(int device) {
+  cudaSetDevice(device);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaFuncSetAttribute(k_umma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  const u32 iters = 20000;
+  k_umma_probe<<<sms, 128, 160 * 1024>>>(100);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0);
+    k_umma_probe<<<sms, 128, 160 * 1024>>>(iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return static_cast<double>(sms) * iters * 128.0 * 256.0 * 32.0 / (best * 1e-3);  // int8 MAC/s
 }
 
 // ---------------------------------------------------------------------------

@@ -39,5 +39,6 @@ int launch_pack_weights_tc_w(const u64* W, uint8_t* Wp, u32 K, u32 M, u32 Mpad, 
 int launch_mac_dense_tc_w(MacDenseTcWArgs a, const void* P, cudaStream_t s);
 int launch_pack_weights_tc(const u32* W, uint8_t* Wp, u32 K, u32 M, u32 Mpad, u32 level, cudaStream_t s);
 int launch_mac_dense_tc(MacDenseTcArgs a, const Basis& B, cudaStream_t s);
+double bench_tc_i8_peak(int device);  // measured kind::i8 MMA rate (MAC/s), roofline denominator
 
 }  // namespace hg

@@ -541,7 +541,7 @@ def execute(ctx: CkksContext, model: PlainModel, plan: RescalePlan, inp: CipherT
 
 def bench_int_peak(device: int = 0, kind: int = 0) -> float:
     """Measured integer-pipe peak, lane-ops/s (kind 0 IMAD, 1 IMAD.WIDE (= one 32x32->64 MAC), 2 IMAD.HI,
-    3 Shoup lazy modular product = IMAD.HI + 2 IMAD)."""
+    3 Shoup lazy modular product = IMAD.HI + 2 IMAD, 4 int8 tensor-core MAC/s)."""
     v = C.c_double()
     check(lib.hg_bench_int_peak(device, kind, C.byref(v)))
     return v.value
