@@ -1259,53 +1259,91 @@ static cudaStream_t aux_stream() {
   return streams[dev];
 }
 
+// One relinearisation chain (digits -> special + limb key switches -> mod-down) on stream
+// s; the special-prime key switch runs on `ss` (== s, or an auxiliary stream it forks to).
+template <int LN>
+static void relin_chain(const RelinArgs& a, const Basis& B, cudaStream_t s, cudaStream_t aux_special) {
+  const size_t sm1 = sizeof(u32) * Ntt<LN, true>::SMEM_WORDS;         // digits (staged twiddles)
+  const size_t smk = sizeof(u32) * (Ntt<LN, true>::SMEM_WORDS + 4);  // key switch, mod-down
+  const int T = 1 << (LN - 5);
+  const bool prod = a.mode != 0;
+  auto dk = prod ? k_relin_digits<LN, 1> : k_relin_digits<LN, 0>;
+  auto kn = prod ? k_relin_keysw<LN, 1, false> : k_relin_keysw<LN, 0, false>;
+  auto ks = prod ? k_relin_keysw<LN, 1, true> : k_relin_keysw<LN, 0, true>;
+  set_smem(dk, sm1);
+  set_smem(kn, smk);
+  set_smem(ks, smk);
+  { ProfScope ps("k_relin_digits", s);
+  dk<<<a.count * a.level, T, sm1, s>>>(a, B);
+  }
+  cudaEvent_t fork = nullptr, join = nullptr;
+  if (aux_special) {
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    cudaEventRecord(fork, s);
+    cudaStreamWaitEvent(aux_special, fork, 0);
+  }
+  const cudaStream_t ss = aux_special ? aux_special : s;
+  { ProfScope ps("k_relin_keysw", ss);
+  ks<<<a.count, T, smk, ss>>>(a, B);
+  }
+  { ProfScope ps("k_relin_keysw", s);
+  kn<<<a.count * a.level, T, smk, s>>>(a, B);
+  }
+  if (aux_special) {
+    cudaEventRecord(join, aux_special);
+    cudaStreamWaitEvent(s, join, 0);
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+  }
+  { ProfScope ps("k_relin_moddown", s);
+  const int md = a.mode == 0 ? 0 : (a.A == a.Bm ? 1 : 2);
+  auto mdk = md == 0 ? (a.rescale ? k_relin_moddown<LN, 0, true> : k_relin_moddown<LN, 0, false>)
+           : md == 1 ? (a.rescale ? k_relin_moddown<LN, 1, true> : k_relin_moddown<LN, 1, false>)
+                     : (a.rescale ? k_relin_moddown<LN, 2, true> : k_relin_moddown<LN, 2, false>);
+  set_smem(mdk, smk);
+  mdk<<<a.count * 2, T, smk, s>>>(a, B);
+  }
+}
+
 int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s) {
   if (a.count == 0) return 0;
+  // Large batches run as two halves on two streams: one half's key switch (L1-bound) then
+  // shares SMs with the other half's mod-down (ALU/FMA-bound).  Small batches keep one chain,
+  // with the special-prime key switch on the auxiliary stream (its `count` CTAs alone would
+  // leave most SMs idle).
+  static const u64 split_min = [] {
+    const char* e = getenv("HG_RELIN_SPLIT_MIN");
+    return e ? static_cast<u64>(atoll(e)) : 256ull;
+  }();
+  cudaStream_t aux = aux_stream();
   HG_LOGN_SWITCH(logn, {
-    const size_t sm1 = sizeof(u32) * Ntt<LN, true>::SMEM_WORDS;  // digits (staged twiddles)
-    const size_t smk = sizeof(u32) * (Ntt<LN, true>::SMEM_WORDS + 4);  // key switch, mod-down
-    const int T = 1 << (LN - 5);
-    const bool prod = a.mode != 0;
-    auto dk = prod ? k_relin_digits<LN, 1> : k_relin_digits<LN, 0>;
-    auto kn = prod ? k_relin_keysw<LN, 1, false> : k_relin_keysw<LN, 0, false>;
-    auto ks = prod ? k_relin_keysw<LN, 1, true> : k_relin_keysw<LN, 0, true>;
-    set_smem(dk, sm1);
-    set_smem(kn, smk);
-    set_smem(ks, smk);
-    { ProfScope ps("k_relin_digits", s);
-    dk<<<a.count * a.level, T, sm1, s>>>(a, B);
-    }
-    // the special-prime and the limb key switches are independent: the special one runs on
-    // an auxiliary stream so each fills the other's tail wave (act2 has only `count` special
-    // CTAs for 148 SMs)
-    cudaStream_t aux = aux_stream();
-    cudaEvent_t fork = nullptr, join = nullptr;
-    if (aux) {
+    const u64 N = 1ull << LN, L = a.level, Lout = a.rescale ? L - 1 : L;
+    if (aux && split_min > 0 && a.count >= split_min) {
+      const u64 n0 = a.count / 2;
+      RelinArgs h0 = a, h1 = a;
+      h0.count = n0;
+      h1.count = a.count - n0;
+      const u64 in_polys = a.mode == 0 ? 3 : 2;
+      h1.A = a.A + n0 * in_polys * L * N;
+      h1.Bm = a.Bm == a.A ? h1.A : a.Bm + n0 * 2 * L * N;
+      h1.D = a.D + n0 * L * N;
+      h1.ACC = a.ACC + n0 * 2 * L * N;
+      h1.CORR = a.CORR + n0 * 2 * N;
+      h1.out = a.out + n0 * 2 * Lout * N;
+      cudaEvent_t fork, join;
       cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
       cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
       cudaEventRecord(fork, s);
       cudaStreamWaitEvent(aux, fork, 0);
-    }
-    const cudaStream_t ss = aux ? aux : s;
-    { ProfScope ps("k_relin_keysw", ss);
-    ks<<<a.count, T, smk, ss>>>(a, B);
-    }
-    { ProfScope ps("k_relin_keysw", s);
-    kn<<<a.count * a.level, T, smk, s>>>(a, B);
-    }
-    if (aux) {
+      relin_chain<LN>(h0, B, s, nullptr);
+      relin_chain<LN>(h1, B, aux, nullptr);
       cudaEventRecord(join, aux);
       cudaStreamWaitEvent(s, join, 0);
       cudaEventDestroy(fork);
       cudaEventDestroy(join);
-    }
-    { ProfScope ps("k_relin_moddown", s);
-    const int md = a.mode == 0 ? 0 : (a.A == a.Bm ? 1 : 2);
-    auto mdk = md == 0 ? (a.rescale ? k_relin_moddown<LN, 0, true> : k_relin_moddown<LN, 0, false>)
-             : md == 1 ? (a.rescale ? k_relin_moddown<LN, 1, true> : k_relin_moddown<LN, 1, false>)
-                       : (a.rescale ? k_relin_moddown<LN, 2, true> : k_relin_moddown<LN, 2, false>);
-    set_smem(mdk, smk);
-    mdk<<<a.count * 2, T, smk, s>>>(a, B);
+    } else {
+      relin_chain<LN>(a, B, s, aux);
     }
   });
   return 3;
