@@ -340,8 +340,10 @@ def b200_run(args, ws, rank, local):
     e2e = None
     if not args.no_e2e:
         # End to end through the C ABI with host buffers.  Every step uploads its own 617 MB of
-        # reference-format u64 words from pinned memory (hg_tensor_upload: H2D + narrowing +
-        # residue validation), executes, and downloads its logits (hg_tensor_download).  As a
+        # reference-format u64 words from pinned memory (hg_tensor_upload: residue validation +
+        # narrowing to u32 by host threads, chunk by chunk, each chunk's H2D overlapping the
+        # packing of the next -- 308 MB over PCIe; HG_UPLOAD_HOST_NARROW=0 copies the u64 words
+        # and narrows on the GPU), executes, and downloads its logits (hg_tensor_download).  As a
         # serving loop would, step i+1's upload runs on a second stream from a helper thread
         # while step i executes (ctypes calls release the GIL); the sequential loop is reported
         # beside it.
@@ -397,6 +399,7 @@ def b200_run(args, ws, rank, local):
                 torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
             return float(te.item())
 
+        host_narrow = os.environ.get("HG_UPLOAD_HOST_NARROW", "1") != "0"
         n_e2e = max(10, args.steps)
         # three trials of each loop, medians reported (the helper thread makes single trials
         # sensitive to host scheduling)
@@ -406,13 +409,17 @@ def b200_run(args, ws, rank, local):
         seq_trials = [timed(sequential, n_e2e) for _ in range(3)]
         e_ms, seq_ms = statistics.median(pipe_trials), statistics.median(seq_trials)
         e2e = {"value": IMAGES_PER_STEP * ws / (e_ms / 1e3), "unit": "images/s",
-               "h2d_bytes_per_step": int(words.nbytes), "d2h_bytes_per_step": int(out_host.nbytes),
+               "h2d_bytes_per_step": int(words.nbytes // (2 if host_narrow else 1)),
+               "d2h_bytes_per_step": int(out_host.nbytes),
+               "host_input_bytes_per_step": int(words.nbytes),
                "ms_per_step": e_ms, "steps": n_e2e, "trials_ms_per_step": pipe_trials,
                "sequential": {"value": IMAGES_PER_STEP * ws / (seq_ms / 1e3), "ms_per_step": seq_ms,
                               "trials_ms_per_step": seq_trials},
                "host_numa_node": numa,
-               "path": "hg_tensor_upload(u64 host words, second stream, next step) + hg_execute + "
-                       "hg_tensor_download, double-buffered"}
+               "path": "hg_tensor_upload(u64 host words, " +
+                       ("validated and packed to u32 by host threads, chunked H2D" if host_narrow else
+                        "u64 H2D, GPU narrowing") +
+                       ", second stream, next step) + hg_execute + hg_tensor_download, double-buffered"}
 
     # ---- per-kernel roofline pass (CUDA events around every launch) ----
     H.prof_enable(True)

@@ -1584,6 +1584,11 @@ int hg_tensor_upload(hg_tensor* t, const uint64_t* words, void* stream) {
     const Context& ctx = *t->ctx;
     cudaStream_t s = ctx.pick(stream);
     const u64 n = t->b.words(ctx.n);
+    if (!ctx.wide && host_narrow_enabled()) {
+      require(host_narrow_upload(ctx.core->device, words, t->b.data(), n, t->b.level, ctx.n, ctx.chain.data(), s),
+              "residue out of range");
+      return;
+    }
     int r;
     const size_t need = (ctx.wide ? 0 : n * 8) + sizeof(int);
     if (!t->stage || t->stage->bytes < need) {

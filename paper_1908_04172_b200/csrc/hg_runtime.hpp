@@ -33,6 +33,12 @@ inline void require(bool cond, const std::string& what) {
 }
 void cuda_check(cudaError_t e, const char* what);
 
+// hg_upload.cpp: reference u64 words -> device u32 residues, validated and packed by host
+// threads and DMA'd chunk by chunk (HG_UPLOAD_HOST_NARROW=0: copy u64, narrow on the GPU).
+bool host_narrow_enabled();
+bool host_narrow_upload(int device, const uint64_t* words, uint32_t* dst, uint64_t n_words, uint32_t level,
+                        uint32_t N, const uint64_t* chain, cudaStream_t s);
+
 // Shared device state: the stream and device; kept alive by every buffer.
 struct DeviceCore {
   int device = 0;

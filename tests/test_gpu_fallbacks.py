@@ -7,6 +7,7 @@ runs in its own subprocess and compares with the reference (oracle/_ref).
   HG_WIDE_TC=0    the 40-bit limb of a wide Dot on the CUDA-core 128-bit MAC kernel
   HG_CONV_FP64=0  convolution MACs all on IMAD.WIDE (no DFMA split)
   HG_AUX_STREAM=0 special-prime key switch on the main stream
+  HG_UPLOAD_HOST_NARROW=0  hg_tensor_upload copies u64 words and narrows them on the GPU
 """
 import os
 import subprocess
@@ -61,6 +62,7 @@ print("OK")
     ({"HG_DENSE_TC": "0"}, "toy"),
     ({"HG_CONV_FP64": "0"}, "toy"),
     ({"HG_AUX_STREAM": "0"}, "toy"),
+    ({"HG_UPLOAD_HOST_NARROW": "0"}, "toy"),
     ({"HG_WIDE_TC": "0"}, "wide"),
     ({"HG_DENSE_TC": "0"}, "wide"),
 ])
