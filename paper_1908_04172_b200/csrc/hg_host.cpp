@@ -963,10 +963,9 @@ class Executor {
     const auto& np = plan_.nodes.at(n.id);
     const bool naive = plan_.mode == HG_RESCALE_NAIVE;
     const bool layer_rescale = np.decision == HG_RESCALE_AFTER;
-    if (naive && layer_rescale)
-      throw Error(HG_ERR_UNSUPPORTED, "naive per-term rescaling of Dot/Convolution is not implemented on the GPU path");
     WeightTensor& w = model_.weights.at(n.weight_ref);
     WeightTensor* b = n.bias_ref.empty() ? nullptr : &model_.weights.at(n.bias_ref);
+    if (naive && layer_rescale) return eval_linear_naive(n, x, w, b);
     const double s = ctx.default_scale;
     const u32 L = x.level;
     const u32 N = ctx.n;
@@ -1292,6 +1291,160 @@ class Executor {
       rescales_ += M;
     }
     return v;
+  }
+
+  // Naive plan (mac_output, henet/graph.hpp:905-933, naive && RescaleAfter): every product
+  // x[i] * enc(w) is rescaled before it is accumulated; the bias goes in afterwards at the
+  // rescaled level and scale.  Round r multiplies every output's r-th tap (ascending
+  // eval_dot / eval_convolution order; a zero term where an output has fewer taps, and
+  // rescale(0) = 0), rescales the M terms as one batch and adds them into the accumulators.
+  Value eval_linear_naive(const Node& n, const CtBatch& x, WeightTensor& w, WeightTensor* b) {
+    const Context& ctx = *ctx_;
+    if (ctx.wide)
+      throw Error(HG_ERR_UNSUPPORTED, "naive per-term rescaling with primes >= 2^30 is not implemented on the GPU path");
+    require(x.level >= 2, "cannot rescale below level 1");
+    const double s = ctx.default_scale;
+    const u32 L = x.level;
+    const auto& out_shape = model_.shapes.at(n.id);
+    const u64 M = elem_count(out_shape);
+    check_scalar_encodable(ctx, w.max_abs, L, s);
+    std::vector<std::vector<std::pair<u32, u32>>> taps(M);  // (input element, weight index)
+    if (n.op == HG_OP_DOT) {
+      const u32 K = w.dims[0], Mo = w.dims[1];
+      for (u32 m = 0; m < Mo; ++m)
+        for (u32 k = 0; k < K; ++k) taps[m].emplace_back(k, k * Mo + m);
+    } else {
+      const auto& in = x.shape;
+      require(in.size() == 3, "Convolution expects a (C,H,W) input");
+      const u32 F = n.attrs.filters, C = in[0], IH = in[1], IW = in[2], win = n.attrs.window;
+      const u32 OH = out_shape[1], OW = out_shape[2];
+      for (u32 f = 0; f < F; ++f)
+        for (u32 oy = 0; oy < OH; ++oy)
+          for (u32 ox = 0; ox < OW; ++ox)
+            for (u32 c = 0; c < C; ++c)
+              for (u32 ky = 0; ky < win; ++ky)
+                for (u32 kx = 0; kx < win; ++kx) {
+                  const int iy = static_cast<int>(oy * n.attrs.stride + ky) - static_cast<int>(n.attrs.pad[0]);
+                  const int ix = static_cast<int>(ox * n.attrs.stride + kx) - static_cast<int>(n.attrs.pad[1]);
+                  if (iy < 0 || iy >= static_cast<int>(IH) || ix < 0 || ix >= static_cast<int>(IW)) continue;
+                  taps[(f * OH + oy) * OW + ox].emplace_back((c * IH + static_cast<u32>(iy)) * IW + static_cast<u32>(ix),
+                                                             ((f * C + c) * win + ky) * win + kx);
+                }
+    }
+    u64 R = 0, terms = 0;
+    for (const auto& t : taps) {
+      require(!t.empty(), "empty accumulation");
+      R = std::max<u64>(R, t.size());
+      terms += t.size();
+    }
+    std::vector<u32> gidx(R * M, 0xFFFFFFFFu), gw(R * M, 0u);
+    for (u64 m = 0; m < M; ++m)
+      for (u64 r = 0; r < taps[m].size(); ++r) {
+        gidx[r * M + m] = taps[m][r].first;
+        gw[r * M + m] = taps[m][r].second;
+      }
+    BufPtr tab = ctx.alloc(2 * R * M * 4, s_);
+    u32* d_gidx = static_cast<u32*>(tab->ptr);
+    u32* d_gw = d_gidx + R * M;
+    cuda_check(cudaMemcpyAsync(d_gidx, gidx.data(), R * M * 4, cudaMemcpyHostToDevice, s_), "h2d");
+    cuda_check(cudaMemcpyAsync(d_gw, gw.data(), R * M * 4, cudaMemcpyHostToDevice, s_), "h2d");
+    // weight residues element-major [count][L]
+    const float* wd = weight_dev(ctx, w, s_);
+    const u64 wc = w.data.size();
+    BufPtr wres = ctx.alloc(wc * L * 4, s_);
+    check_launch(encode_f32(ctx, wd, wc, 1, L, 1, L, s, wres->ptr, s_), "encode weights");
+
+    CtBatch term;
+    term.packing = x.packing;
+    term.scale = x.scale * s;  // term.scale = x.scale * pt.scale (henet/ckks.hpp:384)
+    ensure(ctx, term, M, 2, L, s_);
+    CtBatch acc;
+    for (u64 r = 0; r < R; ++r) {
+      EwArgs e{};
+      e.op = EwOp::GatherMul;
+      e.a = x.data();
+      e.res = static_cast<const u32*>(wres->ptr);
+      e.gidx = d_gidx + r * M;
+      e.gw = d_gw + r * M;
+      e.out = term.data();
+      e.count = M;
+      e.polys_a = 2;
+      e.polys_out = 2;
+      e.level = L;
+      run_ew(ctx, e, s_);
+      CtBatch t = do_rescale(ctx, term, L - 1, s_);
+      if (r == 0) {
+        acc = t;
+      } else {
+        EwArgs a{};
+        a.op = EwOp::AddCC;
+        a.a = acc.data();
+        a.b = t.data();
+        a.out = acc.data();
+        a.count = M;
+        a.polys_a = 2;
+        a.polys_out = 2;
+        a.level = L - 1;
+        run_ew(ctx, a, s_);
+      }
+    }
+    rescales_ += terms;
+    acc.shape = out_shape;
+    acc.packing = x.packing;
+    if (b) {
+      const u32 bl = L - 1;
+      check_scalar_encodable(ctx, b->max_abs, bl, acc.scale);
+      const u32 pt_div = n.op == HG_OP_DOT ? 1 : out_shape[1] * out_shape[2];
+      EwArgs e{};
+      e.a = acc.data();
+      e.out = acc.data();
+      e.per_element = 1;
+      e.pt_div = pt_div;
+      e.count = M;
+      e.polys_a = 2;
+      e.polys_out = 2;
+      e.level = bl;
+      BufPtr bias_res;
+      if (x.packing == HG_PACKING_REAL) {
+        // encode_broadcast of a real scalar: the expanded constant (henet/encoding.hpp:210-219)
+        const float* bd = weight_dev(ctx, *b, s_);
+        bias_res = ctx.alloc(b->data.size() * bl * 4, s_);
+        check_launch(encode_f32(ctx, bd, b->data.size(), 1, bl, 1, bl, acc.scale, bias_res->ptr, s_), "encode bias");
+        e.op = EwOp::AddScalar;
+        e.res = static_cast<const u32*>(bias_res->ptr);
+      } else {
+        bias_res = complex_bias(*b, bl, acc.scale);
+        e.op = EwOp::AddVector;
+        e.b = static_cast<const u32*>(bias_res->ptr);
+      }
+      run_ew(ctx, e, s_);
+      cuda_check(cudaStreamSynchronize(s_), "bias");  // host-side bias buffers leave scope
+    }
+    Value v;
+    v.is_cipher = true;
+    v.cipher = acc;
+    return v;
+  }
+
+  // encode_broadcast under complex packing: encode_vector of (b + b i) in every slot
+  // (henet/encoding.hpp:275-283) at (level, scale); one plaintext per bias value.
+  BufPtr complex_bias(const WeightTensor& b, u32 level, double scale) {
+    const Context& ctx = *ctx_;
+    const u64 nb = b.data.size();
+    std::vector<double> slots(nb * ctx.n);
+    for (u64 i = 0; i < nb; ++i)
+      for (u32 j = 0; j < ctx.n / 2; ++j) {
+        slots[(i * ctx.n / 2 + j) * 2] = b.data[i];
+        slots[(i * ctx.n / 2 + j) * 2 + 1] = b.data[i];
+      }
+    BufPtr ds = ctx.alloc(slots.size() * sizeof(double), s_);
+    cuda_check(cudaMemcpyAsync(ds->ptr, slots.data(), slots.size() * sizeof(double), cudaMemcpyHostToDevice, s_),
+               "h2d");
+    std::vector<unsigned long long> mant;
+    std::vector<int> ex;
+    BufPtr pt = encode_vectors_dev(ctx, static_cast<const double*>(ds->ptr), ctx.n / 2, nb, level, scale, s_, mant, ex);
+    cuda_check(cudaStreamSynchronize(s_), "bias");  // the host slot vector leaves scope
+    return pt;
   }
 
   Value eval_square(const Node& n, std::map<std::string, Value>& values) {

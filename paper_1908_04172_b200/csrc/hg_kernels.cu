@@ -919,6 +919,17 @@ __global__ void k_ew(EwArgs a, Basis B) {
       }
       break;
     }
+    case EwOp::GatherMul: {
+      const u32 src = a.gidx[e];
+      if (src == 0xFFFFFFFFu) {
+        o = make_uint4(0, 0, 0, 0);
+      } else {
+        const uint4 x = *reinterpret_cast<const uint4*>(a.a + ((static_cast<u64>(src) * a.polys_a + poly) * a.level + limb) * N + n);
+        const u32 r = a.res[static_cast<u64>(a.gw[e]) * a.level + limb];
+        o = make_uint4(mulmod(x.x, r, P), mulmod(x.y, r, P), mulmod(x.z, r, P), mulmod(x.w, r, P));
+      }
+      break;
+    }
     case EwOp::Copy:
     default:
       o = ld(a.a, a.polys_a, poly);

@@ -74,7 +74,7 @@ struct RelinArgs {
   u32 pmP[kMaxPrimes];  // multiple of q_i >= floor(P/2): special-prime correction + pmP >= 0
 };
 
-enum class EwOp : int { AddCC = 0, MulScalar = 1, AddScalar = 2, AddVector = 3, Tensor = 4, Copy = 5 };
+enum class EwOp : int { AddCC = 0, MulScalar = 1, AddScalar = 2, AddVector = 3, Tensor = 4, Copy = 5, GatherMul = 6 };
 
 struct EwArgs {
   EwOp op;
@@ -86,6 +86,9 @@ struct EwArgs {
   u32* out;
   u64 count;
   u32 polys_a, polys_out, level, N;
+  // GatherMul: out[e] = a[gidx[e]] * res[gw[e]][limb] (zero where gidx[e] == ~0u)
+  const u32* gidx;
+  const u32* gw;
 };
 
 int launch_ntt(int logn, u32* data, u64 rows, u32 level, bool inverse, const Basis& B,

@@ -86,16 +86,17 @@ def _gauss(rng: np.random.Generator, shape, sigma) -> np.ndarray:
     return (rng.standard_normal(int(np.prod(shape))) * sigma).astype(np.float32)
 
 
-def dense_layer(seed: int = 1, k: int = 845, m: int = 100, batch: int = 4096) -> Workload:
+def dense_layer(seed: int = 1, k: int = 845, m: int = 100, batch: int = 4096, packing: int = 0) -> Workload:
     """Config 1: single encrypted dense layer 845 -> 100 with bias, W ~ N(0, 0.05^2),
-    b ~ N(0, 0.01^2); one lazy rescale per output (patched plan)."""
+    b ~ N(0, 0.01^2); one lazy rescale per output (patched plan).  packing=1: complex
+    packing (two images per slot), the bias encoded by encode_vector."""
     rng = np.random.default_rng(seed)
     blob = Blob()
     blob.add("fc_w", [k, m], _gauss(rng, (k, m), 0.05))
     blob.add("fc_b", [m], _gauss(rng, (m,), 0.01))
     j = {
         "name": "dense-845-100",
-        "packing": "real",
+        "packing": "complex" if packing else "real",
         "preset": "P13",
         "weights": blob.table,
         "nodes": [
@@ -104,7 +105,7 @@ def dense_layer(seed: int = 1, k: int = 845, m: int = 100, batch: int = 4096) ->
             _node("out", "Output", ["fc"]),
         ],
     }
-    return Workload("c1_dense_845_100", json.dumps(j), blob.bytes(), [k], 0, batch, patch_terminal_rescale=True)
+    return Workload("c1_dense_845_100", json.dumps(j), blob.bytes(), [k], packing, batch, patch_terminal_rescale=True)
 
 
 def cryptonets(seed: int = 2, batch: int = 4096, sigma: float = 0.05) -> Workload:

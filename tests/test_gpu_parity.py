@@ -123,19 +123,19 @@ def test_encode_vector_bit_exact(env):
             assert np.array_equal(got, want), (n_slots, cplx, level)
 
 
-def _run_both(env, wl, seed=21, threads=0, check_plan=True):
+def _run_both(env, wl, seed=21, threads=0, check_plan=True, mode=0):
     ctx, ref, keys, rk = env["ctx"], env["ref"], env["keys"], env["rk"]
     imgs = W.synthetic_images(wl.input_shape, wl.batch, seed)
     words, sc = ref.encrypt_tensor(keys, imgs, seed + 1, packing=wl.packing)
-    want, want_sc, st = ref.execute(keys, wl.manifest, wl.blob, words, sc, patch=wl.patch_terminal_rescale,
-                                    threads=threads, refresh_seed=99)
+    want, want_sc, st = ref.execute(keys, wl.manifest, wl.blob, words, sc, mode=mode,
+                                    patch=wl.patch_terminal_rescale, threads=threads, refresh_seed=99)
     model = H.PlainModel.load(wl.manifest, wl.blob)
-    rp = ref.plan(wl.manifest, wl.blob, patch=wl.patch_terminal_rescale)
+    rp = ref.plan(wl.manifest, wl.blob, mode=mode, patch=wl.patch_terminal_rescale)
     nodes = {n["id"]: (n["decision"], n["level_in"], n["level_out"],
                        np.array([n["scale_out_bits"]], dtype=np.uint64).view(np.float64)[0]) for n in rp["nodes"]}
-    plan = H.RescalePlan.from_nodes(0, rp["planned_rescale_ops"], nodes)
+    plan = H.RescalePlan.from_nodes(mode, rp["planned_rescale_ops"], nodes)
     if check_plan and not wl.patch_terminal_rescale:
-        own = H.RescalePlan.plan(ctx, model)
+        own = H.RescalePlan.plan(ctx, model, mode)
         assert own.planned_rescale_ops == rp["planned_rescale_ops"]
         for nid, v in nodes.items():
             assert own.node(nid) == v, nid
@@ -170,3 +170,21 @@ def test_execute_c2_cryptonets_bit_exact(env):
 @pytest.mark.slow
 def test_execute_c3_relu_complex_bit_exact(env):
     _run_both(env, W.cryptonets_relu())
+
+
+# Naive rescaling (henet/graph.hpp:905-933 under RescaleMode::Naive): every ct x pt term is
+# rescaled before accumulation and the bias is added at the rescaled level and scale.
+def test_execute_toy_naive_bit_exact(env):
+    _run_both(env, W.toy_cryptonets(), mode=1)
+
+
+def test_execute_dense_naive_bias_bit_exact(env):
+    _run_both(env, W.dense_layer(seed=5, k=40, m=7), mode=1)
+
+
+def test_execute_dense_naive_complex_bias_bit_exact(env):
+    _run_both(env, W.dense_layer(seed=6, k=24, m=5, batch=8192, packing=1), mode=1)
+
+
+def test_execute_dense_lazy_complex_bias_bit_exact(env):
+    _run_both(env, W.dense_layer(seed=6, k=24, m=5, batch=8192, packing=1))
