@@ -192,6 +192,27 @@ int hg_encode_vector(hg_ctx* ctx, const double* slots_re_im, uint32_t n_slots, u
                      uint32_t level, double scale, uint64_t* out_words);
 
 /* ------------------------------------------------------------------ */
+/* Client side on the GPU (u32-residue contexts)                       */
+/* ------------------------------------------------------------------ */
+typedef struct hg_secret_key hg_secret_key; /* SecretKey (henet/ckks.hpp:21-23) on device */
+/* s in NTT form over the full basis, chain limbs then the special limb, in the word order
+ * of serialize_secret_key (henet/serialize.hpp:129-136): (chain_len + 1) x N words. */
+int hg_secret_key_upload(hg_ctx* ctx, const uint64_t* words, uint64_t n_words, hg_secret_key** out);
+void hg_secret_key_destroy(hg_secret_key* sk);
+/* encrypt_tensor (henet/graph.hpp:68-91): samples[s * count + e] is element e of sample s
+ * (BatchInput::samples); ciphertext e = encrypt_batch(values of element e, sk,
+ * derive_seed(seed, e)) at the top level and default scale (henet/ckks.hpp:229-254).
+ * `out` is overwritten with the count ciphertexts. */
+int hg_encrypt_tensor(hg_ctx* ctx, const hg_secret_key* sk, const double* samples, uint32_t batch,
+                      uint64_t count, uint64_t seed, int packing, hg_tensor* out, void* stream);
+/* decrypt (henet/ckks.hpp:256-268): plaintext residues count x level x N (u64, NTT domain). */
+int hg_decrypt(hg_ctx* ctx, const hg_secret_key* sk, const hg_tensor* ct, uint64_t* pt_words,
+               void* stream);
+/* decrypt_tensor (henet/graph.hpp:93-103): out[s * count + e], s < batch. */
+int hg_decrypt_tensor(hg_ctx* ctx, const hg_secret_key* sk, const hg_tensor* ct, uint32_t batch,
+                      double* out, void* stream);
+
+/* ------------------------------------------------------------------ */
 /* Graph level: PlainModel / RescalePlan / execute                     */
 /* ------------------------------------------------------------------ */
 typedef struct hg_node_desc {

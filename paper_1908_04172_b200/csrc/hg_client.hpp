@@ -1,0 +1,50 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// GPU encrypt / decrypt (hg_client.cu): the client side of henet/graph.hpp:68-103.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "hg_kernels.hpp"
+
+namespace hg {
+
+constexpr int kCrtWords = 4;  // Q < 2^256 (chains of <= 8 primes below 2^32)
+
+struct EncArgs {
+  u32* ct;          // [count][2][level][N]: c1 = a written by the sampler, c0 by combine
+  u32* err;         // [count][level][N]: error lifted into every limb (then NTT'd in place)
+  const u32* pt;    // [count][level][N]: encoded plaintexts (NTT domain)
+  const u32* sk;    // [full][N]: secret key s (NTT domain)
+  int* flags;       // [count]: 1 if the counter-mode draw hit a rejection / u1 == 0
+  u64 seed;         // encrypt_tensor seed; ciphertext e uses derive_seed(seed, e), stream 1
+  u64 thr[kMaxPrimes];  // next_below rejection thresholds (2^64 mod q)
+  u32 count, level, N;
+};
+
+struct CrtTables {
+  u64 q_over_p[kMaxPrimes][kCrtWords + 1];  // Q / q_i
+  u64 big_q[kCrtWords + 1];                 // Q = prod q_i
+  u64 q_half[kCrtWords + 1];                // floor(Q / 2)
+  u32 inv[kMaxPrimes];                      // (Q / q_i)^-1 mod q_i
+};
+
+struct DecArgs {
+  const u32* ct;    // [count][polys][level][N]
+  const u32* sk;    // [full][N]
+  u32* m;           // [count][level][N]: decrypted plaintext residues
+  double* coeffs;   // [count][N] (nullptr: residues only)
+  double inv_scale;
+  CrtTables crt;
+  u32 count, polys, level, N, words;
+};
+
+int launch_enc_sample(const EncArgs& a, const Basis& B, cudaStream_t s);
+int launch_enc_serial(const EncArgs& a, const u32* list, u32 n_list, const Basis& B, cudaStream_t s);
+int launch_enc_combine(const EncArgs& a, const Basis& B, cudaStream_t s);
+// decrypt (k_dec_combine) and, when a.coeffs is set, decode: INTT, CRT, forward embedding
+// into slots [count][N/2][2]
+int launch_dec(const DecArgs& a, int logn, const Basis& B, const double2* roots, const double2* twist,
+               double2* scratch, double* slots, cudaStream_t s);
+
+}  // namespace hg

@@ -2274,3 +2274,227 @@ int hg_last_exec_node_ms(hg_ctx* ctx, double* ms_by_op) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Client side on the GPU (hg_client.cu): secret key, encrypt_tensor, decrypt,
+// decrypt_tensor (henet/graph.hpp:68-103, henet/ckks.hpp:229-263).
+// ---------------------------------------------------------------------------
+namespace {
+using namespace hg;
+
+// little-endian multi-word helpers for the CRT tables
+void mw_mul_small(std::vector<u64>& x, u64 m) {
+  unsigned __int128 carry = 0;
+  for (auto& w : x) {
+    const unsigned __int128 t = static_cast<unsigned __int128>(w) * m + carry;
+    w = static_cast<u64>(t);
+    carry = t >> 64;
+  }
+  if (carry) x.push_back(static_cast<u64>(carry));
+}
+u64 mw_mod(const std::vector<u64>& x, u64 q) {
+  unsigned __int128 r = 0;
+  for (size_t i = x.size(); i-- > 0;) r = ((r << 64) | x[i]) % q;
+  return static_cast<u64>(r);
+}
+
+void check_client_ctx(const Context& c) {
+  if (c.wide) throw Error(HG_ERR_UNSUPPORTED, "GPU encrypt/decrypt with primes >= 2^30 is not implemented yet");
+}
+}  // namespace
+
+int hg_secret_key_upload(hg_ctx* ctx, const uint64_t* words, uint64_t n_words, hg_secret_key** out) {
+  return guard([&] {
+    require(ctx && words && out, "null argument");
+    const Context& c = *ctx->c;
+    check_client_ctx(c);
+    const u64 full = c.chain_len() + (c.has_special ? 1 : 0), n = c.n;
+    require(n_words == full * n, "secret key basis does not match the context");
+    std::vector<u32> h(n_words);
+    for (u64 i = 0; i < n_words; ++i) {
+      require(words[i] < c.basis_mod(i / n), "residue out of range");
+      h[i] = static_cast<u32>(words[i]);
+    }
+    auto* k = new hg_secret_key;
+    k->ctx = ctx->c;
+    k->s = c.alloc(n_words * 4, c.core->stream);
+    cuda_check(cudaMemcpyAsync(k->s->ptr, h.data(), n_words * 4, cudaMemcpyHostToDevice, c.core->stream), "h2d");
+    cuda_check(cudaStreamSynchronize(c.core->stream), "secret key");
+    *out = k;
+  });
+}
+
+void hg_secret_key_destroy(hg_secret_key* sk) { delete sk; }
+
+int hg_encrypt_tensor(hg_ctx* ctx, const hg_secret_key* sk, const double* samples, uint32_t batch, uint64_t count,
+                      uint64_t seed, int packing, hg_tensor* out, void* stream) {
+  return guard([&] {
+    require(ctx && sk && samples && out, "null argument");
+    const Context& c = *ctx->c;
+    check_client_ctx(c);
+    cudaStream_t s = c.pick(stream);
+    require(packing == HG_PACKING_REAL || packing == HG_PACKING_COMPLEX, "unknown packing mode");
+    require(batch >= 1, "batch must be non-empty");
+    require(batch <= (packing == HG_PACKING_REAL ? c.n / 2 : c.n), "batch exceeds slot capacity");
+    if (packing == HG_PACKING_COMPLEX) require(batch % 2 == 0, "complex packing needs an even batch");
+    require(count >= 1, "tensor must be non-empty");
+    const u32 L = static_cast<u32>(c.chain_len()), N = c.n;
+    // batch_to_slots per element (henet/encoding.hpp:72-87), then encode_vector at the top
+    // level and the default scale (encrypt_batch, henet/ckks.hpp:250-254)
+    const u32 n_slots = packing == HG_PACKING_REAL ? batch : batch / 2;
+    std::vector<double> slots(count * n_slots * 2);
+    for (u64 e = 0; e < count; ++e)
+      for (u32 j = 0; j < n_slots; ++j) {
+        double* d = &slots[(e * n_slots + j) * 2];
+        if (packing == HG_PACKING_REAL) {
+          d[0] = samples[static_cast<u64>(j) * count + e];
+          d[1] = 0.0;
+        } else {
+          d[0] = samples[static_cast<u64>(j) * count + e];
+          d[1] = samples[static_cast<u64>(j + n_slots) * count + e];
+        }
+      }
+    BufPtr ds = c.alloc(slots.size() * sizeof(double), s);
+    cuda_check(cudaMemcpyAsync(ds->ptr, slots.data(), slots.size() * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
+    std::vector<unsigned long long> mant;
+    std::vector<int> ex;
+    BufPtr pt = encode_vectors_dev(c, static_cast<const double*>(ds->ptr), n_slots, count, L, c.default_scale, s, mant, ex);
+
+    CtBatch o;
+    o.packing = packing;
+    o.scale = c.default_scale;
+    ensure(c, o, count, 2, L, s);
+    o.shape = {static_cast<u32>(count)};
+    BufPtr err = c.alloc(count * L * static_cast<u64>(N) * 4, s);
+    BufPtr flags = c.alloc(count * sizeof(int), s);
+    cuda_check(cudaMemsetAsync(flags->ptr, 0, count * sizeof(int), s), "memset");
+    EncArgs a{};
+    a.ct = o.data();
+    a.err = static_cast<u32*>(err->ptr);
+    a.pt = static_cast<const u32*>(pt->ptr);
+    a.sk = static_cast<const u32*>(sk->s->ptr);
+    a.flags = static_cast<int*>(flags->ptr);
+    a.seed = seed;
+    for (u32 i = 0; i < L; ++i) a.thr[i] = (0 - c.chain[i]) % c.chain[i];  // next_below threshold
+    a.count = static_cast<u32>(count);
+    a.level = L;
+    a.N = N;
+    check_launch(launch_enc_sample(a, c.basis, s), "encrypt sample");
+    // draws the counter-mode pass could not place (a rejection, u1 == 0): regenerate those
+    // ciphertexts by walking their streams; HG_ENC_SERIAL=1 walks every stream (tests)
+    std::vector<int> hf(count);
+    cuda_check(cudaMemcpyAsync(hf.data(), flags->ptr, count * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaStreamSynchronize(s), "encrypt");
+    const char* ser = getenv("HG_ENC_SERIAL");
+    const bool all = ser != nullptr && ser[0] == '1';
+    std::vector<u32> list;
+    for (u64 e = 0; e < count; ++e)
+      if (all || hf[e]) list.push_back(static_cast<u32>(e));
+    BufPtr dl;
+    if (!list.empty()) {
+      dl = c.alloc(list.size() * 4, s);
+      cuda_check(cudaMemcpyAsync(dl->ptr, list.data(), list.size() * 4, cudaMemcpyHostToDevice, s), "h2d");
+      check_launch(launch_enc_serial(a, static_cast<const u32*>(dl->ptr), static_cast<u32>(list.size()), c.basis, s),
+                   "encrypt serial");
+    }
+    check_launch(launch_ntt(static_cast<int>(c.logn), a.err, count * L, L, false, c.basis, s), "ntt");
+    check_launch(launch_enc_combine(a, c.basis, s), "encrypt combine");
+    cuda_check(cudaStreamSynchronize(s), "encrypt");
+    out->b = o;
+  });
+}
+
+namespace {
+DecArgs dec_args(const Context& c, const hg_secret_key* sk, const CtBatch& ct) {
+  require(ct.polys == 2 || ct.polys == 3, "ciphertext must have 2 or 3 polynomials");
+  require(ct.level >= 1, "ciphertext level must be at least 1");
+  DecArgs a{};
+  a.ct = ct.data();
+  a.sk = static_cast<const u32*>(sk->s->ptr);
+  a.count = static_cast<u32>(ct.count);
+  a.polys = ct.polys;
+  a.level = ct.level;
+  a.N = c.n;
+  return a;
+}
+}  // namespace
+
+int hg_decrypt(hg_ctx* ctx, const hg_secret_key* sk, const hg_tensor* ct, uint64_t* pt_words, void* stream) {
+  return guard([&] {
+    require(ctx && sk && ct && pt_words, "null argument");
+    const Context& c = *ctx->c;
+    check_client_ctx(c);
+    cudaStream_t s = c.pick(stream);
+    DecArgs a = dec_args(c, sk, ct->b);
+    const u64 nw = ct->b.count * ct->b.level * static_cast<u64>(c.n);
+    BufPtr m = c.alloc(nw * 4, s);
+    a.m = static_cast<u32*>(m->ptr);
+    check_launch(launch_dec(a, static_cast<int>(c.logn), c.basis, nullptr, nullptr, nullptr, nullptr, s), "decrypt");
+    std::vector<u32> h(nw);
+    cuda_check(cudaMemcpyAsync(h.data(), m->ptr, nw * 4, cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaStreamSynchronize(s), "decrypt");
+    for (u64 i = 0; i < nw; ++i) pt_words[i] = h[i];
+  });
+}
+
+int hg_decrypt_tensor(hg_ctx* ctx, const hg_secret_key* sk, const hg_tensor* ct, uint32_t batch, double* out,
+                      void* stream) {
+  return guard([&] {
+    require(ctx && sk && ct && out, "null argument");
+    const Context& c = *ctx->c;
+    check_client_ctx(c);
+    cudaStream_t s = c.pick(stream);
+    const CtBatch& b = ct->b;
+    DecArgs a = dec_args(c, sk, b);
+    const u32 half = c.n / 2;
+    if (b.packing == HG_PACKING_REAL) {
+      require(batch <= half, "batch larger than decoded slots");
+    } else {
+      require(batch % 2 == 0, "complex batch size must be even");
+      require(batch / 2 <= half, "batch larger than decoded slots");
+    }
+    // CRT tables for this level (decode_slots, henet/encoding.hpp:226-243)
+    const u32 L = b.level;
+    std::vector<u64> big{1};
+    for (u32 i = 0; i < L; ++i) mw_mul_small(big, c.chain[i]);
+    require(big.size() <= static_cast<size_t>(kCrtWords), "modulus too large for the GPU decoder");
+    a.words = static_cast<u32>(big.size());
+    for (u32 k = 0; k < a.words; ++k) a.crt.big_q[k] = big[k];
+    for (u32 k = 0; k < a.words; ++k) a.crt.q_half[k] = (big[k] >> 1) | (k + 1 < a.words ? (big[k + 1] << 63) : 0);
+    for (u32 i = 0; i < L; ++i) {
+      std::vector<u64> qi{1};
+      for (u32 j = 0; j < L; ++j)
+        if (j != i) mw_mul_small(qi, c.chain[j]);
+      for (u32 k = 0; k < qi.size() && k < static_cast<size_t>(kCrtWords); ++k) a.crt.q_over_p[i][k] = qi[k];
+      a.crt.inv[i] = static_cast<u32>(nt::inv(mw_mod(qi, c.chain[i]), c.chain[i]));
+    }
+    a.inv_scale = 1.0 / b.scale;
+    const u64 count = b.count, N = c.n;
+    BufPtr m = c.alloc(count * L * N * 4, s);
+    BufPtr co = c.alloc(count * N * sizeof(double), s);
+    BufPtr scratch = c.alloc(count * N * sizeof(double2), s);
+    BufPtr sl = c.alloc(count * N * sizeof(double), s);  // [count][N/2][2]
+    a.m = static_cast<u32*>(m->ptr);
+    a.coeffs = static_cast<double*>(co->ptr);
+    const double2* roots = static_cast<const double2*>(c.fft_tables->ptr);
+    check_launch(launch_dec(a, static_cast<int>(c.logn), c.basis, roots, roots + N / 2,
+                            static_cast<double2*>(scratch->ptr), static_cast<double*>(sl->ptr), s),
+                 "decrypt");
+    std::vector<double> h(count * N);
+    cuda_check(cudaMemcpyAsync(h.data(), sl->ptr, count * N * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaStreamSynchronize(s), "decrypt");
+    // slots_to_batch (henet/encoding.hpp:89-107), samples[s][e]
+    for (u64 e = 0; e < count; ++e) {
+      const double* v = &h[e * N];
+      if (b.packing == HG_PACKING_REAL) {
+        for (u32 j = 0; j < batch; ++j) out[j * count + e] = v[2 * j];
+      } else {
+        const u32 k = batch / 2;
+        for (u32 j = 0; j < k; ++j) {
+          out[j * count + e] = v[2 * j];
+          out[(j + k) * count + e] = v[2 * j + 1];
+        }
+      }
+    }
+  });
+}

@@ -21,6 +21,7 @@
 #include "hg_kernels.hpp"
 #include "hg_wide.hpp"
 #include "hg_tc.hpp"
+#include "hg_client.hpp"
 
 namespace hg {
 
@@ -167,6 +168,10 @@ struct hg_tensor {
 struct hg_relin_key {
   std::shared_ptr<hg::Context> ctx;
   hg::RelinKeyDev k;
+};
+struct hg_secret_key {
+  std::shared_ptr<hg::Context> ctx;
+  hg::BufPtr s;  // [full][N] u32, NTT domain (SecretKey::s, henet/ckks.hpp:21-23)
 };
 struct hg_model {
   hg::Model m;

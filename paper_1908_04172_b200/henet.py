@@ -231,6 +231,55 @@ class RelinKey:
         return self._h
 
 
+class SecretKey:
+    """SecretKey (henet/ckks.hpp:21-23): s in NTT form over the full basis (chain limbs,
+    then the special limb), serialize_secret_key word order; on the device for the GPU
+    client side (encrypt_tensor / decrypt / decrypt_tensor)."""
+
+    def __init__(self, ctx: CkksContext, words: np.ndarray):
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        h = C.c_void_p()
+        check(lib.hg_secret_key_upload(ctx.handle, _ptr(w), w.size, C.byref(h)))
+        self._h = h
+        self.ctx = ctx
+
+    def __del__(self):
+        if getattr(self, "_h", None) and lib is not None:
+            lib.hg_secret_key_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+
+def encrypt_tensor(ctx: CkksContext, sk: SecretKey, samples: np.ndarray, seed: int, packing: int = PACKING_REAL,
+                   shape: Optional[Sequence[int]] = None) -> "CipherTensor":
+    """encrypt_tensor (henet/graph.hpp:68-91) on the GPU: samples (batch, count), one
+    ciphertext per element, encrypt_batch with derive_seed(seed, e)."""
+    s = np.ascontiguousarray(samples, dtype=np.float64)
+    batch, count = s.shape
+    out = CipherTensor(ctx, count, 2, len(ctx.chain), ctx.default_scale, packing)
+    check(lib.hg_encrypt_tensor(ctx.handle, sk.handle, _ptr(s), batch, count, seed, packing, out.handle, None))
+    if shape is not None:
+        out.set_shape(shape)
+    return out
+
+
+def decrypt(ctx: CkksContext, sk: SecretKey, ct: "CipherTensor") -> np.ndarray:
+    """decrypt (henet/ckks.hpp:256-268): plaintext words (count, level, N), NTT domain."""
+    out = np.empty((ct.count, ct.level, ctx.n), dtype=np.uint64)
+    check(lib.hg_decrypt(ctx.handle, sk.handle, ct.handle, _ptr(out), None))
+    return out
+
+
+def decrypt_tensor(ctx: CkksContext, sk: SecretKey, ct: "CipherTensor", batch: int) -> np.ndarray:
+    """decrypt_tensor (henet/graph.hpp:93-103): (batch, count) decoded values."""
+    out = np.empty((batch, ct.count), dtype=np.float64)
+    check(lib.hg_decrypt_tensor(ctx.handle, sk.handle, ct.handle, batch, _ptr(out), None))
+    return out
+
+
 def _empty_like(ctx: CkksContext, ct: CipherTensor) -> CipherTensor:
     return CipherTensor(ctx, 0, 2, 1, 1.0)
 

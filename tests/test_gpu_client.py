@@ -1,0 +1,125 @@
+# SPDX-License-Identifier: Apache-2.0
+"""GPU client side against the reference library (oracle/_ref):
+
+* encrypt_tensor (henet/graph.hpp:68-91): ciphertext words bit-exact for real and
+  complex packing, both through the counter-mode ChaCha20 sampler and through the serial
+  stream walk that handles rejections (HG_ENC_SERIAL=1 forces it for every ciphertext).
+* decrypt (henet/ckks.hpp:256-268): plaintext residues c0 + c1 s (+ c2 s^2), exact.
+* decrypt_tensor (henet/graph.hpp:93-103): decoded values within 1e-9 of the reference's
+  (the decoder's long double CRT conversion is done in double here), on fresh encryptions,
+  on size-3 ciphertexts and on a network's output."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import refbind as R
+from paper_1908_04172_b200 import henet as H
+from paper_1908_04172_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    p = W.N8192
+    ctx = H.CkksContext(p["n"], p["chain"], p["special"], p["scale"])
+    ref = R.RefContext(p["n"], p["chain"], p["special"], p["scale"])
+    keys = ref.keygen(31, True)
+    sk = H.SecretKey(ctx, keys.sk_words())
+    return dict(p=p, ctx=ctx, ref=ref, keys=keys, sk=sk)
+
+
+@pytest.mark.parametrize("packing,batch,count,serial", [(0, 4096, 12, False), (1, 8192, 7, False),
+                                                        (0, 1000, 3, True), (1, 2, 2, True), (0, 1, 1, False)])
+def test_encrypt_tensor_bit_exact(env, packing, batch, count, serial):
+    ctx, ref, keys, sk = env["ctx"], env["ref"], env["keys"], env["sk"]
+    rng = np.random.default_rng(batch + count)
+    samples = rng.uniform(-1, 1, (batch, count))
+    want, wsc = ref.encrypt_tensor(keys, samples, 1234 + count, packing=packing)
+    if serial:
+        os.environ["HG_ENC_SERIAL"] = "1"
+    try:
+        got = H.encrypt_tensor(ctx, sk, samples, 1234 + count, packing)
+    finally:
+        os.environ.pop("HG_ENC_SERIAL", None)
+    assert got.scale == wsc
+    assert np.array_equal(got.to_words(), want)
+
+
+def test_encrypt_rejects_like_reference(env):
+    ctx, sk = env["ctx"], env["sk"]
+    with pytest.raises(H.ValidationError, match="batch exceeds slot capacity"):
+        H.encrypt_tensor(ctx, sk, np.zeros((4097, 1)), 1, 0)
+    with pytest.raises(H.ValidationError, match="complex packing needs an even batch"):
+        H.encrypt_tensor(ctx, sk, np.zeros((3, 1)), 1, 1)
+    with pytest.raises(H.ValidationError, match="exceeds q_level/2|too large"):
+        H.encrypt_tensor(ctx, sk, np.full((4, 1), 1e30), 1, 0)
+
+
+def _decrypt_np(p, skw, words):
+    """m = c0 + c1 s (+ c2 s^2) mod q_i, the definition (henet/ckks.hpp:256-268)."""
+    cnt, polys, level, n = words.shape
+    q = np.array(p["chain"][:level], dtype=np.uint64)[:, None]
+    s = skw[:level]
+    m = (words[:, 0] + (words[:, 1] * s) % q) % q
+    if polys == 3:
+        m = (m + (words[:, 2] * ((s * s) % q)) % q) % q
+    return m
+
+
+def test_decrypt_residues_exact(env):
+    ctx, p, keys, sk = env["ctx"], env["p"], env["keys"], env["sk"]
+    skw = keys.sk_words()
+    for level, polys in ((6, 2), (3, 2), (5, 3), (1, 2)):
+        words = W.random_ciphertexts(p, 5, seed=level * 10 + polys, level=level)
+        if polys == 3:
+            words = np.concatenate([words, W.random_ciphertexts(p, 5, seed=99, level=level)[:, :1]], axis=1)
+        t = H.CipherTensor.from_words(ctx, words, 2.0 ** 30)
+        assert np.array_equal(H.decrypt(ctx, sk, t), _decrypt_np(p, skw, words))
+
+
+@pytest.mark.parametrize("packing,batch", [(0, 4096), (1, 8192), (0, 10)])
+def test_decrypt_tensor_fresh_vs_reference(env, packing, batch):
+    ctx, ref, keys, sk = env["ctx"], env["ref"], env["keys"], env["sk"]
+    samples = np.random.default_rng(batch).uniform(-2, 2, (max(batch, 2), 6))
+    words, sc = ref.encrypt_tensor(keys, samples, 77, packing=packing)
+    t = H.CipherTensor.from_words(ctx, words, sc, packing=packing)
+    got = H.decrypt_tensor(ctx, sk, t, batch)
+    want = ref.decrypt_tensor(keys, words, sc, packing, batch)
+    assert np.abs(got - want).max() < 1e-9
+    assert np.abs(got - samples[:batch]).max() < 1e-3
+
+
+def test_decrypt_tensor_network_output_and_size3(env):
+    ctx, ref, keys, sk, p = env["ctx"], env["ref"], env["keys"], env["sk"], env["p"]
+    wl = W.toy_cryptonets()
+    imgs = W.synthetic_images(wl.input_shape, wl.batch, 5)
+    words, sc = ref.encrypt_tensor(keys, imgs, 9)
+    out_w, out_sc, _ = ref.execute(keys, wl.manifest, wl.blob, words, sc)
+    t = H.CipherTensor.from_words(ctx, out_w, out_sc)
+    got = H.decrypt_tensor(ctx, sk, t, wl.batch)
+    want = ref.decrypt_tensor(keys, out_w, out_sc, 0, wl.batch)
+    assert np.abs(got - want).max() < 1e-9
+    # size-3 (square without relinearisation) at level 6
+    sq, sq_sc = ref.square(words[:3], sc)
+    t3 = H.CipherTensor.from_words(ctx, sq, sq_sc)
+    got3 = H.decrypt_tensor(ctx, sk, t3, wl.batch)
+    want3 = ref.decrypt_tensor(keys, sq, sq_sc, 0, wl.batch)
+    assert np.abs(got3 - want3).max() < 1e-9
+
+
+def test_encrypt_execute_decrypt_on_gpu(env):
+    """The whole client-server-client loop on the GPU vs the reference's plaintext logits."""
+    ctx, ref, keys, sk = env["ctx"], env["ref"], env["keys"], env["sk"]
+    wl = W.toy_cryptonets()
+    imgs = W.synthetic_images(wl.input_shape, wl.batch, 6)
+    rk = H.RelinKey(ctx, keys.rk_words())
+    x = H.encrypt_tensor(ctx, sk, imgs, 11, shape=wl.input_shape)
+    model = H.PlainModel.load(wl.manifest, wl.blob)
+    out = H.execute(ctx, model, H.RescalePlan.plan(ctx, model), x, rk)
+    got = H.decrypt_tensor(ctx, sk, out, wl.batch)
+    words, sc = ref.encrypt_tensor(keys, imgs, 11)
+    out_w, out_sc, _ = ref.execute(keys, wl.manifest, wl.blob, words, sc)
+    assert np.array_equal(out.to_words(), out_w)
+    assert np.abs(got - ref.decrypt_tensor(keys, out_w, out_sc, 0, wl.batch)).max() < 1e-9
