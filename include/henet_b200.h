@@ -278,6 +278,16 @@ int hg_execute(hg_ctx* ctx, const hg_model* m, const hg_plan* plan, const hg_ten
                const hg_relin_key* rk, hg_nonlin_fn provider, void* provider_user,
                hg_tensor** output, hg_exec_stats* stats, void* stream);
 
+/* NonlinearityEngine / LocalProvider (henet/graph.hpp:699-752) on the GPU: decrypt and
+ * decode every request ciphertext, ReLU or the per-slot window max, encode_vector at the
+ * top level and default scale, encrypt with derive_seed(derive_seed(seed, layer_seq), g).
+ * Pass hg_refresh_engine_apply as hg_execute's provider with the engine as provider_user. */
+typedef struct hg_refresh_engine hg_refresh_engine;
+int hg_refresh_engine_create(hg_ctx* ctx, const hg_secret_key* sk, uint64_t seed, hg_refresh_engine** out);
+void hg_refresh_engine_destroy(hg_refresh_engine* e);
+int hg_refresh_engine_apply(void* engine, int kind, uint32_t window, uint32_t layer_seq,
+                            const hg_tensor* request, hg_tensor* response);
+
 /* ------------------------------------------------------------------ */
 /* Measurement helpers (not part of the reference surface)             */
 /* ------------------------------------------------------------------ */

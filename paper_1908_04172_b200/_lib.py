@@ -96,6 +96,9 @@ PROTOTYPES = {
     "hg_encrypt_tensor": (C.c_int, [vp, vp, vp, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int, vp, vp]),
     "hg_decrypt": (C.c_int, [vp, vp, vp, vp, vp]),
     "hg_decrypt_tensor": (C.c_int, [vp, vp, vp, C.c_uint32, vp, vp]),
+    "hg_refresh_engine_create": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(vp)]),
+    "hg_refresh_engine_destroy": (None, [vp]),
+    "hg_refresh_engine_apply": (C.c_int, [vp, C.c_int, C.c_uint32, C.c_uint32, vp, vp]),
     "hg_model_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
     "hg_model_destroy": (None, [vp]),
     "hg_model_add_weight": (C.c_int, [vp, C.c_char_p, u32p, C.c_uint32, vp]),

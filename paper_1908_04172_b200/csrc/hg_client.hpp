@@ -34,7 +34,8 @@ struct DecArgs {
   const u32* sk;    // [full][N]
   u32* m;           // [count][level][N]: decrypted plaintext residues
   double* coeffs;   // [count][N] (nullptr: residues only)
-  double inv_scale;
+  u64 inv_mant;     // 1.0L / scale as an x87 long double: inv_mant * 2^inv_exp (host-computed)
+  int inv_exp;
   CrtTables crt;
   u32 count, polys, level, N, words;
 };
@@ -46,5 +47,8 @@ int launch_enc_combine(const EncArgs& a, const Basis& B, cudaStream_t s);
 // into slots [count][N/2][2]
 int launch_dec(const DecArgs& a, int logn, const Basis& B, const double2* roots, const double2* twist,
                double2* scratch, double* slots, cudaStream_t s);
+// NonlinearityEngine::apply's per-slot function (henet/graph.hpp:714-731): slots
+// [groups * window][N/2][2] -> [groups][N/2][2]; kind 1 = ReLU (window 1), 2 = max.
+int launch_refresh_slots(const double* in, double* out, u32 groups, u32 window, u32 half, int kind, cudaStream_t s);
 
 }  // namespace hg

@@ -2301,6 +2301,54 @@ u64 mw_mod(const std::vector<u64>& x, u64 q) {
 void check_client_ctx(const Context& c) {
   if (c.wide) throw Error(HG_ERR_UNSUPPORTED, "GPU encrypt/decrypt with primes >= 2^30 is not implemented yet");
 }
+
+// encrypt (henet/ckks.hpp:229-248) of `count` encoded top-level plaintexts [count][L][N]:
+// ciphertext e draws from derive_seed(seed, e), stream 1 (encrypt_tensor's per-element
+// seeds, and NonlinearityEngine's per-group seeds with seed = derive_seed(seed, layer)).
+CtBatch encrypt_pts(const Context& c, const hg_secret_key* sk, const BufPtr& pt, u64 count, u64 seed, int packing,
+                    cudaStream_t s) {
+    const u32 L = static_cast<u32>(c.chain_len()), N = c.n;
+    CtBatch o;
+    o.packing = packing;
+    o.scale = c.default_scale;
+    ensure(c, o, count, 2, L, s);
+    BufPtr err = c.alloc(count * L * static_cast<u64>(N) * 4, s);
+    BufPtr flags = c.alloc(count * sizeof(int), s);
+    cuda_check(cudaMemsetAsync(flags->ptr, 0, count * sizeof(int), s), "memset");
+    EncArgs a{};
+    a.ct = o.data();
+    a.err = static_cast<u32*>(err->ptr);
+    a.pt = static_cast<const u32*>(pt->ptr);
+    a.sk = static_cast<const u32*>(sk->s->ptr);
+    a.flags = static_cast<int*>(flags->ptr);
+    a.seed = seed;
+    for (u32 i = 0; i < L; ++i) a.thr[i] = (0 - c.chain[i]) % c.chain[i];  // next_below threshold
+    a.count = static_cast<u32>(count);
+    a.level = L;
+    a.N = N;
+    check_launch(launch_enc_sample(a, c.basis, s), "encrypt sample");
+    // draws the counter-mode pass could not place (a rejection, u1 == 0): regenerate those
+    // ciphertexts by walking their streams; HG_ENC_SERIAL=1 walks every stream (tests)
+    std::vector<int> hf(count);
+    cuda_check(cudaMemcpyAsync(hf.data(), flags->ptr, count * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaStreamSynchronize(s), "encrypt");
+    const char* ser = getenv("HG_ENC_SERIAL");
+    const bool all = ser != nullptr && ser[0] == '1';
+    std::vector<u32> list;
+    for (u64 e = 0; e < count; ++e)
+      if (all || hf[e]) list.push_back(static_cast<u32>(e));
+    BufPtr dl;
+    if (!list.empty()) {
+      dl = c.alloc(list.size() * 4, s);
+      cuda_check(cudaMemcpyAsync(dl->ptr, list.data(), list.size() * 4, cudaMemcpyHostToDevice, s), "h2d");
+      check_launch(launch_enc_serial(a, static_cast<const u32*>(dl->ptr), static_cast<u32>(list.size()), c.basis, s),
+                   "encrypt serial");
+    }
+    check_launch(launch_ntt(static_cast<int>(c.logn), a.err, count * L, L, false, c.basis, s), "ntt");
+    check_launch(launch_enc_combine(a, c.basis, s), "encrypt combine");
+    cuda_check(cudaStreamSynchronize(s), "encrypt");
+    return o;
+}
 }  // namespace
 
 int hg_secret_key_upload(hg_ctx* ctx, const uint64_t* words, uint64_t n_words, hg_secret_key** out) {
@@ -2360,47 +2408,8 @@ int hg_encrypt_tensor(hg_ctx* ctx, const hg_secret_key* sk, const double* sample
     std::vector<int> ex;
     BufPtr pt = encode_vectors_dev(c, static_cast<const double*>(ds->ptr), n_slots, count, L, c.default_scale, s, mant, ex);
 
-    CtBatch o;
-    o.packing = packing;
-    o.scale = c.default_scale;
-    ensure(c, o, count, 2, L, s);
-    o.shape = {static_cast<u32>(count)};
-    BufPtr err = c.alloc(count * L * static_cast<u64>(N) * 4, s);
-    BufPtr flags = c.alloc(count * sizeof(int), s);
-    cuda_check(cudaMemsetAsync(flags->ptr, 0, count * sizeof(int), s), "memset");
-    EncArgs a{};
-    a.ct = o.data();
-    a.err = static_cast<u32*>(err->ptr);
-    a.pt = static_cast<const u32*>(pt->ptr);
-    a.sk = static_cast<const u32*>(sk->s->ptr);
-    a.flags = static_cast<int*>(flags->ptr);
-    a.seed = seed;
-    for (u32 i = 0; i < L; ++i) a.thr[i] = (0 - c.chain[i]) % c.chain[i];  // next_below threshold
-    a.count = static_cast<u32>(count);
-    a.level = L;
-    a.N = N;
-    check_launch(launch_enc_sample(a, c.basis, s), "encrypt sample");
-    // draws the counter-mode pass could not place (a rejection, u1 == 0): regenerate those
-    // ciphertexts by walking their streams; HG_ENC_SERIAL=1 walks every stream (tests)
-    std::vector<int> hf(count);
-    cuda_check(cudaMemcpyAsync(hf.data(), flags->ptr, count * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
-    cuda_check(cudaStreamSynchronize(s), "encrypt");
-    const char* ser = getenv("HG_ENC_SERIAL");
-    const bool all = ser != nullptr && ser[0] == '1';
-    std::vector<u32> list;
-    for (u64 e = 0; e < count; ++e)
-      if (all || hf[e]) list.push_back(static_cast<u32>(e));
-    BufPtr dl;
-    if (!list.empty()) {
-      dl = c.alloc(list.size() * 4, s);
-      cuda_check(cudaMemcpyAsync(dl->ptr, list.data(), list.size() * 4, cudaMemcpyHostToDevice, s), "h2d");
-      check_launch(launch_enc_serial(a, static_cast<const u32*>(dl->ptr), static_cast<u32>(list.size()), c.basis, s),
-                   "encrypt serial");
-    }
-    check_launch(launch_ntt(static_cast<int>(c.logn), a.err, count * L, L, false, c.basis, s), "ntt");
-    check_launch(launch_enc_combine(a, c.basis, s), "encrypt combine");
-    cuda_check(cudaStreamSynchronize(s), "encrypt");
-    out->b = o;
+    out->b = encrypt_pts(c, sk, pt, count, seed, packing, s);
+    out->b.shape = {static_cast<u32>(count)};
   });
 }
 
@@ -2416,6 +2425,47 @@ DecArgs dec_args(const Context& c, const hg_secret_key* sk, const CtBatch& ct) {
   a.level = ct.level;
   a.N = c.n;
   return a;
+}
+
+// decode_slots(decrypt(ct)) (henet/encoding.hpp:223-264, henet/ckks.hpp:256-268) of every
+// ciphertext of `b` on the GPU: slots [count][N/2][2] doubles, bit-exact.
+BufPtr decode_slots_dev(const Context& c, const hg_secret_key* sk, const CtBatch& b, cudaStream_t s) {
+    DecArgs a = dec_args(c, sk, b);
+    // CRT tables for this level (decode_slots, henet/encoding.hpp:226-243)
+    const u32 L = b.level;
+    std::vector<u64> big{1};
+    for (u32 i = 0; i < L; ++i) mw_mul_small(big, c.chain[i]);
+    require(big.size() <= static_cast<size_t>(kCrtWords), "modulus too large for the GPU decoder");
+    a.words = static_cast<u32>(big.size());
+    for (u32 k = 0; k < a.words; ++k) a.crt.big_q[k] = big[k];
+    for (u32 k = 0; k < a.words; ++k) a.crt.q_half[k] = (big[k] >> 1) | (k + 1 < a.words ? (big[k + 1] << 63) : 0);
+    for (u32 i = 0; i < L; ++i) {
+      std::vector<u64> qi{1};
+      for (u32 j = 0; j < L; ++j)
+        if (j != i) mw_mul_small(qi, c.chain[j]);
+      for (u32 k = 0; k < qi.size() && k < static_cast<size_t>(kCrtWords); ++k) a.crt.q_over_p[i][k] = qi[k];
+      a.crt.inv[i] = static_cast<u32>(nt::inv(mw_mod(qi, c.chain[i]), c.chain[i]));
+    }
+    {
+      // 1.0L / (long double)scale (decode_slots, henet/encoding.hpp:248), x87 on the host
+      const long double li = 1.0L / static_cast<long double>(b.scale);
+      int ex = 0;
+      const long double fr = std::frexp(li, &ex);  // li = fr * 2^ex, fr in [0.5, 1)
+      a.inv_mant = static_cast<u64>(std::ldexp(fr, 64));
+      a.inv_exp = ex - 64;
+    }
+    const u64 count = b.count, N = c.n;
+    BufPtr m = c.alloc(count * L * N * 4, s);
+    BufPtr co = c.alloc(count * N * sizeof(double), s);
+    BufPtr scratch = c.alloc(count * N * sizeof(double2), s);
+    BufPtr sl = c.alloc(count * N * sizeof(double), s);  // [count][N/2][2]
+    a.m = static_cast<u32*>(m->ptr);
+    a.coeffs = static_cast<double*>(co->ptr);
+    const double2* roots = static_cast<const double2*>(c.fft_tables->ptr);
+    check_launch(launch_dec(a, static_cast<int>(c.logn), c.basis, roots, roots + N / 2,
+                            static_cast<double2*>(scratch->ptr), static_cast<double*>(sl->ptr), s),
+                 "decrypt");
+    return sl;
 }
 }  // namespace
 
@@ -2445,7 +2495,6 @@ int hg_decrypt_tensor(hg_ctx* ctx, const hg_secret_key* sk, const hg_tensor* ct,
     check_client_ctx(c);
     cudaStream_t s = c.pick(stream);
     const CtBatch& b = ct->b;
-    DecArgs a = dec_args(c, sk, b);
     const u32 half = c.n / 2;
     if (b.packing == HG_PACKING_REAL) {
       require(batch <= half, "batch larger than decoded slots");
@@ -2453,33 +2502,8 @@ int hg_decrypt_tensor(hg_ctx* ctx, const hg_secret_key* sk, const hg_tensor* ct,
       require(batch % 2 == 0, "complex batch size must be even");
       require(batch / 2 <= half, "batch larger than decoded slots");
     }
-    // CRT tables for this level (decode_slots, henet/encoding.hpp:226-243)
-    const u32 L = b.level;
-    std::vector<u64> big{1};
-    for (u32 i = 0; i < L; ++i) mw_mul_small(big, c.chain[i]);
-    require(big.size() <= static_cast<size_t>(kCrtWords), "modulus too large for the GPU decoder");
-    a.words = static_cast<u32>(big.size());
-    for (u32 k = 0; k < a.words; ++k) a.crt.big_q[k] = big[k];
-    for (u32 k = 0; k < a.words; ++k) a.crt.q_half[k] = (big[k] >> 1) | (k + 1 < a.words ? (big[k + 1] << 63) : 0);
-    for (u32 i = 0; i < L; ++i) {
-      std::vector<u64> qi{1};
-      for (u32 j = 0; j < L; ++j)
-        if (j != i) mw_mul_small(qi, c.chain[j]);
-      for (u32 k = 0; k < qi.size() && k < static_cast<size_t>(kCrtWords); ++k) a.crt.q_over_p[i][k] = qi[k];
-      a.crt.inv[i] = static_cast<u32>(nt::inv(mw_mod(qi, c.chain[i]), c.chain[i]));
-    }
-    a.inv_scale = 1.0 / b.scale;
     const u64 count = b.count, N = c.n;
-    BufPtr m = c.alloc(count * L * N * 4, s);
-    BufPtr co = c.alloc(count * N * sizeof(double), s);
-    BufPtr scratch = c.alloc(count * N * sizeof(double2), s);
-    BufPtr sl = c.alloc(count * N * sizeof(double), s);  // [count][N/2][2]
-    a.m = static_cast<u32*>(m->ptr);
-    a.coeffs = static_cast<double*>(co->ptr);
-    const double2* roots = static_cast<const double2*>(c.fft_tables->ptr);
-    check_launch(launch_dec(a, static_cast<int>(c.logn), c.basis, roots, roots + N / 2,
-                            static_cast<double2*>(scratch->ptr), static_cast<double*>(sl->ptr), s),
-                 "decrypt");
+    BufPtr sl = decode_slots_dev(c, sk, b, s);
     std::vector<double> h(count * N);
     cuda_check(cudaMemcpyAsync(h.data(), sl->ptr, count * N * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
     cuda_check(cudaStreamSynchronize(s), "decrypt");
@@ -2496,5 +2520,70 @@ int hg_decrypt_tensor(hg_ctx* ctx, const hg_secret_key* sk, const hg_tensor* ct,
         }
       }
     }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// NonlinearityEngine (henet/graph.hpp:699-741) on the GPU: decrypt + decode, ReLU or
+// window max per slot, encode_vector at the top level, encrypt with
+// derive_seed(derive_seed(seed, layer_seq), group) -- a drop-in hg_nonlin_fn.
+// ---------------------------------------------------------------------------
+struct hg_refresh_engine {
+  std::shared_ptr<hg::Context> ctx;
+  const hg_secret_key* sk;
+  hg_secret_key sk_copy;
+  uint64_t seed;
+};
+
+namespace {
+u64 derive_seed_host(u64 seed, u64 tag) {  // henet/rng.hpp:101-106
+  u64 z = seed + 0x9e3779b97f4a7c15ULL * (tag + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+}  // namespace
+
+int hg_refresh_engine_create(hg_ctx* ctx, const hg_secret_key* sk, uint64_t seed, hg_refresh_engine** out) {
+  return guard([&] {
+    require(ctx && sk && out, "null argument");
+    check_client_ctx(*ctx->c);
+    auto* e = new hg_refresh_engine;
+    e->ctx = ctx->c;
+    e->sk_copy.ctx = sk->ctx;
+    e->sk_copy.s = sk->s;  // shares the device key
+    e->sk = &e->sk_copy;
+    e->seed = seed;
+    *out = e;
+  });
+}
+
+void hg_refresh_engine_destroy(hg_refresh_engine* e) { delete e; }
+
+int hg_refresh_engine_apply(void* engine, int kind, uint32_t window, uint32_t layer_seq, const hg_tensor* request,
+                            hg_tensor* response) {
+  return guard([&] {
+    require(engine && request && response, "null argument");
+    auto* eng = static_cast<hg_refresh_engine*>(engine);
+    const Context& c = *eng->ctx;
+    cudaStream_t s = c.core->stream;
+    const CtBatch& b = request->b;
+    require(window >= 1, "window must be at least 1");
+    require(b.count % window == 0, "ciphertext count is not a multiple of the window");
+    require(kind == HG_NONLIN_RELU || kind == HG_NONLIN_MAXPOOL, "unknown nonlinearity");
+    if (kind == HG_NONLIN_RELU) require(window == 1, "ReLU is element-wise");
+    const u64 groups = b.count / window;
+    const u32 half = c.n / 2;
+    BufPtr sl = decode_slots_dev(c, eng->sk, b, s);
+    BufPtr res = c.alloc(groups * half * 2 * sizeof(double), s);
+    check_launch(launch_refresh_slots(static_cast<const double*>(sl->ptr), static_cast<double*>(res->ptr),
+                                      static_cast<u32>(groups), window, half, kind, s),
+                 "refresh slots");
+    std::vector<unsigned long long> mant;
+    std::vector<int> ex;
+    BufPtr pt = encode_vectors_dev(c, static_cast<const double*>(res->ptr), half, groups,
+                                   static_cast<u32>(c.chain_len()), c.default_scale, s, mant, ex);
+    response->b = encrypt_pts(c, eng->sk, pt, groups, derive_seed_host(eng->seed, layer_seq), b.packing, s);
+    response->b.shape = {static_cast<u32>(groups)};
   });
 }

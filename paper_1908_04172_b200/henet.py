@@ -280,6 +280,34 @@ def decrypt_tensor(ctx: CkksContext, sk: SecretKey, ct: "CipherTensor", batch: i
     return out
 
 
+class RefreshEngine:
+    """NonlinearityEngine + LocalProvider (henet/graph.hpp:699-752) on the GPU: pass it as
+    execute()'s provider; the request never leaves the device."""
+
+    def __init__(self, ctx: CkksContext, sk: SecretKey, seed: int):
+        h = C.c_void_p()
+        check(lib.hg_refresh_engine_create(ctx.handle, sk.handle, seed, C.byref(h)))
+        self._h = h
+        self.ctx = ctx
+        self.sk = sk
+
+    def __del__(self):
+        if getattr(self, "_h", None) and lib is not None:
+            lib.hg_refresh_engine_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def apply(self, kind: int, window: int, layer_seq: int, request: "CipherTensor") -> "CipherTensor":
+        """NonlinearityEngine::apply on a device tensor; returns the fresh encryptions."""
+        out = CipherTensor(self.ctx, request.count // window, 2, len(self.ctx.chain), self.ctx.default_scale,
+                           request.info()[4])
+        check(lib.hg_refresh_engine_apply(self._h, kind, window, layer_seq, request.handle, out.handle))
+        return out
+
+
 def _empty_like(ctx: CkksContext, ct: CipherTensor) -> CipherTensor:
     return CipherTensor(ctx, 0, 2, 1, 1.0)
 
@@ -550,7 +578,7 @@ Provider = Callable[[int, int, int, CipherTensor], np.ndarray]
 
 
 def execute(ctx: CkksContext, model: PlainModel, plan: RescalePlan, inp: CipherTensor,
-            relin: Optional[RelinKey] = None, provider: Optional[Provider] = None,
+            relin: Optional[RelinKey] = None, provider: "Optional[Provider | RefreshEngine]" = None,
             stats: Optional[ExecutionStats] = None) -> CipherTensor:
     """execute, henet/graph.hpp:1121-1126 -- the whole graph on the GPU."""
     errors: List[BaseException] = []
@@ -571,10 +599,15 @@ def execute(ctx: CkksContext, model: PlainModel, plan: RescalePlan, inp: CipherT
             errors.append(e)
             return 1
 
-    cb = NONLIN_FN(_cb) if provider is not None else NONLIN_FN()
+    user = None
+    if isinstance(provider, RefreshEngine):  # native provider: hg_refresh_engine_apply on the engine
+        cb = C.cast(lib.hg_refresh_engine_apply, NONLIN_FN)
+        user = provider.handle
+    else:
+        cb = NONLIN_FN(_cb) if provider is not None else NONLIN_FN()
     out = C.c_void_p()
     st = hg_exec_stats()
-    rc = lib.hg_execute(ctx.handle, model.handle, plan.handle, inp.handle, relin.handle if relin else None, cb, None,
+    rc = lib.hg_execute(ctx.handle, model.handle, plan.handle, inp.handle, relin.handle if relin else None, cb, user,
                         C.byref(out), C.byref(st) if stats is not None else None, None)
     if errors:
         raise errors[0]

@@ -5,9 +5,12 @@
   complex packing, both through the counter-mode ChaCha20 sampler and through the serial
   stream walk that handles rejections (HG_ENC_SERIAL=1 forces it for every ciphertext).
 * decrypt (henet/ckks.hpp:256-268): plaintext residues c0 + c1 s (+ c2 s^2), exact.
-* decrypt_tensor (henet/graph.hpp:93-103): decoded values within 1e-9 of the reference's
-  (the decoder's long double CRT conversion is done in double here), on fresh encryptions,
-  on size-3 ciphertexts and on a network's output."""
+* decrypt_tensor (henet/graph.hpp:93-103): decoded values bit-exact (the decoder's x87
+  long double conversion is emulated), on fresh encryptions, on size-3 ciphertexts and on
+  a network's output.
+* NonlinearityEngine (henet/graph.hpp:699-741) on the GPU (RefreshEngine): refreshed
+  ciphertexts bit-exact for ReLU and window max, real and complex packing, and as the
+  provider of whole CryptoNets-ReLU executions."""
 import os
 
 import numpy as np
@@ -87,7 +90,7 @@ def test_decrypt_tensor_fresh_vs_reference(env, packing, batch):
     t = H.CipherTensor.from_words(ctx, words, sc, packing=packing)
     got = H.decrypt_tensor(ctx, sk, t, batch)
     want = ref.decrypt_tensor(keys, words, sc, packing, batch)
-    assert np.abs(got - want).max() < 1e-9
+    assert np.array_equal(got, want)
     assert np.abs(got - samples[:batch]).max() < 1e-3
 
 
@@ -100,13 +103,13 @@ def test_decrypt_tensor_network_output_and_size3(env):
     t = H.CipherTensor.from_words(ctx, out_w, out_sc)
     got = H.decrypt_tensor(ctx, sk, t, wl.batch)
     want = ref.decrypt_tensor(keys, out_w, out_sc, 0, wl.batch)
-    assert np.abs(got - want).max() < 1e-9
+    assert np.array_equal(got, want)
     # size-3 (square without relinearisation) at level 6
     sq, sq_sc = ref.square(words[:3], sc)
     t3 = H.CipherTensor.from_words(ctx, sq, sq_sc)
     got3 = H.decrypt_tensor(ctx, sk, t3, wl.batch)
     want3 = ref.decrypt_tensor(keys, sq, sq_sc, 0, wl.batch)
-    assert np.abs(got3 - want3).max() < 1e-9
+    assert np.array_equal(got3, want3)
 
 
 def test_encrypt_execute_decrypt_on_gpu(env):
@@ -122,4 +125,36 @@ def test_encrypt_execute_decrypt_on_gpu(env):
     words, sc = ref.encrypt_tensor(keys, imgs, 11)
     out_w, out_sc, _ = ref.execute(keys, wl.manifest, wl.blob, words, sc)
     assert np.array_equal(out.to_words(), out_w)
-    assert np.abs(got - ref.decrypt_tensor(keys, out_w, out_sc, 0, wl.batch)).max() < 1e-9
+    assert np.array_equal(got, ref.decrypt_tensor(keys, out_w, out_sc, 0, wl.batch))
+
+
+@pytest.mark.parametrize("kind,window,packing", [(1, 1, 0), (1, 1, 1), (2, 4, 0), (2, 9, 1)])
+def test_refresh_engine_bit_exact(env, kind, window, packing):
+    ctx, ref, keys, sk, p = env["ctx"], env["ref"], env["keys"], env["sk"], env["p"]
+    batch = 4096 if packing == 0 else 8192
+    samples = np.random.default_rng(window).uniform(-1, 1, (batch, 3 * window))
+    words, sc = ref.encrypt_tensor(keys, samples, 5, packing=packing)
+    # a rescaled product, like a layer output: scale != 2^24, level 5
+    res = ref.encode_scalar(0.75, 6, p["scale"])
+    prod, psc = ref.mul_ct_pt_scalar(words, sc, res, p["scale"], packing)
+    low, lsc = ref.rescale(prod, psc, 5, packing)
+    eng = H.RefreshEngine(ctx, sk, 1234)
+    for layer_seq in (0, 3):
+        want = ref.nonlin_apply(keys, kind, window, layer_seq, 1234, low, lsc, packing)
+        got = eng.apply(kind, window, layer_seq, H.CipherTensor.from_words(ctx, low, lsc, packing=packing))
+        assert np.array_equal(got.to_words(), want)
+
+
+@pytest.mark.parametrize("packing", [1, 0])
+def test_refresh_engine_as_provider_cryptonets_relu(env, packing):
+    """c3 (CryptoNets-ReLU, client-aided refresh) executed with the GPU engine as provider."""
+    ctx, ref, keys, sk = env["ctx"], env["ref"], env["keys"], env["sk"]
+    wl = W.cryptonets_relu(packing=packing, batch=8192 if packing else 4096)
+    imgs = W.synthetic_images(wl.input_shape, wl.batch, 8)
+    words, sc = ref.encrypt_tensor(keys, imgs, 9, packing=packing)
+    want, want_sc, _ = ref.execute(keys, wl.manifest, wl.blob, words, sc, refresh_seed=99)
+    model = H.PlainModel.load(wl.manifest, wl.blob)
+    inp = H.CipherTensor.from_words(ctx, words, sc, packing=packing, shape=wl.input_shape)
+    out = H.execute(ctx, model, H.RescalePlan.plan(ctx, model), inp, None, H.RefreshEngine(ctx, sk, 99))
+    assert out.scale == want_sc
+    assert np.array_equal(out.to_words(), want)
