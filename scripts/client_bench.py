@@ -41,3 +41,20 @@ print(f"encrypt_tensor 4096 x 784 (c2 batch): GPU {g_ms:.1f} ms, reference CPU (
       f"{r_ms:.1f} ms, {r_ms / g_ms:.1f}x; bit-exact")
 print(f"decrypt_tensor 10 logits x 4096: GPU {gd_ms:.2f} ms, reference CPU (1 thread, its decrypt_tensor is serial) "
       f"{rd_ms:.1f} ms, {rd_ms / gd_ms:.1f}x")
+
+# c3: CryptoNets-ReLU under complex packing (8192 images), client-aided ReLU refreshes --
+# GPU engine as the provider vs the reference's execute with its LocalProvider (host threads)
+wl = Wk.cryptonets_relu()
+imgs3 = Wk.synthetic_images(wl.input_shape, wl.batch, 8)
+words3, sc3 = ref.encrypt_tensor(keys, imgs3, 9, packing=1)
+model = H.PlainModel.load(wl.manifest, wl.blob)
+plan = H.RescalePlan.plan(ctx, model)
+inp = H.CipherTensor.from_words(ctx, words3, sc3, packing=1, shape=wl.input_shape)
+eng = H.RefreshEngine(ctx, sk, 99)
+H.execute(ctx, model, plan, inp, None, eng)
+g3_ms, out3 = best(lambda: H.execute(ctx, model, plan, inp, None, eng), 3)
+r3_ms, (want3, _, _) = best(lambda: ref.execute(keys, wl.manifest, wl.blob, words3, sc3, refresh_seed=99), 1)
+assert np.array_equal(out3.to_words(), want3)
+print(f"c3 execute with client-aided ReLU refreshes (8192 images): GPU {g3_ms:.1f} ms "
+      f"({8192 / g3_ms * 1e3:.0f} img/s), reference CPU ({os.cpu_count()} threads) {r3_ms:.0f} ms "
+      f"({8192 / r3_ms * 1e3:.0f} img/s), {r3_ms / g3_ms:.0f}x; bit-exact")
