@@ -120,6 +120,16 @@ int hg_tensor_get_shape(const hg_tensor* t, uint32_t* dims, uint32_t* ndims /* i
  * checked < q_limb on upload, like deserialize_ciphertext (henet/serialize.hpp:66-77). */
 int hg_tensor_upload(hg_tensor* t, const uint64_t* words, void* stream);
 int hg_tensor_download(const hg_tensor* t, uint64_t* words, void* stream);
+/* Wire format (put_tensor / get_tensor, henet/protocol.hpp:335-358, around
+ * serialize_ciphertext, henet/serialize.hpp:95-124): u8 ndims, u32 dims, u32 count, then
+ * per ciphertext u64 length + "NGH2" header + moduli + little-endian u64 residues.
+ * Deserialisation validates every header and residue like deserialize_ciphertext (same
+ * messages) and packs the words straight into a new device tensor; every element must share
+ * level, size, packing and scale (HG_ERR_UNSUPPORTED otherwise).  *consumed = bytes read. */
+int hg_tensor_deserialize(hg_ctx* ctx, const uint8_t* bytes, uint64_t len, uint64_t* consumed,
+                          hg_tensor** out, void* stream);
+uint64_t hg_tensor_serialized_size(const hg_tensor* t);
+int hg_tensor_serialize(const hg_tensor* t, uint8_t* out, uint64_t cap, void* stream);
 /* Same, in the device's compact u32 word order (no widening). */
 int hg_tensor_upload_u32(hg_tensor* t, const uint32_t* words, void* stream);
 int hg_tensor_download_u32(const hg_tensor* t, uint32_t* words, void* stream);

@@ -444,4 +444,40 @@ int ref_nonlin_apply(void* c, void* k, int kind, uint32_t window, uint32_t layer
   });
 }
 
+// Wire format (test fixture side): detail::put_tensor / get_tensor, henet/protocol.hpp:335-358.
+int ref_put_tensor(void* c, const uint64_t* words, uint64_t count, uint32_t polys, uint32_t level, double scale,
+                   int packing, const uint32_t* dims, uint32_t ndims, uint8_t* out, uint64_t cap, uint64_t* out_len) {
+  return guard([&] {
+    auto& ctx = *static_cast<RefCtx*>(c)->ctx;
+    CipherTensor t;
+    for (uint32_t i = 0; i < ndims; ++i) t.shape.dims.push_back(dims[i]);
+    t.elems = cts_from(ctx, words, count, polys, level, scale, packing);
+    std::vector<u8> bytes;
+    detail::put_tensor(bytes, ctx, t);
+    *out_len = bytes.size();
+    if (out != nullptr) {
+      require(cap >= bytes.size(), "buffer too small");
+      std::memcpy(out, bytes.data(), bytes.size());
+    }
+  });
+}
+
+int ref_get_tensor(void* c, const uint8_t* bytes, uint64_t len, uint64_t* out_words, uint64_t cap_words,
+                   uint64_t* count, uint32_t* polys, uint32_t* level, double* scale) {
+  return guard([&] {
+    auto& ctx = *static_cast<RefCtx*>(c)->ctx;
+    ByteReader in(bytes, len);
+    CipherTensor t = detail::get_tensor(in, ctx);
+    *count = t.elems.size();
+    *polys = static_cast<uint32_t>(t.elems[0].size());
+    *level = static_cast<uint32_t>(t.elems[0].level());
+    *scale = t.elems[0].scale;
+    u64 need = 0;
+    for (const auto& ct : t.elems)
+      for (const auto& p : ct.polys) need += p.words().size();
+    require(need <= cap_words, "buffer too small");
+    cts_to(t.elems, out_words);
+  });
+}
+
 }  // extern "C"

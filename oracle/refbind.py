@@ -62,6 +62,10 @@ _PROTOS = {
                               C.c_uint, C.c_uint64, vp, C.c_uint64, u64p, C.POINTER(C.c_uint32),
                               C.POINTER(C.c_double), C.POINTER(C.c_double), u64p, u64p]),
     "ref_set_relu_clip": (None, [C.c_double]),
+    "ref_put_tensor": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_double, C.c_int, vp, C.c_uint32,
+                                 vp, C.c_uint64, u64p]),
+    "ref_get_tensor": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, u64p, C.POINTER(C.c_uint32),
+                                 C.POINTER(C.c_uint32), C.POINTER(C.c_double)]),
     "ref_nonlin_apply": (C.c_int, [vp, vp, C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, vp, C.c_uint64, C.c_uint32,
                                    C.c_double, C.c_int, vp]),
 }
@@ -245,6 +249,30 @@ class RefContext:
         n_words = oc.value * 2 * ol.value * self.n
         res = out[:n_words].reshape(oc.value, 2, ol.value, self.n).copy()
         return res, osc.value, dict(exec_ms=ms.value, rescale_ops=rs.value, relin_ops=rl.value)
+
+    def put_tensor(self, words, scale, packing=0, dims=None) -> bytes:
+        """detail::put_tensor (henet/protocol.hpp:335-344): the wire bytes of a CipherTensor."""
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        count, polys, level, _ = w.shape
+        d = np.ascontiguousarray(dims if dims is not None else [count], dtype=np.uint32)
+        n = C.c_uint64()
+        _chk(lib().ref_put_tensor(self._h, _p(w), count, polys, level, scale, packing, _p(d), d.size, None, 0,
+                                  C.byref(n)))
+        out = np.empty(n.value, dtype=np.uint8)
+        _chk(lib().ref_put_tensor(self._h, _p(w), count, polys, level, scale, packing, _p(d), d.size, _p(out),
+                                  out.size, C.byref(n)))
+        return out.tobytes()
+
+    def get_tensor(self, data: bytes):
+        """detail::get_tensor (henet/protocol.hpp:346-358) -> (words, scale)."""
+        b = np.frombuffer(data, dtype=np.uint8)
+        cap = b.size // 8 + 1
+        out = np.empty(cap, dtype=np.uint64)
+        cnt, polys, level, sc = C.c_uint64(), C.c_uint32(), C.c_uint32(), C.c_double()
+        _chk(lib().ref_get_tensor(self._h, _p(b), b.size, _p(out), cap, C.byref(cnt), C.byref(polys), C.byref(level),
+                                  C.byref(sc)))
+        nw = cnt.value * polys.value * level.value * self.n
+        return out[:nw].reshape(cnt.value, polys.value, level.value, self.n).copy(), sc.value
 
     def nonlin_apply(self, keys, kind, window, layer_seq, refresh_seed, words, scale, packing):
         w = np.ascontiguousarray(words, dtype=np.uint64)

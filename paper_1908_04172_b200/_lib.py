@@ -97,6 +97,9 @@ PROTOTYPES = {
     "hg_decrypt": (C.c_int, [vp, vp, vp, vp, vp]),
     "hg_decrypt_tensor": (C.c_int, [vp, vp, vp, C.c_uint32, vp, vp]),
     "hg_refresh_engine_create": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(vp)]),
+    "hg_tensor_deserialize": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(vp), vp]),
+    "hg_tensor_serialized_size": (C.c_uint64, [vp]),
+    "hg_tensor_serialize": (C.c_int, [vp, vp, C.c_uint64, vp]),
     "hg_refresh_engine_destroy": (None, [vp]),
     "hg_refresh_engine_apply": (C.c_int, [vp, C.c_int, C.c_uint32, C.c_uint32, vp, vp]),
     "hg_model_create": (C.c_int, [C.c_int, C.POINTER(vp)]),

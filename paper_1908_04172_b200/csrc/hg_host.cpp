@@ -2587,3 +2587,156 @@ int hg_refresh_engine_apply(void* engine, int kind, uint32_t window, uint32_t la
     response->b.shape = {static_cast<u32>(groups)};
   });
 }
+
+// ---------------------------------------------------------------------------
+// Wire format: put_tensor / get_tensor (henet/protocol.hpp:335-358)
+// around serialize_ciphertext / deserialize_ciphertext (henet/serialize.hpp:95-124).
+// Deserialisation parses the headers on the host and packs the residue words straight
+// from the message into the device layout (the upload path of hg_tensor_upload, one
+// segment per ciphertext), so a received request never becomes a host CipherTensor.
+// ---------------------------------------------------------------------------
+static_assert(__BYTE_ORDER__ == __ORDER_LITTLE_ENDIAN__, "the wire words are little-endian u64");
+
+namespace {
+struct WireReader {  // ByteReader, henet/common.hpp:90-122
+  const uint8_t* d;
+  u64 n, pos = 0;
+  const uint8_t* take(u64 k) {
+    if (pos + k > n) throw Error(HG_ERR_VALIDATION, "serialized data truncated");
+    const uint8_t* p = d + pos;
+    pos += k;
+    return p;
+  }
+  uint8_t u8v() { return take(1)[0]; }
+  u32 u32v() {
+    const uint8_t* p = take(4);
+    return static_cast<u32>(p[0]) | static_cast<u32>(p[1]) << 8 | static_cast<u32>(p[2]) << 16 |
+           static_cast<u32>(p[3]) << 24;
+  }
+  u64 u64v() {
+    const uint8_t* p = take(8);
+    u64 v = 0;
+    for (int i = 7; i >= 0; --i) v = (v << 8) | p[i];
+    return v;
+  }
+};
+constexpr u64 kWireHeader = 20;  // magic 4 | version 1 | N 4 | level 1 | packing 1 | scale 8 | polys 1
+void put_le(uint8_t*& o, u64 v, int bytes) {
+  for (int i = 0; i < bytes; ++i) *o++ = static_cast<uint8_t>(v >> (8 * i));
+}
+}  // namespace
+
+int hg_tensor_deserialize(hg_ctx* ctx, const uint8_t* bytes, uint64_t len, uint64_t* consumed, hg_tensor** out,
+                          void* stream) {
+  return guard([&] {
+    require(ctx && bytes && out, "null argument");
+    const Context& c = *ctx->c;
+    cudaStream_t s = c.pick(stream);
+    WireReader in{bytes, len};
+    std::vector<u32> dims(in.u8v());
+    for (auto& d : dims) d = in.u32v();
+    const u32 count = in.u32v();
+    u64 elems = 1;
+    for (u32 d : dims) elems *= d;
+    require(count == elems, "tensor element count mismatch");
+    require(count >= 1, "tensor must be non-empty");
+    std::vector<const uint8_t*> segs(count);
+    u32 level = 0, polys = 0;
+    int packing = 0;
+    double scale = 0;
+    for (u32 e = 0; e < count; ++e) {
+      const u64 ct_len = in.u64v();
+      WireReader r{in.take(ct_len), ct_len};
+      if (std::memcmp(r.take(4), "NGH2", 4) != 0) throw Error(HG_ERR_VALIDATION, "bad magic");
+      if (r.u8v() != 1) throw Error(HG_ERR_VALIDATION, "unsupported wire version");
+      const u32 degree = r.u32v();
+      const u32 lv = r.u8v();
+      const u32 pk = r.u8v();
+      const u64 sbits = r.u64v();
+      double sc;
+      std::memcpy(&sc, &sbits, 8);
+      const u32 pc = r.u8v();
+      std::vector<u64> moduli(lv);
+      for (auto& q : moduli) q = r.u64v();
+      // check_moduli_prefix + deserialize_ciphertext's checks, in the reference's order
+      require(degree == c.n, "degree does not match the context");
+      require(lv >= 1 && lv <= c.chain_len(), "level outside the context chain");
+      for (u32 i = 0; i < lv; ++i) require(moduli[i] == c.chain[i], "modulus list does not match the context");
+      require(pc == 2 || pc == 3, "ciphertext must have 2 or 3 polynomials");
+      require(pk <= 1, "unknown packing mode");
+      require(sc > 0.0, "scale must be positive");
+      segs[e] = r.take(static_cast<u64>(pc) * lv * c.n * 8);
+      if (e == 0) {
+        level = lv;
+        polys = pc;
+        packing = static_cast<int>(pk);
+        scale = sc;
+      } else if (lv != level || pc != polys || static_cast<int>(pk) != packing || sc != scale) {
+        throw Error(HG_ERR_UNSUPPORTED, "device tensors carry one level, size, packing and scale for all elements");
+      }
+    }
+    auto* t = new hg_tensor;
+    std::unique_ptr<hg_tensor> guard_t(t);
+    t->ctx = ctx->c;
+    t->b.scale = scale;
+    t->b.packing = packing;
+    ensure(c, t->b, count, polys, level, s);
+    t->b.shape = dims;
+    const u64 seg_words = static_cast<u64>(polys) * level * c.n;
+    if (!c.wide && host_narrow_enabled()) {
+      require(host_narrow_upload(c.core->device, nullptr, t->b.data(), seg_words * count, level, c.n,
+                                 c.chain.data(), s, segs.data(), seg_words),
+              "residue out of range");
+    } else {
+      std::vector<u64> w(seg_words * count);
+      for (u32 e = 0; e < count; ++e) std::memcpy(&w[e * seg_words], segs[e], seg_words * 8);
+      const int rc = hg_tensor_upload(t, w.data(), stream);
+      if (rc != HG_OK) throw Error(rc, g_last_error);
+    }
+    if (consumed) *consumed = in.pos;
+    *out = guard_t.release();
+  });
+}
+
+uint64_t hg_tensor_serialized_size(const hg_tensor* t) {
+  if (!t) return 0;
+  const u64 ct = kWireHeader + 8ull * t->b.level + 8ull * t->b.polys * t->b.level * t->ctx->n;
+  return 1 + 4ull * t->b.shape.size() + 4 + t->b.count * (8 + ct);
+}
+
+int hg_tensor_serialize(const hg_tensor* t, uint8_t* out, uint64_t cap, void* stream) {
+  return guard([&] {
+    require(t && out, "null argument");
+    const Context& c = *t->ctx;
+    require(cap >= hg_tensor_serialized_size(t), "output buffer too small");
+    const CtBatch& b = t->b;
+    u64 elems = 1;
+    for (u32 d : b.shape) elems *= d;
+    require(elems == b.count, "tensor element count mismatch");
+    const u64 seg_words = static_cast<u64>(b.polys) * b.level * c.n;
+    std::vector<u64> w(seg_words * b.count);
+    const int rc = hg_tensor_download(t, w.data(), stream);
+    if (rc != HG_OK) throw Error(rc, g_last_error);
+    uint8_t* o = out;
+    put_le(o, b.shape.size(), 1);
+    for (u32 d : b.shape) put_le(o, d, 4);
+    put_le(o, b.count, 4);
+    const u64 ct_len = kWireHeader + 8ull * b.level + 8 * seg_words;
+    u64 sbits;
+    std::memcpy(&sbits, &b.scale, 8);
+    for (u64 e = 0; e < b.count; ++e) {
+      put_le(o, ct_len, 8);
+      std::memcpy(o, "NGH2", 4);
+      o += 4;
+      put_le(o, 1, 1);
+      put_le(o, c.n, 4);
+      put_le(o, b.level, 1);
+      put_le(o, static_cast<u64>(b.packing), 1);
+      put_le(o, sbits, 8);
+      put_le(o, b.polys, 1);
+      for (u32 i = 0; i < b.level; ++i) put_le(o, c.chain[i], 8);
+      std::memcpy(o, &w[e * seg_words], seg_words * 8);
+      o += seg_words * 8;
+    }
+  });
+}

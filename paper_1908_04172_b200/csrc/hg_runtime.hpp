@@ -38,7 +38,8 @@ void cuda_check(cudaError_t e, const char* what);
 // threads and DMA'd chunk by chunk (HG_UPLOAD_HOST_NARROW=0: copy u64, narrow on the GPU).
 bool host_narrow_enabled();
 bool host_narrow_upload(int device, const uint64_t* words, uint32_t* dst, uint64_t n_words, uint32_t level,
-                        uint32_t N, const uint64_t* chain, cudaStream_t s);
+                        uint32_t N, const uint64_t* chain, cudaStream_t s, const uint8_t* const* segs = nullptr,
+                        uint64_t seg_words = 0);
 
 // Shared device state: the stream and device; kept alive by every buffer.
 struct DeviceCore {

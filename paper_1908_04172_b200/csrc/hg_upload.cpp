@@ -155,9 +155,11 @@ bool host_narrow_enabled() {
 }
 
 // words: [count][polys][level][N] u64 (reference order) -> dst (device, u32, same order).
+// With segs != nullptr the words come from n_words / seg_words separate, possibly unaligned
+// segments (one serialized ciphertext each) instead of `words`.
 // Returns false if some word is not below its limb's prime; dst is then unspecified.
 bool host_narrow_upload(int device, const u64* words, u32* dst, u64 n_words, u32 level, u32 N, const u64* chain,
-                        cudaStream_t s) {
+                        cudaStream_t s, const uint8_t* const* segs, u64 seg_words) {
   Workers& W = workers(device);
   std::lock_guard<std::mutex> g(W.mu);
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
@@ -183,7 +185,11 @@ bool host_narrow_upload(int device, const u64* words, u32* dst, u64 n_words, u32
         u32* out = W.stage[ei];
         const u64 b = c * kChunkWords, e = std::min(n_words, b + kChunkWords);
         for (u64 r = b; r < e; r += N) {  // one limb run of N words: a single prime
-          my_bad |= !pack_run(words + r, out + (r - b), N, static_cast<u32>(chain[(r / N) % level]));
+          // source run: contiguous words, or word (r % seg_words) of segment r / seg_words
+          const u64* src = segs == nullptr
+                               ? words + r
+                               : reinterpret_cast<const u64*>(segs[r / seg_words] + (r % seg_words) * 8);
+          my_bad |= !pack_run(src, out + (r - b), N, static_cast<u32>(chain[(r / N) % level]));
         }
         _mm_sfence();  // the streaming stores are visible before the DMA reads the chunk
         cuda_check(cudaMemcpyAsync(dst + b, out, (e - b) * 4, cudaMemcpyHostToDevice, ws), "h2d");

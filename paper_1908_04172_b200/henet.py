@@ -172,6 +172,21 @@ class CipherTensor:
         check(lib.hg_tensor_download(self._h, _ptr(out), None))
         return out
 
+    @classmethod
+    def deserialize(cls, ctx: CkksContext, data: bytes) -> "CipherTensor":
+        """get_tensor (henet/protocol.hpp:346-358): wire bytes straight into a device tensor."""
+        b = np.frombuffer(data, dtype=np.uint8)
+        h = C.c_void_p()
+        used = C.c_uint64()
+        check(lib.hg_tensor_deserialize(ctx.handle, _ptr(b), b.size, C.byref(used), C.byref(h), None))
+        return cls(ctx, 0, _handle=h)
+
+    def serialize(self) -> bytes:
+        """put_tensor (henet/protocol.hpp:335-344)."""
+        out = np.empty(lib.hg_tensor_serialized_size(self._h), dtype=np.uint8)
+        check(lib.hg_tensor_serialize(self._h, _ptr(out), out.size, None))
+        return out.tobytes()
+
     def upload_u32(self, words: np.ndarray) -> None:
         w = np.ascontiguousarray(words, dtype=np.uint32)
         check(lib.hg_tensor_upload_u32(self._h, _ptr(w), None))
