@@ -1738,7 +1738,22 @@ int hg_tensor_upload(hg_tensor* t, const uint64_t* words, void* stream) {
     cudaStream_t s = ctx.pick(stream);
     const u64 n = t->b.words(ctx.n);
     if (!ctx.wide && host_narrow_enabled()) {
-      require(host_narrow_upload(ctx.core->device, words, t->b.data(), n, t->b.level, ctx.n, ctx.chain.data(), s),
+      // PCIe and the host packers both bound this path: the last ~15% of the ciphertexts
+      // cross as raw u64 and are narrowed on the GPU while the host packs the rest
+      const u64 per_ct = static_cast<u64>(t->b.polys) * t->b.level * ctx.n;
+      const u64 dcts = static_cast<u64>(static_cast<double>(t->b.count) * upload_direct_fraction());
+      DirectShare ds{dcts * per_ct, nullptr, nullptr, &ctx.basis};
+      if (ds.words) {
+        const size_t need = ds.words * 8 + sizeof(int);
+        if (!t->stage || t->stage->bytes < need) {
+          t->stage = ctx.alloc(need, ctx.core->stream);
+          cuda_check(cudaStreamSynchronize(ctx.core->stream), "upload staging");
+        }
+        ds.stage = static_cast<u64*>(t->stage->ptr);
+        ds.bad = reinterpret_cast<int*>(static_cast<char*>(t->stage->ptr) + ds.words * 8);
+      }
+      require(host_narrow_upload(ctx.core->device, words, t->b.data(), n - ds.words, t->b.level, ctx.n,
+                                 ctx.chain.data(), s, nullptr, 0, &ds),
               "residue out of range");
       return;
     }

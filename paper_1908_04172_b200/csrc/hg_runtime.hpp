@@ -37,9 +37,19 @@ void cuda_check(cudaError_t e, const char* what);
 // hg_upload.cpp: reference u64 words -> device u32 residues, validated and packed by host
 // threads and DMA'd chunk by chunk (HG_UPLOAD_HOST_NARROW=0: copy u64, narrow on the GPU).
 bool host_narrow_enabled();
+// Optional share of the words (the tail, whole limb runs at a ciphertext boundary) sent as
+// raw u64 through `stage` and narrowed + validated on the GPU while the host packs the rest.
+struct DirectShare {
+  uint64_t words;
+  uint64_t* stage;  // device, words * 8 bytes
+  int* bad;         // device flag
+  const Basis* basis;
+};
+// fraction of ciphertexts hg_tensor_upload sends raw (HG_UPLOAD_DIRECT_FRAC, default 0.15)
+double upload_direct_fraction();
 bool host_narrow_upload(int device, const uint64_t* words, uint32_t* dst, uint64_t n_words, uint32_t level,
                         uint32_t N, const uint64_t* chain, cudaStream_t s, const uint8_t* const* segs = nullptr,
-                        uint64_t seg_words = 0);
+                        uint64_t seg_words = 0, const DirectShare* direct = nullptr);
 
 // Shared device state: the stream and device; kept alive by every buffer.
 struct DeviceCore {

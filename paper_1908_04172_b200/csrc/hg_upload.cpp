@@ -95,13 +95,15 @@ struct Workers {
   std::vector<cudaEvent_t> events;  // [worker][slot]
   std::vector<u32*> stage;          // [worker][slot] pinned
   cudaEvent_t start = nullptr;
+  cudaStream_t direct = nullptr;    // the raw-u64 share: H2D + GPU narrowing
   std::mutex mu;                    // one upload at a time per device
 };
 
 int worker_count() {
   if (const char* e = getenv("HG_UPLOAD_THREADS")) return std::max(1, atoi(e));
+  // all but two host threads (the caller's serving loop keeps launching kernels meanwhile)
   const unsigned hc = std::thread::hardware_concurrency();
-  return static_cast<int>(std::min(16u, std::max(1u, hc)));
+  return static_cast<int>(std::min(16u, std::max(1u, hc > 4 ? hc - 2 : hc)));
 }
 
 Workers& workers(int device) {
@@ -121,6 +123,7 @@ Workers& workers(int device) {
     for (auto& p : w->stage)
       cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&p), kChunkWords * 4, cudaHostAllocPortable), "pinned stage");
     cuda_check(cudaEventCreateWithFlags(&w->start, cudaEventDisableTiming), "event");
+    cuda_check(cudaStreamCreateWithFlags(&w->direct, cudaStreamNonBlocking), "stream");
   }
   return *w;
 }
@@ -146,6 +149,15 @@ inline bool pack_run(const u64* src, u32* dst, u32 n, u32 q) {
 
 }  // namespace
 
+double upload_direct_fraction() {
+  static const double f = [] {
+    const char* e = getenv("HG_UPLOAD_DIRECT_FRAC");
+    const double v = e ? atof(e) : 0.15;
+    return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+  }();
+  return f;
+}
+
 bool host_narrow_enabled() {
   static const bool on = [] {
     const char* e = getenv("HG_UPLOAD_HOST_NARROW");
@@ -159,12 +171,22 @@ bool host_narrow_enabled() {
 // segments (one serialized ciphertext each) instead of `words`.
 // Returns false if some word is not below its limb's prime; dst is then unspecified.
 bool host_narrow_upload(int device, const u64* words, u32* dst, u64 n_words, u32 level, u32 N, const u64* chain,
-                        cudaStream_t s, const uint8_t* const* segs, u64 seg_words) {
+                        cudaStream_t s, const uint8_t* const* segs, u64 seg_words, const DirectShare* direct) {
   Workers& W = workers(device);
   std::lock_guard<std::mutex> g(W.mu);
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   // the copies are ordered after the work already queued on s (readers of dst)
   cuda_check(cudaEventRecord(W.start, s), "event");
+  if (direct != nullptr && direct->words != 0) {
+    // the raw share (words [n_words, n_words + direct->words)) crosses the bus as u64 and is
+    // validated and narrowed on the GPU, alongside the host-packed chunks
+    cuda_check(cudaStreamWaitEvent(W.direct, W.start, 0), "wait");
+    cuda_check(cudaMemsetAsync(direct->bad, 0, sizeof(int), W.direct), "memset");
+    cuda_check(cudaMemcpyAsync(direct->stage, words + n_words, direct->words * 8, cudaMemcpyHostToDevice, W.direct),
+               "h2d");
+    if (launch_narrow(direct->stage, dst + n_words, direct->words, level, N, *direct->basis, direct->bad, W.direct) < 0)
+      throw Error(HG_ERR_CUDA, "narrow launch failed");
+  }
   const int nw = W.pool->size();
   const u64 chunks = (n_words + kChunkWords - 1) / kChunkWords;
   std::atomic<bool> bad{false};
@@ -203,6 +225,12 @@ bool host_narrow_upload(int device, const u64* words, u32* dst, u64 n_words, u32
     }
   });
   if (err.load()) throw Error(HG_ERR_CUDA, err_msg);
+  if (direct != nullptr && direct->words != 0) {
+    int hbad = 0;
+    cuda_check(cudaMemcpyAsync(&hbad, direct->bad, sizeof(int), cudaMemcpyDeviceToHost, W.direct), "d2h");
+    cuda_check(cudaStreamSynchronize(W.direct), "upload");
+    if (hbad != 0) bad = true;
+  }
   return !bad.load();
 }
 

@@ -8,6 +8,7 @@ runs in its own subprocess and compares with the reference (oracle/_ref).
   HG_CONV_FP64=0  convolution MACs all on IMAD.WIDE (no DFMA split)
   HG_AUX_STREAM=0 special-prime key switch on the main stream
   HG_UPLOAD_HOST_NARROW=0  hg_tensor_upload copies u64 words and narrows them on the GPU
+  HG_UPLOAD_DIRECT_FRAC=0 / 1  host packing only / everything raw through the GPU narrowing
 """
 import os
 import subprocess
@@ -63,6 +64,8 @@ print("OK")
     ({"HG_CONV_FP64": "0"}, "toy"),
     ({"HG_AUX_STREAM": "0"}, "toy"),
     ({"HG_UPLOAD_HOST_NARROW": "0"}, "toy"),
+    ({"HG_UPLOAD_DIRECT_FRAC": "0"}, "toy"),
+    ({"HG_UPLOAD_DIRECT_FRAC": "1"}, "toy"),
     ({"HG_WIDE_TC": "0"}, "wide"),
     ({"HG_DENSE_TC": "0"}, "wide"),
 ])
