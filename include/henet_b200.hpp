@@ -13,6 +13,10 @@
 //   henet::relinearize    henet/ckks.hpp:442-499      -> henet::gpu::relinearize
 //   henet::rescale        henet/ckks.hpp:504-519      -> henet::gpu::rescale
 //   henet::mul_ct_pt_scalar henet/ckks.hpp:387-392    -> henet::gpu::mul_ct_pt_scalar
+//   henet::encrypt_tensor henet/graph.hpp:68-91       -> henet::gpu::encrypt_tensor
+//   henet::decrypt_tensor henet/graph.hpp:93-103      -> henet::gpu::decrypt_tensor
+//   henet::LocalProvider  henet/graph.hpp:743-752     -> henet::gpu::LocalProvider (its
+//       NonlinearityEngine on the GPU; gpu::execute hands it device tensors directly)
 //
 // Device state (context tables, relin key, model weights) is cached per
 // CkksContext / RelinKey / PlainModel object, so repeated calls -- the
@@ -58,6 +62,8 @@ class Device {
   }
   ~Device() {
     for (auto& kv : keys_) hg_relin_key_destroy(kv.second);
+    for (auto& kv : secrets_) hg_secret_key_destroy(kv.second);
+    for (auto& kv : engines_) hg_refresh_engine_destroy(kv.second);
     for (auto& kv : models_) hg_model_destroy(kv.second);
     hg_ctx_destroy(ctx_);
   }
@@ -79,6 +85,31 @@ class Device {
     check(hg_relin_key_upload(ctx_, w.data(), w.size(), &k));
     keys_[key] = k;
     return k;
+  }
+
+  const hg_secret_key* secret(const SecretKey& sk) {
+    const auto& w = sk.s.words();
+    const u64 key = fnv(w.data(), w.size() * sizeof(u64));
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = secrets_.find(key);
+    if (it != secrets_.end()) return it->second;
+    hg_secret_key* k = nullptr;
+    check(hg_secret_key_upload(ctx_, w.data(), w.size(), &k));
+    secrets_[key] = k;
+    return k;
+  }
+
+  // one device NonlinearityEngine per (secret key, refresh seed)
+  hg_refresh_engine* engine(const SecretKey& sk, u64 seed) {
+    const hg_secret_key* k = secret(sk);
+    const u64 key = fnv(&seed, sizeof(seed), fnv(&k, sizeof(k)));
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = engines_.find(key);
+    if (it != engines_.end()) return it->second;
+    hg_refresh_engine* e = nullptr;
+    check(hg_refresh_engine_create(ctx_, k, seed, &e));
+    engines_[key] = e;
+    return e;
   }
 
   static u64 fingerprint(const PlainModel& m) {
@@ -144,6 +175,8 @@ class Device {
   std::mutex mu_;
   std::map<u64, hg_relin_key*> keys_;
   std::map<u64, hg_model*> models_;
+  std::map<u64, hg_secret_key*> secrets_;
+  std::map<u64, hg_refresh_engine*> engines_;
 };
 
 inline Device& device_for(const CkksContext& ctx) {
@@ -229,6 +262,72 @@ inline int provider_trampoline(void* user, int kind, uint32_t window, uint32_t l
 
 }  // namespace detail
 
+// LocalProvider (henet/graph.hpp:743-752) whose NonlinearityEngine (decrypt, decode, ReLU /
+// window max, encode, encrypt with derive_seed(derive_seed(seed, layer), group)) runs on
+// the GPU.  gpu::execute recognises it and refreshes on device; any other caller gets the
+// usual host-Ciphertext NonlinearityProvider interface.  Output bit-identical to
+// henet::LocalProvider(NonlinearityEngine(ctx, sk, seed)).
+class LocalProvider : public NonlinearityProvider {
+ public:
+  LocalProvider(std::shared_ptr<const CkksContext> ctx, SecretKey sk, u64 seed)
+      : ctx_(std::move(ctx)), sk_(std::move(sk)), seed_(seed) {}
+  hg_refresh_engine* engine(Device& dev) const { return dev.engine(sk_, seed_); }
+  const CkksContext& context() const { return *ctx_; }
+
+  std::vector<Ciphertext> apply(NonlinKind kind, u32 window, u32 layer_seq,
+                                const std::vector<Ciphertext>& cts) override {
+    Device& dev = device_for(*ctx_);
+    detail::Tensor in, out;
+    detail::upload(dev, cts, {}, in);
+    check(hg_tensor_create(dev.ctx(), cts.size() / (window ? window : 1), 2, 1, 1.0, 0, &out.t));
+    check(hg_refresh_engine_apply(engine(dev), kind == NonlinKind::Relu ? HG_NONLIN_RELU : HG_NONLIN_MAXPOOL, window,
+                                  layer_seq, in.t, out.t));
+    return detail::download(dev, out.t);
+  }
+
+ private:
+  std::shared_ptr<const CkksContext> ctx_;
+  SecretKey sk_;
+  u64 seed_;
+};
+
+// encrypt_tensor, henet/graph.hpp:68-91 (threads is ignored: the GPU does the parallelism).
+inline CipherTensor encrypt_tensor(const CkksContext& ctx, const BatchInput& input, const SecretKey& sk, u64 seed,
+                                   PackingMode packing, unsigned threads = 1) {
+  (void)threads;
+  require(!input.samples.empty(), "batch must be non-empty");
+  Device& dev = device_for(ctx);
+  const std::size_t batch = input.samples.size(), count = input.shape.elem_count();
+  std::vector<double> flat(batch * count);
+  for (std::size_t s = 0; s < batch; ++s) {
+    require(input.samples[s].size() == count, "sample size does not match the tensor shape");
+    std::memcpy(&flat[s * count], input.samples[s].data(), count * sizeof(double));
+  }
+  detail::Tensor out;
+  check(hg_tensor_create(dev.ctx(), count, 2, 1, 1.0, 0, &out.t));
+  check(hg_encrypt_tensor(dev.ctx(), dev.secret(sk), flat.data(), static_cast<uint32_t>(batch), count, seed,
+                          static_cast<int>(packing), out.t, nullptr));
+  CipherTensor t;
+  t.shape = input.shape;
+  t.elems = detail::download(dev, out.t);
+  return t;
+}
+
+// decrypt_tensor, henet/graph.hpp:93-103.
+inline std::vector<std::vector<double>> decrypt_tensor(const CkksContext& ctx, const CipherTensor& ct,
+                                                       const SecretKey& sk, std::size_t batch) {
+  Device& dev = device_for(ctx);
+  detail::Tensor in;
+  detail::upload(dev, ct.elems, {}, in);
+  const std::size_t count = ct.elems.size();
+  std::vector<double> flat(batch * count);
+  check(hg_decrypt_tensor(dev.ctx(), dev.secret(sk), in.t, static_cast<uint32_t>(batch), flat.data(), nullptr));
+  std::vector<std::vector<double>> samples(batch, std::vector<double>(ct.shape.elem_count()));
+  for (std::size_t s = 0; s < batch; ++s)
+    for (std::size_t e = 0; e < count; ++e) samples[s][e] = flat[s * count + e];
+  return samples;
+}
+
 // execute, henet/graph.hpp:1121-1126 -- the whole graph on the B200.
 inline CipherTensor execute(std::shared_ptr<const CkksContext> ctx, const PlainModel& model, const RescalePlan& plan,
                             const CipherTensor& input, const ExecutionConfig& cfg, ExecutionStats* stats = nullptr) {
@@ -248,8 +347,13 @@ inline CipherTensor execute(std::shared_ptr<const CkksContext> ctx, const PlainM
   detail::ProviderCtx pc{&dev, cfg.provider};
   hg_exec_stats st{};
   detail::Tensor out;
-  check(hg_execute(dev.ctx(), hm, hp, in.t, rk, cfg.provider ? detail::provider_trampoline : nullptr, &pc, &out.t,
-                   stats ? &st : nullptr, nullptr));
+  hg_nonlin_fn fn = cfg.provider ? detail::provider_trampoline : nullptr;
+  void* user = &pc;
+  if (auto* lp = dynamic_cast<LocalProvider*>(cfg.provider)) {  // refresh on device
+    fn = hg_refresh_engine_apply;
+    user = lp->engine(dev);
+  }
+  check(hg_execute(dev.ctx(), hm, hp, in.t, rk, fn, user, &out.t, stats ? &st : nullptr, nullptr));
   CipherTensor result;
   uint32_t dims[8], nd = 8;
   check(hg_tensor_get_shape(out.t, dims, &nd));

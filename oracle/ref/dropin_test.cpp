@@ -5,7 +5,8 @@
 // include/henet_b200.hpp, linked to the product libhenet_b200.so.  Runs the
 // reference's own model generators through henet::execute (CPU) and
 // henet::gpu::execute (B200) with identical arguments and requires
-// bit-identical ciphertexts, scales and statistics.  Exit code 0 = pass.
+// bit-identical ciphertexts, scales and statistics; likewise the client side
+// (encrypt_tensor, decrypt_tensor, LocalProvider).  Exit code 0 = pass.
 #include <cstdio>
 #include <thread>
 
@@ -68,6 +69,36 @@ int main() {
   ok &= run_model(ctx, keys, make_cryptonets_relu(Preset::P13, PackingMode::Complex, 2), PackingMode::Complex, 8192,
                   "make_cryptonets_relu complex (c3)");
   ok &= run_model(ctx, keys, make_cryptonets_shaped_toy(Preset::P13, 3), PackingMode::Real, 64, "cryptonets toy");
+  // client side: encrypt_tensor / decrypt_tensor, and execute with the GPU LocalProvider
+  {
+    PlainModel model = load_model(make_cryptonets_relu(Preset::P13, PackingMode::Complex, 2).manifest,
+                                  std::span<const u8>(make_cryptonets_relu(Preset::P13, PackingMode::Complex, 2).blob));
+    BatchInput in = make_random_input(model.shapes.at(model.input_node().id), 8192, 6);
+    CipherTensor xc = encrypt_tensor(*ctx, in, keys.secret, 78, PackingMode::Complex, std::thread::hardware_concurrency());
+    CipherTensor xg = henet::gpu::encrypt_tensor(*ctx, in, keys.secret, 78, PackingMode::Complex);
+    ok &= same(xc, xg, "encrypt_tensor complex (c3 input)");
+    RescalePlan plan = plan_lazy_rescaling(*ctx, model);
+    LocalProvider prov(NonlinearityEngine(ctx, keys.secret, 99));
+    henet::gpu::LocalProvider gprov(ctx, keys.secret, 99);
+    ExecutionConfig cfg;
+    cfg.threads = std::thread::hardware_concurrency();
+    cfg.provider = &prov;
+    CipherTensor want = henet::execute(ctx, model, plan, xc, cfg);
+    cfg.provider = &gprov;
+    CipherTensor got = henet::gpu::execute(ctx, model, plan, xc, cfg);
+    ok &= same(want, got, "c3 with gpu::LocalProvider (device refresh)");
+    auto dc = decrypt_tensor(*ctx, want, keys.secret, 8192);
+    auto dg = henet::gpu::decrypt_tensor(*ctx, got, keys.secret, 8192);
+    const bool dec_ok = dc == dg;
+    std::printf("%-40s %s\n", "decrypt_tensor (c3 logits)", dec_ok ? "bit-identical" : "MISMATCH");
+    // the GPU provider through the host interface, as another executor would call it
+    std::vector<Ciphertext> some(xc.elems.begin(), xc.elems.begin() + 4);
+    const bool pv_ok = prov.apply(NonlinKind::Relu, 1, 3, some).size() == 4 &&
+                       prov.apply(NonlinKind::MaxPool, 4, 5, some)[0].polys == gprov.apply(NonlinKind::MaxPool, 4, 5, some)[0].polys &&
+                       prov.apply(NonlinKind::Relu, 1, 3, some)[2].polys == gprov.apply(NonlinKind::Relu, 1, 3, some)[2].polys;
+    std::printf("%-40s %s\n", "gpu::LocalProvider::apply (host ciphertexts)", pv_ok ? "bit-identical" : "MISMATCH");
+    ok &= dec_ok && pv_ok;
+  }
   // op level
   {
     std::vector<double> v(4096, 0.25);
