@@ -142,7 +142,8 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
   // Shoup companions), staged per NTT pass in the order the kernels consume them.
   const u32 LOGT = logn - 5, CB = logn >= 14 ? logn - 10 : 3, MB = LOGT - CB;
   const u32 rowsB = 1u << MB, rowsT = 1u << LOGT;
-  const size_t per_prime = 2 * (static_cast<size_t>(rowsB) * 32 + static_cast<size_t>(rowsT) * 4);
+  const u32 FC = 1u << CB;  // pass-C scale factors per thread (Ntt::scale_C)
+  const size_t per_prime = 2 * (static_cast<size_t>(rowsB) * 32 + static_cast<size_t>(rowsT) * FC);
   std::vector<uint2> staged(static_cast<size_t>(full) * per_prime);
   auto jmapB = [&](u32 tid, u32 k) -> u32 {
     const u32 CBm = (1u << CB) - 1, MBm = (1u << MB) - 1;
@@ -183,10 +184,11 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
         }
     }
     for (u32 t = 0; t < rowsT; ++t)
-      for (u32 bb = 0; bb < 4; ++bb) {
-        u64 v = 1;
-        if (bb < CB) v = nt::powmod(root, nt::bit_reverse(t << (CB - bb - 1), logn), q);
-        tbase[static_cast<size_t>(t) * 4 + bb] = make_uint2(static_cast<u32>(v), nt::shoup(v, q));
+      for (u32 k = 0; k < FC; ++k) {
+        u64 v = 1;  // F_k(t) = prod over the set bits b of k of T_b(t)
+        for (u32 bb = 0; bb < CB; ++bb)
+          if ((k >> bb) & 1) v = nt::mulmod(v, nt::powmod(root, nt::bit_reverse(t << (CB - bb - 1), logn), q), q);
+        tbase[static_cast<size_t>(t) * FC + k] = make_uint2(static_cast<u32>(v), nt::shoup(v, q));
       }
   };
   std::vector<uint2> f(n), g(n);
@@ -228,8 +230,8 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
     uint2* base = &staged[static_cast<size_t>(i) * per_prime];
     stage_rowsB(false, f, base);
     stage_C(false, psi, q, P.tvC, base + rowsB * 32);
-    stage_rowsB(true, g, base + rowsB * 32 + rowsT * 4);
-    stage_C(true, psi_inv, q, P.itvC, base + 2 * rowsB * 32 + rowsT * 4);
+    stage_rowsB(true, g, base + rowsB * 32 + rowsT * FC);
+    stage_C(true, psi_inv, q, P.itvC, base + 2 * rowsB * 32 + rowsT * FC);
   }
   if (ctx->wide) {
     // u64 path: natural-order tables with 64-bit Shoup companions (hg_wide.cuh)
@@ -279,8 +281,8 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
     const uint2* base = static_cast<const uint2*>(ctx->tables->ptr) + static_cast<size_t>(i) * per_prime;
     ctx->basis.p[i].fwdB = base;
     ctx->basis.p[i].fwdT = base + rowsB * 32;
-    ctx->basis.p[i].invB = base + rowsB * 32 + rowsT * 4;
-    ctx->basis.p[i].invT = base + 2 * rowsB * 32 + rowsT * 4;
+    ctx->basis.p[i].invB = base + rowsB * 32 + rowsT * FC;
+    ctx->basis.p[i].invT = base + 2 * rowsB * 32 + rowsT * FC;
   }
   cuda_check(cudaStreamSynchronize(ctx->core->stream), "upload tables");
 
