@@ -202,7 +202,7 @@ int hg_encode_vector(hg_ctx* ctx, const double* slots_re_im, uint32_t n_slots, u
                      uint32_t level, double scale, uint64_t* out_words);
 
 /* ------------------------------------------------------------------ */
-/* Client side on the GPU (u32-residue contexts)                       */
+/* Client side on the GPU                                              */
 /* ------------------------------------------------------------------ */
 typedef struct hg_secret_key hg_secret_key; /* SecretKey (henet/ckks.hpp:21-23) on device */
 /* s in NTT form over the full basis, chain limbs then the special limb, in the word order
@@ -297,6 +297,9 @@ int hg_refresh_engine_create(hg_ctx* ctx, const hg_secret_key* sk, uint64_t seed
 void hg_refresh_engine_destroy(hg_refresh_engine* e);
 int hg_refresh_engine_apply(void* engine, int kind, uint32_t window, uint32_t layer_seq,
                             const hg_tensor* request, hg_tensor* response);
+/* hi > 0: ReLU refreshes clamp each slot to [0, hi] instead (v < 0 ? 0 : v > hi ? hi : v) --
+ * the client-aided ReLU6 of BASELINE config 4; hi <= 0 restores ReLU. */
+int hg_refresh_engine_set_relu_clip(hg_refresh_engine* e, double hi);
 
 /* ------------------------------------------------------------------ */
 /* Measurement helpers (not part of the reference surface)             */

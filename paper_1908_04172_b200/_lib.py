@@ -102,6 +102,7 @@ PROTOTYPES = {
     "hg_tensor_serialize": (C.c_int, [vp, vp, C.c_uint64, vp]),
     "hg_refresh_engine_destroy": (None, [vp]),
     "hg_refresh_engine_apply": (C.c_int, [vp, C.c_int, C.c_uint32, C.c_uint32, vp, vp]),
+    "hg_refresh_engine_set_relu_clip": (C.c_int, [vp, C.c_double]),
     "hg_model_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
     "hg_model_destroy": (None, [vp]),
     "hg_model_add_weight": (C.c_int, [vp, C.c_char_p, u32p, C.c_uint32, vp]),

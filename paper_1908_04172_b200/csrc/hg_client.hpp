@@ -11,11 +11,12 @@ namespace hg {
 
 constexpr int kCrtWords = 4;  // Q < 2^256 (chains of <= 8 primes below 2^32)
 
+// Residue pointers are u32 words, or u64 words in wide contexts (the launchers' `wide`).
 struct EncArgs {
-  u32* ct;          // [count][2][level][N]: c1 = a written by the sampler, c0 by combine
-  u32* err;         // [count][level][N]: error lifted into every limb (then NTT'd in place)
-  const u32* pt;    // [count][level][N]: encoded plaintexts (NTT domain)
-  const u32* sk;    // [full][N]: secret key s (NTT domain)
+  void* ct;         // [count][2][level][N]: c1 = a written by the sampler, c0 by combine
+  void* err;        // [count][level][N]: error lifted into every limb (then NTT'd in place)
+  const void* pt;   // [count][level][N]: encoded plaintexts (NTT domain)
+  const void* sk;   // [full][N]: secret key s (NTT domain)
   int* flags;       // [count]: 1 if the counter-mode draw hit a rejection / u1 == 0
   u64 seed;         // encrypt_tensor seed; ciphertext e uses derive_seed(seed, e), stream 1
   u64 thr[kMaxPrimes];  // next_below rejection thresholds (2^64 mod q)
@@ -26,13 +27,13 @@ struct CrtTables {
   u64 q_over_p[kMaxPrimes][kCrtWords + 1];  // Q / q_i
   u64 big_q[kCrtWords + 1];                 // Q = prod q_i
   u64 q_half[kCrtWords + 1];                // floor(Q / 2)
-  u32 inv[kMaxPrimes];                      // (Q / q_i)^-1 mod q_i
+  u64 inv[kMaxPrimes];                      // (Q / q_i)^-1 mod q_i
 };
 
 struct DecArgs {
-  const u32* ct;    // [count][polys][level][N]
-  const u32* sk;    // [full][N]
-  u32* m;           // [count][level][N]: decrypted plaintext residues
+  const void* ct;   // [count][polys][level][N]
+  const void* sk;   // [full][N]
+  void* m;          // [count][level][N]: decrypted plaintext residues
   double* coeffs;   // [count][N] (nullptr: residues only)
   u64 inv_mant;     // 1.0L / scale as an x87 long double: inv_mant * 2^inv_exp (host-computed)
   int inv_exp;
@@ -40,15 +41,18 @@ struct DecArgs {
   u32 count, polys, level, N, words;
 };
 
-int launch_enc_sample(const EncArgs& a, const Basis& B, cudaStream_t s);
-int launch_enc_serial(const EncArgs& a, const u32* list, u32 n_list, const Basis& B, cudaStream_t s);
-int launch_enc_combine(const EncArgs& a, const Basis& B, cudaStream_t s);
+// B: the context's Basis, or its BasisW when `wide`
+int launch_enc_sample(const EncArgs& a, const void* B, bool wide, cudaStream_t s);
+int launch_enc_serial(const EncArgs& a, const u32* list, u32 n_list, const void* B, bool wide, cudaStream_t s);
+int launch_enc_combine(const EncArgs& a, const void* B, bool wide, cudaStream_t s);
 // decrypt (k_dec_combine) and, when a.coeffs is set, decode: INTT, CRT, forward embedding
 // into slots [count][N/2][2]
-int launch_dec(const DecArgs& a, int logn, const Basis& B, const double2* roots, const double2* twist,
+int launch_dec(const DecArgs& a, int logn, const void* B, bool wide, const double2* roots, const double2* twist,
                double2* scratch, double* slots, cudaStream_t s);
 // NonlinearityEngine::apply's per-slot function (henet/graph.hpp:714-731): slots
 // [groups * window][N/2][2] -> [groups][N/2][2]; kind 1 = ReLU (window 1), 2 = max.
-int launch_refresh_slots(const double* in, double* out, u32 groups, u32 window, u32 half, int kind, cudaStream_t s);
+// clip > 0: ReLU is the clamp to [0, clip] (the ReLU6 refresh of BASELINE c4)
+int launch_refresh_slots(const double* in, double* out, u32 groups, u32 window, u32 half, int kind, double clip,
+                         cudaStream_t s);
 
 }  // namespace hg

@@ -2315,8 +2315,9 @@ u64 mw_mod(const std::vector<u64>& x, u64 q) {
   return static_cast<u64>(r);
 }
 
-void check_client_ctx(const Context& c) {
-  if (c.wide) throw Error(HG_ERR_UNSUPPORTED, "GPU encrypt/decrypt with primes >= 2^30 is not implemented yet");
+void check_client_ctx(const Context& c) { (void)c; }
+const void* client_basis(const Context& c) {
+  return c.wide ? static_cast<const void*>(&c.basisw) : static_cast<const void*>(&c.basis);
 }
 
 // encrypt (henet/ckks.hpp:229-248) of `count` encoded top-level plaintexts [count][L][N]:
@@ -2329,21 +2330,21 @@ CtBatch encrypt_pts(const Context& c, const hg_secret_key* sk, const BufPtr& pt,
     o.packing = packing;
     o.scale = c.default_scale;
     ensure(c, o, count, 2, L, s);
-    BufPtr err = c.alloc(count * L * static_cast<u64>(N) * 4, s);
+    BufPtr err = c.alloc(count * L * static_cast<u64>(N) * c.word_bytes(), s);
     BufPtr flags = c.alloc(count * sizeof(int), s);
     cuda_check(cudaMemsetAsync(flags->ptr, 0, count * sizeof(int), s), "memset");
     EncArgs a{};
-    a.ct = o.data();
-    a.err = static_cast<u32*>(err->ptr);
-    a.pt = static_cast<const u32*>(pt->ptr);
-    a.sk = static_cast<const u32*>(sk->s->ptr);
+    a.ct = o.buf->ptr;
+    a.err = err->ptr;
+    a.pt = pt->ptr;
+    a.sk = sk->s->ptr;
     a.flags = static_cast<int*>(flags->ptr);
     a.seed = seed;
     for (u32 i = 0; i < L; ++i) a.thr[i] = (0 - c.chain[i]) % c.chain[i];  // next_below threshold
     a.count = static_cast<u32>(count);
     a.level = L;
     a.N = N;
-    check_launch(launch_enc_sample(a, c.basis, s), "encrypt sample");
+    check_launch(launch_enc_sample(a, client_basis(c), c.wide, s), "encrypt sample");
     // draws the counter-mode pass could not place (a rejection, u1 == 0): regenerate those
     // ciphertexts by walking their streams; HG_ENC_SERIAL=1 walks every stream (tests)
     std::vector<int> hf(count);
@@ -2358,11 +2359,16 @@ CtBatch encrypt_pts(const Context& c, const hg_secret_key* sk, const BufPtr& pt,
     if (!list.empty()) {
       dl = c.alloc(list.size() * 4, s);
       cuda_check(cudaMemcpyAsync(dl->ptr, list.data(), list.size() * 4, cudaMemcpyHostToDevice, s), "h2d");
-      check_launch(launch_enc_serial(a, static_cast<const u32*>(dl->ptr), static_cast<u32>(list.size()), c.basis, s),
+      check_launch(launch_enc_serial(a, static_cast<const u32*>(dl->ptr), static_cast<u32>(list.size()),
+                                     client_basis(c), c.wide, s),
                    "encrypt serial");
     }
-    check_launch(launch_ntt(static_cast<int>(c.logn), a.err, count * L, L, false, c.basis, s), "ntt");
-    check_launch(launch_enc_combine(a, c.basis, s), "encrypt combine");
+    check_launch(c.wide ? launch_ntt_w(static_cast<int>(c.logn), static_cast<u64*>(a.err), count * L, L, false,
+                                       c.basisw, s)
+                        : launch_ntt(static_cast<int>(c.logn), static_cast<u32*>(a.err), count * L, L, false, c.basis,
+                                     s),
+                 "ntt");
+    check_launch(launch_enc_combine(a, client_basis(c), c.wide, s), "encrypt combine");
     cuda_check(cudaStreamSynchronize(s), "encrypt");
     return o;
 }
@@ -2375,15 +2381,17 @@ int hg_secret_key_upload(hg_ctx* ctx, const uint64_t* words, uint64_t n_words, h
     check_client_ctx(c);
     const u64 full = c.chain_len() + (c.has_special ? 1 : 0), n = c.n;
     require(n_words == full * n, "secret key basis does not match the context");
-    std::vector<u32> h(n_words);
+    std::vector<u32> h(c.wide ? 0 : n_words);
     for (u64 i = 0; i < n_words; ++i) {
       require(words[i] < c.basis_mod(i / n), "residue out of range");
-      h[i] = static_cast<u32>(words[i]);
+      if (!c.wide) h[i] = static_cast<u32>(words[i]);
     }
     auto* k = new hg_secret_key;
     k->ctx = ctx->c;
-    k->s = c.alloc(n_words * 4, c.core->stream);
-    cuda_check(cudaMemcpyAsync(k->s->ptr, h.data(), n_words * 4, cudaMemcpyHostToDevice, c.core->stream), "h2d");
+    k->s = c.alloc(n_words * c.word_bytes(), c.core->stream);
+    cuda_check(cudaMemcpyAsync(k->s->ptr, c.wide ? static_cast<const void*>(words) : static_cast<const void*>(h.data()),
+                               n_words * c.word_bytes(), cudaMemcpyHostToDevice, c.core->stream),
+               "h2d");
     cuda_check(cudaStreamSynchronize(c.core->stream), "secret key");
     *out = k;
   });
@@ -2435,8 +2443,8 @@ DecArgs dec_args(const Context& c, const hg_secret_key* sk, const CtBatch& ct) {
   require(ct.polys == 2 || ct.polys == 3, "ciphertext must have 2 or 3 polynomials");
   require(ct.level >= 1, "ciphertext level must be at least 1");
   DecArgs a{};
-  a.ct = ct.data();
-  a.sk = static_cast<const u32*>(sk->s->ptr);
+  a.ct = ct.buf->ptr;
+  a.sk = sk->s->ptr;
   a.count = static_cast<u32>(ct.count);
   a.polys = ct.polys;
   a.level = ct.level;
@@ -2461,7 +2469,7 @@ BufPtr decode_slots_dev(const Context& c, const hg_secret_key* sk, const CtBatch
       for (u32 j = 0; j < L; ++j)
         if (j != i) mw_mul_small(qi, c.chain[j]);
       for (u32 k = 0; k < qi.size() && k < static_cast<size_t>(kCrtWords); ++k) a.crt.q_over_p[i][k] = qi[k];
-      a.crt.inv[i] = static_cast<u32>(nt::inv(mw_mod(qi, c.chain[i]), c.chain[i]));
+      a.crt.inv[i] = nt::inv(mw_mod(qi, c.chain[i]), c.chain[i]);
     }
     {
       // 1.0L / (long double)scale (decode_slots, henet/encoding.hpp:248), x87 on the host
@@ -2472,14 +2480,14 @@ BufPtr decode_slots_dev(const Context& c, const hg_secret_key* sk, const CtBatch
       a.inv_exp = ex - 64;
     }
     const u64 count = b.count, N = c.n;
-    BufPtr m = c.alloc(count * L * N * 4, s);
+    BufPtr m = c.alloc(count * L * N * c.word_bytes(), s);
     BufPtr co = c.alloc(count * N * sizeof(double), s);
     BufPtr scratch = c.alloc(count * N * sizeof(double2), s);
     BufPtr sl = c.alloc(count * N * sizeof(double), s);  // [count][N/2][2]
-    a.m = static_cast<u32*>(m->ptr);
+    a.m = m->ptr;
     a.coeffs = static_cast<double*>(co->ptr);
     const double2* roots = static_cast<const double2*>(c.fft_tables->ptr);
-    check_launch(launch_dec(a, static_cast<int>(c.logn), c.basis, roots, roots + N / 2,
+    check_launch(launch_dec(a, static_cast<int>(c.logn), client_basis(c), c.wide, roots, roots + N / 2,
                             static_cast<double2*>(scratch->ptr), static_cast<double*>(sl->ptr), s),
                  "decrypt");
     return sl;
@@ -2494,13 +2502,19 @@ int hg_decrypt(hg_ctx* ctx, const hg_secret_key* sk, const hg_tensor* ct, uint64
     cudaStream_t s = c.pick(stream);
     DecArgs a = dec_args(c, sk, ct->b);
     const u64 nw = ct->b.count * ct->b.level * static_cast<u64>(c.n);
-    BufPtr m = c.alloc(nw * 4, s);
-    a.m = static_cast<u32*>(m->ptr);
-    check_launch(launch_dec(a, static_cast<int>(c.logn), c.basis, nullptr, nullptr, nullptr, nullptr, s), "decrypt");
-    std::vector<u32> h(nw);
-    cuda_check(cudaMemcpyAsync(h.data(), m->ptr, nw * 4, cudaMemcpyDeviceToHost, s), "d2h");
-    cuda_check(cudaStreamSynchronize(s), "decrypt");
-    for (u64 i = 0; i < nw; ++i) pt_words[i] = h[i];
+    BufPtr m = c.alloc(nw * c.word_bytes(), s);
+    a.m = m->ptr;
+    check_launch(launch_dec(a, static_cast<int>(c.logn), client_basis(c), c.wide, nullptr, nullptr, nullptr, nullptr, s),
+                 "decrypt");
+    if (c.wide) {
+      cuda_check(cudaMemcpyAsync(pt_words, m->ptr, nw * 8, cudaMemcpyDeviceToHost, s), "d2h");
+      cuda_check(cudaStreamSynchronize(s), "decrypt");
+    } else {
+      std::vector<u32> h(nw);
+      cuda_check(cudaMemcpyAsync(h.data(), m->ptr, nw * 4, cudaMemcpyDeviceToHost, s), "d2h");
+      cuda_check(cudaStreamSynchronize(s), "decrypt");
+      for (u64 i = 0; i < nw; ++i) pt_words[i] = h[i];
+    }
   });
 }
 
@@ -2550,6 +2564,7 @@ struct hg_refresh_engine {
   const hg_secret_key* sk;
   hg_secret_key sk_copy;
   uint64_t seed;
+  double relu_clip = 0.0;  // > 0: ReLU refreshes clamp to [0, relu_clip] (ReLU6, BASELINE c4)
 };
 
 namespace {
@@ -2594,7 +2609,7 @@ int hg_refresh_engine_apply(void* engine, int kind, uint32_t window, uint32_t la
     BufPtr sl = decode_slots_dev(c, eng->sk, b, s);
     BufPtr res = c.alloc(groups * half * 2 * sizeof(double), s);
     check_launch(launch_refresh_slots(static_cast<const double*>(sl->ptr), static_cast<double*>(res->ptr),
-                                      static_cast<u32>(groups), window, half, kind, s),
+                                      static_cast<u32>(groups), window, half, kind, eng->relu_clip, s),
                  "refresh slots");
     std::vector<unsigned long long> mant;
     std::vector<int> ex;
@@ -2755,5 +2770,12 @@ int hg_tensor_serialize(const hg_tensor* t, uint8_t* out, uint64_t cap, void* st
       std::memcpy(o, &w[e * seg_words], seg_words * 8);
       o += seg_words * 8;
     }
+  });
+}
+
+int hg_refresh_engine_set_relu_clip(hg_refresh_engine* e, double hi) {
+  return guard([&] {
+    require(e != nullptr, "null argument");
+    e->relu_clip = hi;
   });
 }

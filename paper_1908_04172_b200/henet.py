@@ -315,6 +315,10 @@ class RefreshEngine:
     def handle(self):
         return self._h
 
+    def set_relu_clip(self, hi: float) -> None:
+        """hi > 0: ReLU refreshes clamp to [0, hi] (the client-aided ReLU6 of BASELINE c4)."""
+        check(lib.hg_refresh_engine_set_relu_clip(self._h, float(hi)))
+
     def apply(self, kind: int, window: int, layer_seq: int, request: "CipherTensor") -> "CipherTensor":
         """NonlinearityEngine::apply on a device tensor; returns the fresh encryptions."""
         out = CipherTensor(self.ctx, request.count // window, 2, len(self.ctx.chain), self.ctx.default_scale,

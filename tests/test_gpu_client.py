@@ -158,3 +158,62 @@ def test_refresh_engine_as_provider_cryptonets_relu(env, packing):
     out = H.execute(ctx, model, H.RescalePlan.plan(ctx, model), inp, None, H.RefreshEngine(ctx, sk, 99))
     assert out.scale == want_sc
     assert np.array_equal(out.to_words(), want)
+
+
+# ---- wide contexts (BASELINE c4/c5b parameters: N = 16384, 40-bit limb 0, u64 residues) ----
+@pytest.fixture(scope="module")
+def wenv():
+    p = W.N16384
+    ctx = H.CkksContext(p["n"], p["chain"], p["special"], p["scale"])
+    ref = R.RefContext(p["n"], p["chain"], p["special"], p["scale"])
+    keys = ref.keygen(41, False)
+    sk = H.SecretKey(ctx, keys.sk_words())
+    return dict(p=p, ctx=ctx, ref=ref, keys=keys, sk=sk)
+
+
+@pytest.mark.parametrize("packing,serial", [(0, False), (1, False), (0, True)])
+def test_wide_encrypt_decrypt_bit_exact(wenv, packing, serial):
+    ctx, ref, keys, sk, p = wenv["ctx"], wenv["ref"], wenv["keys"], wenv["sk"], wenv["p"]
+    batch = 8192 if packing == 0 else 16384
+    samples = np.random.default_rng(3).normal(0, 1, (batch, 3))
+    want, wsc = ref.encrypt_tensor(keys, samples, 55, packing=packing)
+    if serial:
+        os.environ["HG_ENC_SERIAL"] = "1"
+    try:
+        got = H.encrypt_tensor(ctx, sk, samples, 55, packing)
+    finally:
+        os.environ.pop("HG_ENC_SERIAL", None)
+    assert got.scale == wsc
+    assert np.array_equal(got.to_words(), want)
+    dec = H.decrypt_tensor(ctx, sk, got, batch)
+    assert np.array_equal(dec, ref.decrypt_tensor(keys, want, wsc, packing, batch))
+    # plaintext residues c0 + c1 s, checked with Python integers on a slice
+    m = H.decrypt(ctx, sk, got)
+    skw = keys.sk_words()
+    for limb in (0, 3, 7):
+        q = p["chain"][limb]
+        for n in (0, 1, 4095, 16383):
+            c0, c1 = int(want[1, 0, limb, n]), int(want[1, 1, limb, n])
+            assert int(m[1, limb, n]) == (c0 + c1 * int(skw[limb, n])) % q
+
+
+def test_wide_c4_block_gpu_relu6_refresh_bit_exact(wenv):
+    """BASELINE c4 on a 4x4 tile with both client-aided ReLU6 refreshes on the GPU engine
+    (clamp to [0, 6]) vs the reference executor with the harness's clamp provider."""
+    ctx, ref, keys, sk = wenv["ctx"], wenv["ref"], wenv["keys"], wenv["sk"]
+    wl = W.mobilenet_block(hw=4, cin=4, expand=6, cout=3)
+    acts = np.random.default_rng(12).normal(0, 1, (ctx.slot_count(), wl.input_count))
+    words, sc = ref.encrypt_tensor(keys, acts, 13)
+    R.set_relu_clip(6.0)
+    try:
+        want, want_sc, _ = ref.execute(keys, wl.manifest, wl.blob, words, sc, refresh_seed=77)
+    finally:
+        R.set_relu_clip(0.0)
+    model = H.PlainModel.load(wl.manifest, wl.blob)
+    eng = H.RefreshEngine(ctx, sk, 77)
+    eng.set_relu_clip(6.0)
+    x = H.encrypt_tensor(ctx, sk, acts, 13, shape=wl.input_shape)
+    assert np.array_equal(x.to_words(), words)
+    out = H.execute(ctx, model, H.RescalePlan.plan(ctx, model), x, None, eng)
+    assert out.scale == want_sc
+    assert np.array_equal(out.to_words(), want)
