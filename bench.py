@@ -358,16 +358,22 @@ def b200_run(args, ws, rank, local):
         copy_stream = torch.cuda.Stream(device=local)
         used = [torch.cuda.Event(), torch.cuda.Event()]
 
+        up_ms, step_ms = [], []
+
         def upload(k, strm=None):
+            t0 = time.perf_counter()
             if strm is not None:
                 copy_stream.wait_event(used[k])  # the step that last read buffer k is done with it
             check(lib.hg_tensor_upload(bufs[k].handle, H._ptr(host_in),
                                        ctypes.c_void_p(strm.cuda_stream) if strm is not None else None))
+            up_ms.append((time.perf_counter() - t0) * 1e3)
 
         def run_step(k):
+            t0 = time.perf_counter()
             o = H.execute(ctx, model, plan, bufs[k], rk)
             used[k].record(stream)
             check(lib.hg_tensor_download(o.handle, H._ptr(out_host), None))
+            step_ms.append((time.perf_counter() - t0) * 1e3)
 
         def sequential(n):
             for _ in range(n):
@@ -405,8 +411,14 @@ def b200_run(args, ws, rank, local):
         # sensitive to host scheduling)
         with concurrent.futures.ThreadPoolExecutor(1) as pool:
             pipelined(2, pool)  # warm-up (both buffers, both streams)
+            up_ms.clear()
+            step_ms.clear()
             pipe_trials = [timed(lambda n: pipelined(n, pool), n_e2e) for _ in range(3)]
+            pipe_up, pipe_step = statistics.median(up_ms), statistics.median(step_ms)
+        up_ms.clear()
+        step_ms.clear()
         seq_trials = [timed(sequential, n_e2e) for _ in range(3)]
+        seq_up, seq_step = statistics.median(up_ms), statistics.median(step_ms)
         e_ms, seq_ms = statistics.median(pipe_trials), statistics.median(seq_trials)
         e2e = {"value": IMAGES_PER_STEP * ws / (e_ms / 1e3), "unit": "images/s",
                "h2d_bytes_per_step": int(words.nbytes // (2 if host_narrow else 1)),
@@ -416,6 +428,8 @@ def b200_run(args, ws, rank, local):
                "sequential": {"value": IMAGES_PER_STEP * ws / (seq_ms / 1e3), "ms_per_step": seq_ms,
                               "trials_ms_per_step": seq_trials},
                "host_numa_node": numa,
+               "host_ms_median": {"pipelined": {"upload": pipe_up, "execute_download": pipe_step},
+                                  "sequential": {"upload": seq_up, "execute_download": seq_step}},
                "path": "hg_tensor_upload(u64 host words, " +
                        ("validated and packed to u32 by host threads, chunked H2D" if host_narrow else
                         "u64 H2D, GPU narrowing") +
