@@ -250,6 +250,11 @@ int hg_model_add_node(hg_model* m, const hg_node_desc* node);
 /* Topological sort, shape inference and structural checks of load_model
  * (henet/graph.hpp:297-436). */
 int hg_model_finalize(hg_model* m);
+/* on != 0: weight encodings (residues at each consumer's level and scale, tensor-core byte
+ * planes) are built on the first execute and reused by later ones -- the reference's shared
+ * WeightEncoder cache after precompile_weights (henet/graph.hpp:595-679); results are
+ * identical either way.  on == 0 (default): encoded per execute, like a per-call encoder. */
+int hg_model_keep_encodings(hg_model* m, int on);
 int hg_model_node_count(const hg_model* m, uint32_t* n);
 int hg_model_shape(const hg_model* m, const char* id, uint32_t* dims, uint32_t* ndims);
 

@@ -333,6 +333,9 @@ inline CipherTensor execute(std::shared_ptr<const CkksContext> ctx, const PlainM
                             const CipherTensor& input, const ExecutionConfig& cfg, ExecutionStats* stats = nullptr) {
   Device& dev = device_for(*ctx);
   const hg_model* hm = dev.model(model);
+  // a shared WeightEncoder (ExecutionConfig::encoder, henet/graph.hpp:773) keeps encodings
+  // across calls; without one the reference encodes per call -- mirrored on the device
+  check(hg_model_keep_encodings(const_cast<hg_model*>(hm), cfg.encoder != nullptr ? 1 : 0));
   hg_plan* hp = nullptr;
   check(hg_plan_create(static_cast<int>(plan.mode), plan.planned_rescale_ops, &hp));
   std::unique_ptr<hg_plan, void (*)(hg_plan*)> plan_guard(hp, hg_plan_destroy);

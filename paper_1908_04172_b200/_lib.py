@@ -97,6 +97,7 @@ PROTOTYPES = {
     "hg_decrypt": (C.c_int, [vp, vp, vp, vp, vp]),
     "hg_decrypt_tensor": (C.c_int, [vp, vp, vp, C.c_uint32, vp, vp]),
     "hg_refresh_engine_create": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(vp)]),
+    "hg_model_keep_encodings": (C.c_int, [vp, C.c_int]),
     "hg_tensor_deserialize": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(vp), vp]),
     "hg_tensor_serialized_size": (C.c_uint64, [vp]),
     "hg_tensor_serialize": (C.c_int, [vp, vp, C.c_uint64, vp]),

@@ -959,6 +959,39 @@ class Executor {
 
  private:
   // Dot / Convolution: mac_output over every output (henet/graph.hpp:905-993).
+  // A weight tensor's device encoding for `key`, built by `build` -- per execute (the
+  // reference's per-call WeightEncoder), or once per model and context when the model keeps
+  // encodings (hg_model_keep_encodings; precompile_weights, henet/graph.hpp:657-679).
+  BufPtr encoding(WeightTensor& w, std::vector<u64> key, size_t bytes, const std::function<void(void*)>& build) {
+    key.insert(key.begin(), reinterpret_cast<u64>(ctx_.get()));
+    if (model_.keep_encodings) {
+      auto it = w.enc.find(key);
+      if (it != w.enc.end()) return it->second;
+    }
+    if (!model_.keep_encodings) {
+      BufPtr b = ctx_->alloc(bytes, s_);
+      build(b->ptr);
+      return b;
+    }
+    // a kept encoding is allocated on the context's stream (it outlives any caller stream)
+    BufPtr b = ctx_->alloc(bytes, ctx_->core->stream);
+    if (s_ != ctx_->core->stream) {
+      cudaEvent_t ev;
+      cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+      cuda_check(cudaEventRecord(ev, ctx_->core->stream), "event");
+      cuda_check(cudaStreamWaitEvent(s_, ev, 0), "event");
+      cudaEventDestroy(ev);
+    }
+    build(b->ptr);
+    w.enc[key] = b;
+    return b;
+  }
+  static u64 bits(double d) {
+    u64 u;
+    std::memcpy(&u, &d, 8);
+    return u;
+  }
+
   Value eval_linear(const Node& n, std::map<std::string, Value>& values) {
     const Context& ctx = *ctx_;
     const CtBatch& x = values.at(n.inputs[0]).cipher;
@@ -993,16 +1026,18 @@ class Executor {
       const u32 K = w.dims[0], Mo = w.dims[1];
       const u32 BM = ctx.wide ? mac_dense_w_bm() : mac_dense_warps(Mo) * 4;
       const u32 Mpad = (Mo + BM - 1) / BM * BM;
-      BufPtr wres = ctx.alloc(static_cast<u64>(L) * K * Mpad * wb, s_);
-      cuda_check(cudaMemsetAsync(wres->ptr, 0, static_cast<u64>(L) * K * Mpad * wb, s_), "memset");
-      int r = encode_f32(ctx, wd, w.data.size(), Mo, Mpad, static_cast<u64>(K) * Mpad, L, s, wres->ptr, s_);
-      check_launch(r, "encode weights");
+      BufPtr wres = encoding(w, {1, L, bits(s), Mpad}, static_cast<u64>(L) * K * Mpad * wb, [&](void* p) {
+        cuda_check(cudaMemsetAsync(p, 0, static_cast<u64>(L) * K * Mpad * wb, s_), "memset");
+        check_launch(encode_f32(ctx, wd, w.data.size(), Mo, Mpad, static_cast<u64>(K) * Mpad, L, s, p, s_),
+                     "encode weights");
+      });
+      int r = 1;
       if (b && x.packing == HG_PACKING_REAL) {
         check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
         const float* bd = weight_dev(ctx, *b, s_);
-        bias_res = ctx.alloc(static_cast<u64>(L) * Mpad * wb, s_);
-        r = encode_f32(ctx, bd, Mo, Mo, Mpad, Mpad, L, acc_scale, bias_res->ptr, s_);
-        check_launch(r, "encode bias");
+        bias_res = encoding(*b, {2, L, bits(acc_scale), Mpad}, static_cast<u64>(L) * Mpad * wb, [&](void* p) {
+          check_launch(encode_f32(ctx, bd, Mo, Mo, Mpad, Mpad, L, acc_scale, p, s_), "encode bias");
+        });
       }
       if (ctx.wide) {
         // Limbs whose prime is < 2^30 (BASELINE c4/c5b: limbs 1..7) go through the int8 tensor
@@ -1109,9 +1144,11 @@ class Executor {
         }
       } else if (ctx.dense_tc && K <= 8192) {
         // tensor-core path: byte-plane weights packed once per call, then tcgen05.mma.kind::i8
-        BufPtr wp = ctx.alloc(tc_packed_weight_bytes(K, Mo, L), s_);
-        r = launch_pack_weights_tc(static_cast<const u32*>(wres->ptr), static_cast<uint8_t*>(wp->ptr), K, Mo, Mpad, L, s_);
-        check_launch(r, "pack weights");
+        BufPtr wp = encoding(w, {3, L, bits(s), Mpad}, tc_packed_weight_bytes(K, Mo, L), [&](void* p) {
+          check_launch(launch_pack_weights_tc(static_cast<const u32*>(wres->ptr), static_cast<uint8_t*>(p), K, Mo,
+                                              Mpad, L, s_),
+                       "pack weights");
+        });
         MacDenseTcArgs a{};
         a.X = x.data();
         a.Y = v.cipher.data();
@@ -1150,16 +1187,18 @@ class Executor {
       const auto& in_shape = x.shape;
       require(in_shape.size() == 3, "Convolution expects a (C,H,W) input");
       const u32 F = n.attrs.filters, C = in_shape[0], win = n.attrs.window;
-      BufPtr wres = ctx.alloc(static_cast<u64>(L) * w.data.size() * wb, s_);
-      int r = encode_f32(ctx, wd, w.data.size(), static_cast<u32>(w.data.size()), static_cast<u32>(w.data.size()),
-                         w.data.size(), L, s, wres->ptr, s_);
-      check_launch(r, "encode weights");
+      BufPtr wres = encoding(w, {4, L, bits(s)}, static_cast<u64>(L) * w.data.size() * wb, [&](void* p) {
+        check_launch(encode_f32(ctx, wd, w.data.size(), static_cast<u32>(w.data.size()),
+                                static_cast<u32>(w.data.size()), w.data.size(), L, s, p, s_),
+                     "encode weights");
+      });
+      int r = 1;
       if (b && x.packing == HG_PACKING_REAL) {
         check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
         const float* bd = weight_dev(ctx, *b, s_);
-        bias_res = ctx.alloc(static_cast<u64>(L) * F * wb, s_);
-        r = encode_f32(ctx, bd, F, F, F, F, L, acc_scale, bias_res->ptr, s_);
-        check_launch(r, "encode bias");
+        bias_res = encoding(*b, {5, L, bits(acc_scale)}, static_cast<u64>(L) * F * wb, [&](void* p) {
+          check_launch(encode_f32(ctx, bd, F, F, F, F, L, acc_scale, p, s_), "encode bias");
+        });
       }
       if (ctx.wide) {
         MacConvArgsW a{};
@@ -2777,5 +2816,14 @@ int hg_refresh_engine_set_relu_clip(hg_refresh_engine* e, double hi) {
   return guard([&] {
     require(e != nullptr, "null argument");
     e->relu_clip = hi;
+  });
+}
+
+int hg_model_keep_encodings(hg_model* m, int on) {
+  return guard([&] {
+    require(m != nullptr, "null argument");
+    m->m.keep_encodings = on != 0;
+    if (!on)
+      for (auto& kv : m->m.weights) kv.second.enc.clear();
   });
 }

@@ -124,6 +124,9 @@ struct WeightTensor {
   float max_abs = 0;
   // device copy (uploaded lazily, per device)
   BufPtr dev;
+  // encodings kept across executes when the model caches weights (Model::keep_encodings):
+  // (context, layout, level, scale bits, ...) -> device residues / packed planes
+  std::map<std::vector<u64>, BufPtr> enc;
 };
 
 struct NodeAttrs {
@@ -147,6 +150,9 @@ struct Model {
   std::map<std::string, std::vector<u32>> shapes;
   std::map<std::string, size_t> index;
   bool finalized = false;
+  // Weight encodings persist across executes, like the reference's shared WeightEncoder
+  // cache filled by precompile_weights (henet/graph.hpp:595-679); off = per-call encoding.
+  bool keep_encodings = false;
   const Node& node(const std::string& id) const { return nodes[index.at(id)]; }
 };
 

@@ -470,6 +470,11 @@ class PlainModel:
     def handle(self):
         return self._h
 
+    def keep_encodings(self, on: bool = True) -> None:
+        """Weight encodings persist across executes (the reference's shared WeightEncoder
+        after precompile_weights, henet/graph.hpp:595-679); results are identical."""
+        check(lib.hg_model_keep_encodings(self._h, int(on)))
+
     def add_weight(self, name: str, dims: Sequence[int], data: np.ndarray) -> None:
         d = np.ascontiguousarray(data, dtype=np.float32).reshape(-1)
         arr = (C.c_uint32 * len(dims))(*dims)

@@ -188,3 +188,22 @@ def test_execute_dense_naive_complex_bias_bit_exact(env):
 
 def test_execute_dense_lazy_complex_bias_bit_exact(env):
     _run_both(env, W.dense_layer(seed=6, k=24, m=5, batch=8192, packing=1))
+
+
+def test_kept_encodings_equal_jit(env):
+    """JIT == precompiled (proj/tests/test_graph.cpp:404-439): a model that keeps its weight
+    encodings across executes gives bit-identical ciphertexts on every run, and again after the
+    cache is dropped."""
+    ctx, ref, keys, rk = env["ctx"], env["ref"], env["keys"], env["rk"]
+    for wl in (W.toy_cryptonets(), W.dense_layer(seed=7, k=60, m=9)):
+        imgs = W.synthetic_images(wl.input_shape, wl.batch, 4)
+        words, sc = ref.encrypt_tensor(keys, imgs, 5, packing=wl.packing)
+        model = H.PlainModel.load(wl.manifest, wl.blob)
+        plan = H.RescalePlan.plan(ctx, model)
+        inp = H.CipherTensor.from_words(ctx, words, sc, shape=wl.input_shape)
+        jit = H.execute(ctx, model, plan, inp, rk).to_words()
+        model.keep_encodings(True)
+        for _ in range(3):
+            assert np.array_equal(H.execute(ctx, model, plan, inp, rk).to_words(), jit)
+        model.keep_encodings(False)
+        assert np.array_equal(H.execute(ctx, model, plan, inp, rk).to_words(), jit)
