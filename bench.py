@@ -581,7 +581,9 @@ def c5b_run(args, ws, rank, local):
     p = Wk.N16384
     ctx = H.CkksContext(p["n"], p["chain"], p["special"], p["scale"], device=local)
     L = len(p["chain"])
-    layer = OutputShardedDense(ctx, Wk.wide_dense_weights(k=C5B_K, m=C5B_M), rank, ws)
+    # ranks > 1: 4 column chunks per rank, each chunk's NCCL all-gather overlapping the next
+    # chunk's evaluation (each chunk is >= 128 neurons: no extra input traffic)
+    layer = OutputShardedDense(ctx, Wk.wide_dense_weights(k=C5B_K, m=C5B_M), rank, ws, chunks=4 if ws > 1 else 1)
     # inputs generated on the device (seeded uniform residues per limb; 8.6 GB)
     x = H.CipherTensor(ctx, C5B_K, 2, L, p["scale"], shape=[C5B_K])
     ctx.synchronize()

@@ -33,3 +33,18 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def chunk_shards(n_items: int, world: int, chunks: int):
+    """Row blocks of a chunked, rank-sharded output: entry [c][r] is the range of global
+    rows rank r produces in its chunk c (rank r's shard split into `chunks` contiguous
+    pieces), so chunk c of every rank can be gathered while chunk c + 1 is computed."""
+    out = []
+    for c in range(chunks):
+        row = []
+        for r in range(world):
+            blk = shard(n_items, r, world)
+            sub = shard(len(blk), c, chunks)
+            row.append(range(blk.start + sub.start, blk.start + sub.stop))
+        out.append(row)
+    return out

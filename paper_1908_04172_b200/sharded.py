@@ -67,44 +67,94 @@ def gather_rows(local, total: int, world: int, group=None):
     return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0)
 
 
+def gather_chunk_into(dst, local, blocks, group=None):
+    """All-gather one chunk: `blocks[r]` is the global row range rank r contributes (its
+    `local` rows on this rank); every rank's rows land in place in `dst` (total, cols)."""
+    import torch
+    import torch.distributed as tdist
+    world = len(blocks)
+    if world == 1:
+        dst[blocks[0].start:blocks[0].stop].copy_(local)
+        return
+    width = max(len(b) for b in blocks)
+    cols = dst.shape[1]
+    send = local
+    if local.shape[0] != width:
+        send = torch.zeros((width, cols), dtype=local.dtype, device=local.device)
+        send[: local.shape[0]] = local
+    parts = torch.empty((world * width, cols), dtype=local.dtype, device=local.device)
+    tdist.all_gather_into_tensor(parts, send.contiguous(), group=group)
+    for r, b in enumerate(blocks):
+        dst[b.start:b.stop].copy_(parts[r * width: r * width + len(b)])
+
+
 class OutputShardedDense:
     """One dense layer K -> M (W row-major K x M, f32) split by output neuron over
     `world` ranks; `forward` returns all M output ciphertexts on every rank."""
 
     def __init__(self, ctx: H.CkksContext, weights, rank: int, world: int, preset: str = "P14",
-                 rescale: bool = True, bias: Optional[Sequence[float]] = None):
+                 rescale: bool = True, bias: Optional[Sequence[float]] = None, chunks: int = 1):
+        """chunks > 1: the rank's neurons are evaluated in `chunks` column blocks, and each
+        block's all-gather (torch's stream) overlaps the next block's evaluation (the
+        context stream).  Chunks of >= 128 neurons cost no extra input traffic: the
+        tensor-core kernel already re-reads the inputs per 128-neuron tile."""
         import numpy as np
-        from . import workloads as Wk
         self.ctx, self.rank, self.world = ctx, rank, world
         w = np.asarray(weights, dtype=np.float32)
         self.K, self.M = w.shape
         self.rows = dist.shard(self.M, rank, world)
+        self.blocks = dist.chunk_shards(self.M, world, max(1, chunks))
+        b = np.asarray(bias, np.float32) if bias is not None else None
+        self.parts = [self._build(w, b, blk[rank], preset, rescale, f"c{c}") for c, blk in enumerate(self.blocks)]
+        self.model, self.plan = self.parts[0] if len(self.parts) == 1 else (None, None)
+
+    def _build(self, w, b, rows, preset, rescale, tag):
+        from . import workloads as Wk
         blob = Wk.Blob()
-        blob.add("fc_w", [self.K, len(self.rows)], w[:, self.rows.start:self.rows.stop])
+        blob.add("fc_w", [self.K, len(rows)], w[:, rows.start:rows.stop])
         nodes = [Wk._node("input", "Input", attrs={"shape": [self.K]}),
                  Wk._node("fc", "Dot", ["input"], weight_ref="fc_w"),
                  Wk._node("out", "Output", ["fc"])]
-        if bias is not None:
-            blob.add("fc_b", [len(self.rows)], np.asarray(bias, np.float32)[self.rows.start:self.rows.stop])
+        if b is not None:
+            blob.add("fc_b", [len(rows)], b[rows.start:rows.stop])
             nodes[1] = Wk._node("fc", "Dot", ["input"], weight_ref="fc_w", bias_ref="fc_b")
-        manifest = json.dumps({"name": f"dense-{self.K}-{self.M}-shard{rank}of{world}", "packing": "real",
-                               "preset": preset, "weights": blob.table, "nodes": nodes})
-        self.manifest, self.blob = manifest, blob.bytes()
-        self.model = H.PlainModel.load(manifest, self.blob)
-        plan = H.RescalePlan.plan(ctx, self.model)
+        manifest = json.dumps({"name": f"dense-{self.K}-{self.M}-shard{self.rank}of{self.world}-{tag}",
+                               "packing": "real", "preset": preset, "weights": blob.table, "nodes": nodes})
+        model = H.PlainModel.load(manifest, blob.bytes())
+        plan = H.RescalePlan.plan(self.ctx, model)
         if rescale:
-            n = len(self.rows)
-            plan = patch_terminal_rescale(ctx.chain, ctx.default_scale, manifest, plan,
+            n = len(rows)
+            plan = patch_terminal_rescale(self.ctx.chain, self.ctx.default_scale, manifest, plan,
                                           {"input": self.K, "fc": n, "out": n})
-        self.plan = plan
+        return model, plan
 
     def local(self, x: H.CipherTensor) -> H.CipherTensor:
-        """This rank's output ciphertexts (rows `self.rows`)."""
+        """This rank's output ciphertexts (rows `self.rows`; single-chunk layers)."""
+        assert len(self.parts) == 1, "local() is for single-chunk layers; use forward()"
         return H.execute(self.ctx, self.model, self.plan, x)
 
     def forward(self, x: H.CipherTensor, group=None) -> H.CipherTensor:
-        y = self.local(x)
-        return self.gather(y, group)
+        if len(self.parts) == 1:
+            return self.gather(self.local(x), group)
+        import torch
+        dev = self.ctx.device
+        ext = torch.cuda.ExternalStream(self.ctx.stream(), device=dev)
+        cur = torch.cuda.current_stream(dev)
+        full = None
+        keep = []
+        for c, (model, plan) in enumerate(self.parts):
+            y = H.execute(self.ctx, model, plan, x)  # enqueued on the context stream
+            if full is None:
+                cnt, polys, level, scale, packing = y.info()
+                full = H.CipherTensor(self.ctx, self.M, polys, level, scale, packing, shape=[self.M])
+            ev = torch.cuda.Event()
+            ev.record(ext)
+            cur.wait_event(ev)  # chunk c's gather waits for chunk c only
+            gather_chunk_into(full.torch_view(dev), y.torch_view(dev), self.blocks[c], group)
+            keep.append(y)  # freed after the gathers (ext waits on cur below)
+        ext.wait_stream(cur)
+        del keep
+        return full
 
     def gather(self, y: H.CipherTensor, group=None) -> H.CipherTensor:
         """All-gather the output ciphertexts.  Stream-ordered, no host synchronisation:

@@ -29,6 +29,56 @@ def _gather_worker(rank, world, port, q):
     tdist.destroy_process_group()
 
 
+def _chunk_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as tdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1908_04172_b200.sharded import gather_chunk_into
+    out = []
+    for total in (5, 6, 13, 2):
+        for chunks in (1, 2, 3):
+            blocks = dist.chunk_shards(total, world, chunks)
+            dst = torch.full((total, 7), -1, dtype=torch.int64)
+            for c in range(chunks):
+                mine = blocks[c][rank]
+                local = torch.tensor([[1000 * i + k for k in range(7)] for i in mine], dtype=torch.int64).reshape(-1, 7)
+                gather_chunk_into(dst, local, blocks[c])
+            out.append(dst.numpy())
+    q.put((rank, out))
+    tdist.destroy_process_group()
+
+
+def test_chunked_gather_gloo_world2():
+    """Chunk c of every rank's shard lands in its global rows (the overlapped c5b gather)."""
+    mp = pytest.importorskip("torch.multiprocessing")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_chunk_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    k = 0
+    for total in (5, 6, 13, 2):
+        for chunks in (1, 2, 3):
+            want = np.array([[1000 * i + c for c in range(7)] for i in range(total)], dtype=np.int64)
+            assert np.array_equal(res[0][k], want) and np.array_equal(res[1][k], want), (total, chunks)
+            k += 1
+    # every row is produced exactly once
+    for total in (5, 6, 13, 2):
+        for world in (1, 2, 3, 8):
+            for chunks in (1, 2, 4):
+                rows = [i for c in dist.chunk_shards(total, world, chunks) for b in c for i in b]
+                assert sorted(rows) == list(range(total)), (total, world, chunks)
+
+
 def test_gather_rows_gloo_world2():
     mp = pytest.importorskip("torch.multiprocessing")
     s = socket.socket()
@@ -94,3 +144,5 @@ def test_output_sharded_dense_bit_exact():
     assert np.array_equal(full.to_words(), want)
     one = OutputShardedDense(ctx, wts, 0, 1)
     assert np.array_equal(one.forward(xt).to_words(), want)  # world 1: local + gather path
+    chunked = OutputShardedDense(ctx, wts, 0, 1, chunks=3)  # overlapped-gather path
+    assert np.array_equal(chunked.forward(xt).to_words(), want)
