@@ -366,6 +366,8 @@ static void run_ew(const Context& ctx, EwArgs a, cudaStream_t s) {
     w.polys_out = a.polys_out;
     w.level = a.level;
     w.N = a.N;
+    w.gidx = a.gidx;
+    w.gw = a.gw;
     r = launch_elementwise_w(w, ctx.basisw, s);
   } else {
     r = launch_elementwise(a, ctx.basis, s);
@@ -1341,9 +1343,8 @@ class Executor {
   // rescale(0) = 0), rescales the M terms as one batch and adds them into the accumulators.
   Value eval_linear_naive(const Node& n, const CtBatch& x, WeightTensor& w, WeightTensor* b) {
     const Context& ctx = *ctx_;
-    if (ctx.wide)
-      throw Error(HG_ERR_UNSUPPORTED, "naive per-term rescaling with primes >= 2^30 is not implemented on the GPU path");
     require(x.level >= 2, "cannot rescale below level 1");
+    const size_t wb = ctx.word_bytes();
     const double s = ctx.default_scale;
     const u32 L = x.level;
     const auto& out_shape = model_.shapes.at(n.id);
@@ -1392,7 +1393,7 @@ class Executor {
     // weight residues element-major [count][L]
     const float* wd = weight_dev(ctx, w, s_);
     const u64 wc = w.data.size();
-    BufPtr wres = ctx.alloc(wc * L * 4, s_);
+    BufPtr wres = ctx.alloc(wc * L * wb, s_);
     check_launch(encode_f32(ctx, wd, wc, 1, L, 1, L, s, wres->ptr, s_), "encode weights");
 
     CtBatch term;
@@ -1449,7 +1450,7 @@ class Executor {
       if (x.packing == HG_PACKING_REAL) {
         // encode_broadcast of a real scalar: the expanded constant (henet/encoding.hpp:210-219)
         const float* bd = weight_dev(ctx, *b, s_);
-        bias_res = ctx.alloc(b->data.size() * bl * 4, s_);
+        bias_res = ctx.alloc(b->data.size() * bl * wb, s_);
         check_launch(encode_f32(ctx, bd, b->data.size(), 1, bl, 1, bl, acc.scale, bias_res->ptr, s_), "encode bias");
         e.op = EwOp::AddScalar;
         e.res = static_cast<const u32*>(bias_res->ptr);

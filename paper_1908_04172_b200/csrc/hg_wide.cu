@@ -269,6 +269,18 @@ __global__ void k_ew_w(EwArgsW a, BasisW B) {
       }
       break;
     }
+    case EwOp::GatherMul: {
+      const u32 src = a.gidx[e];
+      if (src == 0xFFFFFFFFu) {
+        o = make_ulonglong2(0, 0);
+      } else {
+        const ulonglong2 x =
+            *reinterpret_cast<const ulonglong2*>(a.a + ((static_cast<u64>(src) * a.polys_a + poly) * a.level + limb) * N + n);
+        const u64 r = a.res[static_cast<u64>(a.gw[e]) * a.level + limb];
+        o = make_ulonglong2(mulmod_w(x.x, r, P), mulmod_w(x.y, r, P));
+      }
+      break;
+    }
     case EwOp::AddVector: {
       o = ld(a.a, a.polys_a, poly);
       if (poly == 0) {

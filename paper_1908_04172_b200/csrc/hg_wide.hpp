@@ -49,6 +49,8 @@ struct EwArgsW {
   u64* out;
   u64 count;
   u32 polys_a, polys_out, level, N;
+  const u32* gidx;  // GatherMul (EwArgs)
+  const u32* gw;
 };
 
 int launch_ntt_w(int logn, u64* data, u64 rows, u32 level, bool inverse, const BasisW& B, cudaStream_t s);

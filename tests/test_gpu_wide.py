@@ -63,14 +63,15 @@ def test_encoders_wide(env):
     assert np.array_equal(H.encode_vector(ctx, s, 8, p["scale"]), ref.encode_vector(s, 8, p["scale"]))
 
 
-def _run_both(env, wl, count_override=None, seed=7):
+def _run_both(env, wl, count_override=None, seed=7, mode=0):
     ctx, ref, p = env["ctx"], env["ref"], env["p"]
     x = W.random_ciphertexts(p, wl.input_count, seed=seed)
-    want, want_sc, st = ref.execute(None, wl.manifest, wl.blob, x, p["scale"], patch=wl.patch_terminal_rescale)
-    rp = ref.plan(wl.manifest, wl.blob, patch=wl.patch_terminal_rescale)
+    want, want_sc, st = ref.execute(None, wl.manifest, wl.blob, x, p["scale"], mode=mode,
+                                    patch=wl.patch_terminal_rescale)
+    rp = ref.plan(wl.manifest, wl.blob, mode=mode, patch=wl.patch_terminal_rescale)
     nodes = {n["id"]: (n["decision"], n["level_in"], n["level_out"],
                        np.array([n["scale_out_bits"]], dtype=np.uint64).view(np.float64)[0]) for n in rp["nodes"]}
-    plan = H.RescalePlan.from_nodes(0, rp["planned_rescale_ops"], nodes)
+    plan = H.RescalePlan.from_nodes(mode, rp["planned_rescale_ops"], nodes)
     model = H.PlainModel.load(wl.manifest, wl.blob)
     out = H.execute(ctx, model, plan, H.CipherTensor.from_words(ctx, x, p["scale"], shape=wl.input_shape))
     assert out.scale == want_sc
@@ -80,6 +81,11 @@ def _run_both(env, wl, count_override=None, seed=7):
 def test_dense_c5b_shape_small_bit_exact(env):
     """c5b topology (dense + one rescale per output, 40-bit limb 0) at K=96, M=40."""
     _run_both(env, W.wide_dense(k=96, m=40))
+
+
+def test_dense_naive_wide_bit_exact(env):
+    """Naive per-term rescaling with the 40-bit limb (hybrid u32 / u64 rescale per term)."""
+    _run_both(env, W.wide_dense(k=12, m=5), mode=1)
 
 
 def test_conv_c4_shape_small_bit_exact(env):
