@@ -106,7 +106,7 @@ __global__ void k_pack_weights_tc(const u32* W, uint8_t* Wp, u32 K, u32 Mpad, u3
 }
 
 // ---------------------------------------------------------------------------
-// Main kernel.  grid = (N / 64, Mtiles, polys * level), 288 threads:
+// Main kernel.  grid = (Mtiles, N / TN, polys * level), 288 threads:
 //   warps 0-7  producers: X(ks) -> byte planes B[ks % S]; then the epilogue
 //   warp 8     lane 0: weight planes by cp.async.bulk into A[], MMA issue, commits
 // Rings: full_a (tx bytes), full_b (256 producer arrivals), empty (MMA commit).
@@ -117,8 +117,10 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
   TcSmem<TN>& S = *reinterpret_cast<TcSmem<TN>*>(tc_raw);
   constexpr u32 kCols = tc_cols<TN>();
   const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const u32 n0 = blockIdx.x * TN;
-  const u32 mt = blockIdx.y;
+  // M tiles fastest: the CTAs in flight share their input columns (read from HBM once, the
+  // other M tiles hit L2) while each M tile's weight planes stay L2-resident across N tiles
+  const u32 mt = blockIdx.x;
+  const u32 n0 = blockIdx.y * TN;
   const u32 poly = blockIdx.z / a.level, limb = blockIdx.z % a.level;
   const DevPrime& P = B.p[limb];
   const u32 planes = a.planes[limb];  // 3 for q < 2^24, 4 otherwise
@@ -329,8 +331,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc_w(MacDenseTcWArg
   extern __shared__ __align__(1024) uint8_t tcw_raw[];
   TcSmemW& S = *reinterpret_cast<TcSmemW*>(tcw_raw);
   const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const u32 n0 = blockIdx.x * kTwN;
-  const u32 mt = blockIdx.y;
+  const u32 mt = blockIdx.x;  // M tiles fastest (see k_mac_dense_tc)
+  const u32 n0 = blockIdx.y * kTwN;
   const u32 poly = blockIdx.z;
   const u32 KS = a.Ksteps;
 
@@ -590,7 +592,7 @@ int launch_mac_dense_tc_w(MacDenseTcWArgs a, const void* P, cudaStream_t s) {
     cudaFuncSetAttribute(k_mac_dense_tc_w, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
-  dim3 grid(a.N / kTwN, a.Mtiles, a.polys);
+  dim3 grid(a.Mtiles, a.N / kTwN, a.polys);
   ProfScope ps("k_mac_dense_tc_w", s);
   k_mac_dense_tc_w<<<grid, kTcThreads, smem, s>>>(a, *static_cast<const DevPrimeW*>(P));
   return 1;
@@ -607,7 +609,7 @@ static void tc_launch(const MacDenseTcArgs& a, const Basis& B, cudaStream_t s) {
     cudaFuncSetAttribute(k_mac_dense_tc<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
-  dim3 grid(a.N / TN, a.Mtiles, a.polys * a.level);
+  dim3 grid(a.Mtiles, a.N / TN, a.polys * a.level);
   ProfScope ps("k_mac_dense_tc", s);
   k_mac_dense_tc<TN><<<grid, kTcThreads, smem, s>>>(a, B);
 }
