@@ -1104,13 +1104,9 @@ class Executor {
         if (r >= 0 && tc_lo < L) {
           check_launch(r, "mac_dense_w");
           const u32 cnt = L - tc_lo;
-          // u32 copies: inputs [K][2][cnt][N], weights [cnt][K][Mpad], bias [cnt][Mpad]
-          BufPtr xn = ctx.alloc(static_cast<u64>(K) * 2 * cnt * N * 4, s_);
-          BufPtr yn = ctx.alloc(static_cast<u64>(Mo) * 2 * cnt * N * 4, s_);
+          // the kernel reads and writes those limbs of the u64 tensors in place; u32 copies
+          // of the (small) weights [cnt][K][Mpad] and bias [cnt][Mpad]
           BufPtr wn = ctx.alloc(static_cast<u64>(cnt) * K * Mpad * 4, s_);
-          check_launch(launch_limbs_to_u32(x.data64(), static_cast<u32*>(xn->ptr), static_cast<u64>(K) * 2, x.level,
-                                           tc_lo, cnt, N, s_),
-                       "narrow inputs");
           check_launch(launch_limbs_to_u32(static_cast<const u64*>(wres->ptr), static_cast<u32*>(wn->ptr), 1, L, tc_lo,
                                            cnt, static_cast<u32>(static_cast<u64>(K) * Mpad), s_),
                        "narrow weights");
@@ -1128,8 +1124,10 @@ class Executor {
           Basis sub{};  // the narrow constants of limbs tc_lo.. (every basis entry < 2^32 is valid)
           for (u32 i = 0; i < cnt; ++i) sub.p[i] = ctx.basis.p[tc_lo + i];
           MacDenseTcArgs t{};
-          t.X = static_cast<const u32*>(xn->ptr);
-          t.Y = static_cast<u32*>(yn->ptr);
+          t.X64 = x.data64();
+          t.Y64 = v.cipher.data64();
+          t.limb_off = tc_lo;
+          t.y_level = L;
           t.Wp = static_cast<const uint8_t*>(wp->ptr);
           t.bias = bn ? static_cast<const u32*>(bn->ptr) : nullptr;
           t.K = K;
@@ -1138,11 +1136,9 @@ class Executor {
           t.N = N;
           t.level = cnt;
           t.polys = 2;
-          t.x_level = cnt;
+          t.x_level = x.level;
           for (u32 i = 0; i < cnt; ++i) t.planes[i] = ctx.chain[tc_lo + i] < (1ull << 24) ? 3 : 4;
-          check_launch(launch_mac_dense_tc(t, sub, s_), "mac_dense_tc");
-          r = launch_limbs_to_u64(static_cast<const u32*>(yn->ptr), v.cipher.data64(), static_cast<u64>(Mo) * 2, L, tc_lo,
-                                  cnt, N, s_);
+          r = launch_mac_dense_tc(t, sub, s_);
         }
       } else if (ctx.dense_tc && K <= 8192) {
         // tensor-core path: byte-plane weights packed once per call, then tcgen05.mma.kind::i8

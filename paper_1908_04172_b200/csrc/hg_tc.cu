@@ -44,13 +44,15 @@ constexpr int kTcCols = 512;                      // TMEM columns of the wide ke
 #endif
 constexpr u32 kTcSmallK = HG_TC_SMALLK;           // K at or below which the N = 32 tile is used
 
-template <int TN>
+// XW: the input residue word -- u32, or u64 when the limbs are read straight out of a wide
+// (u64) tensor (the 30-bit limbs of BASELINE c4/c5b), so no narrowed copy is needed.
+template <int TN, typename XW = u32>
 struct TcSmem {
   uint8_t a[kTcS][4][kTcPlaneA];  // weight planes (K-major core matrices), filled by cp.async.bulk
   uint8_t b[kTcS][4][TN * kTcK];  // input planes, written by the producer warps; the planes of a
                                   // stage are consecutive, i.e. one K-major (planes*TN) x 32 matrix
   uint8_t zero_a[kTcPlaneA];      // zero weight plane: initialises the upper accumulators
-  u32 xs[kTcXS][kTcK][TN];        // input residues staged by cp.async (producer ring)
+  XW xs[kTcXS][kTcK][TN];         // input residues staged by cp.async (producer ring)
   unsigned long long full_a[kTcS], full_b[kTcS], empty[kTcS];
   u32 tmem;
 };
@@ -111,10 +113,11 @@ __global__ void k_pack_weights_tc(const u32* W, uint8_t* Wp, u32 K, u32 Mpad, u3
 //   warp 8     lane 0: weight planes by cp.async.bulk into A[], MMA issue, commits
 // Rings: full_a (tx bytes), full_b (256 producer arrivals), empty (MMA commit).
 // ---------------------------------------------------------------------------
-template <int TN>
+template <int TN, typename XW = u32>
 __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(MacDenseTcArgs a, Basis B) {
   extern __shared__ __align__(1024) uint8_t tc_raw[];
-  TcSmem<TN>& S = *reinterpret_cast<TcSmem<TN>*>(tc_raw);
+  TcSmem<TN, XW>& S = *reinterpret_cast<TcSmem<TN, XW>*>(tc_raw);
+  constexpr bool kWide = sizeof(XW) == 8;
   constexpr u32 kCols = tc_cols<TN>();
   const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // M tiles fastest: the CTAs in flight share their input columns (read from HBM once, the
@@ -202,15 +205,17 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
     // them back (so a __syncwarp, not a CTA barrier, orders the two) and writes their byte
     // planes, lane l for columns l and l + 32; one elected lane arrives per warp. =====
     const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
-    const u32* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n0;
+    const XW* Xb = static_cast<const XW*>(kWide ? static_cast<const void*>(a.X64) : static_cast<const void*>(a.X)) +
+                   (static_cast<u64>(poly) * a.x_level + a.limb_off + limb) * a.N + n0;
     const u32 r0 = warp * 4;
+    constexpr int kPer = 16 / sizeof(XW);  // residues per 16-byte chunk
     auto issue = [&](u32 ks) {
-      // 4 rows x TN residues = TN chunks of 16 B, TN / 32 per lane; rows >= K zero-fill
+      // 4 rows x TN residues = 4 TN / kPer chunks of 16 B per warp; rows >= K zero-fill
 #pragma unroll
-      for (int i = 0; i < TN / 32; ++i) {
-        const u32 c = lane + i * 32, row = r0 + c / (TN / 4), c4 = (c % (TN / 4)) * 4;
+      for (int i = 0; i < 4 * TN / kPer / 32; ++i) {
+        const u32 c = lane + i * 32, row = r0 + c / (TN / kPer), c4 = (c % (TN / kPer)) * kPer;
         const u32 k = ks * kTcK + row;
-        const u32* src = Xb + static_cast<u64>(k < a.K ? k : 0) * xstride + c4;
+        const XW* src = Xb + static_cast<u64>(k < a.K ? k : 0) * xstride + c4;
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(&S.xs[ks % kTcXS][row][c4])),
                      "l"(src), "r"(k < a.K ? 16 : 0));
       }
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
 #pragma unroll
       for (int h = 0; h < TN / 32; ++h)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[h][i] = S.xs[ks % kTcXS][r0 + i][lane + 32 * h];
+        for (int i = 0; i < 4; ++i) v[h][i] = static_cast<u32>(S.xs[ks % kTcXS][r0 + i][lane + 32 * h]);
       __syncwarp();  // step ks's rows are consumed before the ring slot is refilled
       if (ks + kTcXS - 1 < KS) issue(ks + kTcXS - 1);
       asm volatile("cp.async.commit_group;\n" ::);
@@ -279,9 +284,15 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
         u32 o[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) o[i] = addmod(reduce64(acc[i], P), bv, q);
-        u32* yp = a.Y + ((static_cast<u64>(m) * a.polys + poly) * a.level + limb) * a.N + n0 + col;
-        *reinterpret_cast<uint4*>(yp) = make_uint4(o[0], o[1], o[2], o[3]);
-        *reinterpret_cast<uint4*>(yp + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+        if constexpr (kWide) {
+          u64* yp = a.Y64 + ((static_cast<u64>(m) * a.polys + poly) * a.y_level + a.limb_off + limb) * a.N + n0 + col;
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) *reinterpret_cast<ulonglong2*>(yp + i) = make_ulonglong2(o[i], o[i + 1]);
+        } else {
+          u32* yp = a.Y + ((static_cast<u64>(m) * a.polys + poly) * a.level + limb) * a.N + n0 + col;
+          *reinterpret_cast<uint4*>(yp) = make_uint4(o[0], o[1], o[2], o[3]);
+          *reinterpret_cast<uint4*>(yp + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+        }
       }
     }
   }
@@ -598,20 +609,21 @@ int launch_mac_dense_tc_w(MacDenseTcWArgs a, const void* P, cudaStream_t s) {
   return 1;
 }
 
-template <int TN>
+template <int TN, typename XW>
 static void tc_launch(const MacDenseTcArgs& a, const Basis& B, cudaStream_t s) {
   // TN = 64: request enough shared memory that only one CTA is resident per SM (512 TMEM
-  // columns), so no CTA spins in tcgen05.alloc; TN = 32: two CTAs of 256 columns.
-  constexpr size_t smem = TN == 64 ? (sizeof(TcSmem<TN>) > 120 * 1024 ? sizeof(TcSmem<TN>) : 120 * 1024)
-                                   : sizeof(TcSmem<TN>);
+  // columns), so no CTA spins in tcgen05.alloc; TN = 32: two CTAs of 256 columns (one with
+  // u64 inputs, whose staging ring is twice the size).
+  constexpr size_t smem = TN == 64 ? (sizeof(TcSmem<TN, XW>) > 120 * 1024 ? sizeof(TcSmem<TN, XW>) : 120 * 1024)
+                                   : sizeof(TcSmem<TN, XW>);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_mac_dense_tc<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_mac_dense_tc<TN, XW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
   dim3 grid(a.Mtiles, a.N / TN, a.polys * a.level);
   ProfScope ps("k_mac_dense_tc", s);
-  k_mac_dense_tc<TN><<<grid, kTcThreads, smem, s>>>(a, B);
+  k_mac_dense_tc<TN, XW><<<grid, kTcThreads, smem, s>>>(a, B);
 }
 
 int launch_mac_dense_tc(MacDenseTcArgs a, const Basis& B, cudaStream_t s) {
@@ -632,10 +644,11 @@ int launch_mac_dense_tc(MacDenseTcArgs a, const Basis& B, cudaStream_t s) {
     return e ? atoi(e) : 0;
   }();
   const int tn = tn_env ? tn_env : (a.K <= kTcSmallK ? 32 : 64);
+  const bool wio = a.X64 != nullptr;
   if (tn == 32)
-    tc_launch<32>(a, B, s);
+    wio ? tc_launch<32, u64>(a, B, s) : tc_launch<32, u32>(a, B, s);
   else
-    tc_launch<64>(a, B, s);
+    wio ? tc_launch<64, u64>(a, B, s) : tc_launch<64, u32>(a, B, s);
   return 1;
 }
 

@@ -16,6 +16,12 @@ struct MacDenseTcArgs {
   const u32* bias;       // [level][Mpad] or nullptr
   u32 K, M, Mpad, N, level, polys, x_level;
   u32 Mtiles, Ksteps;    // filled by the launcher
+  // Wide I/O (X64 != nullptr): limbs [limb_off, limb_off + level) of u64 tensors are read and
+  // written in place -- X64 [K][x_polys][x_level][N], Y64 [M][polys][y_level][N] -- instead
+  // of X / Y; the Basis passed covers those limbs (index 0 = limb_off)
+  const u64* X64;
+  u64* Y64;
+  u32 limb_off, y_level;
   u32 planes[kMaxPrimes];  // byte planes per limb: 3 if q < 2^24 else 4
   u64 cs[kMaxPrimes][7];   // 2^(8s) mod q per limb (filled by the launcher)
 };
