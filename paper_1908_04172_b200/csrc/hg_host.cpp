@@ -1184,117 +1184,163 @@ class Executor {
     } else {
       const auto& in_shape = x.shape;
       require(in_shape.size() == 3, "Convolution expects a (C,H,W) input");
-      const u32 F = n.attrs.filters, C = in_shape[0], win = n.attrs.window;
-      BufPtr wres = encoding(w, {4, L, bits(s)}, static_cast<u64>(L) * w.data.size() * wb, [&](void* p) {
-        check_launch(encode_f32(ctx, wd, w.data.size(), static_cast<u32>(w.data.size()),
-                                static_cast<u32>(w.data.size()), w.data.size(), L, s, p, s_),
-                     "encode weights");
-      });
-      int r = 1;
-      if (b && x.packing == HG_PACKING_REAL) {
-        check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
-        const float* bd = weight_dev(ctx, *b, s_);
-        bias_res = encoding(*b, {5, L, bits(acc_scale)}, static_cast<u64>(L) * F * wb, [&](void* p) {
-          check_launch(encode_f32(ctx, bd, F, F, F, F, L, acc_scale, p, s_), "encode bias");
-        });
-      }
-      if (ctx.wide) {
-        MacConvArgsW a{};
-        a.X = x.data64();
-        a.Y = v.cipher.data64();
-        a.W = static_cast<const u64*>(wres->ptr);
-        a.bias = bias_res ? static_cast<const u64*>(bias_res->ptr) : nullptr;
-        a.C = C;
-        a.IH = in_shape[1];
-        a.IW = in_shape[2];
-        a.F = F;
-        a.OH = out_shape[1];
-        a.OW = out_shape[2];
-        a.win = win;
-        a.stride = n.attrs.stride;
-        a.pad_top = n.attrs.pad[0];
-        a.pad_left = n.attrs.pad[1];
-        a.level = L;
-        a.polys = 2;
-        a.x_level = x.level;
-        a.N = N;
-        r = launch_mac_conv_w(a, ctx.basisw, s_);
-      } else {
-        MacConvArgs a{};
-        a.X = x.data();
-        a.Y = v.cipher.data();
-        a.W = static_cast<const u32*>(wres->ptr);
-        a.bias = bias_res ? static_cast<const u32*>(bias_res->ptr) : nullptr;
-        a.C = C;
-        a.IH = in_shape[1];
-        a.IW = in_shape[2];
-        a.F = F;
-        a.OH = out_shape[1];
-        a.OW = out_shape[2];
-        a.win = win;
-        a.stride = n.attrs.stride;
-        a.pad_top = n.attrs.pad[0];
-        a.pad_left = n.attrs.pad[1];
-        a.level = L;
-        a.polys = 2;
-        a.x_level = x.level;
-        a.N = N;
-        // valid-tap table per output position (geometry only; henet/graph.hpp:976-989),
-        // cached on the context: (input element, window tap), ascending per position
-        {
-          const u32 npos = a.OH * a.OW;
-          // entries carry the input's word offset (element * polys * x_level * N): no address
-          // multiply per tap in the kernel
-          const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
-          require(static_cast<u64>(C) * a.IH * a.IW * xstride < (1ull << 32),
-                  "convolution input too large for 32-bit tap offsets");
-          const std::vector<u32> key = {C, a.IH, a.IW, a.OH, a.OW, win, a.stride, a.pad_top, a.pad_left,
-                                        static_cast<u32>(xstride)};
-          std::lock_guard<std::mutex> g(ctx.geo_mu);
-          BufPtr& tb = ctx.geo_cache[key];
-          const size_t toff = ((npos + 1) * 4 + 15) / 16 * 16;
-          if (!tb) {
-            std::vector<u32> tab(npos + 1);
-            std::vector<uint2> taps;
-            for (u32 oy = 0; oy < a.OH; ++oy)
-              for (u32 ox = 0; ox < a.OW; ++ox) {
-                for (u32 c = 0; c < C; ++c)
-                  for (u32 ky = 0; ky < win; ++ky)
-                    for (u32 kx = 0; kx < win; ++kx) {
-                      const int iy = static_cast<int>(oy * a.stride + ky) - static_cast<int>(a.pad_top);
-                      const int ix = static_cast<int>(ox * a.stride + kx) - static_cast<int>(a.pad_left);
-                      if (iy < 0 || iy >= static_cast<int>(a.IH) || ix < 0 || ix >= static_cast<int>(a.IW)) continue;
-                      taps.push_back(make_uint2(
-                          static_cast<u32>(((c * a.IH + static_cast<u32>(iy)) * a.IW + static_cast<u32>(ix)) * xstride),
-                          (c * win + ky) * win + kx));
-                    }
-                tab[oy * a.OW + ox + 1] = static_cast<u32>(taps.size());
-              }
-            tb = ctx.alloc(toff + taps.size() * 8 + 16, s_);
-            cuda_check(cudaMemcpyAsync(tb->ptr, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, s_), "taps");
-            if (!taps.empty())
-              cuda_check(cudaMemcpyAsync(static_cast<char*>(tb->ptr) + toff, taps.data(), taps.size() * 8,
-                                         cudaMemcpyHostToDevice, s_),
-                         "taps");
-            cuda_check(cudaStreamSynchronize(s_), "taps");  // host vectors leave scope
+      const u32 F = n.attrs.filters, C = in_shape[0], win = n.attrs.window, T2 = win * win;
+      // one launch of the convolution kernel on (X, Y, Wr, Bi) with Cc channels, Ff filters
+      auto run_conv = [&](const void* X, void* Y, const void* Wr, const void* Bi, u32 Cc, u32 Ff) {
+        int r = 1;
+        if (ctx.wide) {
+          MacConvArgsW a{};
+          a.X = static_cast<const u64*>(X);
+          a.Y = static_cast<u64*>(Y);
+          a.W = static_cast<const u64*>(Wr);
+          a.bias = static_cast<const u64*>(Bi);
+          a.C = Cc;
+          a.IH = in_shape[1];
+          a.IW = in_shape[2];
+          a.F = Ff;
+          a.OH = out_shape[1];
+          a.OW = out_shape[2];
+          a.win = win;
+          a.stride = n.attrs.stride;
+          a.pad_top = n.attrs.pad[0];
+          a.pad_left = n.attrs.pad[1];
+          a.level = L;
+          a.polys = 2;
+          a.x_level = x.level;
+          a.N = N;
+          r = launch_mac_conv_w(a, ctx.basisw, s_);
+        } else {
+          MacConvArgs a{};
+          a.X = static_cast<const u32*>(X);
+          a.Y = static_cast<u32*>(Y);
+          a.W = static_cast<const u32*>(Wr);
+          a.bias = static_cast<const u32*>(Bi);
+          a.C = Cc;
+          a.IH = in_shape[1];
+          a.IW = in_shape[2];
+          a.F = Ff;
+          a.OH = out_shape[1];
+          a.OW = out_shape[2];
+          a.win = win;
+          a.stride = n.attrs.stride;
+          a.pad_top = n.attrs.pad[0];
+          a.pad_left = n.attrs.pad[1];
+          a.level = L;
+          a.polys = 2;
+          a.x_level = x.level;
+          a.N = N;
+          // valid-tap table per output position (geometry only; henet/graph.hpp:976-989),
+          // cached on the context: (input element, window tap), ascending per position
+          {
+            const u32 npos = a.OH * a.OW;
+            // entries carry the input's word offset (element * polys * x_level * N): no address
+            // multiply per tap in the kernel
+            const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
+            require(static_cast<u64>(Cc) * a.IH * a.IW * xstride < (1ull << 32),
+                    "convolution input too large for 32-bit tap offsets");
+            const std::vector<u32> key = {Cc, a.IH, a.IW, a.OH, a.OW, win, a.stride, a.pad_top, a.pad_left,
+                                          static_cast<u32>(xstride)};
+            std::lock_guard<std::mutex> g(ctx.geo_mu);
+            BufPtr& tb = ctx.geo_cache[key];
+            const size_t toff = ((npos + 1) * 4 + 15) / 16 * 16;
+            if (!tb) {
+              std::vector<u32> tab(npos + 1);
+              std::vector<uint2> taps;
+              for (u32 oy = 0; oy < a.OH; ++oy)
+                for (u32 ox = 0; ox < a.OW; ++ox) {
+                  for (u32 c = 0; c < Cc; ++c)
+                    for (u32 ky = 0; ky < win; ++ky)
+                      for (u32 kx = 0; kx < win; ++kx) {
+                        const int iy = static_cast<int>(oy * a.stride + ky) - static_cast<int>(a.pad_top);
+                        const int ix = static_cast<int>(ox * a.stride + kx) - static_cast<int>(a.pad_left);
+                        if (iy < 0 || iy >= static_cast<int>(a.IH) || ix < 0 || ix >= static_cast<int>(a.IW)) continue;
+                        taps.push_back(make_uint2(
+                            static_cast<u32>(((c * a.IH + static_cast<u32>(iy)) * a.IW + static_cast<u32>(ix)) * xstride),
+                            (c * win + ky) * win + kx));
+                      }
+                  tab[oy * a.OW + ox + 1] = static_cast<u32>(taps.size());
+                }
+              tb = ctx.alloc(toff + taps.size() * 8 + 16, s_);
+              cuda_check(cudaMemcpyAsync(tb->ptr, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, s_), "taps");
+              if (!taps.empty())
+                cuda_check(cudaMemcpyAsync(static_cast<char*>(tb->ptr) + toff, taps.data(), taps.size() * 8,
+                                           cudaMemcpyHostToDevice, s_),
+                           "taps");
+              cuda_check(cudaStreamSynchronize(s_), "taps");  // host vectors leave scope
+            }
+            a.tap_off = static_cast<const u32*>(tb->ptr);
+            a.taps = reinterpret_cast<const uint2*>(static_cast<const char*>(tb->ptr) + toff);
           }
-          a.tap_off = static_cast<const u32*>(tb->ptr);
-          a.taps = reinterpret_cast<const uint2*>(static_cast<const char*>(tb->ptr) + toff);
+          static const bool fp64_on = [] {
+            const char* e = getenv("HG_CONV_FP64");
+            return !(e != nullptr && e[0] == '0');
+          }();
+          for (u32 i = 0; i < L; ++i) {
+            const long double qm1 = static_cast<long double>(ctx.chain[i] - 1);
+            const u32 taps = Cc * win * win;
+            a.fold[i] = (qm1 * qm1 * taps >= 18446744073709551616.0L) ? 1 : 0;
+            // a sum of `taps` products of residues is an integer < 2^53: exact in double
+            a.fp64[i] = (fp64_on && taps <= 32 && qm1 * qm1 * taps < 9007199254740992.0L) ? 1 : 0;
+          }
+          r = launch_mac_conv(a, ctx.basis, s_);
         }
-        static const bool fp64_on = [] {
-          const char* e = getenv("HG_CONV_FP64");
-          return !(e != nullptr && e[0] == '0');
-        }();
-        for (u32 i = 0; i < L; ++i) {
-          const long double qm1 = static_cast<long double>(ctx.chain[i] - 1);
-          const u32 taps = C * win * win;
-          a.fold[i] = (qm1 * qm1 * taps >= 18446744073709551616.0L) ? 1 : 0;
-          // a sum of `taps` products of residues is an integer < 2^53: exact in double
-          a.fp64[i] = (fp64_on && taps <= 32 && qm1 * qm1 * taps < 9007199254740992.0L) ? 1 : 0;
-        }
-        r = launch_mac_conv(a, ctx.basis, s_);
+        check_launch(r, "mac_conv");
+      };
+      // Depthwise weights (F == C, w[f][c] == 0 for f != c): the reference evaluates them as a
+      // full convolution whose off-diagonal taps are exact zeros (it has no grouped
+      // convolution); a zero residue adds nothing to a canonical sum, so each
+      // channel runs as its own 1 -> 1 convolution on its slices (9 taps instead of 9 C).
+      if (w.depthwise < 0) {
+        bool dw = F == C && C > 1;
+        for (u32 f = 0; dw && f < F; ++f)
+          for (u32 c = 0; dw && c < C; ++c)
+            if (c != f)
+              for (u32 t = 0; dw && t < T2; ++t) dw = w.data[(static_cast<u64>(f) * C + c) * T2 + t] == 0.0f;
+        w.depthwise = dw ? 1 : 0;
       }
-      check_launch(r, "mac_conv");
+      if (w.depthwise == 1) {
+        BufPtr dg = encoding(w, {6}, static_cast<u64>(C) * T2 * 4, [&](void* p) {
+          std::vector<float> diag(static_cast<u64>(C) * T2);
+          for (u32 c = 0; c < C; ++c)
+            for (u32 t = 0; t < T2; ++t) diag[c * T2 + t] = w.data[(static_cast<u64>(c) * C + c) * T2 + t];
+          cuda_check(cudaMemcpyAsync(p, diag.data(), diag.size() * 4, cudaMemcpyHostToDevice, s_), "h2d");
+          cuda_check(cudaStreamSynchronize(s_), "h2d");  // the host vector leaves scope
+        });
+        // residues per channel: [C][L][T2] (a channel's slice is a [L][T2] weight table)
+        BufPtr wres = encoding(w, {7, L, bits(s)}, static_cast<u64>(C) * L * T2 * wb, [&](void* p) {
+          check_launch(encode_f32(ctx, static_cast<const float*>(dg->ptr), static_cast<u64>(C) * T2, T2, L * T2, T2, L,
+                                  s, p, s_),
+                       "encode weights");
+        });
+        if (b && x.packing == HG_PACKING_REAL) {
+          check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
+          const float* bd = weight_dev(ctx, *b, s_);
+          bias_res = encoding(*b, {8, L, bits(acc_scale)}, static_cast<u64>(C) * L * wb, [&](void* p) {
+            check_launch(encode_f32(ctx, bd, C, 1, L, 1, L, acc_scale, p, s_), "encode bias");  // [C][L]
+          });
+        }
+        const u64 xs = static_cast<u64>(in_shape[1]) * in_shape[2] * 2 * x.level * N * wb;  // bytes per channel
+        const u64 ys = static_cast<u64>(out_shape[1]) * out_shape[2] * 2 * L * N * wb;
+        for (u32 c = 0; c < C; ++c)
+          run_conv(static_cast<const char*>(x.buf->ptr) + c * xs, static_cast<char*>(v.cipher.buf->ptr) + c * ys,
+                   static_cast<const char*>(wres->ptr) + static_cast<u64>(c) * L * T2 * wb,
+                   bias_res ? static_cast<const char*>(bias_res->ptr) + static_cast<u64>(c) * L * wb : nullptr, 1, 1);
+      } else {
+        BufPtr wres = encoding(w, {4, L, bits(s)}, static_cast<u64>(L) * w.data.size() * wb, [&](void* p) {
+          check_launch(encode_f32(ctx, wd, w.data.size(), static_cast<u32>(w.data.size()),
+                                  static_cast<u32>(w.data.size()), w.data.size(), L, s, p, s_),
+                       "encode weights");
+        });
+        int r = 1;
+        if (b && x.packing == HG_PACKING_REAL) {
+          check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
+          const float* bd = weight_dev(ctx, *b, s_);
+          bias_res = encoding(*b, {5, L, bits(acc_scale)}, static_cast<u64>(L) * F * wb, [&](void* p) {
+            check_launch(encode_f32(ctx, bd, F, F, F, F, L, acc_scale, p, s_), "encode bias");
+          });
+        }
+        run_conv(x.buf->ptr, v.cipher.buf->ptr, wres->ptr, bias_res ? bias_res->ptr : nullptr, C, F);
+      }
     }
     if (b && x.packing == HG_PACKING_COMPLEX) {
       // encode_broadcast under complex packing: encode_vector of (b + b i) in every slot

@@ -127,6 +127,7 @@ struct WeightTensor {
   // encodings kept across executes when the model caches weights (Model::keep_encodings):
   // (context, layout, level, scale bits, ...) -> device residues / packed planes
   std::map<std::vector<u64>, BufPtr> enc;
+  int depthwise = -1;  // conv weights (F, C, k, k) with F == C and zero off-diagonal taps; -1 unknown
 };
 
 struct NodeAttrs {

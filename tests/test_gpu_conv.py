@@ -48,6 +48,24 @@ CASES = [
 ]
 
 
+def test_depthwise_conv_vs_oracle(env):
+    """Block-diagonal weights (a depthwise layer as the reference sees it): the
+    GPU runs one 1 -> 1 convolution per channel; the result is the full convolution's."""
+    p, oc = env["p"], env["oc"]
+    C, IH, IW, win = 6, 7, 7, 3
+    rng = np.random.default_rng(31)
+    w = np.zeros((C, C, win, win), np.float32)
+    for c in range(C):
+        w[c, c] = rng.normal(0, 0.1, (win, win))
+    b = rng.normal(0, 0.01, C).astype(np.float32)
+    x = W.random_ciphertexts(p, C * IH * IW, seed=32)
+    got = _run(env["ctx"], x, (C, IH, IW), w, b, 1, (1, 1, 1, 1), p["scale"])
+    sel = [0, 6, 24, 48, 49, 100, 150, 293, 294 - 1]
+    want = oc.conv(x, w, (C, IH, IW), 1, (1, 1, 1, 1), 6, p["scale"], bias=b, rescale=False, outputs=sel)
+    for k, e in enumerate(sel):
+        assert np.array_equal(got[e], want[k]), e
+
+
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"C{c[0]}_{c[1]}x{c[2]}_F{c[3]}_w{c[4]}_s{c[5]}_L{c[7]}")
 def test_conv_vs_oracle_geometries(env, case):
     C, IH, IW, F, win, stride, pad, level, bias, edge = case
