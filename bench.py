@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c5b"],
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5b", "c4"],
                     help="c2 (default, the BASELINE metric) or c5b: wide dense 4096->4096 at N=16384, "
                          "output-sharded over the ranks with an NCCL all-gather")
     return ap.parse_args()
@@ -689,9 +689,157 @@ def c5b_reference_run(args, ws, rank):
     return 0
 
 
+# ---- BASELINE config 4: MobileNetV2 block, one spatial tile -------------------------------
+C4_METRIC = "encrypted images/sec, MobileNetV2 inverted-residual block 56x56x16 (BASELINE config 4, tiled)"
+C4_HW, C4_TILE = 56, 8  # the 56 x 56 activations as 7 x 7 tiles of 8 x 8 outputs (+1-pixel halo)
+
+
+def c4_secret_key(H, ctx, p, seed):
+    """A uniform ternary secret (keygen's distribution), NTT'd by the library under the chain
+    primes; the special limb (unused by encrypt / decrypt) is zero."""
+    import numpy as np
+    L, n = len(p["chain"]), p["n"]
+    s = np.random.default_rng(seed).integers(-1, 2, n)
+    w = np.zeros((1, 2, L, n), dtype=np.uint64)
+    for i, q in enumerate(p["chain"]):
+        w[0, 0, i] = np.where(s < 0, q - 1, s).astype(np.uint64)
+    t = H.CipherTensor.from_words(ctx, w, 1.0)
+    H.ntt_forward(ctx, t)
+    sk = np.zeros((L + 1, n), dtype=np.uint64)
+    sk[:L] = t.to_words()[0, 0]
+    return H.SecretKey(ctx, sk)
+
+
+def c4_run(args, ws, rank, local):
+    """One 8 x 8-output tile (10 x 10 x 16 input with its halo) of the block per GPU step:
+    1x1 expand 16->96, client-aided ReLU6 refresh, 3x3 depthwise (pad 1), ReLU6 refresh, 1x1
+    project 96->24, all on the device (the refreshes by the GPU NonlinearityEngine with the
+    [0, 6] clamp).  The input tile is resident; 49 tiles make one 8192-image 56 x 56 batch."""
+    import numpy as np
+    import torch
+    from paper_1908_04172_b200 import henet as H
+    from paper_1908_04172_b200 import workloads as Wk
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p = Wk.N16384
+    ctx = H.CkksContext(p["n"], p["chain"], p["special"], p["scale"], device=local)
+    hw = C4_TILE + 2
+    wl = Wk.mobilenet_block(hw=hw)
+    model = H.PlainModel.load(wl.manifest, wl.blob)
+    plan = H.RescalePlan.plan(ctx, model)
+    sk = c4_secret_key(H, ctx, p, 5 + rank)
+    acts = np.random.default_rng(6 + rank).normal(0, 1, (ctx.slot_count(), wl.input_count))
+    x = H.encrypt_tensor(ctx, sk, acts, 7 + rank, shape=wl.input_shape)
+    eng = H.RefreshEngine(ctx, sk, 77)
+    eng.set_relu_clip(6.0)
+    ctx.synchronize()
+    ext = torch.cuda.ExternalStream(ctx.stream(), device=local)
+    clocks = Clocks(local)
+    for _ in range(max(args.warmup, 1)):
+        out = H.execute(ctx, model, plan, x, None, eng)
+    ctx.synchronize()
+    steps = max(1, min(args.steps, 3))
+    l0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(ext)
+    for _ in range(steps):
+        out = H.execute(ctx, model, plan, x, None, eng)
+    e1.record(ext)
+    e1.synchronize()
+    launches = ctx.launch_count() - l0
+    clk = clocks.stop()
+    t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=f"cuda:{local}")
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    tile_ms = float(t.item())
+    tiles = (C4_HW // C4_TILE) ** 2
+    value = ws * 8192 / (tiles * tile_ms / 1e3)
+    # decrypted check of the tile's interior against the cleartext block (ReLU6 semantics)
+    dec = H.decrypt_tensor(ctx, sk, out, 16).reshape(16, 24, hw, hw)
+    w = {k: np.frombuffer(wl.blob, dtype="<f4") for k in ("all",)}["all"]
+    man = json.loads(wl.manifest)["weights"]
+    g = lambda k, shp: w[man[k]["offset"] // 4:][:int(np.prod(shp))].reshape(shp).astype(np.float64)
+    ew, dw, pw = g("exp_w", (96, 16, 1, 1))[:, :, 0, 0], g("dw_w", (96, 96, 3, 3)), g("proj_w", (24, 96, 1, 1))[:, :, 0, 0]
+    a0 = acts[:16].reshape(16, 16, hw, hw)
+    h1 = np.clip(np.einsum("fc,bchw->bfhw", ew, a0), 0, 6)
+    hp = np.pad(h1, ((0, 0), (0, 0), (1, 1), (1, 1)))
+    h2 = np.zeros_like(h1)
+    for c in range(96):
+        for ky in range(3):
+            for kx in range(3):
+                h2[:, c] += dw[c, c, ky, kx] * hp[:, c, ky:ky + hw, kx:kx + hw]
+    want = np.einsum("fc,bchw->bfhw", pw, np.clip(h2, 0, 6))
+    err = float(np.abs(dec - want)[:, :, 1:-1, 1:-1].max())
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = c4_reference_sample()
+        except Exception as e:  # reported, not fatal
+            cpu = {"error": str(e)}
+    if rank == 0:
+        print(json.dumps({
+            "metric": C4_METRIC, "value": value, "unit": "images/s", "n_gpus": ws, "steps": steps,
+            "warmup": max(args.warmup, 1), "ms_per_step": tile_ms * tiles, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues, 40/30-bit primes)",
+            "data": "synthetic N(0,1) activations encrypted on the GPU; W ~ N(0, 0.1^2) f32",
+            "config": {"workload": "c4 MobileNetV2 block 56x56x16 -> expand 96 -> ReLU6 -> dw 3x3 -> ReLU6 -> project 24",
+                       "ring": "N=16384, chain [40,30x7]+40, scale 2^30", "images_per_batch": 8192,
+                       "tiling": f"{tiles} tiles of {C4_TILE}x{C4_TILE} outputs, each computed on a "
+                                 f"{hw}x{hw} input (1-pixel halo); one tile per step, the 56x56 batch = {tiles} steps",
+                       "refresh": "client-aided ReLU6 on the GPU (hg_refresh_engine, clamp [0, 6])",
+                       "parallelism": f"replicas x{ws}"},
+            "tile_ms": tile_ms, "roofline": None,
+            "roofline_note": "dominated by the client-aided refreshes (decrypt/decode/encode/encrypt of 2 x 9600 ciphertexts per tile); see the kernel shares",
+            "cpu_baseline": cpu, "e2e": None, "gpu_launches": launches, "clocks": clk,
+            "check": {"max_abs_err_vs_cleartext_interior": err, "images_checked": 16}}))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def c4_reference_sample():
+    """The reference on a 1 x 1 tile (one position: 16 -> 96 -> ReLU6 -> depthwise (centre
+    tap) -> ReLU6 -> 24, the harness's clamp provider; its NonlinearityEngine refreshes one
+    ciphertext after another), per position, scaled to the 56 x 56 batch."""
+    import numpy as np
+    from oracle import refbind as R
+    from paper_1908_04172_b200 import workloads as Wk
+    p = Wk.N16384
+    ref = R.RefContext(p["n"], p["chain"], p["special"], p["scale"])
+    keys = ref.keygen(9, False)
+    wl = Wk.mobilenet_block(hw=1)
+    acts = np.random.default_rng(3).normal(0, 1, (8192, wl.input_count))
+    words, sc = ref.encrypt_tensor(keys, acts, 4)
+    R.set_relu_clip(6.0)
+    try:
+        t0 = time.perf_counter()
+        ref.execute(keys, wl.manifest, wl.blob, words, sc, refresh_seed=77)
+        dt = time.perf_counter() - t0
+    finally:
+        R.set_relu_clip(0.0)
+    per_position = dt
+    v = 8192 / (per_position * C4_HW * C4_HW)
+    return {"value": v, "unit": "images/s", "cores": os.cpu_count() or 1, "kind": "reference",
+            "sample": f"1x1 tile (one position, {dt:.1f} s) through henet::execute with the clamp provider, "
+                      f"scaled by position to 56x56 (extrapolated)"}
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
+    if args.workload == "c4":
+        if args.impl == "reference":
+            if rank == 0:
+                c = c4_reference_sample()
+                print(json.dumps({"metric": C4_METRIC, "impl": "reference", "value": c["value"], "unit": "images/s",
+                                  "higher_is_better": True, "cpu_baseline": c,
+                                  "e2e": {"value": c["value"], "unit": "images/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}))
+            return 0
+        return c4_run(args, ws, rank, local)
     if args.workload == "c5b":
         return c5b_reference_run(args, ws, rank) if args.impl == "reference" else c5b_run(args, ws, rank, local)
     if args.impl == "reference":

@@ -21,6 +21,7 @@ struct EncArgs {
   u64 seed;         // encrypt_tensor seed; ciphertext e uses derive_seed(seed, e), stream 1
   u64 thr[kMaxPrimes];  // next_below rejection thresholds (2^64 mod q)
   u32 count, level, N;
+  u32 e0;           // index of ciphertext 0 in the seed sequence (chunked refreshes)
 };
 
 struct CrtTables {
@@ -41,6 +42,8 @@ struct DecArgs {
   u32 count, polys, level, N, words;
 };
 
+int launch_batch_to_slots(const double* samples, u64 count, u64 e0, u32 cnt, u32 n_slots, int complex_pack,
+                          double* slots, cudaStream_t s);
 // B: the context's Basis, or its BasisW when `wide`
 int launch_enc_sample(const EncArgs& a, const void* B, bool wide, cudaStream_t s);
 int launch_enc_serial(const EncArgs& a, const u32* list, u32 n_list, const void* B, bool wide, cudaStream_t s);

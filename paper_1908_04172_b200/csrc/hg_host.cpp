@@ -1331,7 +1331,6 @@ class Executor {
                                   static_cast<u32>(w.data.size()), w.data.size(), L, s, p, s_),
                        "encode weights");
         });
-        int r = 1;
         if (b && x.packing == HG_PACKING_REAL) {
           check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
           const float* bd = weight_dev(ctx, *b, s_);
@@ -2405,21 +2404,19 @@ const void* client_basis(const Context& c) {
 // encrypt (henet/ckks.hpp:229-248) of `count` encoded top-level plaintexts [count][L][N]:
 // ciphertext e draws from derive_seed(seed, e), stream 1 (encrypt_tensor's per-element
 // seeds, and NonlinearityEngine's per-group seeds with seed = derive_seed(seed, layer)).
-CtBatch encrypt_pts(const Context& c, const hg_secret_key* sk, const BufPtr& pt, u64 count, u64 seed, int packing,
-                    cudaStream_t s) {
+// ... into `ct_out` (count top-level ciphertexts); ciphertext e uses seed index e0 + e.
+void encrypt_into(const Context& c, const hg_secret_key* sk, const void* pt, u64 count, u64 seed, u64 e0,
+                  void* ct_out, cudaStream_t s) {
     const u32 L = static_cast<u32>(c.chain_len()), N = c.n;
-    CtBatch o;
-    o.packing = packing;
-    o.scale = c.default_scale;
-    ensure(c, o, count, 2, L, s);
     BufPtr err = c.alloc(count * L * static_cast<u64>(N) * c.word_bytes(), s);
     BufPtr flags = c.alloc(count * sizeof(int), s);
     cuda_check(cudaMemsetAsync(flags->ptr, 0, count * sizeof(int), s), "memset");
     EncArgs a{};
-    a.ct = o.buf->ptr;
+    a.ct = ct_out;
     a.err = err->ptr;
-    a.pt = pt->ptr;
+    a.pt = pt;
     a.sk = sk->s->ptr;
+    a.e0 = static_cast<u32>(e0);
     a.flags = static_cast<int*>(flags->ptr);
     a.seed = seed;
     for (u32 i = 0; i < L; ++i) a.thr[i] = (0 - c.chain[i]) % c.chain[i];  // next_below threshold
@@ -2452,8 +2449,8 @@ CtBatch encrypt_pts(const Context& c, const hg_secret_key* sk, const BufPtr& pt,
                  "ntt");
     check_launch(launch_enc_combine(a, client_basis(c), c.wide, s), "encrypt combine");
     cuda_check(cudaStreamSynchronize(s), "encrypt");
-    return o;
 }
+
 }  // namespace
 
 int hg_secret_key_upload(hg_ctx* ctx, const uint64_t* words, uint64_t n_words, hg_secret_key** out) {
@@ -2494,52 +2491,62 @@ int hg_encrypt_tensor(hg_ctx* ctx, const hg_secret_key* sk, const double* sample
     if (packing == HG_PACKING_COMPLEX) require(batch % 2 == 0, "complex packing needs an even batch");
     require(count >= 1, "tensor must be non-empty");
     const u32 L = static_cast<u32>(c.chain_len()), N = c.n;
-    // batch_to_slots per element (henet/encoding.hpp:72-87), then encode_vector at the top
-    // level and the default scale (encrypt_batch, henet/ckks.hpp:250-254)
+    // the samples go to the device as they are; batch_to_slots (henet/encoding.hpp:72-87),
+    // encode_vector at the top level and default scale (encrypt_batch, henet/ckks.hpp:250-254)
+    // and encrypt then run per chunk of 1024 ciphertexts (bounded scratch)
     const u32 n_slots = packing == HG_PACKING_REAL ? batch : batch / 2;
-    std::vector<double> slots(count * n_slots * 2);
-    for (u64 e = 0; e < count; ++e)
-      for (u32 j = 0; j < n_slots; ++j) {
-        double* d = &slots[(e * n_slots + j) * 2];
-        if (packing == HG_PACKING_REAL) {
-          d[0] = samples[static_cast<u64>(j) * count + e];
-          d[1] = 0.0;
-        } else {
-          d[0] = samples[static_cast<u64>(j) * count + e];
-          d[1] = samples[static_cast<u64>(j + n_slots) * count + e];
-        }
-      }
-    BufPtr ds = c.alloc(slots.size() * sizeof(double), s);
-    cuda_check(cudaMemcpyAsync(ds->ptr, slots.data(), slots.size() * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
-    std::vector<unsigned long long> mant;
-    std::vector<int> ex;
-    BufPtr pt = encode_vectors_dev(c, static_cast<const double*>(ds->ptr), n_slots, count, L, c.default_scale, s, mant, ex);
-
-    out->b = encrypt_pts(c, sk, pt, count, seed, packing, s);
+    BufPtr dsm = c.alloc(static_cast<u64>(batch) * count * sizeof(double), s);
+    cuda_check(cudaMemcpyAsync(dsm->ptr, samples, static_cast<u64>(batch) * count * sizeof(double),
+                               cudaMemcpyHostToDevice, s),
+               "h2d");
+    CtBatch o;
+    o.packing = packing;
+    o.scale = c.default_scale;
+    ensure(c, o, count, 2, L, s);
+    const u64 chunk = 1024, out_ct = 2ull * L * N * c.word_bytes();
+    BufPtr ds = c.alloc(std::min<u64>(count, chunk) * n_slots * 2 * sizeof(double), s);
+    for (u64 e0 = 0; e0 < count; e0 += chunk) {
+      const u64 ne = std::min(chunk, count - e0);
+      check_launch(launch_batch_to_slots(static_cast<const double*>(dsm->ptr), count, e0, static_cast<u32>(ne),
+                                         n_slots, packing == HG_PACKING_COMPLEX, static_cast<double*>(ds->ptr), s),
+                   "batch to slots");
+      std::vector<unsigned long long> mant;
+      std::vector<int> ex;
+      BufPtr pt = encode_vectors_dev(c, static_cast<const double*>(ds->ptr), n_slots, ne, L, c.default_scale, s, mant,
+                                     ex);
+      encrypt_into(c, sk, pt->ptr, ne, seed, e0, static_cast<char*>(o.buf->ptr) + e0 * out_ct, s);
+    }
+    cuda_check(cudaStreamSynchronize(s), "encrypt");
+    out->b = o;
     out->b.shape = {static_cast<u32>(count)};
   });
 }
 
 namespace {
-DecArgs dec_args(const Context& c, const hg_secret_key* sk, const CtBatch& ct) {
-  require(ct.polys == 2 || ct.polys == 3, "ciphertext must have 2 or 3 polynomials");
-  require(ct.level >= 1, "ciphertext level must be at least 1");
+DecArgs dec_args(const Context& c, const hg_secret_key* sk, const void* ct, u64 count, u32 polys, u32 level) {
+  require(polys == 2 || polys == 3, "ciphertext must have 2 or 3 polynomials");
+  require(level >= 1, "ciphertext level must be at least 1");
   DecArgs a{};
-  a.ct = ct.buf->ptr;
+  a.ct = ct;
   a.sk = sk->s->ptr;
-  a.count = static_cast<u32>(ct.count);
-  a.polys = ct.polys;
-  a.level = ct.level;
+  a.count = static_cast<u32>(count);
+  a.polys = polys;
+  a.level = level;
   a.N = c.n;
   return a;
+}
+DecArgs dec_args(const Context& c, const hg_secret_key* sk, const CtBatch& ct) {
+  return dec_args(c, sk, ct.buf->ptr, ct.count, ct.polys, ct.level);
 }
 
 // decode_slots(decrypt(ct)) (henet/encoding.hpp:223-264, henet/ckks.hpp:256-268) of every
 // ciphertext of `b` on the GPU: slots [count][N/2][2] doubles, bit-exact.
-BufPtr decode_slots_dev(const Context& c, const hg_secret_key* sk, const CtBatch& b, cudaStream_t s) {
-    DecArgs a = dec_args(c, sk, b);
+// `count` ciphertexts at `ct` (polys x level limbs each) -> slots [count][N/2][2] in `sl`.
+void decode_into(const Context& c, const hg_secret_key* sk, const void* ct, u64 count, u32 polys, u32 level,
+                 double scale, double* sl, cudaStream_t s) {
+    DecArgs a = dec_args(c, sk, ct, count, polys, level);
     // CRT tables for this level (decode_slots, henet/encoding.hpp:226-243)
-    const u32 L = b.level;
+    const u32 L = level;
     std::vector<u64> big{1};
     for (u32 i = 0; i < L; ++i) mw_mul_small(big, c.chain[i]);
     require(big.size() <= static_cast<size_t>(kCrtWords), "modulus too large for the GPU decoder");
@@ -2555,23 +2562,27 @@ BufPtr decode_slots_dev(const Context& c, const hg_secret_key* sk, const CtBatch
     }
     {
       // 1.0L / (long double)scale (decode_slots, henet/encoding.hpp:248), x87 on the host
-      const long double li = 1.0L / static_cast<long double>(b.scale);
+      const long double li = 1.0L / static_cast<long double>(scale);
       int ex = 0;
       const long double fr = std::frexp(li, &ex);  // li = fr * 2^ex, fr in [0.5, 1)
       a.inv_mant = static_cast<u64>(std::ldexp(fr, 64));
       a.inv_exp = ex - 64;
     }
-    const u64 count = b.count, N = c.n;
+    const u64 N = c.n;
     BufPtr m = c.alloc(count * L * N * c.word_bytes(), s);
     BufPtr co = c.alloc(count * N * sizeof(double), s);
     BufPtr scratch = c.alloc(count * N * sizeof(double2), s);
-    BufPtr sl = c.alloc(count * N * sizeof(double), s);  // [count][N/2][2]
     a.m = m->ptr;
     a.coeffs = static_cast<double*>(co->ptr);
     const double2* roots = static_cast<const double2*>(c.fft_tables->ptr);
     check_launch(launch_dec(a, static_cast<int>(c.logn), client_basis(c), c.wide, roots, roots + N / 2,
-                            static_cast<double2*>(scratch->ptr), static_cast<double*>(sl->ptr), s),
+                            static_cast<double2*>(scratch->ptr), sl, s),
                  "decrypt");
+}
+
+BufPtr decode_slots_dev(const Context& c, const hg_secret_key* sk, const CtBatch& b, cudaStream_t s) {
+    BufPtr sl = c.alloc(b.count * static_cast<u64>(c.n) * sizeof(double), s);  // [count][N/2][2]
+    decode_into(c, sk, b.buf->ptr, b.count, b.polys, b.level, b.scale, static_cast<double*>(sl->ptr), s);
     return sl;
 }
 }  // namespace
@@ -2688,16 +2699,33 @@ int hg_refresh_engine_apply(void* engine, int kind, uint32_t window, uint32_t la
     if (kind == HG_NONLIN_RELU) require(window == 1, "ReLU is element-wise");
     const u64 groups = b.count / window;
     const u32 half = c.n / 2;
-    BufPtr sl = decode_slots_dev(c, eng->sk, b, s);
-    BufPtr res = c.alloc(groups * half * 2 * sizeof(double), s);
-    check_launch(launch_refresh_slots(static_cast<const double*>(sl->ptr), static_cast<double*>(res->ptr),
-                                      static_cast<u32>(groups), window, half, kind, eng->relu_clip, s),
-                 "refresh slots");
-    std::vector<unsigned long long> mant;
-    std::vector<int> ex;
-    BufPtr pt = encode_vectors_dev(c, static_cast<const double*>(res->ptr), half, groups,
-                                   static_cast<u32>(c.chain_len()), c.default_scale, s, mant, ex);
-    response->b = encrypt_pts(c, eng->sk, pt, groups, derive_seed_host(eng->seed, layer_seq), b.packing, s);
+    const u32 L = static_cast<u32>(c.chain_len());
+    CtBatch o;
+    o.packing = b.packing;
+    o.scale = c.default_scale;
+    ensure(c, o, groups, 2, L, s);
+    // in chunks of ~1024 request ciphertexts: the decode / encode / encrypt scratch is
+    // ~5 words per residue, so a whole layer at once would need several times its size
+    const u64 cg = std::max<u64>(1, 1024 / window);
+    const u64 in_ct = static_cast<u64>(b.polys) * b.level * c.n * c.word_bytes();  // bytes per ciphertext
+    const u64 out_ct = 2ull * L * c.n * c.word_bytes();
+    BufPtr sl = c.alloc(std::min(groups, cg) * window * half * 2 * sizeof(double), s);
+    BufPtr res = c.alloc(std::min(groups, cg) * half * 2 * sizeof(double), s);
+    const u64 seed = derive_seed_host(eng->seed, layer_seq);
+    for (u64 g0 = 0; g0 < groups; g0 += cg) {
+      const u64 ng = std::min(cg, groups - g0);
+      decode_into(c, eng->sk, static_cast<const char*>(b.buf->ptr) + g0 * window * in_ct, ng * window, b.polys,
+                  b.level, b.scale, static_cast<double*>(sl->ptr), s);
+      check_launch(launch_refresh_slots(static_cast<const double*>(sl->ptr), static_cast<double*>(res->ptr),
+                                        static_cast<u32>(ng), window, half, kind, eng->relu_clip, s),
+                   "refresh slots");
+      std::vector<unsigned long long> mant;
+      std::vector<int> ex;
+      BufPtr pt = encode_vectors_dev(c, static_cast<const double*>(res->ptr), half, ng, L, c.default_scale, s, mant,
+                                     ex);
+      encrypt_into(c, eng->sk, pt->ptr, ng, seed, g0, static_cast<char*>(o.buf->ptr) + g0 * out_ct, s);
+    }
+    response->b = o;
     response->b.shape = {static_cast<u32>(groups)};
   });
 }
