@@ -222,6 +222,11 @@ int hg_decrypt(hg_ctx* ctx, const hg_secret_key* sk, const hg_tensor* ct, uint64
 int hg_decrypt_tensor(hg_ctx* ctx, const hg_secret_key* sk, const hg_tensor* ct, uint32_t batch,
                       double* out, void* stream);
 
+/* decode_slots (henet/encoding.hpp:223-264) of `count` plaintexts (level x N u64 words each,
+ * NTT domain) at `scale`: N/2 slots per plaintext as interleaved (re, im), bit-exact. */
+int hg_decode_vector(hg_ctx* ctx, const uint64_t* pt_words, uint64_t count, uint32_t level, double scale,
+                     double* out_re_im);
+
 /* ------------------------------------------------------------------ */
 /* Graph level: PlainModel / RescalePlan / execute                     */
 /* ------------------------------------------------------------------ */

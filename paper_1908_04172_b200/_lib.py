@@ -92,6 +92,7 @@ PROTOTYPES = {
     "hg_encode_scalars": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, C.c_double, vp]),
     "hg_encode_vector": (C.c_int, [vp, vp, C.c_uint32, C.c_uint64, C.c_uint32, C.c_double, vp]),
     "hg_secret_key_upload": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(vp)]),
+    "hg_decode_vector": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, C.c_double, vp]),
     "hg_secret_key_destroy": (None, [vp]),
     "hg_encrypt_tensor": (C.c_int, [vp, vp, vp, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int, vp, vp]),
     "hg_decrypt": (C.c_int, [vp, vp, vp, vp, vp]),

@@ -2524,11 +2524,12 @@ int hg_encrypt_tensor(hg_ctx* ctx, const hg_secret_key* sk, const double* sample
 
 namespace {
 DecArgs dec_args(const Context& c, const hg_secret_key* sk, const void* ct, u64 count, u32 polys, u32 level) {
-  require(polys == 2 || polys == 3, "ciphertext must have 2 or 3 polynomials");
+  // polys == 1: a plaintext (no secret key)
+  require(polys == 1 || polys == 2 || polys == 3, "ciphertext must have 2 or 3 polynomials");
   require(level >= 1, "ciphertext level must be at least 1");
   DecArgs a{};
   a.ct = ct;
-  a.sk = sk->s->ptr;
+  a.sk = sk != nullptr ? sk->s->ptr : nullptr;
   a.count = static_cast<u32>(count);
   a.polys = polys;
   a.level = level;
@@ -2896,5 +2897,31 @@ int hg_model_keep_encodings(hg_model* m, int on) {
     m->m.keep_encodings = on != 0;
     if (!on)
       for (auto& kv : m->m.weights) kv.second.enc.clear();
+  });
+}
+
+int hg_decode_vector(hg_ctx* ctx, const uint64_t* pt_words, uint64_t count, uint32_t level, double scale,
+                     double* out_re_im) {
+  return guard([&] {
+    require(ctx && pt_words && out_re_im, "null argument");
+    const Context& c = *ctx->c;
+    require(level >= 1 && level <= c.chain_len(), "plaintext level out of range");
+    cudaStream_t s = c.core->stream;
+    const u64 nw = count * level * static_cast<u64>(c.n);
+    for (u64 i = 0; i < nw; ++i) require(pt_words[i] < c.chain[(i / c.n) % level], "residue out of range");
+    BufPtr d = c.alloc(nw * c.word_bytes(), s);
+    if (c.wide) {
+      cuda_check(cudaMemcpyAsync(d->ptr, pt_words, nw * 8, cudaMemcpyHostToDevice, s), "h2d");
+    } else {
+      std::vector<u32> h(pt_words, pt_words + nw);
+      cuda_check(cudaMemcpyAsync(d->ptr, h.data(), nw * 4, cudaMemcpyHostToDevice, s), "h2d");
+      cuda_check(cudaStreamSynchronize(s), "h2d");  // the host vector leaves scope
+    }
+    BufPtr sl = c.alloc(count * static_cast<u64>(c.n) * sizeof(double), s);
+    decode_into(c, nullptr, d->ptr, count, 1, level, scale, static_cast<double*>(sl->ptr), s);
+    cuda_check(cudaMemcpyAsync(out_re_im, sl->ptr, count * static_cast<u64>(c.n) * sizeof(double),
+                               cudaMemcpyDeviceToHost, s),
+               "d2h");
+    cuda_check(cudaStreamSynchronize(s), "decode");
   });
 }

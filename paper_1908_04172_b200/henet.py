@@ -447,6 +447,15 @@ def encode_vector(ctx, slots, level, scale) -> np.ndarray:
     return encode_vectors(ctx, np.asarray(slots)[None, :], level, scale)[0]
 
 
+def decode_vector(ctx, words: np.ndarray, scale: float) -> np.ndarray:
+    """decode_slots (henet/encoding.hpp:223-264) of one (level, N) plaintext: N/2 complex slots."""
+    w = np.ascontiguousarray(words, dtype=np.uint64)
+    level = w.shape[0]
+    out = np.empty(ctx.n, dtype=np.float64)
+    check(lib.hg_decode_vector(ctx.handle, _ptr(w), 1, level, float(scale), _ptr(out)))
+    return out[0::2] + 1j * out[1::2]
+
+
 # ---------------------------------------------------------------------------
 # Graph level (henet/graph.hpp)
 # ---------------------------------------------------------------------------

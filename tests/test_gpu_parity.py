@@ -123,6 +123,21 @@ def test_encode_vector_bit_exact(env):
             assert np.array_equal(got, want), (n_slots, cplx, level)
 
 
+def test_decode_vector_bit_exact(env):
+    """decode_slots of plaintexts: encode -> decode round trips and arbitrary residues, equal
+    to the reference's doubles bit for bit."""
+    ctx, ref, p = env["ctx"], env["ref"], env["p"]
+    rng = np.random.default_rng(8)
+    for level in (6, 3, 1):
+        slots = rng.uniform(-1, 1, 4096) + 1j * rng.uniform(-1, 1, 4096)
+        pt = ref.encode_vector(slots, level, p["scale"])
+        got = H.decode_vector(ctx, pt, p["scale"])
+        assert np.array_equal(got, ref.decode(pt, p["scale"]))
+        assert np.abs(got - slots).max() < 1e-3
+        raw = W.random_ciphertexts(p, 1, seed=level, level=level)[0, 0]
+        assert np.array_equal(H.decode_vector(ctx, raw, 2.0 ** 40), ref.decode(raw, 2.0 ** 40))
+
+
 def _run_both(env, wl, seed=21, threads=0, check_plan=True, mode=0):
     ctx, ref, keys, rk = env["ctx"], env["ref"], env["keys"], env["rk"]
     imgs = W.synthetic_images(wl.input_shape, wl.batch, seed)
