@@ -171,10 +171,23 @@ __global__ void __launch_bounds__(kWWarps * 32) k_mac_dense_w(MacDenseArgsW a, B
 constexpr int kWMaxTaps = 1024;
 constexpr int kWFT = 8;
 
+// Window taps in ascending (c, ky, kx) order with the padding skipped (henet/graph.hpp:976-989),
+// walked by every thread (uniform control flow, no serial tap-list prologue).
+template <typename F>
+__device__ __forceinline__ void for_each_tap(const MacConvArgsW& a, u32 oy, u32 ox, F&& body) {
+  for (u32 c = 0; c < a.C; ++c)
+    for (u32 ky = 0; ky < a.win; ++ky) {
+      const int iy = static_cast<int>(oy * a.stride + ky) - static_cast<int>(a.pad_top);
+      if (iy < 0 || iy >= static_cast<int>(a.IH)) continue;
+      for (u32 kx = 0; kx < a.win; ++kx) {
+        const int ix = static_cast<int>(ox * a.stride + kx) - static_cast<int>(a.pad_left);
+        if (ix < 0 || ix >= static_cast<int>(a.IW)) continue;
+        body((c * a.IH + static_cast<u32>(iy)) * a.IW + static_cast<u32>(ix), (c * a.win + ky) * a.win + kx);
+      }
+    }
+}
+
 __global__ void __launch_bounds__(128) k_mac_conv_w(MacConvArgsW a, BasisW B) {
-  __shared__ u32 tap_in[kWMaxTaps];
-  __shared__ u32 tap_w[kWMaxTaps];
-  __shared__ u32 ntaps_s;
   const u32 tid = threadIdx.x;
   const u32 pos = blockIdx.y;
   const u32 oy = pos / a.OW, ox = pos % a.OW;
@@ -185,48 +198,64 @@ __global__ void __launch_bounds__(128) k_mac_conv_w(MacConvArgsW a, BasisW B) {
   const DevPrimeW& P = B.p[limb];
   const u32 n = (blockIdx.x * blockDim.x + tid) * 2;
   const u32 taps_all = a.C * a.win * a.win;
-  if (tid == 0) {
-    u32 cnt = 0;
-    for (u32 c = 0; c < a.C; ++c)
-      for (u32 ky = 0; ky < a.win; ++ky)
-        for (u32 kx = 0; kx < a.win; ++kx) {
-          const int iy = static_cast<int>(oy * a.stride + ky) - static_cast<int>(a.pad_top);
-          const int ix = static_cast<int>(ox * a.stride + kx) - static_cast<int>(a.pad_left);
-          if (iy < 0 || iy >= static_cast<int>(a.IH) || ix < 0 || ix >= static_cast<int>(a.IW)) continue;
-          tap_in[cnt] = (c * a.IH + iy) * a.IW + ix;
-          tap_w[cnt] = (c * a.win + ky) * a.win + kx;
-          ++cnt;
-        }
-    ntaps_s = cnt;
-  }
-  __syncthreads();
-  const u32 ntaps = ntaps_s;
   const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
   const u64* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n;
   const u64* Wl = a.W + static_cast<u64>(limb) * a.F * taps_all;
-  Acc128 acc[kWFT][2];
-#pragma unroll
-  for (int f = 0; f < kWFT; ++f) acc[f][0] = acc[f][1] = {0, 0};
-  for (u32 t = 0; t < ntaps; ++t) {
-    const ulonglong2 xv = __ldg(reinterpret_cast<const ulonglong2*>(Xb + static_cast<u64>(tap_in[t]) * xstride));
-#pragma unroll
-    for (int f = 0; f < kWFT; ++f) {
-      if (f0 + f >= a.F) break;
-      const u64 w = __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + tap_w[t]]);
-      mac128(acc[f][0], xv.x, w);
-      mac128(acc[f][1], xv.y, w);
-    }
-  }
-#pragma unroll
-  for (int f = 0; f < kWFT; ++f) {
+  auto store = [&](int f, u64 v0, u64 v1) {
     const u32 ff = f0 + f;
-    if (ff >= a.F) continue;
     const u64 bv = (a.bias != nullptr && poly == 0) ? __ldg(&a.bias[static_cast<u64>(limb) * a.F + ff]) : 0;
     const u64 e = static_cast<u64>(ff) * a.OH * a.OW + pos;
     u64* yp = a.Y + ((e * a.polys + poly) * a.level + limb) * a.N + n;
-    *reinterpret_cast<ulonglong2*>(yp) = make_ulonglong2(addmod_w(barrett128(acc[f][0].lo, acc[f][0].hi, P), bv, P.q),
-                                                         addmod_w(barrett128(acc[f][1].lo, acc[f][1].hi, P), bv, P.q));
+    *reinterpret_cast<ulonglong2*>(yp) = make_ulonglong2(addmod_w(v0, bv, P.q), addmod_w(v1, bv, P.q));
+  };
+  if (P.q < (1ull << 30)) {
+    // a limb below 2^30 (the 30-bit limbs of c4/c5b): one 32 x 32 -> 64 IMAD.WIDE per MAC
+    // (products < 2^60), folded (acc = lo + hi * (2^32 mod q) < 2^62 + 2^32) every 8 taps, so
+    // the sums stay below 2^64
+    const u64 r32 = (1ull << 32) % P.q;
+    u64 acc[kWFT][2];
+#pragma unroll
+    for (int f = 0; f < kWFT; ++f) acc[f][0] = acc[f][1] = 0;
+    u32 cnt = 0;
+    for_each_tap(a, oy, ox, [&](u32 tin, u32 tw) {
+      const ulonglong2 xv = __ldg(reinterpret_cast<const ulonglong2*>(Xb + static_cast<u64>(tin) * xstride));
+      const u32 x0 = static_cast<u32>(xv.x), x1 = static_cast<u32>(xv.y);
+#pragma unroll
+      for (int f = 0; f < kWFT; ++f) {
+        if (f0 + f >= a.F) break;
+        const u32 w = static_cast<u32>(__ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + tw]));
+        acc[f][0] += static_cast<u64>(x0) * w;
+        acc[f][1] += static_cast<u64>(x1) * w;
+      }
+      if ((++cnt & 7) == 0) {
+#pragma unroll
+        for (int f = 0; f < kWFT; ++f)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) acc[f][j] = (acc[f][j] & 0xffffffffull) + (acc[f][j] >> 32) * r32;
+      }
+    });
+#pragma unroll
+    for (int f = 0; f < kWFT; ++f)
+      if (f0 + f < a.F) store(f, barrett128(acc[f][0], 0, P), barrett128(acc[f][1], 0, P));
+    return;
   }
+  Acc128 acc[kWFT][2];
+#pragma unroll
+  for (int f = 0; f < kWFT; ++f) acc[f][0] = acc[f][1] = {0, 0};
+  for_each_tap(a, oy, ox, [&](u32 tin, u32 tw) {
+    const ulonglong2 xv = __ldg(reinterpret_cast<const ulonglong2*>(Xb + static_cast<u64>(tin) * xstride));
+#pragma unroll
+    for (int f = 0; f < kWFT; ++f) {
+      if (f0 + f >= a.F) break;
+      const u64 w = __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + tw]);
+      mac128(acc[f][0], xv.x, w);
+      mac128(acc[f][1], xv.y, w);
+    }
+  });
+#pragma unroll
+  for (int f = 0; f < kWFT; ++f)
+    if (f0 + f < a.F)
+      store(f, barrett128(acc[f][0].lo, acc[f][0].hi, P), barrett128(acc[f][1].lo, acc[f][1].hi, P));
 }
 
 // ---------------------------------------------------------------------------
