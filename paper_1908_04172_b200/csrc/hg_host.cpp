@@ -424,14 +424,14 @@ static CtBatch do_rescale(const Context& ctx, const CtBatch& in, u32 target, cud
       r = launch_rescale_w(static_cast<int>(ctx.logn), a, ctx.basisw, s);
       if (hybrid && r >= 0) {
         check_launch(r, "rescale (wide limb)");
-        const u32 cnt = L - 1;  // limbs 1 .. L-1 (the dropped one last)
+        const u32 cnt = L - 1;  // limbs 1 .. L-1 (the dropped one last), in place in the u64 rows
         const u64 rows = cur.count * cur.polys;
-        BufPtr xn = ctx.alloc(rows * cnt * ctx.n * 4, s), yn = ctx.alloc(rows * (cnt - 1) * ctx.n * 4, s);
-        check_launch(launch_limbs_to_u32(cur.data64(), static_cast<u32*>(xn->ptr), rows, L, 1, cnt, ctx.n, s),
-                     "narrow limbs");
         RescaleArgs na{};
-        na.in = static_cast<const u32*>(xn->ptr);
-        na.out = static_cast<u32*>(yn->ptr);
+        na.in64 = cur.data64();
+        na.out64 = out.data64();
+        na.io_level_in = L;
+        na.io_level_out = L - 1;
+        na.io_off = 1;
         na.rows = rows;
         na.level = cnt;
         na.lazy = 1;
@@ -444,8 +444,7 @@ static CtBatch do_rescale(const Context& ctx, const CtBatch& in, u32 target, cud
           na.pm[i] = static_cast<u32>((p / 2 + q - 1) / q * q);
           if (na.pm[i] + p / 2 >= 4 * q) na.lazy = 0;
         }
-        check_launch(launch_rescale(static_cast<int>(ctx.logn), na, sub, s), "rescale (narrow limbs)");
-        r = launch_limbs_to_u64(static_cast<const u32*>(yn->ptr), out.data64(), rows, L - 1, 1, cnt - 1, ctx.n, s);
+        r = launch_rescale(static_cast<int>(ctx.logn), na, sub, s);
       }
     } else {
       RescaleArgs a{};

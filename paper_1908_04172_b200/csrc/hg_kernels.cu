@@ -51,10 +51,33 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_NTT_TWS_MINB
 // ===========================================================================
 // LAZY: the centred correction c (|c| <= q_{L-1}/2) enters each forward transform as
 // c + pm_i < 4 q_i (the lazy transform's input range) instead of being reduced mod q_i.
-template <int LOGN, bool LAZY>
+// four consecutive residues of a u32 or u64 (WIO) row as a uint4
+template <typename W>
+__device__ __forceinline__ uint4 ld4(const W* p) {
+  if constexpr (sizeof(W) == 4) {
+    return __ldg(reinterpret_cast<const uint4*>(p));
+  } else {
+    const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(p));
+    const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(p) + 1);
+    return make_uint4(static_cast<u32>(a.x), static_cast<u32>(a.y), static_cast<u32>(b.x), static_cast<u32>(b.y));
+  }
+}
+template <typename W>
+__device__ __forceinline__ void st4(W* p, uint4 v) {
+  if constexpr (sizeof(W) == 4) {
+    *reinterpret_cast<uint4*>(p) = v;
+  } else {
+    reinterpret_cast<ulonglong2*>(p)[0] = make_ulonglong2(v.x, v.y);
+    reinterpret_cast<ulonglong2*>(p)[1] = make_ulonglong2(v.z, v.w);
+  }
+}
+
+// W = u64: the limbs are read and written in place in wide (u64) tensors (a.in64 / a.out64).
+template <int LOGN, bool LAZY, typename W = u32>
 __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_RESCALE_MINB : 1)) k_rescale(RescaleArgs a, Basis B) {
   using NT = Ntt<LOGN, true>;  // staged pass-B twiddles: 3 CTAs per SM
   constexpr int N = NT::N;
+  constexpr bool kWide = sizeof(W) == 8;
   extern __shared__ u32 sm[];
   const u32 tid = threadIdx.x;
   // rounding correction: thread-private row in tensor memory (cells [0, 32), i32 bits)
@@ -62,13 +85,27 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_RESCALE_MINB
   tm.alloc(sm + NT::SMEM_WORDS, tid);
   const u64 row = blockIdx.x;
   const u32 L = a.level;
-  const u32* src = a.in + row * L * N;
-  u32* dst = a.out + row * (L - 1) * N;
+  const W* src;
+  W* dst;
+  if constexpr (kWide) {
+    src = a.in64 + (row * a.io_level_in + a.io_off) * N;
+    dst = a.out64 + (row * a.io_level_out + a.io_off) * N;
+  } else {
+    src = a.in + row * L * N;
+    dst = a.out + row * (L - 1) * N;
+  }
 
   u32 x[32];
   {
     const DevPrime& Pl = B.p[L - 1];
-    NT::gload_C(x, src + static_cast<u64>(L - 1) * N, tid);
+#pragma unroll
+    for (int k = 0; k < 32; k += 4) {
+      const uint4 v = ld4(src + static_cast<u64>(L - 1) * N + NT::jC(tid, k));
+      x[k] = v.x;
+      x[k + 1] = v.y;
+      x[k + 2] = v.z;
+      x[k + 3] = v.w;
+    }
     NT::inverse(x, sm, tid, Pl);
 #pragma unroll
     for (int c = 0; c < 32; c += 8) {
@@ -95,11 +132,11 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_RESCALE_MINB
 #pragma unroll
       for (int k = 0; k < 32; ++k) x[k] = reduce32(x[k], Pi);
     }
-    const u32* in_i = src + static_cast<u64>(i) * N;
-    u32* out_i = dst + static_cast<u64>(i) * N;
+    const W* in_i = src + static_cast<u64>(i) * N;
+    W* out_i = dst + static_cast<u64>(i) * N;
     uint4 yv[8];  // issued before the transform so the loads overlap it
 #pragma unroll
-    for (int g = 0; g < 8; ++g) yv[g] = __ldg(reinterpret_cast<const uint4*>(in_i + NT::jC(tid, 4 * g)));
+    for (int g = 0; g < 8; ++g) yv[g] = ld4(in_i + NT::jC(tid, 4 * g));
     NT::forward(x, sm, tid, Pi);
     const u32 q = Pi.q, pv = a.pinv[i], ps = a.pinv_sh[i];
 #pragma unroll
@@ -111,7 +148,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_RESCALE_MINB
       o.y = mul_shoup(y.y + q - x[k + 1], pv, ps, q);
       o.z = mul_shoup(y.z + q - x[k + 2], pv, ps, q);
       o.w = mul_shoup(y.w + q - x[k + 3], pv, ps, q);
-      *reinterpret_cast<uint4*>(out_i + j) = o;
+      st4(out_i + j, o);
     }
   }
   tm.free(tid);
@@ -1206,7 +1243,8 @@ int launch_rescale(int logn, const RescaleArgs& a, const Basis& B, cudaStream_t 
   if (a.rows == 0) return 0;
   HG_LOGN_SWITCH(logn, {
     const size_t sm = sizeof(u32) * (Ntt<LN, true>::SMEM_WORDS + 4);
-    auto rk = a.lazy ? k_rescale<LN, true> : k_rescale<LN, false>;
+    auto rk = a.in64 != nullptr ? (a.lazy ? k_rescale<LN, true, u64> : k_rescale<LN, false, u64>)
+                                : (a.lazy ? k_rescale<LN, true> : k_rescale<LN, false>);
     set_smem(rk, sm);
     ProfScope ps("k_rescale", s);
     rk<<<a.rows, 1 << (LN - 5), sm, s>>>(a, B);

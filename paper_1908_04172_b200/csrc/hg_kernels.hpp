@@ -23,6 +23,11 @@ struct RescaleArgs {
   u32 pinv_sh[kMaxPrimes];
   u32 pm[kMaxPrimes];       // multiple of q_i >= floor(q_{level-1}/2): correction + pm >= 0
   int lazy;                 // every pm_i + floor(q_{level-1}/2) < 4 q_i: feed c + pm_i unreduced
+  // Wide I/O (in64 != nullptr): the `level` limbs are limbs [io_off, io_off + level) of u64
+  // rows of io_level_in limbs (output: io_level_out limbs), read and written in place
+  const u64* in64;
+  u64* out64;
+  u32 io_level_in, io_level_out, io_off;
 };
 
 struct MacDenseArgs {
