@@ -46,14 +46,20 @@ constexpr u32 kTcSmallK = HG_TC_SMALLK;           // K at or below which the N =
 
 // XW: the input residue word -- u32, or u64 when the limbs are read straight out of a wide
 // (u64) tensor (the 30-bit limbs of BASELINE c4/c5b), so no narrowed copy is needed.
+// weight / plane ring depth: 5 for the one-CTA-per-SM N = 64 tile (measured 4% faster on
+// c5b than 4), 4 for N = 32 (two CTAs per SM must fit)
+template <int TN>
+constexpr int tc_stages() { return TN == 64 ? 5 : 4; }
+
 template <int TN, typename XW = u32>
 struct TcSmem {
-  uint8_t a[kTcS][4][kTcPlaneA];  // weight planes (K-major core matrices), filled by cp.async.bulk
-  uint8_t b[kTcS][4][TN * kTcK];  // input planes, written by the producer warps; the planes of a
+  static constexpr int kS = tc_stages<TN>();
+  uint8_t a[kS][4][kTcPlaneA];  // weight planes (K-major core matrices), filled by cp.async.bulk
+  uint8_t b[kS][4][TN * kTcK];  // input planes, written by the producer warps; the planes of a
                                   // stage are consecutive, i.e. one K-major (planes*TN) x 32 matrix
   uint8_t zero_a[kTcPlaneA];      // zero weight plane: initialises the upper accumulators
   XW xs[kTcXS][kTcK][TN];         // input residues staged by cp.async (producer ring)
-  unsigned long long full_a[kTcS], full_b[kTcS], empty[kTcS];
+  unsigned long long full_a[kS], full_b[kS], empty[kS];
   u32 tmem;
 };
 // TMEM columns: 7 diagonal accumulators of TN columns (512 for TN = 64: one CTA per SM;
@@ -118,6 +124,7 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
   extern __shared__ __align__(1024) uint8_t tc_raw[];
   TcSmem<TN, XW>& S = *reinterpret_cast<TcSmem<TN, XW>*>(tc_raw);
   constexpr bool kWide = sizeof(XW) == 8;
+  constexpr int kS = tc_stages<TN>();
   constexpr u32 kCols = tc_cols<TN>();
   const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // M tiles fastest: the CTAs in flight share their input columns (read from HBM once, the
@@ -135,7 +142,7 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
   }
   if (tid == 0) {
-    for (int i = 0; i < kTcS; ++i) {
+    for (int i = 0; i < kS; ++i) {
       mbar_init(&S.full_a[i], 1);
       mbar_init(&S.full_b[i], kTcProducers / 32);  // one arrive per producer warp
       mbar_init(&S.empty[i], 1);
@@ -156,7 +163,7 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
       const uint8_t* Wt = a.Wp + ((static_cast<u64>(limb) * a.Mtiles + mt) * KS) * 4 * kTcPlaneA;
       const u32 bytes = planes * kTcPlaneA;
       auto load_a = [&](u32 j) {
-        const u32 st = j % kTcS;
+        const u32 st = j % kS;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(&S.full_a[st])),
                      "r"(bytes));
         asm volatile(
@@ -164,7 +171,7 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
                 smem_addr(&S.a[st][0][0])),
             "l"(Wt + static_cast<u64>(j) * 4 * kTcPlaneA), "r"(bytes), "r"(smem_addr(&S.full_a[st])));
       };
-      for (u32 j = 0; j < kTcS - 1 && j < KS; ++j) load_a(j);
+      for (u32 j = 0; j < kS - 1 && j < KS; ++j) load_a(j);
       // One MMA per weight plane pa against all input planes at once: B = the stage's planes
       // stacked along N (planes * 64 rows), D at TMEM column pa * 64, so input plane pb lands
       // in columns (pa + pb) * 64: the diagonal accumulator D_s, s = pa + pb, with no
@@ -172,10 +179,10 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
       const u32 idesc = (2u << 4) | (((planes * TN) >> 3) << 17) | ((kTcM >> 4) << 24);
       const u64 zd = umma_desc(smem_addr(&S.zero_a[0]));
       for (u32 ks = 0; ks < KS; ++ks) {
-        const u32 st = ks % kTcS, use = ks / kTcS;
-        const u32 j = ks + kTcS - 1;
+        const u32 st = ks % kS, use = ks / kS;
+        const u32 j = ks + kS - 1;
         if (j < KS) {
-          if (j >= kTcS) mbar_wait(&S.empty[j % kTcS], ((j / kTcS) - 1) & 1);
+          if (j >= kS) mbar_wait(&S.empty[j % kS], ((j / kS) - 1) & 1);
           load_a(j);
         }
         mbar_wait(&S.full_a[st], use & 1);
@@ -226,7 +233,7 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
       asm volatile("cp.async.commit_group;\n" ::);
     }
     for (u32 ks = 0; ks < KS; ++ks) {
-      const u32 st = ks % kTcS, use = ks / kTcS;
+      const u32 st = ks % kS, use = ks / kS;
       asm volatile("cp.async.wait_group %0;\n" ::"n"(kTcXS - 2));
       __syncwarp();
       u32 v[TN / 32][4];
@@ -237,7 +244,7 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
       __syncwarp();  // step ks's rows are consumed before the ring slot is refilled
       if (ks + kTcXS - 1 < KS) issue(ks + kTcXS - 1);
       asm volatile("cp.async.commit_group;\n" ::);
-      if (ks >= kTcS) mbar_wait(&S.empty[st], (use - 1) & 1);
+      if (ks >= kS) mbar_wait(&S.empty[st], (use - 1) & 1);
 #pragma unroll
       for (int h = 0; h < TN / 32; ++h) {
         // 4 x 4 byte transpose (8 PRMT): plane p gets byte p of the 4 residues k = r0 .. r0+3
@@ -256,7 +263,7 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
     asm volatile("cp.async.wait_group 0;\n" ::);
 
     // ===== epilogue: warp w reads TMEM lanes 32*(w%4).., columns (w/4)*32 .. +32 =====
-    mbar_wait(&S.empty[(KS - 1) % kTcS], ((KS - 1) / kTcS) & 1);
+    mbar_wait(&S.empty[(KS - 1) % kS], ((KS - 1) / kS) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
     const u32 lg = warp & 3, ch = warp >> 2;
     const u32 m = mt * kTcM + lg * 32 + lane;
