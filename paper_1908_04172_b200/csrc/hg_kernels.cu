@@ -1020,33 +1020,51 @@ __device__ __forceinline__ double2 cmul_exact(double2 x, double2 w) {
 __device__ __forceinline__ u32 bitrev_n(u32 i, u32 logn) { return __brev(i) >> (32 - logn); }
 
 // One CTA per plaintext; the FFT works on a global scratch row (L2 resident).
+// SMEM: the n-point working array in shared memory (n <= 8192: 128 KB, one CTA per SM),
+// else a global scratch row per plaintext (L2-resident).
+template <bool SMEM>
 __global__ void __launch_bounds__(512) k_fft_encode(const double* slots, u32 n_slots, u32 n, u32 logn, u32 level,
                                                     double scale, const double2* roots, const double2* twist,
                                                     double2* scratch, ulonglong2* mags, unsigned long long* max_mant,
                                                     int* max_exp) {
+  extern __shared__ double2 fft_sm[];
   const u64 pt = blockIdx.x;
   const u32 tid = threadIdx.x;
-  double2* a = scratch + pt * n;
+  double2* a = SMEM ? fft_sm : scratch + pt * n;
+  const double2* rt = roots;
+  if (SMEM) {  // the n/2 roots staged next to the working array
+    double2* r = fft_sm + n;
+    for (u32 i = tid; i < n / 2; i += blockDim.x) r[i] = roots[i];
+    rt = r;
+  }
   const double* s = slots + pt * 2 * static_cast<u64>(n_slots);
-  // conjugate extension (henet/fft.hpp:59-63), then the bit-reversal permutation (:89-92)
-  for (u32 i = tid; i < n; i += blockDim.x) {
-    const u32 j = bitrev_n(i, logn);
+  // conjugate extension (henet/fft.hpp:59-63), then the bit-reversal permutation (:89-92):
+  // element j lands at a[bitrev(j)] (coalesced slot reads)
+  for (u32 j = tid; j < n; j += blockDim.x) {
     double2 e = make_double2(0.0, 0.0);
     if (j < n_slots) e = make_double2(s[2 * j], s[2 * j + 1]);
     else if (n - 1 - j < n_slots) { const u32 jj = n - 1 - j; e = make_double2(s[2 * jj], -s[2 * jj + 1]); }
-    __stcg(&a[i], e);
+    const u32 i = bitrev_n(j, logn);
+    if (SMEM) a[i] = e; else __stcg(&a[i], e);
   }
   __syncthreads();
   // radix-2 DIT stages (henet/fft.hpp:93-104)
-  for (u32 len = 2; len <= n; len <<= 1) {
-    const u32 half = len >> 1, step = n / len;
+  for (u32 lh = 0; lh < logn; ++lh) {  // len = 2^(lh + 1), half = 2^lh (powers of two: shifts)
+    const u32 half = 1u << lh, len = half << 1, step = n >> (lh + 1);
     for (u32 idx = tid; idx < n / 2; idx += blockDim.x) {
-      const u32 base = (idx / half) * len, k = idx % half;
-      const double2 w = roots[k * step];
-      const double2 u = __ldcg(&a[base + k]);
-      const double2 v = cmul_exact(__ldcg(&a[base + k + half]), w);
-      __stcg(&a[base + k], make_double2(__dadd_rn(u.x, v.x), __dadd_rn(u.y, v.y)));
-      __stcg(&a[base + k + half], make_double2(__dsub_rn(u.x, v.x), __dsub_rn(u.y, v.y)));
+      const u32 base = (idx >> lh) << (lh + 1), k = idx & (half - 1);
+      const double2 w = rt[k * step];
+      const double2 u = SMEM ? a[base + k] : __ldcg(&a[base + k]);
+      const double2 v = cmul_exact(SMEM ? a[base + k + half] : __ldcg(&a[base + k + half]), w);
+      const double2 o0 = make_double2(__dadd_rn(u.x, v.x), __dadd_rn(u.y, v.y));
+      const double2 o1 = make_double2(__dsub_rn(u.x, v.x), __dsub_rn(u.y, v.y));
+      if (SMEM) {
+        a[base + k] = o0;
+        a[base + k + half] = o1;
+      } else {
+        __stcg(&a[base + k], o0);
+        __stcg(&a[base + k + half], o1);
+      }
     }
     __syncthreads();
   }
@@ -1058,7 +1076,7 @@ __global__ void __launch_bounds__(512) k_fft_encode(const double* slots, u32 n_s
   unsigned long long bm = 0;
   int be = -100000;
   for (u32 k = tid; k < n; k += blockDim.x) {
-    const double2 e = __ldcg(&a[k]);
+    const double2 e = SMEM ? a[k] : __ldcg(&a[k]);
     const double2 tw = twist[k];
     const double re = __dsub_rn(__dmul_rn(e.x, tw.x), __dmul_rn(e.y, -tw.y));
     const double coeff = __dmul_rn(re, inv_n);
@@ -1067,12 +1085,24 @@ __global__ void __launch_bounds__(512) k_fft_encode(const double* slots, u32 n_s
     const unsigned __int128 mag = x87_roundl_mag(x);
     mags[pt * n + k] = make_ulonglong2(static_cast<u64>(mag), static_cast<u64>(mag >> 64) | (x.neg ? (1ull << 63) : 0));
   }
-  s_mant[tid] = bm;
-  s_exp[tid] = be;
+  // largest magnitude: warp shuffles, then one entry per warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, bm, o);
+    const int e2 = __shfl_xor_sync(0xffffffffu, be, o);
+    if (m2 != 0 && (bm == 0 || e2 > be || (e2 == be && m2 > bm))) { bm = m2; be = e2; }
+  }
+  if ((tid & 31) == 0) {
+    s_mant[tid >> 5] = bm;
+    s_exp[tid >> 5] = be;
+  }
   __syncthreads();
   if (tid == 0) {
-    for (u32 t = 1; t < blockDim.x; ++t) {
-      if (s_mant[t] != 0 && (s_exp[t] > be || (s_exp[t] == be && s_mant[t] > bm))) { bm = s_mant[t]; be = s_exp[t]; }
+    for (u32 t = 1; t < blockDim.x / 32; ++t) {
+      if (s_mant[t] != 0 && (bm == 0 || s_exp[t] > be || (s_exp[t] == be && s_mant[t] > bm))) {
+        bm = s_mant[t];
+        be = s_exp[t];
+      }
     }
     max_mant[pt] = bm;
     max_exp[pt] = be;
@@ -1446,8 +1476,20 @@ int launch_fft_encode(const double* slots, u32 n_slots, u64 count, u32 n, u32 le
   u32 logn = 0;
   while ((1u << logn) < n) ++logn;
   ProfScope ps("k_fft_encode", s);
-  k_fft_encode<<<count, 512, 0, s>>>(slots, n_slots, n, logn, level, scale, roots, twist, scratch, mags, max_mant,
-                                      max_exp);
+  if (n <= 8192) {
+    const size_t sm = static_cast<size_t>(n) * sizeof(double2) * 3 / 2;  // array + n/2 roots
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_fft_encode<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           8192 * sizeof(double2) * 3 / 2);
+      attr = true;
+    }
+    k_fft_encode<true><<<count, 512, sm, s>>>(slots, n_slots, n, logn, level, scale, roots, twist, scratch, mags,
+                                             max_mant, max_exp);
+  } else {
+    k_fft_encode<false><<<count, 512, 0, s>>>(slots, n_slots, n, logn, level, scale, roots, twist, scratch, mags,
+                                              max_mant, max_exp);
+  }
   return 1;
 }
 

@@ -68,13 +68,16 @@ __device__ __forceinline__ unsigned __int128 x87_roundl_mag(const X87& x) {
 }
 
 __device__ __forceinline__ u32 residue_mag(unsigned __int128 mag, bool neg, const DevPrime& P) {
-  const u64 q = P.q;
+  // Barrett (reduce64) instead of u64 '%': (hi mod q) 2^64 + lo, with 2^64 mod q =
+  // (2^32 mod q)^2 mod q; every partial product stays below 2^64 for q < 2^32
   const u64 hi = static_cast<u64>(mag >> 64), lo = static_cast<u64>(mag);
-  // 2^64 mod q
-  const u64 t64 = (0xffffffffffffffffull % q + 1) % q;
-  u64 r = ((hi % q) * t64 + lo % q) % q;
-  if (neg && r != 0) r = q - r;
-  return static_cast<u32>(r);
+  u32 r = reduce64(lo, P);
+  if (hi != 0) {
+    const u32 t64 = reduce64(static_cast<u64>(P.r32) * P.r32, P);
+    r = reduce64(static_cast<u64>(reduce64(hi, P)) * t64 + r, P);
+  }
+  if (neg && r != 0) r = P.q - r;
+  return r;
 }
 
 // |roundl(v * s)| as a 128-bit magnitude plus its sign.
