@@ -10,6 +10,7 @@
 namespace hg {
 
 constexpr int kCrtWords = 4;  // Q < 2^256 (chains of <= 8 primes below 2^32)
+constexpr int kCrtLimbs = 8;  // the GPU decoder's level limit (Q within kCrtWords words)
 
 // Residue pointers are u32 words, or u64 words in wide contexts (the launchers' `wide`).
 struct EncArgs {
@@ -29,6 +30,8 @@ struct CrtTables {
   u64 big_q[kCrtWords + 1];                 // Q = prod q_i
   u64 q_half[kCrtWords + 1];                // floor(Q / 2)
   u64 inv[kMaxPrimes];                      // (Q / q_i)^-1 mod q_i
+  u64 ginv[kCrtLimbs][kCrtLimbs];           // Garner: q_j^-1 mod q_i (j < i)
+  u64 q[kCrtLimbs];                         // the level's primes
 };
 
 struct DecArgs {

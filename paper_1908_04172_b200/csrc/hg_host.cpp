@@ -2549,7 +2549,12 @@ void decode_into(const Context& c, const hg_secret_key* sk, const void* ct, u64 
     const u32 L = level;
     std::vector<u64> big{1};
     for (u32 i = 0; i < L; ++i) mw_mul_small(big, c.chain[i]);
-    require(big.size() <= static_cast<size_t>(kCrtWords), "modulus too large for the GPU decoder");
+    require(big.size() <= static_cast<size_t>(kCrtWords) && L <= static_cast<u32>(kCrtLimbs),
+            "modulus too large for the GPU decoder");
+    for (u32 i = 0; i < L; ++i) {
+      a.crt.q[i] = c.chain[i];
+      for (u32 j = 0; j < i; ++j) a.crt.ginv[i][j] = nt::inv(c.chain[j] % c.chain[i], c.chain[i]);
+    }
     a.words = static_cast<u32>(big.size());
     for (u32 k = 0; k < a.words; ++k) a.crt.big_q[k] = big[k];
     for (u32 k = 0; k < a.words; ++k) a.crt.q_half[k] = (big[k] >> 1) | (k + 1 < a.words ? (big[k + 1] << 63) : 0);
