@@ -1023,7 +1023,7 @@ __device__ __forceinline__ u32 bitrev_n(u32 i, u32 logn) { return __brev(i) >> (
 // SMEM: the n-point working array in shared memory (n <= 8192: 128 KB, one CTA per SM),
 // else a global scratch row per plaintext (L2-resident).
 template <bool SMEM>
-__global__ void __launch_bounds__(512) k_fft_encode(const double* slots, u32 n_slots, u32 n, u32 logn, u32 level,
+__global__ void __launch_bounds__(1024) k_fft_encode(const double* slots, u32 n_slots, u32 n, u32 logn, u32 level,
                                                     double scale, const double2* roots, const double2* twist,
                                                     double2* scratch, ulonglong2* mags, unsigned long long* max_mant,
                                                     int* max_exp) {
@@ -1484,7 +1484,7 @@ int launch_fft_encode(const double* slots, u32 n_slots, u64 count, u32 n, u32 le
                            8192 * sizeof(double2) * 3 / 2);
       attr = true;
     }
-    k_fft_encode<true><<<count, 512, sm, s>>>(slots, n_slots, n, logn, level, scale, roots, twist, scratch, mags,
+    k_fft_encode<true><<<count, 1024, sm, s>>>(slots, n_slots, n, logn, level, scale, roots, twist, scratch, mags,
                                              max_mant, max_exp);
   } else {
     k_fft_encode<false><<<count, 512, 0, s>>>(slots, n_slots, n, logn, level, scale, roots, twist, scratch, mags,
