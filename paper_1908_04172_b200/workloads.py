@@ -86,13 +86,15 @@ def _gauss(rng: np.random.Generator, shape, sigma) -> np.ndarray:
     return (rng.standard_normal(int(np.prod(shape))) * sigma).astype(np.float32)
 
 
-def dense_layer(seed: int = 1, k: int = 845, m: int = 100, batch: int = 4096, packing: int = 0) -> Workload:
+def dense_layer(seed: int = 1, k: int = 845, m: int = 100, batch: int = 4096, packing: int = 0,
+                w_scale: float = 1.0) -> Workload:
     """Config 1: single encrypted dense layer 845 -> 100 with bias, W ~ N(0, 0.05^2),
     b ~ N(0, 0.01^2); one lazy rescale per output (patched plan).  packing=1: complex
-    packing (two images per slot), the bias encoded by encode_vector."""
+    packing (two images per slot), the bias encoded by encode_vector.  w_scale = 0: all-zero
+    weights (the output decrypts to the bias alone, proj/tests/test_graph.cpp:247)."""
     rng = np.random.default_rng(seed)
     blob = Blob()
-    blob.add("fc_w", [k, m], _gauss(rng, (k, m), 0.05))
+    blob.add("fc_w", [k, m], (_gauss(rng, (k, m), 0.05) * np.float32(w_scale)).astype(np.float32))
     blob.add("fc_b", [m], _gauss(rng, (m,), 0.01))
     j = {
         "name": "dense-845-100",

@@ -58,6 +58,8 @@ def test_encrypt_rejects_like_reference(env):
         H.encrypt_tensor(ctx, sk, np.zeros((3, 1)), 1, 1)
     with pytest.raises(H.ValidationError, match="exceeds q_level/2|too large"):
         H.encrypt_tensor(ctx, sk, np.full((4, 1), 1e30), 1, 0)
+    with pytest.raises(H.ValidationError, match="batch must be non-empty"):
+        H.encrypt_tensor(ctx, sk, np.zeros((0, 1)), 1, 0)
 
 
 def _decrypt_np(p, skw, words):

@@ -205,6 +205,14 @@ def test_execute_dense_lazy_complex_bias_bit_exact(env):
     _run_both(env, W.dense_layer(seed=6, k=24, m=5, batch=8192, packing=1))
 
 
+def test_execute_zero_weights_bit_exact(env):
+    """All-zero (and signed-zero) weights: the output is the bias alone
+    (proj/tests/test_graph.cpp:247), bit-exact against the reference for both packings."""
+    _run_both(env, W.dense_layer(seed=8, k=30, m=6, w_scale=0.0))
+    _run_both(env, W.dense_layer(seed=9, k=30, m=6, batch=8192, packing=1, w_scale=0.0))
+    _run_both(env, W.dense_layer(seed=10, k=30, m=6, w_scale=0.0), mode=1)
+
+
 def test_kept_encodings_equal_jit(env):
     """JIT == precompiled (proj/tests/test_graph.cpp:404-439): a model that keeps its weight
     encodings across executes gives bit-identical ciphertexts on every run, and again after the
