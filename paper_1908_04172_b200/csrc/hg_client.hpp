@@ -49,6 +49,7 @@ int launch_batch_to_slots(const double* samples, u64 count, u64 e0, u32 cnt, u32
                           double* slots, cudaStream_t s);
 // B: the context's Basis, or its BasisW when `wide`
 int launch_enc_sample(const EncArgs& a, const void* B, bool wide, cudaStream_t s);
+// list == nullptr: walks the ciphertexts in [0, n_list) whose a.flags entry is set
 int launch_enc_serial(const EncArgs& a, const u32* list, u32 n_list, const void* B, bool wide, cudaStream_t s);
 int launch_enc_combine(const EncArgs& a, const void* B, bool wide, cudaStream_t s);
 // decrypt (k_dec_combine) and, when a.coeffs is set, decode: INTT, CRT, forward embedding

@@ -549,9 +549,39 @@ static void check_scalar_encodable(const Context& ctx, double max_abs, u32 level
 }
 
 // encode_vector on the GPU: FFT encoder + NTT; returns device plaintexts [count][level][N].
+// magnitude checks with the reference's long double arithmetic (henet/encoding.hpp:122-138)
+static void check_magnitudes(const Context& ctx, u32 level, const unsigned long long* mant, const int* ex, u64 count) {
+  for (u64 i = 0; i < count; ++i) {
+    const long double mx = mant[i] ? std::ldexp(static_cast<long double>(mant[i]), ex[i]) : 0.0L;
+    require(std::fabs(static_cast<double>(mx)) < std::ldexp(1.0, 100), "scaled magnitude too large to encode");
+    require(mx < ctx.modulus_products.at(level) / 2.0L, "scaled magnitude exceeds q_level/2");
+  }
+}
+
+// Deferred checks for chunked encoders: every chunk's per-vector maximum magnitudes stay on
+// the device, and one read-back after the last chunk applies check_magnitudes (no host round
+// trip per chunk).
+struct DeferredMagnitudes {
+  BufPtr buf;
+  u64 count = 0;
+  DeferredMagnitudes(const Context& c, u64 n, cudaStream_t s)
+      : buf(c.alloc(n * (sizeof(unsigned long long) + sizeof(int)), s)), count(n) {}
+  unsigned long long* mant(u64 e0) const { return static_cast<unsigned long long*>(buf->ptr) + e0; }
+  int* ex(u64 e0) const { return reinterpret_cast<int*>(static_cast<unsigned long long*>(buf->ptr) + count) + e0; }
+  void check(const Context& c, u32 level, cudaStream_t s) const {
+    std::vector<unsigned long long> m(count);
+    std::vector<int> e(count);
+    cuda_check(cudaMemcpyAsync(m.data(), mant(0), count * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaMemcpyAsync(e.data(), ex(0), count * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaStreamSynchronize(s), "encode_vector");
+    check_magnitudes(c, level, m.data(), e.data(), count);
+  }
+};
+
+// defer != nullptr: the magnitudes go to defer at entry e0 and are checked later (no sync)
 static BufPtr encode_vectors_dev(const Context& ctx, const double* d_slots, u32 n_slots, u64 count, u32 level,
                                  double scale, cudaStream_t s, std::vector<unsigned long long>& mant,
-                                 std::vector<int>& ex) {
+                                 std::vector<int>& ex, const DeferredMagnitudes* defer = nullptr, u64 e0 = 0) {
   require(level >= 1 && level <= ctx.chain_len(), "encode level out of range");
   require(scale > 0.0, "scale must be positive");
   require(n_slots <= ctx.n / 2, "more slots than the parameters provide");
@@ -559,9 +589,9 @@ static BufPtr encode_vectors_dev(const Context& ctx, const double* d_slots, u32 
   BufPtr out = ctx.alloc(count * level * static_cast<u64>(n) * ctx.word_bytes(), s);
   BufPtr scratch = ctx.alloc(count * static_cast<u64>(n) * sizeof(double2), s);
   BufPtr mags = ctx.alloc(count * static_cast<u64>(n) * sizeof(ulonglong2), s);
-  BufPtr mm = ctx.alloc(count * (sizeof(unsigned long long) + sizeof(int)), s);
-  auto* d_mant = static_cast<unsigned long long*>(mm->ptr);
-  auto* d_exp = reinterpret_cast<int*>(d_mant + count);
+  BufPtr mm = defer ? nullptr : ctx.alloc(count * (sizeof(unsigned long long) + sizeof(int)), s);
+  auto* d_mant = defer ? defer->mant(e0) : static_cast<unsigned long long*>(mm->ptr);
+  auto* d_exp = defer ? defer->ex(e0) : reinterpret_cast<int*>(d_mant + count);
   const double2* roots = static_cast<const double2*>(ctx.fft_tables->ptr);
   const double2* twist = roots + n / 2;
   int r = launch_fft_encode(d_slots, n_slots, count, n, level, scale, roots, twist, static_cast<double2*>(scratch->ptr),
@@ -579,17 +609,13 @@ static BufPtr encode_vectors_dev(const Context& ctx, const double* d_slots, u32 
     r = launch_ntt(static_cast<int>(ctx.logn), static_cast<u32*>(out->ptr), count * level, level, false, ctx.basis, s);
   }
   check_launch(r, "ntt");
+  if (defer) return out;
   mant.resize(count);
   ex.resize(count);
   cuda_check(cudaMemcpyAsync(mant.data(), d_mant, count * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s), "d2h");
   cuda_check(cudaMemcpyAsync(ex.data(), d_exp, count * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
   cuda_check(cudaStreamSynchronize(s), "encode_vector");
-  // magnitude checks with the reference's long double arithmetic (henet/encoding.hpp:122-138)
-  for (u64 i = 0; i < count; ++i) {
-    const long double mx = mant[i] ? std::ldexp(static_cast<long double>(mant[i]), ex[i]) : 0.0L;
-    require(std::fabs(static_cast<double>(mx)) < std::ldexp(1.0, 100), "scaled magnitude too large to encode");
-    require(mx < ctx.modulus_products.at(level) / 2.0L, "scaled magnitude exceeds q_level/2");
-  }
+  check_magnitudes(ctx, level, mant.data(), ex.data(), count);
   return out;
 }
 
@@ -2423,31 +2449,28 @@ void encrypt_into(const Context& c, const hg_secret_key* sk, const void* pt, u64
     a.level = L;
     a.N = N;
     check_launch(launch_enc_sample(a, client_basis(c), c.wide, s), "encrypt sample");
-    // draws the counter-mode pass could not place (a rejection, u1 == 0): regenerate those
-    // ciphertexts by walking their streams; HG_ENC_SERIAL=1 walks every stream (tests)
-    std::vector<int> hf(count);
-    cuda_check(cudaMemcpyAsync(hf.data(), flags->ptr, count * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
-    cuda_check(cudaStreamSynchronize(s), "encrypt");
+    // draws the counter-mode pass could not place (a rejection, u1 == 0): those ciphertexts
+    // are regenerated by walking their streams, selected on the device by their flags;
+    // HG_ENC_SERIAL=1 walks every stream (tests)
     const char* ser = getenv("HG_ENC_SERIAL");
-    const bool all = ser != nullptr && ser[0] == '1';
-    std::vector<u32> list;
-    for (u64 e = 0; e < count; ++e)
-      if (all || hf[e]) list.push_back(static_cast<u32>(e));
     BufPtr dl;
-    if (!list.empty()) {
-      dl = c.alloc(list.size() * 4, s);
-      cuda_check(cudaMemcpyAsync(dl->ptr, list.data(), list.size() * 4, cudaMemcpyHostToDevice, s), "h2d");
-      check_launch(launch_enc_serial(a, static_cast<const u32*>(dl->ptr), static_cast<u32>(list.size()),
-                                     client_basis(c), c.wide, s),
-                   "encrypt serial");
+    if (ser != nullptr && ser[0] == '1') {
+      std::vector<u32> list(count);
+      for (u64 e = 0; e < count; ++e) list[e] = static_cast<u32>(e);
+      dl = c.alloc(count * 4, s);
+      cuda_check(cudaMemcpyAsync(dl->ptr, list.data(), count * 4, cudaMemcpyHostToDevice, s), "h2d");
+      cuda_check(cudaStreamSynchronize(s), "encrypt");  // the pageable list outlives the copy
     }
+    check_launch(launch_enc_serial(a, dl ? static_cast<const u32*>(dl->ptr) : nullptr, static_cast<u32>(count),
+                                   client_basis(c), c.wide, s),
+                 "encrypt serial");
     check_launch(c.wide ? launch_ntt_w(static_cast<int>(c.logn), static_cast<u64*>(a.err), count * L, L, false,
                                        c.basisw, s)
                         : launch_ntt(static_cast<int>(c.logn), static_cast<u32*>(a.err), count * L, L, false, c.basis,
                                      s),
                  "ntt");
     check_launch(launch_enc_combine(a, client_basis(c), c.wide, s), "encrypt combine");
-    cuda_check(cudaStreamSynchronize(s), "encrypt");
+    // no synchronisation: err / flags are freed stream-ordered after the combine
 }
 
 }  // namespace
@@ -2504,6 +2527,7 @@ int hg_encrypt_tensor(hg_ctx* ctx, const hg_secret_key* sk, const double* sample
     ensure(c, o, count, 2, L, s);
     const u64 chunk = 1024, out_ct = 2ull * L * N * c.word_bytes();
     BufPtr ds = c.alloc(std::min<u64>(count, chunk) * n_slots * 2 * sizeof(double), s);
+    const DeferredMagnitudes mags(c, count, s);
     for (u64 e0 = 0; e0 < count; e0 += chunk) {
       const u64 ne = std::min(chunk, count - e0);
       check_launch(launch_batch_to_slots(static_cast<const double*>(dsm->ptr), count, e0, static_cast<u32>(ne),
@@ -2512,10 +2536,10 @@ int hg_encrypt_tensor(hg_ctx* ctx, const hg_secret_key* sk, const double* sample
       std::vector<unsigned long long> mant;
       std::vector<int> ex;
       BufPtr pt = encode_vectors_dev(c, static_cast<const double*>(ds->ptr), n_slots, ne, L, c.default_scale, s, mant,
-                                     ex);
+                                     ex, &mags, e0);
       encrypt_into(c, sk, pt->ptr, ne, seed, e0, static_cast<char*>(o.buf->ptr) + e0 * out_ct, s);
     }
-    cuda_check(cudaStreamSynchronize(s), "encrypt");
+    mags.check(c, L, s);  // synchronises the stream
     out->b = o;
     out->b.shape = {static_cast<u32>(count)};
   });
@@ -2717,6 +2741,7 @@ int hg_refresh_engine_apply(void* engine, int kind, uint32_t window, uint32_t la
     BufPtr sl = c.alloc(std::min(groups, cg) * window * half * 2 * sizeof(double), s);
     BufPtr res = c.alloc(std::min(groups, cg) * half * 2 * sizeof(double), s);
     const u64 seed = derive_seed_host(eng->seed, layer_seq);
+    const DeferredMagnitudes mags(c, groups, s);
     for (u64 g0 = 0; g0 < groups; g0 += cg) {
       const u64 ng = std::min(cg, groups - g0);
       decode_into(c, eng->sk, static_cast<const char*>(b.buf->ptr) + g0 * window * in_ct, ng * window, b.polys,
@@ -2727,9 +2752,10 @@ int hg_refresh_engine_apply(void* engine, int kind, uint32_t window, uint32_t la
       std::vector<unsigned long long> mant;
       std::vector<int> ex;
       BufPtr pt = encode_vectors_dev(c, static_cast<const double*>(res->ptr), half, ng, L, c.default_scale, s, mant,
-                                     ex);
+                                     ex, &mags, g0);
       encrypt_into(c, eng->sk, pt->ptr, ng, seed, g0, static_cast<char*>(o.buf->ptr) + g0 * out_ct, s);
     }
+    mags.check(c, L, s);  // one read-back per layer; synchronises the stream
     response->b = o;
     response->b.shape = {static_cast<u32>(groups)};
   });
