@@ -741,14 +741,16 @@ def c4_run(args, ws, rank, local):
     for _ in range(max(args.warmup, 1)):
         out = H.execute(ctx, model, plan, x, None, eng)
     ctx.synchronize()
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 6))
     l0 = ctx.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    e0, e1 = ev[0], ev[-1]
     e0.record(ext)
-    for _ in range(steps):
+    for i in range(steps):
         out = H.execute(ctx, model, plan, x, None, eng)
-    e1.record(ext)
+        ev[i + 1].record(ext)
     e1.synchronize()
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
     launches = ctx.launch_count() - l0
     clk = clocks.stop()
     t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=f"cuda:{local}")
@@ -791,7 +793,7 @@ def c4_run(args, ws, rank, local):
                                  f"{hw}x{hw} input (1-pixel halo); one tile per step, the 56x56 batch = {tiles} steps",
                        "refresh": "client-aided ReLU6 on the GPU (hg_refresh_engine, clamp [0, 6])",
                        "parallelism": f"replicas x{ws}"},
-            "tile_ms": tile_ms, "roofline": None,
+            "tile_ms": tile_ms, "tile_ms_steps": step_ms, "roofline": None,
             "roofline_note": "dominated by the client-aided refreshes (decrypt/decode/encode/encrypt of 2 x 9600 ciphertexts per tile); see the kernel shares",
             "cpu_baseline": cpu, "e2e": None, "gpu_launches": launches, "clocks": clk,
             "check": {"max_abs_err_vs_cleartext_interior": err, "images_checked": 16}}))

@@ -17,7 +17,7 @@ x = H.encrypt_tensor(ctx, sk, acts, 7, shape=wl.input_shape)
 eng = H.RefreshEngine(ctx, sk, 77); eng.set_relu_clip(6.0)
 ext = torch.cuda.ExternalStream(ctx.stream())
 out = None
-for i in range(8):
+for i in range(int(os.environ.get('ITERS', '8'))):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     prof = i % 2 == 1
     H.prof_enable(prof)
@@ -29,4 +29,11 @@ for i in range(8):
     if prof:
         rep = H.prof_report()
         ks = f" kernel sum {sum(v['ms'] for v in rep.values()):.1f} ms (" + ", ".join(f"{k} {v['ms']:.0f}" for k, v in sorted(rep.items(), key=lambda kv: -kv[1]['ms'])[:4]) + ")"
-    print(f"execute {i}: device {e0.elapsed_time(e1):.1f} ms wall {1e3*(t1-t0):.1f} ms{ks}")
+    nm = ""
+    if os.environ.get("HG_NODE_TIMING"):
+        import ctypes
+        from paper_1908_04172_b200._lib import lib
+        arr = (ctypes.c_double * 11)()
+        lib.hg_last_exec_node_ms(ctx.handle, arr)
+        nm = " nodes: conv %.0f relu %.0f" % (arr[6], arr[8])
+    print(f"execute {i}: device {e0.elapsed_time(e1):.1f} ms wall {1e3*(t1-t0):.1f} ms{ks}{nm}")
