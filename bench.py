@@ -46,6 +46,19 @@ METRIC = "encrypted images/sec, CryptoNets-shaped N=8192 net; % of HBM/INT32 roo
 IMAGES_PER_STEP = 4096
 
 
+def _h2d_bytes(words, host_narrow):
+    """Bytes hg_tensor_upload moves over PCIe: with host narrowing, the last
+    HG_UPLOAD_DIRECT_FRAC of the ciphertexts (default 0.15, hg_upload.cpp
+    upload_direct_fraction) cross raw as u64 and the rest as packed u32."""
+    if not host_narrow:
+        return int(words.nbytes)
+    f = min(1.0, max(0.0, float(os.environ.get("HG_UPLOAD_DIRECT_FRAC", "0.15"))))
+    count = words.shape[0]
+    per_ct = words.nbytes // count
+    direct = int(count * f)
+    return int((count - direct) * per_ct // 2 + direct * per_ct)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -421,7 +434,7 @@ def b200_run(args, ws, rank, local):
         seq_up, seq_step = statistics.median(up_ms), statistics.median(step_ms)
         e_ms, seq_ms = statistics.median(pipe_trials), statistics.median(seq_trials)
         e2e = {"value": IMAGES_PER_STEP * ws / (e_ms / 1e3), "unit": "images/s",
-               "h2d_bytes_per_step": int(words.nbytes // (2 if host_narrow else 1)),
+               "h2d_bytes_per_step": _h2d_bytes(words, host_narrow),
                "d2h_bytes_per_step": int(out_host.nbytes),
                "host_input_bytes_per_step": int(words.nbytes),
                "ms_per_step": e_ms, "steps": n_e2e, "trials_ms_per_step": pipe_trials,

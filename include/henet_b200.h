@@ -130,6 +130,12 @@ int hg_tensor_deserialize(hg_ctx* ctx, const uint8_t* bytes, uint64_t len, uint6
                           hg_tensor** out, void* stream);
 uint64_t hg_tensor_serialized_size(const hg_tensor* t);
 int hg_tensor_serialize(const hg_tensor* t, uint8_t* out, uint64_t cap, void* stream);
+/* Same word order, one pointer per polynomial (RingElement) instead of one contiguous array:
+ * segs[e * polys + k] -> level * N words of polynomial k of element e.  The upload's packer
+ * threads read each segment in place, so a caller holding std::vector<Ciphertext> (the
+ * reference's CipherTensor) never builds a contiguous copy; checked like hg_tensor_upload. */
+int hg_tensor_upload_segments(hg_tensor* t, const uint64_t* const* segs, void* stream);
+int hg_tensor_download_segments(const hg_tensor* t, uint64_t* const* segs, void* stream);
 /* Same, in the device's compact u32 word order (no widening). */
 int hg_tensor_upload_u32(hg_tensor* t, const uint32_t* words, void* stream);
 int hg_tensor_download_u32(const hg_tensor* t, uint32_t* words, void* stream);
@@ -297,6 +303,13 @@ typedef struct hg_exec_stats {
 int hg_execute(hg_ctx* ctx, const hg_model* m, const hg_plan* plan, const hg_tensor* input,
                const hg_relin_key* rk, hg_nonlin_fn provider, void* provider_user,
                hg_tensor** output, hg_exec_stats* stats, void* stream);
+
+/* ExecutionStats::layer_ms (henet/graph.hpp:776-782, filled at :860-866): one (node id, ms)
+ * entry per node in execution order, from CUDA events around each node on the execute's
+ * stream, for the most recent hg_execute on the calling thread that passed `stats` (or ran
+ * with HG_NODE_TIMING set).  `*id` stays valid until the next hg_execute on this thread. */
+int hg_last_exec_layer_count(uint32_t* n);
+int hg_last_exec_layer(uint32_t index, const char** id, double* ms);
 
 /* NonlinearityEngine / LocalProvider (henet/graph.hpp:699-752) on the GPU: decrypt and
  * decode every request ciphertext, ReLU or the per-slot window max, encode_vector at the

@@ -43,13 +43,30 @@ inline void check(int rc) {
 }
 
 // Device mirror of one CkksContext (+ its relin keys and models), created lazily.
-// FNV-1a over bytes; device caches are keyed by content, never by address
-// (a freed object's address can be reused by a different model or key).
-inline u64 fnv(const void* p, std::size_t n, u64 h = 1469598103934665603ull) {
+// Device caches are keyed by content, never by address (a freed object's address can be
+// reused by a different model or key).  The content hash reads the words in place, four
+// independent xxHash64-style lanes of 8-byte words (~10+ GB/s), so keying a 5.5 MB relin
+// key or 64 MB of c5b weights costs well under the upload it saves.
+inline u64 hash_bytes(const void* p, std::size_t n, u64 h = 0x9E3779B97F4A7C15ull) {
+  constexpr u64 P1 = 0x9E3779B185EBCA87ull, P2 = 0xC2B2AE3D27D4EB4Full;
+  auto rotl = [](u64 x, int r) { return (x << r) | (x >> (64 - r)); };
+  auto round = [&](u64 acc, u64 w) { return rotl(acc + w * P2, 31) * P1; };
   const auto* b = static_cast<const unsigned char*>(p);
-  for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
-  return h;
+  u64 v[4] = {h + P1 + P2, h + P2, h, h - P1};
+  std::size_t i = 0;
+  for (; i + 32 <= n; i += 32) {
+    u64 w[4];
+    std::memcpy(w, b + i, 32);
+    for (int k = 0; k < 4; ++k) v[k] = round(v[k], w[k]);
+  }
+  u64 acc = rotl(v[0], 1) + rotl(v[1], 7) + rotl(v[2], 12) + rotl(v[3], 18) + n;
+  for (; i < n; ++i) acc = (acc ^ b[i]) * 1099511628211ull;
+  acc ^= acc >> 33;
+  acc *= P2;
+  acc ^= acc >> 29;
+  return acc;
 }
+inline u64 fnv(const void* p, std::size_t n, u64 h = 1469598103934665603ull) { return hash_bytes(p, n, h); }
 
 class Device {
  public:
@@ -74,13 +91,15 @@ class Device {
   u32 degree() const { return n_; }
 
   const hg_relin_key* relin(const RelinKey& rk) {
-    std::vector<u64> w;
+    u64 key = 0x52454c494eull;
     for (const auto& part : rk.parts)
-      for (const auto& p : part) w.insert(w.end(), p.words().begin(), p.words().end());
-    const u64 key = fnv(w.data(), w.size() * sizeof(u64));
+      for (const auto& p : part) key = hash_bytes(p.words().data(), p.words().size() * sizeof(u64), key);
     std::lock_guard<std::mutex> g(mu_);
     auto it = keys_.find(key);
     if (it != keys_.end()) return it->second;
+    std::vector<u64> w;
+    for (const auto& part : rk.parts)
+      for (const auto& p : part) w.insert(w.end(), p.words().begin(), p.words().end());
     hg_relin_key* k = nullptr;
     check(hg_relin_key_upload(ctx_, w.data(), w.size(), &k));
     keys_[key] = k;
@@ -133,9 +152,11 @@ class Device {
     return h;
   }
 
-  // PlainModel -> hg_model (weights + nodes); load_model's checks rerun device-side.
-  const hg_model* model(const PlainModel& m) {
-    const u64 key = fingerprint(m);
+  // PlainModel -> hg_model (weights + nodes); load_model's checks rerun device-side.  One
+  // device model per (content, keep_encodings): the flag is fixed when the model is created,
+  // so concurrent executes with and without a shared WeightEncoder never toggle it.
+  const hg_model* model(const PlainModel& m, bool keep_encodings) {
+    const u64 key = fingerprint(m) ^ (keep_encodings ? 0x4b454550ull : 0);
     std::lock_guard<std::mutex> g(mu_);
     auto it = models_.find(key);
     if (it != models_.end()) return it->second;
@@ -165,6 +186,7 @@ class Device {
       check(hg_model_add_node(hm, &d));
     }
     check(hg_model_finalize(hm));
+    check(hg_model_keep_encodings(hm, keep_encodings ? 1 : 0));
     models_[key] = hm;
     return hm;
   }
@@ -200,41 +222,44 @@ struct Tensor {
   ~Tensor() { hg_tensor_destroy(t); }
 };
 
+// Ciphertexts -> device tensor.  The library's packer threads read every RingElement's words
+// in place (hg_tensor_upload_segments), so no contiguous host copy of the tensor is built.
 inline void upload(Device& dev, const std::vector<Ciphertext>& cts, const std::vector<u32>& shape, Tensor& out) {
   require(!cts.empty(), "empty cipher tensor");
   const u32 polys = static_cast<u32>(cts[0].size());
   const u32 level = static_cast<u32>(cts[0].level());
   check(hg_tensor_create(dev.ctx(), cts.size(), polys, level, cts[0].scale, static_cast<int>(cts[0].packing), &out.t));
-  std::vector<u64> w;
-  w.reserve(cts.size() * polys * level * dev.degree());
+  std::vector<const uint64_t*> segs;
+  segs.reserve(cts.size() * polys);
   for (const auto& ct : cts) {
     require(ct.size() == polys && ct.level() == level, "ciphertext shape mismatch inside tensor");
-    for (const auto& p : ct.polys) w.insert(w.end(), p.words().begin(), p.words().end());
+    for (const auto& p : ct.polys) segs.push_back(p.words().data());
   }
-  check(hg_tensor_upload(out.t, w.data(), nullptr));
+  check(hg_tensor_upload_segments(out.t, segs.data(), nullptr));
   if (!shape.empty()) check(hg_tensor_set_shape(out.t, shape.data(), static_cast<uint32_t>(shape.size())));
 }
 
+// Device tensor -> ciphertexts, written straight into each RingElement's words.
 inline std::vector<Ciphertext> download(Device& dev, const hg_tensor* t) {
   uint64_t count = 0;
   uint32_t polys = 0, level = 0;
   double scale = 0;
   int packing = 0;
   check(hg_tensor_info(t, &count, &polys, &level, &scale, &packing));
-  std::vector<u64> w(count * polys * level * dev.degree());
-  check(hg_tensor_download(t, w.data(), nullptr));
   std::vector<Ciphertext> out(count);
-  const std::size_t pw = static_cast<std::size_t>(level) * dev.degree();
+  std::vector<uint64_t*> segs;
+  segs.reserve(count * polys);
   for (uint64_t e = 0; e < count; ++e) {
+    out[e].polys.reserve(polys);
     for (u32 p = 0; p < polys; ++p) {
-      RingElement r(dev.degree(), level, PolyDomain::Ntt);
-      std::memcpy(r.words().data(), w.data() + (e * polys + p) * pw, pw * sizeof(u64));
-      out[e].polys.push_back(std::move(r));
+      out[e].polys.emplace_back(dev.degree(), level, PolyDomain::Ntt);
+      segs.push_back(out[e].polys.back().words().data());
     }
     out[e].scale = scale;
     out[e].packing = static_cast<PackingMode>(packing);
     out[e].slots = dev.degree() / 2;
   }
+  check(hg_tensor_download_segments(t, segs.data(), nullptr));
   return out;
 }
 
@@ -251,10 +276,10 @@ inline int provider_trampoline(void* user, int kind, uint32_t window, uint32_t l
     auto req = download(*pc->dev, request);
     auto fresh = pc->provider->apply(kind == HG_NONLIN_RELU ? NonlinKind::Relu : NonlinKind::MaxPool, window,
                                      layer_seq, req);
-    std::vector<u64> w;
+    std::vector<const uint64_t*> segs;
     for (const auto& ct : fresh)
-      for (const auto& p : ct.polys) w.insert(w.end(), p.words().begin(), p.words().end());
-    return hg_tensor_upload(response, w.data(), nullptr);
+      for (const auto& p : ct.polys) segs.push_back(p.words().data());
+    return hg_tensor_upload_segments(response, segs.data(), nullptr);
   } catch (...) {
     return 1;
   }
@@ -332,10 +357,9 @@ inline std::vector<std::vector<double>> decrypt_tensor(const CkksContext& ctx, c
 inline CipherTensor execute(std::shared_ptr<const CkksContext> ctx, const PlainModel& model, const RescalePlan& plan,
                             const CipherTensor& input, const ExecutionConfig& cfg, ExecutionStats* stats = nullptr) {
   Device& dev = device_for(*ctx);
-  const hg_model* hm = dev.model(model);
   // a shared WeightEncoder (ExecutionConfig::encoder, henet/graph.hpp:773) keeps encodings
   // across calls; without one the reference encodes per call -- mirrored on the device
-  check(hg_model_keep_encodings(const_cast<hg_model*>(hm), cfg.encoder != nullptr ? 1 : 0));
+  const hg_model* hm = dev.model(model, cfg.encoder != nullptr);
   hg_plan* hp = nullptr;
   check(hg_plan_create(static_cast<int>(plan.mode), plan.planned_rescale_ops, &hp));
   std::unique_ptr<hg_plan, void (*)(hg_plan*)> plan_guard(hp, hg_plan_destroy);
@@ -367,6 +391,16 @@ inline CipherTensor execute(std::shared_ptr<const CkksContext> ctx, const PlainM
     stats->relin_ops = st.relin_ops;
     stats->nonlin_elements = st.nonlin_elements;
     stats->wall_ms = st.wall_ms;
+    // layer_ms: one (node id, ms) per node in execution order (henet/graph.hpp:860-866),
+    // from CUDA events around each node
+    uint32_t nl = 0;
+    check(hg_last_exec_layer_count(&nl));
+    for (uint32_t i = 0; i < nl; ++i) {
+      const char* id = nullptr;
+      double ms = 0;
+      check(hg_last_exec_layer(i, &id, &ms));
+      stats->layer_ms.emplace_back(id, ms);
+    }
   }
   return result;
 }

@@ -47,6 +47,7 @@ _PROTOS = {
                           C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, vp, vp, C.c_int,
                           C.c_int, vp, C.c_uint32, vp]),
     "oc_square_layer": (None, [vp, vp, C.c_uint64, C.c_uint32, vp, C.c_int, vp]),
+    "oc_dense_lazy": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, vp, C.c_int, vp]),
 }
 
 _lib = None
@@ -240,6 +241,17 @@ class OracleContext:
         if lib().oc_dense(self._h, _p(x), K, M, level, float(x_scale), _p(w), _p(b) if b is not None else None,
                           packing, int(rescale), _p(outs) if outs is not None else None, cnt, _p(out)):
             raise OracleError("dense: validation error")
+        return out
+
+    def dense_lazy(self, x, w, level, rescale=True):
+        """oc_dense without a bias, 128-bit sums reduced once (large-K checks)."""
+        x = _u64(x)
+        w = np.ascontiguousarray(w, dtype=np.float32)
+        K, M = w.shape
+        lo = level - 1 if rescale else level
+        out = np.empty((M, 2, lo, self.n), dtype=np.uint64)
+        if lib().oc_dense_lazy(self._h, _p(x), K, M, level, _p(w), int(rescale), _p(out)):
+            raise OracleError("dense_lazy: validation error")
         return out
 
     def conv(self, x, w, in_shape, stride, pad, level, x_scale, bias=None, packing=0, rescale=True, outputs=None):

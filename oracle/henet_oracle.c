@@ -999,6 +999,71 @@ int oc_dense(const oc_ctx* c, const uint64_t* x, uint32_t K, uint32_t M, uint32_
   return err;
 }
 
+/* oc_dense for large K without a bias (the c5b shape): the same residues as mac_output's
+ * per-tap mul_ct_pt_scalar + add_ct_ct chain (henet/graph.hpp:905-933), computed as one
+ * 128-bit sum of the products per residue and a single Barrett128 at the end:
+ * sum_i (a_i b_i mod p) mod p == (sum_i a_i b_i) mod p, and K < 2^48 terms of < 2^80 fit
+ * in 128 bits.  Blocked over residues so x streams through memory once for all outputs.
+ * tests/test_oracle_golden.py checks it against oc_dense. */
+int oc_dense_lazy(const oc_ctx* c, const uint64_t* x, uint32_t K, uint32_t M, uint32_t level,
+                  const float* w, int rescale, uint64_t* out) {
+  const u32 n = c->n;
+  const size_t cw = 2 * (size_t)level * n;
+  u64* wres = malloc(sizeof(u64) * (size_t)K * M * level); /* [limb][k][m] */
+  u64* acc = malloc(sizeof(u64) * (size_t)M * cw);         /* canonical sums, [m][poly][limb][N] */
+  int err = 0;
+  for (u32 k = 0; k < K && !err; ++k)
+    for (u32 m = 0; m < M && !err; ++m) {
+      u64 r[MAXB];
+      if (oc_encode_scalar(c, (double)w[(size_t)k * M + m], level, c->scale, r)) err = 1;
+      for (u32 i = 0; i < level; ++i) wres[((size_t)i * K + k) * M + m] = r[i];
+    }
+  if (err) {
+    free(wres);
+    free(acc);
+    return 1;
+  }
+  enum { RB = 64 };
+  const size_t nblk = cw / RB;
+#pragma omp parallel
+  {
+    u128* s = malloc(sizeof(u128) * (size_t)M * RB);
+#pragma omp for schedule(dynamic)
+    for (size_t b = 0; b < nblk; ++b) {
+      const size_t r0 = b * RB;
+      const u32 limb = (u32)((r0 / n) % level);
+      const u64* wl = wres + (size_t)limb * K * M;
+      memset(s, 0, sizeof(u128) * (size_t)M * RB);
+      for (u32 k = 0; k < K; ++k) {
+        const u64* xk = x + (size_t)k * cw + r0;
+        const u64* wk = wl + (size_t)k * M;
+        for (u32 m = 0; m < M; ++m) {
+          const u64 wv = wk[m];
+          u128* sm = s + (size_t)m * RB;
+          for (u32 t = 0; t < RB; ++t) sm[t] += (u128)xk[t] * wv;
+        }
+      }
+      const prime_t* q = &c->p[limb];
+      for (u32 m = 0; m < M; ++m)
+        for (u32 t = 0; t < RB; ++t) {
+          const u128 z = s[(size_t)m * RB + t];
+          acc[(size_t)m * cw + r0 + t] = oc_barrett_reduce_128_p((u64)z, (u64)(z >> 64), q);
+        }
+    }
+    free(s);
+  }
+  const u32 lo = rescale ? level - 1 : level;
+  const size_t ow = 2 * (size_t)lo * n;
+#pragma omp parallel for schedule(dynamic) reduction(| : err)
+  for (u32 m = 0; m < M; ++m) {
+    if (rescale) err |= oc_rescale(c, acc + (size_t)m * cw, 2, level, level - 1, out + (size_t)m * ow);
+    else memcpy(out + (size_t)m * ow, acc + (size_t)m * cw, sizeof(u64) * cw);
+  }
+  free(wres);
+  free(acc);
+  return err;
+}
+
 int oc_conv(const oc_ctx* c, const uint64_t* x, uint32_t C, uint32_t IH, uint32_t IW, uint32_t F, uint32_t win,
             uint32_t stride, uint32_t pad_top, uint32_t pad_left, uint32_t OH, uint32_t OW, uint32_t level,
             double x_scale, const float* w, const float* bias, int packing, int rescale, const uint32_t* outputs,

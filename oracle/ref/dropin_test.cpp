@@ -7,7 +7,11 @@
 // henet::gpu::execute (B200) with identical arguments and requires
 // bit-identical ciphertexts, scales and statistics; likewise the client side
 // (encrypt_tensor, decrypt_tensor, LocalProvider).  Exit code 0 = pass.
+#include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <thread>
 
 #include "henet/henet.hpp"
@@ -54,6 +58,12 @@ static bool run_model(std::shared_ptr<const CkksContext> ctx, const KeyPair& key
   bool ok = same(want, got, name);
   ok = ok && s_cpu.rescale_ops == s_gpu.rescale_ops && s_cpu.relin_ops == s_gpu.relin_ops &&
        s_cpu.nonlin_elements == s_gpu.nonlin_elements;
+  // layer_ms: one entry per node, same ids in the same order (henet/graph.hpp:860-866)
+  bool layers_ok = s_cpu.layer_ms.size() == s_gpu.layer_ms.size();
+  for (std::size_t i = 0; layers_ok && i < s_cpu.layer_ms.size(); ++i)
+    layers_ok = s_cpu.layer_ms[i].first == s_gpu.layer_ms[i].first && s_gpu.layer_ms[i].second >= 0.0;
+  std::printf("  layer_ms: %zu entries %s\n", s_gpu.layer_ms.size(), layers_ok ? "ids match" : "MISMATCH");
+  ok = ok && layers_ok;
   std::printf("  stats cpu (rescale %llu relin %llu nonlin %llu, %.0f ms)  gpu (rescale %llu relin %llu nonlin %llu)\n",
               (unsigned long long)s_cpu.rescale_ops, (unsigned long long)s_cpu.relin_ops,
               (unsigned long long)s_cpu.nonlin_elements, s_cpu.wall_ms, (unsigned long long)s_gpu.rescale_ops,
@@ -61,7 +71,38 @@ static bool run_model(std::shared_ptr<const CkksContext> ctx, const KeyPair& key
   return ok;
 }
 
-int main() {
+// --bench K: the drop-in's end-to-end time per call -- henet::gpu::execute on the c2
+// CryptoNets-shaped network (make_cryptonets, 4096 images, BASELINE context) with host
+// CipherTensors in and out, i.e. upload + execute + download as a reference user sees it.
+static int bench(int steps) {
+  auto ctx = baseline_ctx();
+  KeyPair keys = keygen(*ctx, 2024, true);
+  auto gm = make_cryptonets(Preset::P13, 1);
+  PlainModel model = load_model(gm.manifest, std::span<const u8>(gm.blob.data(), gm.blob.size()));
+  RescalePlan plan = plan_lazy_rescaling(*ctx, model);
+  BatchInput in = make_random_input(model.shapes.at(model.input_node().id), 4096, 5);
+  CipherTensor x = henet::gpu::encrypt_tensor(*ctx, in, keys.secret, 77, PackingMode::Real);
+  ExecutionConfig cfg;
+  cfg.relin = &*keys.relin;
+  std::vector<double> ms;
+  for (int i = 0; i < steps + 3; ++i) {
+    const auto t0 = std::chrono::steady_clock::now();
+    CipherTensor y = henet::gpu::execute(ctx, model, plan, x, cfg);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (i >= 3) ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+    if (y.elems.size() != 10) return 1;
+  }
+  std::sort(ms.begin(), ms.end());
+  double sum = 0;
+  for (double v : ms) sum += v;
+  std::printf("{\"dropin_ms_median\": %.4f, \"dropin_ms_mean\": %.4f, \"dropin_ms_min\": %.4f, \"steps\": %d, "
+              "\"images\": 4096, \"input_cts\": %zu}\n",
+              ms[ms.size() / 2], sum / ms.size(), ms[0], steps, x.elems.size());
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 2 && std::string(argv[1]) == "--bench") return bench(std::atoi(argv[2]));
   auto ctx = baseline_ctx();
   KeyPair keys = keygen(*ctx, 2024, true);
   bool ok = true;

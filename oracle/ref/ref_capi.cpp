@@ -360,12 +360,15 @@ std::vector<Ciphertext> clip_apply(const std::shared_ptr<const CkksContext>& sct
   const double hi = g_relu_clip_hi;
   auto clamp = [hi](double v) { return v < 0.0 ? 0.0 : (v > hi ? hi : v); };
   std::vector<Ciphertext> out(cts.size());
-  for (std::size_t g = 0; g < cts.size(); ++g) {
+  // Groups are independent and seeded per group (derive_seed(derive_seed(seed, layer), g)),
+  // so the harness spreads them over the host threads with the reference's parallel_for;
+  // the result is identical to the serial loop.
+  parallel_for(cts.size(), std::thread::hardware_concurrency(), [&](std::size_t g) {
     auto slots = decode_slots(ctx, decrypt(ctx, cts[g], sk));
     for (auto& z : slots) z = {clamp(z.real()), clamp(z.imag())};
     auto pt = encode_vector(ctx, slots, ctx.chain_length(), ctx.params().default_scale);
     out[g] = encrypt(ctx, pt, sk, derive_seed(derive_seed(seed, layer_seq), g), cts[g].packing);
-  }
+  });
   return out;
 }
 

@@ -71,6 +71,8 @@ PROTOTYPES = {
     "hg_tensor_get_shape": (C.c_int, [vp, u32p, u32p]),
     "hg_tensor_upload": (C.c_int, [vp, vp, vp]),
     "hg_tensor_download": (C.c_int, [vp, vp, vp]),
+    "hg_tensor_upload_segments": (C.c_int, [vp, vp, vp]),
+    "hg_tensor_download_segments": (C.c_int, [vp, vp, vp]),
     "hg_tensor_upload_u32": (C.c_int, [vp, vp, vp]),
     "hg_tensor_download_u32": (C.c_int, [vp, vp, vp]),
     "hg_tensor_device_ptr": (vp, [vp]),
@@ -122,6 +124,8 @@ PROTOTYPES = {
     "hg_execute": (C.c_int, [vp, vp, vp, vp, vp, NONLIN_FN, vp, C.POINTER(vp), C.POINTER(hg_exec_stats), vp]),
     "hg_bench_int_peak": (C.c_int, [C.c_int, C.c_int, dblp]),
     "hg_last_exec_node_ms": (C.c_int, [vp, dblp]),
+    "hg_last_exec_layer_count": (C.c_int, [u32p]),
+    "hg_last_exec_layer": (C.c_int, [C.c_uint32, C.POINTER(C.c_char_p), dblp]),
     "hg_prof_enable": (C.c_int, [C.c_int]),
     "hg_prof_report": (C.c_int, [C.c_char_p, C.c_uint64]),
 }

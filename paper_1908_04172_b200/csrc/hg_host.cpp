@@ -529,14 +529,30 @@ static CtBatch do_relin(const Context& ctx, const RelinKeyDev& rk, const CtBatch
   return out;
 }
 
-// Upload a float weight tensor once per model (device copy cached on the weight).
+static std::shared_ptr<CUevent_st> record_ready(cudaStream_t s) {
+  cudaEvent_t ev;
+  cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventRecord(ev, s), "event");
+  return std::shared_ptr<CUevent_st>(ev, [](cudaEvent_t e) { cudaEventDestroy(e); });
+}
+
+// Upload a float weight tensor once per model and device.  The copy is allocated on the
+// context's stream (it outlives the caller's stream) and enqueued on `s`; executes on other
+// streams wait on its ready event.  Caller holds the model mutex.
 static const float* weight_dev(const Context& ctx, WeightTensor& w, cudaStream_t s) {
-  if (!w.dev) {
-    w.dev = ctx.alloc(w.data.size() * sizeof(float), s);
-    cuda_check(cudaMemcpyAsync(w.dev->ptr, w.data.data(), w.data.size() * sizeof(float), cudaMemcpyHostToDevice, s),
-               "upload weights");
+  auto it = w.dev.find(ctx.core.get());
+  if (it != w.dev.end()) {
+    cuda_check(cudaStreamWaitEvent(s, it->second.ready.get(), 0), "event");
+    return static_cast<const float*>(it->second.buf->ptr);
   }
-  return static_cast<const float*>(w.dev->ptr);
+  KeptBuf k;
+  k.buf = ctx.alloc(w.data.size() * sizeof(float), ctx.core->stream);
+  if (s != ctx.core->stream) cuda_check(cudaStreamWaitEvent(s, record_ready(ctx.core->stream).get(), 0), "event");
+  cuda_check(cudaMemcpyAsync(k.buf->ptr, w.data.data(), w.data.size() * sizeof(float), cudaMemcpyHostToDevice, s),
+             "upload weights");
+  k.ready = record_ready(s);
+  w.dev[ctx.core.get()] = k;
+  return static_cast<const float*>(k.buf->ptr);
 }
 
 // encode_scalar validation (henet/encoding.hpp:122-126, 180-188) for |value| <= max_abs.
@@ -878,6 +894,9 @@ struct Value {
   WeightTensor* plain = nullptr;
 };
 
+// (node id, ms) of the most recent hg_execute on this thread that asked for stats.
+thread_local std::vector<std::pair<std::string, double>> g_last_layers;
+
 class Executor {
  public:
   Executor(const std::shared_ptr<Context>& ctx, Model& model, const Plan& plan, const RelinKeyDev* rk,
@@ -899,7 +918,14 @@ class Executor {
     for (const auto& n : model_.nodes)
       for (const auto& in : n.inputs) ++uses[in];
 
-    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> evs;
+    // per-node CUDA events (ExecutionStats::layer_ms, henet/graph.hpp:860-866) when stats are
+    // requested or HG_NODE_TIMING is set
+    const bool timed = timing_ || stats != nullptr;
+    std::vector<std::pair<const Node*, std::pair<cudaEvent_t, cudaEvent_t>>> evs;
+    {
+      std::lock_guard<std::mutex> g(*model_.mu);
+      keep_ = model_.keep_encodings;
+    }
     std::map<std::string, Value> values;
     u32 layer_seq = 0;
     const std::string out_id = [&] {
@@ -909,7 +935,7 @@ class Executor {
     }();
     for (const auto& n : model_.nodes) {
       cudaEvent_t e0 = nullptr, e1 = nullptr;
-      if (timing_) {
+      if (timed) {
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0, s_);
@@ -925,16 +951,20 @@ class Executor {
           v.plain = &model_.weights.at(n.weight_ref);
           break;
         case HG_OP_ADD:
-        case HG_OP_MULTIPLY:
+        case HG_OP_MULTIPLY: {
+          std::lock_guard<std::mutex> g(*model_.mu);  // lazily built weight state
           v = eval_elementwise(n, values);
           break;
+        }
         case HG_OP_SQUARE:
           v = eval_square(n, values);
           break;
         case HG_OP_DOT:
-        case HG_OP_CONVOLUTION:
+        case HG_OP_CONVOLUTION: {
+          std::lock_guard<std::mutex> g(*model_.mu);  // lazily built weight state
           v = eval_linear(n, values);
           break;
+        }
         case HG_OP_RESHAPE:
         case HG_OP_OUTPUT:
           v = values.at(n.inputs[0]);
@@ -950,9 +980,9 @@ class Executor {
       if (v.is_cipher) {
         require(v.cipher.level == plan_.nodes.at(n.id).level_out, "executed level diverged from the plan at node " + n.id);
       }
-      if (timing_) {
+      if (timed) {
         cudaEventRecord(e1, s_);
-        evs.push_back({n.op, {e0, e1}});
+        evs.push_back({&n, {e0, e1}});
       }
       for (const auto& in : n.inputs)
         if (--uses[in] == 0) values.erase(in);
@@ -967,10 +997,12 @@ class Executor {
       cuda_check(cudaStreamSynchronize(s_), "execute");
     }
     if (node_ms) node_ms->fill(0.0);
+    g_last_layers.clear();
     for (auto& e : evs) {
       float ms = 0;
       cudaEventElapsedTime(&ms, e.second.first, e.second.second);
-      if (node_ms) (*node_ms)[e.first] += ms;
+      if (node_ms) (*node_ms)[e.first->op] += ms;
+      g_last_layers.emplace_back(e.first->id, static_cast<double>(ms));
       cudaEventDestroy(e.second.first);
       cudaEventDestroy(e.second.second);
     }
@@ -991,27 +1023,24 @@ class Executor {
   // encodings (hg_model_keep_encodings; precompile_weights, henet/graph.hpp:657-679).
   BufPtr encoding(WeightTensor& w, std::vector<u64> key, size_t bytes, const std::function<void(void*)>& build) {
     key.insert(key.begin(), reinterpret_cast<u64>(ctx_.get()));
-    if (model_.keep_encodings) {
-      auto it = w.enc.find(key);
-      if (it != w.enc.end()) return it->second;
-    }
-    if (!model_.keep_encodings) {
+    if (!keep_) {
       BufPtr b = ctx_->alloc(bytes, s_);
       build(b->ptr);
       return b;
     }
-    // a kept encoding is allocated on the context's stream (it outlives any caller stream)
-    BufPtr b = ctx_->alloc(bytes, ctx_->core->stream);
-    if (s_ != ctx_->core->stream) {
-      cudaEvent_t ev;
-      cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
-      cuda_check(cudaEventRecord(ev, ctx_->core->stream), "event");
-      cuda_check(cudaStreamWaitEvent(s_, ev, 0), "event");
-      cudaEventDestroy(ev);
+    auto it = w.enc.find(key);
+    if (it != w.enc.end()) {
+      cuda_check(cudaStreamWaitEvent(s_, it->second.ready.get(), 0), "event");
+      return it->second.buf;
     }
-    build(b->ptr);
-    w.enc[key] = b;
-    return b;
+    // a kept encoding is allocated on the context's stream (it outlives any caller stream)
+    KeptBuf k;
+    k.buf = ctx_->alloc(bytes, ctx_->core->stream);
+    if (s_ != ctx_->core->stream) cuda_check(cudaStreamWaitEvent(s_, record_ready(ctx_->core->stream).get(), 0), "event");
+    build(k.buf->ptr);
+    k.ready = record_ready(s_);
+    w.enc[key] = k;
+    return k.buf;
   }
   static u64 bits(double d) {
     u64 u;
@@ -1746,6 +1775,7 @@ class Executor {
   void* user_;
   cudaStream_t s_;
   bool timing_;
+  bool keep_ = false;  // model_.keep_encodings, read once per execute under the model mutex
   u64 rescales_ = 0, relins_ = 0;
   u64 launches0_ = launches_total();  // kernel launches are counted process-wide
 };
@@ -1903,6 +1933,63 @@ int hg_tensor_download(const hg_tensor* t, uint64_t* words, void* stream) {
       check_launch(r, "widen");
       cuda_check(cudaMemcpyAsync(words, stage->ptr, n * 8, cudaMemcpyDeviceToHost, s), "d2h");
     }
+    cuda_check(cudaStreamSynchronize(s), "download");
+  });
+}
+
+int hg_tensor_upload_segments(hg_tensor* t, const uint64_t* const* segs, void* stream) {
+  return guard([&] {
+    require(t != nullptr && segs != nullptr, "null argument");
+    const Context& ctx = *t->ctx;
+    cudaStream_t s = ctx.pick(stream);
+    const u64 seg_words = static_cast<u64>(t->b.level) * ctx.n;
+    const u64 nseg = t->b.count * t->b.polys;
+    const u64 n = nseg * seg_words;
+    if (!ctx.wide && host_narrow_enabled()) {
+      // the packer threads read each segment in place (as hg_tensor_deserialize does)
+      require(host_narrow_upload(ctx.core->device, nullptr, t->b.data(), n, t->b.level, ctx.n, ctx.chain.data(), s,
+                                 reinterpret_cast<const uint8_t* const*>(segs), seg_words),
+              "residue out of range");
+      return;
+    }
+    const size_t need = (ctx.wide ? 0 : n * 8) + sizeof(int);
+    if (!t->stage || t->stage->bytes < need) {
+      t->stage = ctx.alloc(need, ctx.core->stream);
+      cuda_check(cudaStreamSynchronize(ctx.core->stream), "upload staging");
+    }
+    BufPtr stage = t->stage;
+    int* bad = reinterpret_cast<int*>(static_cast<char*>(stage->ptr) + (ctx.wide ? 0 : n * 8));
+    cuda_check(cudaMemsetAsync(bad, 0, sizeof(int), s), "memset");
+    u64* dst = ctx.wide ? t->b.data64() : static_cast<u64*>(stage->ptr);
+    for (u64 i = 0; i < nseg; ++i)
+      cuda_check(cudaMemcpyAsync(dst + i * seg_words, segs[i], seg_words * 8, cudaMemcpyHostToDevice, s), "h2d");
+    const int r = ctx.wide ? launch_validate_w(t->b.data64(), n, t->b.level, ctx.n, ctx.basisw, bad, s)
+                           : launch_narrow(dst, t->b.data(), n, t->b.level, ctx.n, ctx.basis, bad, s);
+    check_launch(r, "narrow");
+    int hbad = 0;
+    cuda_check(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaStreamSynchronize(s), "upload");
+    require(hbad == 0, "residue out of range");
+  });
+}
+
+int hg_tensor_download_segments(const hg_tensor* t, uint64_t* const* segs, void* stream) {
+  return guard([&] {
+    require(t != nullptr && segs != nullptr, "null argument");
+    const Context& ctx = *t->ctx;
+    cudaStream_t s = ctx.pick(stream);
+    const u64 seg_words = static_cast<u64>(t->b.level) * ctx.n;
+    const u64 nseg = t->b.count * t->b.polys;
+    const u64 n = nseg * seg_words;
+    BufPtr stage;
+    const u64* src = ctx.wide ? t->b.data64() : nullptr;
+    if (!ctx.wide) {
+      stage = ctx.alloc(n * 8, s);
+      check_launch(launch_widen(t->b.data(), static_cast<u64*>(stage->ptr), n, s), "widen");
+      src = static_cast<const u64*>(stage->ptr);
+    }
+    for (u64 i = 0; i < nseg; ++i)
+      cuda_check(cudaMemcpyAsync(segs[i], src + i * seg_words, seg_words * 8, cudaMemcpyDeviceToHost, s), "d2h");
     cuda_check(cudaStreamSynchronize(s), "download");
   });
 }
@@ -2390,6 +2477,21 @@ int hg_prof_report(char* buf, uint64_t cap) {
   });
 }
 
+int hg_last_exec_layer_count(uint32_t* n) {
+  return guard([&] {
+    require(n != nullptr, "null argument");
+    *n = static_cast<uint32_t>(g_last_layers.size());
+  });
+}
+
+int hg_last_exec_layer(uint32_t i, const char** id, double* ms) {
+  return guard([&] {
+    require(i < g_last_layers.size() && id && ms, "layer index out of range");
+    *id = g_last_layers[i].first.c_str();
+    *ms = g_last_layers[i].second;
+  });
+}
+
 int hg_last_exec_node_ms(hg_ctx* ctx, double* ms_by_op) {
   return guard([&] {
     for (int i = 0; i < 11; ++i) ms_by_op[i] = ctx->last_node_ms[i];
@@ -2775,7 +2877,7 @@ struct WireReader {  // ByteReader, henet/common.hpp:90-122
   const uint8_t* d;
   u64 n, pos = 0;
   const uint8_t* take(u64 k) {
-    if (pos + k > n) throw Error(HG_ERR_VALIDATION, "serialized data truncated");
+    if (k > n - pos) throw Error(HG_ERR_VALIDATION, "serialized data truncated");  // pos <= n always
     const uint8_t* p = d + pos;
     pos += k;
     return p;
@@ -2924,6 +3026,7 @@ int hg_refresh_engine_set_relu_clip(hg_refresh_engine* e, double hi) {
 int hg_model_keep_encodings(hg_model* m, int on) {
   return guard([&] {
     require(m != nullptr, "null argument");
+    std::lock_guard<std::mutex> g(*m->m.mu);
     m->m.keep_encodings = on != 0;
     if (!on)
       for (auto& kv : m->m.weights) kv.second.enc.clear();

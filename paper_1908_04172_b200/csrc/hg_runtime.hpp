@@ -118,15 +118,22 @@ struct RelinKeyDev {
   u32 chain_len = 0;
 };
 
+// A device buffer shared between executes, with the event its producing work recorded:
+// a later execute on another stream waits on `ready` before reading it.
+struct KeptBuf {
+  BufPtr buf;
+  std::shared_ptr<CUevent_st> ready;
+};
+
 struct WeightTensor {
   std::vector<u32> dims;
   std::vector<float> data;
   float max_abs = 0;
-  // device copy (uploaded lazily, per device)
-  BufPtr dev;
+  // f32 device copy, uploaded lazily once per device (keyed by the context's DeviceCore)
+  std::map<const DeviceCore*, KeptBuf> dev;
   // encodings kept across executes when the model caches weights (Model::keep_encodings):
   // (context, layout, level, scale bits, ...) -> device residues / packed planes
-  std::map<std::vector<u64>, BufPtr> enc;
+  std::map<std::vector<u64>, KeptBuf> enc;
   int depthwise = -1;  // conv weights (F, C, k, k) with F == C and zero off-diagonal taps; -1 unknown
 };
 
@@ -154,6 +161,10 @@ struct Model {
   // Weight encodings persist across executes, like the reference's shared WeightEncoder
   // cache filled by precompile_weights (henet/graph.hpp:595-679); off = per-call encoding.
   bool keep_encodings = false;
+  // Guards the lazily built per-weight state above (dev, enc, depthwise) and keep_encodings:
+  // concurrent executes of one model (the reference allows them, henet/graph.hpp:601,616)
+  // share it.
+  std::shared_ptr<std::mutex> mu = std::make_shared<std::mutex>();
   const Node& node(const std::string& id) const { return nodes[index.at(id)]; }
 };
 

@@ -604,6 +604,7 @@ class ExecutionStats:
     nonlin_elements: int = 0
     wall_ms: float = 0.0
     kernel_launches: int = 0
+    layer_ms: List = field(default_factory=list)  # [(node id, ms)] in execution order
 
 
 # provider(kind, window, layer_seq, request: CipherTensor) -> uint64 words (groups, 2, L, N)
@@ -651,6 +652,13 @@ def execute(ctx: CkksContext, model: PlainModel, plan: RescalePlan, inp: CipherT
         stats.nonlin_elements = st.nonlin_elements
         stats.wall_ms = st.wall_ms
         stats.kernel_launches = st.kernel_launches
+        n = C.c_uint32()
+        check(lib.hg_last_exec_layer_count(C.byref(n)))
+        stats.layer_ms = []
+        for i in range(n.value):
+            nid, ms = C.c_char_p(), C.c_double()
+            check(lib.hg_last_exec_layer(i, C.byref(nid), C.byref(ms)))
+            stats.layer_ms.append((nid.value.decode(), ms.value))
     return CipherTensor(ctx, 0, _handle=out)
 
 

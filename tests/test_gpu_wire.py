@@ -70,3 +70,16 @@ def test_wire_rejects_like_reference(env):
             H.CipherTensor.deserialize(ctx, bytes(b))
         with pytest.raises(Exception, match=msg):
             env["ref"].get_tensor(bytes(b))
+
+
+@pytest.mark.parametrize("ct_len", [2 ** 64 - 1, 2 ** 64 - 8, None])
+def test_wire_rejects_oversized_ciphertext_length(env, ct_len):
+    """A ciphertext length field past the end of the message (or near 2^64, where pos + len
+    would wrap) is 'truncated', never a read outside the buffer."""
+    data, _ = _msg(env)
+    hdr = 1 + 4 + 4  # ndims, dims[0], count
+    bad = bytearray(data)
+    remaining = len(data) - hdr - 8
+    struct.pack_into("<Q", bad, hdr, ct_len if ct_len is not None else remaining + 1)
+    with pytest.raises(H.ValidationError, match="truncated"):
+        H.CipherTensor.deserialize(env["ctx"], bytes(bad))

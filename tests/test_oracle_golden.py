@@ -173,3 +173,18 @@ def test_scalar_encoding_lemma():
         res = oc.encode_scalar(r, level, 2.0 ** 30)
         vec = oc.encode_vector(np.full(2048, r, dtype=np.complex128), level, 2.0 ** 30)
         assert np.array_equal(vec, np.repeat(res[:, None], 4096, axis=1))
+
+
+@pytest.mark.parametrize("params,k,m", [("N8192", 40, 7), ("N16384", 24, 5)])
+def test_dense_lazy_matches_mac_chain(params, k, m):
+    """oc_dense_lazy (one 128-bit sum per residue, used for the K = 4096 c5b check) gives the
+    residues of mac_output's per-tap mul + add chain (oc_dense), rescale included."""
+    from paper_1908_04172_b200 import workloads as W
+    p = getattr(W, params)
+    oc = O.OracleContext(p["n"], p["chain"], p["special"], p["scale"])
+    x = W.random_ciphertexts(p, k, seed=3)
+    w = np.random.default_rng(4).normal(0, 0.1, (k, m)).astype(np.float32)
+    w[0, 0] = 0.0
+    L = len(p["chain"])
+    for rescale in (True, False):
+        assert np.array_equal(oc.dense_lazy(x, w, L, rescale), oc.dense(x, w, L, p["scale"], rescale=rescale))
