@@ -92,12 +92,22 @@ static int bench(int steps) {
     if (i >= 3) ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
     if (y.elems.size() != 10) return 1;
   }
+  // the upload alone (hg_tensor_upload_segments from the RingElements), for the breakdown
+  std::vector<double> up;
+  henet::gpu::Device& dev = henet::gpu::device_for(*ctx);
+  for (int i = 0; i < steps; ++i) {
+    henet::gpu::detail::Tensor t;
+    const auto t0 = std::chrono::steady_clock::now();
+    henet::gpu::detail::upload(dev, x.elems, x.shape.dims, t);
+    up.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
   std::sort(ms.begin(), ms.end());
+  std::sort(up.begin(), up.end());
   double sum = 0;
   for (double v : ms) sum += v;
-  std::printf("{\"dropin_ms_median\": %.4f, \"dropin_ms_mean\": %.4f, \"dropin_ms_min\": %.4f, \"steps\": %d, "
-              "\"images\": 4096, \"input_cts\": %zu}\n",
-              ms[ms.size() / 2], sum / ms.size(), ms[0], steps, x.elems.size());
+  std::printf("{\"dropin_ms_median\": %.4f, \"dropin_ms_mean\": %.4f, \"dropin_ms_min\": %.4f, "
+              "\"upload_ms_median\": %.4f, \"steps\": %d, \"images\": 4096, \"input_cts\": %zu}\n",
+              ms[ms.size() / 2], sum / ms.size(), ms[0], up[up.size() / 2], steps, x.elems.size());
   return 0;
 }
 
@@ -110,6 +120,24 @@ int main(int argc, char** argv) {
   ok &= run_model(ctx, keys, make_cryptonets_relu(Preset::P13, PackingMode::Complex, 2), PackingMode::Complex, 8192,
                   "make_cryptonets_relu complex (c3)");
   ok &= run_model(ctx, keys, make_cryptonets_shaped_toy(Preset::P13, 3), PackingMode::Real, 64, "cryptonets toy");
+  // the reference's own parameter presets (henet/params.hpp:74-101) through
+  // CkksContext::create, as `henet run` builds them (proj/tools/henet.cpp:377): 41/51-bit
+  // primes (P13, P14), a 41-bit special prime over ~2^30 primes (P12), and N = 2^11 with a
+  // single 54-bit prime and no special prime (P11, client-aided ReLU network)
+  for (Preset pr : {Preset::P12, Preset::P13, Preset::P14, Preset::P11}) {
+    auto pctx = CkksContext::create(pr);
+    KeyPair pkeys = keygen(*pctx, 2025, pctx->has_special());
+    const std::string nm = std::string("preset ") + preset_name(pr);
+    if (pr == Preset::P11) {
+      ok &= run_model(pctx, pkeys, make_cryptonets_relu(pr, PackingMode::Real, 4), PackingMode::Real, 1024,
+                      (nm + " make_cryptonets_relu").c_str());
+    } else if (pr == Preset::P13) {
+      ok &= run_model(pctx, pkeys, make_cryptonets(pr, 1), PackingMode::Real, 4096, (nm + " make_cryptonets").c_str());
+    } else {
+      ok &= run_model(pctx, pkeys, make_cryptonets_shaped_toy(pr, 3), PackingMode::Real, 64,
+                      (nm + " cryptonets toy").c_str());
+    }
+  }
   // client side: encrypt_tensor / decrypt_tensor, and execute with the GPU LocalProvider
   {
     PlainModel model = load_model(make_cryptonets_relu(Preset::P13, PackingMode::Complex, 2).manifest,

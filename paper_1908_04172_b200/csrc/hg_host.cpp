@@ -80,8 +80,8 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
   require(chain_len >= 1, "modulus chain must be non-empty");
   u32 logn = 0;
   while ((1u << logn) < n) ++logn;
-  if (logn < 12 || logn > 14)
-    throw Error(HG_ERR_UNSUPPORTED, "B200 kernels implement ring degrees 2^12..2^14 (got " + std::to_string(n) + ")");
+  if (logn < 11 || logn > 14 || (1u << logn) != n)
+    throw Error(HG_ERR_UNSUPPORTED, "B200 kernels implement ring degrees 2^11..2^14 (got " + std::to_string(n) + ")");
   const u32 full = chain_len + (special ? 1 : 0);
   if (full > static_cast<u32>(kMaxPrimes)) throw Error(HG_ERR_UNSUPPORTED, "too many basis moduli");
 
@@ -96,8 +96,9 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
     const u64 q = ctx->basis_mod(i);
     require(q >= 2, "modulus must be at least 2");
     require(nt::is_prime(q), "modulus must be prime");
-    if (q >= (1ull << 50))
-      throw Error(HG_ERR_UNSUPPORTED, "B200 kernels implement primes below 2^50 (got " + std::to_string(q) + ")");
+    // u64 residues with lazy values in [0, 4q) (hg_wide.cuh): any prime below 2^62
+    if (q >= (1ull << 62))
+      throw Error(HG_ERR_UNSUPPORTED, "B200 kernels implement primes below 2^62 (got " + std::to_string(q) + ")");
     if (q >= (1ull << 30)) ctx->wide = true;
     for (u32 j = 0; j < i; ++j) {
       if (ctx->basis_mod(j) == q) {
@@ -107,6 +108,9 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
     }
     if ((q - 1) % (2ull * n) != 0) throw Error(HG_ERR_VALIDATION, "modulus admits no 2N-th root of unity (q != 1 mod 2N)");
   }
+  // N = 2^11 (preset P11) runs on the u64 kernels whatever its primes: the u32 kernels keep
+  // per-thread rows in tensor memory, which needs CTAs of >= 128 threads (N >= 2^12).
+  if (logn < 12) ctx->wide = true;
   long double acc = 1.0L;
   ctx->modulus_products.push_back(acc);
   for (u64 q : ctx->chain) {
@@ -398,8 +402,6 @@ static CtBatch do_rescale(const Context& ctx, const CtBatch& in, u32 target, cud
     const u64 p = ctx.chain[L - 1];
     int r;
     if (ctx.wide) {
-      if (p >= (1ull << 32))
-        throw Error(HG_ERR_UNSUPPORTED, "rescale by a prime >= 2^32 is not implemented on the B200 path");
       // Limbs with primes < 2^30 (all but the 40-bit limb 0 of the BASELINE wide chain) are
       // rescaled by the u32 kernel on a copy of their residues; the wide kernel then only
       // handles limb 0 (it repeats the dropped limb's inverse transform for its correction).
@@ -416,6 +418,11 @@ static CtBatch do_rescale(const Context& ctx, const CtBatch& in, u32 target, cud
       a.rows = cur.count * cur.polys;
       a.level = L;
       a.limb_cnt = hybrid ? 1 : 0;
+      BufPtr corr64;
+      if (p >= (1ull << 32)) {  // centred corrections beyond i32: a global row per polynomial
+        corr64 = ctx.alloc(a.rows * ctx.n * sizeof(i64), s);
+        a.corr64 = static_cast<i64*>(corr64->ptr);
+      }
       for (u32 i = 0; i + 1 < L; ++i) {
         const u64 q = ctx.chain[i];
         a.pinv[i] = nt::inv(p % q, q);
@@ -469,13 +476,67 @@ static CtBatch do_rescale(const Context& ctx, const CtBatch& in, u32 target, cud
   return cur;
 }
 
+// relinearize for u64 contexts (any primes < 2^62; presets P11-P14): the size-3 input is
+// formed by the element-wise tensor kernel (square: a == b), then the three kernels of
+// launch_relin_w, then an optional separate rescale.
+static CtBatch do_relin_wide(const Context& ctx, const RelinKeyDev& rk, const CtBatch* a, const CtBatch* b, int mode,
+                             bool rescale, cudaStream_t s) {
+  const u32 L = a->level;
+  const u32 n = ctx.n;
+  if (rescale) require(L >= 2, "cannot rescale below level 1");
+  CtBatch c3;
+  const CtBatch* in3 = a;
+  if (mode != 0) {
+    c3.packing = a->packing;
+    c3.shape = a->shape;
+    c3.scale = a->scale * (b ? b->scale : a->scale);
+    ensure(ctx, c3, a->count, 3, L, s);
+    EwArgs e{};
+    e.op = EwOp::Tensor;
+    e.a = a->data();
+    e.b = b ? b->data() : a->data();
+    e.out = c3.data();
+    e.count = a->count;
+    e.polys_a = 2;
+    e.polys_out = 3;
+    e.level = L;
+    run_ew(ctx, e, s);
+    in3 = &c3;
+  }
+  CtBatch out;
+  out.packing = a->packing;
+  out.shape = a->shape;
+  out.scale = in3->scale;
+  ensure(ctx, out, a->count, 2, L, s);
+  BufPtr D = ctx.alloc(a->count * L * static_cast<u64>(n) * 8, s);
+  BufPtr ACC = ctx.alloc(a->count * 2 * (L + 1) * static_cast<u64>(n) * 8, s);
+  BufPtr CORR = ctx.alloc(a->count * 2 * static_cast<u64>(n) * 8, s);
+  RelinArgsW r{};
+  r.A = in3->data64();
+  r.out = out.data64();
+  r.D = static_cast<u64*>(D->ptr);
+  r.ACC = static_cast<u64*>(ACC->ptr);
+  r.CORR = static_cast<i64*>(CORR->ptr);
+  r.key = static_cast<const u64*>(rk.key->ptr);
+  r.count = a->count;
+  r.level = L;
+  r.chain_len = static_cast<u32>(ctx.chain_len());
+  for (u32 i = 0; i < L; ++i) {
+    const u64 q = ctx.chain[i];
+    r.pinvP[i] = nt::inv(ctx.special % q, q);
+    r.pinvP_sh[i] = static_cast<u64>((static_cast<nt::u128>(r.pinvP[i]) << 64) / q);
+  }
+  check_launch(launch_relin_w(static_cast<int>(ctx.logn), r, ctx.basisw, s), "relinearize (wide)");
+  if (!rescale) return out;
+  return do_rescale(ctx, out, L - 1, s);
+}
+
 // relinearize(square / tensor / size-3) with optional fused rescale.
 static CtBatch do_relin(const Context& ctx, const RelinKeyDev& rk, const CtBatch* a, const CtBatch* b, int mode,
                         bool rescale, cudaStream_t s) {
   require(ctx.has_special, "relinearization needs a special prime");
   require(rk.chain_len == ctx.chain_len(), "relinearization key has the wrong basis");
-  if (ctx.wide)
-    throw Error(HG_ERR_UNSUPPORTED, "relinearization with primes >= 2^30 is not implemented on the B200 path yet");
+  if (ctx.wide) return do_relin_wide(ctx, rk, a, b, mode, rescale, s);
   const u32 L = a->level;
   const u32 n = ctx.n;
   if (rescale) require(L >= 2, "cannot rescale below level 1");
@@ -1120,6 +1181,10 @@ class Executor {
         a.x_level = x.level;
         a.limb_lo = 0;
         a.limb_cnt = tc_lo;
+        for (u32 i = 0; i < L; ++i) {  // 128-bit sums of K products (< (q-1)^2 each)
+          const long double qm1 = static_cast<long double>(ctx.chain[i] - 1);
+          a.fold[i] = (qm1 * qm1 * K + ctx.chain[i] >= 0x1p128L) ? 1 : 0;
+        }
         // the 40-bit limb itself on the tensor cores (5 byte planes, k_mac_dense_tc_w) when
         // the rest of the layer is there too and K keeps its diagonal sums < 2^31
         static const bool wide_tc = [] {
@@ -1262,6 +1327,10 @@ class Executor {
           a.polys = 2;
           a.x_level = x.level;
           a.N = N;
+          for (u32 i = 0; i < L; ++i) {
+            const long double qm1 = static_cast<long double>(ctx.chain[i] - 1);
+            a.fold[i] = (qm1 * qm1 * (static_cast<long double>(Cc) * T2) + ctx.chain[i] >= 0x1p128L) ? 1 : 0;
+          }
           r = launch_mac_conv_w(a, ctx.basisw, s_);
         } else {
           MacConvArgs a{};
@@ -2021,9 +2090,26 @@ int hg_relin_key_upload(hg_ctx* ctx, const uint64_t* words, uint64_t n_words, hg
   return guard([&] {
     const Context& c = *ctx->c;
     require(c.has_special, "relinearization keys need a special prime (not present in these parameters)");
-    if (c.wide) throw Error(HG_ERR_UNSUPPORTED, "relinearization keys with primes >= 2^30 are not implemented yet");
     const u64 L = c.chain_len(), n = c.n;
     require(n_words == L * 2 * (L + 1) * n, "malformed relinearization key");
+    if (c.wide) {
+      // u64 contexts: the serialized words as they are ([j][c][t][N]), range-checked
+      for (u64 j = 0; j < L; ++j)
+        for (u64 p = 0; p < 2; ++p)
+          for (u64 t = 0; t <= L; ++t) {
+            const u64 q = c.basis_mod(t);
+            const u64 base = ((j * 2 + p) * (L + 1) + t) * n;
+            for (u64 i = 0; i < n; ++i) require(words[base + i] < q, "residue out of range");
+          }
+      auto* rk = new hg_relin_key;
+      rk->ctx = ctx->c;
+      rk->k.chain_len = static_cast<u32>(L);
+      rk->k.key = c.alloc(n_words * 8, nullptr);
+      cuda_check(cudaMemcpyAsync(rk->k.key->ptr, words, n_words * 8, cudaMemcpyHostToDevice, c.core->stream), "h2d");
+      cuda_check(cudaStreamSynchronize(c.core->stream), "relin key upload");
+      *out = rk;
+      return;
+    }
     // device layout (hg::kKeyShoup): (value, shoup) pairs, or values only
     const size_t esz = kKeyShoup ? sizeof(uint2) : sizeof(u32);
     std::vector<unsigned char> k(n_words * esz);

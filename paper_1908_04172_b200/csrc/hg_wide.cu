@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_rescale_w(RescaleArgsW a
   constexpr int N = NT::N;
   constexpr int T = NT::T;
   extern __shared__ u64 smw[];
-  i32* cs = reinterpret_cast<i32*>(smw + NT::SMEM_WORDS);  // |correction| < p_last/2 < 2^31 (checked by the host)
+  i32* cs = reinterpret_cast<i32*>(smw + NT::SMEM_WORDS);  // |correction| < p_last/2 < 2^31 (p < 2^32)
+  i64* cg = a.corr64 ? a.corr64 + blockIdx.x * static_cast<u64>(N) : nullptr;  // p >= 2^32: global row
   const u32 tid = threadIdx.x;
   const u64 row = blockIdx.x;
   const u32 L = a.level;
@@ -52,13 +53,17 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_rescale_w(RescaleArgsW a
     NT::gload_C(x, src + static_cast<u64>(L - 1) * N, tid);
     NT::inverse(x, smw, tid, Pl);
 #pragma unroll
-    for (int k = 0; k < 32; ++k) cs[k * T + tid] = static_cast<i32>(centered_round_rem_w(x[k], Pl));
+    for (int k = 0; k < 32; ++k) {
+      const i64 c = centered_round_rem_w(x[k], Pl);
+      if (cg) cg[k * T + tid] = c;
+      else cs[k * T + tid] = static_cast<i32>(c);
+    }
   }
   const u32 kept = a.limb_cnt ? a.limb_cnt : L - 1;
   for (u32 i = 0; i < kept; ++i) {
     const DevPrimeW& Pi = B.p[i];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) x[k] = signed_residue_w(cs[k * T + tid], Pi);
+    for (int k = 0; k < 32; ++k) x[k] = signed_residue_w(cg ? cg[k * T + tid] : cs[k * T + tid], Pi);
     NT::forward(x, smw, tid, Pi);
     const u64 q = Pi.q, pv = a.pinv[i], ps = a.pinv_sh[i];
     const u64* in_i = src + static_cast<u64>(i) * N;
@@ -128,6 +133,13 @@ __global__ void __launch_bounds__(kWWarps * 32) k_mac_dense_w(MacDenseArgsW a, B
           mac128(acc[i][2], x23.x, w);
           mac128(acc[i][3], x23.y, w);
         }
+      }
+      if (a.fold[limb]) {
+        // primes near 2^62: r + 16 (q-1)^2 < 2^128 only after a reduction per k-tile
+#pragma unroll
+        for (int i = 0; i < kWTM; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = {barrett128(acc[i][j].lo, acc[i][j].hi, P), 0};
       }
     } else {
       // narrow limb stored wide: 32x32 products into the low word, folded every 8 taps
@@ -242,6 +254,8 @@ __global__ void __launch_bounds__(128) k_mac_conv_w(MacConvArgsW a, BasisW B) {
   Acc128 acc[kWFT][2];
 #pragma unroll
   for (int f = 0; f < kWFT; ++f) acc[f][0] = acc[f][1] = {0, 0};
+  const bool fold = a.fold[limb] != 0;
+  u32 cnt = 0;
   for_each_tap(a, oy, ox, [&](u32 tin, u32 tw) {
     const ulonglong2 xv = __ldg(reinterpret_cast<const ulonglong2*>(Xb + static_cast<u64>(tin) * xstride));
 #pragma unroll
@@ -250,6 +264,12 @@ __global__ void __launch_bounds__(128) k_mac_conv_w(MacConvArgsW a, BasisW B) {
       const u64 w = __ldg(&Wl[static_cast<u64>(f0 + f) * taps_all + tw]);
       mac128(acc[f][0], xv.x, w);
       mac128(acc[f][1], xv.y, w);
+    }
+    if (fold && (++cnt & 7) == 0) {  // primes near 2^62: keep r + 8 (q-1)^2 < 2^128
+#pragma unroll
+      for (int f = 0; f < kWFT; ++f)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[f][j] = {barrett128(acc[f][j].lo, acc[f][j].hi, P), 0};
     }
   });
 #pragma unroll
@@ -366,10 +386,111 @@ __global__ void k_encode_scalars_w(const T* vals, u64 count, u32 row_len, u32 ro
 }
 
 // ---------------------------------------------------------------------------
+// Relinearization (henet/ckks.hpp:442-499) for u64 residues, any primes < 2^62.
+// ---------------------------------------------------------------------------
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_relin_digits_w(RelinArgsW a, BasisW B) {
+  using NT = NttW<LOGN>;
+  extern __shared__ u64 smw[];
+  const u32 tid = threadIdx.x;
+  const u64 ct = blockIdx.x / a.level;
+  const u32 j = blockIdx.x % a.level;
+  u64 x[32];
+  NT::gload_C(x, a.A + ((ct * 3 + 2) * a.level + j) * NT::N, tid);
+  NT::inverse(x, smw, tid, B.p[j]);  // c2 limb j to the coefficient domain (:450-451)
+  NT::gstore_A(x, a.D + (ct * a.level + j) * NT::N, tid);
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_relin_keysw_w(RelinArgsW a, BasisW B) {
+  using NT = NttW<LOGN>;
+  constexpr int N = NT::N;
+  extern __shared__ u64 smw[];
+  const u32 tid = threadIdx.x;
+  const u32 L = a.level;
+  const u64 ct = blockIdx.x / (L + 1);
+  const u32 t = blockIdx.x % (L + 1);
+  const bool special = t == L;
+  const u32 bidx = special ? a.chain_len : t;  // the key's special limb sits at chain_len (:448)
+  const DevPrimeW& P = B.p[bidx];
+  const u64 q = P.q;
+  u64* acc0 = a.ACC + ((ct * 2 + 0) * (L + 1) + t) * N;
+  u64* acc1 = a.ACC + ((ct * 2 + 1) * (L + 1) + t) * N;
+  for (u32 j = 0; j < L; ++j) {
+    u64 y[32];
+    NT::gload_A(y, a.D + (ct * L + j) * N, tid);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) y[k] = y[k] < q ? y[k] : barrett128(y[k], 0, P);  // :463
+    NT::forward(y, smw, tid, P);
+    const u64* k0 = a.key + ((static_cast<u64>(j) * 2 + 0) * (a.chain_len + 1) + bidx) * N;
+    const u64* k1 = a.key + ((static_cast<u64>(j) * 2 + 1) * (a.chain_len + 1) + bidx) * N;
+#pragma unroll
+    for (int k = 0; k < 32; k += 2) {
+      const u32 jj = NT::NT::jC(tid, k);  // this thread's own positions: no barrier needed
+      const ulonglong2 w0 = __ldg(reinterpret_cast<const ulonglong2*>(k0 + jj));
+      const ulonglong2 w1 = __ldg(reinterpret_cast<const ulonglong2*>(k1 + jj));
+      ulonglong2 p0 = make_ulonglong2(mulmod_w(y[k], w0.x, P), mulmod_w(y[k + 1], w0.y, P));
+      ulonglong2 p1 = make_ulonglong2(mulmod_w(y[k], w1.x, P), mulmod_w(y[k + 1], w1.y, P));
+      if (j != 0) {
+        const ulonglong2 s0 = *reinterpret_cast<const ulonglong2*>(acc0 + jj);
+        const ulonglong2 s1 = *reinterpret_cast<const ulonglong2*>(acc1 + jj);
+        p0 = make_ulonglong2(addmod_w(s0.x, p0.x, q), addmod_w(s0.y, p0.y, q));
+        p1 = make_ulonglong2(addmod_w(s1.x, p1.x, q), addmod_w(s1.y, p1.y, q));
+      }
+      *reinterpret_cast<ulonglong2*>(acc0 + jj) = p0;
+      *reinterpret_cast<ulonglong2*>(acc1 + jj) = p1;
+    }
+  }
+  if (!special) return;
+  // divide_round_last by P (:478-495): r = (INTT(acc_P) + floor(P/2)) mod P, centred
+  for (int c = 0; c < 2; ++c) {
+    u64 y[32];
+    NT::gload_C(y, c ? acc1 : acc0, tid);
+    NT::inverse(y, smw, tid, P);
+    i64* cr = a.CORR + (ct * 2 + c) * N;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) cr[NT::NT::jA(tid, k)] = centered_round_rem_w(y[k], P);
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_relin_moddown_w(RelinArgsW a, BasisW B) {
+  using NT = NttW<LOGN>;
+  constexpr int N = NT::N;
+  extern __shared__ u64 smw[];
+  const u32 tid = threadIdx.x;
+  const u32 L = a.level;
+  const u64 ct = blockIdx.x / (2 * L);
+  const u32 poly = (blockIdx.x / L) % 2;
+  const u32 i = blockIdx.x % L;
+  const DevPrimeW& Pi = B.p[i];
+  const u64 q = Pi.q, pv = a.pinvP[i], ps = a.pinvP_sh[i];
+  const i64* cr = a.CORR + (ct * 2 + poly) * N;
+  u64 z[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) z[k] = signed_residue_w(cr[NT::NT::jA(tid, k)], Pi);
+  NT::forward(z, smw, tid, Pi);  // NTT_i(c mod q_i)
+  const u64* accp = a.ACC + ((ct * 2 + poly) * (L + 1) + i) * N;
+  const u64* dp = a.A + ((ct * 3 + poly) * L + i) * N;
+  u64* op = a.out + ((ct * 2 + poly) * L + i) * N;
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    const u32 jj = NT::NT::jC(tid, k);
+    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(accp + jj));
+    const ulonglong2 d = __ldg(reinterpret_cast<const ulonglong2*>(dp + jj));
+    // (x_i - c) * P^-1 mod q_i, then + c_poly (add_inplace)
+    *reinterpret_cast<ulonglong2*>(op + jj) =
+        make_ulonglong2(addmod_w(d.x, mul_shoup64(v.x + q - z[k], pv, ps, q), q),
+                        addmod_w(d.y, mul_shoup64(v.y + q - z[k + 1], pv, ps, q), q));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------
 #define HG_LOGN_SWITCH_W(logn, ...)                  \
   switch (logn) {                                    \
+    case 11: { constexpr int LN = 11; __VA_ARGS__; } break; \
     case 12: { constexpr int LN = 12; __VA_ARGS__; } break; \
     case 13: { constexpr int LN = 13; __VA_ARGS__; } break; \
     case 14: { constexpr int LN = 14; __VA_ARGS__; } break; \
@@ -407,6 +528,27 @@ int launch_rescale_w(int logn, const RescaleArgsW& a, const BasisW& B, cudaStrea
     set_smem_w(k_rescale_w<LN>, sm);
     { ProfScope ps_("k_rescale_w", s);
     k_rescale_w<LN><<<a.rows, 1 << (LN - 5), sm, s>>>(a, B);
+    }
+  });
+  return 1;
+}
+
+int launch_relin_w(int logn, const RelinArgsW& a, const BasisW& B, cudaStream_t s) {
+  if (a.count == 0) return 0;
+  HG_LOGN_SWITCH_W(logn, {
+    const size_t sm = sizeof(u64) * NttW<LN>::SMEM_WORDS;
+    const u32 T = 1u << (LN - 5);
+    set_smem_w(k_relin_digits_w<LN>, sm);
+    set_smem_w(k_relin_keysw_w<LN>, sm);
+    set_smem_w(k_relin_moddown_w<LN>, sm);
+    { ProfScope ps_("k_relin_digits_w", s);
+    k_relin_digits_w<LN><<<a.count * a.level, T, sm, s>>>(a, B);
+    }
+    { ProfScope ps_("k_relin_keysw_w", s);
+    k_relin_keysw_w<LN><<<a.count * (a.level + 1), T, sm, s>>>(a, B);
+    }
+    { ProfScope ps_("k_relin_moddown_w", s);
+    k_relin_moddown_w<LN><<<a.count * 2 * a.level, T, sm, s>>>(a, B);
     }
   });
   return 1;

@@ -19,6 +19,28 @@ struct RescaleArgsW {
   u32 level;
   u32 limb_cnt;  // kept limbs computed: [0, limb_cnt); 0 = all (level - 1)
   u64 pinv[kMaxPrimes], pinv_sh[kMaxPrimes];
+  // dropped prime >= 2^32: its centred corrections (|c| <= p/2) do not fit the i32 row in
+  // shared memory; they go through this global scratch instead ([rows][N] i64)
+  i64* corr64;
+};
+
+// Relinearization with u64 residues (henet/ckks.hpp:442-499) for any basis of primes
+// < 2^62: the reference's algorithm in the NTT domain, three kernels
+//   k_relin_digits_w  (ct, j):      digit j = INTT_j(c2_j)                 -> D
+//   k_relin_keysw_w   (ct, t<=L):   acc_t = sum_j NTT_t(digit_j mod q_t) * key[j][.][t]
+//                                   (t == L: the special prime P, whose accumulators are
+//                                   INTT'd into the centred corrections c)  -> ACC, CORR
+//   k_relin_moddown_w (ct, poly, i): out_i = c_poly,i + (acc_i - NTT_i(c mod q_i)) * P^-1
+struct RelinArgsW {
+  const u64* A;     // size-3 ciphertexts [count][3][level][N]
+  u64* out;         // [count][2][level][N]
+  u64* D;           // [count][level][N], coefficient domain
+  u64* ACC;         // [count][2][level + 1][N]
+  i64* CORR;        // [count][2][N]
+  const u64* key;   // [chain][2][chain + 1][N]
+  u64 count;
+  u32 level, chain_len;
+  u64 pinvP[kMaxPrimes], pinvP_sh[kMaxPrimes];  // P^-1 mod q_i and its 64-bit Shoup companion
 };
 
 struct MacDenseArgsW {
@@ -28,6 +50,7 @@ struct MacDenseArgsW {
   const u64* bias;  // [level][Mpad] or nullptr
   u32 K, M, Mpad, N, level, polys, x_level;
   u32 limb_lo, limb_cnt;  // limbs computed: [limb_lo, limb_lo + limb_cnt); limb_cnt 0 = all
+  uint8_t fold[kMaxPrimes];  // 1: K (q-1)^2 may overflow 128 bits -> reduce every 16 taps
 };
 
 struct MacConvArgsW {
@@ -37,6 +60,7 @@ struct MacConvArgsW {
   const u64* bias;  // [level][F]
   u32 C, IH, IW, F, OH, OW, win, stride, pad_top, pad_left;
   u32 level, polys, x_level, N;
+  uint8_t fold[kMaxPrimes];  // 1: taps (q-1)^2 may overflow 128 bits -> reduce every 8 taps
 };
 
 struct EwArgsW {
@@ -55,6 +79,7 @@ struct EwArgsW {
 
 int launch_ntt_w(int logn, u64* data, u64 rows, u32 level, bool inverse, const BasisW& B, cudaStream_t s);
 int launch_rescale_w(int logn, const RescaleArgsW& a, const BasisW& B, cudaStream_t s);
+int launch_relin_w(int logn, const RelinArgsW& a, const BasisW& B, cudaStream_t s);
 u32 mac_dense_w_bm();  // Mpad must be a multiple of this
 int launch_mac_dense_w(const MacDenseArgsW& a, const BasisW& B, cudaStream_t s);
 // Limb range copies between u64 tensors [E][P][Lw][N] and u32 tensors [E][P][cnt][N]

@@ -33,6 +33,19 @@ N16384 = dict(
 )
 
 
+# The reference's own parameter presets, make_parameters (henet/params.hpp:74-101): P11 has
+# no special prime (0 here); P12-P14 use primes above 2^30 (u64 residues on the GPU path).
+PRESETS = {
+    "P11": dict(n=2048, chain=[18014398509404161], special=0, scale=float(2 ** 24)),
+    "P12": dict(n=4096, chain=[1073750017, 1073815553, 1073872897], special=1099511799809, scale=float(2 ** 30)),
+    "P13": dict(n=8192, chain=[1125899906990081, 1099511922689, 1099512004609, 1099512266753, 1099512299521,
+                              1099512365057], special=1125899907219457, scale=float(2 ** 40)),
+    "P14": dict(n=16384, chain=[1125899908022273, 1099511922689, 1099512938497, 1099514314753, 1099514478593,
+                               1099515691009, 1099515789313, 1099515985921], special=1125899908612097,
+                scale=float(2 ** 40)),
+}
+
+
 class Blob:
     """Mirror of the reference's BlobBuilder layout (henet/models.hpp:22-61): one
     little-endian f32 blob, entries at 4-byte offsets."""
@@ -196,6 +209,37 @@ def toy_cryptonets(seed: int = 4, batch: int = 64) -> Workload:
         ],
     }
     return Workload("toy_cryptonets", json.dumps(j), blob.bytes(), [1, 8, 8], 0, batch)
+
+
+def toy_cryptonets_relu(seed: int = 5, batch: int = 64, packing: int = 0) -> Workload:
+    """The CryptoNets-ReLU topology (henet/models.hpp:110-136) scaled down like
+    make_cryptonets_shaped_toy: conv 3x3/2 (2 filters, bias) -> Relu -> dense 18->4 (bias) ->
+    Relu -> dense 4->2 (bias); client-aided refreshes, no rescales."""
+    rng = np.random.default_rng(seed)
+    blob = Blob()
+    blob.add("conv_w", [2, 1, 3, 3], _gauss(rng, (2, 1, 3, 3), 0.3))
+    blob.add("conv_b", [2], _gauss(rng, (2,), 0.05))
+    blob.add("fc1_w", [18, 4], _gauss(rng, (18, 4), 0.25))
+    blob.add("fc1_b", [4], _gauss(rng, (4,), 0.05))
+    blob.add("fc2_w", [4, 2], _gauss(rng, (4, 2), 0.5))
+    blob.add("fc2_b", [2], _gauss(rng, (2,), 0.05))
+    j = {
+        "name": "cryptonets-relu-toy",
+        "packing": "complex" if packing else "real",
+        "preset": "P11",
+        "weights": blob.table,
+        "nodes": [
+            _node("input", "Input", attrs={"shape": [1, 8, 8]}),
+            _node("conv", "Convolution", ["input"], {"stride": 2, "window": 3, "filters": 2}, "conv_w", "conv_b"),
+            _node("act1", "Relu", ["conv"]),
+            _node("flatten", "Reshape", ["act1"], {"shape": [18]}),
+            _node("fc1", "Dot", ["flatten"], weight_ref="fc1_w", bias_ref="fc1_b"),
+            _node("act2", "Relu", ["fc1"]),
+            _node("fc2", "Dot", ["act2"], weight_ref="fc2_w", bias_ref="fc2_b"),
+            _node("out", "Output", ["fc2"]),
+        ],
+    }
+    return Workload("toy_cryptonets_relu", json.dumps(j), blob.bytes(), [1, 8, 8], packing, batch)
 
 
 def synthetic_images(shape, batch: int, seed: int) -> np.ndarray:
