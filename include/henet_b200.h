@@ -130,6 +130,10 @@ int hg_tensor_deserialize(hg_ctx* ctx, const uint8_t* bytes, uint64_t len, uint6
                           hg_tensor** out, void* stream);
 uint64_t hg_tensor_serialized_size(const hg_tensor* t);
 int hg_tensor_serialize(const hg_tensor* t, uint8_t* out, uint64_t cap, void* stream);
+/* dst takes src's contents (count, polys, level, scale, packing, shape and residues; the
+ * device buffer is shared, not copied).  Both tensors must belong to one context.  Lets an
+ * hg_nonlin_fn hand back a tensor it obtained elsewhere (e.g. from hg_tensor_deserialize). */
+int hg_tensor_assign(hg_tensor* dst, const hg_tensor* src);
 /* Same word order, one pointer per polynomial (RingElement) instead of one contiguous array:
  * segs[e * polys + k] -> level * N words of polynomial k of element e.  The upload's packer
  * threads read each segment in place, so a caller holding std::vector<Ciphertext> (the

@@ -23,8 +23,12 @@
 // InferenceServer pattern (henet/protocol.hpp:528) -- upload only ciphertexts.
 #pragma once
 
+#include <atomic>
+#include <chrono>
 #include <cstring>
+#include <exception>
 #include <map>
+#include <thread>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -353,6 +357,33 @@ inline std::vector<std::vector<double>> decrypt_tensor(const CkksContext& ctx, c
   return samples;
 }
 
+namespace detail {
+// RescalePlan -> hg_plan (the reference's plan passes through unchanged)
+inline std::unique_ptr<hg_plan, void (*)(hg_plan*)> device_plan(const RescalePlan& plan) {
+  hg_plan* hp = nullptr;
+  check(hg_plan_create(static_cast<int>(plan.mode), plan.planned_rescale_ops, &hp));
+  std::unique_ptr<hg_plan, void (*)(hg_plan*)> guard(hp, hg_plan_destroy);
+  for (const auto& [id, np] : plan.nodes) {
+    check(hg_plan_set_node(hp, id.c_str(), static_cast<int>(np.decision), static_cast<uint32_t>(np.level_in),
+                           static_cast<uint32_t>(np.level_out), np.scale_out));
+  }
+  return guard;
+}
+
+inline std::vector<std::pair<std::string, double>> last_layers() {
+  std::vector<std::pair<std::string, double>> out;
+  uint32_t nl = 0;
+  check(hg_last_exec_layer_count(&nl));
+  for (uint32_t i = 0; i < nl; ++i) {
+    const char* id = nullptr;
+    double ms = 0;
+    check(hg_last_exec_layer(i, &id, &ms));
+    out.emplace_back(id, ms);
+  }
+  return out;
+}
+}  // namespace detail
+
 // execute, henet/graph.hpp:1121-1126 -- the whole graph on the B200.
 inline CipherTensor execute(std::shared_ptr<const CkksContext> ctx, const PlainModel& model, const RescalePlan& plan,
                             const CipherTensor& input, const ExecutionConfig& cfg, ExecutionStats* stats = nullptr) {
@@ -360,13 +391,8 @@ inline CipherTensor execute(std::shared_ptr<const CkksContext> ctx, const PlainM
   // a shared WeightEncoder (ExecutionConfig::encoder, henet/graph.hpp:773) keeps encodings
   // across calls; without one the reference encodes per call -- mirrored on the device
   const hg_model* hm = dev.model(model, cfg.encoder != nullptr);
-  hg_plan* hp = nullptr;
-  check(hg_plan_create(static_cast<int>(plan.mode), plan.planned_rescale_ops, &hp));
-  std::unique_ptr<hg_plan, void (*)(hg_plan*)> plan_guard(hp, hg_plan_destroy);
-  for (const auto& [id, np] : plan.nodes) {
-    check(hg_plan_set_node(hp, id.c_str(), static_cast<int>(np.decision), static_cast<uint32_t>(np.level_in),
-                           static_cast<uint32_t>(np.level_out), np.scale_out));
-  }
+  auto plan_guard = detail::device_plan(plan);
+  hg_plan* hp = plan_guard.get();
   require(input.elems.size() == input.shape.elem_count(), "input shape does not match the model");
   detail::Tensor in;
   detail::upload(dev, input.elems, input.shape.dims, in);
@@ -393,17 +419,201 @@ inline CipherTensor execute(std::shared_ptr<const CkksContext> ctx, const PlainM
     stats->wall_ms = st.wall_ms;
     // layer_ms: one (node id, ms) per node in execution order (henet/graph.hpp:860-866),
     // from CUDA events around each node
-    uint32_t nl = 0;
-    check(hg_last_exec_layer_count(&nl));
-    for (uint32_t i = 0; i < nl; ++i) {
-      const char* id = nullptr;
-      double ms = 0;
-      check(hg_last_exec_layer(i, &id, &ms));
-      stats->layer_ms.emplace_back(id, ms);
-    }
+    stats->layer_ms = detail::last_layers();
   }
   return result;
 }
+
+// InferenceServer (henet/protocol.hpp:449-598) with the evaluator on the B200: the same
+// sessions, frames, checks, error codes and byte accounting, but the ciphertexts never become
+// host Ciphertext objects.  INFER_REQ payloads are validated and packed straight into a device
+// tensor (hg_tensor_deserialize, the checks of deserialize_ciphertext), the graph runs through
+// hg_execute, every NONLIN_REQ is serialized from the device tensor (hg_tensor_serialize) and
+// its NONLIN_RESP deserialized back onto the device, and the RESULT frame is
+// hg_tensor_serialize of the output.  Bytes on the wire are identical to the reference
+// server's (oracle/ref/dropin_test.cpp checks a loopback session against it).
+class InferenceServer {
+ public:
+  struct ModelEntry {
+    std::shared_ptr<const CkksContext> ctx;
+    PlainModel model;
+    RescalePlan plan;
+  };
+
+  void add_model(const std::string& id, PlainModel model, std::shared_ptr<const CkksContext> ctx = nullptr) {
+    if (!ctx) ctx = CkksContext::create(model.preset);
+    auto plan = plan_lazy_rescaling(*ctx, model);
+    models_.emplace(id, ModelEntry{std::move(ctx), std::move(model), std::move(plan)});
+  }
+
+  // kept for interface parity: the GPU does the parallelism
+  void set_threads(unsigned threads) { threads_ = threads; }
+
+  const ModelEntry& entry(const std::string& id) const { return models_.at(id); }
+
+  SessionStats handle_session(Stream& stream) const {
+    SessionStats stats;
+    auto t0 = std::chrono::steady_clock::now();
+    try {
+      Frame hello = read_frame(stream, &stats);
+      if (hello.type != FrameType::Hello) {
+        fail(stream, stats, 4, "expected HELLO");
+        return stats;
+      }
+      SessionConfig config;
+      try {
+        config = henet::detail::decode_hello(hello.payload);
+      } catch (const ValidationError& e) {
+        fail(stream, stats, 3, std::string("bad HELLO: ") + e.what());
+        return stats;
+      }
+      if (config.version != kProtocolVersion) {
+        fail(stream, stats, 1, "protocol version mismatch");
+        return stats;
+      }
+      auto it = models_.find(config.model_id);
+      if (it == models_.end()) {
+        fail(stream, stats, 2, "unknown model: " + config.model_id);
+        return stats;
+      }
+      const ModelEntry& entry = it->second;
+      if (config.preset != entry.model.preset) {
+        fail(stream, stats, 2, "model is registered under a different preset");
+        return stats;
+      }
+      if (config.packing != entry.model.packing) {
+        fail(stream, stats, 2, "model is registered under a different packing");
+        return stats;
+      }
+      if (config.batch == 0 || config.batch > batch_capacity(*entry.ctx, config.packing)) {
+        fail(stream, stats, 3, "batch size outside slot capacity");
+        return stats;
+      }
+      stats.batch = config.batch;
+      write_frame(stream, FrameType::HelloAck, henet::detail::encode_hello(config), &stats);
+
+      Frame infer = read_frame(stream, &stats);
+      if (infer.type != FrameType::InferReq) {
+        fail(stream, stats, 4, infer.type == FrameType::Hello ? "HELLO replayed mid-session" : "expected INFER_REQ");
+        return stats;
+      }
+      Device& dev = device_for(*entry.ctx);
+      detail::Tensor input;
+      {
+        uint64_t consumed = 0;
+        const int rc = hg_tensor_deserialize(dev.ctx(), infer.payload.data(), infer.payload.size(), &consumed,
+                                             &input.t, nullptr);
+        if (rc == HG_ERR_VALIDATION) {
+          fail(stream, stats, 3, std::string("bad INFER_REQ: ") + hg_last_error());
+          return stats;
+        }
+        check(rc);
+      }
+      const hg_model* hm = dev.model(entry.model, false);
+      auto plan = detail::device_plan(entry.plan);
+      Remote remote{&dev, &stream, &stats, nullptr};
+      hg_exec_stats st{};
+      detail::Tensor out;
+      const int rc = hg_execute(dev.ctx(), hm, plan.get(), input.t, nullptr, remote_apply, &remote, &out.t, &st,
+                                nullptr);
+      if (remote.error) std::rethrow_exception(remote.error);
+      check(rc);
+      stats.layer_ms = detail::last_layers();
+      std::vector<u8> result(hg_tensor_serialized_size(out.t));
+      check(hg_tensor_serialize(out.t, result.data(), result.size(), nullptr));
+      write_frame(stream, FrameType::Result, result, &stats);
+    } catch (const TransportError&) {
+      // peer went away
+    } catch (const ValidationError& e) {
+      try {
+        fail(stream, stats, 3, e.what());
+      } catch (...) {
+      }
+    }
+    stats.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return stats;
+  }
+
+  // Accept loop: one thread per connection, sessions independent (henet/protocol.hpp:548-560).
+  void serve(TcpListener& listener, const std::atomic<bool>& stop) const {
+    std::vector<std::thread> sessions;
+    while (!stop.load()) {
+      std::unique_ptr<TcpStream> conn;
+      try {
+        conn = listener.accept();
+      } catch (const TransportError&) {
+        break;
+      }
+      sessions.emplace_back([this, c = std::move(conn)]() mutable { handle_session(*c); });
+    }
+    for (auto& t : sessions) t.join();
+  }
+
+ private:
+  struct Remote {
+    Device* dev;
+    Stream* stream;
+    SessionStats* stats;
+    std::exception_ptr error;
+  };
+
+  // RemoteProvider::apply (henet/protocol.hpp:566-583) over device tensors: NONLIN_REQ =
+  // kind u8 | layer u32 | window u32 | the request's ciphertext list; NONLIN_RESP = the fresh
+  // ciphertext list, deserialized onto the device.
+  static int remote_apply(void* user, int kind, uint32_t window, uint32_t layer_seq, const hg_tensor* request,
+                          hg_tensor* response) {
+    auto* r = static_cast<Remote*>(user);
+    try {
+      std::vector<u8> tensor(hg_tensor_serialized_size(request));
+      check(hg_tensor_serialize(request, tensor.data(), tensor.size(), nullptr));
+      uint32_t dims[16], nd = 16;
+      check(hg_tensor_get_shape(request, dims, &nd));
+      const std::size_t skip = 1 + 4 * static_cast<std::size_t>(nd);  // put_tensor's shape prefix
+      std::vector<u8> payload;
+      payload.reserve(9 + tensor.size() - skip);
+      put_u8(payload, static_cast<u8>(kind));
+      put_u32(payload, layer_seq);
+      put_u32(payload, window);
+      payload.insert(payload.end(), tensor.begin() + static_cast<std::ptrdiff_t>(skip), tensor.end());
+      write_frame(*r->stream, FrameType::NonlinReq, payload, r->stats, /*interactive=*/true);
+      Frame resp = read_frame(*r->stream, r->stats, /*interactive=*/true);
+      if (resp.type != FrameType::NonlinResp)
+        throw TransportError("expected NONLIN_RESP at layer " + std::to_string(layer_seq));
+      require(resp.payload.size() >= 4, "serialized data truncated");
+      const u32 count = static_cast<u32>(resp.payload[0]) | static_cast<u32>(resp.payload[1]) << 8 |
+                        static_cast<u32>(resp.payload[2]) << 16 | static_cast<u32>(resp.payload[3]) << 24;
+      std::vector<u8> msg;  // the list as a put_tensor message of shape [count]
+      msg.reserve(5 + resp.payload.size());
+      put_u8(msg, 1);
+      put_u32(msg, count);
+      msg.insert(msg.end(), resp.payload.begin(), resp.payload.end());
+      detail::Tensor fresh;
+      uint64_t consumed = 0;
+      check(hg_tensor_deserialize(r->dev->ctx(), msg.data(), msg.size(), &consumed, &fresh.t, nullptr));
+      uint64_t req_count = 0;
+      uint32_t polys = 0, level = 0;
+      double scale = 0;
+      int packing = 0;
+      check(hg_tensor_info(request, &req_count, &polys, &level, &scale, &packing));
+      const uint64_t expected = kind == HG_NONLIN_RELU ? req_count : req_count / window;
+      require(count == expected, "provider returned the wrong element count");
+      ++r->stats->nonlin_round_trips;
+      check(hg_tensor_assign(response, fresh.t));
+      return 0;
+    } catch (...) {
+      r->error = std::current_exception();
+      return 1;
+    }
+  }
+
+  void fail(Stream& stream, SessionStats& stats, u16 code, const std::string& message) const {
+    write_frame(stream, FrameType::Error, henet::detail::encode_error(code, message), &stats);
+    stream.close();
+  }
+
+  std::map<std::string, ModelEntry> models_;
+  unsigned threads_ = 1;
+};
 
 // ---- op level ----
 inline Ciphertext relinearize(const CkksContext& ctx, const Ciphertext& ct, const RelinKey& rk) {

@@ -11,6 +11,8 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <future>
+#include <tuple>
 #include <string>
 #include <thread>
 
@@ -111,6 +113,90 @@ static int bench(int steps) {
   return 0;
 }
 
+// One client session (the reference's client_infer) against a server over the in-process
+// pipe (ServerRun, proj/tests/test_protocol.cpp:32-46); returns the client's result, or the
+// rejection message, and the server's accounting.
+template <class Server>
+static std::pair<ClientResult, SessionStats> session(const Server& server, std::shared_ptr<const CkksContext> ctx,
+                                                     const SessionConfig& config, const BatchInput& input,
+                                                     const SecretKey& sk, u64 seed, std::string* error) {
+  auto [a, b] = make_pipe();
+  std::shared_ptr<Stream> server_end(std::move(b));
+  auto fut = std::async(std::launch::async, [&server, server_end] {
+    auto st = server.handle_session(*server_end);
+    server_end->close();
+    return st;
+  });
+  ClientResult r;
+  try {
+    r = client_infer(*a, ctx, config, input, sk, seed);
+  } catch (const std::exception& e) {
+    if (error) *error = e.what();
+  }
+  a->close();
+  return {r, fut.get()};
+}
+
+static bool same_stats(const SessionStats& x, const SessionStats& y) {
+  return x.bytes_sent == y.bytes_sent && x.bytes_received == y.bytes_received &&
+         x.interactive_bytes == y.interactive_bytes && x.nonlin_round_trips == y.nonlin_round_trips &&
+         x.batch == y.batch && x.layer_ms.size() == y.layer_ms.size();
+}
+
+// InferenceServer::handle_session (henet/protocol.hpp:465-545) with the GPU evaluator against
+// the reference server: the loopback case of proj/tests/test_protocol.cpp:207-246 (P11,
+// client-aided ReLU network, bit-exact decrypted outputs, one round trip per ReLU layer),
+// the same at P13 under complex packing, and rejected sessions; wire bytes and accounting
+// must be identical.
+static bool protocol_checks() {
+  bool ok = true;
+  for (auto [pr, packing, batch] : {std::tuple{Preset::P11, PackingMode::Real, 4u},
+                                    std::tuple{Preset::P13, PackingMode::Complex, 64u}}) {
+    auto ctx = CkksContext::create(pr);
+    KeyPair keys = keygen(*ctx, 11, false);
+    auto gm = make_cryptonets_relu(pr, packing, 71);
+    PlainModel model = load_model(gm.manifest, std::span<const u8>(gm.blob.data(), gm.blob.size()));
+    auto input = make_random_input(model.shapes.at("input"), batch, 99);
+    InferenceServer ref_server;
+    ref_server.set_threads(std::thread::hardware_concurrency());
+    ref_server.add_model("cryptonets-relu", model, ctx);
+    henet::gpu::InferenceServer gpu_server;
+    gpu_server.add_model("cryptonets-relu", model, ctx);
+    SessionConfig config;
+    config.preset = pr;
+    config.packing = packing;
+    config.model_id = "cryptonets-relu";
+    config.batch = batch;
+    std::string e1, e2;
+    auto [rc, rs] = session(ref_server, ctx, config, input, keys.secret, 1234, &e1);
+    auto [gc, gs] = session(gpu_server, ctx, config, input, keys.secret, 1234, &e2);
+    const bool good = e1.empty() && e2.empty() && rc.outputs == gc.outputs && !gc.outputs.empty() &&
+                      gc.stats.nonlin_round_trips == 2 && same_stats(rc.stats, gc.stats) && same_stats(rs, gs) &&
+                      gs.interactive_bytes == gc.stats.interactive_bytes;
+    std::printf("%-40s %s (%zu outputs x %zu, %llu bytes sent by the server, %zu layer timings)\n",
+                (std::string("server session ") + preset_name(pr)).c_str(), good ? "bit-identical" : "MISMATCH",
+                gc.outputs.size(), gc.outputs.empty() ? 0 : gc.outputs[0].size(),
+                (unsigned long long)gs.bytes_sent, gs.layer_ms.size());
+    if (!good) std::printf("  ref error '%s' gpu error '%s'\n", e1.c_str(), e2.c_str());
+    ok &= good;
+    // rejected sessions: unknown model, wrong preset, batch outside capacity
+    for (int k = 0; k < 3; ++k) {
+      SessionConfig bad = config;
+      if (k == 0) bad.model_id = "nope";
+      if (k == 1) bad.preset = pr == Preset::P11 ? Preset::P13 : Preset::P11;
+      if (k == 2) bad.batch = batch_capacity(*ctx, packing) + 1;
+      std::string r1, r2;
+      auto in2 = make_random_input(model.shapes.at("input"), bad.batch, 5);
+      auto [x1, y1] = session(ref_server, ctx, bad, in2, keys.secret, 1, &r1);
+      auto [x2, y2] = session(gpu_server, ctx, bad, in2, keys.secret, 1, &r2);
+      const bool same = r1 == r2 && same_stats(y1, y2);
+      std::printf("  rejected session %d: %s (%s)\n", k, same ? "identical" : "MISMATCH", r2.c_str());
+      ok &= same;
+    }
+  }
+  return ok;
+}
+
 int main(int argc, char** argv) {
   if (argc > 2 && std::string(argv[1]) == "--bench") return bench(std::atoi(argv[2]));
   auto ctx = baseline_ctx();
@@ -128,7 +214,7 @@ int main(int argc, char** argv) {
     auto pctx = CkksContext::create(pr);
     KeyPair pkeys = keygen(*pctx, 2025, pctx->has_special());
     const std::string nm = std::string("preset ") + preset_name(pr);
-    if (pr == Preset::P11) {
+    if (pr == Preset::P11 || pr == Preset::P12) {  // depth-1 client-aided networks
       ok &= run_model(pctx, pkeys, make_cryptonets_relu(pr, PackingMode::Real, 4), PackingMode::Real, 1024,
                       (nm + " make_cryptonets_relu").c_str());
     } else if (pr == Preset::P13) {
@@ -195,6 +281,7 @@ int main(int argc, char** argv) {
     std::printf("ValidationError on rescale below level 1: %s\n", threw ? "ok" : "MISSING");
     ok &= threw;
   }
+  ok &= protocol_checks();
   std::printf(ok ? "DROPIN OK\n" : "DROPIN FAILED\n");
   return ok ? 0 : 1;
 }

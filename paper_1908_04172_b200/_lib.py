@@ -72,6 +72,7 @@ PROTOTYPES = {
     "hg_tensor_upload": (C.c_int, [vp, vp, vp]),
     "hg_tensor_download": (C.c_int, [vp, vp, vp]),
     "hg_tensor_upload_segments": (C.c_int, [vp, vp, vp]),
+    "hg_tensor_assign": (C.c_int, [vp, vp]),
     "hg_tensor_download_segments": (C.c_int, [vp, vp, vp]),
     "hg_tensor_upload_u32": (C.c_int, [vp, vp, vp]),
     "hg_tensor_download_u32": (C.c_int, [vp, vp, vp]),

@@ -9,8 +9,8 @@
 
 namespace hg {
 
-constexpr int kCrtWords = 4;  // Q < 2^256 (chains of <= 8 primes below 2^32)
-constexpr int kCrtLimbs = 8;  // the GPU decoder's level limit (Q within kCrtWords words)
+constexpr int kCrtWords = 8;   // Q < 2^512 (P14's 338-bit Q included)
+constexpr int kCrtLimbs = 16;  // the GPU decoder's level limit (Q within kCrtWords words)
 
 // Residue pointers are u32 words, or u64 words in wide contexts (the launchers' `wide`).
 struct EncArgs {
@@ -25,11 +25,11 @@ struct EncArgs {
   u32 e0;           // index of ciphertext 0 in the seed sequence (chunked refreshes)
 };
 
+// Garner recomposition constants (k_dec_crt); passed by value next to the Basis, so only
+// what the kernel reads is here.
 struct CrtTables {
-  u64 q_over_p[kMaxPrimes][kCrtWords + 1];  // Q / q_i
   u64 big_q[kCrtWords + 1];                 // Q = prod q_i
   u64 q_half[kCrtWords + 1];                // floor(Q / 2)
-  u64 inv[kMaxPrimes];                      // (Q / q_i)^-1 mod q_i
   u64 ginv[kCrtLimbs][kCrtLimbs];           // Garner: q_j^-1 mod q_i (j < i)
   u64 q[kCrtLimbs];                         // the level's primes
 };

@@ -2006,6 +2006,14 @@ int hg_tensor_download(const hg_tensor* t, uint64_t* words, void* stream) {
   });
 }
 
+int hg_tensor_assign(hg_tensor* dst, const hg_tensor* src) {
+  return guard([&] {
+    require(dst != nullptr && src != nullptr, "null argument");
+    require(dst->ctx == src->ctx, "tensors belong to different contexts");
+    dst->b = src->b;  // shares the device buffer (reference counted)
+  });
+}
+
 int hg_tensor_upload_segments(hg_tensor* t, const uint64_t* const* segs, void* stream) {
   return guard([&] {
     require(t != nullptr && segs != nullptr, "null argument");
@@ -2603,12 +2611,6 @@ void mw_mul_small(std::vector<u64>& x, u64 m) {
   }
   if (carry) x.push_back(static_cast<u64>(carry));
 }
-u64 mw_mod(const std::vector<u64>& x, u64 q) {
-  unsigned __int128 r = 0;
-  for (size_t i = x.size(); i-- > 0;) r = ((r << 64) | x[i]) % q;
-  return static_cast<u64>(r);
-}
-
 void check_client_ctx(const Context& c) { (void)c; }
 const void* client_basis(const Context& c) {
   return c.wide ? static_cast<const void*>(&c.basisw) : static_cast<const void*>(&c.basis);
@@ -2770,13 +2772,6 @@ void decode_into(const Context& c, const hg_secret_key* sk, const void* ct, u64 
     a.words = static_cast<u32>(big.size());
     for (u32 k = 0; k < a.words; ++k) a.crt.big_q[k] = big[k];
     for (u32 k = 0; k < a.words; ++k) a.crt.q_half[k] = (big[k] >> 1) | (k + 1 < a.words ? (big[k + 1] << 63) : 0);
-    for (u32 i = 0; i < L; ++i) {
-      std::vector<u64> qi{1};
-      for (u32 j = 0; j < L; ++j)
-        if (j != i) mw_mul_small(qi, c.chain[j]);
-      for (u32 k = 0; k < qi.size() && k < static_cast<size_t>(kCrtWords); ++k) a.crt.q_over_p[i][k] = qi[k];
-      a.crt.inv[i] = nt::inv(mw_mod(qi, c.chain[i]), c.chain[i]);
-    }
     {
       // 1.0L / (long double)scale (decode_slots, henet/encoding.hpp:248), x87 on the host
       const long double li = 1.0L / static_cast<long double>(scale);

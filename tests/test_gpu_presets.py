@@ -96,11 +96,12 @@ def test_preset_relinearize_bit_exact(penv):
 
 def test_preset_network_bit_exact(penv):
     """A whole network per preset on real encryptions: the CryptoNets-shaped toy (conv ->
-    square -> dense -> square -> dense, lazy plan) where there is a special prime, the
-    CryptoNets-ReLU topology with client-aided refreshes (the reference's engine) at P11."""
+    square -> dense -> square -> dense, lazy plan, four rescales) where the chain is deep
+    enough (P13, P14), the CryptoNets-ReLU topology with client-aided refreshes (the
+    reference's engine, depth 1) at P11 and P12."""
     ctx, ref, p, keys = penv["ctx"], penv["ref"], penv["p"], penv["keys"]
     slots = p["n"] // 2
-    if p["special"]:
+    if len(p["chain"]) >= 5:
         wl = W.toy_cryptonets(batch=64)
         imgs = W.synthetic_images(wl.input_shape, 64, 3)
         words, sc = ref.encrypt_tensor(keys, imgs, 5)

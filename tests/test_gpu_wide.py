@@ -138,10 +138,18 @@ def test_c4_block_relu6_provider_bit_exact(env):
     assert stats.nonlin_elements == 2 * 6 * 4 * 4  # two ReLU6 layers over (6, 4, 4)
 
 
-def test_wide_relin_is_refused_not_wrong(env):
-    ctx, p = env["ctx"], env["p"]
-    t = H.CipherTensor.from_words(ctx, W.random_ciphertexts(p, 1, seed=11), 1.0)
-    sq = H.square(ctx, t)
-    assert sq.polys == 3
-    with pytest.raises(H.UnsupportedError):
-        H.RelinKey(ctx, np.zeros((8, 2, 9, p["n"]), dtype=np.uint64))
+def test_wide_relinearize_bit_exact(env):
+    """Relinearization with the 40-bit limb 0 and special prime (u64 kernels,
+    henet/ckks.hpp:442-499), and square -> relinearize -> rescale, against the reference."""
+    ctx, ref, p = env["ctx"], env["ref"], env["p"]
+    keys = ref.keygen(5, True)
+    rk = H.RelinKey(ctx, keys.rk_words())
+    for level in (8, 3):
+        x = W.random_ciphertexts(p, 2, seed=11 + level, level=level)
+        sq, sq_sc = ref.square(x, p["scale"])
+        want = ref.relinearize(keys, sq, sq_sc)
+        got = H.relinearize(ctx, H.CipherTensor.from_words(ctx, sq, sq_sc), rk)
+        assert np.array_equal(got.to_words(), want), level
+        want_r, want_sc = ref.rescale(want, sq_sc, level - 1)
+        got_r = H.square_relin(ctx, H.CipherTensor.from_words(ctx, x, p["scale"]), rk, rescale=True)
+        assert got_r.scale == want_sc and np.array_equal(got_r.to_words(), want_r), level
