@@ -329,6 +329,34 @@ int hg_refresh_engine_apply(void* engine, int kind, uint32_t window, uint32_t la
 int hg_refresh_engine_set_relu_clip(hg_refresh_engine* e, double hi);
 
 /* ------------------------------------------------------------------ */
+/* Multi-GPU, one process per GPU.  The reference has no  */
+/* multi-device executor; these are the pieces a C/C++ caller needs to  */
+/* shard a layer's output neurons (BASELINE c5b) without torch: a       */
+/* contiguous block partition, an NCCL communicator bound to a context, */
+/* and a byte-exact all-gather of the ranks' output ciphertexts.  NCCL  */
+/* is loaded at run time (libnccl.so.2); without it these return        */
+/* HG_ERR_UNSUPPORTED.                                                  */
+/* ------------------------------------------------------------------ */
+#define HG_COMM_ID_BYTES 128
+typedef struct hg_comm hg_comm;
+/* Block partition of `total` items over `nranks` (sizes differ by <= 1, lower ranks larger):
+ * rank owns [*begin, *begin + *count). */
+int hg_shard_range(uint64_t total, int rank, int nranks, uint64_t* begin, uint64_t* count);
+/* ncclGetUniqueId: call on one rank and pass the bytes to every rank (any side channel). */
+int hg_comm_unique_id(uint8_t* id /* HG_COMM_ID_BYTES */);
+/* ncclCommInitRank on the context's device (collective over the nranks processes). */
+int hg_comm_create(hg_ctx* ctx, const uint8_t* id, int nranks, int rank, hg_comm** out);
+void hg_comm_destroy(hg_comm* c);
+/* `local` holds this rank's block hg_shard_range(total, rank, nranks) of a tensor of `total`
+ * ciphertexts (same polys / level / scale on every rank); *out (new, shape [total]) receives
+ * every rank's block in place, stream-ordered (no host synchronisation).  Residue words are
+ * copied, never recomputed, so the gathered tensor is bit-identical to an unsharded run. */
+int hg_allgather_tensor(hg_comm* c, const hg_tensor* local, uint64_t total, hg_tensor** out, void* stream);
+/* ncclBroadcast of a tensor's residues from `root` (every rank's tensor has the same
+ * count / polys / level), e.g. the c5b input ciphertexts staged on one rank. */
+int hg_broadcast_tensor(hg_comm* c, hg_tensor* t, int root, void* stream);
+
+/* ------------------------------------------------------------------ */
 /* Measurement helpers (not part of the reference surface)             */
 /* ------------------------------------------------------------------ */
 /* Register-only integer-pipe microbenchmark (the INT32 roofline denominator):

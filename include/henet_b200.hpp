@@ -23,6 +23,7 @@
 // InferenceServer pattern (henet/protocol.hpp:528) -- upload only ciphertexts.
 #pragma once
 
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cstring>
@@ -614,6 +615,84 @@ class InferenceServer {
   std::map<std::string, ModelEntry> models_;
   unsigned threads_ = 1;
 };
+
+// ---- multi-GPU: one process per GPU, NCCL inside the library ----
+using CommId = std::array<uint8_t, HG_COMM_ID_BYTES>;
+inline CommId comm_unique_id() {
+  CommId id{};
+  check(hg_comm_unique_id(id.data()));
+  return id;
+}
+
+class Communicator {
+ public:
+  Communicator(const CkksContext& ctx, const CommId& id, int nranks, int rank)
+      : dev_(&device_for(ctx)), nranks_(nranks), rank_(rank) {
+    check(hg_comm_create(dev_->ctx(), id.data(), nranks, rank, &c_));
+  }
+  ~Communicator() { hg_comm_destroy(c_); }
+  Communicator(const Communicator&) = delete;
+  Communicator& operator=(const Communicator&) = delete;
+  hg_comm* get() const { return c_; }
+  Device& device() const { return *dev_; }
+  int nranks() const { return nranks_; }
+  int rank() const { return rank_; }
+
+ private:
+  Device* dev_;
+  hg_comm* c_ = nullptr;
+  int nranks_, rank_;
+};
+
+// A single-Dot model (Input -> Dot [+bias] -> Output, BASELINE c5b) evaluated with its output
+// neurons split over the ranks: rank r runs the reference's eval_dot on the column block
+// hg_shard_range(M, r, n) of W (same plan decisions, so the same arithmetic per output), and
+// hg_allgather_tensor assembles all M output ciphertexts on every rank.  Bit-identical to
+// henet::execute on the whole layer.  Lazy plans only (naive rescale counts differ per
+// shard in a way the plan does not record).
+inline CipherTensor execute_output_sharded(std::shared_ptr<const CkksContext> ctx, const PlainModel& model,
+                                           const RescalePlan& plan, const CipherTensor& input, Communicator& comm) {
+  require(plan.mode == RescaleMode::Lazy, "output sharding needs a lazy plan");
+  const Node* dot = nullptr;
+  for (const auto& n : model.nodes)
+    if (n.op == OpKind::Dot) {
+      require(dot == nullptr, "output sharding expects a single Dot node");
+      dot = &n;
+    }
+  require(dot != nullptr, "output sharding expects a Dot node");
+  const PlainTensor& w = model.weights.at(dot->weight_ref);
+  const u32 K = w.shape.dims[0], M = w.shape.dims[1];
+  uint64_t b0 = 0, cnt = 0;
+  check(hg_shard_range(M, comm.rank(), comm.nranks(), &b0, &cnt));
+  PlainModel part = model;  // the rank's column block of W (and of the bias)
+  PlainTensor& pw = part.weights.at(dot->weight_ref);
+  pw.shape.dims = {K, static_cast<u32>(cnt)};
+  pw.data.assign(static_cast<std::size_t>(K) * cnt, 0.0f);
+  for (u32 k = 0; k < K; ++k)
+    for (uint64_t j = 0; j < cnt; ++j) pw.data[k * cnt + j] = w.data[static_cast<std::size_t>(k) * M + b0 + j];
+  if (!dot->bias_ref.empty()) {
+    const PlainTensor& b = model.weights.at(dot->bias_ref);
+    PlainTensor& pb = part.weights.at(dot->bias_ref);
+    pb.shape.dims = {static_cast<u32>(cnt)};
+    pb.data.assign(b.data.begin() + static_cast<std::ptrdiff_t>(b0), b.data.begin() + static_cast<std::ptrdiff_t>(b0 + cnt));
+  }
+  RescalePlan pplan = plan;  // one rescale per output of a RescaleAfter Dot
+  if (plan.nodes.at(dot->id).decision == RescaleDecision::RescaleAfter)
+    pplan.planned_rescale_ops = plan.planned_rescale_ops - (M - cnt);
+  Device& dev = comm.device();
+  const hg_model* hm = dev.model(part, false);
+  auto hp = detail::device_plan(pplan);
+  detail::Tensor in;
+  detail::upload(dev, input.elems, input.shape.dims, in);
+  detail::Tensor local, full;
+  hg_exec_stats st{};
+  check(hg_execute(dev.ctx(), hm, hp.get(), in.t, nullptr, nullptr, nullptr, &local.t, &st, nullptr));
+  check(hg_allgather_tensor(comm.get(), local.t, M, &full.t, nullptr));
+  CipherTensor out;
+  out.shape = model.shapes.at(model.output_node().id);
+  out.elems = detail::download(dev, full.t);
+  return out;
+}
 
 // ---- op level ----
 inline Ciphertext relinearize(const CkksContext& ctx, const Ciphertext& ct, const RelinKey& rk) {

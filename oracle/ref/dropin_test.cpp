@@ -282,6 +282,31 @@ int main(int argc, char** argv) {
     ok &= threw;
   }
   ok &= protocol_checks();
+  // output-sharded Dot through the library's NCCL communicator (one GPU here: world size 1)
+  {
+    henet::detail::BlobBuilder blob(7);
+    blob.add_random("w", {96, 40}, 0.1);
+    blob.add_random("b", {40}, 0.01);
+    nlohmann::json j;
+    j["name"] = "dense-96-40";
+    j["packing"] = "real";
+    j["preset"] = "P13";
+    j["weights"] = blob.table();
+    j["nodes"] = nlohmann::json::array(
+        {henet::detail::node_json("input", "Input", {}, {{"shape", {96}}}),
+         henet::detail::node_json("fc", "Dot", {"input"}, nlohmann::json::object(), "w", "b"),
+         henet::detail::node_json("out", "Output", {"fc"})});
+    auto bytes = blob.take_bytes();
+    PlainModel m = load_model(j.dump(), std::span<const u8>(bytes.data(), bytes.size()));
+    RescalePlan plan = plan_lazy_rescaling(*ctx, m);
+    BatchInput in = make_random_input(m.shapes.at("input"), 256, 8);
+    CipherTensor x = encrypt_tensor(*ctx, in, keys.secret, 81, PackingMode::Real, std::thread::hardware_concurrency());
+    ExecutionConfig cfg;
+    cfg.threads = std::thread::hardware_concurrency();
+    CipherTensor want = henet::execute(ctx, m, plan, x, cfg);
+    henet::gpu::Communicator comm(*ctx, henet::gpu::comm_unique_id(), 1, 0);
+    ok &= same(want, henet::gpu::execute_output_sharded(ctx, m, plan, x, comm), "output-sharded Dot (NCCL, 1 rank)");
+  }
   std::printf(ok ? "DROPIN OK\n" : "DROPIN FAILED\n");
   return ok ? 0 : 1;
 }

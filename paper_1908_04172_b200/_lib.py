@@ -73,6 +73,12 @@ PROTOTYPES = {
     "hg_tensor_download": (C.c_int, [vp, vp, vp]),
     "hg_tensor_upload_segments": (C.c_int, [vp, vp, vp]),
     "hg_tensor_assign": (C.c_int, [vp, vp]),
+    "hg_shard_range": (C.c_int, [C.c_uint64, C.c_int, C.c_int, u64p, u64p]),
+    "hg_comm_unique_id": (C.c_int, [vp]),
+    "hg_comm_create": (C.c_int, [vp, vp, C.c_int, C.c_int, C.POINTER(vp)]),
+    "hg_comm_destroy": (None, [vp]),
+    "hg_allgather_tensor": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(vp), vp]),
+    "hg_broadcast_tensor": (C.c_int, [vp, vp, C.c_int, vp]),
     "hg_tensor_download_segments": (C.c_int, [vp, vp, vp]),
     "hg_tensor_upload_u32": (C.c_int, [vp, vp, vp]),
     "hg_tensor_download_u32": (C.c_int, [vp, vp, vp]),

@@ -3139,3 +3139,166 @@ int hg_decode_vector(hg_ctx* ctx, const uint64_t* pt_words, uint64_t count, uint
     cuda_check(cudaStreamSynchronize(s), "decode");
   });
 }
+
+// ---------------------------------------------------------------------------
+// Multi-GPU: NCCL communicator on a context, block sharding and the
+// all-gather of output ciphertexts for output-sharded layers (BASELINE c5b), so C/C++
+// callers shard without torch.  NCCL is resolved at run time (dlopen "libnccl.so.2"): a
+// process whose torch already loaded its NCCL shares that copy, and the library itself
+// never needs NCCL unless a communicator is created.
+// ---------------------------------------------------------------------------
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) return a;
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+    a.broadcast = reinterpret_cast<decltype(a.broadcast)>(dlsym(h, "ncclBroadcast"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    return a;
+  }();
+  if (!api.get_unique_id || !api.comm_init_rank || !api.all_gather || !api.broadcast)
+    throw Error(HG_ERR_UNSUPPORTED, "NCCL (libnccl.so.2) is not available in this process");
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw Error(HG_ERR_CUDA, std::string(what) + ": " + (nccl().error_string ? nccl().error_string(r) : "NCCL error"));
+}
+
+// contiguous block partition, sizes differ by <= 1 (paper_1908_04172_b200/dist.py shard)
+void shard_range(u64 total, int rank, int nranks, u64* begin, u64* count) {
+  const u64 base = total / static_cast<u64>(nranks), rem = total % static_cast<u64>(nranks);
+  const u64 r = static_cast<u64>(rank);
+  *begin = r * base + std::min<u64>(r, rem);
+  *count = base + (r < rem ? 1 : 0);
+}
+}  // namespace
+
+struct hg_comm {
+  std::shared_ptr<hg::Context> ctx;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  ~hg_comm() {
+    if (comm) nccl().comm_destroy(comm);
+  }
+};
+
+extern "C" {
+
+int hg_shard_range(uint64_t total, int rank, int nranks, uint64_t* begin, uint64_t* count) {
+  return guard([&] {
+    require(nranks >= 1 && rank >= 0 && rank < nranks && begin && count, "bad shard arguments");
+    shard_range(total, rank, nranks, begin, count);
+  });
+}
+
+int hg_comm_unique_id(uint8_t* id) {
+  return guard([&] {
+    require(id != nullptr, "null argument");
+    static_assert(sizeof(ncclUniqueId) == HG_COMM_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId u;
+    nccl_check(nccl().get_unique_id(&u), "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+int hg_comm_create(hg_ctx* ctx, const uint8_t* id, int nranks, int rank, hg_comm** out) {
+  return guard([&] {
+    require(ctx && id && out && nranks >= 1 && rank >= 0 && rank < nranks, "bad communicator arguments");
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    auto c = std::make_unique<hg_comm>();
+    c->ctx = ctx->c;
+    c->nranks = nranks;
+    c->rank = rank;
+    cuda_check(cudaSetDevice(ctx->c->core->device), "cudaSetDevice");
+    nccl_check(nccl().comm_init_rank(&c->comm, nranks, u, rank), "ncclCommInitRank");
+    *out = c.release();
+  });
+}
+
+void hg_comm_destroy(hg_comm* c) { delete c; }
+
+int hg_allgather_tensor(hg_comm* c, const hg_tensor* local, uint64_t total, hg_tensor** out, void* stream) {
+  return guard([&] {
+    require(c && local && out, "null argument");
+    require(local->ctx == c->ctx, "tensor and communicator belong to different contexts");
+    const Context& ctx = *c->ctx;
+    cudaStream_t s = ctx.pick(stream);
+    u64 b0 = 0, mine = 0;
+    shard_range(total, c->rank, c->nranks, &b0, &mine);
+    require(local->b.count == mine, "local tensor does not hold this rank's shard");
+    const u64 ct_bytes = static_cast<u64>(local->b.polys) * local->b.level * ctx.n * ctx.word_bytes();
+    u64 width = 0;
+    for (int r = 0; r < c->nranks; ++r) {
+      u64 b = 0, n = 0;
+      shard_range(total, r, c->nranks, &b, &n);
+      width = std::max(width, n);
+    }
+    auto* t = new hg_tensor;
+    std::unique_ptr<hg_tensor> guard_t(t);
+    t->ctx = c->ctx;
+    t->b.packing = local->b.packing;
+    t->b.scale = local->b.scale;
+    t->b.shape = {static_cast<u32>(total)};
+    t->b.count = total;
+    t->b.polys = local->b.polys;
+    t->b.level = local->b.level;
+    t->b.buf = ctx.alloc(std::max<u64>(1, total * ct_bytes), s);
+    if (width * static_cast<u64>(c->nranks) == total) {
+      // equal blocks: gathered straight into place (a byte copy: residues unchanged)
+      nccl_check(nccl().all_gather(local->b.buf->ptr, t->b.buf->ptr, width * ct_bytes, ncclUint8, c->comm, s),
+                 "ncclAllGather");
+    } else {
+      // unequal blocks: padded send / receive buffers, then each rank's rows moved into place
+      BufPtr send = ctx.alloc(width * ct_bytes, s);
+      BufPtr recv = ctx.alloc(width * ct_bytes * c->nranks, s);
+      cuda_check(cudaMemsetAsync(send->ptr, 0, width * ct_bytes, s), "memset");
+      if (mine)
+        cuda_check(cudaMemcpyAsync(send->ptr, local->b.buf->ptr, mine * ct_bytes, cudaMemcpyDeviceToDevice, s), "copy");
+      nccl_check(nccl().all_gather(send->ptr, recv->ptr, width * ct_bytes, ncclUint8, c->comm, s), "ncclAllGather");
+      for (int r = 0; r < c->nranks; ++r) {
+        u64 b = 0, n = 0;
+        shard_range(total, r, c->nranks, &b, &n);
+        if (n)
+          cuda_check(cudaMemcpyAsync(static_cast<char*>(t->b.buf->ptr) + b * ct_bytes,
+                                     static_cast<char*>(recv->ptr) + static_cast<u64>(r) * width * ct_bytes,
+                                     n * ct_bytes, cudaMemcpyDeviceToDevice, s),
+                     "copy");
+      }
+    }
+    *out = guard_t.release();
+  });
+}
+
+int hg_broadcast_tensor(hg_comm* c, hg_tensor* t, int root, void* stream) {
+  return guard([&] {
+    require(c && t && root >= 0 && root < c->nranks, "bad broadcast arguments");
+    require(t->ctx == c->ctx, "tensor and communicator belong to different contexts");
+    const Context& ctx = *c->ctx;
+    const u64 bytes = t->b.words(ctx.n) * ctx.word_bytes();
+    nccl_check(nccl().broadcast(t->b.buf->ptr, t->b.buf->ptr, bytes, ncclUint8, root, c->comm, ctx.pick(stream)),
+               "ncclBroadcast");
+  });
+}
+
+}  // extern "C"

@@ -295,6 +295,46 @@ def decrypt_tensor(ctx: CkksContext, sk: SecretKey, ct: "CipherTensor", batch: i
     return out
 
 
+def shard_range(total: int, rank: int, nranks: int) -> range:
+    """hg_shard_range: rank's contiguous block of `total` items (sizes differ by <= 1)."""
+    b, c = C.c_uint64(), C.c_uint64()
+    check(lib.hg_shard_range(int(total), int(rank), int(nranks), C.byref(b), C.byref(c)))
+    return range(b.value, b.value + c.value)
+
+
+def comm_unique_id() -> bytes:
+    """hg_comm_unique_id (ncclGetUniqueId): create on one rank, send to all."""
+    buf = (C.c_uint8 * 128)()
+    check(lib.hg_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Communicator:
+    """hg_comm: an NCCL communicator bound to a context's device, one process per GPU."""
+
+    def __init__(self, ctx: CkksContext, unique_id: bytes, nranks: int, rank: int):
+        assert len(unique_id) == 128
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        check(lib.hg_comm_create(ctx.handle, buf, int(nranks), int(rank), C.byref(h)))
+        self._h, self.ctx, self.nranks, self.rank = h, ctx, nranks, rank
+
+    def __del__(self):
+        if getattr(self, "_h", None) and lib is not None:
+            lib.hg_comm_destroy(self._h)
+            self._h = None
+
+    def allgather(self, local: CipherTensor, total: int) -> CipherTensor:
+        """hg_allgather_tensor: every rank's block (shard_range(total, r, n)) of the output
+        ciphertexts, gathered in place on the context stream."""
+        h = C.c_void_p()
+        check(lib.hg_allgather_tensor(self._h, local.handle, int(total), C.byref(h), None))
+        return CipherTensor(self.ctx, 0, _handle=h)
+
+    def broadcast(self, t: CipherTensor, root: int = 0) -> None:
+        check(lib.hg_broadcast_tensor(self._h, t.handle, int(root), None))
+
+
 class RefreshEngine:
     """NonlinearityEngine + LocalProvider (henet/graph.hpp:699-752) on the GPU: pass it as
     execute()'s provider; the request never leaves the device."""

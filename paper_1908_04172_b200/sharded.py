@@ -156,6 +156,13 @@ class OutputShardedDense:
         del keep
         return full
 
+    def gather_native(self, y: H.CipherTensor, comm: "H.Communicator") -> H.CipherTensor:
+        """All-gather through the C ABI (hg_allgather_tensor, NCCL inside the library, on the
+        context stream): the same byte copy as gather(), without torch."""
+        assert comm.nranks == self.world and comm.rank == self.rank
+        assert list(H.shard_range(self.M, self.rank, self.world)) == list(self.rows)
+        return comm.allgather(y, self.M)
+
     def gather(self, y: H.CipherTensor, group=None) -> H.CipherTensor:
         """All-gather the output ciphertexts.  Stream-ordered, no host synchronisation:
         the collective runs on torch's current stream after the context stream's work,
