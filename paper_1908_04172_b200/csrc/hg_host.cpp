@@ -3163,8 +3163,12 @@ struct NcclApi {
 const NcclApi& nccl() {
   static const NcclApi api = [] {
     NcclApi a;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (h == nullptr) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    // an NCCL the process already loaded (e.g. torch's bundled copy) wins; otherwise
+    // $HG_NCCL_LIB, then the loader's libnccl.so.2
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (h == nullptr && getenv("HG_NCCL_LIB") != nullptr) h = dlopen(getenv("HG_NCCL_LIB"), RTLD_NOW);
+    if (h == nullptr) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (h == nullptr) h = dlopen("libnccl.so", RTLD_NOW);
     if (h == nullptr) return a;
     a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
     a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));

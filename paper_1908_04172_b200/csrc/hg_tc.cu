@@ -51,6 +51,14 @@ constexpr u32 kTcSmallK = HG_TC_SMALLK;           // K at or below which the N =
 template <int TN>
 constexpr int tc_stages() { return TN == 64 ? 5 : 4; }
 
+// Staged input rows are padded (TN + 4 residues) so the producers' transposed reads of a
+// k-block hit distinct banks (see the producer loop); the wide TN = 64 ring is one stage
+// shallower to stay within 227 KB.
+template <int TN, typename XW>
+constexpr int tc_xs() { return (TN == 64 && sizeof(XW) == 8) ? kTcXS - 1 : kTcXS; }
+template <int TN>
+constexpr int tc_xpitch() { return TN + 4; }
+
 template <int TN, typename XW = u32>
 struct TcSmem {
   static constexpr int kS = tc_stages<TN>();
@@ -58,7 +66,7 @@ struct TcSmem {
   uint8_t b[kS][4][TN * kTcK];  // input planes, written by the producer warps; the planes of a
                                   // stage are consecutive, i.e. one K-major (planes*TN) x 32 matrix
   uint8_t zero_a[kTcPlaneA];      // zero weight plane: initialises the upper accumulators
-  XW xs[kTcXS][kTcK][TN];         // input residues staged by cp.async (producer ring)
+  XW xs[tc_xs<TN, XW>()][kTcK][tc_xpitch<TN>()];  // input residues staged by cp.async (producer ring)
   unsigned long long full_a[kS], full_b[kS], empty[kS];
   u32 tmem;
 };
@@ -207,54 +215,93 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
       }
     }
   } else {
-    // ===== producers: residues -> shared memory by cp.async (kTcXS steps in flight, no
-    // register cost).  Warp w owns k rows [4w, 4w+4) of every step: it copies them, reads
-    // them back (so a __syncwarp, not a CTA barrier, orders the two) and writes their byte
-    // planes, lane l for columns l and l + 32; one elected lane arrives per warp. =====
+    // ===== producers: residues -> shared memory by cp.async (XS steps in flight, no register
+    // cost), then byte planes.  Warp w owns the 16-row k-block kb = w / 4 and the column
+    // block TN/4 * (w % 4) of every step; it copies exactly that block, so a __syncwarp (not
+    // a CTA barrier) orders the copy and the reads.  Each thread transposes the bytes of KQ
+    // consecutive k of one column n (KQ = 8 for TN = 64: one 8-byte run of a K-major core
+    // matrix row per plane; KQ = 4 for TN = 32: 4 bytes) and stores them with one STS per
+    // plane.  Lane -> (n, k) is chosen so that the stores of a phase cover all 32 banks
+    // (plane writes bank-conflict free), and each thread walks its k rows rotated by ROT so
+    // the reads of a phase do too (padded pitch TN + 4); the rotation is undone in registers.
+    // One elected lane arrives per warp. =====
+    constexpr int XS = tc_xs<TN, XW>();
+    constexpr int XP = tc_xpitch<TN>();
+    constexpr int KQ = TN == 64 ? 8 : 4;              // k per thread
+    constexpr int CW = TN / 4;                         // columns per warp
+    // ROT: rows by which odd-phase threads rotate their reads (bank offset 16 against the
+    // even phase): pitch XP words (u32) or 2 XP words (u64)
+    constexpr int ROT = TN == 64 ? (sizeof(XW) == 4 ? 4 : 2) : 2;
     const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
     const XW* Xb = static_cast<const XW*>(kWide ? static_cast<const void*>(a.X64) : static_cast<const void*>(a.X)) +
                    (static_cast<u64>(poly) * a.x_level + a.limb_off + limb) * a.N + n0;
-    const u32 r0 = warp * 4;
-    constexpr int kPer = 16 / sizeof(XW);  // residues per 16-byte chunk
+    const u32 kb = warp >> 2, cb = (warp & 3) * CW;
+    // this thread's column and first k within the step
+    u32 n_t, k_t;
+    bool rot;
+    if constexpr (TN == 64) {
+      n_t = cb + 8 * (lane >> 4) + (lane & 7);
+      k_t = 16 * kb + 8 * ((lane >> 3) & 1);
+      rot = ((lane >> 3) & 1) != 0;
+    } else {
+      n_t = cb + (lane & 7);
+      k_t = 16 * kb + 4 * (lane >> 3);
+      rot = sizeof(XW) == 4 ? ((lane >> 4) & 1) != 0 : ((lane >> 3) & 1) != 0;
+    }
+    constexpr int kPer = 16 / sizeof(XW);              // residues per 16-byte chunk
+    constexpr int kCpr = CW / kPer;                    // chunks per row of the warp's block
     auto issue = [&](u32 ks) {
-      // 4 rows x TN residues = 4 TN / kPer chunks of 16 B per warp; rows >= K zero-fill
 #pragma unroll
-      for (int i = 0; i < 4 * TN / kPer / 32; ++i) {
-        const u32 c = lane + i * 32, row = r0 + c / (TN / kPer), c4 = (c % (TN / kPer)) * kPer;
+      for (int i = 0; i < 16 * kCpr / 32; ++i) {
+        const u32 c = lane + i * 32, row = 16 * kb + c / kCpr, col = cb + (c % kCpr) * kPer;
         const u32 k = ks * kTcK + row;
-        const XW* src = Xb + static_cast<u64>(k < a.K ? k : 0) * xstride + c4;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(&S.xs[ks % kTcXS][row][c4])),
+        const XW* src = Xb + static_cast<u64>(k < a.K ? k : 0) * xstride + col;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(&S.xs[ks % XS][row][col])),
                      "l"(src), "r"(k < a.K ? 16 : 0));
       }
     };
 #pragma unroll 1
-    for (u32 j = 0; j < kTcXS - 1; ++j) {
+    for (u32 j = 0; j < XS - 1; ++j) {
       if (j < KS) issue(j);
       asm volatile("cp.async.commit_group;\n" ::);
     }
     for (u32 ks = 0; ks < KS; ++ks) {
       const u32 st = ks % kS, use = ks / kS;
-      asm volatile("cp.async.wait_group %0;\n" ::"n"(kTcXS - 2));
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(XS - 2));
       __syncwarp();
-      u32 v[TN / 32][4];
+      u32 v[KQ];
 #pragma unroll
-      for (int h = 0; h < TN / 32; ++h)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) v[h][i] = static_cast<u32>(S.xs[ks % kTcXS][r0 + i][lane + 32 * h]);
+      for (int i = 0; i < KQ; ++i) {
+        const u32 r = rot ? ((i + ROT) & (KQ - 1)) : static_cast<u32>(i);
+        v[i] = static_cast<u32>(S.xs[ks % XS][k_t + r][n_t]);
+      }
       __syncwarp();  // step ks's rows are consumed before the ring slot is refilled
-      if (ks + kTcXS - 1 < KS) issue(ks + kTcXS - 1);
+      if (ks + XS - 1 < KS) issue(ks + XS - 1);
       asm volatile("cp.async.commit_group;\n" ::);
+      // undo the rotation: w[t] = residue of k_t + t
+      u32 w[KQ];
+#pragma unroll
+      for (int t = 0; t < KQ; ++t) w[t] = rot ? v[(t - ROT) & (KQ - 1)] : v[t];
       if (ks >= kS) mbar_wait(&S.empty[st], (use - 1) & 1);
 #pragma unroll
-      for (int h = 0; h < TN / 32; ++h) {
-        // 4 x 4 byte transpose (8 PRMT): plane p gets byte p of the 4 residues k = r0 .. r0+3
-        const u32 t0 = __byte_perm(v[h][0], v[h][1], 0x5140), t1 = __byte_perm(v[h][0], v[h][1], 0x7362);
-        const u32 t2 = __byte_perm(v[h][2], v[h][3], 0x5140), t3 = __byte_perm(v[h][2], v[h][3], 0x7362);
-        const u32 o[4] = {__byte_perm(t0, t2, 0x5410), __byte_perm(t0, t2, 0x7632), __byte_perm(t1, t3, 0x5410),
-                          __byte_perm(t1, t3, 0x7632)};
+      for (int h = 0; h < KQ / 4; ++h) {
+        // 4 x 4 byte transpose (8 PRMT): plane p gets byte p of the residues k_t + 4h .. +3
+        const u32 t0 = __byte_perm(w[4 * h], w[4 * h + 1], 0x5140), t1 = __byte_perm(w[4 * h], w[4 * h + 1], 0x7362);
+        const u32 t2 = __byte_perm(w[4 * h + 2], w[4 * h + 3], 0x5140),
+                  t3 = __byte_perm(w[4 * h + 2], w[4 * h + 3], 0x7362);
+        v[4 * h + 0] = __byte_perm(t0, t2, 0x5410);
+        v[4 * h + 1] = __byte_perm(t0, t2, 0x7632);
+        v[4 * h + 2] = __byte_perm(t1, t3, 0x5410);
+        v[4 * h + 3] = __byte_perm(t1, t3, 0x7632);
+      }
 #pragma unroll
-        for (u32 p = 0; p < 4; ++p)
-          if (p < planes) *reinterpret_cast<u32*>(&S.b[st][p][cm_off(lane + 32 * h, r0)]) = o[p];
+      for (u32 p = 0; p < 4; ++p) {
+        if (p >= planes) break;
+        uint8_t* dst = &S.b[st][p][cm_off(n_t, k_t)];
+        if constexpr (KQ == 8)
+          *reinterpret_cast<uint2*>(dst) = make_uint2(v[p], v[4 + p]);
+        else
+          *reinterpret_cast<u32*>(dst) = v[p];
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::);
       __syncwarp();

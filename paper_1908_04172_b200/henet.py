@@ -302,8 +302,18 @@ def shard_range(total: int, rank: int, nranks: int) -> range:
     return range(b.value, b.value + c.value)
 
 
+def _load_torch_nccl() -> None:
+    """The library resolves NCCL at run time and prefers a copy already in the process:
+    load torch's (newer, and the one torch.distributed needs) before the first hg_comm call."""
+    try:
+        import torch  # noqa: F401  (libtorch_cuda links its bundled libnccl.so.2)
+    except Exception:  # pragma: no cover - torch absent: the system NCCL is used
+        pass
+
+
 def comm_unique_id() -> bytes:
     """hg_comm_unique_id (ncclGetUniqueId): create on one rank, send to all."""
+    _load_torch_nccl()
     buf = (C.c_uint8 * 128)()
     check(lib.hg_comm_unique_id(buf))
     return bytes(buf)
@@ -314,6 +324,7 @@ class Communicator:
 
     def __init__(self, ctx: CkksContext, unique_id: bytes, nranks: int, rank: int):
         assert len(unique_id) == 128
+        _load_torch_nccl()
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         h = C.c_void_p()
         check(lib.hg_comm_create(ctx.handle, buf, int(nranks), int(rank), C.byref(h)))
