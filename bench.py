@@ -97,6 +97,9 @@ def workload_config(n_gpus):
 class Clocks:
     def __init__(self, device):
         self.f = tempfile.NamedTemporaryFile(prefix="clocks", suffix=".csv", delete=False)
+        if os.environ.get("HG_BENCH_NO_CLOCKS"):  # diagnostic runs only: no clock evidence
+            self.p = None
+            return
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -758,10 +761,14 @@ def c4_run(args, ws, rank, local):
     l0 = ctx.launch_count()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
     e0, e1 = ev[0], ev[-1]
+    node_timing = os.environ.get("HG_NODE_TIMING") is not None  # diagnostic: per-node event times
     e0.record(ext)
     for i in range(steps):
-        out = H.execute(ctx, model, plan, x, None, eng)
+        st = H.ExecutionStats() if node_timing else None
+        out = H.execute(ctx, model, plan, x, None, eng, stats=st)
         ev[i + 1].record(ext)
+        if st is not None:
+            print("c4 step", i, "nodes", [(k, round(v, 2)) for k, v in st.layer_ms], file=sys.stderr)
     e1.synchronize()
     step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
     launches = ctx.launch_count() - l0

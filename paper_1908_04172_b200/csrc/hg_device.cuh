@@ -139,6 +139,11 @@ __device__ __forceinline__ u32 mulmod(u32 a, u32 b, const DevPrime& P) {
 __device__ __forceinline__ u32 addmod(u32 a, u32 b, u32 q) { return csub(a + b, q); }
 __device__ __forceinline__ u32 submod(u32 a, u32 b, u32 q) { return csub(a + q - b, q); }
 
+// u32 -> double with the 2^52 pair trick (MOV + DADD), not the slow I2F.F64 (conversion pipe).
+__device__ __forceinline__ double u32_to_f64(u32 x) {
+  return __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(x)), 4503599627370496.0);
+}
+
 // Signed value |c| < q -> residue in [0, q).
 __device__ __forceinline__ u32 from_signed(i32 c, u32 q) {
   return c < 0 ? static_cast<u32>(c + static_cast<i32>(q)) : static_cast<u32>(c);

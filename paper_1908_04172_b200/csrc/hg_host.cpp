@@ -53,9 +53,54 @@ static void check_launch(int r, const char* what) {
   cuda_check(cudaGetLastError(), what);
 }
 
+static constexpr size_t kBufCacheMin = size_t(256) << 20;
+static size_t buf_cache_max(int device) {
+  static std::mutex mu;
+  static std::map<int, size_t> v;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = v.find(device);
+  if (it != v.end()) return it->second;
+  size_t cap = 0;
+  const char* off = getenv("HG_BUF_CACHE");
+  if (!(off != nullptr && off[0] == '0')) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) cap = tot / 2;  // default: half the device
+    if (const char* e = getenv("HG_BUF_CACHE_MAX_GB")) cap = static_cast<size_t>(atof(e) * 1073741824.0);
+  }
+  v[device] = cap;
+  return cap;
+}
+
+void* DeviceCore::take(size_t bytes) {
+  std::lock_guard<std::mutex> g(cache_mu);
+  auto it = cache.find(bytes);
+  if (it == cache.end()) return nullptr;
+  void* p = it->second;
+  cache.erase(it);
+  cached -= bytes;
+  return p;
+}
+
+bool DeviceCore::put(void* p, size_t bytes) {
+  const size_t cap = buf_cache_max(device);
+  std::lock_guard<std::mutex> g(cache_mu);
+  if (cached + bytes > cap) return false;
+  cache.emplace(bytes, p);
+  cached += bytes;
+  return true;
+}
+
+void DeviceCore::flush() {
+  std::lock_guard<std::mutex> g(cache_mu);
+  for (auto& e : cache) cudaFreeAsync(e.second, stream);
+  cache.clear();
+  cached = 0;
+}
+
 DeviceCore::~DeviceCore() {
   if (stream) {
     cudaSetDevice(device);
+    flush();
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
   }
@@ -64,11 +109,23 @@ DeviceCore::~DeviceCore() {
 DeviceBuffer::DeviceBuffer(std::shared_ptr<DeviceCore> c, size_t b, cudaStream_t s) : core(std::move(c)), bytes(b) {
   stream = s ? s : core->stream;
   if (bytes == 0) return;
-  cuda_check(cudaMallocAsync(&ptr, bytes, stream), "cudaMallocAsync");
+  const bool cacheable = bytes >= kBufCacheMin && stream == core->stream;
+  if (cacheable && (ptr = core->take(bytes)) != nullptr) return;
+  cudaError_t e = cudaMallocAsync(&ptr, bytes, stream);
+  if (e == cudaErrorMemoryAllocation && core->cached > 0) {
+    // the cache holds the memory: release it (stream-ordered) and retry once
+    cudaGetLastError();
+    core->flush();
+    cudaStreamSynchronize(core->stream);
+    e = cudaMallocAsync(&ptr, bytes, stream);
+  }
+  cuda_check(e, "cudaMallocAsync");
 }
 
 DeviceBuffer::~DeviceBuffer() {
-  if (ptr) cudaFreeAsync(ptr, stream);
+  if (!ptr) return;
+  if (bytes >= kBufCacheMin && stream == core->stream && core->put(ptr, bytes)) return;
+  cudaFreeAsync(ptr, stream);
 }
 
 // ---------------------------------------------------------------------------
@@ -958,6 +1015,20 @@ struct Value {
 // (node id, ms) of the most recent hg_execute on this thread that asked for stats.
 thread_local std::vector<std::pair<std::string, double>> g_last_layers;
 
+// Batching of the Dot contraction over output positions (MacDenseTcArgs::npos and strides).
+struct DotBatch {
+  u32 npos = 1;
+  u64 xk = 1, xp = 0, ym = 1, yp = 0;
+  template <typename A>
+  void apply(A& a) const {
+    a.npos = npos;
+    a.x_kstride = xk;
+    a.x_pstride = xp;
+    a.y_mstride = ym;
+    a.y_pstride = yp;
+  }
+};
+
 class Executor {
  public:
   Executor(const std::shared_ptr<Context>& ctx, Model& model, const Plan& plan, const RelinKeyDev* rk,
@@ -1139,23 +1210,13 @@ class Executor {
     BufPtr bias_pt;
 
     const size_t wb = ctx.word_bytes();
-    if (n.op == HG_OP_DOT) {
-      const u32 K = w.dims[0], Mo = w.dims[1];
-      const u32 BM = ctx.wide ? mac_dense_w_bm() : mac_dense_warps(Mo) * 4;
-      const u32 Mpad = (Mo + BM - 1) / BM * BM;
-      BufPtr wres = encoding(w, {1, L, bits(s), Mpad}, static_cast<u64>(L) * K * Mpad * wb, [&](void* p) {
-        cuda_check(cudaMemsetAsync(p, 0, static_cast<u64>(L) * K * Mpad * wb, s_), "memset");
-        check_launch(encode_f32(ctx, wd, w.data.size(), Mo, Mpad, static_cast<u64>(K) * Mpad, L, s, p, s_),
-                     "encode weights");
-      });
+    // The Dot contraction (henet/graph.hpp:935-954) of x with weight residues wres [L][K][Mpad]
+    // and bias_res [L][Mpad] into v.  bt batches it over output positions (a 1x1, stride-1
+    // convolution: one Dot per position, positions as extra columns of the same kernels);
+    // tag keeps the packed-weight cache keys of the two uses apart.
+    auto dot_dispatch = [&](WeightTensor& w, const BufPtr& wres, const BufPtr& bias_res, u32 K, u32 Mo, u32 Mpad,
+                            u64 tag, const DotBatch& bt) -> int {
       int r = 1;
-      if (b && x.packing == HG_PACKING_REAL) {
-        check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
-        const float* bd = weight_dev(ctx, *b, s_);
-        bias_res = encoding(*b, {2, L, bits(acc_scale), Mpad}, static_cast<u64>(L) * Mpad * wb, [&](void* p) {
-          check_launch(encode_f32(ctx, bd, Mo, Mo, Mpad, Mpad, L, acc_scale, p, s_), "encode bias");
-        });
-      }
       if (ctx.wide) {
         // Limbs whose prime is < 2^30 (BASELINE c4/c5b: limbs 1..7) go through the int8 tensor
         // cores on a u32 copy of their residues; the rest (the 40-bit limb 0) on the wide
@@ -1192,6 +1253,7 @@ class Executor {
           return !(e != nullptr && e[0] == '0');
         }();
         const bool limb0_tc = wide_tc && tc_lo == 1 && ctx.chain[0] < (1ull << 40) && K <= 6605;
+        if (bt.npos > 1 && !limb0_tc) return -2;  // the CUDA-core wide kernels run plain Dots only
         if (limb0_tc) {
           BufPtr wp0 = ctx.alloc(tc_packed_weight_bytes_w(K, Mo), s_);
           check_launch(launch_pack_weights_tc_w(static_cast<const u64*>(wres->ptr), static_cast<uint8_t*>(wp0->ptr), K,
@@ -1216,6 +1278,7 @@ class Executor {
             t.cs[i] = c;
             c = static_cast<u64>((static_cast<nt::u128>(c) << 8) % q0);
           }
+          bt.apply(t);
           r = launch_mac_dense_tc_w(t, &ctx.basisw.p[0], s_);
         } else {
           r = launch_mac_dense_w(a, ctx.basisw, s_);
@@ -1257,11 +1320,12 @@ class Executor {
           t.polys = 2;
           t.x_level = x.level;
           for (u32 i = 0; i < cnt; ++i) t.planes[i] = ctx.chain[tc_lo + i] < (1ull << 24) ? 3 : 4;
+          bt.apply(t);
           r = launch_mac_dense_tc(t, sub, s_);
         }
       } else if (ctx.dense_tc && K <= 8192) {
         // tensor-core path: byte-plane weights packed once per call, then tcgen05.mma.kind::i8
-        BufPtr wp = encoding(w, {3, L, bits(s), Mpad}, tc_packed_weight_bytes(K, Mo, L), [&](void* p) {
+        BufPtr wp = encoding(w, {tag + 3, L, bits(s), Mpad}, tc_packed_weight_bytes(K, Mo, L), [&](void* p) {
           check_launch(launch_pack_weights_tc(static_cast<const u32*>(wres->ptr), static_cast<uint8_t*>(p), K, Mo,
                                               Mpad, L, s_),
                        "pack weights");
@@ -1279,8 +1343,10 @@ class Executor {
         a.polys = 2;
         a.x_level = x.level;
         for (u32 i = 0; i < L; ++i) a.planes[i] = ctx.chain[i] < (1ull << 24) ? 3 : 4;
+        bt.apply(a);
         r = launch_mac_dense_tc(a, ctx.basis, s_);
       } else {
+        if (bt.npos > 1) return -2;  // the CUDA-core kernel runs plain Dots only
         MacDenseArgs a{};
         a.X = x.data();
         a.Y = v.cipher.data();
@@ -1299,16 +1365,92 @@ class Executor {
         }
         r = launch_mac_dense(a, ctx.basis, s_);
       }
+      return r;
+    };
+
+    if (n.op == HG_OP_DOT) {
+      const u32 K = w.dims[0], Mo = w.dims[1];
+      const u32 BM = ctx.wide ? mac_dense_w_bm() : mac_dense_warps(Mo) * 4;
+      const u32 Mpad = (Mo + BM - 1) / BM * BM;
+      BufPtr wres = encoding(w, {1, L, bits(s), Mpad}, static_cast<u64>(L) * K * Mpad * wb, [&](void* p) {
+        cuda_check(cudaMemsetAsync(p, 0, static_cast<u64>(L) * K * Mpad * wb, s_), "memset");
+        check_launch(encode_f32(ctx, wd, w.data.size(), Mo, Mpad, static_cast<u64>(K) * Mpad, L, s, p, s_),
+                     "encode weights");
+      });
+      int r = 1;
+      if (b && x.packing == HG_PACKING_REAL) {
+        check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
+        const float* bd = weight_dev(ctx, *b, s_);
+        bias_res = encoding(*b, {2, L, bits(acc_scale), Mpad}, static_cast<u64>(L) * Mpad * wb, [&](void* p) {
+          check_launch(encode_f32(ctx, bd, Mo, Mo, Mpad, Mpad, L, acc_scale, p, s_), "encode bias");
+        });
+      }
+      r = dot_dispatch(w, wres, bias_res, K, Mo, Mpad, 0, DotBatch{});
       check_launch(r, "mac_dense");
     } else {
       const auto& in_shape = x.shape;
       require(in_shape.size() == 3, "Convolution expects a (C,H,W) input");
       const u32 F = n.attrs.filters, C = in_shape[0], win = n.attrs.window, T2 = win * win;
+      // 1x1, stride-1, unpadded windows (the MobileNetV2 expand / project layers): every output
+      // position is a Dot of its C input channels, so the layer runs as one batched Dot on the
+      // tensor-core contraction (positions as extra columns) instead of the tap-gather kernel.
+      bool conv1x1_done = false;
+      static const bool conv1x1_on = [] {
+        const char* e = getenv("HG_CONV1X1_DOT");
+        return !(e != nullptr && e[0] == '0');
+      }();
+      if (conv1x1_on && win == 1 && n.attrs.stride == 1 && n.attrs.pad[0] == 0 && n.attrs.pad[1] == 0 &&
+          n.attrs.pad[2] == 0 && n.attrs.pad[3] == 0 && in_shape[1] == out_shape[1] && in_shape[2] == out_shape[2]) {
+        const u32 K = C, Mo = F;
+        const u32 BM = ctx.wide ? mac_dense_w_bm() : mac_dense_warps(Mo) * 4;
+        const u32 Mpad = (Mo + BM - 1) / BM * BM;
+        // weights [F][C] -> [C][F] (the Dot layout [K][M]), then encoded like a Dot's
+        BufPtr wt = encoding(w, {109}, static_cast<u64>(K) * Mo * 4, [&](void* p) {
+          std::vector<float> t(static_cast<u64>(K) * Mo);
+          for (u32 f = 0; f < F; ++f)
+            for (u32 c = 0; c < C; ++c) t[static_cast<u64>(c) * F + f] = w.data[static_cast<u64>(f) * C + c];
+          cuda_check(cudaMemcpyAsync(p, t.data(), t.size() * 4, cudaMemcpyHostToDevice, s_), "h2d");
+          cuda_check(cudaStreamSynchronize(s_), "h2d");  // the host vector leaves scope
+        });
+        BufPtr wres = encoding(w, {101, L, bits(s), Mpad}, static_cast<u64>(L) * K * Mpad * wb, [&](void* p) {
+          cuda_check(cudaMemsetAsync(p, 0, static_cast<u64>(L) * K * Mpad * wb, s_), "memset");
+          check_launch(encode_f32(ctx, static_cast<const float*>(wt->ptr), static_cast<u64>(K) * Mo, Mo, Mpad,
+                                  static_cast<u64>(K) * Mpad, L, s, p, s_),
+                       "encode weights");
+        });
+        BufPtr bres;
+        if (b && x.packing == HG_PACKING_REAL) {
+          check_scalar_encodable(ctx, b->max_abs, L, acc_scale);
+          const float* bd = weight_dev(ctx, *b, s_);
+          bres = encoding(*b, {102, L, bits(acc_scale), Mpad}, static_cast<u64>(L) * Mpad * wb, [&](void* p) {
+            check_launch(encode_f32(ctx, bd, Mo, Mo, Mpad, Mpad, L, acc_scale, p, s_), "encode bias");
+          });
+        }
+        const u32 HW = in_shape[1] * in_shape[2];
+        DotBatch bt;
+        bt.npos = HW;
+        bt.xk = HW;  // input channel c of position p: element c * HW + p
+        bt.xp = 1;
+        bt.ym = HW;  // output filter f of position p: element f * HW + p
+        bt.yp = 1;
+        const int r = dot_dispatch(w, wres, bres, K, Mo, Mpad, 100, bt);
+        if (r != -2) {
+          check_launch(r, "mac_conv1x1");
+          conv1x1_done = true;
+        }
+      }
+      if (!conv1x1_done) {
       // one launch of the convolution kernel on (X, Y, Wr, Bi) with Cc channels, Ff filters
-      auto run_conv = [&](const void* X, void* Y, const void* Wr, const void* Bi, u32 Cc, u32 Ff) {
+      auto run_conv = [&](const void* X, void* Y, const void* Wr, const void* Bi, u32 Cc, u32 Ff, u32 groups = 1,
+                          u64 gx = 0, u64 gy = 0, u64 gw = 0, u64 gb = 0) {
         int r = 1;
         if (ctx.wide) {
           MacConvArgsW a{};
+          a.groups = groups;
+          a.gx = gx;
+          a.gy = gy;
+          a.gw = gw;
+          a.gb = gb;
           a.X = static_cast<const u64*>(X);
           a.Y = static_cast<u64*>(Y);
           a.W = static_cast<const u64*>(Wr);
@@ -1444,10 +1586,17 @@ class Executor {
         }
         const u64 xs = static_cast<u64>(in_shape[1]) * in_shape[2] * 2 * x.level * N * wb;  // bytes per channel
         const u64 ys = static_cast<u64>(out_shape[1]) * out_shape[2] * 2 * L * N * wb;
-        for (u32 c = 0; c < C; ++c)
-          run_conv(static_cast<const char*>(x.buf->ptr) + c * xs, static_cast<char*>(v.cipher.buf->ptr) + c * ys,
-                   static_cast<const char*>(wres->ptr) + static_cast<u64>(c) * L * T2 * wb,
-                   bias_res ? static_cast<const char*>(bias_res->ptr) + static_cast<u64>(c) * L * wb : nullptr, 1, 1);
+        if (ctx.wide) {
+          // every channel in one launch (groups = C): 96 launches of one channel's positions
+          // each left the GPU mostly idle
+          run_conv(x.buf->ptr, v.cipher.buf->ptr, wres->ptr, bias_res ? bias_res->ptr : nullptr, 1, 1, C, xs / wb,
+                   ys / wb, static_cast<u64>(L) * T2, L);
+        } else {
+          for (u32 c = 0; c < C; ++c)
+            run_conv(static_cast<const char*>(x.buf->ptr) + c * xs, static_cast<char*>(v.cipher.buf->ptr) + c * ys,
+                     static_cast<const char*>(wres->ptr) + static_cast<u64>(c) * L * T2 * wb,
+                     bias_res ? static_cast<const char*>(bias_res->ptr) + static_cast<u64>(c) * L * wb : nullptr, 1, 1);
+        }
       } else {
         BufPtr wres = encoding(w, {4, L, bits(s)}, static_cast<u64>(L) * w.data.size() * wb, [&](void* p) {
           check_launch(encode_f32(ctx, wd, w.data.size(), static_cast<u32>(w.data.size()),
@@ -1463,6 +1612,7 @@ class Executor {
         }
         run_conv(x.buf->ptr, v.cipher.buf->ptr, wres->ptr, bias_res ? bias_res->ptr : nullptr, C, F);
       }
+      }  // !conv1x1_done
     }
     if (b && x.packing == HG_PACKING_COMPLEX) {
       // encode_broadcast under complex packing: encode_vector of (b + b i) in every slot
@@ -1822,8 +1972,15 @@ class Executor {
     resp.ctx = ctx_;
     resp.b.packing = x.packing;
     resp.b.scale = ctx.default_scale;
+    static const bool trace = getenv("HG_REFRESH_TRACE") != nullptr;
+    const auto t_a = std::chrono::steady_clock::now();
     ensure(ctx, resp.b, elem_count(out_shape), 2, static_cast<u32>(ctx.chain_len()), s_);
+    const auto t_b = std::chrono::steady_clock::now();
     cuda_check(cudaStreamSynchronize(s_), "nonlinearity");
+    if (trace)
+      std::fprintf(stderr, "nonlinearity %s: response alloc %.2f ms, sync %.2f ms\n", n.id.c_str(),
+                   std::chrono::duration<double, std::milli>(t_b - t_a).count(),
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_b).count());
     const int rc = provider_(user_, n.op == HG_OP_RELU ? HG_NONLIN_RELU : HG_NONLIN_MAXPOOL, window, layer_seq, &req, &resp);
     if (rc != 0) throw Error(HG_ERR_VALIDATION, "nonlinearity provider failed: " + g_last_error);
     require(resp.b.count == elem_count(out_shape), "provider returned the wrong element count");
@@ -2912,7 +3069,12 @@ int hg_refresh_engine_apply(void* engine, int kind, uint32_t window, uint32_t la
     const u64 groups = b.count / window;
     const u32 half = c.n / 2;
     const u32 L = static_cast<u32>(c.chain_len());
+    using clk = std::chrono::steady_clock;
+    const auto t_in = clk::now();
+    // the response buffer the executor already allocated (eval_nonlinear) is reused when it
+    // is large enough: one fewer layer-sized allocation at the block's memory peak
     CtBatch o;
+    o.buf = std::move(response->b.buf);
     o.packing = b.packing;
     o.scale = c.default_scale;
     ensure(c, o, groups, 2, L, s);
@@ -2925,7 +3087,12 @@ int hg_refresh_engine_apply(void* engine, int kind, uint32_t window, uint32_t la
     BufPtr res = c.alloc(std::min(groups, cg) * half * 2 * sizeof(double), s);
     const u64 seed = derive_seed_host(eng->seed, layer_seq);
     const DeferredMagnitudes mags(c, groups, s);
+    // HG_REFRESH_TRACE: host time of each chunk's enqueue and of the final read-back (stderr)
+    static const bool trace = getenv("HG_REFRESH_TRACE") != nullptr;
+    const auto t0 = clk::now();
+    std::string tr;
     for (u64 g0 = 0; g0 < groups; g0 += cg) {
+      const auto tc = clk::now();
       const u64 ng = std::min(cg, groups - g0);
       decode_into(c, eng->sk, static_cast<const char*>(b.buf->ptr) + g0 * window * in_ct, ng * window, b.polys,
                   b.level, b.scale, static_cast<double*>(sl->ptr), s);
@@ -2937,8 +3104,15 @@ int hg_refresh_engine_apply(void* engine, int kind, uint32_t window, uint32_t la
       BufPtr pt = encode_vectors_dev(c, static_cast<const double*>(res->ptr), half, ng, L, c.default_scale, s, mant,
                                      ex, &mags, g0);
       encrypt_into(c, eng->sk, pt->ptr, ng, seed, g0, static_cast<char*>(o.buf->ptr) + g0 * out_ct, s);
+      if (trace) tr += " " + std::to_string(std::chrono::duration<double, std::milli>(clk::now() - tc).count());
     }
+    const auto t1 = clk::now();
     mags.check(c, L, s);  // one read-back per layer; synchronises the stream
+    if (trace)
+      std::fprintf(stderr, "refresh layer %u: setup %.2f ms; enqueue chunks [ms]%s; enqueue total %.2f ms, read-back wait %.2f ms\n",
+                   layer_seq, std::chrono::duration<double, std::milli>(t0 - t_in).count(), tr.c_str(),
+                   std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                   std::chrono::duration<double, std::milli>(clk::now() - t1).count());
     response->b = o;
     response->b.shape = {static_cast<u32>(groups)};
   });

@@ -306,10 +306,8 @@ constexpr u32 kConvPos = HG_CONV_PP;  // output positions per CTA
 // IMAD.WIDE (fma pipe, u64 accumulators), filters [KI, FT) as DFMAs on the FP64 pipe.
 // Exact: residues < 2^24-ish and at most 32 taps keep every partial sum an integer
 // < 2^53 (host flag fp64[limb]); both accumulators are reduced the same way at the end.
-// A u32 becomes a double with the 2^52 pair trick (MOV + DADD), not the slow I2F.F64.
-__device__ __forceinline__ double u32_to_f64(u32 x) {
-  return __hiloint2double(0x43300000, static_cast<int>(x)) - 4503599627370496.0;
-}
+// A u32 becomes a double with the 2^52 pair trick (MOV + DADD), not the slow I2F.F64
+// (u32_to_f64, hg_device.cuh).
 
 template <int FT>
 struct ConvSplit {

@@ -55,6 +55,16 @@ bool host_narrow_upload(int device, const uint64_t* words, uint32_t* dst, uint64
 struct DeviceCore {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // Large-buffer cache: buffers >= kBufCacheMin allocated on `stream` are kept on release and
+  // handed to the next request of exactly that size (stream-ordered like cudaFreeAsync /
+  // cudaMallocAsync on the same stream).  A layer-sized cudaMallocAsync at a workload's memory
+  // peak can otherwise spend ~30-130 ms remapping pool memory (the c4 block).
+  std::mutex cache_mu;
+  std::multimap<size_t, void*> cache;
+  size_t cached = 0;
+  void* take(size_t bytes);
+  bool put(void* p, size_t bytes);
+  void flush();  // cudaFreeAsync every cached buffer on `stream`
   ~DeviceCore();
 };
 

@@ -21,6 +21,9 @@
 // plane against all input planes stacked along N.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "hg_tc.hpp"
 #include "hg_wide.cuh"
 
@@ -28,6 +31,11 @@ namespace hg {
 
 #ifndef HG_TC_STAGES
 #define HG_TC_STAGES 4
+#endif
+// L2 prefetch size hint of the producers' input loads: a CTA reads TN residues per input row,
+// the neighbouring column tiles (other CTAs in flight) the rest of the row
+#ifndef HG_TC_L2PF
+#define HG_TC_L2PF ".L2::256B"
 #endif
 constexpr int kTcM = 128, kTcN = 64, kTcK = 32, kTcS = HG_TC_STAGES;
 constexpr int kTcProducers = 256;                 // 8 warps split X into byte planes
@@ -53,9 +61,9 @@ constexpr int tc_stages() { return TN == 64 ? 5 : 4; }
 
 // Staged input rows are padded (TN + 4 residues) so the producers' transposed reads of a
 // k-block hit distinct banks (see the producer loop); the wide TN = 64 ring is one stage
-// shallower to stay within 227 KB.
+// shallower to stay within 227 KB, the wide TN = 32 ring 3 deep so two CTAs fit per SM.
 template <int TN, typename XW>
-constexpr int tc_xs() { return (TN == 64 && sizeof(XW) == 8) ? kTcXS - 1 : kTcXS; }
+constexpr int tc_xs() { return sizeof(XW) == 8 ? (TN == 64 ? kTcXS - 1 : 3) : kTcXS; }
 template <int TN>
 constexpr int tc_xpitch() { return TN + 4; }
 
@@ -67,7 +75,7 @@ struct TcSmem {
                                   // stage are consecutive, i.e. one K-major (planes*TN) x 32 matrix
   uint8_t zero_a[kTcPlaneA];      // zero weight plane: initialises the upper accumulators
   XW xs[tc_xs<TN, XW>()][kTcK][tc_xpitch<TN>()];  // input residues staged by cp.async (producer ring)
-  unsigned long long full_a[kS], full_b[kS], empty[kS];
+  unsigned long long full_a[kS], full_b[kS], empty[kS], acc_full, acc_empty;
   u32 tmem;
 };
 // TMEM columns: 7 diagonal accumulators of TN columns (512 for TN = 64: one CTA per SM;
@@ -122,12 +130,19 @@ __global__ void k_pack_weights_tc(const u32* W, uint8_t* Wp, u32 K, u32 Mpad, u3
 }
 
 // ---------------------------------------------------------------------------
-// Main kernel.  grid = (Mtiles, N / TN, polys * level), 288 threads:
+// Main kernel.  grid = (Mtiles * N/TN * position chunks, 1, polys * level), 288 threads:
 //   warps 0-7  producers: X(ks) -> byte planes B[ks % S]; then the epilogue
 //   warp 8     lane 0: weight planes by cp.async.bulk into A[], MMA issue, commits
 // Rings: full_a (tx bytes), full_b (256 producer arrivals), empty (MMA commit).
+// Batched contractions (npos > 1, a 1x1 convolution) whose k steps all fit the weight ring
+// keep the weights resident and walk a chunk of a.ppc positions per CTA: iteration
+// it = p * KS + ks over (position, k step); after a position's last k step the MMA commit
+// arrives on acc_full, the producers drain the accumulators (epilogue) and arrive on
+// acc_empty before the next position's first MMA overwrites them.
 // ---------------------------------------------------------------------------
-template <int TN, typename XW = u32>
+// BATCH: more than one position per CTA (the epilogue runs inside the k loop); otherwise the
+// single position's epilogue follows the loop, as in a plain Dot.
+template <int TN, typename XW = u32, bool BATCH = false>
 __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(MacDenseTcArgs a, Basis B) {
   extern __shared__ __align__(1024) uint8_t tc_raw[];
   TcSmem<TN, XW>& S = *reinterpret_cast<TcSmem<TN, XW>*>(tc_raw);
@@ -137,12 +152,17 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
   const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // M tiles fastest: the CTAs in flight share their input columns (read from HBM once, the
   // other M tiles hit L2) while each M tile's weight planes stay L2-resident across N tiles
-  const u32 mt = blockIdx.x;
-  const u32 n0 = blockIdx.y * TN;
+  const u32 ntiles = a.N / TN;
+  const u32 mt = blockIdx.x % a.Mtiles;
+  const u32 nt = (blockIdx.x / a.Mtiles) % ntiles, pc = blockIdx.x / a.Mtiles / ntiles;
+  const u32 n0 = nt * TN;
+  const u32 pos0 = pc * a.ppc, NP = min(a.ppc, a.npos - pos0);  // this CTA's positions
   const u32 poly = blockIdx.z / a.level, limb = blockIdx.z % a.level;
   const DevPrime& P = B.p[limb];
   const u32 planes = a.planes[limb];  // 3 for q < 2^24, 4 otherwise
   const u32 KS = a.Ksteps;
+  const bool resident = BATCH && KS <= static_cast<u32>(kS);  // all weight k steps held at once
+  const u32 IT = NP * KS;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_addr(&S.tmem)),
@@ -155,6 +175,8 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
       mbar_init(&S.full_b[i], kTcProducers / 32);  // one arrive per producer warp
       mbar_init(&S.empty[i], 1);
     }
+    mbar_init(&S.acc_full, 1);
+    mbar_init(&S.acc_empty, kTcProducers / 32);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
   }
   for (u32 i = tid; i < kTcPlaneA / 16; i += kTcThreads)
@@ -179,21 +201,30 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
                 smem_addr(&S.a[st][0][0])),
             "l"(Wt + static_cast<u64>(j) * 4 * kTcPlaneA), "r"(bytes), "r"(smem_addr(&S.full_a[st])));
       };
-      for (u32 j = 0; j < kS - 1 && j < KS; ++j) load_a(j);
+      if (resident) {
+        for (u32 j = 0; j < KS; ++j) load_a(j);
+      } else {
+        for (u32 j = 0; j < kS - 1 && j < KS; ++j) load_a(j);
+      }
       // One MMA per weight plane pa against all input planes at once: B = the stage's planes
       // stacked along N (planes * 64 rows), D at TMEM column pa * 64, so input plane pb lands
       // in columns (pa + pb) * 64: the diagonal accumulator D_s, s = pa + pb, with no
       // per-(pa, pb) MMA.  idesc: D s32, A/B u8, K-major, N = planes * 64, M = 128.
       const u32 idesc = (2u << 4) | (((planes * TN) >> 3) << 17) | ((kTcM >> 4) << 24);
       const u64 zd = umma_desc(smem_addr(&S.zero_a[0]));
-      for (u32 ks = 0; ks < KS; ++ks) {
-        const u32 st = ks % kS, use = ks / kS;
-        const u32 j = ks + kS - 1;
-        if (j < KS) {
-          if (j >= kS) mbar_wait(&S.empty[j % kS], ((j / kS) - 1) & 1);
-          load_a(j);
+      // (p, ks) = (it / KS, it % KS), kept incrementally
+      for (u32 it = 0, p = 0, ks = 0; it < IT; ++it, ks = (ks + 1 == KS) ? 0 : ks + 1, p += (ks == 0) ? 1 : 0) {
+        const u32 st = it % kS, use = it / kS;
+        if (!resident) {  // NP == 1: it == ks
+          const u32 j = ks + kS - 1;
+          if (j < KS) {
+            if (j >= kS) mbar_wait(&S.empty[j % kS], ((j / kS) - 1) & 1);
+            load_a(j);
+          }
         }
-        mbar_wait(&S.full_a[st], use & 1);
+        const u32 ast = resident ? ks : st;
+        if (!resident || p == 0) mbar_wait(&S.full_a[ast], resident ? 0u : (use & 1));
+        if (BATCH && ks == 0 && p > 0) mbar_wait(&S.acc_empty, (p - 1) & 1);  // position p-1 drained
         mbar_wait(&S.full_b[st], use & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
         const u64 bd = umma_desc(smem_addr(&S.b[st][0][0]));
@@ -203,7 +234,7 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
                        "l"(zd), "l"(bd), "r"(idesc));
         }
         for (u32 pa = 0; pa < planes; ++pa) {
-          const u64 ad = umma_desc(smem_addr(&S.a[st][pa][0]));
+          const u64 ad = umma_desc(smem_addr(&S.a[ast][pa][0]));
           const u32 accum = (ks > 0 || pa > 0) ? 1u : 0u;  // pa = 0 of step 0 initialises s < planes
           asm volatile(
               "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -212,6 +243,9 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
             smem_addr(&S.empty[st])));
+        if (ks == KS - 1)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+              smem_addr(&S.acc_full)));
       }
     }
   } else {
@@ -232,9 +266,11 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
     // ROT: rows by which odd-phase threads rotate their reads (bank offset 16 against the
     // even phase): pitch XP words (u32) or 2 XP words (u64)
     constexpr int ROT = TN == 64 ? (sizeof(XW) == 4 ? 4 : 2) : 2;
-    const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
+    const u64 xelem = static_cast<u64>(a.polys) * a.x_level * a.N;  // words per input element
+    const u64 xstride = a.x_kstride * xelem;
     const XW* Xb = static_cast<const XW*>(kWide ? static_cast<const void*>(a.X64) : static_cast<const void*>(a.X)) +
-                   (static_cast<u64>(poly) * a.x_level + a.limb_off + limb) * a.N + n0;
+                   pos0 * a.x_pstride * xelem + (static_cast<u64>(poly) * a.x_level + a.limb_off + limb) * a.N + n0;
+    const u64 xpstep = a.x_pstride * xelem;
     const u32 kb = warp >> 2, cb = (warp & 3) * CW;
     // this thread's column and first k within the step
     u32 n_t, k_t;
@@ -250,39 +286,103 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
     }
     constexpr int kPer = 16 / sizeof(XW);              // residues per 16-byte chunk
     constexpr int kCpr = CW / kPer;                    // chunks per row of the warp's block
-    auto issue = [&](u32 ks) {
+    u32 ip = 0, iks = 0;  // (position, k step) of the next issue(): called for it = 0, 1, 2, ...
+    auto issue = [&](u32 it) {
+      const u32 p = ip, ks = iks;
+      if (++iks == KS) {
+        iks = 0;
+        ++ip;
+      }
+      const XW* Xp = Xb + p * xpstep;
 #pragma unroll
       for (int i = 0; i < 16 * kCpr / 32; ++i) {
         const u32 c = lane + i * 32, row = 16 * kb + c / kCpr, col = cb + (c % kCpr) * kPer;
         const u32 k = ks * kTcK + row;
-        const XW* src = Xb + static_cast<u64>(k < a.K ? k : 0) * xstride + col;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(&S.xs[ks % XS][row][col])),
+        const XW* src = Xp + static_cast<u64>(k < a.K ? k : 0) * xstride + col;
+        asm volatile("cp.async.cg.shared.global" HG_TC_L2PF " [%0], [%1], 16, %2;\n" ::"r"(smem_addr(&S.xs[it % XS][row][col])),
                      "l"(src), "r"(k < a.K ? 16 : 0));
       }
     };
 #pragma unroll 1
     for (u32 j = 0; j < XS - 1; ++j) {
-      if (j < KS) issue(j);
+      if (j < IT) issue(j);
       asm volatile("cp.async.commit_group;\n" ::);
     }
-    for (u32 ks = 0; ks < KS; ++ks) {
-      const u32 st = ks % kS, use = ks / kS;
+    const u32 lg = warp & 3, ch = warp >> 2;
+    const u32 m = mt * kTcM + lg * 32 + lane;
+    const u32 q = P.q;
+    const u32* cs = a.cs[limb];  // 2^(8s) mod q (host)
+    const u32 nacc = 2 * planes - 1;
+    const u32 bv = (a.bias != nullptr && poly == 0 && m < a.M) ? __ldg(&a.bias[static_cast<u64>(limb) * a.Mpad + m]) : 0u;
+    // ===== epilogue of position pos0 + p: warp w reads TMEM lanes 32*(w%4).., columns
+    // (w/4)*TN/2 .. +TN/2 =====
+    auto epilogue = [&](u32 p) {
+      mbar_wait(&S.acc_full, p & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      const u64 ye = m * a.y_mstride + (pos0 + p) * a.y_pstride;  // output element
+#pragma unroll
+      for (u32 cc = 0; cc < TN / 2; cc += 8) {
+        const u32 col = ch * (TN / 2) + cc;
+        u64 acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0;
+        // two diagonals per TMEM wait; diagonal 2 planes - 1 (read when nacc is odd) is
+        // zeroed by the ks == 0 MMA and never accumulated.  D_s < 2^31 and 2^(8s) mod q < 2^30:
+        // one IMAD.WIDE.U32 per term, the sum of 8 stays < 2^64.
+        for (u32 s = 0; s < nacc; s += 2) {
+          u32 r[8], r2[8];
+          const u32 taddr = tmem + ((lg * 32) << 16) + s * TN + col;
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                       : "r"(taddr));
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                       : "=r"(r2[0]), "=r"(r2[1]), "=r"(r2[2]), "=r"(r2[3]), "=r"(r2[4]), "=r"(r2[5]), "=r"(r2[6]),
+                         "=r"(r2[7])
+                       : "r"(taddr + TN));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+          const u32 c0 = cs[s], c1 = cs[s + 1];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] += static_cast<u64>(r[i]) * c0 + static_cast<u64>(r2[i]) * c1;
+        }
+        if (m < a.M) {
+          u32 o[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o[i] = addmod(reduce64(acc[i], P), bv, q);
+          if constexpr (kWide) {
+            u64* yp = a.Y64 + ((ye * a.polys + poly) * a.y_level + a.limb_off + limb) * a.N + n0 + col;
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) *reinterpret_cast<ulonglong2*>(yp + i) = make_ulonglong2(o[i], o[i + 1]);
+          } else {
+            u32* yp = a.Y + ((ye * a.polys + poly) * a.level + limb) * a.N + n0 + col;
+            *reinterpret_cast<uint4*>(yp) = make_uint4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<uint4*>(yp + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+          }
+        }
+      }
+      if (p + 1 < NP) {  // the accumulators are free for the next position
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.acc_empty);
+      }
+    };
+    for (u32 it = 0, p = 0, ks = 0; it < IT; ++it, ks = (ks + 1 == KS) ? 0 : ks + 1, p += (ks == 0) ? 1 : 0) {
+      const u32 st = it % kS, use = it / kS;
       asm volatile("cp.async.wait_group %0;\n" ::"n"(XS - 2));
       __syncwarp();
       u32 v[KQ];
 #pragma unroll
       for (int i = 0; i < KQ; ++i) {
         const u32 r = rot ? ((i + ROT) & (KQ - 1)) : static_cast<u32>(i);
-        v[i] = static_cast<u32>(S.xs[ks % XS][k_t + r][n_t]);
+        v[i] = static_cast<u32>(S.xs[it % XS][k_t + r][n_t]);
       }
-      __syncwarp();  // step ks's rows are consumed before the ring slot is refilled
-      if (ks + XS - 1 < KS) issue(ks + XS - 1);
+      __syncwarp();  // step it's rows are consumed before the ring slot is refilled
+      if (it + XS - 1 < IT) issue(it + XS - 1);
       asm volatile("cp.async.commit_group;\n" ::);
       // undo the rotation: w[t] = residue of k_t + t
       u32 w[KQ];
 #pragma unroll
       for (int t = 0; t < KQ; ++t) w[t] = rot ? v[(t - ROT) & (KQ - 1)] : v[t];
-      if (ks >= kS) mbar_wait(&S.empty[st], (use - 1) & 1);
+      if (it >= static_cast<u32>(kS)) mbar_wait(&S.empty[st], (use - 1) & 1);
 #pragma unroll
       for (int h = 0; h < KQ / 4; ++h) {
         // 4 x 4 byte transpose (8 PRMT): plane p gets byte p of the residues k_t + 4h .. +3
@@ -295,60 +395,23 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
         v[4 * h + 3] = __byte_perm(t1, t3, 0x7632);
       }
 #pragma unroll
-      for (u32 p = 0; p < 4; ++p) {
-        if (p >= planes) break;
-        uint8_t* dst = &S.b[st][p][cm_off(n_t, k_t)];
+      for (u32 pl = 0; pl < 4; ++pl) {
+        if (pl >= planes) break;
+        uint8_t* dst = &S.b[st][pl][cm_off(n_t, k_t)];
         if constexpr (KQ == 8)
-          *reinterpret_cast<uint2*>(dst) = make_uint2(v[p], v[4 + p]);
+          *reinterpret_cast<uint2*>(dst) = make_uint2(v[pl], v[4 + pl]);
         else
-          *reinterpret_cast<u32*>(dst) = v[p];
+          *reinterpret_cast<u32*>(dst) = v[pl];
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::);
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.full_b[st]);
+      if constexpr (BATCH) {
+        if (ks == KS - 1) epilogue(p);
+      }
     }
+    if constexpr (!BATCH) epilogue(0);
     asm volatile("cp.async.wait_group 0;\n" ::);
-
-    // ===== epilogue: warp w reads TMEM lanes 32*(w%4).., columns (w/4)*32 .. +32 =====
-    mbar_wait(&S.empty[(KS - 1) % kS], ((KS - 1) / kS) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-    const u32 lg = warp & 3, ch = warp >> 2;
-    const u32 m = mt * kTcM + lg * 32 + lane;
-    const u32 q = P.q;
-    const u64* cs = a.cs[limb];  // 2^(8s) mod q (host)
-    const u32 nacc = 2 * planes - 1;
-    const u32 bv = (a.bias != nullptr && poly == 0 && m < a.M) ? __ldg(&a.bias[static_cast<u64>(limb) * a.Mpad + m]) : 0u;
-#pragma unroll
-    for (u32 cc = 0; cc < TN / 2; cc += 8) {
-      const u32 col = ch * (TN / 2) + cc;
-      u64 acc[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = 0;
-      for (u32 s = 0; s < nacc; ++s) {
-        u32 r[8];
-        const u32 taddr = tmem + ((lg * 32) << 16) + s * TN + col;
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                     : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] += static_cast<u64>(r[i]) * cs[s];
-      }
-      if (m < a.M) {
-        u32 o[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = addmod(reduce64(acc[i], P), bv, q);
-        if constexpr (kWide) {
-          u64* yp = a.Y64 + ((static_cast<u64>(m) * a.polys + poly) * a.y_level + a.limb_off + limb) * a.N + n0 + col;
-#pragma unroll
-          for (int i = 0; i < 8; i += 2) *reinterpret_cast<ulonglong2*>(yp + i) = make_ulonglong2(o[i], o[i + 1]);
-        } else {
-          u32* yp = a.Y + ((static_cast<u64>(m) * a.polys + poly) * a.level + limb) * a.N + n0 + col;
-          *reinterpret_cast<uint4*>(yp) = make_uint4(o[0], o[1], o[2], o[3]);
-          *reinterpret_cast<uint4*>(yp + 4) = make_uint4(o[4], o[5], o[6], o[7]);
-        }
-      }
-    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
   __syncthreads();
@@ -372,7 +435,7 @@ struct TcSmemW {
   uint8_t b[kTcS][kTwP][kTwPlaneB];
   uint8_t zero_a[kTcPlaneA];
   u64 xs[kTcXS][kTcK][kTwN];
-  unsigned long long full_a[kTcS], full_b[kTcS], empty[kTcS];
+  unsigned long long full_a[kTcS], full_b[kTcS], empty[kTcS], acc_full, acc_empty;
   u32 tmem;
 };
 
@@ -396,10 +459,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc_w(MacDenseTcWArg
   extern __shared__ __align__(1024) uint8_t tcw_raw[];
   TcSmemW& S = *reinterpret_cast<TcSmemW*>(tcw_raw);
   const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const u32 mt = blockIdx.x;  // M tiles fastest (see k_mac_dense_tc)
-  const u32 n0 = blockIdx.y * kTwN;
+  // M tiles fastest (see k_mac_dense_tc), then N tiles, then position chunks
+  const u32 ntiles = a.N / kTwN;
+  const u32 mt = blockIdx.x % a.Mtiles;
+  const u32 n0 = ((blockIdx.x / a.Mtiles) % ntiles) * kTwN, pc = blockIdx.x / a.Mtiles / ntiles;
+  const u32 pos0 = pc * a.ppc, NP = min(a.ppc, a.npos - pos0);
   const u32 poly = blockIdx.z;
   const u32 KS = a.Ksteps;
+  const bool resident = KS <= static_cast<u32>(kTcS);  // see k_mac_dense_tc
+  const u32 IT = NP * KS;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_addr(&S.tmem)),
@@ -412,6 +480,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc_w(MacDenseTcWArg
       mbar_init(&S.full_b[i], kTcProducers / 32);
       mbar_init(&S.empty[i], 1);
     }
+    mbar_init(&S.acc_full, 1);
+    mbar_init(&S.acc_empty, kTcProducers / 32);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
   }
   for (u32 i = tid; i < kTcPlaneA / 16; i += kTcThreads) reinterpret_cast<uint4*>(S.zero_a)[i] = make_uint4(0, 0, 0, 0);
@@ -434,17 +504,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc_w(MacDenseTcWArg
                 smem_addr(&S.a[st][0][0])),
             "l"(Wt + static_cast<u64>(j) * kTwP * kTcPlaneA), "r"(bytes), "r"(smem_addr(&S.full_a[st])));
       };
-      for (u32 j = 0; j < kTcS - 1 && j < KS; ++j) load_a(j);
+      if (resident) {
+        for (u32 j = 0; j < KS; ++j) load_a(j);
+      } else {
+        for (u32 j = 0; j < kTcS - 1 && j < KS; ++j) load_a(j);
+      }
       constexpr u32 idesc = (2u << 4) | (((kTwP * kTwN) >> 3) << 17) | ((kTcM >> 4) << 24);
       const u64 zd = umma_desc(smem_addr(&S.zero_a[0]));
-      for (u32 ks = 0; ks < KS; ++ks) {
-        const u32 st = ks % kTcS, use = ks / kTcS;
-        const u32 j = ks + kTcS - 1;
-        if (j < KS) {
-          if (j >= kTcS) mbar_wait(&S.empty[j % kTcS], ((j / kTcS) - 1) & 1);
-          load_a(j);
+      for (u32 it = 0, p = 0, ks = 0; it < IT; ++it, ks = (ks + 1 == KS) ? 0 : ks + 1, p += (ks == 0) ? 1 : 0) {
+        const u32 st = it % kTcS, use = it / kTcS;
+        if (!resident) {  // NP == 1: it == ks
+          const u32 j = ks + kTcS - 1;
+          if (j < KS) {
+            if (j >= kTcS) mbar_wait(&S.empty[j % kTcS], ((j / kTcS) - 1) & 1);
+            load_a(j);
+          }
         }
-        mbar_wait(&S.full_a[st], use & 1);
+        const u32 ast = resident ? ks : st;
+        if (!resident || p == 0) mbar_wait(&S.full_a[ast], resident ? 0u : (use & 1));
+        if (ks == 0 && p > 0) mbar_wait(&S.acc_empty, (p - 1) & 1);
         mbar_wait(&S.full_b[st], use & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
         const u64 bd = umma_desc(smem_addr(&S.b[st][0][0]));
@@ -453,7 +531,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc_w(MacDenseTcWArg
                        "l"(bd), "r"(idesc));
 #pragma unroll
         for (u32 pa = 0; pa < kTwP; ++pa) {
-          const u64 ad = umma_desc(smem_addr(&S.a[st][pa][0]));
+          const u64 ad = umma_desc(smem_addr(&S.a[ast][pa][0]));
           const u32 accum = (ks > 0 || pa > 0) ? 1u : 0u;
           asm volatile(
               "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -462,90 +540,120 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc_w(MacDenseTcWArg
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
             smem_addr(&S.empty[st])));
+        if (ks == KS - 1)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+              smem_addr(&S.acc_full)));
       }
     }
   } else {
     // producers: warp w owns k rows [4w, 4w+4) of every step; lane = column
-    const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
-    const u64* Xb = a.X + (static_cast<u64>(poly) * a.x_level + a.limb) * a.N + n0;
+    const u64 xelem = static_cast<u64>(a.polys) * a.x_level * a.N;
+    const u64 xstride = a.x_kstride * xelem, xpstep = a.x_pstride * xelem;
+    const u64* Xb = a.X + pos0 * xpstep + (static_cast<u64>(poly) * a.x_level + a.limb) * a.N + n0;
     const u32 r0 = warp * 4;
-    auto issue = [&](u32 ks) {
+    u32 ip = 0, iks = 0;  // (position, k step) of the next issue(): called for it = 0, 1, 2, ...
+    auto issue = [&](u32 it) {
+      const u32 p = ip, ks = iks;
+      if (++iks == KS) {
+        iks = 0;
+        ++ip;
+      }
       // 4 rows x 32 residues (u64) = 64 chunks of 16 B, two per lane; rows >= K zero-fill
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const u32 c = lane + i * 32, row = r0 + (c >> 4), c2 = (c & 15) * 2;
         const u32 k = ks * kTcK + row;
-        const u64* src = Xb + static_cast<u64>(k < a.K ? k : 0) * xstride + c2;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(&S.xs[ks % kTcXS][row][c2])),
+        const u64* src = Xb + p * xpstep + static_cast<u64>(k < a.K ? k : 0) * xstride + c2;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(&S.xs[it % kTcXS][row][c2])),
                      "l"(src), "r"(k < a.K ? 16 : 0));
       }
     };
 #pragma unroll 1
     for (u32 j = 0; j < kTcXS - 1; ++j) {
-      if (j < KS) issue(j);
+      if (j < IT) issue(j);
       asm volatile("cp.async.commit_group;\n" ::);
     }
-    for (u32 ks = 0; ks < KS; ++ks) {
-      const u32 st = ks % kTcS, use = ks / kTcS;
+    const u32 lg = warp & 3, ch = warp >> 2;
+    const u32 m = mt * kTcM + lg * 32 + lane;
+    const u64 bv = (a.bias != nullptr && poly == 0 && m < a.M) ? __ldg(&a.bias[m]) : 0ull;
+    for (u32 it = 0, p = 0, ks = 0; it < IT; ++it, ks = (ks + 1 == KS) ? 0 : ks + 1, p += (ks == 0) ? 1 : 0) {
+      const u32 st = it % kTcS, use = it / kTcS;
       asm volatile("cp.async.wait_group %0;\n" ::"n"(kTcXS - 2));
       __syncwarp();
       u64 v[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = S.xs[ks % kTcXS][r0 + i][lane];
+      for (int i = 0; i < 4; ++i) v[i] = S.xs[it % kTcXS][r0 + i][lane];
       __syncwarp();
-      if (ks + kTcXS - 1 < KS) issue(ks + kTcXS - 1);
+      if (it + kTcXS - 1 < IT) issue(it + kTcXS - 1);
       asm volatile("cp.async.commit_group;\n" ::);
-      if (ks >= kTcS) mbar_wait(&S.empty[st], (use - 1) & 1);
+      if (it >= static_cast<u32>(kTcS)) mbar_wait(&S.empty[st], (use - 1) & 1);
 #pragma unroll
-      for (u32 p = 0; p < kTwP; ++p) {
-        const u32 sh = 8 * p;
+      for (u32 pl = 0; pl < kTwP; ++pl) {
+        const u32 sh = 8 * pl;
         const u32 b4 = static_cast<u32>((v[0] >> sh) & 255) | (static_cast<u32>((v[1] >> sh) & 255) << 8) |
                        (static_cast<u32>((v[2] >> sh) & 255) << 16) | (static_cast<u32>((v[3] >> sh) & 255) << 24);
-        *reinterpret_cast<u32*>(&S.b[st][p][cm_off(lane, r0)]) = b4;
+        *reinterpret_cast<u32*>(&S.b[st][pl][cm_off(lane, r0)]) = b4;
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::);
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.full_b[st]);
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::);
+      if (ks != KS - 1) continue;
 
-    // epilogue: warp w reads TMEM lanes 32 (w % 4) .., columns 16 (w / 4) .. + 16
-    mbar_wait(&S.empty[(KS - 1) % kTcS], ((KS - 1) / kTcS) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-    const u32 lg = warp & 3, ch = warp >> 2;
-    const u32 m = mt * kTcM + lg * 32 + lane;
-    const u64 bv = (a.bias != nullptr && poly == 0 && m < a.M) ? __ldg(&a.bias[m]) : 0ull;
+      // epilogue of position pos0 + p: warp w reads TMEM lanes 32 (w % 4) .., columns
+      // 16 (w / 4) .. + 16
+      mbar_wait(&S.acc_full, p & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      const u64 ye = m * a.y_mstride + (pos0 + p) * a.y_pstride;
 #pragma unroll
-    for (u32 cc = 0; cc < 16; cc += 8) {
-      const u32 col = ch * 16 + cc;
-      u64 lo[8], hi[8];
+      for (u32 cc = 0; cc < 16; cc += 8) {
+        const u32 col = ch * 16 + cc;
+        // sum_s D_s (2^(8s) mod q) with the multiplier split at bit 20: D_s < 2^31 and both
+        // halves < 2^20, so each half-sum of 10 terms (diagonal 9 is zero, see k_mac_dense_tc)
+        // stays < 2^55 with one IMAD.WIDE.U32 per term
+        u64 al[8], ah[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) lo[i] = hi[i] = 0;
+        for (int i = 0; i < 8; ++i) al[i] = ah[i] = 0;
 #pragma unroll 1
-      for (u32 s = 0; s < 2 * kTwP - 1; ++s) {
-        u32 r[8];
-        const u32 taddr = tmem + ((lg * 32) << 16) + s * kTwN + col;
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                     : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-        const u64 c = a.cs[s];
+        for (u32 s = 0; s < 2 * kTwP - 1; s += 2) {
+          u32 r[8], r2[8];
+          const u32 taddr = tmem + ((lg * 32) << 16) + s * kTwN + col;
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                       : "r"(taddr));
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                       : "=r"(r2[0]), "=r"(r2[1]), "=r"(r2[2]), "=r"(r2[3]), "=r"(r2[4]), "=r"(r2[5]), "=r"(r2[6]),
+                         "=r"(r2[7])
+                       : "r"(taddr + kTwN));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+          const u64 c = a.cs[s], c2 = a.cs[s + 1];
+          const u32 cl = static_cast<u32>(c & 0xFFFFF), ch_ = static_cast<u32>(c >> 20);
+          const u32 cl2 = static_cast<u32>(c2 & 0xFFFFF), ch2 = static_cast<u32>(c2 >> 20);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const u64 pl = static_cast<u64>(r[i]) * c, ph = __umul64hi(static_cast<u64>(r[i]), c);
-          lo[i] += pl;
-          hi[i] += ph + (lo[i] < pl ? 1 : 0);
+          for (int i = 0; i < 8; ++i) {
+            al[i] += static_cast<u64>(r[i]) * cl + static_cast<u64>(r2[i]) * cl2;
+            ah[i] += static_cast<u64>(r[i]) * ch_ + static_cast<u64>(r2[i]) * ch2;
+          }
+        }
+        if (m < a.M) {
+          u64 o[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const u64 lo = al[i] + (ah[i] << 20);
+            const u64 hi = (ah[i] >> 44) + (lo < al[i] ? 1 : 0);
+            o[i] = addmod_w(barrett128(lo, hi, P), bv, P.q);
+          }
+          u64* yp = a.Y + ((ye * a.polys + poly) * a.level + a.limb) * a.N + n0 + col;
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) *reinterpret_cast<ulonglong2*>(yp + i) = make_ulonglong2(o[i], o[i + 1]);
         }
       }
-      if (m < a.M) {
-        u64 o[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = addmod_w(barrett128(lo[i], hi[i], P), bv, P.q);
-        u64* yp = a.Y + ((static_cast<u64>(m) * a.polys + poly) * a.level + a.limb) * a.N + n0 + col;
-#pragma unroll
-        for (int i = 0; i < 8; i += 2) *reinterpret_cast<ulonglong2*>(yp + i) = make_ulonglong2(o[i], o[i + 1]);
+      if (p + 1 < NP) {
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.acc_empty);
       }
     }
+    asm volatile("cp.async.wait_group 0;\n" ::);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
   __syncthreads();
@@ -621,6 +729,16 @@ double bench_tc_i8_peak(int device) {
 // ---------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------
+// Positions per CTA of a batched contraction with resident weights (HG_TC_PPC, default 16).
+static u32 tc_positions_per_cta() {
+  static const u32 v = [] {
+    const char* e = getenv("HG_TC_PPC");
+    const int x = e ? atoi(e) : 16;
+    return static_cast<u32>(x < 1 ? 1 : x);
+  }();
+  return v;
+}
+
 u64 tc_packed_weight_bytes(u32 K, u32 M, u32 level) {
   const u32 Mtiles = (M + kTcM - 1) / kTcM, Ksteps = (K + kTcK - 1) / kTcK;
   return static_cast<u64>(level) * Mtiles * Ksteps * 4 * kTcPlaneA;
@@ -651,46 +769,69 @@ int launch_mac_dense_tc_w(MacDenseTcWArgs a, const void* P, cudaStream_t s) {
   a.Mtiles = (a.M + kTcM - 1) / kTcM;
   a.Ksteps = (a.K + kTcK - 1) / kTcK;
   if (a.N % kTwN != 0 || a.K > 6605 || a.K == 0) return -1;  // 5 K 255^2 < 2^31
+  if (a.npos == 0) a.npos = 1;
+  if (a.x_kstride == 0) a.x_kstride = 1;
+  if (a.y_mstride == 0) a.y_mstride = 1;
+  a.ppc = a.Ksteps <= static_cast<u32>(kTcS) ? std::min(a.npos, tc_positions_per_cta()) : 1u;
+  const u64 ctas = static_cast<u64>(a.Mtiles) * (a.N / kTwN) * ((a.npos + a.ppc - 1) / a.ppc);
+  if (ctas >= (1ull << 31)) return -1;
   constexpr size_t smem = sizeof(TcSmemW) > 120 * 1024 ? sizeof(TcSmemW) : 120 * 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_mac_dense_tc_w, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
-  dim3 grid(a.Mtiles, a.N / kTwN, a.polys);
+  dim3 grid(static_cast<u32>(ctas), 1, a.polys);
   ProfScope ps("k_mac_dense_tc_w", s);
   k_mac_dense_tc_w<<<grid, kTcThreads, smem, s>>>(a, *static_cast<const DevPrimeW*>(P));
   return 1;
 }
 
-template <int TN, typename XW>
-static void tc_launch(const MacDenseTcArgs& a, const Basis& B, cudaStream_t s) {
+template <int TN, typename XW, bool BATCH>
+static void tc_launch_k(const MacDenseTcArgs& a, const Basis& B, cudaStream_t s) {
   // TN = 64: request enough shared memory that only one CTA is resident per SM (512 TMEM
-  // columns), so no CTA spins in tcgen05.alloc; TN = 32: two CTAs of 256 columns (one with
-  // u64 inputs, whose staging ring is twice the size).
+  // columns), so no CTA spins in tcgen05.alloc; TN = 32: two CTAs of 256 columns.
   constexpr size_t smem = TN == 64 ? (sizeof(TcSmem<TN, XW>) > 120 * 1024 ? sizeof(TcSmem<TN, XW>) : 120 * 1024)
                                    : sizeof(TcSmem<TN, XW>);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_mac_dense_tc<TN, XW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_mac_dense_tc<TN, XW, BATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
     attr = true;
   }
-  dim3 grid(a.Mtiles, a.N / TN, a.polys * a.level);
+  dim3 grid(a.Mtiles * (a.N / TN) * ((a.npos + a.ppc - 1) / a.ppc), 1, a.polys * a.level);
   ProfScope ps("k_mac_dense_tc", s);
-  k_mac_dense_tc<TN, XW><<<grid, kTcThreads, smem, s>>>(a, B);
+  k_mac_dense_tc<TN, XW, BATCH><<<grid, kTcThreads, smem, s>>>(a, B);
+}
+
+template <int TN, typename XW>
+static void tc_launch(MacDenseTcArgs a, const Basis& B, cudaStream_t s) {
+  a.ppc = a.Ksteps <= static_cast<u32>(tc_stages<TN>()) ? std::min(a.npos, tc_positions_per_cta()) : 1u;
+  if constexpr (TN == 32) {  // batched contractions have small K (the N = 32 tile)
+    if (a.ppc > 1) {
+      tc_launch_k<TN, XW, true>(a, B, s);
+      return;
+    }
+  }
+  tc_launch_k<TN, XW, false>(a, B, s);
 }
 
 int launch_mac_dense_tc(MacDenseTcArgs a, const Basis& B, cudaStream_t s) {
   a.Mtiles = (a.M + kTcM - 1) / kTcM;
   a.Ksteps = (a.K + kTcK - 1) / kTcK;
   if (a.N % 64 != 0 || a.K > 8192 || a.K == 0) return -1;
+  if (a.npos == 0) a.npos = 1;
+  if (a.x_kstride == 0) a.x_kstride = 1;
+  if (a.y_mstride == 0) a.y_mstride = 1;
+  if (static_cast<u64>(a.Mtiles) * (a.N / 32) * a.npos >= (1ull << 31)) return -1;
   for (u32 l = 0; l < a.level; ++l) {
     const u64 q = B.p[l].q;
     u64 c = 1;
     for (int i = 0; i < 7; ++i) {
-      a.cs[l][i] = c;
+      a.cs[l][i] = static_cast<u32>(c);
       c = (c << 8) % q;
     }
+    a.cs[l][7] = 0;
   }
   // short contractions are dominated by per-CTA prologue/epilogue: two CTAs per SM overlap them
   static const int tn_env = [] {

@@ -23,7 +23,13 @@ struct MacDenseTcArgs {
   u64* Y64;
   u32 limb_off, y_level;
   u32 planes[kMaxPrimes];  // byte planes per limb: 3 if q < 2^24 else 4
-  u64 cs[kMaxPrimes][7];   // 2^(8s) mod q per limb (filled by the launcher)
+  u32 cs[kMaxPrimes][8];   // 2^(8s) mod q per limb, s < 7, and 0 (filled by the launcher)
+  // Batched contraction (a 1x1, stride-1 convolution: one Dot per output position): npos
+  // positions; input k of position p is element k * x_kstride + p * x_pstride of X, output m
+  // is element m * y_mstride + p * y_pstride of Y.  Zeros mean a plain Dot (1, 1, 0, 0).
+  u32 npos;
+  u64 x_kstride, x_pstride, y_mstride, y_pstride;
+  u32 ppc;  // positions per CTA (filled by the launcher)
 };
 
 // One limb with a prime in [2^30, 2^40) (BASELINE c4/c5b limb 0), u64 residues: 5 byte
@@ -35,7 +41,10 @@ struct MacDenseTcWArgs {
   const u64* bias;       // [Mpad] of this limb or nullptr
   u32 K, M, Mpad, N, level, polys, x_level, limb;
   u32 Mtiles, Ksteps;    // filled by the launcher
-  u64 cs[9];             // 2^(8s) mod q
+  u64 cs[10];            // 2^(8s) mod q, s < 9, and 0
+  u32 npos;              // batched positions, as in MacDenseTcArgs
+  u64 x_kstride, x_pstride, y_mstride, y_pstride;
+  u32 ppc;               // positions per CTA (filled by the launcher)
 };
 
 u64 tc_packed_weight_bytes(u32 K, u32 M, u32 level);

@@ -204,8 +204,14 @@ __global__ void __launch_bounds__(128) k_mac_conv_w(MacConvArgsW a, BasisW B) {
   const u32 pos = blockIdx.y;
   const u32 oy = pos / a.OW, ox = pos % a.OW;
   const u32 nchunks = (a.F + kWFT - 1) / kWFT;
-  const u32 pl = blockIdx.z / nchunks;
-  const u32 f0 = (blockIdx.z % nchunks) * kWFT;
+  const u32 per_group = a.polys * a.level * nchunks;
+  const u32 g = blockIdx.z / per_group, zz = blockIdx.z % per_group;
+  a.X += g * a.gx;
+  a.Y += g * a.gy;
+  a.W += g * a.gw;
+  if (a.bias != nullptr) a.bias += g * a.gb;
+  const u32 pl = zz / nchunks;
+  const u32 f0 = (zz % nchunks) * kWFT;
   const u32 poly = pl / a.level, limb = pl % a.level;
   const DevPrimeW& P = B.p[limb];
   const u32 n = (blockIdx.x * blockDim.x + tid) * 2;
@@ -605,7 +611,9 @@ int launch_limbs_to_u64(const u32* in, u64* out, u64 rows, u32 Lw, u32 lo, u32 c
 int launch_mac_conv_w(const MacConvArgsW& a, const BasisW& B, cudaStream_t s) {
   if (a.C * a.win * a.win > static_cast<u32>(kWMaxTaps) || a.N % 256 != 0) return -1;
   const u32 nchunks = (a.F + kWFT - 1) / kWFT;
-  dim3 grid(a.N / 256, a.OH * a.OW, a.polys * a.level * nchunks);
+  const u32 groups = a.groups ? a.groups : 1;
+  if (static_cast<u64>(a.polys) * a.level * nchunks * groups > 65535) return -1;
+  dim3 grid(a.N / 256, a.OH * a.OW, a.polys * a.level * nchunks * groups);
   { ProfScope ps_("k_mac_conv_w", s);
   k_mac_conv_w<<<grid, 128, 0, s>>>(a, B);
   }

@@ -61,6 +61,11 @@ struct MacConvArgsW {
   u32 C, IH, IW, F, OH, OW, win, stride, pad_top, pad_left;
   u32 level, polys, x_level, N;
   uint8_t fold[kMaxPrimes];  // 1: taps (q-1)^2 may overflow 128 bits -> reduce every 8 taps
+  // groups > 1: independent convolutions in one launch (a depthwise layer: one 1 -> 1
+  // convolution per channel); group g reads X + g * gx, W + g * gw, bias + g * gb and writes
+  // Y + g * gy (words)
+  u32 groups;
+  u64 gx, gy, gw, gb;
 };
 
 struct EwArgsW {

@@ -45,6 +45,10 @@ CASES = [
     (3, 8, 8, 8, 5, 1, (2, 2, 2, 2), 6, True, False),      # 75 taps: 3 k steps, N = 32 on every limb
     (8, 6, 7, 3, 5, 3, (0, 2, 1, 0), 6, False, False),     # 200 taps: 7 k steps, stride 3, ragged
     (2, 5, 5, 6, 3, 2, (1, 0, 0, 1), 6, True, True),       # all (q-1) residues
+    # 1x1, stride 1, unpadded: the batched tensor-core Dot (positions as columns)
+    (16, 5, 6, 24, 1, 1, (0, 0, 0, 0), 6, True, False),    # MobileNetV2 project-like, ragged 5x6
+    (40, 3, 4, 130, 1, 1, (0, 0, 0, 0), 6, True, True),    # 2 k steps, 2 M tiles, all (q-1)
+    (4, 6, 6, 3, 1, 2, (0, 0, 0, 0), 6, False, False),     # 1x1 stride 2: tap-gather kernel
 ]
 
 

@@ -9,6 +9,8 @@ runs in its own subprocess and compares with the reference (oracle/_ref).
   HG_AUX_STREAM=0 special-prime key switch on the main stream
   HG_UPLOAD_HOST_NARROW=0  hg_tensor_upload copies u64 words and narrows them on the GPU
   HG_UPLOAD_DIRECT_FRAC=0 / 1  host packing only / everything raw through the GPU narrowing
+  HG_CONV1X1_DOT=0  1x1 convolutions on the tap-gather kernel instead of the batched Dot
+  HG_TC_PPC=3     3 positions per CTA in the batched Dot (ragged last chunk)
 """
 import os
 import subprocess
@@ -30,7 +32,7 @@ def run(p, wl, seed, keys_relin):
     ctx = H.CkksContext(p["n"], p["chain"], p["special"], p["scale"])
     ref = R.RefContext(p["n"], p["chain"], p["special"], p["scale"])
     keys = ref.keygen(5, keys_relin)
-    if wl.name.startswith("c5b"):
+    if wl.name.startswith("c5b") or wl.name.startswith("c4"):
         x = W.random_ciphertexts(p, wl.input_count, seed=seed)
         sc = p["scale"]
     else:
@@ -50,9 +52,22 @@ def run(p, wl, seed, keys_relin):
     assert out.scale == want_sc, (out.scale, want_sc)
     assert np.array_equal(out.to_words(), want)
 
+def c4_linear():
+    # the c4 block's linear layers (1x1 expand, 3x3 depthwise pad 1, 1x1 project), ReLU6 removed
+    import json
+    wl = W.mobilenet_block(hw=4, cin=4, expand=6, cout=3)
+    j = json.loads(wl.manifest)
+    j["nodes"] = [n for n in j["nodes"] if n["op"] != "Relu"]
+    for n in j["nodes"]:
+        n["inputs"] = [{"relu6a": "expand", "relu6b": "dw"}.get(i, i) for i in n.get("inputs", [])]
+    wl.manifest = json.dumps(j)
+    return wl
+
 which = sys.argv[2]
 if which == "toy":
     run(W.N8192, W.toy_cryptonets(), 3, True)
+elif which == "c4lin":
+    run(W.N16384, c4_linear(), 5, False)
 else:
     run(W.N16384, W.wide_dense(k=96, m=40), 4, False)
 print("OK")
@@ -68,6 +83,10 @@ print("OK")
     ({"HG_UPLOAD_DIRECT_FRAC": "1"}, "toy"),
     ({"HG_WIDE_TC": "0"}, "wide"),
     ({"HG_DENSE_TC": "0"}, "wide"),
+    ({"HG_CONV1X1_DOT": "0"}, "c4lin"),
+    ({"HG_WIDE_TC": "0"}, "c4lin"),
+    ({"HG_TC_PPC": "3"}, "c4lin"),
+    ({}, "c4lin"),
 ])
 def test_alternate_paths_bit_exact(env, which):
     r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, which], env={**os.environ, **env},
