@@ -324,6 +324,7 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
       W.w1n_sh = sh64(W.w1n);
       W.t64 = r1;
     }
+    ctx->basisw.narrow = &ctx->basis;  // the u32 tables of the limbs below 2^30 (launch_ntt_w)
     ctx->wide_tables = ctx->alloc(tw.size() * sizeof(ulonglong2), nullptr);
     cuda_check(cudaMemcpyAsync(ctx->wide_tables->ptr, tw.data(), tw.size() * sizeof(ulonglong2),
                                cudaMemcpyHostToDevice, ctx->core->stream),

@@ -11,14 +11,16 @@ namespace hg {
 // ---------------------------------------------------------------------------
 // Batched NTT / INTT
 // ---------------------------------------------------------------------------
+// Limbs [lo, lo + cnt) of every row of `level` limbs; one CTA per (row, limb).
 template <int LOGN, bool INV>
-__global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_ntt_w(u64* data, u32 level, BasisW B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_ntt_w(u64* data, u32 level, u32 lo, u32 cnt, BasisW B) {
   using NT = NttW<LOGN>;
   extern __shared__ u64 smw[];
   const u32 tid = threadIdx.x;
-  const u64 row = blockIdx.x;
-  const DevPrimeW& P = B.p[row % level];
-  u64* r = data + row * NT::N;
+  const u64 ct = blockIdx.x / cnt;
+  const u32 limb = lo + blockIdx.x % cnt;
+  const DevPrimeW& P = B.p[limb];
+  u64* r = data + (ct * level + limb) * NT::N;
   u64 x[32];
   if (!INV) {
     NT::gload_A(x, r, tid);
@@ -28,6 +30,46 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_ntt_w(u64* data, u32 lev
     NT::gload_C(x, r, tid);
     NT::inverse(x, smw, tid, P);
     NT::gstore_A(x, r, tid);
+  }
+}
+
+// The limbs below 2^30 of a wide tensor on the u32 transform (Ntt<>, one Shoup product per
+// butterfly on 32-bit words instead of the 64-bit Shoup of NttW): residues are narrowed on
+// load and widened on store, in place.  Limbs [lo, level) of every row.
+template <int LOGN, bool INV>
+__global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_ntt_w32(u64* data, u32 level, u32 lo, Basis B) {
+  using NT = Ntt<LOGN, true>;
+  extern __shared__ u32 sm32[];
+  const u32 tid = threadIdx.x;
+  const u32 cnt = level - lo;
+  const u64 ct = blockIdx.x / cnt;
+  const u32 limb = lo + blockIdx.x % cnt;
+  const DevPrime& P = B.p[limb];
+  u64* r = data + (ct * level + limb) * NT::N;
+  u32 x[32];
+  if (!INV) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) x[k] = static_cast<u32>(__ldg(&r[NT::jA(tid, k)]));
+    NT::forward(x, sm32, tid, P);
+#pragma unroll
+    for (int k = 0; k < 32; k += 4) {
+      ulonglong2* o = reinterpret_cast<ulonglong2*>(r + NT::jC(tid, k));
+      o[0] = make_ulonglong2(x[k], x[k + 1]);
+      o[1] = make_ulonglong2(x[k + 2], x[k + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 32; k += 4) {
+      const ulonglong2* in = reinterpret_cast<const ulonglong2*>(r + NT::jC(tid, k));
+      const ulonglong2 a = __ldg(in), b = __ldg(in + 1);
+      x[k] = static_cast<u32>(a.x);
+      x[k + 1] = static_cast<u32>(a.y);
+      x[k + 2] = static_cast<u32>(b.x);
+      x[k + 3] = static_cast<u32>(b.y);
+    }
+    NT::inverse(x, sm32, tid, P);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) r[NT::jA(tid, k)] = x[k];
   }
 }
 
@@ -510,21 +552,35 @@ static void set_smem_w(K kernel, size_t bytes) {
 
 int launch_ntt_w(int logn, u64* data, u64 rows, u32 level, bool inverse, const BasisW& B, cudaStream_t s) {
   if (rows == 0) return 0;
+  // limbs [lo, level) below 2^30 go to the u32 transform (HG_NTT_W32=0: all on the u64 one)
+  static const bool w32 = [] {
+    const char* e = getenv("HG_NTT_W32");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  u32 lo = level;
+  if (w32 && B.narrow != nullptr)
+    while (lo > 0 && B.p[lo - 1].q < (1ull << 30)) --lo;
+  const u64 count = rows / level;
+  int launches = 0;
   HG_LOGN_SWITCH_W(logn, {
-    const size_t sm = sizeof(u64) * NttW<LN>::SMEM_WORDS;
-    if (inverse) {
-      set_smem_w(k_ntt_w<LN, true>, sm);
-      { ProfScope ps_("k_ntt_w", s);
-      k_ntt_w<LN, true><<<rows, 1 << (LN - 5), sm, s>>>(data, level, B);
-      }
-    } else {
-      set_smem_w(k_ntt_w<LN, false>, sm);
-      { ProfScope ps_("k_ntt_w", s);
-      k_ntt_w<LN, false><<<rows, 1 << (LN - 5), sm, s>>>(data, level, B);
-      }
+    if (lo > 0) {
+      const size_t sm = sizeof(u64) * NttW<LN>::SMEM_WORDS;
+      auto k = inverse ? k_ntt_w<LN, true> : k_ntt_w<LN, false>;
+      set_smem_w(k, sm);
+      ProfScope ps_("k_ntt_w", s);
+      k<<<count * lo, 1 << (LN - 5), sm, s>>>(data, level, 0, lo, B);
+      ++launches;
+    }
+    if (lo < level) {
+      const size_t sm = sizeof(u32) * Ntt<LN, true>::SMEM_WORDS;
+      auto k = inverse ? k_ntt_w32<LN, true> : k_ntt_w32<LN, false>;
+      set_smem_w(k, sm);
+      ProfScope ps_("k_ntt_w32", s);
+      k<<<count * (level - lo), 1 << (LN - 5), sm, s>>>(data, level, lo, *static_cast<const Basis*>(B.narrow));
+      ++launches;
     }
   });
-  return 1;
+  return launches;
 }
 
 int launch_rescale_w(int logn, const RescaleArgsW& a, const BasisW& B, cudaStream_t s) {

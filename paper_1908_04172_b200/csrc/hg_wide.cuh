@@ -24,6 +24,9 @@ struct DevPrimeW {
 
 struct BasisW {
   DevPrimeW p[kMaxPrimes];
+  // Host pointer to the context's u32 Basis (Ntt<> tables for every prime < 2^32): launchers
+  // run the limbs below 2^30 on the u32 transforms with u64 I/O.  Not read on the device.
+  const void* narrow;
 };
 
 __device__ __forceinline__ u64 csub64(u64 x, u64 q) { return x >= q ? x - q : x; }
