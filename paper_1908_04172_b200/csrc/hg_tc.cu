@@ -83,6 +83,15 @@ struct TcSmem {
 template <int TN>
 constexpr u32 tc_cols() { return TN == 64 ? 512u : 256u; }
 
+// tcgen05.ld .16x256b.x1: 16 TMEM lanes x 8 columns; thread t receives lane t/4 (r[0..1]) and
+// lane t/4 + 8 (r[2..3]), columns 2 (t % 4) and 2 (t % 4) + 1 (the mma C-fragment layout), so
+// the 4 threads of a lane hold 8 consecutive columns: 64 contiguous bytes of a u64 output row.
+__device__ __forceinline__ void tmem_ld_16x256b(u32 taddr, u32 (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+
 __device__ __forceinline__ u32 smem_addr(const void* p) { return static_cast<u32>(__cvta_generic_to_shared(p)); }
 
 __device__ __forceinline__ u64 umma_desc(u32 saddr) {
@@ -319,40 +328,80 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
     auto epilogue = [&](u32 p) {
       mbar_wait(&S.acc_full, p & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-      const u64 ye = m * a.y_mstride + (pos0 + p) * a.y_pstride;  // output element
+      // two diagonals per TMEM wait; diagonal 2 planes - 1 (read when nacc is odd) is zeroed by
+      // the ks == 0 MMA and never accumulated.  D_s < 2^31 and 2^(8s) mod q < 2^30: one
+      // IMAD.WIDE.U32 per term, the sum of 8 stays < 2^64.
+      if constexpr (kWide) {
+        // u64 outputs: rows lane/4 + {0, 8, 16, 24} of the warp's quarter, column pairs, so a
+        // store instruction writes 8 rows x 64 contiguous bytes (16x256b TMEM loads)
+        const u32 rb = mt * kTcM + lg * 32 + (lane >> 2), cp2 = 2 * (lane & 3);
+        u64 bvr[4];
 #pragma unroll
-      for (u32 cc = 0; cc < TN / 2; cc += 8) {
-        const u32 col = ch * (TN / 2) + cc;
-        u64 acc[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = 0;
-        // two diagonals per TMEM wait; diagonal 2 planes - 1 (read when nacc is odd) is
-        // zeroed by the ks == 0 MMA and never accumulated.  D_s < 2^31 and 2^(8s) mod q < 2^30:
-        // one IMAD.WIDE.U32 per term, the sum of 8 stays < 2^64.
-        for (u32 s = 0; s < nacc; s += 2) {
-          u32 r[8], r2[8];
-          const u32 taddr = tmem + ((lg * 32) << 16) + s * TN + col;
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                       : "r"(taddr));
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                       : "=r"(r2[0]), "=r"(r2[1]), "=r"(r2[2]), "=r"(r2[3]), "=r"(r2[4]), "=r"(r2[5]), "=r"(r2[6]),
-                         "=r"(r2[7])
-                       : "r"(taddr + TN));
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-          const u32 c0 = cs[s], c1 = cs[s + 1];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i] += static_cast<u64>(r[i]) * c0 + static_cast<u64>(r2[i]) * c1;
+        for (int i = 0; i < 4; ++i) {
+          const u32 mi = rb + 8 * i;
+          bvr[i] = (a.bias != nullptr && poly == 0 && mi < a.M) ? __ldg(&a.bias[static_cast<u64>(limb) * a.Mpad + mi]) : 0u;
         }
-        if (m < a.M) {
-          u32 o[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) o[i] = addmod(reduce64(acc[i], P), bv, q);
-          if constexpr (kWide) {
-            u64* yp = a.Y64 + ((ye * a.polys + poly) * a.y_level + a.limb_off + limb) * a.N + n0 + col;
+        for (u32 cc = 0; cc < TN / 2; cc += 8) {
+          const u32 col = ch * (TN / 2) + cc;
+          u64 acc[4][2];
 #pragma unroll
-            for (int i = 0; i < 8; i += 2) *reinterpret_cast<ulonglong2*>(yp + i) = make_ulonglong2(o[i], o[i + 1]);
-          } else {
+          for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0;
+          for (u32 s = 0; s < nacc; s += 2) {
+            u32 ra[4], rb2[4], rc[4], rd[4];
+            const u32 t0 = tmem + ((lg * 32) << 16) + s * TN + col, t1 = t0 + (16u << 16);
+            tmem_ld_16x256b(t0, ra);
+            tmem_ld_16x256b(t1, rb2);
+            tmem_ld_16x256b(t0 + TN, rc);
+            tmem_ld_16x256b(t1 + TN, rd);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+            const u32 c0 = cs[s], c1 = cs[s + 1];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              acc[0][j] += static_cast<u64>(ra[j]) * c0 + static_cast<u64>(rc[j]) * c1;
+              acc[1][j] += static_cast<u64>(ra[2 + j]) * c0 + static_cast<u64>(rc[2 + j]) * c1;
+              acc[2][j] += static_cast<u64>(rb2[j]) * c0 + static_cast<u64>(rd[j]) * c1;
+              acc[3][j] += static_cast<u64>(rb2[2 + j]) * c0 + static_cast<u64>(rd[2 + j]) * c1;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const u32 mi = rb + 8 * i;
+            if (mi >= a.M) continue;
+            const u64 yei = mi * a.y_mstride + (pos0 + p) * a.y_pstride;
+            u64* yp = a.Y64 + ((yei * a.polys + poly) * a.y_level + a.limb_off + limb) * a.N + n0 + col + cp2;
+            *reinterpret_cast<ulonglong2*>(yp) =
+                make_ulonglong2(addmod(reduce64(acc[i][0], P), static_cast<u32>(bvr[i]), q),
+                                addmod(reduce64(acc[i][1], P), static_cast<u32>(bvr[i]), q));
+          }
+        }
+      } else {
+        const u64 ye = m * a.y_mstride + (pos0 + p) * a.y_pstride;  // output element
+#pragma unroll
+        for (u32 cc = 0; cc < TN / 2; cc += 8) {
+          const u32 col = ch * (TN / 2) + cc;
+          u64 acc[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = 0;
+          for (u32 s = 0; s < nacc; s += 2) {
+            u32 r[8], r2[8];
+            const u32 taddr = tmem + ((lg * 32) << 16) + s * TN + col;
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                         : "r"(taddr));
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                         : "=r"(r2[0]), "=r"(r2[1]), "=r"(r2[2]), "=r"(r2[3]), "=r"(r2[4]), "=r"(r2[5]), "=r"(r2[6]),
+                           "=r"(r2[7])
+                         : "r"(taddr + TN));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+            const u32 c0 = cs[s], c1 = cs[s + 1];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] += static_cast<u64>(r[i]) * c0 + static_cast<u64>(r2[i]) * c1;
+          }
+          if (m < a.M) {
+            u32 o[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = addmod(reduce64(acc[i], P), bv, q);
             u32* yp = a.Y + ((ye * a.polys + poly) * a.level + limb) * a.N + n0 + col;
             *reinterpret_cast<uint4*>(yp) = make_uint4(o[0], o[1], o[2], o[3]);
             *reinterpret_cast<uint4*>(yp + 4) = make_uint4(o[4], o[5], o[6], o[7]);
@@ -574,8 +623,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc_w(MacDenseTcWArg
       asm volatile("cp.async.commit_group;\n" ::);
     }
     const u32 lg = warp & 3, ch = warp >> 2;
-    const u32 m = mt * kTcM + lg * 32 + lane;
-    const u64 bv = (a.bias != nullptr && poly == 0 && m < a.M) ? __ldg(&a.bias[m]) : 0ull;
     for (u32 it = 0, p = 0, ks = 0; it < IT; ++it, ks = (ks + 1 == KS) ? 0 : ks + 1, p += (ks == 0) ? 1 : 0) {
       const u32 st = it % kTcS, use = it / kTcS;
       asm volatile("cp.async.wait_group %0;\n" ::"n"(kTcXS - 2));
@@ -600,51 +647,57 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc_w(MacDenseTcWArg
       if (ks != KS - 1) continue;
 
       // epilogue of position pos0 + p: warp w reads TMEM lanes 32 (w % 4) .., columns
-      // 16 (w / 4) .. + 16
+      // 16 (w / 4) .. + 16, as 16x256b loads: rows lane/4 + {0, 8, 16, 24}, column pairs, so a
+      // store instruction writes 8 rows x 64 contiguous bytes
       mbar_wait(&S.acc_full, p & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-      const u64 ye = m * a.y_mstride + (pos0 + p) * a.y_pstride;
+      const u32 rb = mt * kTcM + lg * 32 + (lane >> 2), cp2 = 2 * (lane & 3);
 #pragma unroll
       for (u32 cc = 0; cc < 16; cc += 8) {
         const u32 col = ch * 16 + cc;
         // sum_s D_s (2^(8s) mod q) with the multiplier split at bit 20: D_s < 2^31 and both
         // halves < 2^20, so each half-sum of 10 terms (diagonal 9 is zero, see k_mac_dense_tc)
         // stays < 2^55 with one IMAD.WIDE.U32 per term
-        u64 al[8], ah[8];
+        u64 al[4][2], ah[4][2];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) al[i] = ah[i] = 0;
+        for (int i = 0; i < 4; ++i) al[i][0] = al[i][1] = ah[i][0] = ah[i][1] = 0;
 #pragma unroll 1
         for (u32 s = 0; s < 2 * kTwP - 1; s += 2) {
-          u32 r[8], r2[8];
-          const u32 taddr = tmem + ((lg * 32) << 16) + s * kTwN + col;
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                       : "r"(taddr));
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                       : "=r"(r2[0]), "=r"(r2[1]), "=r"(r2[2]), "=r"(r2[3]), "=r"(r2[4]), "=r"(r2[5]), "=r"(r2[6]),
-                         "=r"(r2[7])
-                       : "r"(taddr + kTwN));
+          u32 ra[4], rb2[4], rc[4], rd[4];
+          const u32 t0 = tmem + ((lg * 32) << 16) + s * kTwN + col, t1 = t0 + (16u << 16);
+          tmem_ld_16x256b(t0, ra);
+          tmem_ld_16x256b(t1, rb2);
+          tmem_ld_16x256b(t0 + kTwN, rc);
+          tmem_ld_16x256b(t1 + kTwN, rd);
           asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
           const u64 c = a.cs[s], c2 = a.cs[s + 1];
-          const u32 cl = static_cast<u32>(c & 0xFFFFF), ch_ = static_cast<u32>(c >> 20);
+          const u32 cl = static_cast<u32>(c & 0xFFFFF), chh = static_cast<u32>(c >> 20);
           const u32 cl2 = static_cast<u32>(c2 & 0xFFFFF), ch2 = static_cast<u32>(c2 >> 20);
+          const u32* d1[4] = {ra, ra + 2, rb2, rb2 + 2};
+          const u32* d2[4] = {rc, rc + 2, rd, rd + 2};
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            al[i] += static_cast<u64>(r[i]) * cl + static_cast<u64>(r2[i]) * cl2;
-            ah[i] += static_cast<u64>(r[i]) * ch_ + static_cast<u64>(r2[i]) * ch2;
-          }
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              al[i][j] += static_cast<u64>(d1[i][j]) * cl + static_cast<u64>(d2[i][j]) * cl2;
+              ah[i][j] += static_cast<u64>(d1[i][j]) * chh + static_cast<u64>(d2[i][j]) * ch2;
+            }
         }
-        if (m < a.M) {
-          u64 o[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const u64 lo = al[i] + (ah[i] << 20);
-            const u64 hi = (ah[i] >> 44) + (lo < al[i] ? 1 : 0);
-            o[i] = addmod_w(barrett128(lo, hi, P), bv, P.q);
+        for (int i = 0; i < 4; ++i) {
+          const u32 mi = rb + 8 * i;
+          if (mi >= a.M) continue;
+          const u64 bvi = (a.bias != nullptr && poly == 0) ? __ldg(&a.bias[mi]) : 0ull;
+          u64 o[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const u64 lo = al[i][j] + (ah[i][j] << 20);
+            const u64 hi = (ah[i][j] >> 44) + (lo < al[i][j] ? 1 : 0);
+            o[j] = addmod_w(barrett128(lo, hi, P), bvi, P.q);
           }
-          u64* yp = a.Y + ((ye * a.polys + poly) * a.level + a.limb) * a.N + n0 + col;
-#pragma unroll
-          for (int i = 0; i < 8; i += 2) *reinterpret_cast<ulonglong2*>(yp + i) = make_ulonglong2(o[i], o[i + 1]);
+          const u64 ye = mi * a.y_mstride + (pos0 + p) * a.y_pstride;
+          u64* yp = a.Y + ((ye * a.polys + poly) * a.level + a.limb) * a.N + n0 + col + cp2;
+          *reinterpret_cast<ulonglong2*>(yp) = make_ulonglong2(o[0], o[1]);
         }
       }
       if (p + 1 < NP) {

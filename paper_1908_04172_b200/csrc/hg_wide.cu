@@ -326,6 +326,82 @@ __global__ void __launch_bounds__(128) k_mac_conv_w(MacConvArgsW a, BasisW B) {
       store(f, barrett128(acc[f][0].lo, acc[f][0].hi, P), barrett128(acc[f][1].lo, acc[f][1].hi, P));
 }
 
+// Grouped 1 -> 1 convolutions (a depthwise layer, MacConvArgsW::groups = C, C = F = 1 per
+// group): one thread per (group, poly, limb, coefficient pair) walks every output position,
+// so its window weights are loaded once and the overlapping windows of neighbouring outputs
+// are re-read from L1 -- instead of one 128-thread CTA per (position, slice) with nine loads
+// each (the tap-gather k_mac_conv_w).  Same sums: taps in (ky, kx) order, padding skipped,
+// 30-bit limbs as u64 IMAD.WIDE sums folded every 8 taps, wider limbs in 128 bits.
+// WIN: the window (3 for MobileNetV2), compile-time so the taps unroll with their
+// row/column validity tests hoisted out of the tap loop.
+template <int WIN>
+__global__ void __launch_bounds__(128) k_dwconv_w(MacConvArgsW a, BasisW B) {
+  constexpr int T2 = WIN * WIN;
+  const u32 g = blockIdx.z;
+  const u32 poly = blockIdx.y / a.level, limb = blockIdx.y % a.level;
+  const u32 n = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (n >= a.N) return;
+  const DevPrimeW& P = B.p[limb];
+  const u64* X = a.X + g * a.gx + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n;
+  const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;  // words per input element
+  u64* Y = a.Y + g * a.gy + (static_cast<u64>(poly) * a.level + limb) * a.N + n;
+  const u64 ystride = static_cast<u64>(a.polys) * a.level * a.N;
+  u64 w[T2];
+#pragma unroll
+  for (int t = 0; t < T2; ++t) w[t] = __ldg(&a.W[g * a.gw + limb * T2 + t]);
+  const u64 bv = (a.bias != nullptr && poly == 0) ? __ldg(&a.bias[g * a.gb + limb]) : 0;
+  const bool narrow = P.q < (1ull << 30);
+  const u64 r32 = narrow ? (1ull << 32) % P.q : 0;
+  const bool fold = a.fold[limb] != 0;
+  for (u32 oy = 0; oy < a.OH; ++oy) {
+    const int iy0 = static_cast<int>(oy * a.stride) - static_cast<int>(a.pad_top);
+    for (u32 ox = 0; ox < a.OW; ++ox) {
+      const int ix0 = static_cast<int>(ox * a.stride) - static_cast<int>(a.pad_left);
+      u64 s0 = 0, s1 = 0;
+      Acc128 c0{0, 0}, c1{0, 0};
+      u32 cnt = 0;
+#pragma unroll
+      for (int ky = 0; ky < WIN; ++ky) {
+        const int iy = iy0 + ky;
+        if (iy < 0 || iy >= static_cast<int>(a.IH)) continue;
+        const u64* Xr = X + static_cast<u64>(iy) * a.IW * xstride;
+#pragma unroll
+        for (int kx = 0; kx < WIN; ++kx) {
+          const int ix = ix0 + kx;
+          if (ix < 0 || ix >= static_cast<int>(a.IW)) continue;
+          const ulonglong2 xv = __ldg(reinterpret_cast<const ulonglong2*>(Xr + static_cast<u64>(ix) * xstride));
+          const u64 wt = w[ky * WIN + kx];
+          if (narrow) {
+            s0 += static_cast<u64>(static_cast<u32>(xv.x)) * static_cast<u32>(wt);
+            s1 += static_cast<u64>(static_cast<u32>(xv.y)) * static_cast<u32>(wt);
+            if (T2 > 8 && (++cnt & 7) == 0) {
+              s0 = (s0 & 0xffffffffull) + (s0 >> 32) * r32;
+              s1 = (s1 & 0xffffffffull) + (s1 >> 32) * r32;
+            }
+          } else {
+            mac128(c0, xv.x, wt);
+            mac128(c1, xv.y, wt);
+            if (T2 > 8 && fold && (++cnt & 7) == 0) {
+              c0 = {barrett128(c0.lo, c0.hi, P), 0};
+              c1 = {barrett128(c1.lo, c1.hi, P), 0};
+            }
+          }
+        }
+      }
+      u64 o0, o1;
+      if (narrow) {
+        o0 = barrett128(s0, 0, P);
+        o1 = barrett128(s1, 0, P);
+      } else {
+        o0 = barrett128(c0.lo, c0.hi, P);
+        o1 = barrett128(c1.lo, c1.hi, P);
+      }
+      *reinterpret_cast<ulonglong2*>(Y + static_cast<u64>(oy * a.OW + ox) * ystride) =
+          make_ulonglong2(addmod_w(o0, bv, P.q), addmod_w(o1, bv, P.q));
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Element-wise
 // ---------------------------------------------------------------------------
@@ -666,6 +742,20 @@ int launch_limbs_to_u64(const u32* in, u64* out, u64 rows, u32 Lw, u32 lo, u32 c
 
 int launch_mac_conv_w(const MacConvArgsW& a, const BasisW& B, cudaStream_t s) {
   if (a.C * a.win * a.win > static_cast<u32>(kWMaxTaps) || a.N % 256 != 0) return -1;
+  static const bool dw_on = [] {
+    const char* e = getenv("HG_DWCONV");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  if (dw_on && a.groups > 1 && a.C == 1 && a.F == 1 && (a.win == 3 || a.win == 5) && a.groups <= 65535 &&
+      a.polys * a.level <= 65535) {
+    dim3 grid(a.N / 256, a.polys * a.level, a.groups);
+    ProfScope ps_("k_dwconv_w", s);
+    if (a.win == 3)
+      k_dwconv_w<3><<<grid, 128, 0, s>>>(a, B);
+    else
+      k_dwconv_w<5><<<grid, 128, 0, s>>>(a, B);
+    return 1;
+  }
   const u32 nchunks = (a.F + kWFT - 1) / kWFT;
   const u32 groups = a.groups ? a.groups : 1;
   if (static_cast<u64>(a.polys) * a.level * nchunks * groups > 65535) return -1;

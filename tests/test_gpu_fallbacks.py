@@ -11,6 +11,8 @@ runs in its own subprocess and compares with the reference (oracle/_ref).
   HG_UPLOAD_DIRECT_FRAC=0 / 1  host packing only / everything raw through the GPU narrowing
   HG_CONV1X1_DOT=0  1x1 convolutions on the tap-gather kernel instead of the batched Dot
   HG_TC_PPC=3     3 positions per CTA in the batched Dot (ragged last chunk)
+  HG_DWCONV=0     depthwise (grouped 1 -> 1) wide convolutions on the tap-gather kernel
+  HG_NTT_W32=0    wide NTTs all on the 64-bit transform
 """
 import os
 import subprocess
@@ -86,6 +88,8 @@ print("OK")
     ({"HG_CONV1X1_DOT": "0"}, "c4lin"),
     ({"HG_WIDE_TC": "0"}, "c4lin"),
     ({"HG_TC_PPC": "3"}, "c4lin"),
+    ({"HG_DWCONV": "0"}, "c4lin"),
+    ({"HG_NTT_W32": "0"}, "c4lin"),
     ({}, "c4lin"),
 ])
 def test_alternate_paths_bit_exact(env, which):
