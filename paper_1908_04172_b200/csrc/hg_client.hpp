@@ -32,6 +32,11 @@ struct CrtTables {
   u64 q_half[kCrtWords + 1];                // floor(Q / 2)
   u64 ginv[kCrtLimbs][kCrtLimbs];           // Garner: q_j^-1 mod q_i (j < i)
   u64 q[kCrtLimbs];                         // the level's primes
+  // Two-limb fast path (wide contexts, k_dec_crt): when q_0 q_1 > 2^66, the centred value of
+  // (r_0, r_1) is the answer iff it matches every other residue -- checked exactly.
+  u32 fast2;
+  u64 q01_lo, q01_hi;                       // q_0 q_1
+  u64 q01_mod[kCrtLimbs];                   // q_0 q_1 mod q_i
 };
 
 struct DecArgs {

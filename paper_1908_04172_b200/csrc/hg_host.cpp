@@ -2930,6 +2930,20 @@ void decode_into(const Context& c, const hg_secret_key* sk, const void* ct, u64 
     a.words = static_cast<u32>(big.size());
     for (u32 k = 0; k < a.words; ++k) a.crt.big_q[k] = big[k];
     for (u32 k = 0; k < a.words; ++k) a.crt.q_half[k] = (big[k] >> 1) | (k + 1 < a.words ? (big[k + 1] << 63) : 0);
+    a.crt.fast2 = 0;
+    static const bool fast_on = [] {
+      const char* e = getenv("HG_CRT_FAST");
+      return !(e != nullptr && e[0] == '0');
+    }();
+    if (fast_on && c.wide && L > 2) {
+      const nt::u128 q01 = static_cast<nt::u128>(c.chain[0]) * c.chain[1];
+      if ((q01 >> 66) != 0) {
+        a.crt.fast2 = 1;
+        a.crt.q01_lo = static_cast<u64>(q01);
+        a.crt.q01_hi = static_cast<u64>(q01 >> 64);
+        for (u32 i = 0; i < L; ++i) a.crt.q01_mod[i] = static_cast<u64>(q01 % c.chain[i]);
+      }
+    }
     {
       // 1.0L / (long double)scale (decode_slots, henet/encoding.hpp:248), x87 on the host
       const long double li = 1.0L / static_cast<long double>(scale);

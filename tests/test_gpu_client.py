@@ -199,6 +199,23 @@ def test_wide_encrypt_decrypt_bit_exact(wenv, packing, serial):
             assert int(m[1, limb, n]) == (c0 + c1 * int(skw[limb, n])) % q
 
 
+def test_wide_decrypt_crt_fast_path_and_fallback_bit_exact(wenv):
+    """The decoder's two-limb CRT fast path (q_0 q_1 ~ 2^70) against the reference's full
+    reconstruction: fresh encryptions (small coefficients, fast path) and uniform residues
+    (coefficients near Q / 2: every one takes the full Garner fallback), in one tensor, and
+    the same tensor with the fast path switched off in a subprocess-free way (HG_CRT_FAST is
+    read once, so only the mixed tensor is checked here)."""
+    ctx, ref, keys, sk, p = wenv["ctx"], wenv["ref"], wenv["keys"], wenv["sk"], wenv["p"]
+    samples = np.random.default_rng(21).normal(0, 1, (8192, 3))
+    fresh, sc = ref.encrypt_tensor(keys, samples, 56)
+    rnd = W.random_ciphertexts(p, 3, seed=57)
+    mixed = np.concatenate([fresh, rnd], axis=0)
+    t = H.CipherTensor.from_words(ctx, mixed, sc)
+    got = H.decrypt_tensor(ctx, sk, t, 8192)
+    want = ref.decrypt_tensor(keys, mixed, sc, 0, 8192)
+    assert np.array_equal(got, want, equal_nan=True)
+
+
 def test_wide_c4_block_gpu_relu6_refresh_bit_exact(wenv):
     """BASELINE c4 on a 4x4 tile with both client-aided ReLU6 refreshes on the GPU engine
     (clamp to [0, 6]) vs the reference executor with the harness's clamp provider."""
