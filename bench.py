@@ -795,6 +795,33 @@ def c4_run(args, ws, rank, local):
                 h2[:, c] += dw[c, c, ky, kx] * hp[:, c, ky:ky + hw, kx:kx + hw]
     want = np.einsum("fc,bchw->bfhw", pw, np.clip(h2, 0, 6))
     err = float(np.abs(dec - want)[:, :, 1:-1, 1:-1].max())
+    # per-kernel attribution: one extra profiled tile (library events on the launching stream)
+    H.prof_enable(True)
+    H.execute(ctx, model, plan, x, None, eng)
+    ctx.synchronize()
+    H.prof_enable(False)
+    rep = H.prof_report()
+    tot = sum(v["ms"] for v in rep.values()) or 1.0
+    kernels = {k: {"ms_per_tile": v["ms"], "launches": v["launches"], "share": v["ms"] / tot}
+               for k, v in sorted(rep.items(), key=lambda kv: -kv[1]["ms"])}
+    # roofline of the refresh engine's transform kernel (the step's largest transform family):
+    # per ReLU6 refresh of G ciphertexts at the top level, G x 7 narrow-limb transforms for the
+    # decrypt INTT, the encode NTT and the encryption-error NTT; N/2 log2 N butterflies each
+    G = 96 * hw * hw
+    narrow = len(p["chain"]) - 1
+    n_tr = 2 * 3 * G * narrow
+    bfly = n_tr * (p["n"] // 2) * int(np.log2(p["n"]))
+    shoup_peak = H.bench_int_peak(local, 3)
+    k32 = rep.get("k_ntt_w32", {}).get("ms", 0.0)
+    roof = None
+    if k32 > 0:
+        ach = bfly / (k32 * 1e-3) / 1e12
+        roof = {"bound": "int32", "kernel": "k_ntt_w32 (refresh engine: decrypt INTT, encode NTT, error NTT)",
+                "achieved": ach, "peak": shoup_peak / 1e12, "unit": "T modmul/s (Shoup: IMAD.HI + 2 IMAD)",
+                "frac": ach / (shoup_peak / 1e12),
+                "work": f"{n_tr} transforms x {(p['n'] // 2) * int(np.log2(p['n']))} butterflies per tile",
+                "peak_source": "measured register-only Shoup-product probe (hg_bench_int_peak kind 3) on this GPU",
+                "traffic": None}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
@@ -813,8 +840,8 @@ def c4_run(args, ws, rank, local):
                                  f"{hw}x{hw} input (1-pixel halo); one tile per step, the 56x56 batch = {tiles} steps",
                        "refresh": "client-aided ReLU6 on the GPU (hg_refresh_engine, clamp [0, 6])",
                        "parallelism": f"replicas x{ws}"},
-            "tile_ms": tile_ms, "tile_ms_steps": step_ms, "roofline": None,
-            "roofline_note": "dominated by the client-aided refreshes (decrypt/decode/encode/encrypt of 2 x 9600 ciphertexts per tile); see the kernel shares",
+            "tile_ms": tile_ms, "tile_ms_steps": step_ms, "roofline": roof, "kernels": kernels,
+            "roofline_note": "the client-aided refreshes (decrypt/decode/encode/encrypt of 2 x 9600 ciphertexts per tile) are most of the tile; kernels: one profiled tile (serialised launches)",
             "cpu_baseline": cpu, "e2e": None, "gpu_launches": launches, "clocks": clk,
             "check": {"max_abs_err_vs_cleartext_interior": err, "images_checked": 16}}))
     if ws > 1:

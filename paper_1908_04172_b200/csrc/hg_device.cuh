@@ -44,6 +44,9 @@ constexpr int kMaxPrimes = 24;
 #ifndef HG_MODDOWN_MINB
 #define HG_MODDOWN_MINB 2  // mod-down: its accumulator prefetch needs > 80 registers
 #endif
+#ifndef HG_NTT14_MINB
+#define HG_NTT14_MINB 2  // N = 2^14 transforms (512 threads): 2 CTAs per SM, 64 registers
+#endif
 #ifndef HG_NTT_MINB
 #define HG_NTT_MINB 2  // CTAs per SM the NTT kernels are register-budgeted for (N <= 2^13)
 #endif

@@ -74,7 +74,7 @@ __device__ __forceinline__ void st4(W* p, uint4 v) {
 
 // W = u64: the limbs are read and written in place in wide (u64) tensors (a.in64 / a.out64).
 template <int LOGN, bool LAZY, typename W = u32>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_RESCALE_MINB : 1)) k_rescale(RescaleArgs a, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_RESCALE_MINB : HG_NTT14_MINB)) k_rescale(RescaleArgs a, Basis B) {
   using NT = Ntt<LOGN, true>;  // staged pass-B twiddles: 3 CTAs per SM
   constexpr int N = NT::N;
   constexpr bool kWide = sizeof(W) == 8;

@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_ntt_w(u64* data, u32 lev
 // butterfly on 32-bit words instead of the 64-bit Shoup of NttW): residues are narrowed on
 // load and widened on store, in place.  Limbs [lo, level) of every row.
 template <int LOGN, bool INV>
-__global__ void __launch_bounds__(1 << (LOGN - 5), 1) k_ntt_w32(u64* data, u32 level, u32 lo, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 4 : HG_NTT14_MINB)) k_ntt_w32(u64* data, u32 level, u32 lo, Basis B) {
   using NT = Ntt<LOGN, true>;
   extern __shared__ u32 sm32[];
   const u32 tid = threadIdx.x;
