@@ -53,7 +53,7 @@ static void check_launch(int r, const char* what) {
   cuda_check(cudaGetLastError(), what);
 }
 
-static constexpr size_t kBufCacheMin = size_t(256) << 20;
+static constexpr size_t kBufCacheMin = size_t(1) << 30;  // layer-sized buffers only (c4, c5b); c2 unchanged
 static size_t buf_cache_max(int device) {
   static std::mutex mu;
   static std::map<int, size_t> v;
