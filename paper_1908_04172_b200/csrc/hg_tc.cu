@@ -64,8 +64,14 @@ constexpr int tc_stages() { return TN == 64 ? 5 : 4; }
 // shallower to stay within 227 KB, the wide TN = 32 ring 3 deep so two CTAs fit per SM.
 template <int TN, typename XW>
 constexpr int tc_xs() { return sizeof(XW) == 8 ? (TN == 64 ? kTcXS - 1 : 3) : kTcXS; }
-template <int TN>
-constexpr int tc_xpitch() { return TN + 4; }
+#ifndef HG_TC_XPAD64
+#define HG_TC_XPAD64 0  // u64 staging rows unpadded (c5b: 61.3 vs 64.0 ms with 4 words of padding)
+#endif
+#ifndef HG_TC_ROT64
+#define HG_TC_ROT64 0
+#endif
+template <int TN, typename XW = u32>
+constexpr int tc_xpitch() { return TN + (sizeof(XW) == 8 ? HG_TC_XPAD64 : 4); }
 
 template <int TN, typename XW = u32>
 struct TcSmem {
@@ -74,7 +80,7 @@ struct TcSmem {
   uint8_t b[kS][4][TN * kTcK];  // input planes, written by the producer warps; the planes of a
                                   // stage are consecutive, i.e. one K-major (planes*TN) x 32 matrix
   uint8_t zero_a[kTcPlaneA];      // zero weight plane: initialises the upper accumulators
-  XW xs[tc_xs<TN, XW>()][kTcK][tc_xpitch<TN>()];  // input residues staged by cp.async (producer ring)
+  XW xs[tc_xs<TN, XW>()][kTcK][tc_xpitch<TN, XW>()];  // input residues staged by cp.async (producer ring)
   unsigned long long full_a[kS], full_b[kS], empty[kS], acc_full, acc_empty;
   u32 tmem;
 };
@@ -269,12 +275,12 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
     // the reads of a phase do too (padded pitch TN + 4); the rotation is undone in registers.
     // One elected lane arrives per warp. =====
     constexpr int XS = tc_xs<TN, XW>();
-    constexpr int XP = tc_xpitch<TN>();
+    constexpr int XP = tc_xpitch<TN, XW>();
     constexpr int KQ = TN == 64 ? 8 : 4;              // k per thread
     constexpr int CW = TN / 4;                         // columns per warp
     // ROT: rows by which odd-phase threads rotate their reads (bank offset 16 against the
     // even phase): pitch XP words (u32) or 2 XP words (u64)
-    constexpr int ROT = TN == 64 ? (sizeof(XW) == 4 ? 4 : 2) : 2;
+    constexpr int ROT = TN == 64 ? (sizeof(XW) == 4 ? 4 : HG_TC_ROT64) : 2;
     const u64 xelem = static_cast<u64>(a.polys) * a.x_level * a.N;  // words per input element
     const u64 xstride = a.x_kstride * xelem;
     const XW* Xb = static_cast<const XW*>(kWide ? static_cast<const void*>(a.X64) : static_cast<const void*>(a.X)) +
