@@ -103,6 +103,27 @@ static int bench(int steps) {
     henet::gpu::detail::upload(dev, x.elems, x.shape.dims, t);
     up.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   }
+  // per-phase host times of the call, for the breakdown: the device-cache lookups (relin key,
+  // model, plan) and the upload; the remainder of the call is hg_execute + the download
+  std::vector<double> t_key, t_model, t_plan;
+  for (int i = 0; i < steps; ++i) {
+    auto t0 = std::chrono::steady_clock::now();
+    dev.relin(*keys.relin);
+    auto t1 = std::chrono::steady_clock::now();
+    dev.model(model, false);
+    auto t2 = std::chrono::steady_clock::now();
+    auto pg = henet::gpu::detail::device_plan(plan);
+    auto t3 = std::chrono::steady_clock::now();
+    t_key.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t_model.push_back(std::chrono::duration<double, std::milli>(t2 - t1).count());
+    t_plan.push_back(std::chrono::duration<double, std::milli>(t3 - t2).count());
+  }
+  auto med = [](std::vector<double> v) {
+    std::sort(v.begin(), v.end());
+    return v[v.size() / 2];
+  };
+  std::fprintf(stderr, "dropin breakdown [ms]: relin key lookup %.3f, model lookup %.3f, plan %.3f\n", med(t_key),
+               med(t_model), med(t_plan));
   std::sort(ms.begin(), ms.end());
   std::sort(up.begin(), up.end());
   double sum = 0;
