@@ -11,6 +11,7 @@
 // and the bus carries 4 bytes per residue.
 #include <cuda_runtime.h>
 #include <emmintrin.h>
+#include <immintrin.h>
 
 #include <algorithm>
 #include <atomic>
@@ -147,6 +148,40 @@ inline bool pack_run(const u64* src, u32* dst, u32 n, u32 q) {
   return _mm_movemask_epi8(_mm_cmpeq_epi32(_mm_or_si128(hi, over), _mm_setzero_si128())) == 0xFFFF;
 }
 
+// AVX-512 variant (one 64-byte load, one unsigned compare against q over the whole u64 word,
+// one VPMOVQD truncation and one 32-byte streaming store per 8 words); picked at run time
+// when the host supports it (HG_UPLOAD_AVX512=0 keeps the SSE2 loop).
+__attribute__((target("avx512f,avx512vl"))) inline bool pack_run_avx512(const u64* src, u32* dst, u32 n, u32 q) {
+  const __m512i qv = _mm512_set1_epi64(static_cast<long long>(q));
+  __mmask8 bad0 = 0, bad1 = 0;
+  u32 j = 0;
+  for (; j + 16 <= n; j += 16) {
+    const __m512i a = _mm512_loadu_si512(src + j), c = _mm512_loadu_si512(src + j + 8);
+    bad0 |= _mm512_cmpge_epu64_mask(a, qv);
+    bad1 |= _mm512_cmpge_epu64_mask(c, qv);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + j), _mm512_cvtepi64_epi32(a));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + j + 8), _mm512_cvtepi64_epi32(c));
+  }
+  for (; j + 8 <= n; j += 8) {
+    const __m512i a = _mm512_loadu_si512(src + j);
+    bad0 |= _mm512_cmpge_epu64_mask(a, qv);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + j), _mm512_cvtepi64_epi32(a));
+  }
+  bool ok = (bad0 | bad1) == 0;
+  if (j < n) ok = pack_run(src + j, dst + j, n - j, q) && ok;  // n % 4 == 0 tail
+  return ok;
+}
+
+bool use_avx512() {
+  static const bool on = [] {
+    const char* e = getenv("HG_UPLOAD_AVX512");
+    if (e != nullptr && e[0] == '0') return false;
+    __builtin_cpu_init();
+    return __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512vl");
+  }();
+  return on;
+}
+
 }  // namespace
 
 double upload_direct_fraction() {
@@ -188,6 +223,7 @@ bool host_narrow_upload(int device, const u64* words, u32* dst, u64 n_words, u32
       throw Error(HG_ERR_CUDA, "narrow launch failed");
   }
   const int nw = W.pool->size();
+  const bool avx512 = use_avx512();
   const u64 chunks = (n_words + kChunkWords - 1) / kChunkWords;
   std::atomic<bool> bad{false};
   std::atomic<int> err{0};
@@ -211,7 +247,8 @@ bool host_narrow_upload(int device, const u64* words, u32* dst, u64 n_words, u32
           const u64* src = segs == nullptr
                                ? words + r
                                : reinterpret_cast<const u64*>(segs[r / seg_words] + (r % seg_words) * 8);
-          my_bad |= !pack_run(src, out + (r - b), N, static_cast<u32>(chain[(r / N) % level]));
+          const u32 q = static_cast<u32>(chain[(r / N) % level]);
+          my_bad |= avx512 ? !pack_run_avx512(src, out + (r - b), N, q) : !pack_run(src, out + (r - b), N, q);
         }
         _mm_sfence();  // the streaming stores are visible before the DMA reads the chunk
         cuda_check(cudaMemcpyAsync(dst + b, out, (e - b) * 4, cudaMemcpyHostToDevice, ws), "h2d");
