@@ -47,7 +47,18 @@ __device__ __forceinline__ u64 barrett128(u64 z_lo, u64 z_hi, const DevPrimeW& P
   return r >= P.q ? r - P.q : r;
 }
 
+// Any u64 -> [0, q) for q < 2^62: Barrett with the 64-bit mu = floor(2^64 / q) (r128_hi);
+// the estimate is at most 2 below floor(x / q), so two conditional subtractions finish it.
+__device__ __forceinline__ u64 red64(u64 x, const DevPrimeW& P) {
+  const u64 r = x - __umul64hi(x, P.r128_hi) * P.q;
+  const u64 r1 = r >= P.q ? r - P.q : r;
+  return r1 >= P.q ? r1 - P.q : r1;
+}
+
+// Primes below 2^31 (the 30-bit limbs of a wide context): operands < 2q keep the product
+// below 2^64, so one 64-bit Barrett replaces the 128-bit one.  The branch is uniform per limb.
 __device__ __forceinline__ u64 mulmod_w(u64 a, u64 b, const DevPrimeW& P) {
+  if (P.q < (1ull << 31)) return red64(a * b, P);
   return barrett128(a * b, __umul64hi(a, b), P);
 }
 
