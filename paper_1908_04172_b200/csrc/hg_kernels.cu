@@ -18,6 +18,8 @@
 
 #include <cstdio>
 
+#include <cooperative_groups.h>
+
 #include "hg_kernels.hpp"
 #include "hg_x87.cuh"
 
@@ -1107,6 +1109,104 @@ __global__ void __launch_bounds__(1024) k_fft_encode(const double* slots, u32 n_
   }
 }
 
+// n = 2^14 (the BASELINE c4 ring): the 256 KB working array does not fit one CTA's shared
+// memory, so a 2-CTA cluster splits it: CTA r holds positions [r n/2, (r+1) n/2) and runs the
+// first log2(n) - 1 stages locally (a block of len <= n/2 never crosses the halves); the last
+// stage pairs (k, k + n/2) across the cluster through distributed shared memory.  Same
+// butterflies, twiddles and roundings as k_fft_encode, so the same bits.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024)
+    k_fft_encode2(const double* slots, u32 n_slots, u32 n, u32 logn, u32 level, double scale, const double2* roots,
+                  const double2* twist, ulonglong2* mags, unsigned long long* max_mant, int* max_exp) {
+  extern __shared__ double2 f2_sm[];
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const u32 r = cluster.block_rank();
+  const u64 pt = blockIdx.x >> 1;
+  const u32 tid = threadIdx.x, HN = n >> 1;
+  double2* a = f2_sm;
+  const double* s = slots + pt * 2 * static_cast<u64>(n_slots);
+  for (u32 ii = tid; ii < HN; ii += blockDim.x) {  // position i = r HN + ii holds element bitrev(i)
+    const u32 j = bitrev_n(r * HN + ii, logn);
+    double2 e = make_double2(0.0, 0.0);
+    if (j < n_slots) e = make_double2(s[2 * j], s[2 * j + 1]);
+    else if (n - 1 - j < n_slots) { const u32 jj = n - 1 - j; e = make_double2(s[2 * jj], -s[2 * jj + 1]); }
+    a[ii] = e;
+  }
+  __syncthreads();
+  for (u32 lh = 0; lh + 1 < logn; ++lh) {
+    const u32 half = 1u << lh, step = n >> (lh + 1);
+    for (u32 idx = tid; idx < HN / 2; idx += blockDim.x) {
+      const u32 base = (idx >> lh) << (lh + 1), k = idx & (half - 1);
+      const double2 w = __ldg(&roots[k * step]);
+      const double2 u = a[base + k];
+      const double2 v = cmul_exact(a[base + k + half], w);
+      a[base + k] = make_double2(__dadd_rn(u.x, v.x), __dadd_rn(u.y, v.y));
+      a[base + k + half] = make_double2(__dsub_rn(u.x, v.x), __dsub_rn(u.y, v.y));
+    }
+    __syncthreads();
+  }
+  cluster.sync();
+  {
+    double2* h0 = cluster.map_shared_rank(a, 0);
+    double2* h1 = cluster.map_shared_rank(a, 1);
+    for (u32 kk = tid; kk < HN / 2; kk += blockDim.x) {  // last stage: step 1, pairs (k, k + HN)
+      const u32 k = r * (HN / 2) + kk;
+      const double2 w = __ldg(&roots[k]);
+      const double2 u = h0[k];
+      const double2 v = cmul_exact(h1[k], w);
+      h0[k] = make_double2(__dadd_rn(u.x, v.x), __dadd_rn(u.y, v.y));
+      h1[k] = make_double2(__dsub_rn(u.x, v.x), __dsub_rn(u.y, v.y));
+    }
+  }
+  cluster.sync();
+  const double inv_n = 1.0 / static_cast<double>(n);
+  __shared__ unsigned long long s_mant[32];
+  __shared__ int s_exp[32];
+  unsigned long long bm = 0;
+  int be = -100000;
+  for (u32 kk = tid; kk < HN; kk += blockDim.x) {
+    const u32 k = r * HN + kk;
+    const double2 e = a[kk];
+    const double2 tw = twist[k];
+    const double re = __dsub_rn(__dmul_rn(e.x, tw.x), __dmul_rn(e.y, -tw.y));
+    const double coeff = __dmul_rn(re, inv_n);
+    const X87 x = x87_mul(coeff, scale);
+    if (x.mant != 0 && (x.exp > be || (x.exp == be && x.mant > bm))) { bm = x.mant; be = x.exp; }
+    const unsigned __int128 mag = x87_roundl_mag(x);
+    mags[pt * n + k] = make_ulonglong2(static_cast<u64>(mag), static_cast<u64>(mag >> 64) | (x.neg ? (1ull << 63) : 0));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, bm, o);
+    const int e2 = __shfl_xor_sync(0xffffffffu, be, o);
+    if (m2 != 0 && (bm == 0 || e2 > be || (e2 == be && m2 > bm))) { bm = m2; be = e2; }
+  }
+  if ((tid & 31) == 0) {
+    s_mant[tid >> 5] = bm;
+    s_exp[tid >> 5] = be;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (u32 t = 1; t < blockDim.x / 32; ++t) {
+      if (s_mant[t] != 0 && (bm == 0 || s_exp[t] > be || (s_exp[t] == be && s_mant[t] > bm))) {
+        bm = s_mant[t];
+        be = s_exp[t];
+      }
+    }
+    s_mant[0] = bm;
+    s_exp[0] = be;
+  }
+  cluster.sync();  // both halves' maxima published
+  if (r == 0 && tid == 0) {
+    const unsigned long long m2 = *cluster.map_shared_rank(&s_mant[0], 1);
+    const int e2 = *cluster.map_shared_rank(&s_exp[0], 1);
+    if (m2 != 0 && (bm == 0 || e2 > be || (e2 == be && m2 > bm))) { bm = m2; be = e2; }
+    max_mant[pt] = bm;
+    max_exp[pt] = be;
+  }
+  cluster.sync();  // the peer's shared memory outlives the read above
+}
+
 // Signed 128-bit magnitudes -> residues per limb (coefficient domain), u32 basis.
 __global__ void k_mags_to_residues(const ulonglong2* mags, u64 count_n, u32 n, u32 level, u32* out, Basis B) {
   const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1467,6 +1567,15 @@ int launch_encode_scalars_f64(const double* vals, u64 count, u32 row_len, u32 ro
   return 1;
 }
 
+// HG_FFT_CLUSTER=0: the n = 2^14 FFTs on the single-CTA global-memory kernels
+bool fft_cluster_on() {
+  static const bool on = [] {
+    const char* e = getenv("HG_FFT_CLUSTER");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 int launch_fft_encode(const double* slots, u32 n_slots, u64 count, u32 n, u32 level, double scale,
                       const double2* roots, const double2* twist, double2* scratch, ulonglong2* mags,
                       unsigned long long* max_mant, int* max_exp, cudaStream_t s) {
@@ -1484,6 +1593,15 @@ int launch_fft_encode(const double* slots, u32 n_slots, u64 count, u32 n, u32 le
     }
     k_fft_encode<true><<<count, 1024, sm, s>>>(slots, n_slots, n, logn, level, scale, roots, twist, scratch, mags,
                                              max_mant, max_exp);
+  } else if (n == 16384 && fft_cluster_on()) {
+    const size_t sm = static_cast<size_t>(n / 2) * sizeof(double2);  // half the array per CTA
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_fft_encode2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+      attr = true;
+    }
+    k_fft_encode2<<<count * 2, 1024, sm, s>>>(slots, n_slots, n, logn, level, scale, roots, twist, mags, max_mant,
+                                              max_exp);
   } else {
     k_fft_encode<false><<<count, 512, 0, s>>>(slots, n_slots, n, logn, level, scale, roots, twist, scratch, mags,
                                               max_mant, max_exp);

@@ -124,6 +124,7 @@ int launch_encode_scalars_f64(const double* vals, u64 count, u32 row_len, u32 ro
 // operation order, untwist, x87 scale/round -> signed 128-bit magnitudes
 // (lo, hi | sign << 63) per coefficient.  max_mant/max_exp[pt] = the largest
 // |scaled| as an exact long double (mantissa, exponent).
+bool fft_cluster_on();  // 2-CTA cluster FFTs at n = 2^14 (HG_FFT_CLUSTER)
 int launch_fft_encode(const double* slots, u32 n_slots, u64 count, u32 n, u32 level, double scale,
                       const double2* roots, const double2* twist, double2* scratch, ulonglong2* mags,
                       unsigned long long* max_mant, int* max_exp, cudaStream_t s);

@@ -13,6 +13,8 @@ runs in its own subprocess and compares with the reference (oracle/_ref).
   HG_TC_PPC=3     3 positions per CTA in the batched Dot (ragged last chunk)
   HG_DWCONV=0     depthwise (grouped 1 -> 1) wide convolutions on the tap-gather kernel
   HG_NTT_W32=0    wide NTTs all on the 64-bit transform
+  HG_FFT_CLUSTER=0  N = 2^14 encode/decode FFTs on one CTA in global memory (no 2-CTA cluster)
+  HG_CRT_FAST=0   the decoder's full Garner CRT for every coefficient
 """
 import os
 import subprocess
@@ -65,8 +67,33 @@ def c4_linear():
     wl.manifest = json.dumps(j)
     return wl
 
+def c4_refresh():
+    # the c4 block on a 4x4 tile with both ReLU6 refreshes on the GPU engine (N = 2^14
+    # encrypt / decrypt / FFTs) against the reference executor with the clamp provider
+    p = W.N16384
+    ctx = H.CkksContext(p["n"], p["chain"], p["special"], p["scale"])
+    ref = R.RefContext(p["n"], p["chain"], p["special"], p["scale"])
+    keys = ref.keygen(41, False)
+    sk = H.SecretKey(ctx, keys.sk_words())
+    wl = W.mobilenet_block(hw=4, cin=4, expand=6, cout=3)
+    acts = np.random.default_rng(12).normal(0, 1, (ctx.slot_count(), wl.input_count))
+    words, sc = ref.encrypt_tensor(keys, acts, 13)
+    R.set_relu_clip(6.0)
+    want, want_sc, _ = ref.execute(keys, wl.manifest, wl.blob, words, sc, refresh_seed=77)
+    model = H.PlainModel.load(wl.manifest, wl.blob)
+    eng = H.RefreshEngine(ctx, sk, 77)
+    eng.set_relu_clip(6.0)
+    x = H.encrypt_tensor(ctx, sk, acts, 13, shape=wl.input_shape)
+    assert np.array_equal(x.to_words(), words)
+    out = H.execute(ctx, model, H.RescalePlan.plan(ctx, model), x, None, eng)
+    assert out.scale == want_sc
+    assert np.array_equal(out.to_words(), want)
+    assert np.array_equal(H.decrypt_tensor(ctx, sk, out, 8192), ref.decrypt_tensor(keys, want, want_sc, 0, 8192))
+
 which = sys.argv[2]
-if which == "toy":
+if which == "c4refresh":
+    c4_refresh()
+elif which == "toy":
     run(W.N8192, W.toy_cryptonets(), 3, True)
 elif which == "c4lin":
     run(W.N16384, c4_linear(), 5, False)
@@ -90,6 +117,9 @@ print("OK")
     ({"HG_TC_PPC": "3"}, "c4lin"),
     ({"HG_DWCONV": "0"}, "c4lin"),
     ({"HG_NTT_W32": "0"}, "c4lin"),
+    ({"HG_FFT_CLUSTER": "0"}, "c4refresh"),
+    ({"HG_CRT_FAST": "0"}, "c4refresh"),
+    ({}, "c4refresh"),
     ({}, "c4lin"),
 ])
 def test_alternate_paths_bit_exact(env, which):
