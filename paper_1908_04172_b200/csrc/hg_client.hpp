@@ -23,6 +23,7 @@ struct EncArgs {
   u64 thr[kMaxPrimes];  // next_below rejection thresholds (2^64 mod q)
   u32 count, level, N;
   u32 e0;           // index of ciphertext 0 in the seed sequence (chunked refreshes)
+  u32 limb_cnt;     // k_enc_combine: limbs [0, limb_cnt) only (0: all)
 };
 
 // Garner recomposition constants (k_dec_crt); passed by value next to the Basis, so only
@@ -48,6 +49,7 @@ struct DecArgs {
   int inv_exp;
   CrtTables crt;
   u32 count, polys, level, N, words;
+  u32 limb_cnt;     // k_dec_combine: limbs [0, limb_cnt) only (0: all)
 };
 
 int launch_batch_to_slots(const double* samples, u64 count, u64 e0, u32 cnt, u32 n_slots, int complex_pack,

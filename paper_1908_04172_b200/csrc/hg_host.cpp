@@ -2812,12 +2812,30 @@ void encrypt_into(const Context& c, const hg_secret_key* sk, const void* pt, u64
     check_launch(launch_enc_serial(a, dl ? static_cast<const u32*>(dl->ptr) : nullptr, static_cast<u32>(count),
                                    client_basis(c), c.wide, s),
                  "encrypt serial");
-    check_launch(c.wide ? launch_ntt_w(static_cast<int>(c.logn), static_cast<u64*>(a.err), count * L, L, false,
-                                       c.basisw, s)
-                        : launch_ntt(static_cast<int>(c.logn), static_cast<u32*>(a.err), count * L, L, false, c.basis,
-                                     s),
-                 "ntt");
-    check_launch(launch_enc_combine(a, client_basis(c), c.wide, s), "encrypt combine");
+    static const bool fuse_on = [] {
+      const char* e = getenv("HG_ENC_FUSE");
+      return !(e != nullptr && e[0] == '0');
+    }();
+    const u32 lo = c.wide ? wide_narrow_lo(c.basisw, L) : L;
+    if (c.wide && fuse_on && lo < L) {
+      // limbs below 2^30: the error NTT and the combine in one kernel; the wide limbs as before
+      check_launch(launch_enc_ntt_w(static_cast<int>(c.logn), static_cast<u64*>(a.ct), static_cast<u64*>(a.err),
+                                    static_cast<const u64*>(a.pt), static_cast<const u64*>(a.sk), count, L, c.basisw,
+                                    s),
+                   "encrypt ntt");
+      if (lo > 0) {
+        EncArgs a2 = a;
+        a2.limb_cnt = lo;
+        check_launch(launch_enc_combine(a2, client_basis(c), c.wide, s), "encrypt combine");
+      }
+    } else {
+      check_launch(c.wide ? launch_ntt_w(static_cast<int>(c.logn), static_cast<u64*>(a.err), count * L, L, false,
+                                         c.basisw, s)
+                          : launch_ntt(static_cast<int>(c.logn), static_cast<u32*>(a.err), count * L, L, false,
+                                       c.basis, s),
+                   "ntt");
+      check_launch(launch_enc_combine(a, client_basis(c), c.wide, s), "encrypt combine");
+    }
     // no synchronisation: err / flags are freed stream-ordered after the combine
 }
 

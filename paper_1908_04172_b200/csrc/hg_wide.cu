@@ -73,6 +73,88 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 4 : HG_NTT14_MI
   }
 }
 
+// encrypt's c0 = NTT(e) - a s + pt (henet/ckks.hpp:235-239) fused into the error's forward NTT
+// for the limbs below 2^30: the transformed error never goes back to HBM.
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 4 : HG_NTT14_MINB))
+    k_enc_ntt_w32(u64* ct, const u64* err, const u64* pt, const u64* sk, u32 level, u32 lo, Basis B) {
+  using NT = Ntt<LOGN, true>;
+  extern __shared__ u32 sm32[];
+  const u32 tid = threadIdx.x;
+  const u32 cnt = level - lo;
+  const u64 e = blockIdx.x / cnt;
+  const u32 limb = lo + blockIdx.x % cnt;
+  const DevPrime& P = B.p[limb];
+  const u64 per = static_cast<u64>(level) * NT::N, row = static_cast<u64>(limb) * NT::N;
+  const u64* er = err + e * per + row;
+  u32 x[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) x[k] = static_cast<u32>(__ldg(&er[NT::jA(tid, k)]));
+  NT::forward(x, sm32, tid, P);
+  u64* c0 = ct + e * 2 * per + row;
+  const u64* c1 = c0 + per;
+  const u64* pr = pt + e * per + row;
+  const u64* sr = sk + row;
+  auto ld4 = [](const u64* p) {
+    const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(p)), b = __ldg(reinterpret_cast<const ulonglong2*>(p) + 1);
+    return make_uint4(static_cast<u32>(a.x), static_cast<u32>(a.y), static_cast<u32>(b.x), static_cast<u32>(b.y));
+  };
+#pragma unroll
+  for (int k = 0; k < 32; k += 4) {
+    const u32 j = NT::jC(tid, k);
+    const uint4 av = ld4(c1 + j), sv = ld4(sr + j), pv = ld4(pr + j);
+    const u32 A[4] = {av.x, av.y, av.z, av.w}, S[4] = {sv.x, sv.y, sv.z, sv.w}, Pt[4] = {pv.x, pv.y, pv.z, pv.w};
+    u32 o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = addmod(submod(x[k + i], mulmod(A[i], S[i], P), P.q), Pt[i], P.q);
+    ulonglong2* d = reinterpret_cast<ulonglong2*>(c0 + j);
+    d[0] = make_ulonglong2(o[0], o[1]);
+    d[1] = make_ulonglong2(o[2], o[3]);
+  }
+}
+
+// decrypt's m = c0 + c1 s (+ c2 s^2) (henet/ckks.hpp:256-268) fused into the INTT of the limbs
+// below 2^30: the NTT-domain words are combined in registers (u32 arithmetic) as they are
+// loaded, transformed, and only the coefficient-domain m is written -- no m round trip
+// through HBM between a combine kernel and the transform.
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 4 : HG_NTT14_MINB))
+    k_dec_intt_w32(const u64* ct, const u64* sk, u64* m, u32 polys, u32 level, u32 lo, Basis B) {
+  using NT = Ntt<LOGN, true>;
+  extern __shared__ u32 sm32[];
+  const u32 tid = threadIdx.x;
+  const u32 cnt = level - lo;
+  const u64 e = blockIdx.x / cnt;
+  const u32 limb = lo + blockIdx.x % cnt;
+  const DevPrime& P = B.p[limb];
+  const u64 per = static_cast<u64>(level) * NT::N;
+  const u64* c0 = ct + e * polys * per + static_cast<u64>(limb) * NT::N;
+  const u64* sr = sk + static_cast<u64>(limb) * NT::N;
+  u32 x[32];
+  auto ld4 = [](const u64* p) {
+    const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(p)), b = __ldg(reinterpret_cast<const ulonglong2*>(p) + 1);
+    return make_uint4(static_cast<u32>(a.x), static_cast<u32>(a.y), static_cast<u32>(b.x), static_cast<u32>(b.y));
+  };
+#pragma unroll
+  for (int k = 0; k < 32; k += 4) {
+    const u32 j = NT::jC(tid, k);
+    const uint4 a0 = ld4(c0 + j), a1 = ld4(c0 + per + j), sv = ld4(sr + j);
+    const u32 A0[4] = {a0.x, a0.y, a0.z, a0.w}, A1[4] = {a1.x, a1.y, a1.z, a1.w}, S[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[k + i] = addmod(A0[i], mulmod(A1[i], S[i], P), P.q);
+    if (polys == 3) {
+      const uint4 a2 = ld4(c0 + 2 * per + j);
+      const u32 A2[4] = {a2.x, a2.y, a2.z, a2.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x[k + i] = addmod(x[k + i], mulmod(A2[i], mulmod(S[i], S[i], P), P), P.q);
+    }
+  }
+  NT::inverse(x, sm32, tid, P);
+  u64* out = m + (e * level + limb) * NT::N;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) out[NT::jA(tid, k)] = x[k];
+}
+
 // ---------------------------------------------------------------------------
 // Rescale (henet/ckks.hpp:504-519), NTT-domain form as in k_rescale.
 // ---------------------------------------------------------------------------
@@ -655,6 +737,59 @@ int launch_ntt_w(int logn, u64* data, u64 rows, u32 level, bool inverse, const B
       k<<<count * (level - lo), 1 << (LN - 5), sm, s>>>(data, level, lo, *static_cast<const Basis*>(B.narrow));
       ++launches;
     }
+  });
+  return launches;
+}
+
+u32 wide_narrow_lo(const BasisW& B, u32 level) {
+  u32 lo = level;
+  if (B.narrow != nullptr)
+    while (lo > 0 && B.p[lo - 1].q < (1ull << 30)) --lo;
+  return lo;
+}
+
+int launch_dec_intt_w(int logn, const u64* ct, const u64* sk, u64* m, u64 count, u32 polys, u32 level,
+                      const BasisW& B, cudaStream_t s) {
+  const u32 lo = wide_narrow_lo(B, level);
+  if (count == 0 || lo >= level || (polys != 2 && polys != 3)) return -2;
+  int launches = 0;
+  HG_LOGN_SWITCH_W(logn, {
+    if (lo > 0) {  // the wide limbs: m already combined (k_dec_combine), INTT on the u64 transform
+      const size_t sm = sizeof(u64) * NttW<LN>::SMEM_WORDS;
+      set_smem_w(k_ntt_w<LN, true>, sm);
+      ProfScope ps_("k_ntt_w", s);
+      k_ntt_w<LN, true><<<count * lo, 1 << (LN - 5), sm, s>>>(m, level, 0, lo, B);
+      ++launches;
+    }
+    const size_t sm = sizeof(u32) * Ntt<LN, true>::SMEM_WORDS;
+    set_smem_w(k_dec_intt_w32<LN>, sm);
+    ProfScope ps_("k_dec_intt_w32", s);
+    k_dec_intt_w32<LN><<<count * (level - lo), 1 << (LN - 5), sm, s>>>(ct, sk, m, polys, level, lo,
+                                                                       *static_cast<const Basis*>(B.narrow));
+    ++launches;
+  });
+  return launches;
+}
+
+int launch_enc_ntt_w(int logn, u64* ct, u64* err, const u64* pt, const u64* sk, u64 count, u32 level,
+                     const BasisW& B, cudaStream_t s) {
+  const u32 lo = wide_narrow_lo(B, level);
+  if (count == 0 || lo >= level) return -2;
+  int launches = 0;
+  HG_LOGN_SWITCH_W(logn, {
+    if (lo > 0) {  // the wide limbs: error NTT'd in place (combined afterwards by k_enc_combine)
+      const size_t sm = sizeof(u64) * NttW<LN>::SMEM_WORDS;
+      set_smem_w(k_ntt_w<LN, false>, sm);
+      ProfScope ps_("k_ntt_w", s);
+      k_ntt_w<LN, false><<<count * lo, 1 << (LN - 5), sm, s>>>(err, level, 0, lo, B);
+      ++launches;
+    }
+    const size_t sm = sizeof(u32) * Ntt<LN, true>::SMEM_WORDS;
+    set_smem_w(k_enc_ntt_w32<LN>, sm);
+    ProfScope ps_("k_enc_ntt_w32", s);
+    k_enc_ntt_w32<LN><<<count * (level - lo), 1 << (LN - 5), sm, s>>>(ct, err, pt, sk, level, lo,
+                                                                      *static_cast<const Basis*>(B.narrow));
+    ++launches;
   });
   return launches;
 }

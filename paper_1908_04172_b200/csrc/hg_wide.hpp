@@ -83,6 +83,16 @@ struct EwArgsW {
 };
 
 int launch_ntt_w(int logn, u64* data, u64 rows, u32 level, bool inverse, const BasisW& B, cudaStream_t s);
+// first limb of the suffix of limbs below 2^30 (== level when there is none or no u32 basis)
+u32 wide_narrow_lo(const BasisW& B, u32 level);
+// decrypt's combine + INTT: limbs [0, lo) INTT'd in place in m (combined beforehand), limbs
+// [lo, level) combined from ct / sk and INTT'd in one kernel; -2 when there is no such suffix
+// encrypt's error NTT + combine: limbs [0, lo) NTT'd in place in err (combined afterwards),
+// limbs [lo, level) transformed and combined into c0 in one kernel; -2 without such a suffix
+int launch_enc_ntt_w(int logn, u64* ct, u64* err, const u64* pt, const u64* sk, u64 count, u32 level,
+                     const BasisW& B, cudaStream_t s);
+int launch_dec_intt_w(int logn, const u64* ct, const u64* sk, u64* m, u64 count, u32 polys, u32 level,
+                      const BasisW& B, cudaStream_t s);
 int launch_rescale_w(int logn, const RescaleArgsW& a, const BasisW& B, cudaStream_t s);
 int launch_relin_w(int logn, const RelinArgsW& a, const BasisW& B, cudaStream_t s);
 u32 mac_dense_w_bm();  // Mpad must be a multiple of this

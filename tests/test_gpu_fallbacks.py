@@ -15,6 +15,7 @@ runs in its own subprocess and compares with the reference (oracle/_ref).
   HG_NTT_W32=0    wide NTTs all on the 64-bit transform
   HG_FFT_CLUSTER=0  N = 2^14 encode/decode FFTs on one CTA in global memory (no 2-CTA cluster)
   HG_CRT_FAST=0   the decoder's full Garner CRT for every coefficient
+  HG_DEC_FUSE=0 / HG_ENC_FUSE=0  decrypt combine / encrypt combine as separate kernels
 """
 import os
 import subprocess
@@ -119,6 +120,7 @@ print("OK")
     ({"HG_NTT_W32": "0"}, "c4lin"),
     ({"HG_FFT_CLUSTER": "0"}, "c4refresh"),
     ({"HG_CRT_FAST": "0"}, "c4refresh"),
+    ({"HG_DEC_FUSE": "0", "HG_ENC_FUSE": "0"}, "c4refresh"),
     ({}, "c4refresh"),
     ({}, "c4lin"),
 ])
