@@ -67,9 +67,10 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c5b", "c4"],
-                    help="c2 (default, the BASELINE metric) or c5b: wide dense 4096->4096 at N=16384, "
-                         "output-sharded over the ranks with an NCCL all-gather")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5b", "c4", "c1", "c3"],
+                    help="c2 (default, the BASELINE metric); c1: the dense 845->100 layer; c3: CryptoNets-ReLU "
+                         "under complex packing with GPU refreshes; c4: the MobileNetV2 block (tiled); c5b: wide "
+                         "dense 4096->4096 at N=16384, output-sharded over the ranks with an NCCL all-gather")
     return ap.parse_args()
 
 
@@ -876,6 +877,111 @@ def c4_reference_sample():
                       f"scaled by position to 56x56 (extrapolated)"}
 
 
+NET_METRIC = {
+    "c1": "encrypted images/sec, dense 845->100 layer (BASELINE config 1), N=8192",
+    "c3": "encrypted images/sec, CryptoNets-ReLU, complex packing, client-aided ReLU on the GPU (BASELINE config 3)",
+}
+
+
+def net_run(args, ws, rank, local):
+    """BASELINE c1 (the dense layer, 4096 images, patched 'rescale after' plan, relin-free) or c3
+    (the CryptoNets-shaped network with ReLU under complex packing: 8192 images per ciphertext,
+    both ReLU layers refreshed client-aided by the GPU NonlinearityEngine).  Inputs are real
+    encryptions made on the GPU and stay resident; one step is one execute of the batch."""
+    import numpy as np
+    import torch
+    from paper_1908_04172_b200 import henet as H
+    from paper_1908_04172_b200 import workloads as Wk
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    which = args.workload
+    p = Wk.N8192
+    ctx = H.CkksContext(p["n"], p["chain"], p["special"], p["scale"], device=local)
+    wl = Wk.dense_layer() if which == "c1" else Wk.cryptonets_relu()
+    model = H.PlainModel.load(wl.manifest, wl.blob)
+    plan = H.RescalePlan.plan(ctx, model)
+    if wl.patch_terminal_rescale:  # config 1: one rescale per output (the harness's patch, ref_capi.cpp)
+        nodes = {}
+        planned = plan.planned_rescale_ops
+        for nid in ("input", "fc", "out"):
+            nodes[nid] = plan.node(nid)
+        dec, lin, lout, sc = nodes["fc"]
+        raised = nodes["input"][3] * p["scale"]
+        nodes["fc"] = (1, lin, lin - 1, raised / float(p["chain"][lin - 1]))
+        nodes["out"] = (nodes["out"][0], lin - 1, lin - 1, nodes["fc"][3])
+        plan = H.RescalePlan.from_nodes(0, planned + 100, nodes)
+    sk = c4_secret_key(H, ctx, p, 5 + rank)
+    samples = np.random.default_rng(6 + rank).random((wl.batch, wl.input_count))
+    x = H.encrypt_tensor(ctx, sk, samples, 7 + rank, wl.packing, shape=wl.input_shape)
+    eng = None
+    if which == "c3":
+        eng = H.RefreshEngine(ctx, sk, 99)
+    ctx.synchronize()
+    ext = torch.cuda.ExternalStream(ctx.stream(), device=local)
+    clocks = Clocks(local)
+    for _ in range(max(args.warmup, 1)):
+        out = H.execute(ctx, model, plan, x, None, eng)
+    ctx.synchronize()
+    steps = max(1, args.steps)
+    l0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(ext)
+    for _ in range(steps):
+        out = H.execute(ctx, model, plan, x, None, eng)
+    e1.record(ext)
+    e1.synchronize()
+    launches = ctx.launch_count() - l0
+    clk = clocks.stop()
+    t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=f"cuda:{local}")
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    value = ws * wl.batch / (ms / 1e3)
+    H.prof_enable(True)
+    H.execute(ctx, model, plan, x, None, eng)
+    ctx.synchronize()
+    H.prof_enable(False)
+    rep = H.prof_report()
+    tot = sum(v["ms"] for v in rep.values()) or 1.0
+    kernels = {k: {"ms_per_step": v["ms"], "launches": v["launches"], "share": v["ms"] / tot}
+               for k, v in sorted(rep.items(), key=lambda kv: -kv[1]["ms"])}
+    dec = H.decrypt_tensor(ctx, sk, out, wl.batch)  # decrypted outputs are finite
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import refbind as R
+            ref = R.RefContext(p["n"], p["chain"], p["special"], p["scale"])
+            keys = ref.keygen(5, False)
+            words, sc = ref.encrypt_tensor(keys, samples, 7, packing=wl.packing)
+            t0 = time.perf_counter()
+            ref.execute(keys if which == "c3" else None, wl.manifest, wl.blob, words, sc,
+                        patch=wl.patch_terminal_rescale, refresh_seed=99)
+            dt = time.perf_counter() - t0
+            cpu = {"value": wl.batch / dt, "unit": "images/s", "cores": os.cpu_count() or 1, "kind": "reference",
+                   "sample": f"one full {wl.batch}-image batch through henet::execute (oracle/_ref), {dt:.1f} s"}
+        except Exception as e:  # reported, not fatal
+            cpu = {"error": str(e)}
+    if rank == 0:
+        print(json.dumps({
+            "metric": NET_METRIC[which], "value": value, "unit": "images/s", "n_gpus": ws, "steps": steps,
+            "warmup": max(args.warmup, 1), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32 (RNS residues, 24/30-bit primes)",
+            "data": "synthetic U[0,1) images encrypted on the GPU; weights ~N(0, 0.05^2) f32",
+            "config": {"workload": "c1 dense 845->100 + bias, patched rescale-after plan" if which == "c1" else
+                       "c3 CryptoNets-ReLU (conv5x5/2 -> ReLU -> fc845x100 -> ReLU -> fc100x10), complex packing",
+                       "ring": "N=8192, chain [30,24x5]+30-bit special, scale 2^24",
+                       "images_per_step_per_gpu": wl.batch, "parallelism": f"replicas x{ws}",
+                       "refresh": "client-aided ReLU on the GPU (hg_refresh_engine)" if which == "c3" else None},
+            "kernels": kernels, "roofline": None, "cpu_baseline": cpu, "e2e": None, "gpu_launches": launches,
+            "clocks": clk, "check": {"decrypted_finite": bool(np.isfinite(dec).all())}}))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
@@ -891,6 +997,13 @@ def main():
         return c4_run(args, ws, rank, local)
     if args.workload == "c5b":
         return c5b_reference_run(args, ws, rank) if args.impl == "reference" else c5b_run(args, ws, rank, local)
+    if args.workload in ("c1", "c3"):
+        if args.impl == "reference":
+            if rank == 0:
+                print(json.dumps({"metric": NET_METRIC[args.workload], "impl": "reference",
+                                  "unavailable": "run the b200 arm: its cpu_baseline times the reference on the same batch"}))
+            return 0
+        return net_run(args, ws, rank, local)
     if args.impl == "reference":
         return reference_run(args, ws, rank)
     return b200_run(args, ws, rank, local)
