@@ -162,6 +162,31 @@ def test_refresh_engine_as_provider_cryptonets_relu(env, packing):
     assert np.array_equal(out.to_words(), want)
 
 
+def test_c3_packed_vs_unpacked_slot_for_slot(env):
+    """BASELINE c3's own check: the CryptoNets-ReLU network on 8192 images under complex
+    packing (two images per slot) against the same network on the two 4096-image halves under
+    real packing, all on the GPU (encrypt, execute with the GPU refresh engine, decrypt);
+    decrypted logits agree slot for slot within the north star's 1e-3, and each run is itself
+    bit-exact against the reference elsewhere (test_refresh_engine_as_provider_cryptonets_relu)."""
+    ctx, sk = env["ctx"], env["sk"]
+    imgs = W.synthetic_images([1, 28, 28], 8192, 17)
+    wl_c = W.cryptonets_relu(packing=1, batch=8192)
+    wl_r = W.cryptonets_relu(packing=0, batch=4096)
+    mc, mr = H.PlainModel.load(wl_c.manifest, wl_c.blob), H.PlainModel.load(wl_r.manifest, wl_r.blob)
+    xc = H.encrypt_tensor(ctx, sk, imgs, 18, 1, shape=wl_c.input_shape)
+    yc = H.execute(ctx, mc, H.RescalePlan.plan(ctx, mc), xc, None, H.RefreshEngine(ctx, sk, 99))
+    packed = H.decrypt_tensor(ctx, sk, yc, 8192)
+    halves = []
+    for h in range(2):
+        xr = H.encrypt_tensor(ctx, sk, imgs[h * 4096:(h + 1) * 4096], 19 + h, 0, shape=wl_r.input_shape)
+        yr = H.execute(ctx, mr, H.RescalePlan.plan(ctx, mr), xr, None, H.RefreshEngine(ctx, sk, 100 + h))
+        halves.append(H.decrypt_tensor(ctx, sk, yr, 4096))
+    unpacked = np.concatenate(halves, axis=0)
+    assert packed.shape == unpacked.shape == (8192, 10)
+    assert np.isfinite(packed).all()
+    assert float(np.abs(packed - unpacked).max()) < 1e-3
+
+
 # ---- wide contexts (BASELINE c4/c5b parameters: N = 16384, 40-bit limb 0, u64 residues) ----
 @pytest.fixture(scope="module")
 def wenv():
