@@ -315,6 +315,12 @@ int hg_execute(hg_ctx* ctx, const hg_model* m, const hg_plan* plan, const hg_ten
 int hg_last_exec_layer_count(uint32_t* n);
 int hg_last_exec_layer(uint32_t index, const char** id, double* ms);
 
+/* Host -> device bytes the most recent host-packed upload in this process put on the bus
+ * (hg_tensor_upload / _upload_segments / hg_tensor_deserialize of a u32 context): the packed
+ * chunks (3 bytes per residue of a prime < 2^24 when the host packs 24-bit words, else 4)
+ * plus the raw u64 share.  0 before any such upload.  (bench.py's h2d_bytes_per_step.) */
+int hg_last_upload_h2d_bytes(uint64_t* bytes);
+
 /* NonlinearityEngine / LocalProvider (henet/graph.hpp:699-752) on the GPU: decrypt and
  * decode every request ciphertext, ReLU or the per-slot window max, encode_vector at the
  * top level and default scale, encrypt with derive_seed(derive_seed(seed, layer_seq), g).

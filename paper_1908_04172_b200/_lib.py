@@ -133,6 +133,7 @@ PROTOTYPES = {
     "hg_last_exec_node_ms": (C.c_int, [vp, dblp]),
     "hg_last_exec_layer_count": (C.c_int, [u32p]),
     "hg_last_exec_layer": (C.c_int, [C.c_uint32, C.POINTER(C.c_char_p), dblp]),
+    "hg_last_upload_h2d_bytes": (C.c_int, [u64p]),
     "hg_prof_enable": (C.c_int, [C.c_int]),
     "hg_prof_report": (C.c_int, [C.c_char_p, C.c_uint64]),
 }

@@ -2729,6 +2729,13 @@ int hg_prof_report(char* buf, uint64_t cap) {
   });
 }
 
+int hg_last_upload_h2d_bytes(uint64_t* bytes) {
+  return guard([&] {
+    require(bytes != nullptr, "null argument");
+    *bytes = g_last_upload_h2d.load();
+  });
+}
+
 int hg_last_exec_layer_count(uint32_t* n) {
   return guard([&] {
     require(n != nullptr, "null argument");

@@ -47,6 +47,7 @@ struct DirectShare {
 };
 // fraction of ciphertexts hg_tensor_upload sends raw (HG_UPLOAD_DIRECT_FRAC, default 0.15)
 double upload_direct_fraction();
+extern std::atomic<uint64_t> g_last_upload_h2d;  // bytes of the last host-packed upload (hg_upload.cpp)
 bool host_narrow_upload(int device, const uint64_t* words, uint32_t* dst, uint64_t n_words, uint32_t level,
                         uint32_t N, const uint64_t* chain, cudaStream_t s, const uint8_t* const* segs = nullptr,
                         uint64_t seg_words = 0, const DirectShare* direct = nullptr);

@@ -95,6 +95,7 @@ struct Workers {
   std::vector<cudaStream_t> streams;
   std::vector<cudaEvent_t> events;  // [worker][slot]
   std::vector<u32*> stage;          // [worker][slot] pinned
+  std::vector<uint8_t*> dstage;     // [worker][slot] device staging of 24-bit-packed chunks
   cudaEvent_t start = nullptr;
   cudaStream_t direct = nullptr;    // the raw-u64 share: H2D + GPU narrowing
   std::mutex mu;                    // one upload at a time per device
@@ -123,6 +124,8 @@ Workers& workers(int device) {
     for (auto& e : w->events) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& p : w->stage)
       cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&p), kChunkWords * 4, cudaHostAllocPortable), "pinned stage");
+    w->dstage.resize(w->stage.size());
+    for (auto& p : w->dstage) cuda_check(cudaMalloc(reinterpret_cast<void**>(&p), kChunkWords * 4), "device stage");
     cuda_check(cudaEventCreateWithFlags(&w->start, cudaEventDisableTiming), "event");
     cuda_check(cudaStreamCreateWithFlags(&w->direct, cudaStreamNonBlocking), "stream");
   }
@@ -172,6 +175,97 @@ __attribute__((target("avx512f,avx512vl"))) inline bool pack_run_avx512(const u6
   return ok;
 }
 
+// 16 words -> 16 u32 lanes with each fourth byte dropped (48 valid bytes), range-checked
+__attribute__((target("avx512f,avx512vl,avx512bw,avx512vbmi"))) inline __m512i pack24_x16(const u64* p, __m512i qv,
+                                                                                          __m512i drop,
+                                                                                          __mmask8& bad) {
+  const __m512i a = _mm512_loadu_si512(p), b = _mm512_loadu_si512(p + 8);
+  bad |= _mm512_cmpge_epu64_mask(a, qv) | _mm512_cmpge_epu64_mask(b, qv);
+  return _mm512_permutexvar_epi8(
+      drop, _mm512_inserti64x4(_mm512_castsi256_si512(_mm512_cvtepi64_epi32(a)), _mm512_cvtepi64_epi32(b), 1));
+}
+
+// 24-bit limbs (q < 2^24, five of the six c2 primes) cross the bus as 3 bytes per residue:
+// per 64 words, eight 64-byte loads, eight unsigned compares against q, VPMOVQD to u32, VPERMB
+// to drop each fourth byte and two-source VPERMT2B to splice the 48-byte pieces into three
+// full 64-byte streaming stores.  dst 64-byte aligned, n % 64 == 0.
+__attribute__((target("avx512f,avx512vl,avx512bw,avx512vbmi"))) inline bool pack24_run_avx512(const u64* src,
+                                                                                               uint8_t* dst, u32 n,
+                                                                                               u32 q) {
+  alignas(64) static const uint8_t kDrop[64] = {0,  1,  2,  4,  5,  6,  8,  9,  10, 12, 13, 14, 16, 17, 18, 20,
+                                                21, 22, 24, 25, 26, 28, 29, 30, 32, 33, 34, 36, 37, 38, 40, 41,
+                                                42, 44, 45, 46, 48, 49, 50, 52, 53, 54, 56, 57, 58, 60, 61, 62,
+                                                0,  0,  0,  0,  0,  0,  0,  0,  0,  0,  0,  0,  0,  0,  0,  0};
+  alignas(64) static uint8_t kJ0[64], kJ1[64], kJ2[64];
+  static const bool init = [] {
+    for (int i = 0; i < 64; ++i) {
+      kJ0[i] = static_cast<uint8_t>(i < 48 ? i : 64 + (i - 48));       // p0[0..47] ++ p1[0..15]
+      kJ1[i] = static_cast<uint8_t>(i < 32 ? 16 + i : 64 + (i - 32));  // p1[16..47] ++ p2[0..31]
+      kJ2[i] = static_cast<uint8_t>(i < 16 ? 32 + i : 64 + (i - 16));  // p2[32..47] ++ p3[0..47]
+    }
+    return true;
+  }();
+  (void)init;
+  const __m512i drop = _mm512_load_si512(kDrop), j0 = _mm512_load_si512(kJ0), j1 = _mm512_load_si512(kJ1),
+                j2 = _mm512_load_si512(kJ2);
+  const __m512i qv = _mm512_set1_epi64(static_cast<long long>(q));
+  __mmask8 bad = 0;
+  for (u32 j = 0; j < n; j += 64) {
+    const __m512i p0 = pack24_x16(src + j, qv, drop, bad), p1 = pack24_x16(src + j + 16, qv, drop, bad),
+                  p2 = pack24_x16(src + j + 32, qv, drop, bad), p3 = pack24_x16(src + j + 48, qv, drop, bad);
+    __m512i* d = reinterpret_cast<__m512i*>(dst + 3 * j);
+    _mm512_stream_si512(d, _mm512_permutex2var_epi8(p0, j0, p1));
+    _mm512_stream_si512(d + 1, _mm512_permutex2var_epi8(p1, j1, p2));
+    _mm512_stream_si512(d + 2, _mm512_permutex2var_epi8(p2, j2, p3));
+  }
+  return bad == 0;
+}
+
+bool use_pack24() {
+  static const bool on = [] {
+    const char* e = getenv("HG_UPLOAD_PACK24");
+    if (e != nullptr && e[0] == '0') return false;
+    __builtin_cpu_init();
+    return __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512vl") &&
+           __builtin_cpu_supports("avx512bw") && __builtin_cpu_supports("avx512vbmi");
+  }();
+  return on;
+}
+
+// One block per limb run of a packed chunk: run r (global run R0 + r, limb (R0 + r) % level)
+// starts after the runs before it, 3 bytes per residue for the limbs in mask24, else 4.
+__global__ void k_unpack24(const uint8_t* packed, u32* dst, u32 N, u32 R0, u32 level, u32 mask24) {
+  const u32 r = blockIdx.x;
+  u64 off = 0;
+  for (u32 j = 0; j < r; ++j) off += static_cast<u64>(N) * (((mask24 >> ((R0 + j) % level)) & 1u) ? 3 : 4);
+  const bool w3 = (mask24 >> ((R0 + r) % level)) & 1u;
+  u32* out = dst + static_cast<u64>(r) * N;
+  if (w3) {
+    const uint4* in = reinterpret_cast<const uint4*>(packed + off);  // 16 residues per 48 bytes
+    for (u32 g = threadIdx.x; g < N / 16; g += blockDim.x) {
+      const uint4 a = in[3 * g], b = in[3 * g + 1], c = in[3 * g + 2];
+      const u32 w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+      u32 o[16];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const u32 b0 = w[3 * k], b1 = w[3 * k + 1], b2 = w[3 * k + 2];
+        o[4 * k] = b0 & 0xFFFFFFu;
+        o[4 * k + 1] = (b0 >> 24) | ((b1 & 0xFFFFu) << 8);
+        o[4 * k + 2] = (b1 >> 16) | ((b2 & 0xFFu) << 16);
+        o[4 * k + 3] = b2 >> 8;
+      }
+      uint4* d = reinterpret_cast<uint4*>(out + 16 * g);
+      d[0] = make_uint4(o[0], o[1], o[2], o[3]);
+      d[1] = make_uint4(o[4], o[5], o[6], o[7]);
+      d[2] = make_uint4(o[8], o[9], o[10], o[11]);
+      d[3] = make_uint4(o[12], o[13], o[14], o[15]);
+    }
+  } else {
+    const uint4* in = reinterpret_cast<const uint4*>(packed + off);
+    for (u32 g = threadIdx.x; g < N / 4; g += blockDim.x) reinterpret_cast<uint4*>(out)[g] = in[g];
+  }
+}
+
 bool use_avx512() {
   static const bool on = [] {
     const char* e = getenv("HG_UPLOAD_AVX512");
@@ -183,6 +277,8 @@ bool use_avx512() {
 }
 
 }  // namespace
+
+std::atomic<u64> g_last_upload_h2d{0};  // hg_last_upload_h2d_bytes
 
 double upload_direct_fraction() {
   static const double f = [] {
@@ -224,9 +320,14 @@ bool host_narrow_upload(int device, const u64* words, u32* dst, u64 n_words, u32
   }
   const int nw = W.pool->size();
   const bool avx512 = use_avx512();
+  u32 mask24 = 0;  // limbs whose residues cross the bus as 3 bytes
+  for (u32 l = 0; l < level && l < 32; ++l)
+    if (chain[l] < (1ull << 24)) mask24 |= 1u << l;
+  const bool pack24 = mask24 != 0 && level <= 32 && N % 64 == 0 && use_pack24();
   const u64 chunks = (n_words + kChunkWords - 1) / kChunkWords;
   std::atomic<bool> bad{false};
   std::atomic<int> err{0};
+  std::atomic<u64> h2d{direct != nullptr ? direct->words * 8 : 0};
   std::string err_msg;
   std::mutex err_mu;
   W.pool->run([&](int w) {
@@ -242,16 +343,37 @@ bool host_narrow_upload(int device, const u64* words, u32* dst, u64 n_words, u32
         if (used >= kSlots) cuda_check(cudaEventSynchronize(W.events[ei]), "event");
         u32* out = W.stage[ei];
         const u64 b = c * kChunkWords, e = std::min(n_words, b + kChunkWords);
+        u64 pbytes = 0;  // packed bytes of the chunk (pack24)
         for (u64 r = b; r < e; r += N) {  // one limb run of N words: a single prime
           // source run: contiguous words, or word (r % seg_words) of segment r / seg_words
           const u64* src = segs == nullptr
                                ? words + r
                                : reinterpret_cast<const u64*>(segs[r / seg_words] + (r % seg_words) * 8);
           const u32 q = static_cast<u32>(chain[(r / N) % level]);
-          my_bad |= avx512 ? !pack_run_avx512(src, out + (r - b), N, q) : !pack_run(src, out + (r - b), N, q);
+          if (pack24) {
+            uint8_t* ob = reinterpret_cast<uint8_t*>(out) + pbytes;
+            if (q < (1u << 24)) {
+              my_bad |= !pack24_run_avx512(src, ob, N, q);
+              pbytes += static_cast<u64>(N) * 3;
+            } else {
+              my_bad |= !pack_run_avx512(src, reinterpret_cast<u32*>(ob), N, q);
+              pbytes += static_cast<u64>(N) * 4;
+            }
+          } else {
+            my_bad |= avx512 ? !pack_run_avx512(src, out + (r - b), N, q) : !pack_run(src, out + (r - b), N, q);
+          }
         }
         _mm_sfence();  // the streaming stores are visible before the DMA reads the chunk
-        cuda_check(cudaMemcpyAsync(dst + b, out, (e - b) * 4, cudaMemcpyHostToDevice, ws), "h2d");
+        h2d += pack24 ? pbytes : (e - b) * 4;
+        if (pack24) {
+          // 3-byte residues over the bus, widened to u32 on the device (k_unpack24)
+          cuda_check(cudaMemcpyAsync(W.dstage[ei], out, pbytes, cudaMemcpyHostToDevice, ws), "h2d");
+          k_unpack24<<<static_cast<u32>((e - b) / N), 256, 0, ws>>>(W.dstage[ei], dst + b, N, static_cast<u32>(b / N),
+                                                                   level, mask24);
+          cuda_check(cudaGetLastError(), "unpack24");
+        } else {
+          cuda_check(cudaMemcpyAsync(dst + b, out, (e - b) * 4, cudaMemcpyHostToDevice, ws), "h2d");
+        }
         cuda_check(cudaEventRecord(W.events[ei], ws), "event");
       }
       if (my_bad) bad = true;
@@ -262,6 +384,7 @@ bool host_narrow_upload(int device, const u64* words, u32* dst, u64 n_words, u32
     }
   });
   if (err.load()) throw Error(HG_ERR_CUDA, err_msg);
+  g_last_upload_h2d = h2d.load();
   if (direct != nullptr && direct->words != 0) {
     int hbad = 0;
     cuda_check(cudaMemcpyAsync(&hbad, direct->bad, sizeof(int), cudaMemcpyDeviceToHost, W.direct), "d2h");

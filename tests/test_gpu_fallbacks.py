@@ -9,6 +9,7 @@ runs in its own subprocess and compares with the reference (oracle/_ref).
   HG_AUX_STREAM=0 special-prime key switch on the main stream
   HG_UPLOAD_HOST_NARROW=0  hg_tensor_upload copies u64 words and narrows them on the GPU
   HG_UPLOAD_DIRECT_FRAC=0 / 1  host packing only / everything raw through the GPU narrowing
+  HG_UPLOAD_PACK24=0 / HG_UPLOAD_AVX512=0  u32 bus words / the SSE2 packer
   HG_CONV1X1_DOT=0  1x1 convolutions on the tap-gather kernel instead of the batched Dot
   HG_TC_PPC=3     3 positions per CTA in the batched Dot (ragged last chunk)
   HG_DWCONV=0     depthwise (grouped 1 -> 1) wide convolutions on the tap-gather kernel
@@ -111,6 +112,8 @@ print("OK")
     ({"HG_UPLOAD_HOST_NARROW": "0"}, "toy"),
     ({"HG_UPLOAD_DIRECT_FRAC": "0"}, "toy"),
     ({"HG_UPLOAD_DIRECT_FRAC": "1"}, "toy"),
+    ({"HG_UPLOAD_PACK24": "0"}, "toy"),
+    ({"HG_UPLOAD_AVX512": "0", "HG_UPLOAD_PACK24": "0"}, "toy"),
     ({"HG_WIDE_TC": "0"}, "wide"),
     ({"HG_DENSE_TC": "0"}, "wide"),
     ({"HG_CONV1X1_DOT": "0"}, "c4lin"),
