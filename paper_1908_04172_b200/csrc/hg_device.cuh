@@ -26,6 +26,9 @@ using i32 = int32_t;
 
 constexpr int kMaxPrimes = 24;
 
+#ifndef HG_DEBUG_CHECKS
+#define HG_DEBUG_CHECKS 0  // self-check build: mbarrier wait timeouts and TMEM allocation checks trap
+#endif
 #ifndef HG_NTT_TWS_MINB
 #define HG_NTT_TWS_MINB 4  // ... and the kernels with staged pass-B twiddles (Ntt<LOGN, true>)
 #endif
@@ -183,6 +186,9 @@ struct TmemScratch {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
     const u32 w = tid >> 5;
+#if HG_DEBUG_CHECKS
+    if (((*slot) >> 16) != 0 || ((*slot) & 0xFFFFu) + kCols > 512u) __trap();  // self-check build
+#endif
     base = *slot + (((w & 3) * 32) << 16) + (w >> 2) * 64;
   }
   __device__ __forceinline__ void free(u32 tid) {

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "hg_tc.hpp"
@@ -64,6 +65,9 @@ constexpr int tc_stages() { return TN == 64 ? 5 : 4; }
 // shallower to stay within 227 KB, the wide TN = 32 ring 3 deep so two CTAs fit per SM.
 template <int TN, typename XW>
 constexpr int tc_xs() { return sizeof(XW) == 8 ? (TN == 64 ? kTcXS - 1 : 3) : kTcXS; }
+#ifndef HG_DEBUG_CHECKS
+#define HG_DEBUG_CHECKS 0
+#endif
 #ifndef HG_TC_XPAD64
 #define HG_TC_XPAD64 0  // u64 staging rows unpadded (c5b: 61.3 vs 64.0 ms with 4 words of padding)
 #endif
@@ -113,11 +117,41 @@ __device__ __forceinline__ void mbar_init(unsigned long long* b, u32 count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(b)), "r"(count));
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, u32 parity) {
+#if HG_DEBUG_CHECKS
+  // self-check build (compute-sanitizer is not available on this pool): a wait that never
+  // completes -- a phase/arrival-count bug -- traps instead of hanging the GPU
+  for (u32 i = 0;; ++i) {
+    u32 done;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_addr(b)), "r"(parity));
+    if (done) return;
+    if (i == (1u << 24)) {
+      printf("hg debug: mbarrier wait timed out (block %d thread %d parity %u)\n", blockIdx.x, threadIdx.x, parity);
+      __trap();
+    }
+  }
+#else
   asm volatile(
       "{\n.reg .pred p;\nLAB_WAIT%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra LAB_WAIT%=;\n}\n" ::"r"(smem_addr(b)),
       "r"(parity));
+#endif
+}
+
+// self-check build: the TMEM allocation lies inside the 512 columns, at lane 0
+__device__ __forceinline__ void tmem_check(u32 base, u32 cols) {
+#if HG_DEBUG_CHECKS
+  if ((base >> 16) != 0 || (base & 0xFFFFu) + cols > 512u) {
+    printf("hg debug: bad TMEM allocation %08x (%u columns)\n", base, cols);
+    __trap();
+  }
+#else
+  (void)base;
+  (void)cols;
+#endif
 }
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(b)));
@@ -201,6 +235,7 @@ __global__ void __launch_bounds__(kTcThreads, TN == 64 ? 1 : 2) k_mac_dense_tc(M
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
   const u32 tmem = S.tmem;
+  tmem_check(tmem, kCols);
 
   if (warp == kTcProducers / 32) {
     // ===== weight loader + MMA issuer (one lane) =====
@@ -545,6 +580,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mac_dense_tc_w(MacDenseTcWArg
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
   const u32 tmem = S.tmem;
+  tmem_check(tmem, kTcCols);
 
   if (warp == kTcProducers / 32) {
     if (lane == 0) {
