@@ -33,11 +33,12 @@ struct CrtTables {
   u64 q_half[kCrtWords + 1];                // floor(Q / 2)
   u64 ginv[kCrtLimbs][kCrtLimbs];           // Garner: q_j^-1 mod q_i (j < i)
   u64 q[kCrtLimbs];                         // the level's primes
-  // Two-limb fast path (wide contexts, k_dec_crt): when q_0 q_1 > 2^66, the centred value of
-  // (r_0, r_1) is the answer iff it matches every other residue -- checked exactly.
-  u32 fast2;
-  u64 q01_lo, q01_hi;                       // q_0 q_1
-  u64 q01_mod[kCrtLimbs];                   // q_0 q_1 mod q_i
+  // K-limb fast path (k_dec_crt): the centred CRT of (r_0 .. r_{K-1}) is the answer iff it
+  // matches every other residue -- checked exactly.  fastk = 0 disables it.
+  u32 fastk;
+  u64 q01_lo, q01_hi;                       // q_0 .. q_{K-1}
+  u64 q01_mod[kCrtLimbs];                   // q_0 .. q_{K-1} mod q_i
+  u64 t64[kCrtLimbs];                       // 2^64 mod q_i (u32 contexts)
 };
 
 struct DecArgs {

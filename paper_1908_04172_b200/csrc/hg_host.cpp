@@ -2955,18 +2955,28 @@ void decode_into(const Context& c, const hg_secret_key* sk, const void* ct, u64 
     a.words = static_cast<u32>(big.size());
     for (u32 k = 0; k < a.words; ++k) a.crt.big_q[k] = big[k];
     for (u32 k = 0; k < a.words; ++k) a.crt.q_half[k] = (big[k] >> 1) | (k + 1 < a.words ? (big[k + 1] << 63) : 0);
-    a.crt.fast2 = 0;
+    a.crt.fastk = 0;
     static const bool fast_on = [] {
       const char* e = getenv("HG_CRT_FAST");
       return !(e != nullptr && e[0] == '0');
     }();
-    if (fast_on && c.wide && L > 2) {
-      const nt::u128 q01 = static_cast<nt::u128>(c.chain[0]) * c.chain[1];
-      if ((q01 >> 66) != 0) {
-        a.crt.fast2 = 1;
-        a.crt.q01_lo = static_cast<u64>(q01);
-        a.crt.q01_hi = static_cast<u64>(q01 >> 64);
-        for (u32 i = 0; i < L; ++i) a.crt.q01_mod[i] = static_cast<u64>(q01 % c.chain[i]);
+    if (fast_on) {
+      // the fewest leading limbs whose product exceeds 2^66 (wide c4/c5b: 2; the 30/24-bit
+      // chains: 3), as long as it stays below 2^127 and leaves limbs to check
+      nt::u128 qk = 1;
+      u32 K = 0;
+      while (K < L && K < 3 && (qk >> 66) == 0) {
+        qk *= c.chain[K];
+        ++K;
+      }
+      if ((qk >> 66) != 0 && (qk >> 126) == 0 && K < L) {
+        a.crt.fastk = K;
+        a.crt.q01_lo = static_cast<u64>(qk);
+        a.crt.q01_hi = static_cast<u64>(qk >> 64);
+        for (u32 i = 0; i < L; ++i) {
+          a.crt.q01_mod[i] = static_cast<u64>(qk % c.chain[i]);
+          a.crt.t64[i] = static_cast<u64>((static_cast<nt::u128>(1) << 64) % c.chain[i]);
+        }
       }
     }
     {

@@ -147,6 +147,19 @@ def test_refresh_engine_bit_exact(env, kind, window, packing):
         assert np.array_equal(got.to_words(), want)
 
 
+def test_decrypt_crt_fast_path_and_fallback_bit_exact_u32(env):
+    """The decoder's three-limb CRT fast path on the 30/24-bit chain (q_0 q_1 q_2 ~ 2^78) and
+    its full-Garner fallback (uniform residues: coefficients near Q / 2) in one tensor."""
+    ctx, ref, keys, sk, p = env["ctx"], env["ref"], env["keys"], env["sk"], env["p"]
+    samples = np.random.default_rng(23).normal(0, 1, (4096, 3))
+    fresh, sc = ref.encrypt_tensor(keys, samples, 24)
+    mixed = np.concatenate([fresh, W.random_ciphertexts(p, 3, seed=25)], axis=0)
+    t = H.CipherTensor.from_words(ctx, mixed, sc)
+    got = H.decrypt_tensor(ctx, sk, t, 4096)
+    want = ref.decrypt_tensor(keys, mixed, sc, 0, 4096)
+    assert np.array_equal(got, want, equal_nan=True)
+
+
 @pytest.mark.parametrize("packing", [1, 0])
 def test_refresh_engine_as_provider_cryptonets_relu(env, packing):
     """c3 (CryptoNets-ReLU, client-aided refresh) executed with the GPU engine as provider."""
