@@ -414,8 +414,10 @@ __global__ void __launch_bounds__(128) k_mac_conv_w(MacConvArgsW a, BasisW B) {
 // are re-read from L1 -- instead of one 128-thread CTA per (position, slice) with nine loads
 // each (the tap-gather k_mac_conv_w).  Same sums: taps in (ky, kx) order, padding skipped,
 // 30-bit limbs as u64 IMAD.WIDE sums folded every 8 taps, wider limbs in 128 bits.
-// WIN: the window (3 for MobileNetV2), compile-time so the taps unroll with their
-// row/column validity tests hoisted out of the tap loop.
+// WIN: the window (3 for MobileNetV2), compile-time.  Along each output row the thread keeps
+// the WIN x WIN input window in registers and slides it one column per output (WIN new loads
+// instead of WIN^2); taps outside the input enter as zeros, which add nothing to the exact
+// sums (the tap-gather kernel skips them), so the results are the same residues.
 template <int WIN>
 __global__ void __launch_bounds__(128) k_dwconv_w(MacConvArgsW a, BasisW B) {
   constexpr int T2 = WIN * WIN;
@@ -435,23 +437,44 @@ __global__ void __launch_bounds__(128) k_dwconv_w(MacConvArgsW a, BasisW B) {
   const bool narrow = P.q < (1ull << 30);
   const u64 r32 = narrow ? (1ull << 32) % P.q : 0;
   const bool fold = a.fold[limb] != 0;
+  auto ld = [&](int iy, int ix) {
+    if (iy < 0 || iy >= static_cast<int>(a.IH) || ix < 0 || ix >= static_cast<int>(a.IW))
+      return make_ulonglong2(0, 0);
+    return __ldg(reinterpret_cast<const ulonglong2*>(X + (static_cast<u64>(iy) * a.IW + static_cast<u32>(ix)) * xstride));
+  };
   for (u32 oy = 0; oy < a.OH; ++oy) {
     const int iy0 = static_cast<int>(oy * a.stride) - static_cast<int>(a.pad_top);
+    const int ix00 = -static_cast<int>(a.pad_left);
+    ulonglong2 xw[WIN][WIN];  // [ky][kx] window of the current output
+#pragma unroll
+    for (int ky = 0; ky < WIN; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < WIN; ++kx) xw[ky][kx] = ld(iy0 + ky, ix00 + kx);
     for (u32 ox = 0; ox < a.OW; ++ox) {
-      const int ix0 = static_cast<int>(ox * a.stride) - static_cast<int>(a.pad_left);
+      if (ox > 0) {  // slide: stride columns shift in (stride 1 for MobileNetV2)
+        const int ixn = static_cast<int>(ox * a.stride) - static_cast<int>(a.pad_left);
+        if (a.stride == 1) {
+#pragma unroll
+          for (int ky = 0; ky < WIN; ++ky) {
+#pragma unroll
+            for (int kx = 0; kx + 1 < WIN; ++kx) xw[ky][kx] = xw[ky][kx + 1];
+            xw[ky][WIN - 1] = ld(iy0 + ky, ixn + WIN - 1);
+          }
+        } else {
+#pragma unroll
+          for (int ky = 0; ky < WIN; ++ky)
+#pragma unroll
+            for (int kx = 0; kx < WIN; ++kx) xw[ky][kx] = ld(iy0 + ky, ixn + kx);
+        }
+      }
       u64 s0 = 0, s1 = 0;
       Acc128 c0{0, 0}, c1{0, 0};
       u32 cnt = 0;
 #pragma unroll
-      for (int ky = 0; ky < WIN; ++ky) {
-        const int iy = iy0 + ky;
-        if (iy < 0 || iy >= static_cast<int>(a.IH)) continue;
-        const u64* Xr = X + static_cast<u64>(iy) * a.IW * xstride;
+      for (int ky = 0; ky < WIN; ++ky)
 #pragma unroll
         for (int kx = 0; kx < WIN; ++kx) {
-          const int ix = ix0 + kx;
-          if (ix < 0 || ix >= static_cast<int>(a.IW)) continue;
-          const ulonglong2 xv = __ldg(reinterpret_cast<const ulonglong2*>(Xr + static_cast<u64>(ix) * xstride));
+          const ulonglong2 xv = xw[ky][kx];
           const u64 wt = w[ky * WIN + kx];
           if (narrow) {
             s0 += static_cast<u64>(static_cast<u32>(xv.x)) * static_cast<u32>(wt);
@@ -469,11 +492,10 @@ __global__ void __launch_bounds__(128) k_dwconv_w(MacConvArgsW a, BasisW B) {
             }
           }
         }
-      }
       u64 o0, o1;
       if (narrow) {
-        o0 = barrett128(s0, 0, P);
-        o1 = barrett128(s1, 0, P);
+        o0 = red64(s0, P);
+        o1 = red64(s1, P);
       } else {
         o0 = barrett128(c0.lo, c0.hi, P);
         o1 = barrett128(c1.lo, c1.hi, P);
