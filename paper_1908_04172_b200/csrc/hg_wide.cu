@@ -506,6 +506,129 @@ __global__ void __launch_bounds__(128) k_dwconv_w(MacConvArgsW a, BasisW B) {
   }
 }
 
+// Depthwise with the whole (channel, poly, limb) input tile of 64 coefficients staged in
+// shared memory (IH IW x 64 u64, 51 KB for the c4 10 x 10 tile): every input word is read
+// from HBM once (the per-thread walk of k_dwconv_w re-read rows from DRAM once the CTAs in
+// flight outgrew L2), then warp w computes outputs w, w + 8, ... from shared memory, lane =
+// coefficient pair (512 contiguous bytes per warp load and store).  Same exact sums.
+// MODE (block-uniform, chosen per limb): 0 = primes < 2^30, u64 IMAD.WIDE sums folded every
+// 8 taps; 1 = primes <= 2^40 (c4's limb 0) as 20-bit halves, x w = xl wl + (xl wh + xh wl)
+// 2^20 + xh wh 2^40 with every partial sum of <= 25 products < 2^46 in a u64 (four
+// IMAD.WIDE.U32 per tap); 2 = any prime, 128-bit sums.
+template <int WIN, int MODE>
+__device__ __forceinline__ void dw_outputs(const MacConvArgsW& a, const DevPrimeW& P, const ulonglong2* dws,
+                                           const u64 (&w)[WIN * WIN], u64 bv, u64* Y, u64 ystride, u32 lane,
+                                           u32 grp) {
+  constexpr int T2 = WIN * WIN;
+  const u64 r32 = MODE == 0 ? (1ull << 32) % P.q : 0;
+  const u32 nout = a.OH * a.OW;
+  u32 oy = grp / a.OW, ox = grp % a.OW;  // advanced incrementally (no division per output)
+  for (u32 o = grp; o < nout; o += 8) {
+    const int iy0 = static_cast<int>(oy * a.stride) - static_cast<int>(a.pad_top);
+    const int ix0 = static_cast<int>(ox * a.stride) - static_cast<int>(a.pad_left);
+    bool rok[WIN], cok[WIN];
+#pragma unroll
+    for (int k = 0; k < WIN; ++k) {
+      rok[k] = static_cast<u32>(iy0 + k) < a.IH;
+      cok[k] = static_cast<u32>(ix0 + k) < a.IW;
+    }
+    const int base = iy0 * static_cast<int>(a.IW) + ix0;
+    u64 s0 = 0, s1 = 0, m0 = 0, m1 = 0, h0 = 0, h1 = 0;
+    Acc128 c0{0, 0}, c1{0, 0};
+    u32 cnt = 0;
+#pragma unroll
+    for (int ky = 0; ky < WIN; ++ky) {
+      const int rowb = base + ky * static_cast<int>(a.IW);
+#pragma unroll
+      for (int kx = 0; kx < WIN; ++kx) {
+        const bool ok = rok[ky] && cok[kx];  // a padding tap adds zero
+        const ulonglong2 xv = ok ? dws[static_cast<u32>(rowb + kx) * 32 + lane] : make_ulonglong2(0, 0);
+        const u64 wt = w[ky * WIN + kx];
+        if constexpr (MODE == 0) {
+          s0 += static_cast<u64>(static_cast<u32>(xv.x)) * static_cast<u32>(wt);
+          s1 += static_cast<u64>(static_cast<u32>(xv.y)) * static_cast<u32>(wt);
+          if (T2 > 8 && (++cnt & 7) == 0) {
+            s0 = (s0 & 0xffffffffull) + (s0 >> 32) * r32;
+            s1 = (s1 & 0xffffffffull) + (s1 >> 32) * r32;
+          }
+        } else if constexpr (MODE == 1) {
+          const u32 wl = static_cast<u32>(wt & 0xFFFFF), wh = static_cast<u32>(wt >> 20);
+          const u32 al = static_cast<u32>(xv.x & 0xFFFFF), ah = static_cast<u32>(xv.x >> 20);
+          const u32 bl = static_cast<u32>(xv.y & 0xFFFFF), bh = static_cast<u32>(xv.y >> 20);
+          s0 += static_cast<u64>(al) * wl;
+          m0 += static_cast<u64>(al) * wh + static_cast<u64>(ah) * wl;
+          h0 += static_cast<u64>(ah) * wh;
+          s1 += static_cast<u64>(bl) * wl;
+          m1 += static_cast<u64>(bl) * wh + static_cast<u64>(bh) * wl;
+          h1 += static_cast<u64>(bh) * wh;
+        } else {
+          mac128(c0, xv.x, wt);
+          mac128(c1, xv.y, wt);
+          if (T2 > 8 && (++cnt & 7) == 0) {  // keep r + 8 (q-1)^2 < 2^128 for primes near 2^62
+            c0 = {barrett128(c0.lo, c0.hi, P), 0};
+            c1 = {barrett128(c1.lo, c1.hi, P), 0};
+          }
+        }
+      }
+    }
+    u64 o0, o1;
+    if constexpr (MODE == 0) {
+      o0 = red64(s0, P);
+      o1 = red64(s1, P);
+    } else if constexpr (MODE == 1) {
+      // l + m 2^20 + h 2^40 as (lo, hi) words, then the reference's 128-bit Barrett
+      auto join = [&](u64 l, u64 m, u64 h) {
+        const u64 ml = m << 20, mh = m >> 44, hl = h << 40, hh = h >> 24;
+        const u64 lo = l + ml;
+        u64 hi = mh + (lo < ml ? 1 : 0);
+        const u64 lo2 = lo + hl;
+        hi += hh + (lo2 < hl ? 1 : 0);
+        return barrett128(lo2, hi, P);
+      };
+      o0 = join(s0, m0, h0);
+      o1 = join(s1, m1, h1);
+    } else {
+      o0 = barrett128(c0.lo, c0.hi, P);
+      o1 = barrett128(c1.lo, c1.hi, P);
+    }
+    *reinterpret_cast<ulonglong2*>(Y + static_cast<u64>(o) * ystride) =
+        make_ulonglong2(addmod_w(o0, bv, P.q), addmod_w(o1, bv, P.q));
+    ox += 8;
+    while (ox >= a.OW) {
+      ox -= a.OW;
+      ++oy;
+    }
+  }
+}
+
+template <int WIN>
+__global__ void __launch_bounds__(256) k_dwconv_ws(MacConvArgsW a, BasisW B) {
+  extern __shared__ ulonglong2 dws[];  // [IH IW][32] coefficient pairs
+  constexpr int T2 = WIN * WIN;
+  const u32 g = blockIdx.z;
+  const u32 poly = blockIdx.y / a.level, limb = blockIdx.y % a.level;
+  const u32 n0 = blockIdx.x * 64, lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const DevPrimeW& P = B.p[limb];
+  const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
+  const u64 ystride = static_cast<u64>(a.polys) * a.level * a.N;
+  const u64* X = a.X + g * a.gx + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n0 + 2 * lane;
+  u64* Y = a.Y + g * a.gy + (static_cast<u64>(poly) * a.level + limb) * a.N + n0 + 2 * lane;
+  const u32 npos = a.IH * a.IW;
+  for (u32 pi = grp; pi < npos; pi += 8)
+    dws[pi * 32 + lane] = __ldg(reinterpret_cast<const ulonglong2*>(X + static_cast<u64>(pi) * xstride));
+  u64 w[T2];
+#pragma unroll
+  for (int t = 0; t < T2; ++t) w[t] = __ldg(&a.W[g * a.gw + limb * T2 + t]);
+  const u64 bv = (a.bias != nullptr && poly == 0) ? __ldg(&a.bias[g * a.gb + limb]) : 0;
+  __syncthreads();
+  if (P.q < (1ull << 30))
+    dw_outputs<WIN, 0>(a, P, dws, w, bv, Y, ystride, lane, grp);
+  else if (P.q <= (1ull << 40) && T2 <= 25)
+    dw_outputs<WIN, 1>(a, P, dws, w, bv, Y, ystride, lane, grp);
+  else
+    dw_outputs<WIN, 2>(a, P, dws, w, bv, Y, ystride, lane, grp);
+}
+
 // ---------------------------------------------------------------------------
 // Element-wise
 // ---------------------------------------------------------------------------
@@ -905,6 +1028,19 @@ int launch_mac_conv_w(const MacConvArgsW& a, const BasisW& B, cudaStream_t s) {
   }();
   if (dw_on && a.groups > 1 && a.C == 1 && a.F == 1 && (a.win == 3 || a.win == 5) && a.groups <= 65535 &&
       a.polys * a.level <= 65535) {
+    const size_t sm = static_cast<size_t>(a.IH) * a.IW * 32 * sizeof(ulonglong2);
+    static const bool smem_on = [] {
+      const char* e = getenv("HG_DWCONV_SMEM");
+      return !(e != nullptr && e[0] == '0');
+    }();
+    if (smem_on && sm <= 112 * 1024 && a.N % 64 == 0) {  // input tile in shared memory
+      auto k = a.win == 3 ? k_dwconv_ws<3> : k_dwconv_ws<5>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+      dim3 grid(a.N / 64, a.polys * a.level, a.groups);
+      ProfScope ps_("k_dwconv_w", s);
+      k<<<grid, 256, sm, s>>>(a, B);
+      return 1;
+    }
     dim3 grid(a.N / 256, a.polys * a.level, a.groups);
     ProfScope ps_("k_dwconv_w", s);
     if (a.win == 3)

@@ -13,6 +13,7 @@ runs in its own subprocess and compares with the reference (oracle/_ref).
   HG_CONV1X1_DOT=0  1x1 convolutions on the tap-gather kernel instead of the batched Dot
   HG_TC_PPC=3     3 positions per CTA in the batched Dot (ragged last chunk)
   HG_DWCONV=0     depthwise (grouped 1 -> 1) wide convolutions on the tap-gather kernel
+  HG_DWCONV_SMEM=0  the depthwise kernel without the shared-memory input tile
   HG_NTT_W32=0    wide NTTs all on the 64-bit transform
   HG_FFT_CLUSTER=0  N = 2^14 encode/decode FFTs on one CTA in global memory (no 2-CTA cluster)
   HG_CRT_FAST=0   the decoder's full Garner CRT for every coefficient
@@ -120,6 +121,7 @@ print("OK")
     ({"HG_WIDE_TC": "0"}, "c4lin"),
     ({"HG_TC_PPC": "3"}, "c4lin"),
     ({"HG_DWCONV": "0"}, "c4lin"),
+    ({"HG_DWCONV_SMEM": "0"}, "c4lin"),
     ({"HG_NTT_W32": "0"}, "c4lin"),
     ({"HG_FFT_CLUSTER": "0"}, "c4refresh"),
     ({"HG_CRT_FAST": "0"}, "c4refresh"),
