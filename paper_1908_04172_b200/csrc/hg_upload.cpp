@@ -120,14 +120,22 @@ Workers& workers(int device) {
     w->streams.resize(n);
     w->events.resize(static_cast<size_t>(n) * kSlots);
     w->stage.resize(static_cast<size_t>(n) * kSlots);
-    for (int i = 0; i < n; ++i) cuda_check(cudaStreamCreateWithFlags(&w->streams[i], cudaStreamNonBlocking), "stream");
+    // the upload's small kernels (24-bit unpack, raw-share narrowing) run at the highest stream
+    // priority, so an execute already filling the SMs does not hold the next step's input back
+    // (HG_UPLOAD_PRIORITY=0: default priority)
+    int lo_pri = 0, hi_pri = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
+    const char* pe = getenv("HG_UPLOAD_PRIORITY");
+    const int pri = (pe != nullptr && pe[0] == '0') ? 0 : hi_pri;
+    for (int i = 0; i < n; ++i)
+      cuda_check(cudaStreamCreateWithPriority(&w->streams[i], cudaStreamNonBlocking, pri), "stream");
     for (auto& e : w->events) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& p : w->stage)
       cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&p), kChunkWords * 4, cudaHostAllocPortable), "pinned stage");
     w->dstage.resize(w->stage.size());
     for (auto& p : w->dstage) cuda_check(cudaMalloc(reinterpret_cast<void**>(&p), kChunkWords * 4), "device stage");
     cuda_check(cudaEventCreateWithFlags(&w->start, cudaEventDisableTiming), "event");
-    cuda_check(cudaStreamCreateWithFlags(&w->direct, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithPriority(&w->direct, cudaStreamNonBlocking, pri), "stream");
   }
   return *w;
 }
