@@ -42,3 +42,33 @@ def test_upload_rejects_out_of_range_any_chunk(ctx, where):
         x[60, 0, 2, 100] = np.uint64(1) << np.uint64(32)
     with pytest.raises(H.ValidationError, match="residue out of range"):
         H.CipherTensor.from_words(ctx, x, 1.0)
+
+
+def test_upload_max_residues_round_trip(ctx):
+    """All-(q - 1) words: the largest 24-bit residue needs all 3 bus bytes (pack24) and the
+    30-bit limb all 4."""
+    p = W.N8192
+    q = np.array(p["chain"], dtype=np.uint64)[None, None, :, None]
+    x = np.broadcast_to(q - np.uint64(1), (40, 2, len(p["chain"]), p["n"])).copy()
+    t = H.CipherTensor.from_words(ctx, x, 1.0)
+    assert np.array_equal(t.to_words(), x)
+
+
+def test_upload_reports_bus_bytes(ctx):
+    """hg_last_upload_h2d_bytes: the raw share (HG_UPLOAD_DIRECT_FRAC of the ciphertexts, u64)
+    plus the packed chunks -- 3 bytes per residue of a prime < 2^24 when the host packs 24-bit
+    words (AVX-512 VBMI), else 4."""
+    import ctypes
+    import os
+    p = W.N8192
+    count, L, n = 300, 6, p["n"]
+    x = W.random_ciphertexts(p, count, seed=9, level=L)
+    H.CipherTensor.from_words(ctx, x, 1.0)
+    got = ctypes.c_uint64(0)
+    H.lib.hg_last_upload_h2d_bytes(ctypes.byref(got))
+    f = float(os.environ.get("HG_UPLOAD_DIRECT_FRAC", "0.15"))
+    direct = int(count * f)
+    per_res_4 = 2 * L * n * 4
+    per_res_p = 2 * n * sum(3 if q < (1 << 24) else 4 for q in p["chain"][:L])
+    raw = direct * 2 * L * n * 8
+    assert got.value in (raw + (count - direct) * per_res_4, raw + (count - direct) * per_res_p), got.value
