@@ -733,10 +733,15 @@ static BufPtr encode_vectors_dev(const Context& ctx, const double* d_slots, u32 
                             static_cast<ulonglong2*>(mags->ptr), d_mant, d_exp, s);
   check_launch(r, "fft encode");
   if (ctx.wide) {
-    r = launch_mags_to_residues_w(static_cast<const ulonglong2*>(mags->ptr), count, n, level,
-                                  static_cast<u64*>(out->ptr), ctx.basisw, s);
-    check_launch(r, "residues");
-    r = launch_ntt_w(static_cast<int>(ctx.logn), static_cast<u64*>(out->ptr), count * level, level, false, ctx.basisw, s);
+    r = launch_pt_residues_ntt_w(static_cast<int>(ctx.logn), static_cast<const ulonglong2*>(mags->ptr), count, level,
+                                 static_cast<u64*>(out->ptr), ctx.basisw, s);
+    if (r == -2) {
+      r = launch_mags_to_residues_w(static_cast<const ulonglong2*>(mags->ptr), count, n, level,
+                                    static_cast<u64*>(out->ptr), ctx.basisw, s);
+      check_launch(r, "residues");
+      r = launch_ntt_w(static_cast<int>(ctx.logn), static_cast<u64*>(out->ptr), count * level, level, false,
+                       ctx.basisw, s);
+    }
   } else {
     r = launch_mags_to_residues(static_cast<const ulonglong2*>(mags->ptr), count, n, level,
                                 static_cast<u32*>(out->ptr), ctx.basis, s);

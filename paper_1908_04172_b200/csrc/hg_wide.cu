@@ -1100,14 +1100,15 @@ int launch_encode_scalars_w_f64(const double* vals, u64 count, u32 row_len, u32 
 
 namespace hg {
 
-__global__ void k_mags_to_residues_w(const ulonglong2* mags, u64 count_n, u32 n, u32 level, u64* out, BasisW B) {
+__global__ void k_mags_to_residues_w(const ulonglong2* mags, u64 count_n, u32 n, u32 level, u32 lcount, u64* out,
+                                     BasisW B) {
   const u64 idx = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= count_n) return;
   const ulonglong2 m = mags[idx];
   const bool neg = (m.y >> 63) != 0;
   const u64 hi = m.y & ~(1ull << 63);
   const u64 pt = idx / n, k = idx % n;
-  for (u32 i = 0; i < level; ++i) {
+  for (u32 i = 0; i < lcount; ++i) {  // limbs [0, lcount)
     const DevPrimeW& P = B.p[i];
     u64 r = barrett128(m.x, hi, P);
     if (neg && r != 0) r = P.q - r;
@@ -1115,12 +1116,82 @@ __global__ void k_mags_to_residues_w(const ulonglong2* mags, u64 count_n, u32 n,
   }
 }
 
+// encode's residues (the signed 128-bit magnitudes mod q, henet/encoding.hpp:160-168) fused
+// into the plaintext NTT for the limbs below 2^30: each (plaintext, limb) CTA reduces its
+// coefficients' magnitudes as it loads them (X mod q = (hi mod q)(2^64 mod q) + lo mod q) and
+// writes only the NTT-domain residues -- no residue array round trip through HBM.
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? 4 : HG_NTT14_MINB))
+    k_pt_ntt_w32(const ulonglong2* mags, u64* out, u32 level, u32 lo, Basis B) {
+  using NT = Ntt<LOGN, true>;
+  extern __shared__ u32 sm32[];
+  const u32 tid = threadIdx.x;
+  const u32 cnt = level - lo;
+  const u64 pt = blockIdx.x / cnt;
+  const u32 limb = lo + blockIdx.x % cnt;
+  const DevPrime& P = B.p[limb];
+  const u32 t64 = mulmod(P.r32, P.r32, P);  // 2^64 mod q
+  const ulonglong2* mg = mags + pt * NT::N;
+  u32 x[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const ulonglong2 m = __ldg(&mg[NT::jA(tid, k)]);
+    const bool neg = (m.y >> 63) != 0;
+    const u32 r = addmod(reduce64(m.x, P), mulmod(reduce64(m.y & ~(1ull << 63), P), t64, P), P.q);
+    x[k] = (neg && r != 0) ? P.q - r : r;
+  }
+  NT::forward(x, sm32, tid, P);
+  u64* o = out + (pt * level + limb) * NT::N;
+#pragma unroll
+  for (int k = 0; k < 32; k += 4) {
+    ulonglong2* d = reinterpret_cast<ulonglong2*>(o + NT::jC(tid, k));
+    d[0] = make_ulonglong2(x[k], x[k + 1]);
+    d[1] = make_ulonglong2(x[k + 2], x[k + 3]);
+  }
+}
+
+int launch_pt_residues_ntt_w(int logn, const ulonglong2* mags, u64 count, u32 level, u64* out, const BasisW& B,
+                             cudaStream_t s) {
+  static const bool on = [] {
+    const char* e = getenv("HG_ENCODE_FUSE");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  const u32 lo = wide_narrow_lo(B, level);
+  if (!on || count == 0 || lo >= level) return -2;
+  const u32 n = 1u << logn;
+  int launches = 0;
+  if (lo > 0) {  // the wide limbs: residues, then their u64 NTT
+    const u64 total = count * n;
+    {
+      ProfScope ps_("k_mags_to_residues_w", s);
+      k_mags_to_residues_w<<<(total + 255) / 256, 256, 0, s>>>(mags, total, n, level, lo, out, B);
+    }
+    ++launches;
+  }
+  HG_LOGN_SWITCH_W(logn, {
+    if (lo > 0) {
+      const size_t sm = sizeof(u64) * NttW<LN>::SMEM_WORDS;
+      set_smem_w(k_ntt_w<LN, false>, sm);
+      ProfScope ps_("k_ntt_w", s);
+      k_ntt_w<LN, false><<<count * lo, 1 << (LN - 5), sm, s>>>(out, level, 0, lo, B);
+      ++launches;
+    }
+    const size_t sm = sizeof(u32) * Ntt<LN, true>::SMEM_WORDS;
+    set_smem_w(k_pt_ntt_w32<LN>, sm);
+    ProfScope ps_("k_pt_ntt_w32", s);
+    k_pt_ntt_w32<LN><<<count * (level - lo), 1 << (LN - 5), sm, s>>>(mags, out, level, lo,
+                                                                     *static_cast<const Basis*>(B.narrow));
+    ++launches;
+  });
+  return launches;
+}
+
 int launch_mags_to_residues_w(const ulonglong2* mags, u64 count, u32 n, u32 level, u64* out, const BasisW& B,
                               cudaStream_t s) {
   const u64 total = count * n;
   if (total == 0) return 0;
   { ProfScope ps_("k_mags_to_residues_w", s);
-  k_mags_to_residues_w<<<(total + 255) / 256, 256, 0, s>>>(mags, total, n, level, out, B);
+  k_mags_to_residues_w<<<(total + 255) / 256, 256, 0, s>>>(mags, total, n, level, level, out, B);
   }
   return 1;
 }

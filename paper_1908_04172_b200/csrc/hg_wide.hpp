@@ -91,6 +91,10 @@ u32 wide_narrow_lo(const BasisW& B, u32 level);
 // limbs [lo, level) transformed and combined into c0 in one kernel; -2 without such a suffix
 int launch_enc_ntt_w(int logn, u64* ct, u64* err, const u64* pt, const u64* sk, u64 count, u32 level,
                      const BasisW& B, cudaStream_t s);
+// encode's signed magnitudes -> NTT-domain residues: limbs [lo, level) reduced and transformed in
+// one kernel, the wide limbs by k_mags_to_residues_w + the u64 NTT; -2 without such a suffix
+int launch_pt_residues_ntt_w(int logn, const ulonglong2* mags, u64 count, u32 level, u64* out, const BasisW& B,
+                             cudaStream_t s);
 int launch_dec_intt_w(int logn, const u64* ct, const u64* sk, u64* m, u64 count, u32 polys, u32 level,
                       const BasisW& B, cudaStream_t s);
 int launch_rescale_w(int logn, const RescaleArgsW& a, const BasisW& B, cudaStream_t s);

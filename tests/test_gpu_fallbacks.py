@@ -18,6 +18,7 @@ runs in its own subprocess and compares with the reference (oracle/_ref).
   HG_FFT_CLUSTER=0  N = 2^14 encode/decode FFTs on one CTA in global memory (no 2-CTA cluster)
   HG_CRT_FAST=0   the decoder's full Garner CRT for every coefficient
   HG_DEC_FUSE=0 / HG_ENC_FUSE=0  decrypt combine / encrypt combine as separate kernels
+  HG_ENCODE_FUSE=0  encode's residues as a separate kernel before the plaintext NTT
 """
 import os
 import subprocess
@@ -126,6 +127,7 @@ print("OK")
     ({"HG_FFT_CLUSTER": "0"}, "c4refresh"),
     ({"HG_CRT_FAST": "0"}, "c4refresh"),
     ({"HG_DEC_FUSE": "0", "HG_ENC_FUSE": "0"}, "c4refresh"),
+    ({"HG_ENCODE_FUSE": "0"}, "c4refresh"),
     ({}, "c4refresh"),
     ({}, "c4lin"),
 ])
