@@ -28,11 +28,14 @@ def launches(path):
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += v
-    # bench.py's roofline-denominator probes are not part of the step: listed, not shared
-    tot = sum(v[1] for k, v in agg.items() if "probe" not in k)
+    # bench.py's roofline-denominator probes and the target's input upload (host-packed chunks
+    # widened on the device, raw share narrowed) are not part of the step: listed, not shared
+    upload = ("k_unpack24", "k_narrow")
+    side = lambda k: "probe" in k or any(u in k for u in upload)
+    tot = sum(v[1] for k, v in agg.items() if not side(k))
     out = ["| kernel | launches | total (ncu units) | share of the step's kernels |", "|---|---:|---:|---:|"]
     for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
-        share = "(peak probe)" if "probe" in k else f"{v[1] / tot:.3f}"
+        share = "(peak probe)" if "probe" in k else ("(input upload)" if side(k) else f"{v[1] / tot:.3f}")
         out.append(f"| {k} | {v[0]} | {v[1]:.1f} | {share} |")
     return "\n".join(out)
 
