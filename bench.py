@@ -169,7 +169,9 @@ def work_model(n=8192):
         # 2 inverse transforms of the special accumulators, 2 key products per digit/limb
         add("k_relin_keysw", modmul=C_ * ((l * l + 2) * bf + 2 * l * (l + 1) * n),
             byts=C_ * (l * n * W + 2 * l * n * W + 2 * n * W) + key_bytes)
-        add("k_relin_moddown", modmul=C_ * (2 * (l + 1) * bf + (6 * l - 2) * n),
+        # mod-down with the rescale merged: per polynomial l-1 forward transforms (kept limbs)
+        # and one inverse (the dropped limb, INTT(d + acc P^-1) - cps P^-1)
+        add("k_relin_moddown", modmul=C_ * (2 * l * bf + (6 * l - 2) * n),
             byts=C_ * (2 * l * n * W + 2 * l * n * W + 2 * n * W + 2 * (l - 1) * n * W))
     # fc1 845 -> 100 at level 4, fc2 100 -> 10 at level 2
     dense_macs = 845 * 100 * 2 * 4 * n + 100 * 10 * 2 * 2 * n

@@ -41,6 +41,30 @@ constexpr int kMaxPrimes = 24;
 #ifndef HG_KEYSW_MINB
 #define HG_KEYSW_MINB 4  // key switch: accumulators in TMEM (4 x 128 columns), 41 KB smem
 #endif
+#ifndef HG_KEYSW_PREFETCH
+#define HG_KEYSW_PREFETCH 1  // next digit loaded into registers during the key products
+#endif
+#ifndef HG_BFLY_ALU_ADD
+#define HG_BFLY_ALU_ADD 1  // butterfly sum X + T as an ALU-pipe min(X + T, ~0) (keeps ptxas from IMAD.IADD)
+#endif
+// Timing-only switches (results are wrong; used to attribute kernel time, never shipped)
+#ifndef HG_T_NOF
+#define HG_T_NOF 0
+#endif
+#ifndef HG_T_NOBAR
+#define HG_T_NOBAR 0
+#endif
+#ifndef HG_T_NOXCHG
+#define HG_T_NOXCHG 0
+#endif
+#if HG_T_NOBAR
+#define HG_NTT_SYNC() ((void)0)
+#else
+#define HG_NTT_SYNC() __syncthreads()
+#endif
+#ifndef HG_MODDOWN_TOPINV
+#define HG_MODDOWN_TOPINV 1  // merged rescale: the dropped limb takes one INTT, not NTT + INTT
+#endif
 #ifndef HG_MODDOWN_PREFETCH
 #define HG_MODDOWN_PREFETCH 1  // accumulator row loaded before the transform (registers)
 #endif
@@ -140,6 +164,18 @@ __device__ __forceinline__ u32 mulmod(u32 a, u32 b, const DevPrime& P) {
   u32 r = static_cast<u32>(x) - __umulhi(xs, P.bmu) * P.q;
   r = min(r, r - P.two_q);  // [0, 3q) -> [0, 2q)
   return csub(r, P.q);
+}
+
+// Butterfly sum.  HG_BFLY_ALU_ADD: issued as one VIADDMNMX (ALU pipe) so that ptxas cannot
+// turn it into IMAD.IADD on the fma pipe, which bounds the transforms.
+__device__ __forceinline__ u32 bfly_add(u32 a, u32 b) {
+#if HG_BFLY_ALU_ADD
+  u32 r;
+  asm("{\n\t.reg .u32 t;\n\tadd.u32 t, %1, %2;\n\tmin.u32 %0, t, %3;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(0xFFFFFFFFu));
+  return r;
+#else
+  return a + b;
+#endif
 }
 
 __device__ __forceinline__ u32 addmod(u32 a, u32 b, u32 q) { return csub(a + b, q); }
@@ -428,7 +464,7 @@ struct Ntt {
             const int k1 = k0 | (1 << rb);
             u32 X = x[k0];
             X = min(X, X - q2);
-            x[k0] = X + Tm[m];
+            x[k0] = bfly_add(X, Tm[m]);
             x[k1] = X - Tm[m] + q2;
             ++m;
           }
@@ -518,17 +554,29 @@ struct Ntt {
     TwB twB;
     load_rowB(twB, P.fwdB, sm, tid, stage_twiddles);  // in flight during pass A
     fwd_pass<0>(x, P, twB);
-    __syncthreads();
+    HG_NTT_SYNC();
+#if !HG_T_NOXCHG
     store<0>(x, sm, tid);
-    __syncthreads();
+#endif
+    HG_NTT_SYNC();
+#if !HG_T_NOXCHG
     load<1>(x, sm, tid);
+#endif
     fwd_pass<1>(x, P, twB);
+#if !HG_T_NOXCHG
     store<1>(x, sm, tid);
+#endif
     uint2 f[FC];
+#if !HG_T_NOF
     load_F(f, P.fwdT, tid);  // while x is in shared memory: the loads cross the barrier
-    __syncthreads();
+#endif
+    HG_NTT_SYNC();
+#if !HG_T_NOXCHG
     load<2>(x, sm, tid);
+#endif
+#if !HG_T_NOF
     apply_F(x, f, P.q);
+#endif
     fwd_pass<2>(x, P, twB);
     const u32 q = P.q, q2 = P.two_q;
 #pragma unroll

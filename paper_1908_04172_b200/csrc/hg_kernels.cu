@@ -674,8 +674,10 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_KEYSW_MINB :
   // test inside it makes ptxas duplicate the transform (instruction-cache misses).
   const u32 skip = special ? L : t;
   const u32 R = special ? L : L - 1;
+#if HG_KEYSW_PREFETCH
   u32 nx[32];
   NT::gload_P(nx, a.D + (ct * L + (skip == 0 ? 1 : 0)) * N, tid);
+#endif
   NT::stage_rowsB(P.fwdB, sm, tid);  // ordered before pass B by the transform's first barrier
 #pragma unroll 1
   for (u32 r = 0; r < R; ++r) {
@@ -684,8 +686,13 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_KEYSW_MINB :
     // and returns canonical values, so only a digit of a prime >= 4 q_t needs reducing
     // (the 30-bit limb 0 under a 24-bit target).
     u32 y[32];
+#if HG_KEYSW_PREFETCH
 #pragma unroll
     for (int k = 0; k < 32; ++k) y[k] = nx[k];
+#else
+    // no register prefetch: the other resident CTAs cover the load (and no 32-register copy)
+    NT::gload_P(y, a.D + (ct * L + j) * N, tid);
+#endif
     // (always reduced in the special-prime kernel: a branch there makes ptxas duplicate the
     // transform, and that kernel runs 1/(l+1) of the transforms)
     if (special || (B.p[j].q >> 2) >= q) {
@@ -693,8 +700,10 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_KEYSW_MINB :
       for (int k = 0; k < 32; ++k) y[k] = reduce32(y[k], P);
     }
     NT::forward(y, sm, tid, P, false);  // one prime per CTA: pass-B twiddles staged once, above
+#if HG_KEYSW_PREFETCH
     const u32 jn = min(r + 1 + (r + 1 >= skip ? 1 : 0), L - 1);
     NT::gload_P(nx, a.D + (ct * L + jn) * N, tid);
+#endif
     mac(y, j);
   }
   TmemScratch<T>::wait_st();
@@ -801,13 +810,50 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_MODDOWN_MINB
                       static_cast<u32>(v.x), static_cast<u32>(v.y), static_cast<u32>(v.z), static_cast<u32>(v.w)};
     tm.st8(4 * c, w);
   }
+#if HG_MODDOWN_TOPINV
+  if constexpr (RS) {
+    // Top limb L-1 (dropped by the merged rescale): only its coefficient-domain value is
+    // needed, for the rescale correction.  INTT is linear, so
+    //   INTT(d + (acc - NTT(cps)) P^-1) = INTT(d + acc P^-1) - cps P^-1,
+    // one inverse transform instead of a forward and an inverse one.
+    const u32 i = L - 1;
+    const DevPrime& Pi = B.p[i];
+    const u32 q = Pi.q, pv = a.pinvP[i], ps = a.pinvP_sh[i], pm = a.pmP[i];
+    u32 y[32];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(accp + static_cast<u64>(i) * N + NT::jC(tid, 4 * g)));
+      const uint4 d = load_d4<MD>(a, ct, poly, i, NT::jC(tid, 4 * g), N, Pi);
+      y[4 * g] = addmod(d.x, mul_shoup(v.x, pv, ps, q), q);
+      y[4 * g + 1] = addmod(d.y, mul_shoup(v.y, pv, ps, q), q);
+      y[4 * g + 2] = addmod(d.z, mul_shoup(v.z, pv, ps, q), q);
+      y[4 * g + 3] = addmod(d.w, mul_shoup(v.w, pv, ps, q), q);
+    }
+    NT::inverse(y, sm, tid, Pi);  // layout A, canonical: the layout of the cps cells
+    TmemScratch<T>::wait_st();
+#pragma unroll
+    for (int c = 0; c < 32; c += 8) {
+      u32 u[8], w[8];
+      tm.ld8(c, u);
+      TmemScratch<T>::wait_ld();
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        w[e] = static_cast<u32>(centered_round_rem(submod(y[c + e], mul_shoup(u[e] + pm, pv, ps, q), q), Pi));
+      tm.st8(32 + c, w);
+    }
+  }
+  constexpr bool kTopInLoop = false;
+#else
+  constexpr bool kTopInLoop = RS;
+#endif
   // One loop, one inlined forward transform (the kernel body otherwise overflows the
-  // instruction cache): iteration 0 is the top limb L-1, whose mod-down result feeds the
-  // rescale correction; iterations 1.. are limbs 0..L-2.
+  // instruction cache).  kTopInLoop (HG_MODDOWN_TOPINV=0): iteration 0 is the top limb
+  // L-1, whose mod-down result feeds the rescale correction; iterations 1.. are limbs
+  // 0..L-2.
 #pragma unroll 1
-  for (u32 it = 0; it < L; ++it) {
-    const bool top = (it == 0);
-    const u32 i = top ? L - 1 : it - 1;
+  for (u32 it = (RS && !kTopInLoop) ? 1 : 0; it < L; ++it) {
+    const bool top = kTopInLoop && (it == 0);
+    const u32 i = RS ? (it == 0 ? L - 1 : it - 1) : it;
     const DevPrime& Pi = B.p[i];
     const u32 q = Pi.q, pv = a.pinvP[i], ps = a.pinvP_sh[i];
     // Transform inputs, lazily reduced (the forward transform takes values < 4q):

@@ -49,6 +49,13 @@ CASES = [
     (16, 5, 6, 24, 1, 1, (0, 0, 0, 0), 6, True, False),    # MobileNetV2 project-like, ragged 5x6
     (40, 3, 4, 130, 1, 1, (0, 0, 0, 0), 6, True, True),    # 2 k steps, 2 M tiles, all (q-1)
     (4, 6, 6, 3, 1, 2, (0, 0, 0, 0), 6, False, False),     # 1x1 stride 2: tap-gather kernel
+    # single channel, 5x5, stride 2 (the CryptoNets first-layer family): padding on every side, ragged outputs
+    (1, 28, 28, 5, 5, 2, (1, 1, 0, 0), 6, True, True),     # c2 conv1 padded top-left, bias, all (q-1)
+    (1, 12, 11, 8, 5, 2, (2, 1, 1, 2), 6, True, False),    # F = 8, 6 x 5 outputs
+    (1, 7, 9, 3, 5, 2, (0, 0, 0, 0), 6, False, False),     # 2 x 3 outputs
+    (1, 5, 5, 1, 5, 2, (0, 0, 0, 0), 6, True, False),      # one output position, F = 1
+    (1, 9, 10, 2, 5, 2, (2, 2, 2, 2), 6, True, True),      # 5 x 5 outputs, padding all round, all (q-1)
+    (1, 10, 9, 7, 5, 2, (0, 1, 1, 0), 6, False, False),    # F = 7
 ]
 
 
