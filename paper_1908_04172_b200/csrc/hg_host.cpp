@@ -2289,9 +2289,11 @@ int hg_relin_key_upload(hg_ctx* ctx, const uint64_t* words, uint64_t n_words, hg
         for (u64 t = 0; t <= L; ++t) {
           const u64 q = c.basis_mod(t);
           const u64 base = ((j * 2 + p) * (L + 1) + t) * n;
+          // chain columns carry the mod-down's P^-1 (hg::kKeyPinv)
+          const u64 fold = (kKeyPinv && t < L) ? nt::inv(c.special % q, q) : 1;
           for (u64 i = 0; i < n; ++i) {
-            const u64 w = words[base + i];
-            require(w < q, "residue out of range");
+            require(words[base + i] < q, "residue out of range");
+            const u64 w = static_cast<u64>(static_cast<nt::u128>(words[base + i]) * fold % q);
             if (kKeyShoup)
               reinterpret_cast<uint2*>(k.data())[base + i] = make_uint2(static_cast<u32>(w), nt::shoup(w, q));
             else

@@ -824,10 +824,12 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_MODDOWN_MINB
     for (int g = 0; g < 8; ++g) {
       const uint4 v = __ldg(reinterpret_cast<const uint4*>(accp + static_cast<u64>(i) * N + NT::jC(tid, 4 * g)));
       const uint4 d = load_d4<MD>(a, ct, poly, i, NT::jC(tid, 4 * g), N, Pi);
-      y[4 * g] = addmod(d.x, mul_shoup(v.x, pv, ps, q), q);
-      y[4 * g + 1] = addmod(d.y, mul_shoup(v.y, pv, ps, q), q);
-      y[4 * g + 2] = addmod(d.z, mul_shoup(v.z, pv, ps, q), q);
-      y[4 * g + 3] = addmod(d.w, mul_shoup(v.w, pv, ps, q), q);
+      // accP: acc * P^-1, canonical (the accumulators carry it already under kKeyPinv)
+      auto accP = [&](u32 w) { return kKeyPinv ? w : mul_shoup(w, pv, ps, q); };
+      y[4 * g] = addmod(d.x, accP(v.x), q);
+      y[4 * g + 1] = addmod(d.y, accP(v.y), q);
+      y[4 * g + 2] = addmod(d.z, accP(v.z), q);
+      y[4 * g + 3] = addmod(d.w, accP(v.w), q);
     }
     NT::inverse(y, sm, tid, Pi);  // layout A, canonical: the layout of the cps cells
     TmemScratch<T>::wait_st();
@@ -879,8 +881,10 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_MODDOWN_MINB
         u32 u[8];
         tm.ld8(c, u);
         TmemScratch<T>::wait_ld();
+        // kKeyPinv: the transform of cps * P^-1 (lazy, < 2q), to be subtracted from acc * P^-1
 #pragma unroll
-        for (int e = 0; e < 8; ++e) z[c + e] = reduce32(u[e] + pm, Pi);
+        for (int e = 0; e < 8; ++e)
+          z[c + e] = kKeyPinv ? mul_shoup_lazy(u[e] + pm, pv, ps, q) : reduce32(u[e] + pm, Pi);
       }
     }
     // accumulator loads issued ahead of the transform; d products computed after it
@@ -905,20 +909,29 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_MODDOWN_MINB
         uint4 o;
         // (d + acc * P^-1 - z) * q_{L-1}^-1 with a lazy inner product: < 4q + q, any u32
         // input is fine for the outer Shoup multiplication, which returns canonical
-        o.x = mul_shoup(d.x + mul_shoup_lazy(v.x, pv, ps, q) + q - z[k], lv, ls, q);
-        o.y = mul_shoup(d.y + mul_shoup_lazy(v.y, pv, ps, q) + q - z[k + 1], lv, ls, q);
-        o.z = mul_shoup(d.z + mul_shoup_lazy(v.z, pv, ps, q) + q - z[k + 2], lv, ls, q);
-        o.w = mul_shoup(d.w + mul_shoup_lazy(v.w, pv, ps, q) + q - z[k + 3], lv, ls, q);
+        auto accP = [&](u32 w) { return kKeyPinv ? w : mul_shoup_lazy(w, pv, ps, q); };
+        o.x = mul_shoup(d.x + accP(v.x) + q - z[k], lv, ls, q);
+        o.y = mul_shoup(d.y + accP(v.y) + q - z[k + 1], lv, ls, q);
+        o.z = mul_shoup(d.z + accP(v.z) + q - z[k + 2], lv, ls, q);
+        o.w = mul_shoup(d.w + accP(v.w) + q - z[k + 3], lv, ls, q);
         *reinterpret_cast<uint4*>(out_i + NT::jC(tid, k)) = o;
       }
     } else {
 #pragma unroll
       for (int k = 0; k < 32; k += 4) {
         const uint4 d = dd[k >> 2], v = HG_MD_V(k >> 2);
-        z[k] = addmod(d.x, mul_shoup(v.x + q - z[k], pv, ps, q), q);
-        z[k + 1] = addmod(d.y, mul_shoup(v.y + q - z[k + 1], pv, ps, q), q);
-        z[k + 2] = addmod(d.z, mul_shoup(v.z + q - z[k + 2], pv, ps, q), q);
-        z[k + 3] = addmod(d.w, mul_shoup(v.w + q - z[k + 3], pv, ps, q), q);
+        // d + (acc - NTT(cps)) P^-1; kKeyPinv: both terms carry P^-1 already, d + v + q - z < 3q
+        auto fin = [&](u32 dd, u32 vv, u32 zz) {
+          if (kKeyPinv) {
+            const u32 r = dd + vv + q - zz;
+            return csub(min(r, r - Pi.two_q), q);
+          }
+          return addmod(dd, mul_shoup(vv + q - zz, pv, ps, q), q);
+        };
+        z[k] = fin(d.x, v.x, z[k]);
+        z[k + 1] = fin(d.y, v.y, z[k + 1]);
+        z[k + 2] = fin(d.z, v.z, z[k + 2]);
+        z[k + 3] = fin(d.w, v.w, z[k + 3]);
       }
       if (!RS) {
         NT::gstore_C(z, out_i, tid);

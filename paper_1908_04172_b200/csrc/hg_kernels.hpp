@@ -61,6 +61,15 @@ struct MacConvArgs {
 // key-switch L1 traffic; the products then use the one-IMAD.HI product Barrett).
 constexpr bool kKeyShoup = HG_KEY_SHOUP != 0;
 
+// Relinearisation key columns t < chain_len stored pre-multiplied by P^-1 mod q_t (done once at
+// upload): the key-switch accumulators then already carry the mod-down's 1/P, one modular
+// product per coefficient and limb less in k_relin_moddown.  The special-prime column is
+// unchanged (its accumulators are the mod-down's rounding corrections).
+#ifndef HG_KEY_PINV
+#define HG_KEY_PINV 1
+#endif
+constexpr bool kKeyPinv = HG_KEY_PINV != 0;
+
 struct RelinArgs {
   const u32* A;   // mode 0: size-3 ciphertexts; mode 1: left operand (size 2)
   const u32* Bm;  // mode 1: right operand (size 2); may equal A (square)
@@ -69,7 +78,7 @@ struct RelinArgs {
   u32 level;
   u32 chain_len;
   u32* D;         // digits   [count][level][N]
-  u32* ACC;       // key-switch accumulators [count][2][level][N]
+  u32* ACC;       // key-switch accumulators [count][2][level][N] (times P^-1 when kKeyPinv)
   i32* CORR;      // special-prime corrections [count][2][N]
   const void* key;   // [chain][2][chain+1][N]: uint2 (value, shoup) if kKeyShoup, else u32 value
   u32* out;       // [count][2][level or level-1][N]
