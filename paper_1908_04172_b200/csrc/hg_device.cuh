@@ -65,11 +65,16 @@ constexpr int kMaxPrimes = 24;
 #ifndef HG_MODDOWN_TOPINV
 #define HG_MODDOWN_TOPINV 1  // merged rescale: the dropped limb takes one INTT, not NTT + INTT
 #endif
+// Mod-down: 4 CTAs per SM at 64 registers without a register prefetch of the accumulator row.
+// With the dropped limb's single INTT and the P^-1 factor folded into the key the body fits 64
+// registers without spills; alone it is as fast as 3 CTAs per SM (0.31 vs 0.30 ms per c2 step,
+// 0.32 for the old 2 CTAs/SM + prefetch at 127 registers), and its small CTAs share SMs better
+// with the other half-batch's key switch: step 1.891 -> 1.834 ms (profiles/r3_experiments.md).
 #ifndef HG_MODDOWN_PREFETCH
-#define HG_MODDOWN_PREFETCH 1  // accumulator row loaded before the transform (registers)
+#define HG_MODDOWN_PREFETCH 0  // 1: accumulator row loaded before the transform (registers)
 #endif
 #ifndef HG_MODDOWN_MINB
-#define HG_MODDOWN_MINB 2  // mod-down: its accumulator prefetch needs > 80 registers
+#define HG_MODDOWN_MINB 4
 #endif
 #ifndef HG_NTT14_MINB
 #define HG_NTT14_MINB 2  // N = 2^14 transforms (512 threads): 2 CTAs per SM, 64 registers
