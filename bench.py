@@ -353,11 +353,15 @@ def b200_run(args, ws, rank, local):
         for l in lanes[1:nl]:
             l[4].wait_event(e0)
         outs = []
+        marks = []  # per-step completion events (each on its lane's stream)
         for i in range(k):
-            c_, rk_, plan_, inp_, _ = lanes[i % nl]
+            c_, rk_, plan_, inp_, st_ = lanes[i % nl]
             outs.append(H.execute(c_, model, plan_, inp_, rk_))
             if len(outs) > 2 * nl:
                 outs.pop(0)
+            m = torch.cuda.Event(enable_timing=True)
+            m.record(st_)
+            marks.append(m)
         for l in lanes[1:nl]:
             ev = torch.cuda.Event()
             ev.record(l[4])
@@ -366,6 +370,11 @@ def b200_run(args, ws, rank, local):
         e1.synchronize()
         nlaunch = sum(l[0].launch_count() for l in lanes) - l0
         dev = e0.elapsed_time(e1)
+        # completion-to-completion intervals: their median is the steady step time, a large
+        # maximum a stall (a host hiccup that let the launch queue run dry)
+        done = sorted(e0.elapsed_time(m) for m in marks)
+        gaps = [b - a for a, b in zip([0.0] + done[:-1], done)]
+        timed_steps.intervals = {"median_ms": statistics.median(gaps), "max_ms": max(gaps)}
         host = (time.perf_counter() - t0) * 1e3
         torch.cuda.synchronize()
         t = torch.tensor([dev], dtype=torch.float64, device=f"cuda:{local}")
@@ -382,6 +391,7 @@ def b200_run(args, ws, rank, local):
         out = lane_step(i)
     torch.cuda.synchronize()
     max_ms, host_ms, launches, out = timed_steps(n_lanes, args.steps)
+    step_intervals = timed_steps.intervals
     clk = clocks.stop()
     ms_per_step = max_ms / args.steps
     value = IMAGES_PER_STEP * ws / (ms_per_step / 1e3)
@@ -593,6 +603,7 @@ def b200_run(args, ws, rank, local):
             "batches_in_flight": n_lanes,
             "lanes": f"the {args.steps} timed steps alternate over {n_lanes} contexts (one stream each) on the GPU; "
                      "every step is one full 4096-image batch"}
+        line["step_completion_intervals"] = step_intervals
         if one_lane:
             line["one_batch_in_flight"] = one_lane
         print(json.dumps(line))

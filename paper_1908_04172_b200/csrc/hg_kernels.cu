@@ -786,7 +786,8 @@ __device__ __forceinline__ uint4 load_d4(const RelinArgs& a, u64 ct, u32 poly, u
 // MD selects the d0/d1 source (load_d4), RS whether the rescale is merged: one
 // instantiation per combination keeps each kernel body inside the instruction cache.
 template <int LOGN, int MD, bool RS>
-__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_MODDOWN_MINB : 1)) k_relin_moddown(RelinArgs a, Basis B) {
+__global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? (MD == 2 && HG_MODDOWN_MINB > 3 ? 3 : HG_MODDOWN_MINB) : 1))
+    k_relin_moddown(RelinArgs a, Basis B) {  // MD == 2 (four input rows per limb) spills at 64 registers
   using NT = Ntt<LOGN, true>;
   constexpr int N = NT::N;
   constexpr int T = NT::T;
