@@ -374,7 +374,8 @@ def b200_run(args, ws, rank, local):
         # maximum a stall (a host hiccup that let the launch queue run dry)
         done = sorted(e0.elapsed_time(m) for m in marks)
         gaps = [b - a for a, b in zip([0.0] + done[:-1], done)]
-        timed_steps.intervals = {"median_ms": statistics.median(gaps), "max_ms": max(gaps)}
+        timed_steps.intervals = {"median_ms": statistics.median(gaps), "max_ms": max(gaps),
+                                 "ms": [round(g, 3) for g in gaps] if len(gaps) <= 64 else None}
         host = (time.perf_counter() - t0) * 1e3
         torch.cuda.synchronize()
         t = torch.tensor([dev], dtype=torch.float64, device=f"cuda:{local}")

@@ -693,9 +693,9 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_KEYSW_MINB :
     // no register prefetch: the other resident CTAs cover the load (and no 32-register copy)
     NT::gload_P(y, a.D + (ct * L + j) * N, tid);
 #endif
-    // (always reduced in the special-prime kernel: a branch there makes ptxas duplicate the
-    // transform, and that kernel runs 1/(l+1) of the transforms)
-    if (special || (B.p[j].q >> 2) >= q) {
+    // (the same test in the special-prime kernel: with P of the size of the largest chain
+    // prime no digit needs reducing there)
+    if ((B.p[j].q >> 2) >= q) {
 #pragma unroll
       for (int k = 0; k < 32; ++k) y[k] = reduce32(y[k], P);
     }

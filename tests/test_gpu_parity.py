@@ -173,6 +173,34 @@ def test_execute_toy_bit_exact(env):
     _run_both(env, W.toy_cryptonets())
 
 
+def test_two_contexts_interleaved_bit_exact(env):
+    """Two contexts on one GPU (bench.py's lanes: independent batches in flight on two streams),
+    executes issued alternately without synchronising in between: every result equals the
+    reference's, so the lanes' kernels share the device (TMEM, auxiliary stream) safely."""
+    p, ref, keys = env["p"], env["ref"], env["keys"]
+    wl = W.toy_cryptonets()
+    model = H.PlainModel.load(wl.manifest, wl.blob)
+    lanes, wants = [], []
+    for lane in range(2):
+        imgs = W.synthetic_images(wl.input_shape, wl.batch, 40 + lane)
+        words, sc = ref.encrypt_tensor(keys, imgs, 50 + lane, packing=wl.packing)
+        want, want_sc, _ = ref.execute(keys, wl.manifest, wl.blob, words, sc, refresh_seed=99)
+        ctx = env["ctx"] if lane == 0 else H.CkksContext(p["n"], p["chain"], p["special"], p["scale"])
+        rk = env["rk"] if lane == 0 else H.RelinKey(ctx, keys.rk_words())
+        plan = H.RescalePlan.plan(ctx, model)
+        inp = H.CipherTensor.from_words(ctx, words, sc, packing=wl.packing, shape=wl.input_shape)
+        lanes.append((ctx, rk, plan, inp))
+        wants.append((want, want_sc))
+    outs = []
+    for i in range(8):
+        ctx, rk, plan, inp = lanes[i % 2]
+        outs.append(H.execute(ctx, model, plan, inp, rk))
+    for i, out in enumerate(outs):
+        want, want_sc = wants[i % 2]
+        assert out.scale == want_sc
+        assert np.array_equal(out.to_words(), want), i
+
+
 def test_execute_c1_dense_bit_exact(env):
     _run_both(env, W.dense_layer())
 
