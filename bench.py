@@ -354,9 +354,12 @@ def b200_run(args, ws, rank, local):
             l[4].wait_event(e0)
         outs = []
         marks = []  # per-step completion events (each on its lane's stream)
+        calls = []  # host time of every execute call
         for i in range(k):
             c_, rk_, plan_, inp_, st_ = lanes[i % nl]
+            tc = time.perf_counter()
             outs.append(H.execute(c_, model, plan_, inp_, rk_))
+            calls.append((time.perf_counter() - tc) * 1e3)
             if len(outs) > 2 * nl:
                 outs.pop(0)
             m = torch.cuda.Event(enable_timing=True)
@@ -375,7 +378,8 @@ def b200_run(args, ws, rank, local):
         done = sorted(e0.elapsed_time(m) for m in marks)
         gaps = [b - a for a, b in zip([0.0] + done[:-1], done)]
         timed_steps.intervals = {"median_ms": statistics.median(gaps), "max_ms": max(gaps),
-                                 "ms": [round(g, 3) for g in gaps] if len(gaps) <= 64 else None}
+                                 "ms": [round(g, 3) for g in gaps] if len(gaps) <= 64 else None,
+                                 "host_call_ms": [round(c, 3) for c in calls] if len(calls) <= 64 else None}
         host = (time.perf_counter() - t0) * 1e3
         torch.cuda.synchronize()
         t = torch.tensor([dev], dtype=torch.float64, device=f"cuda:{local}")

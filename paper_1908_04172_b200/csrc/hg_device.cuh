@@ -24,7 +24,10 @@ using u32 = uint32_t;
 using u64 = uint64_t;
 using i32 = int32_t;
 
-constexpr int kMaxPrimes = 24;
+#ifndef HG_MAX_PRIMES
+#define HG_MAX_PRIMES 24
+#endif
+constexpr int kMaxPrimes = HG_MAX_PRIMES;
 
 #ifndef HG_DEBUG_CHECKS
 #define HG_DEBUG_CHECKS 0  // self-check build: mbarrier wait timeouts and TMEM allocation checks trap
@@ -34,6 +37,9 @@ constexpr int kMaxPrimes = 24;
 #endif
 #ifndef HG_RESCALE_MINB
 #define HG_RESCALE_MINB 4  // rescale: correction row in TMEM, 41 KB smem, 64 registers
+#endif
+#ifndef HG_RESCALE_TMEM_CELLS
+#define HG_RESCALE_TMEM_CELLS 32  // rescale keeps one correction row: half the TMEM columns
 #endif
 #ifndef HG_DIGITS_MINB
 #define HG_DIGITS_MINB 4
@@ -212,9 +218,14 @@ __device__ __forceinline__ i32 centered_round_rem(u32 x, const DevPrime& P) {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ u32 tm_smem_addr(const void* p) { return static_cast<u32>(__cvta_generic_to_shared(p)); }
 
-template <int T>
+// CELLS (64 or 32) private cells per thread: a kernel that needs fewer takes fewer columns,
+// which leaves room for CTAs of other kernels (other streams) on the same SM.
+template <int T, int CELLS = 64>
 struct TmemScratch {
-  static constexpr u32 kCols = 64 * (T / 128) < 32 ? 32 : 64 * (T / 128);
+  static_assert(CELLS == 64 || CELLS == 32, "cells per thread");
+  // warps w and w + 4 share TMEM lanes, so a CTA needs CELLS columns per group of 4 warps
+  // (rounded up: a CTA of 32 or 64 threads still needs CELLS columns)
+  static constexpr u32 kCols = CELLS * ((T + 127) / 128) < 32 ? 32 : CELLS * ((T + 127) / 128);
   u32 base;  // this thread's cell 0: lane | column
   // warp 0 allocates; every thread learns the base after the barrier (slot: one smem word)
   __device__ __forceinline__ void alloc(u32* slot, u32 tid) {
@@ -230,7 +241,7 @@ struct TmemScratch {
 #if HG_DEBUG_CHECKS
     if (((*slot) >> 16) != 0 || ((*slot) & 0xFFFFu) + kCols > 512u) __trap();  // self-check build
 #endif
-    base = *slot + (((w & 3) * 32) << 16) + (w >> 2) * 64;
+    base = *slot + (((w & 3) * 32) << 16) + (w >> 2) * CELLS;
   }
   __device__ __forceinline__ void free(u32 tid) {
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::);

@@ -53,7 +53,17 @@ static void check_launch(int r, const char* what) {
   cuda_check(cudaGetLastError(), what);
 }
 
-static constexpr size_t kBufCacheMin = size_t(1) << 30;  // layer-sized buffers only (c4, c5b); c2 unchanged
+// Buffers of at least 1 MB (HG_BUF_CACHE_MIN_MB) released on the context's stream are recycled
+// by exact size (DeviceCore::take / put) instead of going back to the driver's pool.  The
+// threshold was 1 GiB (c4 / c5b layers only) until the two-batches-in-flight schedule showed
+// cudaMallocAsync itself stalling: with two contexts executing concurrently, the second
+// execute on a context after a device synchronise spent 2-3 ms in its layer-sized allocations
+// every time and 10-500 ms in about one run in five, whatever the pool (device default or
+// per context), the auxiliary stream or the kernel parameter size (profiles/r3_experiments.md).
+static const size_t kBufCacheMin = [] {
+  const char* e = getenv("HG_BUF_CACHE_MIN_MB");
+  return e ? static_cast<size_t>(atof(e) * 1048576.0) : (size_t(1) << 20);
+}();
 static size_t buf_cache_max(int device) {
   static std::mutex mu;
   static std::map<int, size_t> v;
@@ -1071,7 +1081,22 @@ class Executor {
         if (n.op == HG_OP_OUTPUT) return n.id;
       throw Error(HG_ERR_VALIDATION, "graph has no Output node");
     }();
+    // HG_EXEC_TRACE=<ms>: host time per node of every execute that takes the host longer than <ms>
+    static const double trace_ms = [] {
+      const char* e = getenv("HG_EXEC_TRACE");
+      return e ? atof(e) : -1.0;
+    }();
+    std::vector<std::pair<const Node*, double>> host_ms;
     for (const auto& n : model_.nodes) {
+      const auto h0 = std::chrono::steady_clock::now();
+      struct HostMark {
+        std::vector<std::pair<const Node*, double>>* v;
+        const Node* n;
+        std::chrono::steady_clock::time_point t;
+        ~HostMark() {
+          if (v) v->emplace_back(n, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count());
+        }
+      } host_mark{trace_ms >= 0 ? &host_ms : nullptr, &n, h0};
       cudaEvent_t e0 = nullptr, e1 = nullptr;
       if (timed) {
         cudaEventCreate(&e0);
@@ -1125,6 +1150,16 @@ class Executor {
       for (const auto& in : n.inputs)
         if (--uses[in] == 0) values.erase(in);
       values[n.id] = std::move(v);
+    }
+    if (trace_ms >= 0) {
+      double tot = 0;
+      for (auto& h : host_ms) tot += h.second;
+      if (tot > trace_ms) {
+        std::string line = "[hg exec trace] host ms " + std::to_string(tot) + ":";
+        for (auto& h : host_ms)
+          if (h.second > 0.05) line += " " + h.first->id + "=" + std::to_string(h.second);
+        fprintf(stderr, "%s\n", line.c_str());
+      }
     }
     require(rescales_ == plan_.planned_rescale_ops, "executed rescale count diverged from the plan");
     auto it = values.find(out_id);

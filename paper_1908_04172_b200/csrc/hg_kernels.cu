@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_RESCALE_MINB
   extern __shared__ u32 sm[];
   const u32 tid = threadIdx.x;
   // rounding correction: thread-private row in tensor memory (cells [0, 32), i32 bits)
-  TmemScratch<NT::T> tm;
+  TmemScratch<NT::T, HG_RESCALE_TMEM_CELLS> tm;
   tm.alloc(sm + NT::SMEM_WORDS, tid);
   const u64 row = blockIdx.x;
   const u32 L = a.level;
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_RESCALE_MINB
       for (int e = 0; e < 8; ++e) w[e] = static_cast<u32>(centered_round_rem(x[c + e], Pl));
       tm.st8(c, w);
     }
-    TmemScratch<NT::T>::wait_st();
+    decltype(tm)::wait_st();
   }
 #pragma unroll 1
   for (u32 i = 0; i + 1 < L; ++i) {
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), (LOGN <= 13 ? HG_RESCALE_MINB
     for (int c = 0; c < 32; c += 8) {
       u32 v[8];
       tm.ld8(c, v);
-      TmemScratch<NT::T>::wait_ld();
+      decltype(tm)::wait_ld();
 #pragma unroll
       for (int e = 0; e < 8; ++e) x[c + e] = v[e] + pm;
     }

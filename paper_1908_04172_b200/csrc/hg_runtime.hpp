@@ -56,10 +56,11 @@ bool host_narrow_upload(int device, const uint64_t* words, uint32_t* dst, uint64
 struct DeviceCore {
   int device = 0;
   cudaStream_t stream = nullptr;
-  // Large-buffer cache: buffers >= 1 GiB allocated on `stream` are kept on release and
-  // handed to the next request of exactly that size (stream-ordered like cudaFreeAsync /
-  // cudaMallocAsync on the same stream).  A layer-sized cudaMallocAsync at a workload's memory
-  // peak can otherwise spend ~30-130 ms remapping pool memory (the c4 block).
+  // Buffer cache: buffers >= 1 MB (HG_BUF_CACHE_MIN_MB) allocated on `stream` are kept on
+  // release and handed to the next request of exactly that size (stream-ordered like
+  // cudaFreeAsync / cudaMallocAsync on the same stream).  A layer-sized cudaMallocAsync can
+  // otherwise stall the host: 30-130 ms at a workload's memory peak (the c4 block), 10-500 ms
+  // now and then with two contexts executing concurrently.
   std::mutex cache_mu;
   std::multimap<size_t, void*> cache;
   size_t cached = 0;
