@@ -14,6 +14,7 @@
 #include <cstring>
 #include <functional>
 #include <mutex>
+#include <set>
 
 #include "hg_modmath.hpp"
 #include "hg_runtime.hpp"
@@ -81,33 +82,71 @@ static size_t buf_cache_max(int device) {
   return cap;
 }
 
+// Every context on a device has its own cache; the cap (half the device by default) bounds
+// their sum, and an allocation that fails releases all of them before it is retried.
+namespace {
+std::mutex g_cores_mu;
+std::map<int, std::set<DeviceCore*>> g_cores;   // live cores per device
+std::map<int, size_t> g_cached_total;           // bytes held by their caches
+}  // namespace
+
+void DeviceCore::enroll() {
+  std::lock_guard<std::mutex> g(g_cores_mu);
+  g_cores[device].insert(this);
+}
+
+// Lock order: g_cores_mu, then a core's cache_mu.
 void* DeviceCore::take(size_t bytes) {
+  std::lock_guard<std::mutex> gt(g_cores_mu);
   std::lock_guard<std::mutex> g(cache_mu);
   auto it = cache.find(bytes);
   if (it == cache.end()) return nullptr;
   void* p = it->second;
   cache.erase(it);
   cached -= bytes;
+  g_cached_total[device] -= bytes;
   return p;
 }
 
 bool DeviceCore::put(void* p, size_t bytes) {
   const size_t cap = buf_cache_max(device);
+  std::lock_guard<std::mutex> gt(g_cores_mu);
   std::lock_guard<std::mutex> g(cache_mu);
-  if (cached + bytes > cap) return false;
+  if (g_cached_total[device] + bytes > cap) return false;
+  g_cached_total[device] += bytes;
   cache.emplace(bytes, p);
   cached += bytes;
   return true;
 }
 
+// g_cores_mu held
+static void flush_core_locked(DeviceCore* c) {
+  std::lock_guard<std::mutex> g(c->cache_mu);
+  for (auto& e : c->cache) cudaFreeAsync(e.second, c->stream);
+  c->cache.clear();
+  g_cached_total[c->device] -= c->cached;
+  c->cached = 0;
+}
+
 void DeviceCore::flush() {
-  std::lock_guard<std::mutex> g(cache_mu);
-  for (auto& e : cache) cudaFreeAsync(e.second, stream);
-  cache.clear();
-  cached = 0;
+  std::lock_guard<std::mutex> gt(g_cores_mu);
+  flush_core_locked(this);
+}
+
+// Releases the caches of every context on the device and waits for the frees (out-of-memory path).
+static void flush_device_caches(int device) {
+  std::lock_guard<std::mutex> gt(g_cores_mu);
+  for (DeviceCore* c : g_cores[device]) {
+    flush_core_locked(c);
+    cudaStreamSynchronize(c->stream);
+  }
 }
 
 DeviceCore::~DeviceCore() {
+  {
+    std::lock_guard<std::mutex> g(g_cores_mu);
+    g_cores[device].erase(this);
+  }
   if (stream) {
     cudaSetDevice(device);
     flush();
@@ -122,11 +161,11 @@ DeviceBuffer::DeviceBuffer(std::shared_ptr<DeviceCore> c, size_t b, cudaStream_t
   const bool cacheable = bytes >= kBufCacheMin && stream == core->stream;
   if (cacheable && (ptr = core->take(bytes)) != nullptr) return;
   cudaError_t e = cudaMallocAsync(&ptr, bytes, stream);
-  if (e == cudaErrorMemoryAllocation && core->cached > 0) {
-    // the cache holds the memory: release it (stream-ordered) and retry once
+  if (e == cudaErrorMemoryAllocation) {
+    // the caches (this context's or another's on the device) may hold the memory: release
+    // them (stream-ordered) and retry once
     cudaGetLastError();
-    core->flush();
-    cudaStreamSynchronize(core->stream);
+    flush_device_caches(core->device);
     e = cudaMallocAsync(&ptr, bytes, stream);
   }
   cuda_check(e, "cudaMallocAsync");
@@ -208,6 +247,7 @@ static std::shared_ptr<Context> make_context(u32 n, const u64* chain, u32 chain_
   ctx->core = std::make_shared<DeviceCore>();
   ctx->core->device = device;
   cuda_check(cudaStreamCreateWithFlags(&ctx->core->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  ctx->core->enroll();
 
   // NTT tables (root_powers / inv_root_powers in the reference's order, with
   // Shoup companions), staged per NTT pass in the order the kernels consume them.

@@ -67,6 +67,7 @@ struct DeviceCore {
   void* take(size_t bytes);
   bool put(void* p, size_t bytes);
   void flush();  // cudaFreeAsync every cached buffer on `stream`
+  void enroll();  // registers the core with its device's cache accounting (after `device` is set)
   ~DeviceCore();
 };
 
