@@ -1481,21 +1481,24 @@ int launch_mac_conv(const MacConvArgs& a, const Basis& B, cudaStream_t s) {
 }
 
 // One non-blocking auxiliary stream per device for intra-op fork/join (HG_AUX_STREAM=0 off).
-static cudaStream_t aux_stream() {
+static cudaStream_t aux_stream(int idx = 0) {
   static const bool on = [] {
     const char* e = getenv("HG_AUX_STREAM");
     return !(e != nullptr && e[0] == '0');
   }();
   if (!on || g_prof_on) return nullptr;  // the per-kernel profiler serialises launches for attribution
   static std::mutex mu;
-  static cudaStream_t streams[64] = {};
+  static cudaStream_t streams[64][3] = {};
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || idx < 0 || idx >= 3) return nullptr;
   std::lock_guard<std::mutex> g(mu);
-  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
-  return streams[dev];
+  if (!streams[dev][idx]) cudaStreamCreateWithFlags(&streams[dev][idx], cudaStreamNonBlocking);
+  return streams[dev][idx];
 }
 
+#ifndef HG_RELIN_SPECIAL_STREAMS
+#define HG_RELIN_SPECIAL_STREAMS 0
+#endif
 // One relinearisation chain (digits -> special + limb key switches -> mod-down) on stream
 // s; the special-prime key switch runs on `ss` (== s, or an auxiliary stream it forks to).
 template <int LN>
@@ -1573,8 +1576,14 @@ int launch_relin(int logn, const RelinArgs& a, const Basis& B, cudaStream_t s) {
       cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
       cudaEventRecord(fork, s);
       cudaStreamWaitEvent(aux, fork, 0);
+#if HG_RELIN_SPECIAL_STREAMS
+      // each half's special-prime key switch (count CTAs: under three per SM) beside its limb kernel
+      relin_chain<LN>(h0, B, s, aux_stream(1));
+      relin_chain<LN>(h1, B, aux, aux_stream(2));
+#else
       relin_chain<LN>(h0, B, s, nullptr);
       relin_chain<LN>(h1, B, aux, nullptr);
+#endif
       cudaEventRecord(join, aux);
       cudaStreamWaitEvent(s, join, 0);
       cudaEventDestroy(fork);
