@@ -98,6 +98,7 @@ struct Workers {
   std::vector<uint8_t*> dstage;     // [worker][slot] device staging of 24-bit-packed chunks
   cudaEvent_t start = nullptr;
   cudaStream_t direct = nullptr;    // the raw-u64 share: H2D + GPU narrowing
+  cudaEvent_t raw_ev[4] = {};       // dynamic split: raw chunks in flight on `direct`
   std::mutex mu;                    // one upload at a time per device
 };
 
@@ -115,7 +116,9 @@ Workers& workers(int device) {
   auto& w = all[device];
   if (!w) {
     w = std::make_unique<Workers>();
-    const int n = worker_count();
+    // the packers, plus one thread that only feeds raw chunks to the copy engine (it sleeps on
+    // events between chunks; idle with the static split)
+    const int n = worker_count() + 1;
     w->pool = std::make_unique<HostPool>(n);
     w->streams.resize(n);
     w->events.resize(static_cast<size_t>(n) * kSlots);
@@ -136,6 +139,8 @@ Workers& workers(int device) {
     for (auto& p : w->dstage) cuda_check(cudaMalloc(reinterpret_cast<void**>(&p), kChunkWords * 4), "device stage");
     cuda_check(cudaEventCreateWithFlags(&w->start, cudaEventDisableTiming), "event");
     cuda_check(cudaStreamCreateWithPriority(&w->direct, cudaStreamNonBlocking, pri), "stream");
+    for (auto& e : w->raw_ev)
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync), "event");
   }
   return *w;
 }
@@ -274,6 +279,30 @@ __global__ void k_unpack24(const uint8_t* packed, u32* dst, u32 N, u32 R0, u32 l
   }
 }
 
+// Raw u64 chunk -> u32 residues with the < q check: word i of the chunk belongs to limb
+// (R0 + i / N) % level (the dynamic split's raw path; the static split uses k_narrow).
+struct ChainQ {
+  u32 q[32];
+};
+__global__ void k_narrow_chunk(const ulonglong2* in, u32* out, u32 words, u32 N, u32 R0, u32 level, ChainQ cq,
+                               int* bad) {
+  const u32 i = (blockIdx.x * blockDim.x + threadIdx.x) * 4;  // N % 4 == 0: one limb per quad
+  if (i >= words) return;
+  const u32 q = cq.q[(R0 + i / N) % level];
+  const ulonglong2 a = in[i / 2], b = in[i / 2 + 1];
+  if (a.x >= q || a.y >= q || b.x >= q || b.y >= q) atomicExch(bad, 1);
+  *reinterpret_cast<uint4*>(out + i) =
+      make_uint4(static_cast<u32>(a.x), static_cast<u32>(a.y), static_cast<u32>(b.x), static_cast<u32>(b.y));
+}
+
+bool use_dynamic_split() {
+  static const bool on = [] {
+    const char* e = getenv("HG_UPLOAD_DYNAMIC");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 bool use_avx512() {
   static const bool on = [] {
     const char* e = getenv("HG_UPLOAD_AVX512");
@@ -316,7 +345,22 @@ bool host_narrow_upload(int device, const u64* words, u32* dst, u64 n_words, u32
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   // the copies are ordered after the work already queued on s (readers of dst)
   cuda_check(cudaEventRecord(W.start, s), "event");
-  if (direct != nullptr && direct->words != 0) {
+  // Dynamic split (contiguous words with a raw share): the host packers take 2 MB chunks from
+  // the front of the tensor and one feeder thread sends chunks from the back raw (u64 over the
+  // bus, checked and narrowed on the GPU), a few in flight at a time, until the two meet.  How
+  // much goes raw then follows the host's packing speed of the moment instead of a fixed
+  // share: the packing is bound by the host's memory bandwidth, which varies from box to box
+  // and from one minute to the next, while the bus has headroom.
+  static const u64 max_raw_slots = [] {
+    const char* e = getenv("HG_UPLOAD_RAW_SLOTS");
+    return static_cast<u64>(e ? std::min(4, std::max(2, atoi(e))) : 2);  // 2: 6.80-6.88 ms per c2 upload step, 4: 6.84-6.99
+  }();
+  const int raw_slots = (direct != nullptr && direct->words != 0)
+                            ? static_cast<int>(std::min<u64>(max_raw_slots, direct->words / kChunkWords)) : 0;
+  const bool dynamic = use_dynamic_split() && segs == nullptr && raw_slots >= 2 && level <= 32 && N % 4 == 0 &&
+                       W.pool->size() >= 2;
+  if (dynamic) n_words += direct->words;  // the whole tensor is shared out chunk by chunk
+  if (!dynamic && direct != nullptr && direct->words != 0) {
     // the raw share (words [n_words, n_words + direct->words)) crosses the bus as u64 and is
     // validated and narrowed on the GPU, alongside the host-packed chunks
     cuda_check(cudaStreamWaitEvent(W.direct, W.start, 0), "wait");
@@ -326,7 +370,7 @@ bool host_narrow_upload(int device, const u64* words, u32* dst, u64 n_words, u32
     if (launch_narrow(direct->stage, dst + n_words, direct->words, level, N, *direct->basis, direct->bad, W.direct) < 0)
       throw Error(HG_ERR_CUDA, "narrow launch failed");
   }
-  const int nw = W.pool->size();
+  const int nw = W.pool->size() - 1;  // packers: workers [0, nw); worker nw is the raw feeder
   const bool avx512 = use_avx512();
   u32 mask24 = 0;  // limbs whose residues cross the bus as 3 bytes
   for (u32 l = 0; l < level && l < 32; ++l)
@@ -335,17 +379,55 @@ bool host_narrow_upload(int device, const u64* words, u32* dst, u64 n_words, u32
   const u64 chunks = (n_words + kChunkWords - 1) / kChunkWords;
   std::atomic<bool> bad{false};
   std::atomic<int> err{0};
-  std::atomic<u64> h2d{direct != nullptr ? direct->words * 8 : 0};
+  std::atomic<u64> h2d{(!dynamic && direct != nullptr) ? direct->words * 8 : 0};
   std::string err_msg;
   std::mutex err_mu;
+  // unclaimed chunks [lo, hi): packers claim lo, the raw feeder claims hi - 1
+  std::atomic<u64> range{chunks};  // lo in the high 32 bits, hi in the low 32
+  auto claim = [&](bool front, u64& c) {
+    u64 r = range.load(std::memory_order_relaxed);
+    for (;;) {
+      const u64 lo = r >> 32, hi = r & 0xFFFFFFFFull;
+      if (lo >= hi) return false;
+      const u64 nr = front ? (((lo + 1) << 32) | hi) : ((lo << 32) | (hi - 1));
+      if (range.compare_exchange_weak(r, nr, std::memory_order_relaxed)) {
+        c = front ? lo : hi - 1;
+        return true;
+      }
+    }
+  };
+  ChainQ cq{};
+  for (u32 l = 0; l < level && l < 32; ++l) cq.q[l] = static_cast<u32>(chain[l]);
   W.pool->run([&](int w) {
     try {
+      if (w == nw && !dynamic) return;
       cudaSetDevice(device);
+      if (w == nw) {
+        // raw chunks from the back, raw_slots of them in flight on the direct stream
+        cuda_check(cudaStreamWaitEvent(W.direct, W.start, 0), "wait");
+        cuda_check(cudaMemsetAsync(direct->bad, 0, sizeof(int), W.direct), "memset");
+        u64 c = 0;
+        for (int k = 0; claim(false, c); ++k) {
+          const int slot = k % raw_slots;
+          if (k >= raw_slots) cuda_check(cudaEventSynchronize(W.raw_ev[slot]), "event");
+          const u64 b = c * kChunkWords, e = std::min(n_words, b + kChunkWords);
+          u64* st = direct->stage + static_cast<u64>(slot) * kChunkWords;
+          cuda_check(cudaMemcpyAsync(st, words + b, (e - b) * 8, cudaMemcpyHostToDevice, W.direct), "h2d");
+          k_narrow_chunk<<<static_cast<u32>((e - b + 1023) / 1024), 256, 0, W.direct>>>(
+              reinterpret_cast<const ulonglong2*>(st), dst + b, static_cast<u32>(e - b), N, static_cast<u32>(b / N),
+              level, cq, direct->bad);
+          cuda_check(cudaGetLastError(), "narrow chunk");
+          cuda_check(cudaEventRecord(W.raw_ev[slot], W.direct), "event");
+          h2d += (e - b) * 8;
+        }
+        return;  // the caller reads the flag back and synchronises the direct stream
+      }
       cudaStream_t ws = W.streams[w];
       cuda_check(cudaStreamWaitEvent(ws, W.start, 0), "wait");
       bool my_bad = false;
       int used = 0;
-      for (u64 c = static_cast<u64>(w); c < chunks; c += static_cast<u64>(nw), ++used) {
+      u64 c = static_cast<u64>(w);
+      for (; dynamic ? claim(true, c) : c < chunks; c += dynamic ? 0 : static_cast<u64>(nw), ++used) {
         const int slot = used % kSlots;
         const size_t ei = static_cast<size_t>(w) * kSlots + slot;
         if (used >= kSlots) cuda_check(cudaEventSynchronize(W.events[ei]), "event");

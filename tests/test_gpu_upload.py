@@ -71,4 +71,51 @@ def test_upload_reports_bus_bytes(ctx):
     per_res_4 = 2 * L * n * 4
     per_res_p = 2 * n * sum(3 if q < (1 << 24) else 4 for q in p["chain"][:L])
     raw = direct * 2 * L * n * 8
+    if os.environ.get("HG_UPLOAD_DYNAMIC", "1") != "0":
+        # dynamic split: the raw share follows the host's packing speed; every word crosses the bus
+        # once, packed (3 or 4 bytes) or raw (8 bytes), raw in whole 2 MB chunks
+        lo = count * min(per_res_4, per_res_p)
+        assert lo <= got.value <= count * 2 * L * n * 8, got.value
+        return
     assert got.value in (raw + (count - direct) * per_res_4, raw + (count - direct) * per_res_p), got.value
+
+
+def test_upload_static_split_round_trip_and_bus_bytes():
+    """HG_UPLOAD_DYNAMIC=0 (read once per process, hence the subprocess): the fixed raw share
+    -- multi-chunk round trip, an out-of-range word in the raw share and in the packed part,
+    and the bus bytes of the fixed split."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r'''
+import ctypes, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+from paper_1908_04172_b200 import henet as H, workloads as W
+p = W.N8192
+ctx = H.CkksContext(p["n"], p["chain"], p["special"], p["scale"])
+count, L, n = 300, 6, p["n"]
+x = W.random_ciphertexts(p, count, seed=9, level=L)
+t = H.CipherTensor.from_words(ctx, x, 1.0)
+assert np.array_equal(t.to_words(), x)
+got = ctypes.c_uint64(0)
+H.lib.hg_last_upload_h2d_bytes(ctypes.byref(got))
+direct = int(count * 0.15)
+per4 = 2 * L * n * 4
+perp = 2 * n * sum(3 if q < (1 << 24) else 4 for q in p["chain"][:L])
+raw = direct * 2 * L * n * 8
+assert got.value in (raw + (count - direct) * per4, raw + (count - direct) * perp), got.value
+for e in (3, count - 2):  # packed part, raw share (the last 15% of the ciphertexts)
+    y = x.copy()
+    y[e, 1, 2, 77] = p["chain"][2]
+    try:
+        H.CipherTensor.from_words(ctx, y, 1.0)
+        raise SystemExit("accepted an out-of-range word")
+    except H.ValidationError as ex:
+        assert "residue out of range" in str(ex)
+print("OK")
+'''
+    env = {**os.environ, "HG_UPLOAD_DYNAMIC": "0", "HG_UPLOAD_DIRECT_FRAC": "0.15"}
+    r = subprocess.run([sys.executable, "-c", script, root], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
