@@ -483,7 +483,10 @@ def b200_run(args, ws, rank, local):
         # three trials of each loop, medians reported (the helper thread makes single trials
         # sensitive to host scheduling)
         with concurrent.futures.ThreadPoolExecutor(1) as pool:
-            pipelined(2, pool)  # warm-up (both buffers, both streams)
+            # warm-up: both buffers and both streams, and on a fresh box the host side itself
+            # (packer threads, pinned pages, CPU clocks): the first 10-20 loop steps of a
+            # process ran 10-30% slower than the rest (profiles/r3_experiments.md)
+            pipelined(max(args.warmup, 3) + 17, pool)
             up_ms.clear()
             step_ms.clear()
             pipe_trials = [timed(lambda n: pipelined(n, pool), n_e2e) for _ in range(3)]
