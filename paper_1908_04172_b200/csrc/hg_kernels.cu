@@ -297,6 +297,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_mac_dense(MacDenseArgs a,
 //   filter chunks.  Each thread: 4 coefficients x FT filters; the gathered
 //   input of the next tap is prefetched while the current tap is multiplied.
 // ===========================================================================
+#ifndef HG_CONV_PRE
+#define HG_CONV_PRE 4  // gathered inputs in flight per thread: 0.401 ms per c2 step (3: 0.419; 5, 6: spills, 0.457 / 0.469)
+#endif
 constexpr int kMaxTaps = 1024;
 constexpr int kConvThreads = 256;
 #ifndef HG_CONV_PP
@@ -516,7 +519,7 @@ __global__ void __launch_bounds__(kConvThreads, 3) k_mac_conv(MacConvArgs a, Bas
   const u64 xstride = static_cast<u64>(a.polys) * a.x_level * a.N;
   const u32* Xb = a.X + (static_cast<u64>(poly) * a.x_level + limb) * a.N + n;
   const bool fp = a.fp64[limb] != 0;
-  constexpr int kPre = 4;  // gathered inputs in flight
+  constexpr int kPre = HG_CONV_PRE;  // gathered inputs in flight
   const u32 p1 = min(npos, (blockIdx.y + 1) * kConvPos);
 #pragma unroll 1
   for (u32 pos = blockIdx.y * kConvPos; pos < p1; ++pos) {
