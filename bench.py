@@ -1057,6 +1057,11 @@ def net_run(args, ws, rank, local):
 def main():
     args = parse()
     ws, rank, local = dist_env()
+    if ws > 1 and "HG_UPLOAD_THREADS" not in os.environ:
+        # the ranks of one node share its host cores: each rank's upload packers get their share
+        # (the library's default is all but two of the host's threads, right for one rank)
+        per_node = int(os.environ.get("LOCAL_WORLD_SIZE", ws)) or ws
+        os.environ["HG_UPLOAD_THREADS"] = str(max(2, (os.cpu_count() or 16) // per_node - 2))
     if args.workload == "c4":
         if args.impl == "reference":
             if rank == 0:
